@@ -1,0 +1,176 @@
+/*
+ * cluspath_b200.h — the C-ABI drop-in boundary of the B200-native
+ * convex-clustering-path engine (libcluspath_b200.so, sm_100a).
+ *
+ * Every entry point below replaces one function of the reference C++ API
+ * (the headers under /root/reference/proj/include/cluspath, namespace cluspath); the
+ * replaced declaration is cited as header:line.  Plain pointers and sizes
+ * only: no C++ or torch types cross this boundary.
+ *
+ * Layout.  A d x n matrix (Eigen::MatrixXd, column-major, types.hpp:12) is
+ * passed as `const double*` of length d*n with each sample (node) contiguous;
+ * a d x |E| edge matrix likewise with each edge contiguous.  Edges are
+ * (i, j, w) with 0 <= i < j < n, kept sorted lexicographically
+ * (graph.hpp:14-51).  Index = int64_t (types.hpp:11).
+ *
+ * Errors.  Every int-returning call returns CP_OK or an error code; the
+ * message of the calling thread's last error is cp_last_error().  The code
+ * tells the wrapper which exception the reference would throw:
+ * CP_EINVAL -> std::invalid_argument, CP_ERUNTIME -> std::runtime_error.
+ * Non-convergence is not an error (cp_termination.converged = 0,
+ * solver_util.hpp:87-100).
+ *
+ * Ownership.  The caller owns every host buffer.  Device state (data, graph,
+ * per-path solver state) is owned by the handles and lives until destroyed —
+ * the per-path SolveCache of the reference (solvers.hpp:119-123) is held by
+ * the cp_ctx.  One cp_ctx per host thread; calls are synchronous.
+ */
+#ifndef CLUSPATH_B200_H
+#define CLUSPATH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CP_OK 0
+#define CP_EINVAL 1   /* std::invalid_argument */
+#define CP_ERUNTIME 2 /* std::runtime_error    */
+#define CP_ECUDA 3    /* CUDA failure (reported as runtime_error) */
+#define CP_ENCCL 4    /* NCCL failure */
+
+typedef struct cp_ctx cp_ctx;     /* one device, its streams, workspace and SolveCache */
+typedef struct cp_data cp_data;   /* device-resident DataMatrix (types.hpp:16-22)     */
+typedef struct cp_graph cp_graph; /* device-resident WeightedGraph (graph.hpp:23-51)   */
+
+/* SolverConfig (solvers.hpp:72-93); cp_solver_config_default fills the reference defaults. */
+typedef struct cp_solver_config {
+  int32_t algorithm;      /* 0 ADMM, 1 FastAMA, 2 SSNAL (solvers.hpp:15) */
+  int32_t collect_trace;  /* accepted, ignored (trace rows are host-side diagnostics) */
+  double epsilon;         /* 1e-6 */
+  double kkt_factor;      /* 10 */
+  int64_t max_iter;       /* 0 -> 100 outer (SSNAL) or 20000 (ADMM, AMA) */
+  double time_limit;      /* seconds; <= 0 means none */
+  double admm_rho;        /* 1 */
+  double ama_step_safety; /* 0.99 */
+  double ssnal_sigma0;    /* 1 */
+  double armijo_mu;       /* 1e-4 */
+  double backtrack_beta;  /* 0.5 */
+  int64_t ssnal_newton_max; /* 50 */
+  int64_t pcg_max_iter;     /* 500 */
+} cp_solver_config;
+
+/* TerminationRecord (solvers.hpp:45-52) plus work counters. */
+typedef struct cp_termination {
+  double f_primal, f_dual, gap;
+  int64_t iterations;
+  int32_t converged, pad;
+  double wall_time;
+  int64_t newton, cg, armijo, hess_apply; /* counters (not in the reference record) */
+} cp_termination;
+
+/* PathOptions (path.hpp:51-55). */
+typedef struct cp_path_options {
+  int32_t warm_start;        /* 1 */
+  int32_t require_connected; /* 0 */
+  double fuse_tol;           /* 1e-3 */
+} cp_path_options;
+
+/* Per-kernel timing/bytes record for roofline accounting (no reference counterpart). */
+typedef struct cp_kernel_stat {
+  char name[40];
+  int64_t launches;
+  double ms;        /* summed CUDA-event time on the launching stream */
+  double alg_bytes; /* summed algorithmic (compulsory) bytes */
+} cp_kernel_stat;
+
+/* ---- context ------------------------------------------------------------ */
+int cp_ctx_create(int device, cp_ctx** out);
+void cp_ctx_destroy(cp_ctx* ctx);
+const char* cp_last_error(void);
+int cp_ctx_synchronize(cp_ctx* ctx);
+void cp_solver_config_default(cp_solver_config* cfg);
+void cp_path_options_default(cp_path_options* opt);
+/* Kernel statistics: enable CUDA-event timing of the hot kernels. */
+int cp_stats_enable(cp_ctx* ctx, int on);
+int cp_stats_reset(cp_ctx* ctx);
+int cp_stats_get(cp_ctx* ctx, cp_kernel_stat* out, int max_entries, int* count);
+/* Device/library identification: sm major/minor, SM count, kernel build arch. */
+int cp_device_info(cp_ctx* ctx, int* sm_major, int* sm_minor, int* sm_count, int* built_arch);
+
+/* ---- data (types.hpp:16-28; make_data_matrix graph.cpp:10-23) ------------ */
+int cp_data_create(cp_ctx* ctx, const double* A, int64_t d, int64_t n, cp_data** out);
+void cp_data_destroy(cp_data* data);
+
+/* ---- graph (graph.hpp:23-92) --------------------------------------------- */
+/* compute_knn_weights(data, k, phi) (graph.hpp:58; graph.cpp:75-114) */
+int cp_knn_graph(cp_ctx* ctx, const cp_data* data, int64_t k, double phi, cp_graph** out);
+/* WeightedGraph(n, edges): sorts and validates (graph.hpp:29-31; graph.cpp:25-45) */
+int cp_graph_from_edges(cp_ctx* ctx, int64_t n, const int64_t* i, const int64_t* j, const double* w, int64_t E,
+                        cp_graph** out);
+void cp_graph_destroy(cp_graph* g);
+int64_t cp_graph_nodes(const cp_graph* g);      /* graph.hpp:33 */
+int64_t cp_graph_edge_count(const cp_graph* g); /* graph.hpp:34 */
+/* edges() in list order; d2 (nullable) receives the kNN squared distances
+   (NaN for graphs built from an edge list). */
+int cp_graph_export(cp_ctx* ctx, const cp_graph* g, int64_t* i, int64_t* j, double* w, double* d2);
+int cp_graph_degrees(cp_ctx* ctx, const cp_graph* g, int64_t* degree); /* graph.hpp:43-44 */
+
+/* IncidenceOperator::apply_into: X (d x n) -> X B (d x |E|) (graph.hpp:69-70; graph.cpp:122-132) */
+int cp_incidence_apply(cp_ctx* ctx, const cp_graph* g, const double* X, int64_t d, int64_t n, double* out);
+/* IncidenceOperator::apply_transpose_into: Z (d x |E|) -> Z B^T (d x n) (graph.hpp:74-75; graph.cpp:140-152) */
+int cp_incidence_apply_t(cp_ctx* ctx, const cp_graph* g, const double* Z, int64_t d, int64_t E, double* out);
+/* connected_components + component_count (graph.hpp:90-92; graph.cpp:169-202) */
+int cp_connected_components(cp_ctx* ctx, const cp_graph* g, int64_t* labels, int64_t* K);
+/* power_iteration(LinearOperator::sparse(B.laplacian())) (linalg.hpp:84-85; linalg.cpp:194-242) */
+int cp_laplacian_lambda_max(cp_ctx* ctx, const cp_graph* g, double tol, int64_t max_iter, double* lambda);
+
+/* ---- prox (prox.hpp:8-54) ------------------------------------------------- */
+/* q in {1, 2}; prox_columns_into (prox.hpp:28-29; prox.cpp:73-80) */
+int cp_prox_columns(cp_ctx* ctx, int q, const double* V, const double* thresholds, int64_t d, int64_t E,
+                    double* out);
+/* project_columns (prox.hpp:30-31; prox.cpp:82-93) */
+int cp_project_columns(cp_ctx* ctx, int q, const double* Z, const double* radii, int64_t d, int64_t E, double* out);
+/* ProxJacobian::diag for every column (prox.hpp:38-49; prox.cpp:106-132): out d x E */
+int cp_prox_jacobian_diag(cp_ctx* ctx, int q, const double* V, const double* thresholds, int64_t d, int64_t E,
+                          double* out);
+
+/* ---- objectives (solvers.hpp:95-118, 143-156) ----------------------------- */
+int cp_primal_objective(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q, const double* X,
+                        double* out);
+int cp_dual_objective(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q, const double* Z,
+                      double* out);
+int cp_kkt_residual(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q, const double* X,
+                    const double* Z, double* out);
+int cp_ssnal_phi_value(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q, const double* Z,
+                       double sigma, const double* X, double* out);
+int cp_ssnal_phi_gradient(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q, const double* Z,
+                          double sigma, const double* X, double* out);
+int cp_ssnal_hessian_apply(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q, const double* Z,
+                           double sigma, const double* X, const double* D, double* out);
+
+/* ---- solve (solvers.hpp:132-141) ----------------------------------------- */
+/* solve / solve_ssnal / solve_admm / solve_fast_ama.  warmX/warmZ nullable (both or neither);
+   their shapes are (wd x wn) and (wd x wE) and must match the instance. */
+int cp_solve(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q, const cp_solver_config* cfg,
+             const double* warmX, int64_t warm_d, int64_t warm_n, const double* warmZ, int64_t warm_E, double* X,
+             double* Z, cp_termination* term);
+
+/* ---- path (path.hpp:26-78) ------------------------------------------------ */
+/* make_schedule(start, end, count, spacing) (path.hpp:26; path.cpp:21-58); spacing 0 linear, 1 geometric */
+int cp_make_schedule(double start, double end, int64_t count, int geometric, double* out);
+/* extract_clusters (path.hpp:41-42; path.cpp:60-89): labels n, K, centroids d x n (first K columns used) */
+int cp_extract_clusters(cp_ctx* ctx, const cp_graph* g, const double* X, int64_t d, int64_t n, double fuse_tol,
+                        int64_t* labels, int64_t* K, double* centroids);
+/* run_path (path.hpp:71-73; path.cpp:110-142).  Outputs per gamma t (all nullable):
+   X_out[t*d*n], Z_out[t*d*E], labels_out[t*n], K_out[t], terms_out[t]. */
+int cp_run_path(cp_ctx* ctx, const cp_data* A, const cp_graph* g, int q, const double* gammas, int64_t T,
+                const cp_solver_config* cfg, const cp_path_options* opt, double* X_out, double* Z_out,
+                int64_t* labels_out, int64_t* K_out, cp_termination* terms_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CLUSPATH_B200_H */

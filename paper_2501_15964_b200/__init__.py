@@ -1,0 +1,19 @@
+"""paper_2501_15964_b200 — B200-native convex-clustering path engine.
+
+A drop-in for the hot path of the reference ``cluspath`` solver (arXiv
+2501.15964): kNN Gaussian-weight graph, edge operators B / Bᵀ, per-edge
+prox/projection, the SSNAL semismooth-Newton/PCG inner loop (plus fast AMA and
+ADMM), and GPU connected-component labels, swept over a warm-started gamma
+path.  All numerics run in hand-written sm_100a CUDA (libcluspath_b200.so)
+behind the C-ABI of include/cluspath_b200.h; this package is the host-side
+mirror of the reference API.
+"""
+from .cluspath import (Algorithm, ClusterAssignment, Context, DataMatrix, GammaSchedule, IncidenceOperator,
+                       PathOptions, PathResult, PenaltyNorm, ProblemInstance, Solution, SolverConfig, Spacing,
+                       TerminationRecord, WeightedGraph, algorithm_from_name, algorithm_name, component_count,
+                       compute_knn_weights, connected_components, default_context, dual_objective, duality_gap,
+                       extract_clusters, kkt_residual, make_data_matrix, make_schedule, penalty_norm_from_q,
+                       primal_objective, project_columns, prox_columns, prox_jacobian_diag, recover_primal, run_path,
+                       solve, ssnal_hessian_apply, ssnal_phi_gradient, ssnal_phi_value, two_point_closed_form)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

@@ -1,0 +1,604 @@
+"""Host-side mirror of the reference's ``cluspath`` API over the C-ABI.
+
+Names, argument meaning and error behaviour follow the reference headers
+(include/cluspath/*.hpp): ``compute_knn_weights``, ``WeightedGraph``,
+``IncidenceOperator``, ``connected_components``, the prox helpers,
+``SolverConfig``/``ProblemInstance``/``solve``, ``run_path``,
+``extract_clusters`` and ``make_schedule``.  std::invalid_argument surfaces as
+ValueError and std::runtime_error as RuntimeError.
+
+Layout: a reference d x n column-major matrix is a C-contiguous float64 numpy
+array of shape (n, d) here — identical bytes, one sample (or edge) per row.
+Every computation runs on the B200 through libcluspath_b200.so.
+"""
+from __future__ import annotations
+
+import bisect
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+_ctx_cache = {}
+
+
+class Context:
+    """One CUDA device with its stream and workspace (cp_ctx)."""
+
+    def __init__(self, device: int = 0):
+        lib = L.load()
+        h = C.c_void_p()
+        L.check(lib.cp_ctx_create(int(device), C.byref(h)))
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and L._lib is not None:
+            L._lib.cp_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        L.check(L.load().cp_ctx_synchronize(self._h))
+
+    def device_info(self):
+        a, b, c, d = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        L.check(L.load().cp_device_info(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
+        return {"sm": f"{a.value}{b.value}", "sm_count": c.value, "built_arch": d.value}
+
+    # kernel statistics for roofline accounting
+    def stats_enable(self, on=True):
+        L.check(L.load().cp_stats_enable(self._h, 1 if on else 0))
+
+    def stats_reset(self):
+        L.check(L.load().cp_stats_reset(self._h))
+
+    def stats(self):
+        arr = (L.KernelStatC * 64)()
+        cnt = C.c_int()
+        L.check(L.load().cp_stats_get(self._h, arr, 64, C.byref(cnt)))
+        return {arr[k].name.decode(): {"launches": arr[k].launches, "ms": arr[k].ms, "alg_bytes": arr[k].alg_bytes}
+                for k in range(min(cnt.value, 64))}
+
+
+def default_context(device: int = 0) -> Context:
+    ctx = _ctx_cache.get(device)
+    if ctx is None:
+        ctx = Context(device)
+        _ctx_cache[device] = ctx
+    return ctx
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _dp(a):
+    return a.ctypes.data_as(L.D) if a is not None else None
+
+
+def _ip(a):
+    return a.ctypes.data_as(L.I64) if a is not None else None
+
+
+# ---- types.hpp ---------------------------------------------------------------
+
+class DataMatrix:
+    """DataMatrix (types.hpp:16-22) held in HBM.  ``values``: (n, d) samples."""
+
+    def __init__(self, values, feature_names: Optional[Sequence[str]] = None, ctx: Optional[Context] = None):
+        v = np.asarray(values, dtype=np.float64)
+        if v.ndim != 2 or v.shape[0] < 1 or v.shape[1] < 1:
+            raise ValueError("data matrix must have at least one feature and one sample")
+        self.values = np.ascontiguousarray(v)
+        names = list(feature_names or [])
+        if names:
+            if len(names) != v.shape[1]:
+                raise ValueError("feature_names size does not match feature count")
+            if any(not s for s in names):
+                raise ValueError("feature_names entries must be non-empty")
+        self.feature_names = names
+        self.ctx = ctx or default_context()
+        h = C.c_void_p()
+        L.check(L.load().cp_data_create(self.ctx._h, _dp(self.values), v.shape[1], v.shape[0], C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and L._lib is not None:
+            L._lib.cp_data_destroy(self._h)
+            self._h = None
+
+    @property
+    def d(self):
+        return self.values.shape[1]
+
+    @property
+    def n(self):
+        return self.values.shape[0]
+
+
+def make_data_matrix(values, feature_names=None, ctx=None) -> DataMatrix:
+    """make_data_matrix (graph.cpp:10-23)."""
+    return DataMatrix(values, feature_names, ctx)
+
+
+# ---- graph.hpp ---------------------------------------------------------------
+
+class WeightedGraph:
+    """WeightedGraph (graph.hpp:23-51): sorted, validated, device-resident."""
+
+    def __init__(self, n: int = 0, edges: Optional[Sequence] = None, ctx: Optional[Context] = None, _handle=None):
+        self.ctx = ctx or default_context()
+        if _handle is not None:
+            self._h = _handle
+        else:
+            edges = list(edges or [])
+            i = np.array([e[0] for e in edges], dtype=np.int64)
+            j = np.array([e[1] for e in edges], dtype=np.int64)
+            w = np.array([e[2] for e in edges], dtype=np.float64)
+            h = C.c_void_p()
+            L.check(L.load().cp_graph_from_edges(self.ctx._h, int(n), _ip(i), _ip(j), _dp(w), len(edges), C.byref(h)))
+            self._h = h
+        self._arrays = None
+
+    @classmethod
+    def from_arrays(cls, n, i, j, w, ctx=None):
+        ctx = ctx or default_context()
+        i = np.ascontiguousarray(i, dtype=np.int64)
+        j = np.ascontiguousarray(j, dtype=np.int64)
+        w = _f64(w)
+        h = C.c_void_p()
+        L.check(L.load().cp_graph_from_edges(ctx._h, int(n), _ip(i), _ip(j), _dp(w), len(i), C.byref(h)))
+        return cls(ctx=ctx, _handle=h)
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and L._lib is not None:
+            L._lib.cp_graph_destroy(self._h)
+            self._h = None
+
+    def nodes(self) -> int:
+        return L.load().cp_graph_nodes(self._h)
+
+    def edge_count(self) -> int:
+        return L.load().cp_graph_edge_count(self._h)
+
+    def arrays(self):
+        """(i, j, w, d2) in list order; d2 = kNN squared distances (NaN otherwise)."""
+        if self._arrays is None:
+            E = self.edge_count()
+            i = np.empty(E, np.int64)
+            j = np.empty(E, np.int64)
+            w = np.empty(E, np.float64)
+            d2 = np.empty(E, np.float64)
+            L.check(L.load().cp_graph_export(self.ctx._h, self._h, _ip(i), _ip(j), _dp(w), _dp(d2)))
+            self._arrays = (i, j, w, d2)
+        return self._arrays
+
+    def edges(self):
+        i, j, w, _ = self.arrays()
+        return [(int(a), int(b), float(c)) for a, b, c in zip(i, j, w)]
+
+    def edge(self, l):
+        i, j, w, _ = self.arrays()
+        return (int(i[l]), int(j[l]), float(w[l]))
+
+    def weights(self):
+        return self.arrays()[2].copy()
+
+    def degrees(self):
+        deg = np.empty(self.nodes(), np.int64)
+        L.check(L.load().cp_graph_degrees(self.ctx._h, self._h, _ip(deg)))
+        return deg
+
+    def degree(self, v):
+        if v < 0 or v >= self.nodes():
+            raise ValueError("node index out of range")
+        return int(self.degrees()[v])
+
+    def max_degree(self):
+        deg = self.degrees()
+        return int(deg.max()) if len(deg) else 0
+
+    def find_edge(self, i, j):
+        """graph.cpp:47-56: position of (i, j) in the sorted list, or None."""
+        if i > j:
+            i, j = j, i
+        a, b, _, _ = self.arrays()
+        keys = list(zip(a.tolist(), b.tolist()))
+        p = bisect.bisect_left(keys, (i, j))
+        return p if p < len(keys) and keys[p] == (i, j) else None
+
+
+def compute_knn_weights(data: DataMatrix, k: int, phi: float) -> WeightedGraph:
+    """compute_knn_weights (graph.hpp:58; graph.cpp:75-114), on the GPU."""
+    h = C.c_void_p()
+    L.check(L.load().cp_knn_graph(data.ctx._h, data._h, int(k), float(phi), C.byref(h)))
+    return WeightedGraph(ctx=data.ctx, _handle=h)
+
+
+class IncidenceOperator:
+    """IncidenceOperator (graph.hpp:62-86): X B and Z B^T on the GPU."""
+
+    def __init__(self, graph: WeightedGraph):
+        self.graph = graph
+
+    def nodes(self):
+        return self.graph.nodes()
+
+    def edge_count(self):
+        return self.graph.edge_count()
+
+    def apply(self, X):
+        X = _f64(X)
+        if X.ndim != 2:
+            raise ValueError("incidence apply: operand must be a matrix")
+        out = np.empty((self.graph.edge_count(), X.shape[1]))
+        L.check(L.load().cp_incidence_apply(self.graph.ctx._h, self.graph._h, _dp(X), X.shape[1], X.shape[0],
+                                            _dp(out)))
+        return out
+
+    def apply_transpose(self, Z):
+        Z = _f64(Z)
+        if Z.ndim != 2:
+            raise ValueError("incidence adjoint: operand must be a matrix")
+        out = np.empty((self.graph.nodes(), Z.shape[1]))
+        L.check(L.load().cp_incidence_apply_t(self.graph.ctx._h, self.graph._h, _dp(Z), Z.shape[1], Z.shape[0],
+                                              _dp(out)))
+        return out
+
+    def laplacian_lambda_max(self, tol=1e-9, max_iter=10000):
+        """power_iteration(LinearOperator::sparse(laplacian())) (linalg.cpp:194-242)."""
+        out = C.c_double()
+        L.check(L.load().cp_laplacian_lambda_max(self.graph.ctx._h, self.graph._h, tol, int(max_iter), C.byref(out)))
+        return out.value
+
+
+def connected_components(graph: WeightedGraph):
+    """connected_components (graph.cpp:169-196): first-appearance labels."""
+    lab = np.empty(graph.nodes(), np.int64)
+    K = C.c_int64()
+    L.check(L.load().cp_connected_components(graph.ctx._h, graph._h, _ip(lab), C.byref(K)))
+    return lab
+
+
+def component_count(labels) -> int:
+    labels = np.asarray(labels)
+    return int(labels.max()) + 1 if len(labels) else 0
+
+
+# ---- prox.hpp ----------------------------------------------------------------
+
+class PenaltyNorm(enum.IntEnum):
+    l1 = 1
+    l2 = 2
+
+
+def penalty_norm_from_q(q: int) -> PenaltyNorm:
+    if q == 1:
+        return PenaltyNorm.l1
+    if q == 2:
+        return PenaltyNorm.l2
+    raise ValueError(f"penalty norm exponent must be 1 or 2, got {q}")
+
+
+def _cols_call(fn, q, V, t, ctx):
+    V = _f64(V)
+    if V.ndim != 2:
+        raise ValueError("columns must be given as a matrix")
+    t = _f64(t).reshape(-1)
+    if len(t) != V.shape[0]:
+        raise ValueError("one threshold per column required")
+    out = np.empty_like(V)
+    ctx = ctx or default_context()
+    L.check(fn(ctx._h, int(q), _dp(V), _dp(t), V.shape[1], V.shape[0], _dp(out)))
+    return out
+
+
+def prox_columns(V, thresholds, norm=PenaltyNorm.l2, ctx=None):
+    """prox_columns_into (prox.cpp:73-80): per-column prox of t_l ||.||_q."""
+    return _cols_call(L.load().cp_prox_columns, int(norm), V, thresholds, ctx)
+
+
+def project_columns(Z, radii, norm=PenaltyNorm.l2, ctx=None):
+    """project_columns (prox.cpp:82-93): per-column dual-ball projection."""
+    return _cols_call(L.load().cp_project_columns, int(norm), Z, radii, ctx)
+
+
+def prox_jacobian_diag(V, thresholds, norm=PenaltyNorm.l2, ctx=None):
+    """ProxJacobian::diag per column (prox.cpp:106-132)."""
+    return _cols_call(L.load().cp_prox_jacobian_diag, int(norm), V, thresholds, ctx)
+
+
+# ---- solvers.hpp ---------------------------------------------------------------
+
+class Algorithm(enum.IntEnum):
+    ADMM = 0
+    FastAMA = 1
+    SSNAL = 2
+
+
+def algorithm_from_name(name: str) -> Algorithm:
+    if name == "admm":
+        return Algorithm.ADMM
+    if name in ("ama", "fast-ama", "fastama"):
+        return Algorithm.FastAMA
+    if name == "ssnal":
+        return Algorithm.SSNAL
+    raise ValueError(f"unknown solver '{name}' (expected ssnal, admm or ama)")
+
+
+def algorithm_name(a) -> str:
+    return {0: "admm", 1: "ama", 2: "ssnal"}[int(a)]
+
+
+@dataclass
+class SolverConfig:
+    """SolverConfig (solvers.hpp:72-93) with the reference defaults."""
+    algorithm: Algorithm = Algorithm.SSNAL
+    epsilon: float = 1e-6
+    kkt_factor: float = 10.0
+    max_iter: int = 0
+    time_limit: Optional[float] = None
+    admm_rho: float = 1.0
+    ama_step_safety: float = 0.99
+    ssnal_sigma0: float = 1.0
+    armijo_mu: float = 1e-4
+    backtrack_beta: float = 0.5
+    ssnal_newton_max: int = 50
+    pcg_max_iter: int = 500
+    collect_trace: bool = False
+
+    def to_c(self):
+        if self.time_limit is not None and not (self.time_limit > 0):
+            raise ValueError("config: time_limit must be positive when set")
+        alg = self.algorithm if not isinstance(self.algorithm, str) else algorithm_from_name(self.algorithm)
+        return L.SolverConfigC(int(alg), int(self.collect_trace), self.epsilon, self.kkt_factor, int(self.max_iter),
+                               float(self.time_limit or 0.0), self.admm_rho, self.ama_step_safety, self.ssnal_sigma0,
+                               self.armijo_mu, self.backtrack_beta, int(self.ssnal_newton_max),
+                               int(self.pcg_max_iter))
+
+    def resolved_max_iter(self):
+        if self.max_iter > 0:
+            return self.max_iter
+        return 100 if int(self.algorithm) == 2 else 20000
+
+
+@dataclass
+class TerminationRecord:
+    f_primal: float = 0.0
+    f_dual: float = 0.0
+    gap: float = 0.0
+    iterations: int = 0
+    converged: bool = False
+    wall_time: float = 0.0
+    newton: int = 0
+    cg: int = 0
+    armijo: int = 0
+    hess_apply: int = 0
+
+    @classmethod
+    def from_c(cls, t):
+        return cls(t.f_primal, t.f_dual, t.gap, t.iterations, bool(t.converged), t.wall_time, t.newton, t.cg,
+                   t.armijo, t.hess_apply)
+
+
+@dataclass
+class Solution:
+    X: np.ndarray
+    Z: np.ndarray
+    termination: TerminationRecord = field(default_factory=TerminationRecord)
+
+
+class ProblemInstance:
+    """ProblemInstance (solvers.hpp:26-43)."""
+
+    def __init__(self, data: DataMatrix, graph: WeightedGraph, gamma: float, norm=PenaltyNorm.l2):
+        if data.n != graph.nodes():
+            raise ValueError(f"instance: graph has {graph.nodes()} nodes for {data.n} samples")
+        if not (gamma >= 0.0) or not np.isfinite(gamma):
+            raise ValueError("instance: gamma must be finite and >= 0")
+        self.data, self.graph, self.gamma, self.norm = data, graph, float(gamma), int(norm)
+        self.B = IncidenceOperator(graph)
+
+    def penalty_radii(self):
+        return self.gamma * self.graph.weights()
+
+    def d(self):
+        return self.data.d
+
+    def n(self):
+        return self.data.n
+
+    def edge_count(self):
+        return self.graph.edge_count()
+
+    def _args(self):
+        return self.data.ctx._h, self.data._h, self.graph._h, self.gamma, self.norm
+
+
+def primal_objective(inst: ProblemInstance, X) -> float:
+    X = _f64(X)
+    if X.shape != (inst.n(), inst.d()):
+        raise ValueError("primal_objective: X has the wrong shape")
+    out = C.c_double()
+    L.check(L.load().cp_primal_objective(*inst._args(), _dp(X), C.byref(out)))
+    return out.value
+
+
+def dual_objective(inst: ProblemInstance, Z) -> float:
+    Z = _f64(Z)
+    if Z.shape != (inst.edge_count(), inst.d()):
+        raise ValueError("dual_objective: Z has the wrong shape")
+    out = C.c_double()
+    L.check(L.load().cp_dual_objective(*inst._args(), _dp(Z), C.byref(out)))
+    return out.value
+
+
+def duality_gap(f_p, f_d) -> float:
+    return abs(f_p - f_d) / (1.0 + abs(f_p) + abs(f_d))
+
+
+def recover_primal(inst: ProblemInstance, Z):
+    return inst.data.values - inst.B.apply_transpose(Z)
+
+
+def kkt_residual(inst: ProblemInstance, X, Z) -> float:
+    X, Z = _f64(X), _f64(Z)
+    if X.shape != (inst.n(), inst.d()):
+        raise ValueError("kkt_residual: X has the wrong shape")
+    if Z.shape != (inst.edge_count(), inst.d()):
+        raise ValueError("kkt_residual: Z has the wrong shape")
+    out = C.c_double()
+    L.check(L.load().cp_kkt_residual(*inst._args(), _dp(X), _dp(Z), C.byref(out)))
+    return out.value
+
+
+def ssnal_phi_value(inst, Z, sigma, X) -> float:
+    out = C.c_double()
+    L.check(L.load().cp_ssnal_phi_value(*inst._args(), _dp(_f64(Z)), float(sigma), _dp(_f64(X)), C.byref(out)))
+    return out.value
+
+
+def ssnal_phi_gradient(inst, Z, sigma, X):
+    out = np.empty((inst.n(), inst.d()))
+    L.check(L.load().cp_ssnal_phi_gradient(*inst._args(), _dp(_f64(Z)), float(sigma), _dp(_f64(X)), _dp(out)))
+    return out
+
+
+def ssnal_hessian_apply(inst, Z, sigma, X, D):
+    out = np.empty((inst.n(), inst.d()))
+    L.check(L.load().cp_ssnal_hessian_apply(*inst._args(), _dp(_f64(Z)), float(sigma), _dp(_f64(X)), _dp(_f64(D)),
+                                            _dp(out)))
+    return out
+
+
+def solve(inst: ProblemInstance, config: Optional[SolverConfig] = None, warm: Optional[Solution] = None) -> Solution:
+    """solve (objective.cpp:115-123) -> solve_ssnal / solve_admm / solve_fast_ama on the GPU."""
+    config = config or SolverConfig()
+    cfg = config.to_c()
+    n, d, E = inst.n(), inst.d(), inst.edge_count()
+    X = np.empty((n, d))
+    Z = np.empty((E, d))
+    t = L.TerminationC()
+    wx = wz = None
+    wshape = (0, 0, 0)
+    if warm is not None:
+        wx, wz = _f64(warm.X), _f64(warm.Z)
+        if wx.ndim != 2 or wz.ndim != 2 or wx.shape[1] != wz.shape[1]:
+            raise ValueError("warm start does not match the instance shapes")
+        wshape = (wx.shape[1], wx.shape[0], wz.shape[0])
+    L.check(L.load().cp_solve(*inst._args(), C.byref(cfg), _dp(wx), wshape[0], wshape[1], _dp(wz), wshape[2], _dp(X),
+                              _dp(Z), C.byref(t)))
+    return Solution(X, Z, TerminationRecord.from_c(t))
+
+
+# ---- path.hpp --------------------------------------------------------------------
+
+class Spacing(enum.IntEnum):
+    linear = 0
+    geometric = 1
+
+
+@dataclass
+class GammaSchedule:
+    values: List[float]
+    start: float = 0.0
+    end: float = 0.0
+    count: int = 0
+    spacing: Spacing = Spacing.geometric
+
+
+def make_schedule(start, end, count, spacing=Spacing.geometric) -> GammaSchedule:
+    """make_schedule (path.cpp:21-58)."""
+    out = np.empty(max(int(count), 1))
+    L.check(L.load().cp_make_schedule(float(start), float(end), int(count), int(spacing), _dp(out)))
+    return GammaSchedule(out[:int(count)].tolist(), float(start), float(end), int(count), Spacing(int(spacing)))
+
+
+@dataclass
+class ClusterAssignment:
+    labels: np.ndarray
+    K: int
+    centroids: np.ndarray
+
+
+def extract_clusters(X, graph: WeightedGraph, fuse_tol: float = 1e-3) -> ClusterAssignment:
+    """extract_clusters (path.cpp:60-89) on the GPU."""
+    X = _f64(X)
+    n, d = X.shape
+    lab = np.empty(n, np.int64)
+    K = C.c_int64()
+    cent = np.empty((n, d))
+    L.check(L.load().cp_extract_clusters(graph.ctx._h, graph._h, _dp(X), d, n, float(fuse_tol), _ip(lab), C.byref(K),
+                                         _dp(cent)))
+    return ClusterAssignment(lab, K.value, cent[:K.value].copy())
+
+
+@dataclass
+class PathOptions:
+    warm_start: bool = True
+    require_connected: bool = False
+    fuse_tol: float = 1e-3
+
+
+@dataclass
+class PathResult:
+    schedule: GammaSchedule
+    solutions: List[Solution]
+    assignments: List[ClusterAssignment]
+    stats: List[TerminationRecord]
+    solver: SolverConfig
+
+    def all_converged(self):
+        return all(s.converged for s in self.stats)
+
+
+def run_path(data: DataMatrix, graph: WeightedGraph, norm, schedule: GammaSchedule, config: Optional[SolverConfig] = None,
+             options: Optional[PathOptions] = None, keep_solutions: bool = True) -> PathResult:
+    """run_path (path.cpp:110-142): warm-started gamma sweep, all on the GPU."""
+    config = config or SolverConfig()
+    options = options or PathOptions()
+    gam = _f64(schedule.values)
+    T = len(gam)
+    if T == 0:
+        raise ValueError("run_path: empty schedule")
+    n, d, E = data.n, data.d, graph.edge_count()
+    X = np.empty((T, n, d)) if keep_solutions else None
+    Z = np.empty((T, E, d)) if keep_solutions else None
+    lab = np.empty((T, n), np.int64)
+    K = np.empty(T, np.int64)
+    terms = (L.TerminationC * T)()
+    cfg = config.to_c()
+    opt = L.PathOptionsC(int(options.warm_start), int(options.require_connected), float(options.fuse_tol))
+    L.check(L.load().cp_run_path(data.ctx._h, data._h, graph._h, int(norm), _dp(gam), T, C.byref(cfg), C.byref(opt),
+                                 _dp(X), _dp(Z), _ip(lab), _ip(K), terms))
+    stats = [TerminationRecord.from_c(t) for t in terms]
+    sols = [Solution(X[t] if X is not None else None, Z[t] if Z is not None else None, stats[t]) for t in range(T)]
+    asg = [ClusterAssignment(lab[t], int(K[t]), None) for t in range(T)]
+    return PathResult(schedule, sols, asg, stats, config)
+
+
+def two_point_closed_form(a1, a2, w, gamma):
+    """path.cpp:91-103 (host arithmetic, used by tests)."""
+    a1, a2 = np.asarray(a1, float), np.asarray(a2, float)
+    if a1.shape != a2.shape:
+        raise ValueError("two_point_closed_form: dimension mismatch")
+    if not w > 0:
+        raise ValueError("two_point_closed_form: weight must be positive")
+    if not gamma >= 0:
+        raise ValueError("two_point_closed_form: gamma must be >= 0")
+    c = a1 - a2
+    nc = float(np.linalg.norm(c))
+    if nc == 0.0:
+        return a1.copy(), a2.copy()
+    s = min(2.0 * gamma * w / nc, 1.0)
+    return a1 - 0.5 * s * c, a2 + 0.5 * s * c

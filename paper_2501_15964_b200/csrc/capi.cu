@@ -1,0 +1,543 @@
+// The extern "C" boundary (include/cluspath_b200.h).  Every entry point maps
+// host buffers to device state, runs the sm_100a kernels and maps exceptions
+// to return codes (CP_EINVAL = std::invalid_argument, CP_ERUNTIME =
+// std::runtime_error) with a thread-local message.  There is no CPU fallback:
+// without a CUDA device cp_ctx_create fails with CP_ERUNTIME.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "solve.cuh"
+
+struct cp_ctx {
+  std::unique_ptr<cpb::Ctx> c;
+};
+struct cp_data {
+  cpb::Data d;
+};
+struct cp_graph {
+  std::unique_ptr<cpb::Graph> g;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(cp_ctx* ctx, F f) {
+  try {
+    if (ctx && ctx->c) cudaSetDevice(ctx->c->device);
+    f();
+    return CP_OK;
+  } catch (const cpb::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return CP_EINVAL;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return CP_ERUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return CP_ERUNTIME;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) cpb::invalid(std::string(what) + " must not be null");
+}
+void check_q(int q) {
+  if (q != 1 && q != 2) cpb::invalid("penalty norm exponent must be 1 or 2, got " + std::to_string(q));
+}
+
+double* upload(cpb::Ctx& c, const char* name, const double* h, int64_t count) {
+  double* d = c.buf<double>(name, count + 1);
+  cpb::h2d(c, d, h, count * sizeof(double));
+  return d;
+}
+
+__global__ void k_finite(const double* a, int64_t m, int* bad) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (!isfinite(a[p])) atomicOr(bad, 1);
+}
+
+// ProblemInstance validation (objective.cpp:26-33)
+cpb::Prob make_prob(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q) {
+  need(A, "data");
+  need(g, "graph");
+  check_q(q);
+  if (A->d.n != g->g->n)
+    cpb::invalid("instance: graph has " + std::to_string(g->g->n) + " nodes for " + std::to_string(A->d.n) +
+                 " samples");
+  if (!(gamma >= 0.0) || !std::isfinite(gamma)) cpb::invalid("instance: gamma must be finite and >= 0");
+  cpb::Prob P;
+  P.c = ctx->c.get();
+  P.A = const_cast<cpb::Data*>(&A->d);
+  P.g = g->g.get();
+  P.gamma = gamma;
+  P.q = q;
+  P.rad = P.c->buf<double>("api.rad", g->g->E + 1);
+  cpb::make_radii(*P.c, *P.g, gamma, P.rad);
+  return P;
+}
+
+void check_shape(int64_t rows, int64_t cols, int64_t er, int64_t ec, const char* what) {
+  if (rows != er || cols != ec) cpb::invalid(std::string(what) + " has the wrong shape");
+}
+}  // namespace
+
+extern "C" {
+
+const char* cp_last_error(void) { return g_err.c_str(); }
+
+void cp_solver_config_default(cp_solver_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->algorithm = 2;
+  c->epsilon = 1e-6;
+  c->kkt_factor = 10.0;
+  c->max_iter = 0;
+  c->time_limit = 0.0;
+  c->admm_rho = 1.0;
+  c->ama_step_safety = 0.99;
+  c->ssnal_sigma0 = 1.0;
+  c->armijo_mu = 1e-4;
+  c->backtrack_beta = 0.5;
+  c->ssnal_newton_max = 50;
+  c->pcg_max_iter = 500;
+}
+void cp_path_options_default(cp_path_options* o) {
+  o->warm_start = 1;
+  o->require_connected = 0;
+  o->fuse_tol = 1e-3;
+}
+
+int cp_ctx_create(int device, cp_ctx** out) {
+  return guard(nullptr, [&] {
+    need(out, "out");
+    auto* c = new cp_ctx;
+    try {
+      c->c = std::make_unique<cpb::Ctx>(device);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+void cp_ctx_destroy(cp_ctx* ctx) {
+  if (!ctx) return;
+  try {
+    delete ctx;
+  } catch (...) {
+  }
+}
+int cp_ctx_synchronize(cp_ctx* ctx) {
+  return guard(ctx, [&] { ctx->c->sync(); });
+}
+int cp_device_info(cp_ctx* ctx, int* sm_major, int* sm_minor, int* sm_count, int* built_arch) {
+  return guard(ctx, [&] {
+    if (sm_major) *sm_major = ctx->c->sm_major;
+    if (sm_minor) *sm_minor = ctx->c->sm_minor;
+    if (sm_count) *sm_count = ctx->c->sm_count;
+    if (built_arch) *built_arch = 100;
+  });
+}
+int cp_stats_enable(cp_ctx* ctx, int on) {
+  return guard(ctx, [&] { ctx->c->stats_on = on != 0; });
+}
+int cp_stats_reset(cp_ctx* ctx) {
+  return guard(ctx, [&] {
+    ctx->c->sync();
+    ctx->c->drain_stats();
+    ctx->c->stats.clear();
+  });
+}
+int cp_stats_get(cp_ctx* ctx, cp_kernel_stat* out, int max_entries, int* count) {
+  return guard(ctx, [&] {
+    ctx->c->sync();
+    ctx->c->drain_stats();
+    int k = 0;
+    for (auto& [name, st] : ctx->c->stats) {
+      if (k < max_entries && out) {
+        std::memset(&out[k], 0, sizeof(cp_kernel_stat));
+        std::strncpy(out[k].name, name.c_str(), sizeof(out[k].name) - 1);
+        out[k].launches = st.launches;
+        out[k].ms = st.ms;
+        out[k].alg_bytes = st.bytes;
+      }
+      ++k;
+    }
+    if (count) *count = k;
+  });
+}
+
+// ---- data ---------------------------------------------------------------------
+int cp_data_create(cp_ctx* ctx, const double* A, int64_t d, int64_t n, cp_data** out) {
+  return guard(ctx, [&] {
+    need(out, "out");
+    if (d < 1 || n < 1) cpb::invalid("data matrix must have at least one feature and one sample");
+    need(A, "A");
+    cpb::Ctx& c = *ctx->c;
+    auto p = std::make_unique<cp_data>();
+    p->d.d = d;
+    p->d.n = n;
+    p->d.A.resize(d * n);
+    cpb::h2d(c, p->d.A.p, A, d * n * sizeof(double));
+    int* bad = c.buf<int>("api.bad", 1);
+    CPB_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.s));
+    k_finite<<<std::max(1, std::min(cpb::cdiv(d * n, 256), c.sm_count * 4)), 256, 0, c.s>>>(p->d.A.p, d * n, bad);
+    CPB_LAUNCH_CHECK();
+    int h = 0;
+    cpb::d2h(c, &h, bad, sizeof(int));
+    if (h) cpb::invalid("data matrix contains non-finite entries");
+    *out = p.release();
+  });
+}
+void cp_data_destroy(cp_data* data) { delete data; }
+
+// ---- graph --------------------------------------------------------------------
+int cp_knn_graph(cp_ctx* ctx, const cp_data* data, int64_t k, double phi, cp_graph** out) {
+  return guard(ctx, [&] {
+    need(data, "data");
+    need(out, "out");
+    auto g = std::make_unique<cp_graph>();
+    g->g = cpb::knn_graph(*ctx->c, data->d, k, phi);
+    *out = g.release();
+  });
+}
+int cp_graph_from_edges(cp_ctx* ctx, int64_t n, const int64_t* i, const int64_t* j, const double* w, int64_t E,
+                        cp_graph** out) {
+  return guard(ctx, [&] {
+    need(out, "out");
+    if (E < 0) cpb::invalid("edge count must be nonnegative");
+    if (E > 0) {
+      need(i, "i");
+      need(j, "j");
+      need(w, "w");
+    }
+    auto g = std::make_unique<cp_graph>();
+    g->g = cpb::graph_from_edges(*ctx->c, n, i, j, w, E);
+    *out = g.release();
+  });
+}
+void cp_graph_destroy(cp_graph* g) { delete g; }
+int64_t cp_graph_nodes(const cp_graph* g) { return g ? g->g->n : 0; }
+int64_t cp_graph_edge_count(const cp_graph* g) { return g ? g->g->E : 0; }
+int cp_graph_export(cp_ctx* ctx, const cp_graph* g, int64_t* i, int64_t* j, double* w, double* d2) {
+  return guard(ctx, [&] {
+    need(g, "graph");
+    cpb::Ctx& c = *ctx->c;
+    const int64_t E = g->g->E;
+    if (E == 0) return;
+    std::vector<int> tmp(static_cast<size_t>(E));
+    if (i) {
+      cpb::d2h(c, tmp.data(), g->g->ei.p, E * sizeof(int));
+      for (int64_t l = 0; l < E; ++l) i[l] = tmp[static_cast<size_t>(l)];
+    }
+    if (j) {
+      cpb::d2h(c, tmp.data(), g->g->ej.p, E * sizeof(int));
+      for (int64_t l = 0; l < E; ++l) j[l] = tmp[static_cast<size_t>(l)];
+    }
+    if (w) cpb::d2h(c, w, g->g->w.p, E * sizeof(double));
+    if (d2) cpb::d2h(c, d2, g->g->d2.p, E * sizeof(double));
+  });
+}
+int cp_graph_degrees(cp_ctx* ctx, const cp_graph* g, int64_t* degree) {
+  return guard(ctx, [&] {
+    need(g, "graph");
+    need(degree, "degree");
+    const int64_t n = g->g->n;
+    std::vector<int> off(static_cast<size_t>(n + 1));
+    cpb::d2h(*ctx->c, off.data(), g->g->off.p, (n + 1) * sizeof(int));
+    for (int64_t v = 0; v < n; ++v) degree[v] = off[static_cast<size_t>(v + 1)] - off[static_cast<size_t>(v)];
+  });
+}
+
+int cp_incidence_apply(cp_ctx* ctx, const cp_graph* g, const double* X, int64_t d, int64_t n, double* out) {
+  return guard(ctx, [&] {
+    need(g, "graph");
+    if (n != g->g->n)
+      cpb::invalid("incidence apply: operand has " + std::to_string(n) + " columns, graph has " +
+                   std::to_string(g->g->n) + " nodes");
+    if (d < 0) cpb::invalid("incidence apply: negative row count");
+    cpb::Ctx& c = *ctx->c;
+    const int64_t E = g->g->E;
+    if (E * d == 0) return;
+    double* dx = upload(c, "api.x", X, d * n);
+    double* dout = c.buf<double>("api.o", E * d);
+    cpb::incidence_apply_dev(c, *g->g, dx, d, dout);
+    cpb::d2h(c, out, dout, E * d * sizeof(double));
+  });
+}
+int cp_incidence_apply_t(cp_ctx* ctx, const cp_graph* g, const double* Z, int64_t d, int64_t E, double* out) {
+  return guard(ctx, [&] {
+    need(g, "graph");
+    if (E != g->g->E)
+      cpb::invalid("incidence adjoint: operand has " + std::to_string(E) + " columns, graph has " +
+                   std::to_string(g->g->E) + " edges");
+    if (d < 0) cpb::invalid("incidence adjoint: negative row count");
+    cpb::Ctx& c = *ctx->c;
+    const int64_t n = g->g->n;
+    if (n * d == 0) return;
+    double* dz = upload(c, "api.z", Z, d * E);
+    double* dout = c.buf<double>("api.o", n * d);
+    cpb::incidence_apply_t_dev(c, *g->g, dz, d, dout);
+    cpb::d2h(c, out, dout, n * d * sizeof(double));
+  });
+}
+int cp_connected_components(cp_ctx* ctx, const cp_graph* g, int64_t* labels, int64_t* K) {
+  return guard(ctx, [&] {
+    need(g, "graph");
+    cpb::Ctx& c = *ctx->c;
+    const int64_t n = g->g->n;
+    int* lab = c.buf<int>("api.lab", n + 1);
+    const int64_t k = cpb::components_dev(c, *g->g, nullptr, lab);
+    std::vector<int> h(static_cast<size_t>(n));
+    cpb::d2h(c, h.data(), lab, n * sizeof(int));
+    if (labels)
+      for (int64_t v = 0; v < n; ++v) labels[v] = h[static_cast<size_t>(v)];
+    if (K) *K = k;
+  });
+}
+int cp_laplacian_lambda_max(cp_ctx* ctx, const cp_graph* g, double tol, int64_t max_iter, double* lambda) {
+  return guard(ctx, [&] {
+    need(g, "graph");
+    need(lambda, "lambda");
+    *lambda = cpb::laplacian_lambda_max(*ctx->c, *g->g, tol, max_iter);
+  });
+}
+
+// ---- prox ---------------------------------------------------------------------
+}  // extern "C"
+namespace {
+void check_thresholds(const double* t, int64_t E, const char* what) {
+  for (int64_t l = 0; l < E; ++l)
+    if (!(t[l] >= 0.0) || !std::isfinite(t[l]))
+      cpb::invalid(std::string(what) + ": threshold must be finite and >= 0");
+}
+template <class F>
+int columns_call(cp_ctx* ctx, int q, const double* V, const double* t, int64_t d, int64_t E, double* out,
+                 const char* what, F f) {
+  return guard(ctx, [&] {
+    check_q(q);
+    if (d < 0 || E < 0) cpb::invalid(std::string(what) + ": negative shape");
+    if (E > 0) need(t, "thresholds");
+    check_thresholds(t, E, what);
+    if (d * E == 0) return;
+    cpb::Ctx& c = *ctx->c;
+    double* dv = upload(c, "api.v", V, d * E);
+    double* dt = upload(c, "api.t", t, E);
+    double* dout = c.buf<double>("api.o", d * E);
+    f(c, dv, dt, dout);
+    cpb::d2h(c, out, dout, d * E * sizeof(double));
+  });
+}
+}  // namespace
+extern "C" {
+
+int cp_prox_columns(cp_ctx* ctx, int q, const double* V, const double* thresholds, int64_t d, int64_t E,
+                    double* out) {
+  return columns_call(ctx, q, V, thresholds, d, E, out, "prox_norm",
+                      [&](cpb::Ctx& c, double* v, double* t, double* o) { cpb::prox_columns_dev(c, q, v, t, d, E, o); });
+}
+int cp_project_columns(cp_ctx* ctx, int q, const double* Z, const double* radii, int64_t d, int64_t E, double* out) {
+  return columns_call(ctx, q, Z, radii, d, E, out, "project_dual_ball", [&](cpb::Ctx& c, double* v, double* t, double* o) {
+    cpb::project_columns_dev(c, q, v, t, d, E, o);
+  });
+}
+int cp_prox_jacobian_diag(cp_ctx* ctx, int q, const double* V, const double* thresholds, int64_t d, int64_t E,
+                          double* out) {
+  return columns_call(ctx, q, V, thresholds, d, E, out, "prox_jacobian",
+                      [&](cpb::Ctx& c, double* v, double* t, double* o) {
+                        cpb::prox_jacobian_diag_dev(c, q, v, t, d, E, o);
+                      });
+}
+
+// ---- objectives -----------------------------------------------------------------
+int cp_primal_objective(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q, const double* X,
+                        double* out) {
+  return guard(ctx, [&] {
+    cpb::Prob P = make_prob(ctx, A, g, gamma, q);
+    double* dx = upload(*P.c, "api.x", X, P.d() * P.n());
+    *out = cpb::primal_objective_dev(P, dx);
+  });
+}
+int cp_dual_objective(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q, const double* Z,
+                      double* out) {
+  return guard(ctx, [&] {
+    cpb::Prob P = make_prob(ctx, A, g, gamma, q);
+    double* dz = upload(*P.c, "api.z", Z, P.d() * P.E());
+    *out = cpb::dual_objective_dev(P, dz);
+  });
+}
+int cp_kkt_residual(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q, const double* X,
+                    const double* Z, double* out) {
+  return guard(ctx, [&] {
+    cpb::Prob P = make_prob(ctx, A, g, gamma, q);
+    double* dx = upload(*P.c, "api.x", X, P.d() * P.n());
+    double* dz = upload(*P.c, "api.z", Z, P.d() * P.E());
+    *out = cpb::kkt_residual_dev(P, dx, dz);
+  });
+}
+
+}  // extern "C"
+namespace {
+// eval_phi at (Z, sigma, X) into api buffers; returns phi.
+double phi_at(cpb::Prob& P, const double* Z, double sigma, const double* X, double** V, double** nv, double** thr,
+              double** dx) {
+  if (!(sigma > 0.0)) cpb::invalid("ssnal: sigma must be positive");
+  cpb::Ctx& c = *P.c;
+  const int64_t d = P.d(), n = P.n(), E = P.E();
+  *dx = upload(c, "api.x", X, d * n);
+  double* dz = upload(c, "api.z", Z, d * E);
+  *thr = c.buf<double>("api.thr", E + 1);
+  *V = c.buf<double>("api.V", d * E + 1);
+  *nv = c.buf<double>("api.nv", E + 1);
+  cpb::make_thr(c, E, P.rad, sigma, *thr);
+  const double zz = cpb::dot_dev(c, dz, dz, d * E);
+  return cpb::eval_phi(P, *dx, nullptr, 0.0, nullptr, dz, sigma, *thr, zz, *V, *nv);
+}
+}  // namespace
+extern "C" {
+
+int cp_ssnal_phi_value(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q, const double* Z,
+                       double sigma, const double* X, double* out) {
+  return guard(ctx, [&] {
+    cpb::Prob P = make_prob(ctx, A, g, gamma, q);
+    double *V, *nv, *thr, *dx;
+    *out = phi_at(P, Z, sigma, X, &V, &nv, &thr, &dx);
+  });
+}
+int cp_ssnal_phi_gradient(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q, const double* Z,
+                          double sigma, const double* X, double* out) {
+  return guard(ctx, [&] {
+    cpb::Prob P = make_prob(ctx, A, g, gamma, q);
+    cpb::Ctx& c = *P.c;
+    double *V, *nv, *thr, *dx;
+    phi_at(P, Z, sigma, X, &V, &nv, &thr, &dx);
+    const int64_t E = P.E(), m = P.d() * P.n();
+    double* ps = c.buf<double>("api.ps", E + 1);
+    double* jal = c.buf<double>("api.jal", E + 1);
+    double* jbe = c.buf<double>("api.jbe", E + 1);
+    double* G = c.buf<double>("api.G", m);
+    double* diag = c.buf<double>("api.diag", m);
+    cpb::jac_params(P, nv, thr, ps, jal, jbe);
+    cpb::grad_diag(P, dx, V, ps, jal, jbe, thr, sigma, G, diag, false);
+    cpb::d2h(c, out, G, m * sizeof(double));
+  });
+}
+int cp_ssnal_hessian_apply(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q, const double* Z,
+                           double sigma, const double* X, const double* D, double* out) {
+  return guard(ctx, [&] {
+    cpb::Prob P = make_prob(ctx, A, g, gamma, q);
+    cpb::Ctx& c = *P.c;
+    double *V, *nv, *thr, *dx;
+    phi_at(P, Z, sigma, X, &V, &nv, &thr, &dx);
+    const int64_t E = P.E(), m = P.d() * P.n();
+    double* ps = c.buf<double>("api.ps", E + 1);
+    double* jal = c.buf<double>("api.jal", E + 1);
+    double* jbe = c.buf<double>("api.jbe", E + 1);
+    cpb::jac_params(P, nv, thr, ps, jal, jbe);
+    double* dd = upload(c, "api.D", D, m);
+    double* Ap = c.buf<double>("api.Ap", m);
+    double* part = c.buf<double>("api.hpart", 2 * static_cast<size_t>(c.sm_count) * 8 + 2);
+    cpb::hess_apply(P, dd, V, jal, jbe, thr, sigma, Ap, part);
+    cpb::d2h(c, out, Ap, m * sizeof(double));
+  });
+}
+
+// ---- solve / path ---------------------------------------------------------------
+int cp_solve(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int q, const cp_solver_config* cfg,
+             const double* warmX, int64_t warm_d, int64_t warm_n, const double* warmZ, int64_t warm_E, double* X,
+             double* Z, cp_termination* term) {
+  return guard(ctx, [&] {
+    cp_solver_config def;
+    cp_solver_config_default(&def);
+    const cp_solver_config& cf = cfg ? *cfg : def;
+    cpb::Prob P = make_prob(ctx, A, g, gamma, q);
+    cpb::validate_config(cf);
+    cpb::Ctx& c = *P.c;
+    const int64_t d = P.d(), n = P.n(), E = P.E();
+    double* dx = c.buf<double>("api.sX", d * n + 1);
+    double* dz = c.buf<double>("api.sZ", d * E + 1);
+    const bool trivial = !(gamma > 0.0) || E == 0;
+    const bool warm = warmX && warmZ && !trivial;
+    if (warm) {
+      if (warm_d != d || warm_n != n || warm_E != E) cpb::invalid("warm start does not match the instance shapes");
+      cpb::h2d(c, dx, warmX, d * n * sizeof(double));
+      cpb::h2d(c, dz, warmZ, d * E * sizeof(double));
+    }
+    cpb::SolveCache cache;
+    cp_termination t = cpb::solve_dev(P, cf, warm, dx, dz, cache);
+    if (X) cpb::d2h(c, X, dx, d * n * sizeof(double));
+    if (Z && d * E) cpb::d2h(c, Z, dz, d * E * sizeof(double));
+    if (term) *term = t;
+  });
+}
+
+int cp_make_schedule(double start, double end, int64_t count, int geometric, double* out) {
+  return guard(nullptr, [&] {
+    if (!(start > 0.0) || !(end > 0.0) || !std::isfinite(start) || !std::isfinite(end))
+      cpb::invalid("schedule endpoints must be positive and finite");
+    if (count < 1) cpb::invalid("schedule count must be >= 1");
+    if (count > 1 && start == end) cpb::invalid("schedule with count > 1 needs distinct endpoints");
+    need(out, "out");
+    if (count == 1) {
+      out[0] = start;
+      return;
+    }
+    const double lo = std::min(start, end), hi = std::max(start, end);
+    if (!geometric) {
+      for (int64_t t = 0; t < count; ++t)
+        out[t] = lo + (hi - lo) * static_cast<double>(t) / static_cast<double>(count - 1);
+    } else {
+      const double lr = std::log(hi / lo) / static_cast<double>(count - 1);
+      for (int64_t t = 0; t < count; ++t) out[t] = lo * std::exp(static_cast<double>(t) * lr);
+    }
+    out[0] = lo;
+    out[count - 1] = hi;
+    for (int64_t t = 1; t < count; ++t)
+      if (!(out[t] > out[t - 1])) cpb::invalid("schedule endpoints too close: values are not strictly increasing");
+  });
+}
+
+int cp_extract_clusters(cp_ctx* ctx, const cp_graph* g, const double* X, int64_t d, int64_t n, double fuse_tol,
+                        int64_t* labels, int64_t* K, double* centroids) {
+  return guard(ctx, [&] {
+    need(g, "graph");
+    if (n != g->g->n) cpb::invalid("extract_clusters: X column count != node count");
+    if (!(fuse_tol > 0.0)) cpb::invalid("extract_clusters: fuse_tol must be positive");
+    cpb::Ctx& c = *ctx->c;
+    double* dx = upload(c, "api.x", X, d * n);
+    int* lab = c.buf<int>("api.lab", n + 1);
+    double* cent = centroids ? c.buf<double>("api.cent", d * n + 1) : nullptr;
+    const int64_t k = cpb::extract_clusters_dev(c, *g->g, dx, d, fuse_tol, lab, cent);
+    std::vector<int> h(static_cast<size_t>(n));
+    cpb::d2h(c, h.data(), lab, n * sizeof(int));
+    if (labels)
+      for (int64_t v = 0; v < n; ++v) labels[v] = h[static_cast<size_t>(v)];
+    if (K) *K = k;
+    if (centroids) cpb::d2h(c, centroids, cent, d * k * sizeof(double));
+  });
+}
+
+int cp_run_path(cp_ctx* ctx, const cp_data* A, const cp_graph* g, int q, const double* gammas, int64_t T,
+                const cp_solver_config* cfg, const cp_path_options* opt, double* X_out, double* Z_out,
+                int64_t* labels_out, int64_t* K_out, cp_termination* terms_out) {
+  return guard(ctx, [&] {
+    need(A, "data");
+    need(g, "graph");
+    check_q(q);
+    if (T > 0) need(gammas, "gammas");
+    cp_solver_config defc;
+    cp_solver_config_default(&defc);
+    cp_path_options defo;
+    cp_path_options_default(&defo);
+    cpb::run_path_dev(*ctx->c, const_cast<cpb::Data&>(A->d), *g->g, q, gammas, T, cfg ? *cfg : defc,
+                      opt ? *opt : defo, X_out, Z_out, labels_out, K_out, terms_out);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,741 @@
+// Graph construction and graph-level kernels (graph.cpp of the reference).
+//
+//  * knn_graph: compute_knn_weights (graph.cpp:75-114).  The pairwise squared
+//    distances are computed in FP64 in exactly the order Eigen 3.4's SSE2
+//    squaredNorm adds them (four interleaved chains, then the packet tail), so
+//    every distance — and therefore every (dist, j) ranking, the edge set and
+//    the edge order — is bit-identical to the reference.  A fused per-row
+//    top-k (lexicographic (dist, j), ties to the smaller index, graph.cpp:97-98)
+//    keeps only k candidates per row: the n x n matrix is never materialised.
+//  * graph_from_edges: WeightedGraph(n, edges) (graph.cpp:25-45) on device.
+//  * finalize_graph: node CSR (incident edges ascending), degree order.
+//  * incidence operator B / Bᵀ (graph.cpp:122-152): Bᵀ is an atomic-free
+//    node-CSR gather accumulating in ascending edge id, hence bitwise equal to
+//    the reference's scatter loop.
+//  * components_dev: min-label hooking + pointer jumping; labels ranked by
+//    each component's smallest node = DFS first-appearance order (graph.cpp:169-196).
+//  * laplacian_lambda_max: power_iteration on B Bᵀ (linalg.cpp:194-242).
+#include <cub/cub.cuh>
+#include <math_constants.h>
+
+#include <cmath>
+#include <random>
+
+#include "graph.cuh"
+
+namespace cpb {
+
+namespace {
+
+// ---- row-kernel geometry -----------------------------------------------------
+// Rows (nodes or edges) of length d are processed by dx threads (features)
+// times dy rows per 256-thread block.
+struct RowGeom {
+  int dx, dy;
+};
+inline RowGeom row_geom(int64_t d) {
+  int dx = 32;
+  while (dx < d && dx < 256) dx <<= 1;
+  return {dx, 256 / dx};
+}
+inline int row_grid(Ctx& c, int64_t rows, RowGeom g) {
+  return std::max(1, std::min(cdiv(rows, g.dy), c.sm_count * 16));
+}
+
+// ---- kNN: exact FP64 tiled distances + fused top-k -----------------------------
+constexpr int KB_M = 32, KB_N = 64, KB_K = 16, KB_LIST = 32;
+
+__device__ __forceinline__ bool lex_less(double a, int ja, double b, int jb) {
+  return a < b || (a == b && ja < jb);
+}
+
+__device__ __forceinline__ double sqdiff(double a, double b) {
+  const double t = __dsub_rn(a, b);
+  return __dmul_rn(t, t);
+}
+
+// Finish one Eigen-order squared norm from the four chain sums and the packet
+// tail (Redux.h LinearVectorizedTraversal; see oracle/oracle.hpp esum).
+__device__ __forceinline__ double eigen_finish(double c0, double c1, double c2, double c3, const double* __restrict__ x,
+                                               const double* __restrict__ y, int d, int e2) {
+  if (d < 4) {
+    double r = sqdiff(x[0], y[0]);
+    if (d >= 2) r = __dadd_rn(r, sqdiff(x[1], y[1]));
+    if (d == 3) r = __dadd_rn(r, sqdiff(x[2], y[2]));
+    return r;
+  }
+  double p0 = __dadd_rn(c0, c2), p1 = __dadd_rn(c1, c3);
+  if (d - e2 >= 2) {
+    p0 = __dadd_rn(p0, sqdiff(x[e2], y[e2]));
+    p1 = __dadd_rn(p1, sqdiff(x[e2 + 1], y[e2 + 1]));
+  }
+  double r = __dadd_rn(p0, p1);
+  if (d & 1) r = __dadd_rn(r, sqdiff(x[d - 1], y[d - 1]));
+  return r;
+}
+
+// One block: KB_M query rows against all n samples, KB_N columns at a time.
+// Thread (tx, ty) of 16 x 16 owns rows {ty, ty+16} x cols {tx + 16 tn}.
+__global__ void __launch_bounds__(256) k_knn_topk(const double* __restrict__ A, int n, int d, int e2, int k,
+                                                  double* __restrict__ out_d, int* __restrict__ out_j) {
+  __shared__ double sA[KB_K][KB_M];
+  __shared__ double sB[KB_K][KB_N];
+  __shared__ double sD[KB_M][KB_N + 1];
+  __shared__ double sLd[KB_M][KB_LIST];
+  __shared__ int sLj[KB_M][KB_LIST];
+
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int row0 = blockIdx.x * KB_M;
+
+  for (int p = tid; p < KB_M * KB_LIST; p += 256) {
+    sLd[p / KB_LIST][p % KB_LIST] = CUDART_INF;
+    sLj[p / KB_LIST][p % KB_LIST] = 0x7fffffff;
+  }
+
+  for (int col0 = 0; col0 < n; col0 += KB_N) {
+    double acc[2][4][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[a][b][q] = 0.0;
+
+    for (int k0 = 0; k0 < e2; k0 += KB_K) {
+      __syncthreads();
+      for (int p = tid; p < KB_M * KB_K; p += 256) {
+        const int r = p / KB_K, kk = p % KB_K, gr = row0 + r, gk = k0 + kk;
+        sA[kk][r] = (gr < n && gk < e2) ? A[static_cast<int64_t>(gr) * d + gk] : 0.0;
+      }
+      for (int p = tid; p < KB_N * KB_K; p += 256) {
+        const int r = p / KB_K, kk = p % KB_K, gr = col0 + r, gk = k0 + kk;
+        sB[kk][r] = (gr < n && gk < e2) ? A[static_cast<int64_t>(gr) * d + gk] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < KB_K; kk += 4) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double a0 = sA[kk + q][ty], a1 = sA[kk + q][ty + 16];
+          double b[4];
+#pragma unroll
+          for (int tn = 0; tn < 4; ++tn) b[tn] = sB[kk + q][tx + 16 * tn];
+#pragma unroll
+          for (int tn = 0; tn < 4; ++tn) {
+            acc[0][tn][q] = __dadd_rn(acc[0][tn][q], sqdiff(a0, b[tn]));
+            acc[1][tn][q] = __dadd_rn(acc[1][tn][q], sqdiff(a1, b[tn]));
+          }
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int tm = 0; tm < 2; ++tm)
+#pragma unroll
+      for (int tn = 0; tn < 4; ++tn) {
+        const int r = row0 + ty + 16 * tm, cidx = col0 + tx + 16 * tn;
+        double dist = CUDART_INF;
+        if (r < n && cidx < n)
+          dist = eigen_finish(acc[tm][tn][0], acc[tm][tn][1], acc[tm][tn][2], acc[tm][tn][3],
+                              A + static_cast<int64_t>(r) * d, A + static_cast<int64_t>(cidx) * d, d, e2);
+        sD[ty + 16 * tm][tx + 16 * tn] = dist;
+      }
+    __syncthreads();
+    // merge: warp w owns rows 4w..4w+3
+    for (int rr = warp * 4; rr < warp * 4 + 4; ++rr) {
+      const int r = row0 + rr;
+      if (r >= n) continue;
+      for (int half = 0; half < 2; ++half) {
+        const int cl = lane + 32 * half, j = col0 + cl;
+        const double dd = sD[rr][cl];
+        const double td = sLd[rr][k - 1];
+        const int tj = sLj[rr][k - 1];
+        const bool cand = j < n && j != r && lex_less(dd, j, td, tj);
+        unsigned mask = __ballot_sync(0xffffffffu, cand);
+        while (mask) {
+          const int src = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const double cd = __shfl_sync(0xffffffffu, dd, src);
+          const int cj = __shfl_sync(0xffffffffu, j, src);
+          const double kd = sLd[rr][k - 1];
+          const int kj = sLj[rr][k - 1];
+          if (!lex_less(cd, cj, kd, kj)) continue;  // list tightened meanwhile (warp-uniform)
+          double ed = CUDART_INF;
+          int ej = 0x7fffffff;
+          if (lane < k) {
+            ed = sLd[rr][lane];
+            ej = sLj[rr][lane];
+          }
+          const unsigned lt = __ballot_sync(0xffffffffu, lane < k && lex_less(ed, ej, cd, cj));
+          const int pos = __popc(lt);
+          double pd = __shfl_up_sync(0xffffffffu, ed, 1);
+          int pj = __shfl_up_sync(0xffffffffu, ej, 1);
+          __syncwarp();
+          if (lane < k) {
+            if (lane == pos) {
+              sLd[rr][lane] = cd;
+              sLj[rr][lane] = cj;
+            } else if (lane > pos) {
+              sLd[rr][lane] = pd;
+              sLj[rr][lane] = pj;
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int p = tid; p < KB_M * k; p += 256) {
+    const int rr = p / k, m = p % k, r = row0 + rr;
+    if (r < n) {
+      out_d[static_cast<int64_t>(r) * k + m] = sLd[rr][m];
+      out_j[static_cast<int64_t>(r) * k + m] = sLj[rr][m];
+    }
+  }
+}
+
+// Fallback for k > 32: full distance rows (Eigen order, one thread per pair),
+// then a stable segmented radix sort per row.
+__global__ void k_knn_rows(const double* __restrict__ A, int n, int d, int e2, int r0, int rows,
+                           unsigned long long* __restrict__ keys, int* __restrict__ vals) {
+  const int64_t total = static_cast<int64_t>(rows) * n;
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < total;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int rr = static_cast<int>(p / n), j = static_cast<int>(p % n), i = r0 + rr;
+    const double* x = A + static_cast<int64_t>(i) * d;
+    const double* y = A + static_cast<int64_t>(j) * d;
+    double c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    for (int q = 0; q < e2; q += 4) {
+      c0 = __dadd_rn(c0, sqdiff(x[q], y[q]));
+      c1 = __dadd_rn(c1, sqdiff(x[q + 1], y[q + 1]));
+      c2 = __dadd_rn(c2, sqdiff(x[q + 2], y[q + 2]));
+      c3 = __dadd_rn(c3, sqdiff(x[q + 3], y[q + 3]));
+    }
+    const double dist = eigen_finish(c0, c1, c2, c3, x, y, d, e2);
+    keys[p] = (j == i) ? ~0ull : static_cast<unsigned long long>(__double_as_longlong(dist));
+    vals[p] = j;
+  }
+}
+__global__ void k_knn_take(const unsigned long long* __restrict__ keys, const int* __restrict__ vals, int n, int r0,
+                           int rows, int k, double* __restrict__ out_d, int* __restrict__ out_j) {
+  const int64_t total = static_cast<int64_t>(rows) * k;
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < total;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int rr = static_cast<int>(p / k), m = static_cast<int>(p % k);
+    const int64_t src = static_cast<int64_t>(rr) * n + m;
+    out_d[static_cast<int64_t>(r0 + rr) * k + m] = __longlong_as_double(static_cast<long long>(keys[src]));
+    out_j[static_cast<int64_t>(r0 + rr) * k + m] = vals[src];
+  }
+}
+__global__ void k_seg_offsets(int* off, int rows, int n) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t <= rows) off[t] = t * n;
+}
+
+// (min, max) pair keys carrying the squared distance.
+__global__ void k_pair_keys(const double* __restrict__ kd, const int* __restrict__ kj, int n, int k,
+                            unsigned long long* __restrict__ key, double* __restrict__ val) {
+  const int64_t total = static_cast<int64_t>(n) * k;
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < total;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(p / k), j = kj[p];
+    const unsigned long long a = static_cast<unsigned long long>(min(i, j)), b = static_cast<unsigned long long>(max(i, j));
+    key[p] = a * static_cast<unsigned long long>(n) + b;
+    val[p] = kd[p];
+  }
+}
+// Keep the first of each run of equal keys whose weight does not underflow
+// (graph.cpp:104-111); w = exp(-phi * d2).
+__global__ void k_pair_flags(const unsigned long long* __restrict__ key, const double* __restrict__ d2, int64_t m,
+                             double phi, unsigned char* __restrict__ flag, double* __restrict__ w) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double wt = exp(__dmul_rn(-phi, d2[p]));
+    w[p] = wt;
+    flag[p] = (p == 0 || key[p] != key[p - 1]) && wt > 0.0;
+  }
+}
+__global__ void k_decode_pairs(const unsigned long long* __restrict__ key, int64_t E, int n, int* ei, int* ej) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < E;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    ei[p] = static_cast<int>(key[p] / static_cast<unsigned long long>(n));
+    ej[p] = static_cast<int>(key[p] % static_cast<unsigned long long>(n));
+  }
+}
+
+// ---- WeightedGraph(n, edges) ----------------------------------------------------
+__global__ void k_validate_edges(const long long* __restrict__ i, const long long* __restrict__ j,
+                                 const double* __restrict__ w, int64_t E, long long n, int* err) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < E;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const long long a = i[p], b = j[p];
+    const double x = w[p];
+    if (a < 0 || b < 0 || a >= n || b >= n) atomicOr(err, 1);
+    else if (a >= b) atomicOr(err, 2);
+    else if (!(x > 0.0) || !isfinite(x)) atomicOr(err, 4);
+  }
+}
+__global__ void k_edge_keys(const long long* __restrict__ i, const long long* __restrict__ j, int64_t E,
+                            long long n, unsigned long long* key, int* idx) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < E;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    key[p] = static_cast<unsigned long long>(i[p]) * static_cast<unsigned long long>(n) +
+             static_cast<unsigned long long>(j[p]);
+    idx[p] = static_cast<int>(p);
+  }
+}
+__global__ void k_gather_edges(const unsigned long long* __restrict__ key, const int* __restrict__ idx,
+                               const double* __restrict__ win, int64_t E, long long n, int* ei, int* ej, double* w,
+                               double* d2, int* dup) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < E;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    ei[p] = static_cast<int>(key[p] / static_cast<unsigned long long>(n));
+    ej[p] = static_cast<int>(key[p] % static_cast<unsigned long long>(n));
+    w[p] = win[idx[p]];
+    d2[p] = CUDART_NAN;
+    if (p > 0 && key[p] == key[p - 1]) atomicOr(dup, 1);
+  }
+}
+
+// ---- CSR -------------------------------------------------------------------------
+__global__ void k_csr_entries(const int* __restrict__ ei, const int* __restrict__ ej, int E, int* key, int* val,
+                              int* deg) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < E; p += gridDim.x * blockDim.x) {
+    key[p] = ej[p];
+    val[p] = p;
+    key[E + p] = ei[p];
+    val[E + p] = p;
+    atomicAdd(deg + ei[p], 1);
+    atomicAdd(deg + ej[p], 1);
+  }
+}
+__global__ void k_csr_other(const int* __restrict__ key, const int* __restrict__ adj_e, const int* __restrict__ ei,
+                            const int* __restrict__ ej, int m, int* adj_o) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < m; p += gridDim.x * blockDim.x) {
+    const int v = key[p], l = adj_e[p];
+    adj_o[p] = (ei[l] == v) ? ej[l] : ei[l];
+  }
+}
+__global__ void k_iota(int* p, int n) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) p[t] = t;
+}
+
+// ---- incidence operator -----------------------------------------------------------
+__global__ void k_incidence(const double* __restrict__ X, const int* __restrict__ ei, const int* __restrict__ ej,
+                            int64_t E, int d, double* __restrict__ out) {
+  for (int64_t l = blockIdx.x * static_cast<int64_t>(blockDim.y) + threadIdx.y; l < E;
+       l += static_cast<int64_t>(gridDim.x) * blockDim.y) {
+    const double* a = X + static_cast<int64_t>(ei[l]) * d;
+    const double* b = X + static_cast<int64_t>(ej[l]) * d;
+    double* o = out + l * d;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = __dsub_rn(a[f], b[f]);
+  }
+}
+__global__ void k_incidence_t(const double* __restrict__ Z, const int* __restrict__ off, const int* __restrict__ adj_e,
+                              const int* __restrict__ adj_o, int64_t n, int d, double* __restrict__ out) {
+  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.y) + threadIdx.y; v < n;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.y) {
+    const int p0 = off[v], p1 = off[v + 1];
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      double acc = 0.0;
+      for (int p = p0; p < p1; ++p) {
+        const double z = Z[static_cast<int64_t>(adj_e[p]) * d + f];
+        acc = (adj_o[p] > v) ? __dadd_rn(acc, z) : __dsub_rn(acc, z);
+      }
+      out[v * d + f] = acc;
+    }
+  }
+}
+
+// ---- connected components ------------------------------------------------------------
+__global__ void k_cc_hook(const int* __restrict__ ei, const int* __restrict__ ej, const unsigned char* __restrict__ flag,
+                          int E, int* L, int* changed) {
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < E; l += gridDim.x * blockDim.x) {
+    if (flag && !flag[l]) continue;
+    const int a = L[ei[l]], b = L[ej[l]];
+    if (a != b) {
+      atomicMin(L + max(a, b), min(a, b));
+      *changed = 1;
+    }
+  }
+}
+__global__ void k_cc_jump(int* L, int n) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int x = L[v];
+    while (true) {
+      const int y = L[x];
+      if (y == x) break;
+      x = y;
+    }
+    L[v] = x;
+  }
+}
+__global__ void k_cc_roots(const int* __restrict__ L, int n, int* root) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) root[v] = (L[v] == v);
+}
+__global__ void k_cc_label(const int* __restrict__ L, const int* __restrict__ rank, int n, int* labels) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) labels[v] = rank[L[v]];
+}
+
+// ---- Laplacian power iteration -------------------------------------------------------------
+// y_v = sum over column order of L's column-major CSC (SparseDenseProduct.h):
+// neighbours ascending with the degree term at position v.
+__device__ __forceinline__ void lap_apply(const int* __restrict__ off, const int* __restrict__ adj_o,
+                                          const double* __restrict__ x, double* __restrict__ y, int n) {
+  for (int v = threadIdx.x; v < n; v += blockDim.x) {
+    const int p0 = off[v], p1 = off[v + 1];
+    const double deg = static_cast<double>(p1 - p0);
+    double acc = 0.0;
+    bool diag_done = (p1 == p0);
+    for (int p = p0; p < p1; ++p) {
+      const int u = adj_o[p];
+      if (!diag_done && u > v) {
+        acc = __dadd_rn(acc, __dmul_rn(deg, x[v]));
+        diag_done = true;
+      }
+      acc = __dsub_rn(acc, x[u]);
+    }
+    if (!diag_done) acc = __dadd_rn(acc, __dmul_rn(deg, x[v]));
+    y[v] = acc;
+  }
+}
+__device__ double blk_dot(const double* a, const double* b, int n, double* sh) {
+  double s = 0.0;
+  for (int v = threadIdx.x; v < n; v += blockDim.x) s = __dadd_rn(s, __dmul_rn(a[v], b[v]));
+  return block_sum(s, sh);
+}
+__global__ void __launch_bounds__(1024) k_power(const int* __restrict__ off, const int* __restrict__ adj_o,
+                                                const double* __restrict__ start, int n, double tol, long long max_iter,
+                                                double* v, double* w, double* out) {
+  __shared__ double sh[32];
+  const double ns = sqrt(blk_dot(start, start, n, sh));
+  for (int t = threadIdx.x; t < n; t += blockDim.x) v[t] = __ddiv_rn(start[t], ns);
+  __syncthreads();
+  double prev = 0.0, est = 0.0;
+  int dead = 0;
+  for (long long it = 1; it <= max_iter; ++it) {
+    lap_apply(off, adj_o, v, w, n);
+    __syncthreads();
+    const double nw = sqrt(blk_dot(w, w, n, sh));
+    if (nw <= 1e-300) {
+      dead = 1;
+      break;
+    }
+    const double lam = blk_dot(v, w, n, sh);
+    est = lam;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) v[t] = __ddiv_rn(w[t], nw);
+    __syncthreads();
+    if (it > 1 && fabs(lam - prev) <= tol * fmax(fabs(lam), 1e-300)) break;
+    prev = lam;
+  }
+  if (threadIdx.x == 0) {
+    out[0] = est;
+    out[1] = dead;
+  }
+}
+
+// ---- data norms --------------------------------------------------------------------------------
+__global__ void k_sumsq(const double* __restrict__ x, int64_t count, double* partial) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < count;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    s = __dadd_rn(s, __dmul_rn(x[p], x[p]));
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+template <class F>
+void cub_call(Ctx& c, const char* tag, F f) {
+  size_t bytes = 0;
+  CPB_CUDA(f(nullptr, bytes));
+  void* tmp = c.buf<char>(std::string("cub.") + tag, bytes + 16);
+  CPB_CUDA(f(tmp, bytes));
+}
+
+uint64_t next_uid() {
+  static uint64_t u = 0;
+  return ++u;
+}
+
+}  // namespace
+
+// ===========================================================================================
+void finalize_graph(Ctx& c, Graph& g) {
+  const int n = static_cast<int>(g.n), E = static_cast<int>(g.E);
+  g.uid = next_uid();
+  g.off.resize(n + 1);
+  g.adj_e.resize(2 * static_cast<size_t>(E));
+  g.adj_o.resize(2 * static_cast<size_t>(E));
+  g.order.resize(n);
+  int* deg = c.buf<int>("csr.deg", n + 1);
+  CPB_CUDA(cudaMemsetAsync(deg, 0, (n + 1) * sizeof(int), c.s));
+  if (E > 0) {
+    int* key = c.buf<int>("csr.key", 2 * static_cast<size_t>(E));
+    int* val = c.buf<int>("csr.val", 2 * static_cast<size_t>(E));
+    int* key2 = c.buf<int>("csr.key2", 2 * static_cast<size_t>(E));
+    k_csr_entries<<<std::min(cdiv(E, 256), c.sm_count * 8), 256, 0, c.s>>>(g.ei.p, g.ej.p, E, key, val, deg);
+    CPB_LAUNCH_CHECK();
+    int bits = 1;
+    while ((1ll << bits) < n) ++bits;
+    const int m = 2 * E;
+    cub_call(c, "csr.sort", [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, key, key2, val, g.adj_e.p, m, 0, bits, c.s);
+    });
+    k_csr_other<<<std::min(cdiv(m, 256), c.sm_count * 8), 256, 0, c.s>>>(key2, g.adj_e.p, g.ei.p, g.ej.p, m,
+                                                                          g.adj_o.p);
+    CPB_LAUNCH_CHECK();
+  }
+  cub_call(c, "csr.scan", [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, deg, g.off.p, n + 1, c.s);
+  });
+  // max degree and descending-degree node order
+  int* node = c.buf<int>("csr.node", n);
+  int* degs = c.buf<int>("csr.degs", n);
+  k_iota<<<std::max(1, std::min(cdiv(n, 256), c.sm_count * 8)), 256, 0, c.s>>>(node, n);
+  CPB_LAUNCH_CHECK();
+  if (n > 0) {
+    cub_call(c, "csr.order", [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairsDescending(t, b, deg, degs, node, g.order.p, n, 0, 32, c.s);
+    });
+    int md = 0;
+    CPB_CUDA(cudaMemcpyAsync(&md, degs, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+    c.sync();
+    g.max_degree = md;
+  }
+}
+
+std::unique_ptr<Graph> graph_from_edges(Ctx& c, int64_t n, const int64_t* i, const int64_t* j, const double* w,
+                                        int64_t E) {
+  if (n < 0) invalid("graph node count must be nonnegative");
+  if (n >= (1ll << 31) - 1 || 2 * E >= (1ll << 31) - 1) invalid("graph too large for 32-bit indices");
+  auto g = std::make_unique<Graph>();
+  g->n = n;
+  g->E = E;
+  g->ei.resize(E);
+  g->ej.resize(E);
+  g->w.resize(E);
+  g->d2.resize(E);
+  if (E > 0) {
+    long long* di = c.buf<long long>("fe.i", E);
+    long long* dj = c.buf<long long>("fe.j", E);
+    double* dw = c.buf<double>("fe.w", E);
+    int* err = c.buf<int>("fe.err", 2);
+    h2d(c, di, i, E * sizeof(long long));
+    h2d(c, dj, j, E * sizeof(long long));
+    h2d(c, dw, w, E * sizeof(double));
+    CPB_CUDA(cudaMemsetAsync(err, 0, 2 * sizeof(int), c.s));
+    const int grid = std::min(cdiv(E, 256), c.sm_count * 8);
+    k_validate_edges<<<grid, 256, 0, c.s>>>(di, dj, dw, E, n, err);
+    CPB_LAUNCH_CHECK();
+    int herr[2] = {0, 0};
+    d2h(c, herr, err, 2 * sizeof(int));
+    if (herr[0] & 1) invalid("edge endpoint out of range");
+    if (herr[0] & 2) invalid("edges must satisfy i < j");
+    if (herr[0] & 4) invalid("edge weights must be positive and finite");
+    auto* key = c.buf<unsigned long long>("fe.key", E);
+    auto* key2 = c.buf<unsigned long long>("fe.key2", E);
+    int* idx = c.buf<int>("fe.idx", E);
+    int* idx2 = c.buf<int>("fe.idx2", E);
+    k_edge_keys<<<grid, 256, 0, c.s>>>(di, dj, E, n, key, idx);
+    CPB_LAUNCH_CHECK();
+    int bits = 1;
+    while (bits < 64 && (1ull << bits) < static_cast<unsigned long long>(n) * static_cast<unsigned long long>(n)) ++bits;
+    cub_call(c, "fe.sort", [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, key, key2, idx, idx2, static_cast<int>(E), 0, bits, c.s);
+    });
+    k_gather_edges<<<grid, 256, 0, c.s>>>(key2, idx2, dw, E, n, g->ei.p, g->ej.p, g->w.p, g->d2.p, err + 1);
+    CPB_LAUNCH_CHECK();
+    d2h(c, herr, err, 2 * sizeof(int));
+    if (herr[1]) invalid("duplicate edge");
+  }
+  finalize_graph(c, *g);
+  return g;
+}
+
+std::unique_ptr<Graph> knn_graph(Ctx& c, const Data& A, int64_t k, double phi) {
+  const int64_t n = A.n, d = A.d;
+  if (k < 1 || k > n - 1)
+    invalid("compute_knn_weights: k must satisfy 1 <= k <= n-1, got k=" + std::to_string(k) +
+            " with n=" + std::to_string(n));
+  if (!(phi >= 0.0) || !std::isfinite(phi)) invalid("compute_knn_weights: phi must be finite and nonnegative");
+  if (n >= (1ll << 31) - 1 || n * k >= (1ll << 31) - 1) invalid("compute_knn_weights: problem too large");
+  const int e2 = d >= 4 ? static_cast<int>((d / 4) * 4) : 0;
+  const int64_t NK = n * k;
+  double* kd = c.buf<double>("knn.d", NK);
+  int* kj = c.buf<int>("knn.j", NK);
+  {
+    Ctx::Timer tm(&c, "knn_topk", 0.0);
+    if (k <= KB_LIST) {
+      k_knn_topk<<<cdiv(n, KB_M), 256, 0, c.s>>>(A.A.p, static_cast<int>(n), static_cast<int>(d), e2,
+                                                  static_cast<int>(k), kd, kj);
+      CPB_LAUNCH_CHECK();
+    } else {
+      const int64_t rows = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(1) << 26) / n));
+      auto* keys = c.buf<unsigned long long>("knnf.k", rows * n);
+      auto* keys2 = c.buf<unsigned long long>("knnf.k2", rows * n);
+      int* vals = c.buf<int>("knnf.v", rows * n);
+      int* vals2 = c.buf<int>("knnf.v2", rows * n);
+      int* segoff = c.buf<int>("knnf.off", rows + 1);
+      for (int64_t r0 = 0; r0 < n; r0 += rows) {
+        const int rr = static_cast<int>(std::min(rows, n - r0));
+        const int64_t m = static_cast<int64_t>(rr) * n;
+        k_knn_rows<<<std::min(cdiv(m, 256), c.sm_count * 16), 256, 0, c.s>>>(
+            A.A.p, static_cast<int>(n), static_cast<int>(d), e2, static_cast<int>(r0), rr, keys, vals);
+        CPB_LAUNCH_CHECK();
+        k_seg_offsets<<<cdiv(rr + 1, 256), 256, 0, c.s>>>(segoff, rr, static_cast<int>(n));
+        CPB_LAUNCH_CHECK();
+        cub_call(c, "knnf.sort", [&](void* t, size_t& b) {
+          return cub::DeviceSegmentedRadixSort::SortPairs(t, b, keys, keys2, vals, vals2, static_cast<int>(m), rr,
+                                                          segoff, segoff + 1, 0, 64, c.s);
+        });
+        k_knn_take<<<std::min(cdiv(static_cast<int64_t>(rr) * k, 256), c.sm_count * 8), 256, 0, c.s>>>(
+            keys2, vals2, static_cast<int>(n), static_cast<int>(r0), rr, static_cast<int>(k), kd, kj);
+        CPB_LAUNCH_CHECK();
+      }
+    }
+  }
+  // union of (min, max) pairs, sorted and unique, with weights
+  auto* key = c.buf<unsigned long long>("knn.key", NK);
+  auto* key2 = c.buf<unsigned long long>("knn.key2", NK);
+  double* val = c.buf<double>("knn.val", NK);
+  double* val2 = c.buf<double>("knn.val2", NK);
+  double* wv = c.buf<double>("knn.w", NK);
+  auto* flag = c.buf<unsigned char>("knn.flag", NK);
+  const int grid = std::min(cdiv(NK, 256), c.sm_count * 8);
+  k_pair_keys<<<grid, 256, 0, c.s>>>(kd, kj, static_cast<int>(n), static_cast<int>(k), key, val);
+  CPB_LAUNCH_CHECK();
+  int bits = 1;
+  while (bits < 64 && (1ull << bits) < static_cast<unsigned long long>(n) * static_cast<unsigned long long>(n)) ++bits;
+  cub_call(c, "knn.sort", [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, key, key2, val, val2, static_cast<int>(NK), 0, bits, c.s);
+  });
+  k_pair_flags<<<grid, 256, 0, c.s>>>(key2, val2, NK, phi, flag, wv);
+  CPB_LAUNCH_CHECK();
+  int* nsel = c.buf<int>("knn.nsel", 1);
+  // compact keys, d2 and w
+  cub_call(c, "knn.selk", [&](void* t, size_t& b) {
+    return cub::DeviceSelect::Flagged(t, b, key2, flag, key, nsel, static_cast<int>(NK), c.s);
+  });
+  int E = 0;
+  d2h(c, &E, nsel, sizeof(int));
+  auto g = std::make_unique<Graph>();
+  g->n = n;
+  g->E = E;
+  g->ei.resize(E);
+  g->ej.resize(E);
+  g->w.resize(E);
+  g->d2.resize(E);
+  cub_call(c, "knn.seld", [&](void* t, size_t& b) {
+    return cub::DeviceSelect::Flagged(t, b, val2, flag, g->d2.p, nsel, static_cast<int>(NK), c.s);
+  });
+  cub_call(c, "knn.selw", [&](void* t, size_t& b) {
+    return cub::DeviceSelect::Flagged(t, b, wv, flag, g->w.p, nsel, static_cast<int>(NK), c.s);
+  });
+  if (E > 0) {
+    k_decode_pairs<<<std::min(cdiv(E, 256), c.sm_count * 8), 256, 0, c.s>>>(key, E, static_cast<int>(n), g->ei.p,
+                                                                             g->ej.p);
+    CPB_LAUNCH_CHECK();
+  }
+  finalize_graph(c, *g);
+  return g;
+}
+
+void incidence_apply_dev(Ctx& c, const Graph& g, const double* X, int64_t d, double* out) {
+  if (g.E == 0) return;
+  RowGeom rg = row_geom(d);
+  k_incidence<<<row_grid(c, g.E, rg), dim3(rg.dx, rg.dy), 0, c.s>>>(X, g.ei.p, g.ej.p, g.E, static_cast<int>(d), out);
+  CPB_LAUNCH_CHECK();
+}
+
+void incidence_apply_t_dev(Ctx& c, const Graph& g, const double* Z, int64_t d, double* out) {
+  if (g.n == 0) return;
+  RowGeom rg = row_geom(d);
+  k_incidence_t<<<row_grid(c, g.n, rg), dim3(rg.dx, rg.dy), 0, c.s>>>(Z, g.off.p, g.adj_e.p, g.adj_o.p, g.n,
+                                                                      static_cast<int>(d), out);
+  CPB_LAUNCH_CHECK();
+}
+
+int64_t components_dev(Ctx& c, const Graph& g, const unsigned char* flag, int* labels) {
+  const int n = static_cast<int>(g.n), E = static_cast<int>(g.E);
+  if (n == 0) return 0;
+  int* L = c.buf<int>("cc.L", n);
+  int* root = c.buf<int>("cc.root", n + 1);
+  int* rank = c.buf<int>("cc.rank", n + 1);
+  int* changed = c.buf<int>("cc.changed", 1);
+  const int gn = std::max(1, std::min(cdiv(n, 256), c.sm_count * 8));
+  const int ge = std::max(1, std::min(cdiv(E, 256), c.sm_count * 8));
+  k_iota<<<gn, 256, 0, c.s>>>(L, n);
+  CPB_LAUNCH_CHECK();
+  if (E > 0) {
+    for (int iter = 0; iter < 4 * 64 + n; ++iter) {
+      CPB_CUDA(cudaMemsetAsync(changed, 0, sizeof(int), c.s));
+      k_cc_hook<<<ge, 256, 0, c.s>>>(g.ei.p, g.ej.p, flag, E, L, changed);
+      k_cc_jump<<<gn, 256, 0, c.s>>>(L, n);
+      CPB_LAUNCH_CHECK();
+      int h = 0;
+      d2h(c, &h, changed, sizeof(int));
+      if (!h) break;
+    }
+  }
+  k_cc_roots<<<gn, 256, 0, c.s>>>(L, n, root);
+  CPB_CUDA(cudaMemsetAsync(root + n, 0, sizeof(int), c.s));
+  CPB_LAUNCH_CHECK();
+  cub_call(c, "cc.scan", [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, root, rank, n + 1, c.s); });
+  k_cc_label<<<gn, 256, 0, c.s>>>(L, rank, n, labels);
+  CPB_LAUNCH_CHECK();
+  int K = 0;
+  d2h(c, &K, rank + n, sizeof(int));
+  return K;
+}
+
+double laplacian_lambda_max(Ctx& c, const Graph& g, double tol, int64_t max_iter) {
+  if (!(tol > 0.0)) invalid("power_iteration: tol must be positive");
+  if (max_iter < 1) invalid("power_iteration: max_iter must be >= 1");
+  const int64_t n = g.n;
+  if (n == 0) return 0.0;
+  // Probes exactly as linalg.cpp:206-216: two fixed-seed libstdc++ Gaussian draws, then e_0.
+  std::vector<double> starts(3 * static_cast<size_t>(n), 0.0);
+  const uint64_t seeds[2] = {0x5851f42d4c957f2dULL, 0x14057b7ef767814fULL};
+  for (int s = 0; s < 2; ++s) {
+    std::mt19937_64 rng(seeds[s]);
+    std::normal_distribution<double> gauss;
+    for (int64_t v = 0; v < n; ++v) starts[s * n + v] = gauss(rng);
+  }
+  starts[2 * n] = 1.0;
+  double* ds = c.buf<double>("pw.start", 3 * n);
+  double* v = c.buf<double>("pw.v", n);
+  double* w = c.buf<double>("pw.w", n);
+  h2d(c, ds, starts.data(), starts.size() * sizeof(double));
+  double best = 0.0;
+  bool any = false;
+  for (int s = 0; s < 3; ++s) {
+    k_power<<<1, 1024, 0, c.s>>>(g.off.p, g.adj_o.p, ds + s * n, static_cast<int>(n), tol, max_iter, v, w, c.dscal);
+    CPB_LAUNCH_CHECK();
+    double out[2];
+    c.fetch(0, 2, out);
+    if (out[1] == 0.0) {
+      any = true;
+      best = std::max(best, out[0]);
+    }
+  }
+  return any ? best : 0.0;
+}
+
+double data_fro_norm(Ctx& c, Data& A) {
+  if (A.normA >= 0.0) return A.normA;
+  const int64_t m = A.d * A.n;
+  const int grid = std::max(1, std::min(cdiv(m, 256), c.sm_count * 4));
+  double* part = c.buf<double>("norm.part", grid);
+  k_sumsq<<<grid, 256, 0, c.s>>>(A.A.p, m, part);
+  CPB_LAUNCH_CHECK();
+  reduce_sum(c, part, grid, c.dscal);
+  double s;
+  c.fetch(0, 1, &s);
+  A.normA = std::sqrt(s);
+  return A.normA;
+}
+
+}  // namespace cpb

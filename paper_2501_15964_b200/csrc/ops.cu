@@ -1,0 +1,1213 @@
+// Fused solver kernels (see ops.cuh).  Geometry conventions:
+//  * "group" kernels: one row (edge or node) per group of gx = min(32, 2^ceil(log2 d))
+//    lanes of a warp, 256/gx rows per block, lanes striding over the d features;
+//    per-row reductions are group shuffles (no shared memory, no atomics);
+//  * node-gather kernels walk the node CSR (incident edges in ascending edge
+//    id) in descending-degree order so hubs start first;
+//  * "feature-major" kernels (PCG) give every thread a fixed set of features
+//    so per-feature row norms reduce without atomics;
+//  * every reduction is a block partial over a static row partition, then a
+//    fixed-order column reduce: bitwise run-to-run reproducible.
+// All arithmetic is compiled with -fmad=false (elementwise rounding matches the
+// reference's SSE2 build); the cited reference line is given per kernel.
+#include <cmath>
+
+#include "ops.cuh"
+
+namespace cpb {
+
+namespace {
+
+// ---------------------------------------------------------------------------------
+struct GroupGeom {
+  int gx, gy, grid;
+};
+GroupGeom group_geom(Ctx& c, int64_t rows, int64_t d, int per_sm = 8) {
+  int gx = 1;
+  while (gx < d && gx < 32) gx <<= 1;
+  const int gy = 256 / gx;
+  const int grid = std::max(1, std::min(cdiv(rows, gy), c.sm_count * per_sm));
+  return {gx, gy, grid};
+}
+inline int flat_grid(Ctx& c, int64_t m) { return std::max(1, std::min(cdiv(m, 256), c.sm_count * 4)); }
+
+__device__ __forceinline__ double sgnd(double x) { return static_cast<double>((x > 0.0) - (x < 0.0)); }
+// q=1 prox: sign(v) max(|v| - t, 0) (prox.cpp:42)
+__device__ __forceinline__ double soft(double v, double t) { return sgnd(v) * fmax(fabs(v) - t, 0.0); }
+
+#define ROWS_BEGIN(rows)                                                                               \
+  for (int64_t row_ = blockIdx.x * static_cast<int64_t>(blockDim.y) + threadIdx.y; row_ < (rows); \
+       row_ += static_cast<int64_t>(gridDim.x) * blockDim.y)
+
+// ---- flat vector kernels ----------------------------------------------------------
+__global__ void k_scale(const double* __restrict__ x, double s, int64_t m, double* __restrict__ out) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[p] = s * x[p];
+}
+__global__ void k_div(const double* __restrict__ x, double s, int64_t m, double* __restrict__ out) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[p] = x[p] / s;
+}
+__global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b, int64_t m, double* part) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    s += a[p] * b[p];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__global__ void k_maxabs(const double* __restrict__ a, int64_t m, double* part) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    s = fmax(s, fabs(a[p]));
+  s = block_max(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__global__ void k_axpy(double* __restrict__ out, const double* __restrict__ x, double a, const double* __restrict__ y,
+                       int64_t m) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[p] = x[p] + a * y[p];
+}
+__global__ void k_neg(double* __restrict__ out, const double* __restrict__ x, int64_t m) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[p] = -x[p];
+}
+// Xt = X + alpha D (when D) and the partial of ||Xt - A||^2 (ssnal.cpp:37, :174)
+__global__ void k_trial_x(const double* __restrict__ X, const double* __restrict__ D, double alpha,
+                          double* __restrict__ Xt, const double* __restrict__ A, int64_t m, double* part) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double x = X[p];
+    if (D) {
+      x = x + alpha * D[p];
+      Xt[p] = x;
+    }
+    const double t = x - A[p];
+    s += t * t;
+  }
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// ---- prox / projection columns (prox.cpp:33-93, :112-132) -----------------------------
+__global__ void k_prox_cols(int q, const double* __restrict__ V, const double* __restrict__ t, int64_t E, int d,
+                            double* __restrict__ out) {
+  const unsigned gm = group_mask();
+  ROWS_BEGIN(E) {
+    const double* v = V + row_ * d;
+    double* o = out + row_ * d;
+    const double tl = t[row_];
+    if (q == Q_L2) {
+      double ss = 0.0;
+      for (int f = threadIdx.x; f < d; f += blockDim.x) ss += v[f] * v[f];
+      const double nv = sqrt(group_sum(ss, gm));
+      const double s = 1.0 - tl / nv;
+      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = (nv <= tl) ? 0.0 : s * v[f];
+    } else {
+      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = soft(v[f], tl);
+    }
+  }
+}
+__global__ void k_project_cols(int q, const double* __restrict__ Z, const double* __restrict__ r, int64_t E, int d,
+                               double* __restrict__ out) {
+  const unsigned gm = group_mask();
+  ROWS_BEGIN(E) {
+    const double* z = Z + row_ * d;
+    double* o = out + row_ * d;
+    const double rl = r[row_];
+    if (q == Q_L2) {
+      double ss = 0.0;
+      for (int f = threadIdx.x; f < d; f += blockDim.x) ss += z[f] * z[f];
+      const double nz = sqrt(group_sum(ss, gm));
+      const double s = rl / nz;
+      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = (nz <= rl) ? z[f] : s * z[f];
+    } else {
+      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = fmax(fmin(z[f], rl), -rl);
+    }
+  }
+}
+__global__ void k_jac_diag_cols(int q, const double* __restrict__ V, const double* __restrict__ t, int64_t E, int d,
+                                double* __restrict__ out) {
+  const unsigned gm = group_mask();
+  ROWS_BEGIN(E) {
+    const double* v = V + row_ * d;
+    double* o = out + row_ * d;
+    const double tl = t[row_];
+    if (q == Q_L2) {
+      double ss = 0.0;
+      for (int f = threadIdx.x; f < d; f += blockDim.x) ss += v[f] * v[f];
+      const double nv = sqrt(group_sum(ss, gm));
+      double al = 0.0, be = 0.0;
+      if (tl == 0.0) {
+        al = 1.0;
+      } else if (nv > tl) {
+        al = 1.0 - tl / nv;
+        be = tl / (nv * nv * nv);
+      }
+      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = al + (be != 0.0 ? be * v[f] * v[f] : 0.0);
+    } else {
+      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = fabs(v[f]) > tl ? 1.0 : 0.0;
+    }
+  }
+}
+
+// ---- SSNAL: phi edge pass (ssnal.cpp:24-39) -------------------------------------------
+// V = X B + Z / sigma (write), nv = ||V_l||, envelope partial
+//   sum_l gamma w_l ||P_l||_q + sigma/2 ||P_l - V_l||^2.
+__global__ void k_phi_edge(const double* __restrict__ X, const double* __restrict__ Z, const int* __restrict__ ei,
+                           const int* __restrict__ ej, const double* __restrict__ thr, const double* __restrict__ rad,
+                           int64_t E, int d, double sigma, int q, double* __restrict__ V, double* __restrict__ nv,
+                           double* part) {
+  __shared__ double sh[32];
+  const unsigned gm = group_mask();
+  double acc = 0.0;
+  ROWS_BEGIN(E) {
+    const double* xa = X + static_cast<int64_t>(ei[row_]) * d;
+    const double* xb = X + static_cast<int64_t>(ej[row_]) * d;
+    const double* z = Z + row_ * d;
+    double* v = V + row_ * d;
+    const double t = thr[row_];
+    double env;
+    if (q == Q_L2) {
+      double ss = 0.0;
+      for (int f = threadIdx.x; f < d; f += blockDim.x) {
+        const double x = (xa[f] - xb[f]) + z[f] / sigma;
+        v[f] = x;
+        ss += x * x;
+      }
+      ss = group_sum(ss, gm);
+      const double nvl = sqrt(ss);
+      double pn = 0.0, sq = ss;
+      if (!(nvl <= t)) {
+        const double s = 1.0 - t / nvl;
+        double a = 0.0, b = 0.0;
+        for (int f = threadIdx.x; f < d; f += blockDim.x) {
+          const double p = s * v[f];
+          a += p * p;
+          b += (p - v[f]) * (p - v[f]);
+        }
+        pn = sqrt(group_sum(a, gm));
+        sq = group_sum(b, gm);
+      }
+      env = rad[row_] * pn + (0.5 * sigma) * sq;
+      if (threadIdx.x == 0) nv[row_] = nvl;
+    } else {
+      double a = 0.0, b = 0.0;
+      for (int f = threadIdx.x; f < d; f += blockDim.x) {
+        const double x = (xa[f] - xb[f]) + z[f] / sigma;
+        v[f] = x;
+        const double p = soft(x, t);
+        a += fabs(p);
+        b += (p - x) * (p - x);
+      }
+      env = rad[row_] * group_sum(a, gm) + (0.5 * sigma) * group_sum(b, gm);
+      if (threadIdx.x == 0) nv[row_] = 0.0;
+    }
+    if (threadIdx.x == 0) acc += env;
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) part[blockIdx.x] = acc;
+}
+
+// Per-edge prox scale and structural Jacobian (prox.cpp:39-44, :112-132).
+__global__ void k_jac(const double* __restrict__ nv, const double* __restrict__ thr, int64_t E, int q,
+                      double* __restrict__ ps, double* __restrict__ jal, double* __restrict__ jbe, double* part) {
+  __shared__ double sh[32];
+  double cnt = 0.0;
+  for (int64_t l = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; l < E;
+       l += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (q == Q_L2) {
+      const double n = nv[l], t = thr[l];
+      const double s = (n <= t) ? 0.0 : 1.0 - t / n;
+      const double be = (t > 0.0 && n > t) ? t / (n * n * n) : 0.0;
+      ps[l] = s;
+      jal[l] = (t == 0.0) ? 1.0 : s;
+      jbe[l] = be;
+      cnt += (be != 0.0) ? 1.0 : 0.0;
+    } else {
+      cnt += 1.0;
+    }
+  }
+  cnt = block_sum(cnt, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = cnt;
+}
+
+// ---- SSNAL: gradient + Jacobi diagonal (ssnal.cpp:41-44, :68-82) ------------------------
+__global__ void k_grad_diag(const double* __restrict__ X, const double* __restrict__ A, const double* __restrict__ V,
+                            const double* __restrict__ ps, const double* __restrict__ jal,
+                            const double* __restrict__ jbe, const double* __restrict__ thr,
+                            const int* __restrict__ off, const int* __restrict__ adj_e, const int* __restrict__ adj_o,
+                            const int* __restrict__ order, int64_t n, int d, double sigma, int q, int want_diag,
+                            double* __restrict__ G, double* __restrict__ diag, double* part) {
+  __shared__ double sh[32];
+  const unsigned gm = group_mask();
+  double acc = 0.0;
+  ROWS_BEGIN(n) {
+    const int v = order[row_];
+    const int p0 = off[v], p1 = off[v + 1];
+    const int64_t base = static_cast<int64_t>(v) * d;
+    double gg = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      double ag = 0.0, ad = 1.0;
+      for (int p = p0; p < p1; ++p) {
+        const int l = adj_e[p];
+        const double val = V[static_cast<int64_t>(l) * d + f];
+        double u, jd;
+        if (q == Q_L2) {
+          u = val - ps[l] * val;
+          const double be = jbe[l];
+          jd = jal[l] + (be != 0.0 ? be * val * val : 0.0);
+        } else {
+          const double t = thr[l];
+          u = val - soft(val, t);
+          jd = fabs(val) > t ? 1.0 : 0.0;
+        }
+        ag = (adj_o[p] > v) ? ag + u : ag - u;
+        ad += sigma * (1.0 - jd);
+      }
+      const double g = (X[base + f] - A[base + f]) + sigma * ag;
+      G[base + f] = g;
+      if (want_diag) diag[base + f] = ad;
+      gg += g * g;
+    }
+    gg = group_sum(gg, gm);
+    if (threadIdx.x == 0) acc += gg;
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) part[blockIdx.x] = acc;
+}
+
+// ---- SSNAL: Hessian application (ssnal.cpp:56-64) -------------------------------------
+// Ap_v = p_v + sigma sum_{l ni v} +-(I - M_l)(p_i(l) - p_j(l)), gathered in
+// ascending edge id; the group's running sum lives in shared memory.
+__global__ void k_hess(const double* __restrict__ P, const double* __restrict__ V, const double* __restrict__ jal,
+                       const double* __restrict__ jbe, const double* __restrict__ thr, const int* __restrict__ ei,
+                       const int* __restrict__ ej, const int* __restrict__ off, const int* __restrict__ adj_e,
+                       const int* __restrict__ adj_o, const int* __restrict__ order, int64_t n, int d, double sigma,
+                       int q, double* __restrict__ Ap, double* part, const int* active) {
+  if (active && !*active) return;
+  extern __shared__ double dsm[];
+  __shared__ double sh[32];
+  double* acc = dsm + static_cast<int64_t>(threadIdx.y) * d;
+  const unsigned gm = group_mask();
+  double s_pap = 0.0, s_pp = 0.0;
+  ROWS_BEGIN(n) {
+    const int v = order[row_];
+    const int p0 = off[v], p1 = off[v + 1];
+    for (int f = threadIdx.x; f < d; f += blockDim.x) acc[f] = 0.0;
+    for (int p = p0; p < p1; ++p) {
+      const int l = adj_e[p];
+      const bool plus = adj_o[p] > v;
+      const double* pa = P + static_cast<int64_t>(ei[l]) * d;
+      const double* pb = P + static_cast<int64_t>(ej[l]) * d;
+      const double* vl = V + static_cast<int64_t>(l) * d;
+      if (q == Q_L2) {
+        const double al = jal[l], be = jbe[l];
+        if (be != 0.0) {
+          double c = 0.0;
+          for (int f = threadIdx.x; f < d; f += blockDim.x) c += vl[f] * (pa[f] - pb[f]);
+          const double bc = be * group_sum(c, gm);
+          for (int f = threadIdx.x; f < d; f += blockDim.x) {
+            const double w = pa[f] - pb[f];
+            const double y = w - (al * w + bc * vl[f]);
+            acc[f] = plus ? acc[f] + y : acc[f] - y;
+          }
+        } else if (al != 1.0) {
+          for (int f = threadIdx.x; f < d; f += blockDim.x) {
+            const double w = pa[f] - pb[f];
+            const double y = w - al * w;
+            acc[f] = plus ? acc[f] + y : acc[f] - y;
+          }
+        }
+      } else {
+        const double t = thr[l];
+        for (int f = threadIdx.x; f < d; f += blockDim.x) {
+          const double w = pa[f] - pb[f];
+          const double y = w - (fabs(vl[f]) > t ? w : 0.0);
+          acc[f] = plus ? acc[f] + y : acc[f] - y;
+        }
+      }
+    }
+    const int64_t base = static_cast<int64_t>(v) * d;
+    double a = 0.0, b = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double pv = P[base + f];
+      const double o = pv + sigma * acc[f];
+      Ap[base + f] = o;
+      a += pv * o;
+      b += pv * pv;
+    }
+    a = group_sum(a, gm);
+    b = group_sum(b, gm);
+    if (threadIdx.x == 0) {
+      s_pap += a;
+      s_pp += b;
+    }
+  }
+  s_pap = block_sum(s_pap, sh);
+  s_pp = block_sum(s_pp, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    part[2 * blockIdx.x] = s_pap;
+    part[2 * blockIdx.x + 1] = s_pp;
+  }
+}
+
+// ---- PCG (linalg.cpp:143-192) ---------------------------------------------------------
+// Device-resident loop control.  Each iteration is five launches
+//   hess -> s1 -> b -> s2 -> c
+// that all no-op once `active` drops, so the host enqueues iterations in
+// batches and polls the state only between batches.
+struct CgState {
+  double rz, pAp, alpha, beta, relres, tol, pp, rz_next;
+  long long it, maxit;
+  int active, phaseB, phaseC, upd_p, status, pad;
+};
+
+constexpr int kFeatThreads = 256;
+// Feature-major mapping: D1 threads per node row, R rows per pass.
+struct FM {
+  int D1, R, slot, f0;
+  __device__ FM(int d) {
+    D1 = d < kFeatThreads ? d : kFeatThreads;
+    R = kFeatThreads / D1;
+    slot = threadIdx.x / D1;
+    f0 = threadIdx.x % D1;
+  }
+};
+
+// Combine per-thread per-feature partials across slots and store part[b*d + f].
+template <int NF>
+__device__ void fm_store_cols(const FM& fm, const double (&acc)[NF], int d, double* sbuf, double* out) {
+  if (fm.R == 1) {
+#pragma unroll
+    for (int k = 0; k < NF; ++k) {
+      const int f = fm.f0 + fm.D1 * k;
+      if (f < d) out[f] = acc[k];
+    }
+    return;
+  }
+  // d < 256: NF == 1 used
+  sbuf[threadIdx.x] = (fm.slot < fm.R) ? acc[0] : 0.0;
+  __syncthreads();
+  if (fm.slot == 0) {
+    double s = 0.0;
+    for (int r = 0; r < fm.R; ++r) s += sbuf[r * fm.D1 + fm.f0];
+    out[fm.f0] = s;
+  }
+  __syncthreads();
+}
+
+template <int NF>
+__global__ void __launch_bounds__(kFeatThreads) k_pcg_init(const double* __restrict__ rhs, const double* __restrict__ Mx, const double* __restrict__ diag,
+                                                          int64_t n, int d, int64_t chunk, double* __restrict__ x,
+                                                          double* __restrict__ r, double* __restrict__ p,
+                                                          double* part_rz, double* part_bb) {
+  __shared__ double sh[32];
+  __shared__ double sbuf[kFeatThreads];
+  FM fm(d);
+  double acc[NF];
+#pragma unroll
+  for (int k = 0; k < NF; ++k) acc[k] = 0.0;
+  double rz = 0.0;
+  const int64_t v0 = blockIdx.x * chunk, v1 = min(n, v0 + chunk);
+  if (fm.slot < fm.R) {
+    for (int64_t v = v0 + fm.slot; v < v1; v += fm.R) {
+#pragma unroll
+      for (int k = 0; k < NF; ++k) {
+        const int f = fm.f0 + fm.D1 * k;
+        if (f < d) {
+          const int64_t i = v * d + f;
+          const double b = rhs[i];
+          const double rv = Mx ? b - Mx[i] : b;
+          if (!Mx) x[i] = 0.0;
+          r[i] = rv;
+          const double z = rv / diag[i];
+          p[i] = z;
+          rz += rv * z;
+          acc[k] += b * b;
+        }
+      }
+    }
+  }
+  rz = block_sum(rz, sh);
+  if (threadIdx.x == 0) part_rz[blockIdx.x] = rz;
+  fm_store_cols<NF>(fm, acc, d, sbuf, part_bb + static_cast<int64_t>(blockIdx.x) * d);
+}
+
+template <int NF>
+__global__ void __launch_bounds__(kFeatThreads) k_pcg_b(const CgState* __restrict__ st, const double* __restrict__ Ap,
+                                                       const double* __restrict__ diag, int64_t n, int d, int64_t chunk,
+                                                       double* __restrict__ r, double* part_rz, double* part_rr) {
+  if (!st->phaseB) return;
+  __shared__ double sh[32];
+  __shared__ double sbuf[kFeatThreads];
+  const double alpha = st->alpha;
+  FM fm(d);
+  double acc[NF];
+#pragma unroll
+  for (int k = 0; k < NF; ++k) acc[k] = 0.0;
+  double rz = 0.0;
+  const int64_t v0 = blockIdx.x * chunk, v1 = min(n, v0 + chunk);
+  if (fm.slot < fm.R) {
+    for (int64_t v = v0 + fm.slot; v < v1; v += fm.R) {
+#pragma unroll
+      for (int k = 0; k < NF; ++k) {
+        const int f = fm.f0 + fm.D1 * k;
+        if (f < d) {
+          const int64_t i = v * d + f;
+          const double rv = r[i] - alpha * Ap[i];
+          r[i] = rv;
+          rz += rv * (rv / diag[i]);
+          acc[k] += rv * rv;
+        }
+      }
+    }
+  }
+  rz = block_sum(rz, sh);
+  if (threadIdx.x == 0) part_rz[blockIdx.x] = rz;
+  fm_store_cols<NF>(fm, acc, d, sbuf, part_rr + static_cast<int64_t>(blockIdx.x) * d);
+}
+
+// x += alpha p; p = r/diag + beta p (when continuing)
+__global__ void k_pcg_c(const CgState* __restrict__ st, const double* __restrict__ r, const double* __restrict__ diag,
+                        int64_t m, double* __restrict__ x, double* __restrict__ p) {
+  if (!st->phaseC) return;
+  const double alpha = st->alpha, beta = st->beta;
+  const bool upd = st->upd_p != 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double pv = p[i];
+    x[i] = x[i] + alpha * pv;
+    if (upd) p[i] = r[i] / diag[i] + beta * pv;
+  }
+}
+
+// column sums of nb x d partials, then worst relative feature-row residual
+__device__ double pcg_relres(const double* part_rr, int nb, int d, const double* bn, double* sh) {
+  double worst = 0.0;
+  for (int f = threadIdx.x; f < d; f += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part_rr[static_cast<int64_t>(b) * d + f];
+    const double nb_ = bn[f];
+    worst = fmax(worst, sqrt(s) / (nb_ > 0.0 ? nb_ : 1.0));
+  }
+  return block_max(worst, sh);
+}
+__device__ double sum_part(const double* part, int nb, int stride, double* sh) {
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) s += part[static_cast<int64_t>(b) * stride];
+  return block_sum(s, sh);
+}
+
+__global__ void k_pcg_s0(CgState* st, const double* part_rz, const double* part_bb, int nb, int d, double tol,
+                         long long maxit, double* bn, int warm) {
+  __shared__ double sh[32];
+  for (int f = threadIdx.x; f < d; f += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part_bb[static_cast<int64_t>(b) * d + f];
+    bn[f] = sqrt(s);
+  }
+  __syncthreads();
+  const double rel = pcg_relres(part_bb, nb, d, bn, sh);
+  const double rz = sum_part(part_rz, nb, 1, sh);
+  if (threadIdx.x == 0) {
+    st->rz = rz;
+    st->relres = rel;
+    st->tol = tol;
+    st->it = 0;
+    st->maxit = maxit;
+    st->active = (!warm && rel <= tol) ? 0 : 1;
+    st->phaseB = st->phaseC = st->upd_p = 0;
+    st->status = 0;
+  }
+}
+__global__ void k_pcg_s1(CgState* st, const double* part, int nb) {
+  __shared__ double sh[32];
+  if (threadIdx.x == 0) st->phaseC = 0;
+  if (!st->active) {
+    if (threadIdx.x == 0) st->phaseB = 0;
+    return;
+  }
+  const double pAp = sum_part(part, nb, 2, sh);
+  const double pp = sum_part(part + 1, nb, 2, sh);
+  if (threadIdx.x == 0) {
+    st->it += 1;
+    st->pAp = pAp;
+    st->pp = pp;
+    if (pAp <= 0.0) {
+      st->active = 0;
+      st->phaseB = 0;
+      if (pp != 0.0) st->status = 1;  // not positive definite
+    } else {
+      st->alpha = st->rz / pAp;
+      st->phaseB = 1;
+    }
+  }
+}
+__global__ void k_pcg_s2(CgState* st, const double* part_rz, const double* part_rr, int nb, int d,
+                         const double* bn) {
+  __shared__ double sh[32];
+  if (!st->phaseB) {
+    if (threadIdx.x == 0) st->phaseC = 0;
+    return;
+  }
+  const double rel = pcg_relres(part_rr, nb, d, bn, sh);
+  const double rzn = sum_part(part_rz, nb, 1, sh);
+  if (threadIdx.x == 0) {
+    st->phaseB = 0;
+    st->phaseC = 1;
+    st->relres = rel;
+    if (rel <= st->tol || st->it >= st->maxit) {
+      st->active = 0;
+      st->upd_p = 0;
+    } else {
+      st->rz_next = rzn;
+      st->beta = rzn / st->rz;
+      st->rz = rzn;
+      st->upd_p = 1;
+    }
+  }
+}
+
+// ---- objectives / gap (objective.cpp:63-113) ------------------------------------------
+// Edge terms at (X, Z): [0] sum w_l ||XB_l||_q, [1] ||XB - prox_r(XB + Z)||^2,
+// [2] ||XB||^2, [3] ||Z||^2; max dual-ball excess into partmax.
+__device__ __forceinline__ void gap_edge_terms(const double* xa, const double* xb, const double* z, double rl,
+                                               double wl, int d, int q, unsigned gm, double* t4, double& excess) {
+  double xb2 = 0.0, zz = 0.0, uu = 0.0, l1 = 0.0, zmax = 0.0;
+  for (int f = threadIdx.x; f < d; f += blockDim.x) {
+    const double x = xa[f] - xb[f];
+    const double u = x + z[f];
+    xb2 += x * x;
+    zz += z[f] * z[f];
+    uu += u * u;
+    l1 += fabs(x);
+    zmax = fmax(zmax, fabs(z[f]));
+  }
+  xb2 = group_sum(xb2, gm);
+  zz = group_sum(zz, gm);
+  double al = 0.0;
+  if (q == Q_L2) {
+    const double nu = sqrt(group_sum(uu, gm));
+    if (nu <= rl) {
+      al = xb2;
+    } else {
+      const double s = 1.0 - rl / nu;
+      for (int f = threadIdx.x; f < d; f += blockDim.x) {
+        const double x = xa[f] - xb[f];
+        const double e = x - s * (x + z[f]);
+        al += e * e;
+      }
+      al = group_sum(al, gm);
+    }
+    t4[0] = wl * sqrt(xb2);
+    excess = fmax(excess, sqrt(zz) - (rl + 1e-9));
+  } else {
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double x = xa[f] - xb[f];
+      const double e = x - soft(x + z[f], rl);
+      al += e * e;
+    }
+    al = group_sum(al, gm);
+    t4[0] = wl * group_sum(l1, gm);
+    excess = fmax(excess, group_max(zmax, gm) - (rl + 1e-9));
+  }
+  t4[1] = al;
+  t4[2] = xb2;
+  t4[3] = zz;
+}
+
+__global__ void k_gap_edge(const double* __restrict__ X, const double* __restrict__ Z, const int* __restrict__ ei,
+                           const int* __restrict__ ej, const double* __restrict__ rad, const double* __restrict__ w,
+                           int64_t E, int d, int q, double* part) {
+  __shared__ double sh[32];
+  const unsigned gm = group_mask();
+  double s[4] = {0, 0, 0, 0}, excess = -1.0;
+  ROWS_BEGIN(E) {
+    double t4[4];
+    gap_edge_terms(X + static_cast<int64_t>(ei[row_]) * d, X + static_cast<int64_t>(ej[row_]) * d, Z + row_ * d,
+                   rad[row_], w[row_], d, q, gm, t4, excess);
+    if (threadIdx.x == 0)
+      for (int k = 0; k < 4; ++k) s[k] += t4[k];
+  }
+  for (int k = 0; k < 4; ++k) {
+    const double r = block_sum(s[k], sh);
+    if (threadIdx.x == 0 && threadIdx.y == 0) part[5 * blockIdx.x + k] = r;
+  }
+  const double m = block_max(excess, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) part[5 * blockIdx.x + 4] = m;
+}
+
+// Node terms: [0] ||X - A||^2, [1] ||Z B^T||^2, [2] <Z B^T, A>, [3] ||X - A + Z B^T||^2
+__global__ void k_gap_node(const double* __restrict__ X, const double* __restrict__ A, const double* __restrict__ Z,
+                           const int* __restrict__ off, const int* __restrict__ adj_e, const int* __restrict__ adj_o,
+                           const int* __restrict__ order, int64_t n, int d, double* part) {
+  __shared__ double sh[32];
+  const unsigned gm = group_mask();
+  double s[4] = {0, 0, 0, 0};
+  ROWS_BEGIN(n) {
+    const int v = order[row_];
+    const int p0 = off[v], p1 = off[v + 1];
+    const int64_t base = static_cast<int64_t>(v) * d;
+    double t[4] = {0, 0, 0, 0};
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      double acc = 0.0;
+      for (int p = p0; p < p1; ++p) {
+        const double z = Z[static_cast<int64_t>(adj_e[p]) * d + f];
+        acc = (adj_o[p] > v) ? acc + z : acc - z;
+      }
+      const double xa = X[base + f] - A[base + f];
+      const double st = xa + acc;
+      t[0] += xa * xa;
+      t[1] += acc * acc;
+      t[2] += acc * A[base + f];
+      t[3] += st * st;
+    }
+    for (int k = 0; k < 4; ++k) {
+      const double r = group_sum(t[k], gm);
+      if (threadIdx.x == 0) s[k] += r;
+    }
+  }
+  for (int k = 0; k < 4; ++k) {
+    const double r = block_sum(s[k], sh);
+    if (threadIdx.x == 0 && threadIdx.y == 0) part[4 * blockIdx.x + k] = r;
+  }
+}
+
+// ---- SSNAL multiplier (ssnal.cpp:183-195, :205) fused with the edge gap terms -----------
+// part per block: [0..3] gap edge terms at the new Z, [4] ||XB - PV||^2, [5] ||XB||^2 (same as [2]),
+// [6] max |Z + sigma XB| (pre-projection), [7] max |Zenv - Zsum|, [8] dual excess
+__global__ void k_mult(const double* __restrict__ X, double* __restrict__ Z, const double* __restrict__ V,
+                       const double* __restrict__ ps, const double* __restrict__ thr, const double* __restrict__ rad,
+                       const double* __restrict__ w, const int* __restrict__ ei, const int* __restrict__ ej, int64_t E,
+                       int d, double sigma, int q, double* part) {
+  __shared__ double sh[32];
+  const unsigned gm = group_mask();
+  double s[5] = {0, 0, 0, 0, 0}, mx = 0.0, err = 0.0, excess = -1.0;
+  ROWS_BEGIN(E) {
+    const double* xa = X + static_cast<int64_t>(ei[row_]) * d;
+    const double* xb = X + static_cast<int64_t>(ej[row_]) * d;
+    double* z = Z + row_ * d;
+    const double* v = V + row_ * d;
+    const double rl = rad[row_], tl = thr[row_], sl = ps[row_];
+    double nn = 0.0, m = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double zs = z[f] + sigma * (xa[f] - xb[f]);
+      nn += zs * zs;
+      m = fmax(m, fabs(zs));
+    }
+    mx = fmax(mx, m);
+    const double nz = sqrt(group_sum(nn, gm));
+    const double sc = rl / nz;
+    double fr = 0.0, e = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double x = xa[f] - xb[f];
+      const double zs = z[f] + sigma * x;
+      const double zp = (q == Q_L2) ? ((nz <= rl) ? zs : sc * zs) : fmax(fmin(zs, rl), -rl);
+      const double pv = (q == Q_L2) ? sl * v[f] : soft(v[f], tl);
+      const double zenv = sigma * (v[f] - pv);
+      e = fmax(e, fabs(zenv - zp));
+      z[f] = zp;
+      fr += (x - pv) * (x - pv);
+    }
+    err = fmax(err, e);
+    fr = group_sum(fr, gm);
+    double t4[4];
+    gap_edge_terms(xa, xb, z, rl, w[row_], d, q, gm, t4, excess);
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < 4; ++k) s[k] += t4[k];
+      s[4] += fr;
+    }
+  }
+  for (int k = 0; k < 5; ++k) {
+    const double r = block_sum(s[k], sh);
+    if (threadIdx.x == 0 && threadIdx.y == 0) part[9 * blockIdx.x + k] = r;
+  }
+  const double a = block_max(mx, sh);
+  const double b = block_max(err, sh);
+  const double c = block_max(excess, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    part[9 * blockIdx.x + 5] = 0.0;
+    part[9 * blockIdx.x + 6] = a;
+    part[9 * blockIdx.x + 7] = b;
+    part[9 * blockIdx.x + 8] = c;
+  }
+}
+
+// ---- fast AMA (ama.cpp:57-72) -----------------------------------------------------------
+__global__ void k_ama_node(const double* __restrict__ A, const double* __restrict__ Zh, const int* __restrict__ off,
+                           const int* __restrict__ adj_e, const int* __restrict__ adj_o, const int* __restrict__ order,
+                           int64_t n, int d, double* __restrict__ Xh) {
+  ROWS_BEGIN(n) {
+    const int v = order[row_];
+    const int p0 = off[v], p1 = off[v + 1];
+    const int64_t base = static_cast<int64_t>(v) * d;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      double acc = 0.0;
+      for (int p = p0; p < p1; ++p) {
+        const double z = Zh[static_cast<int64_t>(adj_e[p]) * d + f];
+        acc = (adj_o[p] > v) ? acc + z : acc - z;
+      }
+      Xh[base + f] = A[base + f] - acc;
+    }
+  }
+}
+__global__ void k_ama_edge(const double* __restrict__ Xh, double* __restrict__ Zh, double* __restrict__ Zp,
+                           const double* __restrict__ rad, const int* __restrict__ ei, const int* __restrict__ ej,
+                           int64_t E, int d, double step, double mom, int q) {
+  const unsigned gm = group_mask();
+  ROWS_BEGIN(E) {
+    const double* xa = Xh + static_cast<int64_t>(ei[row_]) * d;
+    const double* xb = Xh + static_cast<int64_t>(ej[row_]) * d;
+    double* zh = Zh + row_ * d;
+    double* zp = Zp + row_ * d;
+    const double rl = rad[row_];
+    double nn = 0.0;
+    if (q == Q_L2) {
+      for (int f = threadIdx.x; f < d; f += blockDim.x) {
+        const double zn = zh[f] + step * (xa[f] - xb[f]);
+        nn += zn * zn;
+      }
+    }
+    const double nz = sqrt(group_sum(nn, gm));
+    const double sc = rl / nz;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double zn = zh[f] + step * (xa[f] - xb[f]);
+      const double zpr = (q == Q_L2) ? ((nz <= rl) ? zn : sc * zn) : fmax(fmin(zn, rl), -rl);
+      const double old = zp[f];
+      zh[f] = zpr + mom * (zpr - old);
+      zp[f] = zpr;
+    }
+  }
+}
+
+// ---- host helpers ----------------------------------------------------------------------------
+double* part_buf(Ctx& c, const char* name, size_t count) { return c.buf<double>(name, count + 8); }
+
+double fetch1(Ctx& c) {
+  double v;
+  c.fetch(0, 1, &v);
+  return v;
+}
+
+}  // namespace
+
+// ====================================================================================
+void make_radii(Ctx& c, const Graph& g, double gamma, double* rad) {
+  if (g.E == 0) return;
+  k_scale<<<flat_grid(c, g.E), 256, 0, c.s>>>(g.w.p, gamma, g.E, rad);
+  CPB_LAUNCH_CHECK();
+}
+void make_thr(Ctx& c, int64_t E, const double* rad, double sigma, double* thr) {
+  if (E == 0) return;
+  k_div<<<flat_grid(c, E), 256, 0, c.s>>>(rad, sigma, E, thr);
+  CPB_LAUNCH_CHECK();
+}
+
+double dot_dev(Ctx& c, const double* a, const double* b, int64_t count) {
+  const int grid = flat_grid(c, count);
+  double* part = part_buf(c, "dot.part", grid);
+  k_dot<<<grid, 256, 0, c.s>>>(a, b, count, part);
+  CPB_LAUNCH_CHECK();
+  reduce_sum(c, part, grid, c.dscal);
+  return fetch1(c);
+}
+double max_abs_dev(Ctx& c, const double* x, int64_t count) {
+  const int grid = flat_grid(c, count);
+  double* part = part_buf(c, "max.part", grid);
+  k_maxabs<<<grid, 256, 0, c.s>>>(x, count, part);
+  CPB_LAUNCH_CHECK();
+  reduce_max(c, part, grid, c.dscal);
+  return fetch1(c);
+}
+void axpy_dev(Ctx& c, double* out, const double* x, double a, const double* y, int64_t count) {
+  if (count == 0) return;
+  k_axpy<<<flat_grid(c, count), 256, 0, c.s>>>(out, x, a, y, count);
+  CPB_LAUNCH_CHECK();
+}
+void neg_dev(Ctx& c, double* out, const double* x, int64_t count) {
+  if (count == 0) return;
+  k_neg<<<flat_grid(c, count), 256, 0, c.s>>>(out, x, count);
+  CPB_LAUNCH_CHECK();
+}
+void copy_dev(Ctx& c, double* dst, const double* src, int64_t count) {
+  if (count == 0 || dst == src) return;
+  CPB_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToDevice, c.s));
+}
+
+void prox_columns_dev(Ctx& c, int q, const double* V, const double* t, int64_t d, int64_t E, double* out) {
+  if (E == 0) return;
+  GroupGeom gg = group_geom(c, E, d);
+  k_prox_cols<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(q, V, t, E, static_cast<int>(d), out);
+  CPB_LAUNCH_CHECK();
+}
+void project_columns_dev(Ctx& c, int q, const double* Z, const double* r, int64_t d, int64_t E, double* out) {
+  if (E == 0) return;
+  GroupGeom gg = group_geom(c, E, d);
+  k_project_cols<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(q, Z, r, E, static_cast<int>(d), out);
+  CPB_LAUNCH_CHECK();
+}
+void prox_jacobian_diag_dev(Ctx& c, int q, const double* V, const double* t, int64_t d, int64_t E, double* out) {
+  if (E == 0) return;
+  GroupGeom gg = group_geom(c, E, d);
+  k_jac_diag_cols<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(q, V, t, E, static_cast<int>(d), out);
+  CPB_LAUNCH_CHECK();
+}
+
+double eval_phi(const Prob& P, const double* X, const double* D, double alpha, double* Xt, const double* Z,
+                double sigma, const double* thr, double zz, double* V, double* nv) {
+  Ctx& c = *P.c;
+  const int64_t d = P.d(), n = P.n(), E = P.E(), m = d * n;
+  const int fg = flat_grid(c, m);
+  double* pn = part_buf(c, "phi.pn", fg);
+  const double* Xe = D ? Xt : X;
+  {
+    Ctx::Timer tm(&c, D ? "trial_x" : "phi_node", (D ? 4.0 : 2.0) * m * 8.0);
+    k_trial_x<<<fg, 256, 0, c.s>>>(X, D, alpha, Xt, P.A->A.p, m, pn);
+    CPB_LAUNCH_CHECK();
+  }
+  reduce_sum(c, pn, fg, c.dscal);
+  if (E > 0) {
+    GroupGeom gg = group_geom(c, E, d);
+    double* pe = part_buf(c, "phi.pe", gg.grid);
+    Ctx::Timer tm(&c, "phi_edge", (2.0 * E * d + n * d + 4.0 * E) * 8.0);
+    k_phi_edge<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, E,
+                                                        static_cast<int>(d), sigma, P.q, V, nv, pe);
+    CPB_LAUNCH_CHECK();
+    reduce_sum(c, pe, gg.grid, c.dscal + 1);
+  } else {
+    fill(c, c.dscal + 1, 1, 0.0);
+  }
+  double h[2];
+  c.fetch(0, 2, h);
+  return 0.5 * h[0] + h[1] - zz / (2.0 * sigma);
+}
+
+int64_t jac_params(const Prob& P, const double* nv, const double* thr, double* ps, double* jal, double* jbe) {
+  Ctx& c = *P.c;
+  const int64_t E = P.E();
+  if (E == 0) return 0;
+  const int grid = flat_grid(c, E);
+  double* part = part_buf(c, "jac.part", grid);
+  k_jac<<<grid, 256, 0, c.s>>>(nv, thr, E, P.q, ps, jal, jbe, part);
+  CPB_LAUNCH_CHECK();
+  reduce_sum(c, part, grid, c.dscal);
+  return static_cast<int64_t>(fetch1(c));
+}
+
+double grad_diag(const Prob& P, const double* X, const double* V, const double* ps, const double* jal,
+                 const double* jbe, const double* thr, double sigma, double* G, double* diag, bool want_diag) {
+  Ctx& c = *P.c;
+  const int64_t d = P.d(), n = P.n(), E = P.E();
+  GroupGeom gg = group_geom(c, n, d);
+  double* part = part_buf(c, "grad.part", gg.grid);
+  {
+    Ctx::Timer tm(&c, "grad_diag", (2.0 * E * d + (want_diag ? 4.0 : 3.0) * n * d) * 8.0);
+    k_grad_diag<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(X, P.A->A.p, V, ps, jal, jbe, thr, P.g->off.p, P.g->adj_e.p,
+                                                         P.g->adj_o.p, P.g->order.p, n, static_cast<int>(d), sigma,
+                                                         P.q, want_diag ? 1 : 0, G, diag, part);
+    CPB_LAUNCH_CHECK();
+  }
+  reduce_sum(c, part, gg.grid, c.dscal);
+  return fetch1(c);
+}
+
+int hess_apply(const Prob& P, const double* p, const double* V, const double* jal, const double* jbe,
+               const double* thr, double sigma, double* Ap, double* part, const void* st) {
+  Ctx& c = *P.c;
+  const int64_t d = P.d(), n = P.n();
+  GroupGeom gg = group_geom(c, n, d);
+  size_t smem = static_cast<size_t>(gg.gy) * d * sizeof(double);
+  while (smem > 200 * 1024 && gg.gy > 1) {
+    gg.gy >>= 1;
+    smem = static_cast<size_t>(gg.gy) * d * sizeof(double);
+  }
+  if (smem > 200 * 1024) invalid("hessian apply: feature dimension too large");
+  gg.grid = std::max(1, std::min(cdiv(n, gg.gy), c.sm_count * 8));
+  static bool attr_set = false;
+  if (!attr_set) {
+    CPB_CUDA(cudaFuncSetAttribute(k_hess, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_set = true;
+  }
+  k_hess<<<gg.grid, dim3(gg.gx, gg.gy), smem, c.s>>>(p, V, jal, jbe, thr, P.g->ei.p, P.g->ej.p, P.g->off.p,
+                                                     P.g->adj_e.p, P.g->adj_o.p, P.g->order.p, n, static_cast<int>(d),
+                                                     sigma, P.q, Ap, part,
+                                                     st ? &static_cast<const CgState*>(st)->active : nullptr);
+  CPB_LAUNCH_CHECK();
+  return gg.grid;
+}
+
+const int* cg_active_ptr(const void* st) { return st ? &static_cast<const CgState*>(st)->active : nullptr; }
+
+PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, const char* op_name,
+               const double* rhs, PcgWork w, double tol, int64_t max_iter, bool warm) {
+  const int64_t m = d * n;
+  if (!(tol > 0.0)) invalid("pcg: tol must be positive");
+  if (max_iter < 1) invalid("pcg: max_iter must be >= 1");
+  if (d > 64 * kFeatThreads) invalid("pcg: feature dimension above 16384 is not supported");
+  const int nb = std::max(1, std::min(cdiv(n, 4), c.sm_count * 2));
+  const int64_t chunk = (n + nb - 1) / nb;
+  double* part_rz = part_buf(c, "pcg.rz", nb);
+  double* part_rr = part_buf(c, "pcg.rr", static_cast<size_t>(nb) * d);
+  double* part_h = part_buf(c, "pcg.h", 2 * static_cast<size_t>(c.sm_count) * 8 + 2);
+  double* bn = part_buf(c, "pcg.bn", d);
+  CgState* st = reinterpret_cast<CgState*>(c.dscal + 64);
+  const int nf = d <= kFeatThreads * 4 ? 4 : (d <= kFeatThreads * 16 ? 16 : 64);
+  const double* Mx = nullptr;
+  if (warm) {
+    op(w.x, w.Ap, part_h, nullptr);
+    Mx = w.Ap;
+  }
+  const int di = static_cast<int>(d);
+  if (nf == 4)
+    k_pcg_init<4><<<nb, kFeatThreads, 0, c.s>>>(rhs, Mx, w.diag, n, di, chunk, w.x, w.r, w.p, part_rz, part_rr);
+  else if (nf == 16)
+    k_pcg_init<16><<<nb, kFeatThreads, 0, c.s>>>(rhs, Mx, w.diag, n, di, chunk, w.x, w.r, w.p, part_rz, part_rr);
+  else
+    k_pcg_init<64><<<nb, kFeatThreads, 0, c.s>>>(rhs, Mx, w.diag, n, di, chunk, w.x, w.r, w.p, part_rz, part_rr);
+  CPB_LAUNCH_CHECK();
+  k_pcg_s0<<<1, 1024, 0, c.s>>>(st, part_rz, part_rr, nb, di, tol, max_iter, bn, Mx != nullptr);
+  CPB_LAUNCH_CHECK();
+  auto launch_b = [&]() {
+    if (nf == 4)
+      k_pcg_b<4><<<nb, kFeatThreads, 0, c.s>>>(st, w.Ap, w.diag, n, di, chunk, w.r, part_rz, part_rr);
+    else if (nf == 16)
+      k_pcg_b<16><<<nb, kFeatThreads, 0, c.s>>>(st, w.Ap, w.diag, n, di, chunk, w.r, part_rz, part_rr);
+    else
+      k_pcg_b<64><<<nb, kFeatThreads, 0, c.s>>>(st, w.Ap, w.diag, n, di, chunk, w.r, part_rz, part_rr);
+  };
+  const int fg = flat_grid(c, m);
+  int batch = 4;
+  long long it_before = 0;
+  PcgOut out;
+  for (;;) {
+    for (int b = 0; b < batch; ++b) {
+      int hb;
+      {
+        Ctx::Timer tm(&c, op_name, op_bytes);
+        hb = op(w.p, w.Ap, part_h, st);
+      }
+      k_pcg_s1<<<1, 256, 0, c.s>>>(st, part_h, hb);
+      CPB_LAUNCH_CHECK();
+      {
+        Ctx::Timer tm(&c, "pcg_update_b", 4.0 * m * 8.0);
+        launch_b();
+        CPB_LAUNCH_CHECK();
+      }
+      k_pcg_s2<<<1, 1024, 0, c.s>>>(st, part_rz, part_rr, nb, di, bn);
+      CPB_LAUNCH_CHECK();
+      {
+        Ctx::Timer tm(&c, "pcg_update_c", 6.0 * m * 8.0);
+        k_pcg_c<<<fg, 256, 0, c.s>>>(st, w.r, w.diag, m, w.x, w.p);
+        CPB_LAUNCH_CHECK();
+      }
+    }
+    CgState h;
+    CPB_CUDA(cudaMemcpyAsync(c.hscal, st, sizeof(CgState), cudaMemcpyDeviceToHost, c.s));
+    c.sync();
+    std::memcpy(&h, c.hscal, sizeof(CgState));
+    // launches after the loop ended were no-ops: drop them from the statistics
+    const int wasted = batch - static_cast<int>(h.it - it_before);
+    if (wasted > 0) {
+      c.discard_pending(op_name, wasted);
+      c.discard_pending("pcg_update_b", wasted);
+      c.discard_pending("pcg_update_c", wasted);
+    }
+    it_before = h.it;
+    if (h.status == 1) runtime("pcg: operator is not positive definite (p'Ap <= 0)");
+    if (!h.active) {
+      out.iterations = h.it;
+      out.converged = h.relres <= tol;
+      break;
+    }
+    batch = std::min(batch * 2, 32);
+  }
+  return out;
+}
+
+PcgOut pcg_newton(const Prob& P, const double* V, const double* jal, const double* jbe, const double* thr,
+                  double sigma, const double* rhs, PcgWork w, double tol, int64_t max_iter, int64_t n_active) {
+  const int64_t d = P.d(), n = P.n(), E = P.E(), m = d * n;
+  // Algorithmic bytes per H-apply: p read + Ap write
+  // (2 n d) + the active edge rows (E_a d) + two per-edge scalars + the CSR.
+  const double hess_bytes = (2.0 * m + static_cast<double>(n_active) * d + 2.0 * E) * 8.0 + (2.0 * E + n + 1) * 4.0;
+  PcgOp op = [&](const double* p, double* Ap, double* part, const void* st) {
+    return hess_apply(P, p, V, jal, jbe, thr, sigma, Ap, part, st);
+  };
+  return pcg_dev(*P.c, n, d, op, hess_bytes, "hess_apply", rhs, w, tol, max_iter, false);
+}
+
+// Sum (and max) the columns of a (rows x cols) block-partial table on the host,
+// in block order: deterministic and cheap (rows <= 8 x SM count).
+std::vector<double> host_cols(Ctx& c, const double* part, int rows, int cols, const std::vector<int>& max_cols = {}) {
+  std::vector<double> all(static_cast<size_t>(rows) * cols), out(cols, 0.0);
+  d2h(c, all.data(), part, all.size() * sizeof(double));
+  for (int k : max_cols) out[k] = -1e300;
+  for (int b = 0; b < rows; ++b)
+    for (int k = 0; k < cols; ++k) {
+      const double x = all[static_cast<size_t>(b) * cols + k];
+      bool is_max = false;
+      for (int mk : max_cols) is_max |= (mk == k);
+      out[k] = is_max ? std::max(out[k], x) : out[k] + x;
+    }
+  return out;
+}
+
+GapOut eval_gap(const Prob& P, const double* X, const double* Z) {
+  Ctx& c = *P.c;
+  const int64_t d = P.d(), n = P.n(), E = P.E();
+  GroupGeom gn = group_geom(c, n, d);
+  double* pn = part_buf(c, "gap.pn", 4 * static_cast<size_t>(gn.grid));
+  {
+    Ctx::Timer tm(&c, "gap_node", (2.0 * E * d + 2.0 * n * d) * 8.0);
+    k_gap_node<<<gn.grid, dim3(gn.gx, gn.gy), 0, c.s>>>(X, P.A->A.p, Z, P.g->off.p, P.g->adj_e.p, P.g->adj_o.p,
+                                                        P.g->order.p, n, static_cast<int>(d), pn);
+    CPB_LAUNCH_CHECK();
+  }
+  std::vector<double> h = host_cols(c, pn, gn.grid, 4);
+  std::vector<double> e(5, 0.0);
+  e[4] = -1.0;
+  if (E > 0) {
+    GroupGeom ge = group_geom(c, E, d);
+    double* pe = part_buf(c, "gap.pe", 5 * static_cast<size_t>(ge.grid));
+    {
+      Ctx::Timer tm(&c, "gap_edge", (E * d + n * d) * 8.0);
+      k_gap_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, E,
+                                                          static_cast<int>(d), P.q, pe);
+      CPB_LAUNCH_CHECK();
+    }
+    e = host_cols(c, pe, ge.grid, 5, {4});
+  }
+  if (e[4] > 0.0) invalid("dual_objective: Z violates the dual-ball constraint");
+  const double normA = data_fro_norm(c, *P.A);
+  GapOut g;
+  g.fp = 0.5 * h[0];
+  if (E > 0 && P.gamma != 0.0) g.fp = g.fp + P.gamma * e[0];
+  g.fd = -0.5 * h[1] + h[2];
+  g.gap = std::abs(g.fp - g.fd) / (1.0 + std::abs(g.fp) + std::abs(g.fd));
+  const double stat = std::sqrt(h[3]) / (1.0 + normA);
+  if (E == 0 || P.gamma == 0.0) {
+    g.kkt = stat;
+  } else {
+    const double align = std::sqrt(e[1]) / (1.0 + std::sqrt(e[2]) + std::sqrt(e[3]));
+    g.kkt = std::max(stat, align);
+  }
+  return g;
+}
+
+double primal_objective_dev(const Prob& P, const double* X) {
+  Ctx& c = *P.c;
+  const int64_t d = P.d(), n = P.n(), E = P.E(), m = d * n;
+  const int fg = flat_grid(c, m);
+  double* pn = part_buf(c, "po.pn", fg);
+  k_trial_x<<<fg, 256, 0, c.s>>>(X, nullptr, 0.0, nullptr, P.A->A.p, m, pn);
+  CPB_LAUNCH_CHECK();
+  reduce_sum(c, pn, fg, c.dscal);
+  double value = 0.5 * fetch1(c);
+  if (E == 0 || P.gamma == 0.0) return value;
+  // penalty: gap edge term [0] with a zero dual (Z only enters the other terms)
+  double* Z0 = c.buf<double>("po.z0", static_cast<size_t>(E) * d);
+  CPB_CUDA(cudaMemsetAsync(Z0, 0, static_cast<size_t>(E) * d * sizeof(double), c.s));
+  GroupGeom ge = group_geom(c, E, d);
+  double* pe = part_buf(c, "po.pe", 5 * static_cast<size_t>(ge.grid));
+  k_gap_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z0, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, E,
+                                                      static_cast<int>(d), P.q, pe);
+  CPB_LAUNCH_CHECK();
+  std::vector<double> e = host_cols(c, pe, ge.grid, 5, {4});
+  return value + P.gamma * e[0];
+}
+
+double dual_objective_dev(const Prob& P, const double* Z) {
+  // fd does not depend on X; evaluate with X = A
+  GapOut g = eval_gap(P, P.A->A.p, Z);
+  return g.fd;
+}
+double kkt_residual_dev(const Prob& P, const double* X, const double* Z) {
+  Ctx& c = *P.c;
+  const int64_t d = P.d(), n = P.n(), E = P.E();
+  GroupGeom gn = group_geom(c, n, d);
+  double* pn = part_buf(c, "kkt.pn", 4 * static_cast<size_t>(gn.grid));
+  k_gap_node<<<gn.grid, dim3(gn.gx, gn.gy), 0, c.s>>>(X, P.A->A.p, Z, P.g->off.p, P.g->adj_e.p, P.g->adj_o.p,
+                                                      P.g->order.p, n, static_cast<int>(d), pn);
+  CPB_LAUNCH_CHECK();
+  std::vector<double> h = host_cols(c, pn, gn.grid, 4);
+  const double stat = std::sqrt(h[3]) / (1.0 + data_fro_norm(c, *P.A));
+  if (E == 0 || P.gamma == 0.0) return stat;
+  GroupGeom ge = group_geom(c, E, d);
+  double* pe = part_buf(c, "kkt.pe", 5 * static_cast<size_t>(ge.grid));
+  k_gap_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, E,
+                                                      static_cast<int>(d), P.q, pe);
+  CPB_LAUNCH_CHECK();
+  std::vector<double> e = host_cols(c, pe, ge.grid, 5, {4});
+  return std::max(stat, std::sqrt(e[1]) / (1.0 + std::sqrt(e[2]) + std::sqrt(e[3])));
+}
+
+MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double* V, const double* ps,
+                         const double* thr, double sigma) {
+  Ctx& c = *P.c;
+  const int64_t d = P.d(), n = P.n(), E = P.E();
+  GroupGeom ge = group_geom(c, E, d);
+  double* pe = part_buf(c, "mult.pe", 9 * static_cast<size_t>(ge.grid));
+  {
+    Ctx::Timer tm(&c, "multiplier", (3.0 * E * d + n * d) * 8.0);
+    k_mult<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p, P.g->ej.p, E,
+                                                    static_cast<int>(d), sigma, P.q, pe);
+    CPB_LAUNCH_CHECK();
+  }
+  std::vector<double> s = host_cols(c, pe, ge.grid, 9, {6, 7, 8});
+  const double mx = s[6], err = s[7], excess = s[8];
+  const double scale = 1.0 + mx;
+  if (err > 1e-10 * scale) runtime("ssnal: multiplier self-check failed");
+  if (excess > 0.0) invalid("dual_objective: Z violates the dual-ball constraint");
+  // node terms at (X, new Z)
+  GroupGeom gn = group_geom(c, n, d);
+  double* pn = part_buf(c, "mult.pn", 4 * static_cast<size_t>(gn.grid));
+  {
+    Ctx::Timer tm(&c, "gap_node", (2.0 * E * d + 2.0 * n * d) * 8.0);
+    k_gap_node<<<gn.grid, dim3(gn.gx, gn.gy), 0, c.s>>>(X, P.A->A.p, Z, P.g->off.p, P.g->adj_e.p, P.g->adj_o.p,
+                                                        P.g->order.p, n, static_cast<int>(d), pn);
+    CPB_LAUNCH_CHECK();
+  }
+  std::vector<double> h = host_cols(c, pn, gn.grid, 4);
+  const double normA = data_fro_norm(c, *P.A);
+  MultOut o;
+  GapOut& g = o.gap;
+  g.fp = 0.5 * h[0];
+  if (P.gamma != 0.0) g.fp = g.fp + P.gamma * s[0];
+  g.fd = -0.5 * h[1] + h[2];
+  g.gap = std::abs(g.fp - g.fd) / (1.0 + std::abs(g.fp) + std::abs(g.fd));
+  const double stat = std::sqrt(h[3]) / (1.0 + normA);
+  const double align = std::sqrt(s[1]) / (1.0 + std::sqrt(s[2]) + std::sqrt(s[3]));
+  g.kkt = (P.gamma == 0.0) ? stat : std::max(stat, align);
+  o.feas = std::sqrt(s[4]) / (1.0 + std::sqrt(s[2]));
+  o.zz = s[3];
+  return o;
+}
+
+void ama_primal(const Prob& P, const double* Zh, double* Xh) {
+  Ctx& c = *P.c;
+  const int64_t d = P.d(), n = P.n();
+  GroupGeom gn = group_geom(c, n, d);
+  k_ama_node<<<gn.grid, dim3(gn.gx, gn.gy), 0, c.s>>>(P.A->A.p, Zh, P.g->off.p, P.g->adj_e.p, P.g->adj_o.p,
+                                                      P.g->order.p, n, static_cast<int>(d), Xh);
+  CPB_LAUNCH_CHECK();
+}
+void ama_dual_step(const Prob& P, const double* Xh, double* Zh, double* Zprev, double step, double mom) {
+  Ctx& c = *P.c;
+  const int64_t d = P.d(), E = P.E();
+  GroupGeom ge = group_geom(c, E, d);
+  k_ama_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(Xh, Zh, Zprev, P.rad, P.g->ei.p, P.g->ej.p, E,
+                                                      static_cast<int>(d), step, mom, P.q);
+  CPB_LAUNCH_CHECK();
+}
+
+}  // namespace cpb

@@ -1,0 +1,431 @@
+// Solver drivers and the path engine (see solve.cuh).
+#include <chrono>
+#include <cmath>
+#include <limits>
+
+#include <cub/cub.cuh>
+
+#include "solve.cuh"
+
+namespace cpb {
+
+namespace {
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+bool accepts(const GapOut& g, const cp_solver_config& c) {
+  return g.gap <= c.epsilon && g.kkt <= c.kkt_factor * c.epsilon;  // solver_util.hpp:28-30
+}
+
+cp_termination finish(const GapOut& s, int64_t it, bool conv, double wall) {
+  cp_termination t;
+  std::memset(&t, 0, sizeof(t));
+  t.f_primal = s.fp;
+  t.f_dual = s.fd;
+  t.gap = s.gap;
+  t.iterations = it;
+  t.converged = conv ? 1 : 0;
+  t.wall_time = wall;
+  return t;
+}
+
+// BestIterate (solver_util.hpp:72-85): device copies of the best-gap pair.
+struct Best {
+  double gap = std::numeric_limits<double>::infinity();
+  GapOut s;
+  bool have = false;
+  void offer(Ctx& c, const GapOut& g, const double* X, const double* Z, double* Xb, double* Zb, int64_t m,
+             int64_t me) {
+    if (g.gap < gap) {
+      gap = g.gap;
+      s = g;
+      have = true;
+      copy_dev(c, Xb, X, m);
+      copy_dev(c, Zb, Z, me);
+    }
+  }
+};
+
+// initial_point (solver_util.hpp:56-68)
+void initial_point(Prob& P, bool warm, double* X, double* Z) {
+  Ctx& c = *P.c;
+  const int64_t m = P.d() * P.n(), me = P.d() * P.E();
+  if (warm) {
+    project_columns_dev(c, P.q, Z, P.rad, P.d(), P.E(), Z);
+  } else {
+    copy_dev(c, X, P.A->A.p, m);
+    if (me) CPB_CUDA(cudaMemsetAsync(Z, 0, me * sizeof(double), c.s));
+  }
+}
+
+// ---- SSNAL (ssnal.cpp:113-215) ------------------------------------------------------
+cp_termination ssnal(Prob& P, const cp_solver_config& cfg, bool warm, double* Xout, double* Zout) {
+  Ctx& c = *P.c;
+  const auto t0 = Clock::now();
+  const int64_t d = P.d(), n = P.n(), E = P.E(), m = d * n, me = d * E;
+  initial_point(P, warm, Xout, Zout);
+  {
+    GapOut s0 = eval_gap(P, Xout, Zout);
+    if (accepts(s0, cfg)) return finish(s0, 0, true, since(t0));
+  }
+  double* X = c.buf<double>("s.X", m);
+  double* Xt = c.buf<double>("s.Xt", m);
+  double* Z = Zout;
+  double* V = c.buf<double>("s.V", me);
+  double* Vt = c.buf<double>("s.Vt", me);
+  double* nv = c.buf<double>("s.nv", E);
+  double* nvt = c.buf<double>("s.nvt", E);
+  double* thr = c.buf<double>("s.thr", E);
+  double* ps = c.buf<double>("s.ps", E);
+  double* jal = c.buf<double>("s.jal", E);
+  double* jbe = c.buf<double>("s.jbe", E);
+  double* G = c.buf<double>("s.G", m);
+  PcgWork w{c.buf<double>("s.D", m), c.buf<double>("s.r", m), c.buf<double>("s.p", m), c.buf<double>("s.Ap", m),
+            c.buf<double>("s.diag", m)};
+  double* Xb = c.buf<double>("s.Xb", m);
+  double* Zb = c.buf<double>("s.Zb", me);
+  copy_dev(c, X, Xout, m);
+
+  const double eps = cfg.epsilon;
+  double sigma = cfg.ssnal_sigma0;
+  double feas_prev = std::numeric_limits<double>::infinity();
+  double zz = dot_dev(c, Z, Z, me);
+  Best best;
+  cp_termination cnt;
+  std::memset(&cnt, 0, sizeof(cnt));
+  int64_t done = 0;
+  const int64_t max_outer = resolved_max_iter(cfg);
+  for (int64_t k = 1; k <= max_outer; ++k) {
+    const double eps_k = std::max(eps / 10.0, std::pow(0.5, static_cast<double>(k)));
+    make_thr(c, E, P.rad, sigma, thr);
+    double phi = eval_phi(P, X, nullptr, 0.0, nullptr, Z, sigma, thr, zz, V, nv);
+    for (int64_t j = 0; j < cfg.ssnal_newton_max; ++j) {
+      const int64_t n_active = jac_params(P, nv, thr, ps, jal, jbe);
+      const double gnorm = std::sqrt(grad_diag(P, X, V, ps, jal, jbe, thr, sigma, G, w.diag, true));
+      if (gnorm <= eps_k) break;
+      ++cnt.newton;
+      const double cg_tol = std::max(std::min(0.1, std::sqrt(gnorm)), 1e-12);
+      neg_dev(c, w.r, G, m);
+      PcgOut dir = pcg_newton(P, V, jal, jbe, thr, sigma, w.r, w, cg_tol, cfg.pcg_max_iter, n_active);
+      cnt.cg += dir.iterations;
+      cnt.hess_apply += dir.iterations;
+      double* D = w.x;
+      double descent = dot_dev(c, G, D, m);
+      if (!(descent < 0.0)) {  // inexact CG returned a non-descent direction (ssnal.cpp:166-170)
+        neg_dev(c, D, G, m);
+        descent = -gnorm * gnorm;
+      }
+      double alpha = 1.0, trial = 0.0;
+      bool ok = false;
+      for (int bt = 0; bt < 60; ++bt) {
+        trial = eval_phi(P, X, D, alpha, Xt, Z, sigma, thr, zz, Vt, nvt);
+        ++cnt.armijo;
+        if (trial <= phi + cfg.armijo_mu * alpha * descent) {
+          ok = true;
+          break;
+        }
+        alpha *= cfg.backtrack_beta;
+      }
+      if (ok) {
+        std::swap(X, Xt);  // X + alpha D, bit-identical to the trial point
+      } else {
+        axpy_dev(c, X, X, alpha, D, m);  // reference quirk: alpha halved a 60th time (ssnal.cpp:172-179)
+      }
+      std::swap(V, Vt);
+      std::swap(nv, nvt);
+      phi = trial;
+    }
+    jac_params(P, nv, thr, ps, jal, jbe);  // prox scale at the last accepted V
+    MultOut mo = ssnal_multiplier(P, X, Z, V, ps, thr, sigma);
+    zz = mo.zz;
+    if (accepts(mo.gap, cfg)) {
+      copy_dev(c, Xout, X, m);
+      cp_termination t = finish(mo.gap, k, true, since(t0));
+      t.newton = cnt.newton, t.cg = cnt.cg, t.armijo = cnt.armijo, t.hess_apply = cnt.hess_apply;
+      return t;
+    }
+    best.offer(c, mo.gap, X, Z, Xb, Zb, m, me);
+    if (mo.feas > 0.5 * feas_prev) sigma = std::min(10.0 * sigma, 1e6);
+    feas_prev = mo.feas;
+    done = k;
+    if (cfg.time_limit > 0.0 && since(t0) > cfg.time_limit) break;
+  }
+  copy_dev(c, Xout, Xb, m);
+  copy_dev(c, Zout, Zb, me);
+  cp_termination t = finish(best.s, done, false, since(t0));
+  t.newton = cnt.newton, t.cg = cnt.cg, t.armijo = cnt.armijo, t.hess_apply = cnt.hess_apply;
+  return t;
+}
+
+// ---- fast AMA (ama.cpp:17-89) ---------------------------------------------------------
+cp_termination fast_ama(Prob& P, const cp_solver_config& cfg, bool warm, double* Xout, double* Zout,
+                        SolveCache& cache) {
+  Ctx& c = *P.c;
+  const auto t0 = Clock::now();
+  const int64_t d = P.d(), n = P.n(), E = P.E(), m = d * n, me = d * E;
+  initial_point(P, warm, Xout, Zout);
+  {
+    GapOut s0 = eval_gap(P, Xout, Zout);
+    if (accepts(s0, cfg)) return finish(s0, 0, true, since(t0));
+  }
+  double lmax;
+  auto it = cache.lambda_max.find(P.g->uid);
+  if (it != cache.lambda_max.end() && it->second > 0.0) {
+    lmax = it->second;
+  } else {
+    lmax = laplacian_lambda_max(c, *P.g, 1e-9, 10000);
+    cache.lambda_max[P.g->uid] = lmax;
+  }
+  if (!(lmax > 0.0)) runtime("fast AMA: spectral bound of B B^T is not positive");
+  const double step = cfg.ama_step_safety / lmax;
+  double* Zh = c.buf<double>("a.Zh", me);
+  double* Zp = c.buf<double>("a.Zp", me);
+  double* Xh = c.buf<double>("a.Xh", m);
+  double* Xb = c.buf<double>("a.Xb", m);
+  double* Zb = c.buf<double>("a.Zb", me);
+  copy_dev(c, Zh, Zout, me);
+  copy_dev(c, Zp, Zout, me);
+  double t = 1.0;
+  Best best;
+  const int64_t max_iter = resolved_max_iter(cfg);
+  int64_t k = 0;
+  while (k < max_iter) {
+    ++k;
+    ama_primal(P, Zh, Xh);
+    const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));
+    ama_dual_step(P, Xh, Zh, Zp, step, (t - 1.0) / tn);
+    t = tn;
+    if (k == 1 || k % 10 == 0 || k == max_iter) {
+      ama_primal(P, Zp, Xout);  // X = A - Znew B^T (recover_primal)
+      GapOut s = eval_gap(P, Xout, Zp);
+      if (accepts(s, cfg)) {
+        copy_dev(c, Zout, Zp, me);
+        return finish(s, k, true, since(t0));
+      }
+      best.offer(c, s, Xout, Zp, Xb, Zb, m, me);
+    }
+    if (cfg.time_limit > 0.0 && since(t0) > cfg.time_limit) break;
+  }
+  copy_dev(c, Xout, Xb, m);
+  copy_dev(c, Zout, Zb, me);
+  return finish(best.s, k, false, since(t0));
+}
+
+}  // namespace
+
+// objective.cpp:38-61
+int64_t resolved_max_iter(const cp_solver_config& c) {
+  if (c.max_iter > 0) return c.max_iter;
+  return c.algorithm == 2 ? 100 : 20000;
+}
+void validate_config(const cp_solver_config& c) {
+  if (c.algorithm < 0 || c.algorithm > 2) invalid("solve: unknown algorithm");
+  if (!(c.epsilon > 0.0) || !std::isfinite(c.epsilon)) invalid("config: epsilon must be positive and finite");
+  if (!(c.kkt_factor > 0.0) || !std::isfinite(c.kkt_factor)) invalid("config: kkt_factor must be positive and finite");
+  if (c.max_iter < 0) invalid("config: max_iter must be >= 0");
+  if (!(c.admm_rho > 0.0)) invalid("config: admm_rho must be positive");
+  if (!(c.ama_step_safety > 0.0) || c.ama_step_safety >= 1.0) invalid("config: ama_step_safety must lie in (0, 1)");
+  if (!(c.ssnal_sigma0 > 0.0)) invalid("config: ssnal_sigma0 must be positive");
+  if (!(c.armijo_mu > 0.0) || c.armijo_mu >= 0.5) invalid("config: armijo_mu must lie in (0, 0.5)");
+  if (!(c.backtrack_beta > 0.0) || c.backtrack_beta >= 1.0) invalid("config: backtrack_beta must lie in (0, 1)");
+  if (c.ssnal_newton_max < 1) invalid("config: ssnal_newton_max must be >= 1");
+  if (c.pcg_max_iter < 1) invalid("config: pcg_max_iter must be >= 1");
+}
+
+cp_termination admm_solve(Prob& P, const cp_solver_config& cfg, bool warm, double* X, double* Z, SolveCache& cache);
+
+cp_termination solve_dev(Prob& P, const cp_solver_config& cfg, bool warm, double* X, double* Z, SolveCache& cache) {
+  validate_config(cfg);
+  Ctx& c = *P.c;
+  const int64_t m = P.d() * P.n();
+  // trivial_solution (solver_util.hpp:44-51)
+  if (!(P.gamma > 0.0) || P.E() == 0) {
+    copy_dev(c, X, P.A->A.p, m);
+    if (P.E()) CPB_CUDA(cudaMemsetAsync(Z, 0, P.E() * P.d() * sizeof(double), c.s));
+    cp_termination t;
+    std::memset(&t, 0, sizeof(t));
+    t.converged = 1;
+    return t;
+  }
+  switch (cfg.algorithm) {
+    case 0: return admm_solve(P, cfg, warm, X, Z, cache);
+    case 1: return fast_ama(P, cfg, warm, X, Z, cache);
+    default: return ssnal(P, cfg, warm, X, Z);
+  }
+}
+
+// ---- clusters (path.cpp:60-89) --------------------------------------------------------
+namespace {
+// Eigen-order squared norm of a row (or a row difference) by a quad of lanes,
+// one lane per packet chain (esum in oracle/oracle.hpp).
+__device__ double quad_sqnorm(const double* x, const double* y, int d, int sub, unsigned qm) {
+  auto val = [&](int k) {
+    const double t = y ? x[k] - y[k] : x[k];
+    return t * t;
+  };
+  if (d < 4) {
+    double r = val(0);
+    if (d >= 2) r = r + val(1);
+    if (d == 3) r = r + val(2);
+    return r;
+  }
+  const int e2 = (d / 4) * 4;
+  double acc = 0.0;
+  for (int k = sub; k < e2; k += 4) acc = acc + val(k);
+  const double c0 = __shfl_sync(qm, acc, 0, 4), c1 = __shfl_sync(qm, acc, 1, 4);
+  const double c2 = __shfl_sync(qm, acc, 2, 4), c3 = __shfl_sync(qm, acc, 3, 4);
+  double p0 = c0 + c2, p1 = c1 + c3;
+  if (d - e2 >= 2) {
+    p0 = p0 + val(e2);
+    p1 = p1 + val(e2 + 1);
+  }
+  double r = p0 + p1;
+  if (d & 1) r = r + val(d - 1);
+  return r;
+}
+__device__ __forceinline__ unsigned quad_mask() { return 0xfu << ((threadIdx.x & 31u) & ~3u); }
+
+__global__ void k_row_norm_max(const double* __restrict__ X, int64_t n, int d, double* part) {
+  __shared__ double sh[32];
+  const int sub = threadIdx.x & 3;
+  const unsigned qm = quad_mask();
+  double mx = 0.0;
+  for (int64_t v = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 2; v < n;
+       v += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 2)
+    mx = fmax(mx, sqrt(quad_sqnorm(X + v * d, nullptr, d, sub, qm)));
+  mx = block_max(mx, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = mx;
+}
+__global__ void k_fused_edges(const double* __restrict__ X, const int* __restrict__ ei, const int* __restrict__ ej,
+                              int64_t E, int d, const double* thr, unsigned char* flag) {
+  const int sub = threadIdx.x & 3;
+  const unsigned qm = quad_mask();
+  const double t = *thr;
+  for (int64_t l = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 2; l < E;
+       l += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 2) {
+    const double s = sqrt(quad_sqnorm(X + static_cast<int64_t>(ei[l]) * d, X + static_cast<int64_t>(ej[l]) * d, d,
+                                      sub, qm));
+    if (sub == 0) flag[l] = s <= t;
+  }
+}
+__global__ void k_fuse_thr(const double* mx, double fuse_tol, double* thr) { *thr = fuse_tol * (1.0 + *mx); }
+__global__ void k_count(const int* labels, int n, int* cnt) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) atomicAdd(cnt + labels[v], 1);
+}
+// centroid(c, f) = (sum over members in ascending node order) / size (path.cpp:80-87)
+__global__ void k_centroids(const double* __restrict__ X, const int* __restrict__ members, const int* __restrict__ coff,
+                            int64_t K, int d, double* __restrict__ cent) {
+  const int64_t total = K * d;
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < total;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t cl = p / d;
+    const int f = static_cast<int>(p % d);
+    const int a = coff[cl], b = coff[cl + 1];
+    double s = 0.0;
+    for (int q = a; q < b; ++q) s = s + X[static_cast<int64_t>(members[q]) * d + f];
+    cent[cl * d + f] = s / static_cast<double>(b - a);
+  }
+}
+__global__ void k_iota2(int* p, int n) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) p[t] = t;
+}
+}  // namespace
+
+int64_t extract_clusters_dev(Ctx& c, const Graph& g, const double* X, int64_t d, double fuse_tol, int* labels,
+                             double* centroids) {
+  if (!(fuse_tol > 0.0)) invalid("extract_clusters: fuse_tol must be positive");
+  const int64_t n = g.n, E = g.E;
+  Ctx::Timer tm(&c, "extract_clusters", (n * d + 2.0 * E * d) * 8.0);
+  const int grid = std::max(1, std::min(cdiv(4 * n, 256), c.sm_count * 4));
+  double* part = c.buf<double>("cl.part", grid + 2);
+  double* thr = c.buf<double>("cl.thr", 2);
+  k_row_norm_max<<<grid, 256, 0, c.s>>>(X, n, static_cast<int>(d), part);
+  CPB_LAUNCH_CHECK();
+  reduce_max(c, part, grid, thr + 1);
+  k_fuse_thr<<<1, 1, 0, c.s>>>(thr + 1, fuse_tol, thr);
+  CPB_LAUNCH_CHECK();
+  unsigned char* flag = c.buf<unsigned char>("cl.flag", E + 1);
+  if (E > 0) {
+    const int ge = std::max(1, std::min(cdiv(4 * E, 256), c.sm_count * 8));
+    k_fused_edges<<<ge, 256, 0, c.s>>>(X, g.ei.p, g.ej.p, E, static_cast<int>(d), thr, flag);
+    CPB_LAUNCH_CHECK();
+  }
+  const int64_t K = components_dev(c, g, flag, labels);
+  if (centroids && n > 0) {
+    int* cnt = c.buf<int>("cl.cnt", K + 1);
+    int* coff = c.buf<int>("cl.coff", K + 1);
+    int* node = c.buf<int>("cl.node", n);
+    int* lab2 = c.buf<int>("cl.lab2", n);
+    int* members = c.buf<int>("cl.members", n);
+    CPB_CUDA(cudaMemsetAsync(cnt, 0, (K + 1) * sizeof(int), c.s));
+    const int gn = std::max(1, std::min(cdiv(n, 256), c.sm_count * 4));
+    k_count<<<gn, 256, 0, c.s>>>(labels, static_cast<int>(n), cnt);
+    k_iota2<<<gn, 256, 0, c.s>>>(node, static_cast<int>(n));
+    CPB_LAUNCH_CHECK();
+    size_t bytes = 0;
+    CPB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, coff, static_cast<int>(K + 1), c.s));
+    void* tmp = c.buf<char>("cl.cub1", bytes + 16);
+    CPB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, cnt, coff, static_cast<int>(K + 1), c.s));
+    int bits = 1;
+    while ((1ll << bits) < K) ++bits;
+    bytes = 0;
+    CPB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, labels, lab2, node, members, static_cast<int>(n), 0, bits,
+                                             c.s));
+    tmp = c.buf<char>("cl.cub2", bytes + 16);
+    CPB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, labels, lab2, node, members, static_cast<int>(n), 0, bits,
+                                             c.s));
+    const int gc = std::max(1, std::min(cdiv(K * d, 256), c.sm_count * 8));
+    k_centroids<<<gc, 256, 0, c.s>>>(X, members, coff, K, static_cast<int>(d), centroids);
+    CPB_LAUNCH_CHECK();
+  }
+  return K;
+}
+
+void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, int64_t T,
+                  const cp_solver_config& cfg, const cp_path_options& opt, double* X_out, double* Z_out,
+                  int64_t* labels_out, int64_t* K_out, cp_termination* terms_out) {
+  if (T < 1) invalid("run_path: empty schedule");
+  if (A.n != g.n) invalid("run_path: graph size does not match the data");
+  if (q != 1 && q != 2) invalid("penalty norm exponent must be 1 or 2, got " + std::to_string(q));
+  validate_config(cfg);
+  if (opt.require_connected) {
+    int* lab = c.buf<int>("path.lab0", g.n + 1);
+    const int64_t comps = components_dev(c, g, nullptr, lab);
+    if (comps > 1)
+      runtime("run_path: graph has " + std::to_string(comps) + " connected components; full fusion is unreachable");
+  }
+  const int64_t d = A.d, n = A.n, E = g.E, m = d * n, me = d * E;
+  double* X = c.buf<double>("path.X", m);
+  double* Z = c.buf<double>("path.Z", me);
+  double* rad = c.buf<double>("path.rad", E + 1);
+  int* lab = c.buf<int>("path.lab", n + 1);
+  std::vector<int> hl(static_cast<size_t>(n));
+  SolveCache cache;
+  bool warm = false;
+  for (int64_t t = 0; t < T; ++t) {
+    const double gamma = gammas[t];
+    if (!(gamma >= 0.0) || !std::isfinite(gamma)) invalid("instance: gamma must be finite and >= 0");
+    Prob P;
+    P.c = &c;
+    P.A = &A;
+    P.g = &g;
+    P.gamma = gamma;
+    P.q = q;
+    P.rad = rad;
+    make_radii(c, g, gamma, rad);
+    cp_termination term = solve_dev(P, cfg, warm, X, Z, cache);
+    const int64_t K = extract_clusters_dev(c, g, X, d, opt.fuse_tol, lab, nullptr);
+    if (terms_out) terms_out[t] = term;
+    if (K_out) K_out[t] = K;
+    if (labels_out) {
+      d2h(c, hl.data(), lab, n * sizeof(int));
+      for (int64_t i = 0; i < n; ++i) labels_out[t * n + i] = hl[static_cast<size_t>(i)];
+    }
+    if (X_out) d2h(c, X_out + t * m, X, m * sizeof(double));
+    if (Z_out && me) d2h(c, Z_out + t * me, Z, me * sizeof(double));
+    warm = opt.warm_start != 0;
+  }
+  c.sync();
+}
+
+}  // namespace cpb

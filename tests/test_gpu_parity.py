@@ -1,0 +1,333 @@
+"""GPU parity: the sm_100a path through the C-ABI against the CPU oracle.
+
+Bars: kNN edge set, order and squared distances bit-exact;
+weights within 1 ulp; B / Bᵀ / labels bit-exact; objectives and AL pieces at
+rounding level; solver iterates within 1e-6 relative Frobenius of the oracle
+and labels identical.  Reference test cases are cited per test.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ULP = 2.3e-16
+
+
+def mixture(orc, n_per, d, m=4, seed=42, spread=None, cseed=1001):
+    rng_c = orc.normals(cseed, m * d).reshape(m, d)
+    centers = (3.0 / np.sqrt(d)) * rng_c
+    return orc.gaussian_mixture(centers, spread if spread is not None else 1.0 / np.sqrt(d), n_per, seed)
+
+
+def circle(orc, n_per, m=10, seed=42):
+    ang = 2 * np.pi * np.arange(m) / m
+    centers = np.stack([4 * np.cos(ang), 4 * np.sin(ang)], axis=1)
+    return orc.gaussian_mixture(centers, 0.5, n_per, seed)
+
+
+def check_graph(cp, orc, A, k, phi):
+    g = cp.compute_knn_weights(cp.DataMatrix(A), k, phi)
+    og = orc.knn_weights(A, k, phi)
+    gi, gj, gw, gd2 = g.arrays()
+    oi, oj, ow, od2 = og.arrays()
+    assert np.array_equal(gi, oi) and np.array_equal(gj, oj)
+    assert np.array_equal(gd2, od2)
+    if len(ow):
+        assert np.max(np.abs(gw - ow) / ow) <= 2 * ULP
+    return g, og
+
+
+# ---- kNN (graph.cpp:75-114; test_graph.cpp:91-138) ------------------------------
+
+@pytest.mark.parametrize("n_per,d,k", [(25, 2, 10), (40, 3, 5), (30, 5, 7), (30, 7, 4), (20, 1, 3), (30, 64, 10),
+                                       (40, 784, 10), (25, 97, 15), (10, 4, 1)])
+def test_knn_bit_exact(cp, orc, n_per, d, k):
+    A = mixture(orc, n_per, d)
+    check_graph(cp, orc, A, k, 0.5)
+
+
+def test_knn_c1_shape(cp, orc):
+    check_graph(cp, orc, circle(orc, 100), 10, 0.5)
+
+
+def test_knn_large_k_fallback(cp, orc):
+    check_graph(cp, orc, mixture(orc, 30, 6), 40, 0.5)
+
+
+def test_knn_kats(cp, orc):
+    line = np.array([[0.0], [1.0], [3.0]])
+    g = cp.compute_knn_weights(cp.DataMatrix(line), 1, 0.0)
+    assert g.edges() == [(0, 1, 1.0), (1, 2, 1.0)]
+    g = cp.compute_knn_weights(cp.DataMatrix(line), 1, 0.5)
+    assert g.weights()[0] == pytest.approx(0.6065306597126334, rel=1e-14)
+    assert g.weights()[1] == pytest.approx(0.1353352832366127, rel=1e-14)
+    ties = np.array([[0.0, 0.0], [5.0, 0.0], [-5.0, 0.0], [5.1, 0.0], [-5.1, 0.0]])
+    g = cp.compute_knn_weights(cp.DataMatrix(ties), 1, 0.0)
+    assert g.find_edge(0, 1) is not None and g.find_edge(0, 2) is None and g.edge_count() == 3
+    for k in (0, 3):
+        with pytest.raises(ValueError):
+            cp.compute_knn_weights(cp.DataMatrix(line), k, 0.5)
+    assert cp.compute_knn_weights(cp.DataMatrix(line), 2, 0.5).edge_count() == 3
+    assert cp.compute_knn_weights(cp.DataMatrix(line[:2]), 1, 1e10).edge_count() == 0
+    with pytest.raises(ValueError):
+        cp.compute_knn_weights(cp.DataMatrix(line), 1, -1.0)
+
+
+def test_knn_duplicates_and_ties(cp, orc):
+    rng = np.random.default_rng(0)
+    A = np.round(rng.standard_normal((120, 3)), 1)  # many exact ties and duplicate points
+    A[10] = A[11] = A[12]
+    check_graph(cp, orc, A, 6, 0.5)
+
+
+def test_data_validation(cp):
+    bad = np.ones((3, 2))
+    bad[0, 0] = np.inf
+    with pytest.raises(ValueError):
+        cp.DataMatrix(bad)
+
+
+# ---- WeightedGraph / B / Bᵀ / CC (test_graph.cpp:51-232) ----------------------------
+
+def test_graph_from_edges(cp):
+    g = cp.WeightedGraph(4, [(2, 3, 0.5), (0, 1, 1.0), (1, 3, 2.0)])
+    assert g.edges() == [(0, 1, 1.0), (1, 3, 2.0), (2, 3, 0.5)]
+    assert g.degree(3) == 2 and g.max_degree() == 2 and g.find_edge(3, 1) == 1
+    for bad in ([(1, 1, 1.0)], [(3, 1, 1.0)], [(0, 4, 1.0)], [(0, 1, 0.0)], [(0, 1, -2.0)],
+                [(0, 1, 1.0), (0, 1, 2.0)], [(0, 1, float("nan"))]):
+        with pytest.raises(ValueError):
+            cp.WeightedGraph(4, bad)
+
+
+def test_incidence_bitwise(cp, orc):
+    A = mixture(orc, 40, 13)
+    g, og = check_graph(cp, orc, A, 6, 0.5)
+    B = cp.IncidenceOperator(g)
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal(A.shape)
+    Z = rng.standard_normal((g.edge_count(), A.shape[1]))
+    assert np.array_equal(B.apply(X), orc.B(og, X))
+    assert np.array_equal(B.apply_transpose(Z), orc.Bt(og, Z))
+    g3 = cp.WeightedGraph(3, [(0, 1, 1.0), (1, 2, 1.0)])
+    assert cp.IncidenceOperator(g3).apply(np.array([[5.0], [2.0], [9.0]]))[:, 0].tolist() == [3.0, -7.0]
+    with pytest.raises(ValueError):
+        cp.IncidenceOperator(g3).apply(np.zeros((4, 1)))
+    with pytest.raises(ValueError):
+        cp.IncidenceOperator(g3).apply_transpose(np.zeros((3, 1)))
+
+
+def test_connected_components(cp, orc):
+    assert cp.connected_components(cp.WeightedGraph(5, [(0, 1, 1.0), (2, 3, 1.0)])).tolist() == [0, 0, 1, 1, 2]
+    assert cp.connected_components(cp.WeightedGraph(4, [(2, 3, 1.0)])).tolist() == [0, 1, 2, 2]
+    rng = np.random.default_rng(5)
+    n = 500
+    edges = sorted({(min(a, b), max(a, b)) for a, b in rng.integers(0, n, (300, 2)) if a != b})
+    g = cp.WeightedGraph(n, [(a, b, 1.0) for a, b in edges])
+    og = orc.Graph(n, [(a, b, 1.0) for a, b in edges])
+    assert np.array_equal(cp.connected_components(g), orc.connected_components(og)[0])
+
+
+def test_laplacian_lambda_max(cp, orc):
+    g = cp.WeightedGraph(3, [(0, 1, 1.0), (1, 2, 1.0)])
+    assert cp.IncidenceOperator(g).laplacian_lambda_max() == pytest.approx(3.0, rel=1e-8)
+    A = circle(orc, 30)
+    g, og = check_graph(cp, orc, A, 10, 0.5)
+    assert cp.IncidenceOperator(g).laplacian_lambda_max() == pytest.approx(orc.power_laplacian(og), rel=1e-12)
+
+
+# ---- prox (test_prox.cpp) ------------------------------------------------------------
+
+@pytest.mark.parametrize("q", [1, 2])
+def test_prox_project_jacobian(cp, orc, q):
+    rng = np.random.default_rng(42 + q)
+    for d in (1, 2, 3, 33, 784):
+        V = rng.normal(0, 2.0, (50, d))
+        t = rng.uniform(0, 3.0 * np.sqrt(d), 50)
+        t[0] = 0.0
+        t[1] = np.linalg.norm(V[1])  # kink
+        p = cp.prox_columns(V, t, q)
+        op = orc.prox_columns(q, V, t)
+        assert np.allclose(p, op, rtol=4 * ULP, atol=1e-300)
+        z = cp.project_columns(V, t, q)
+        oz = orc.project_columns(q, V, t)
+        assert np.allclose(z, oz, rtol=4 * ULP, atol=1e-300)
+        # Moreau identity prox + projection = v (test_prox.cpp:78-87)
+        assert np.max(np.abs(p + z - V)) <= 1e-12 * max(1.0, np.max(np.abs(V)))
+        jd = cp.prox_jacobian_diag(V, t, q)
+        ojd = np.stack([orc.prox_jacobian_diag(q, V[l], t[l]) for l in range(50)])
+        assert np.allclose(jd, ojd, rtol=1e-13, atol=1e-15)
+    with pytest.raises(ValueError):
+        cp.prox_columns(np.ones((1, 2)), [-0.5], q)
+    with pytest.raises(ValueError):
+        cp.prox_columns(np.ones((1, 2)), [0.5], 3)
+
+
+# ---- objectives and AL pieces (test_solvers.cpp:108-136, 367-397) ---------------------
+
+FIVE_A = np.array([[0.0, 0.0], [1.0, 0.2], [-0.8, 0.6], [0.3, -0.9], [-0.2, 0.5]])
+FIVE_E = [(0, 1, 1.0), (0, 2, 0.7), (0, 3, 0.9), (0, 4, 1.1), (1, 2, 0.6), (1, 3, 0.8), (1, 4, 1.2),
+          (2, 3, 0.5), (2, 4, 0.95), (3, 4, 0.65)]
+
+
+def test_objectives_two_point(cp):
+    data = cp.DataMatrix([[0.0], [2.0]])
+    g = cp.WeightedGraph(2, [(0, 1, 1.0)])
+    inst = cp.ProblemInstance(data, g, 0.5)
+    assert cp.primal_objective(inst, [[0.5], [1.5]]) == pytest.approx(0.75, rel=1e-14)
+    assert cp.dual_objective(inst, [[-0.5]]) == pytest.approx(0.75, rel=1e-14)
+    with pytest.raises(ValueError):
+        cp.dual_objective(inst, [[-0.6]])
+    with pytest.raises(ValueError):
+        cp.ProblemInstance(data, cp.WeightedGraph(3, [(0, 1, 1.0)]), 0.5)
+    with pytest.raises(ValueError):
+        cp.ProblemInstance(data, g, -0.5)
+
+
+@pytest.mark.parametrize("q", [1, 2])
+def test_objectives_and_al_match_oracle(cp, orc, q):
+    A = mixture(orc, 30, 11)
+    g, og = check_graph(cp, orc, A, 6, 0.5)
+    rng = np.random.default_rng(7)
+    E = g.edge_count()
+    gamma, sigma = 0.3, 1.7
+    inst = cp.ProblemInstance(cp.DataMatrix(A), g, gamma, q)
+    X = A + 0.3 * rng.standard_normal(A.shape)
+    Z = orc.project_columns(q, 0.2 * rng.standard_normal((E, A.shape[1])), gamma * og.arrays()[2])
+    D = rng.standard_normal(A.shape)
+    rel = lambda a, b: abs(a - b) / max(1.0, abs(b))
+    assert rel(cp.primal_objective(inst, X), orc.primal_objective(A, og, gamma, q, X)) <= 1e-13
+    assert rel(cp.dual_objective(inst, Z), orc.dual_objective(A, og, gamma, q, Z)) <= 1e-13
+    assert rel(cp.kkt_residual(inst, X, Z), orc.kkt_residual(A, og, gamma, q, X, Z)) <= 1e-12
+    assert rel(cp.ssnal_phi_value(inst, Z, sigma, X), orc.phi_value(A, og, gamma, q, Z, sigma, X)) <= 1e-13
+    G, OG = cp.ssnal_phi_gradient(inst, Z, sigma, X), orc.phi_gradient(A, og, gamma, q, Z, sigma, X)
+    assert np.linalg.norm(G - OG) <= 1e-13 * np.linalg.norm(OG)
+    H, OH = cp.ssnal_hessian_apply(inst, Z, sigma, X, D), orc.hessian_apply(A, og, gamma, q, Z, sigma, X, D)
+    assert np.linalg.norm(H - OH) <= 1e-13 * np.linalg.norm(OH)
+
+
+# ---- solvers (test_solvers.cpp) ------------------------------------------------------------
+
+ALGOS = ["admm", "ama", "ssnal"]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_two_point_closed_form(cp, algo):
+    rng = np.random.default_rng(77)
+    for trial in range(6):
+        d = 1 + trial % 3
+        a1, a2 = rng.uniform(-2, 2, d), rng.uniform(-2, 2, d)
+        w, gamma = rng.uniform(0.5, 2.0), rng.uniform(0.05, 1.5)
+        inst = cp.ProblemInstance(cp.DataMatrix(np.stack([a1, a2])), cp.WeightedGraph(2, [(0, 1, w)]), gamma)
+        sol = cp.solve(inst, cp.SolverConfig(algorithm=cp.algorithm_from_name(algo), epsilon=1e-8))
+        x1, x2 = cp.two_point_closed_form(a1, a2, w, gamma)
+        assert sol.termination.converged
+        assert np.max(np.abs(sol.X[0] - x1)) <= 1e-6 and np.max(np.abs(sol.X[1] - x2)) <= 1e-6
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_trivial_and_warm(cp, algo):
+    data = cp.DataMatrix([[1.0], [-3.0]])
+    for g, gamma in ((cp.WeightedGraph(2, [(0, 1, 1.0)]), 0.0), (cp.WeightedGraph(2, []), 1.0)):
+        sol = cp.solve(cp.ProblemInstance(data, g, gamma), cp.SolverConfig(algorithm=cp.algorithm_from_name(algo)))
+        assert sol.termination.converged and sol.termination.iterations == 0 and np.array_equal(sol.X, data.values)
+    five = cp.ProblemInstance(cp.DataMatrix(FIVE_A), cp.WeightedGraph(5, FIVE_E), 0.15)
+    cfg = cp.SolverConfig(algorithm=cp.algorithm_from_name(algo), epsilon=1e-7)
+    cold = cp.solve(five, cfg)
+    warm = cp.solve(five, cfg, warm=cold)
+    assert cold.termination.converged and warm.termination.iterations == 0 and np.array_equal(warm.X, cold.X)
+    with pytest.raises(ValueError):
+        cp.solve(five, cfg, warm=cp.Solution(np.zeros((4, 2)), np.zeros((10, 2))))
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("q", [2, 1])
+def test_solver_parity_with_oracle(cp, orc, algo, q):
+    """Same instance, same algorithm: X within 1e-6 relative Frobenius, labels equal."""
+    A = mixture(orc, 25, 4, m=3, seed=9)
+    g, og = check_graph(cp, orc, A, 5, 0.5)
+    for gamma in (0.05, 0.3):
+        inst = cp.ProblemInstance(cp.DataMatrix(A), g, gamma, q)
+        sol = cp.solve(inst, cp.SolverConfig(algorithm=cp.algorithm_from_name(algo)))
+        osol = orc.solve(A, og, gamma, q, orc.config(algo))
+        assert sol.termination.converged == bool(osol.term["converged"])
+        assert np.linalg.norm(sol.X - osol.X) <= 1e-6 * np.linalg.norm(osol.X)
+        assert np.array_equal(cp.extract_clusters(sol.X, g).labels, orc.extract_clusters(osol.X, og)[0])
+
+
+def test_ssnal_iteration_path_matches(cp, orc):
+    A = mixture(orc, 30, 16, m=3, seed=3)
+    g, og = check_graph(cp, orc, A, 6, 0.5)
+    inst = cp.ProblemInstance(cp.DataMatrix(A), g, 0.2)
+    sol = cp.solve(inst)
+    osol = orc.solve(A, og, 0.2, 2)
+    t, ot = sol.termination, osol.term
+    assert (t.iterations, t.newton, t.cg, t.armijo) == (ot["iterations"], ot["newton"], ot["cg"], ot["armijo"])
+    assert np.linalg.norm(sol.X - osol.X) <= 1e-10 * np.linalg.norm(osol.X)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_deterministic(cp, algo):
+    inst = cp.ProblemInstance(cp.DataMatrix(FIVE_A), cp.WeightedGraph(5, FIVE_E), 0.12)
+    cfg = cp.SolverConfig(algorithm=cp.algorithm_from_name(algo))
+    s1, s2 = cp.solve(inst, cfg), cp.solve(inst, cfg)
+    assert np.array_equal(s1.X, s2.X) and np.array_equal(s1.Z, s2.Z)
+    assert s1.termination.iterations == s2.termination.iterations and s1.termination.gap == s2.termination.gap
+
+
+def test_iteration_cap(cp):
+    inst = cp.ProblemInstance(cp.DataMatrix(FIVE_A), cp.WeightedGraph(5, FIVE_E), 0.2)
+    sol = cp.solve(inst, cp.SolverConfig(algorithm=cp.Algorithm.ADMM, epsilon=1e-12, max_iter=3))
+    assert not sol.termination.converged and sol.termination.iterations == 3 and sol.termination.gap > 0
+
+
+# ---- path (test_path.cpp) ------------------------------------------------------------------
+
+def test_schedule_and_clusters(cp):
+    s = cp.make_schedule(1.0, 100.0, 3)
+    assert s.values == pytest.approx([1.0, 10.0, 100.0], rel=1e-14)
+    with pytest.raises(ValueError):
+        cp.make_schedule(0.5, 0.5, 2, cp.Spacing.linear)
+    chain = cp.WeightedGraph(4, [(0, 1, 1.0), (1, 2, 1.0), (2, 3, 1.0)])
+    c = cp.extract_clusters(np.array([[0.0], [1.0], [1.0], [3.0]]), chain)
+    assert c.K == 3 and c.labels.tolist() == [0, 1, 1, 2] and c.centroids[1, 0] == 1.0
+    assert cp.extract_clusters(np.array([[0.0], [1.0], [2.0], [0.0]]), chain).K == 4
+    pair = cp.WeightedGraph(2, [(0, 1, 1.0)])
+    assert cp.extract_clusters(np.array([[1000.0], [1000.5]]), pair).K == 1
+    assert cp.extract_clusters(np.array([[1000.0], [1000.5]]), pair, 1e-5).K == 2
+    with pytest.raises(ValueError):
+        cp.extract_clusters(np.zeros((3, 1)), chain)
+
+
+def test_centroids_bitwise(cp, orc):
+    A = mixture(orc, 40, 9)
+    g, og = check_graph(cp, orc, A, 6, 0.5)
+    X = np.repeat(A[::4], 4, axis=0)  # exact fusions in groups of four
+    c = cp.extract_clusters(X, g)
+    ol, oK, oc = orc.extract_clusters(X, og)
+    assert c.K == oK and np.array_equal(c.labels, ol) and np.array_equal(c.centroids, oc)
+
+
+@pytest.mark.parametrize("algo", ["ssnal", "ama"])
+def test_path_parity(cp, orc, algo):
+    A = circle(orc, 12)
+    g, og = check_graph(cp, orc, A, 10, 0.5)
+    sched = cp.make_schedule(0.01, 10.0, 8)
+    res = cp.run_path(cp.DataMatrix(A), g, 2, sched, cp.SolverConfig(algorithm=cp.algorithm_from_name(algo)))
+    ores = orc.run_path(A, og, 2, sched.values, orc.config(algo))
+    for t in range(len(sched.values)):
+        assert res.stats[t].converged == bool(ores["terms"][t]["converged"])
+        assert np.linalg.norm(res.solutions[t].X - ores["X"][t]) <= 1e-6 * np.linalg.norm(ores["X"][t])
+        assert np.array_equal(res.assignments[t].labels, ores["labels"][t])
+        assert res.assignments[t].K == ores["K"][t]
+
+
+def test_path_validation(cp):
+    data = cp.DataMatrix([[0.0], [1.0], [10.0], [11.0]])
+    g = cp.WeightedGraph(4, [(0, 1, 1.0), (2, 3, 1.0)])
+    sched = cp.make_schedule(0.5, 1.0, 2)
+    with pytest.raises(RuntimeError):
+        cp.run_path(data, g, 2, sched, options=cp.PathOptions(require_connected=True))
+    res = cp.run_path(data, g, 2, sched)
+    assert res.all_converged() and res.assignments[-1].K >= 2
+    with pytest.raises(ValueError):
+        cp.run_path(data, cp.WeightedGraph(3, [(0, 1, 1.0)]), 2, sched)
