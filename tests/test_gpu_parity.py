@@ -145,12 +145,18 @@ def test_prox_project_jacobian(cp, orc, q):
         t = rng.uniform(0, 3.0 * np.sqrt(d), 50)
         t[0] = 0.0
         t[1] = np.linalg.norm(V[1])  # kink
+        # The column norm is a tree sum on the GPU and an Eigen-order sum in the
+        # reference: they agree to a few ulp of ||v||, so compare absolutely at
+        # that scale (the kink column t = ||v|| may land on either side).
+        scale = 8 * ULP * np.linalg.norm(V, axis=1, keepdims=True) * np.sqrt(d)
         p = cp.prox_columns(V, t, q)
         op = orc.prox_columns(q, V, t)
-        assert np.allclose(p, op, rtol=4 * ULP, atol=1e-300)
+        assert np.all(np.abs(p - op) <= scale)
         z = cp.project_columns(V, t, q)
         oz = orc.project_columns(q, V, t)
-        assert np.allclose(z, oz, rtol=4 * ULP, atol=1e-300)
+        assert np.all(np.abs(z - oz) <= scale)
+        if q == 1:
+            assert np.array_equal(p, op) and np.array_equal(z, oz)
         # Moreau identity prox + projection = v (test_prox.cpp:78-87)
         assert np.max(np.abs(p + z - V)) <= 1e-12 * max(1.0, np.max(np.abs(V)))
         jd = cp.prox_jacobian_diag(V, t, q)
