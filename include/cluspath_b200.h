@@ -98,6 +98,20 @@ int cp_stats_reset(cp_ctx* ctx);
 int cp_stats_get(cp_ctx* ctx, cp_kernel_stat* out, int max_entries, int* count);
 /* Device/library identification: sm major/minor, SM count, kernel build arch. */
 int cp_device_info(cp_ctx* ctx, int* sm_major, int* sm_minor, int* sm_count, int* built_arch);
+/* Number of library kernel launches so far (process-wide). */
+unsigned long long cp_launch_count(void);
+/* CUDA-event timer on the context's stream; cp_timer_stop waits and returns ms. */
+int cp_timer_start(cp_ctx* ctx);
+int cp_timer_stop(cp_ctx* ctx, double* ms);
+/* Evict L2 by writing a buffer larger than it (benchmark hygiene). */
+int cp_flush_l2(cp_ctx* ctx);
+
+/* ---- synthetic inputs (io.cpp:142-165; host code, libstdc++ <random>) -------- */
+/* generate_gaussian_mixture(centers, spread, per_center, seed): centers d x m, out d x (m*per_center). */
+int cp_gaussian_mixture(const double* centers, int64_t d, int64_t m, double spread, int64_t per_center, uint64_t seed,
+                        double* out);
+/* count draws of std::normal_distribution<double>(0,1) over std::mt19937_64(seed). */
+int cp_normals(uint64_t seed, int64_t count, double* out);
 
 /* ---- data (types.hpp:16-28; make_data_matrix graph.cpp:10-23) ------------ */
 int cp_data_create(cp_ctx* ctx, const double* A, int64_t d, int64_t n, cp_data** out);

@@ -4,6 +4,7 @@
 // 2 runtime_error; the message is kept per thread.
 #include "oracle.hpp"
 
+#include <chrono>
 #include <cstring>
 
 using namespace oracle;
@@ -355,6 +356,137 @@ int orc_mixture(const double* centers, int64_t d, int64_t m, double spread, int6
     put(gaussian_mixture(c, spread, per_center, seed), out);
   });
 }
+// ---- CPU-baseline unit costs (bench.py cpu_baseline / --impl reference) ----------
+// Seconds for the kNN of the first `rows` samples against all n (graph.cpp:90-103).
+int orc_time_knn_rows(const double* A, int64_t d, int64_t n, int64_t k, int64_t rows, double* seconds) {
+  return guard([&] {
+    Mat Am = wrap(A, d, n);
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::pair<double, Index>> cand;
+    volatile double sink = 0.0;
+    for (Index i = 0; i < rows && i < n; ++i) {
+      cand.clear();
+      for (Index j = 0; j < n; ++j) {
+        if (j == i) continue;
+        const double* x = Am.col(i);
+        const double* y = Am.col(j);
+        cand.emplace_back(esum(d, [&](Index r) {
+                            const double t = x[r] - y[r];
+                            return t * t;
+                          }),
+                          j);
+      }
+      std::partial_sort(cand.begin(), cand.begin() + k, cand.end());
+      sink = sink + cand[0].first;
+    }
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+// Seconds per call of the SSNAL building blocks at (gamma, sigma), X = A, Z = 0:
+// out[0] eval_phi, [1] gradient, [2] jacobians + Jacobi diagonal, [3] Hessian
+// apply, [4] one PCG vector update (x, r, z, p, dots, row norms), [5] gap
+// (primal + dual + KKT), [6] multiplier step (B X, envelope, projection).
+int orc_time_ssnal_units(const double* A, int64_t d, int64_t n, void* gp, double gamma, int q, double sigma,
+                         int reps, double* out) {
+  return guard([&] {
+    Mat Am = wrap(A, d, n);
+    const Graph& g = static_cast<OGraph*>(gp)->g;
+    Instance in(Am, g, gamma, nq(q));
+    Mat Z(d, g.E(), 0.0), X = Am;
+    const Index E = g.E();
+    using C = std::chrono::steady_clock;
+    auto secs = [](C::time_point a) { return std::chrono::duration<double>(C::now() - a).count(); };
+    std::vector<double> thr = in.radii();
+    for (double& x : thr) x /= sigma;
+    double t[7] = {0, 0, 0, 0, 0, 0, 0};
+    volatile double sink = 0.0;
+    for (int r = 0; r < reps; ++r) {
+      auto t0 = C::now();
+      // eval_phi (ssnal.cpp:24-39)
+      Mat V, PV;
+      incidence_apply(g, X, V);
+      for (Index k = 0; k < V.size(); ++k) V.v[static_cast<size_t>(k)] += Z.v[static_cast<size_t>(k)] / sigma;
+      prox_columns_into(V, thr, in.q, PV);
+      double env = 0.0;
+      std::vector<double> diff(static_cast<size_t>(d));
+      for (Index l = 0; l < E; ++l) {
+        for (Index rr = 0; rr < d; ++rr) diff[static_cast<size_t>(rr)] = PV(rr, l) - V(rr, l);
+        env += in.gamma * g.edges[static_cast<size_t>(l)].w * norm_value(PV.col(l), d, in.q) + 0.5 * sigma * sq_norm(diff.data(), d);
+      }
+      sink = sink + env;
+      t[0] += secs(t0);
+      t0 = C::now();
+      Mat U(d, E), T;
+      for (Index k = 0; k < U.size(); ++k) U.v[static_cast<size_t>(k)] = V.v[static_cast<size_t>(k)] - PV.v[static_cast<size_t>(k)];
+      incidence_apply_t(g, U, T);
+      Mat G(d, n);
+      for (Index k = 0; k < G.size(); ++k) G.v[static_cast<size_t>(k)] = X.v[static_cast<size_t>(k)] - Am.v[static_cast<size_t>(k)] + sigma * T.v[static_cast<size_t>(k)];
+      sink = sink + sq_norm(G.v.data(), G.size());
+      t[1] += secs(t0);
+      t0 = C::now();
+      std::vector<ProxJac> J;
+      J.reserve(static_cast<size_t>(E));
+      for (Index l = 0; l < E; ++l) J.push_back(prox_jacobian(V.col(l), d, thr[static_cast<size_t>(l)], in.q));
+      Mat dg(d, n, 1.0);
+      for (Index l = 0; l < E; ++l) {
+        const Edge& e = g.edges[static_cast<size_t>(l)];
+        for (Index rr = 0; rr < d; ++rr) {
+          const double c = sigma * (1.0 - J[static_cast<size_t>(l)].diag(rr));
+          dg(rr, e.i) += c;
+          dg(rr, e.j) += c;
+        }
+      }
+      t[2] += secs(t0);
+      t0 = C::now();
+      Mat W;
+      incidence_apply(g, G, W);
+      std::vector<double> jw(static_cast<size_t>(d));
+      for (Index l = 0; l < E; ++l) {
+        J[static_cast<size_t>(l)].apply(W.col(l), d, jw.data());
+        for (Index rr = 0; rr < d; ++rr) W(rr, l) = W(rr, l) - jw[static_cast<size_t>(rr)];
+      }
+      Mat T2;
+      incidence_apply_t(g, W, T2);
+      Mat H(d, n);
+      for (Index k = 0; k < H.size(); ++k) H.v[static_cast<size_t>(k)] = G.v[static_cast<size_t>(k)] + sigma * T2.v[static_cast<size_t>(k)];
+      t[3] += secs(t0);
+      t0 = C::now();
+      {
+        Mat x(d, n, 0.0), rr = G, p = G;
+        const double alpha = 0.5;
+        for (Index k = 0; k < x.size(); ++k) x.v[static_cast<size_t>(k)] += alpha * p.v[static_cast<size_t>(k)];
+        for (Index k = 0; k < rr.size(); ++k) rr.v[static_cast<size_t>(k)] -= alpha * H.v[static_cast<size_t>(k)];
+        double worst = 0.0;
+        for (Index i = 0; i < d; ++i) worst = std::max(worst, std::sqrt(ssum(n, [&](Index c) { return rr(i, c) * rr(i, c); })));
+        Mat z(d, n);
+        for (Index k = 0; k < z.size(); ++k) z.v[static_cast<size_t>(k)] = rr.v[static_cast<size_t>(k)] / dg.v[static_cast<size_t>(k)];
+        const double rz = dotp(rr.v.data(), z.v.data(), rr.size());
+        const double pAp = dotp(p.v.data(), H.v.data(), p.size());
+        for (Index k = 0; k < p.size(); ++k) p.v[static_cast<size_t>(k)] = z.v[static_cast<size_t>(k)] + 0.3 * p.v[static_cast<size_t>(k)];
+        sink = sink + worst + rz + pAp;
+      }
+      t[4] += secs(t0);
+      t0 = C::now();
+      sink = sink + primal_objective(in, X) + dual_objective(in, Z) + kkt_residual(in, X, Z);
+      t[5] += secs(t0);
+      t0 = C::now();
+      {
+        Mat XB;
+        incidence_apply(g, X, XB);
+        Mat Zenv(d, E), Zsum(d, E);
+        for (Index k = 0; k < Zenv.size(); ++k) {
+          Zenv.v[static_cast<size_t>(k)] = sigma * (V.v[static_cast<size_t>(k)] - PV.v[static_cast<size_t>(k)]);
+          Zsum.v[static_cast<size_t>(k)] = Z.v[static_cast<size_t>(k)] + sigma * XB.v[static_cast<size_t>(k)];
+        }
+        project_columns_inplace(Zsum, in.radii(), in.q);
+        sink = sink + max_abs(Zenv.v.data(), Zenv.size()) + max_abs(Zsum.v.data(), Zsum.size());
+      }
+      t[6] += secs(t0);
+    }
+    for (int k = 0; k < 7; ++k) out[k] = t[k] / reps;
+  });
+}
+
 // N(0,1) draws of libstdc++ normal_distribution over mt19937_64(seed).
 void orc_normals(uint64_t seed, int64_t count, double* out) {
   std::mt19937_64 rng(seed);

@@ -402,6 +402,27 @@ def gaussian_mixture(centers, spread, per_center, seed):
     return out
 
 
+def time_knn_rows(A, k, rows):
+    """Seconds for the reference kNN of the first `rows` samples (graph.cpp:90-103)."""
+    A = _f64(A)
+    n, d = A.shape
+    s = C.c_double()
+    _check(lib().orc_time_knn_rows(_dp(A), _ci(d), _ci(n), _ci(k), _ci(rows), C.byref(s)))
+    return s.value
+
+
+SSNAL_UNITS = ("eval_phi", "gradient", "jacobian_diag", "hess_apply", "pcg_vec", "gap", "multiplier")
+
+
+def time_ssnal_units(A, g, gamma, q=2, sigma=1.0, reps=1):
+    """Seconds per call of each SSNAL building block (ssnal.cpp), dict keyed by SSNAL_UNITS."""
+    A, d, n = _inst(A)
+    out = np.empty(7)
+    _check(lib().orc_time_ssnal_units(_dp(A), _ci(d), _ci(n), g._h, _cd(gamma), q, _cd(sigma), int(reps),
+                                      _dp(out)))
+    return dict(zip(SSNAL_UNITS, out.tolist()))
+
+
 def normals(seed, count):
     out = np.empty(int(count))
     lib().orc_normals(C.c_uint64(seed), _ci(count), _dp(out))

@@ -12,7 +12,8 @@ from .cluspath import (Algorithm, ClusterAssignment, Context, DataMatrix, GammaS
                        PathOptions, PathResult, PenaltyNorm, ProblemInstance, Solution, SolverConfig, Spacing,
                        TerminationRecord, WeightedGraph, algorithm_from_name, algorithm_name, component_count,
                        compute_knn_weights, connected_components, default_context, dual_objective, duality_gap,
-                       extract_clusters, kkt_residual, make_data_matrix, make_schedule, penalty_norm_from_q,
+                       extract_clusters, flush_l2, generate_gaussian_mixture, kkt_residual, launch_count,
+                       make_data_matrix, make_schedule, normals, penalty_norm_from_q, timer_start, timer_stop,
                        primal_objective, project_columns, prox_columns, prox_jacobian_diag, recover_primal, run_path,
                        solve, ssnal_hessian_apply, ssnal_phi_gradient, ssnal_phi_value, two_point_closed_form)
 

@@ -56,6 +56,12 @@ _SIGS = [
     ("cp_stats_get", C.c_int, [VP, C.POINTER(KernelStatC), C.c_int, C.POINTER(C.c_int)]),
     ("cp_device_info", C.c_int, [VP, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                  C.POINTER(C.c_int)]),
+    ("cp_launch_count", C.c_ulonglong, []),
+    ("cp_timer_start", C.c_int, [VP]),
+    ("cp_timer_stop", C.c_int, [VP, D]),
+    ("cp_flush_l2", C.c_int, [VP]),
+    ("cp_gaussian_mixture", C.c_int, [D, C.c_int64, C.c_int64, C.c_double, C.c_int64, C.c_uint64, D]),
+    ("cp_normals", C.c_int, [C.c_uint64, C.c_int64, D]),
     ("cp_data_create", C.c_int, [VP, D, C.c_int64, C.c_int64, C.POINTER(VP)]),
     ("cp_data_destroy", None, [VP]),
     ("cp_knn_graph", C.c_int, [VP, VP, C.c_int64, C.c_double, C.POINTER(VP)]),

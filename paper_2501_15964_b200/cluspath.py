@@ -70,6 +70,41 @@ class Context:
                 for k in range(min(cnt.value, 64))}
 
 
+def launch_count() -> int:
+    """Library kernel launches so far in this process."""
+    return int(L.load().cp_launch_count())
+
+
+def timer_start(ctx: Context):
+    L.check(L.load().cp_timer_start(ctx._h))
+
+
+def timer_stop(ctx: Context) -> float:
+    ms = C.c_double()
+    L.check(L.load().cp_timer_stop(ctx._h, C.byref(ms)))
+    return ms.value
+
+
+def flush_l2(ctx: Context):
+    L.check(L.load().cp_flush_l2(ctx._h))
+
+
+def normals(seed: int, count: int):
+    """libstdc++ N(0,1) draws over mt19937_64(seed) (the generator io.cpp uses)."""
+    out = np.empty(int(count))
+    L.check(L.load().cp_normals(C.c_uint64(seed), int(count), _dp(out)))
+    return out
+
+
+def generate_gaussian_mixture(centers, spread, per_center, seed):
+    """generate_gaussian_mixture (io.cpp:142-165); centers (m, d) -> samples (m*per_center, d)."""
+    c = np.ascontiguousarray(centers, dtype=np.float64)
+    m, d = c.shape
+    out = np.empty((m * int(per_center), d))
+    L.check(L.load().cp_gaussian_mixture(_dp(c), d, m, float(spread), int(per_center), C.c_uint64(seed), _dp(out)))
+    return out
+
+
 def default_context(device: int = 0) -> Context:
     ctx = _ctx_cache.get(device)
     if ctx is None:

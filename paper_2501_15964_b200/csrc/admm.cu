@@ -8,6 +8,7 @@
 #include <cmath>
 #include <limits>
 
+#include "gather.cuh"
 #include "solve.cuh"
 
 namespace cpb {
@@ -33,64 +34,6 @@ __device__ __forceinline__ double soft(double v, double t) {
   return static_cast<double>((v > 0.0) - (v < 0.0)) * fmax(fabs(v) - t, 0.0);
 }
 
-// RHS = A + (rho U - Lam) B^T  (admm.cpp:61)
-__global__ void k_admm_rhs(const double* __restrict__ A, const double* __restrict__ U, const double* __restrict__ L,
-                           double rho, const int* __restrict__ off, const int* __restrict__ adj_e,
-                           const int* __restrict__ adj_o, const int* __restrict__ order, int64_t n, int d,
-                           double* __restrict__ R) {
-  ROWS_BEGIN(n) {
-    const int v = order[row_];
-    const int p0 = off[v], p1 = off[v + 1];
-    const int64_t base = static_cast<int64_t>(v) * d;
-    for (int f = threadIdx.x; f < d; f += blockDim.x) {
-      double acc = 0.0;
-      for (int p = p0; p < p1; ++p) {
-        const int64_t i = static_cast<int64_t>(adj_e[p]) * d + f;
-        const double z = rho * U[i] - L[i];
-        acc = (adj_o[p] > v) ? acc + z : acc - z;
-      }
-      R[base + f] = A[base + f] + acc;
-    }
-  }
-}
-
-// (I + rho L) y and its pAp / pp partials; L y = deg y_v - sum_u y_u.
-__global__ void k_lap_op(const double* __restrict__ y, double rho, const int* __restrict__ off,
-                         const int* __restrict__ adj_o, const int* __restrict__ order, int64_t n, int d,
-                         double* __restrict__ out, double* part, const int* active) {
-  if (active && !*active) return;
-  __shared__ double sh[32];
-  const unsigned gm = group_mask();
-  double s_pap = 0.0, s_pp = 0.0;
-  ROWS_BEGIN(n) {
-    const int v = order[row_];
-    const int p0 = off[v], p1 = off[v + 1];
-    const double deg = static_cast<double>(p1 - p0);
-    const int64_t base = static_cast<int64_t>(v) * d;
-    double a = 0.0, b = 0.0;
-    for (int f = threadIdx.x; f < d; f += blockDim.x) {
-      double nb = 0.0;
-      for (int p = p0; p < p1; ++p) nb += y[static_cast<int64_t>(adj_o[p]) * d + f];
-      const double yv = y[base + f];
-      const double o = yv + rho * (deg * yv - nb);
-      out[base + f] = o;
-      a += yv * o;
-      b += yv * yv;
-    }
-    a = group_sum(a, gm);
-    b = group_sum(b, gm);
-    if (threadIdx.x == 0) {
-      s_pap += a;
-      s_pp += b;
-    }
-  }
-  s_pap = block_sum(s_pap, sh);
-  s_pp = block_sum(s_pp, sh);
-  if (threadIdx.x == 0 && threadIdx.y == 0) {
-    part[2 * blockIdx.x] = s_pap;
-    part[2 * blockIdx.x + 1] = s_pp;
-  }
-}
 __global__ void k_lap_diag(const int* __restrict__ off, int64_t n, int d, double rho, double* __restrict__ diag) {
   const int64_t m = n * d;
   for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
@@ -188,21 +131,16 @@ cp_termination admm_solve(Prob& P, const cp_solver_config& cfg, bool warm, doubl
     k_lap_diag<<<fg, 256, 0, c.s>>>(P.g->off.p, n, static_cast<int>(d), rho, w.diag);
     CPB_LAUNCH_CHECK();
   }
-  GG gn = geom(c, n, d), ge = geom(c, E, d);
+  GG ge = geom(c, E, d);
   const Graph& g = *P.g;
   PcgOp op = [&](const double* p, double* Ap, double* part, const void* st) {
-    k_lap_op<<<gn.grid, dim3(gn.gx, gn.gy), 0, c.s>>>(p, rho, g.off.p, g.adj_o.p, g.order.p, n, static_cast<int>(d),
-                                                      Ap, part, cg_active_ptr(st));
-    CPB_LAUNCH_CHECK();
-    return gn.grid;
+    return gather_lap(c, g, p, rho, d, Ap, part, cg_active_ptr(st));
   };
   double best_gap = std::numeric_limits<double>::infinity();
   GapOut best_s;
   const int64_t max_iter = resolved_max_iter(cfg);
   for (int64_t k = 1; k <= max_iter; ++k) {
-    k_admm_rhs<<<gn.grid, dim3(gn.gx, gn.gy), 0, c.s>>>(P.A->A.p, U, Lam, rho, g.off.p, g.adj_e.p, g.adj_o.p,
-                                                        g.order.p, n, static_cast<int>(d), R);
-    CPB_LAUNCH_CHECK();
+    gather_admm_rhs(c, g, P.A->A.p, U, Lam, rho, d, R);
     pcg_dev(c, n, d, op, (2.0 * m + 2.0 * E) * 8.0, "lap_apply", R, w, 1e-13, 100000, true);
     k_admm_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, U, Lam, Zc, P.rad, g.ei.p, g.ej.p, E,
                                                          static_cast<int>(d), rho, P.q);

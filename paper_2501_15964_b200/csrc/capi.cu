@@ -5,6 +5,7 @@
 // without a CUDA device cp_ctx_create fails with CP_ERUNTIME.
 #include <cmath>
 #include <cstring>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -144,6 +145,62 @@ int cp_device_info(cp_ctx* ctx, int* sm_major, int* sm_minor, int* sm_count, int
     if (built_arch) *built_arch = 100;
   });
 }
+unsigned long long cp_launch_count(void) { return cpb::g_launches; }
+
+int cp_timer_start(cp_ctx* ctx) {
+  return guard(ctx, [&] {
+    cpb::Ctx& c = *ctx->c;
+    c.timer_a = c.timer_a ? c.timer_a : c.get_event();
+    c.timer_b = c.timer_b ? c.timer_b : c.get_event();
+    CPB_CUDA(cudaEventRecord(c.timer_a, c.s));
+  });
+}
+int cp_timer_stop(cp_ctx* ctx, double* ms) {
+  return guard(ctx, [&] {
+    cpb::Ctx& c = *ctx->c;
+    if (!c.timer_a) cpb::invalid("cp_timer_stop without cp_timer_start");
+    CPB_CUDA(cudaEventRecord(c.timer_b, c.s));
+    CPB_CUDA(cudaEventSynchronize(c.timer_b));
+    float f = 0.f;
+    CPB_CUDA(cudaEventElapsedTime(&f, c.timer_a, c.timer_b));
+    if (ms) *ms = f;
+  });
+}
+int cp_flush_l2(cp_ctx* ctx) {
+  return guard(ctx, [&] {
+    cpb::Ctx& c = *ctx->c;
+    const size_t bytes = size_t(512) << 20;  // 4x the 126 MB L2
+    char* p = c.buf<char>("api.flush", bytes);
+    CPB_CUDA(cudaMemsetAsync(p, 1, bytes, c.s));
+    c.sync();
+  });
+}
+
+int cp_gaussian_mixture(const double* centers, int64_t d, int64_t m, double spread, int64_t per_center, uint64_t seed,
+                        double* out) {
+  return guard(nullptr, [&] {
+    if (m < 1) cpb::invalid("mixture needs at least one center");
+    if (per_center < 1) cpb::invalid("mixture needs per_center >= 1");
+    if (!(spread >= 0.0)) cpb::invalid("mixture spread must be >= 0");
+    need(centers, "centers");
+    need(out, "out");
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    int64_t col = 0;
+    for (int64_t c = 0; c < m; ++c)
+      for (int64_t s = 0; s < per_center; ++s, ++col)
+        for (int64_t r = 0; r < d; ++r) out[col * d + r] = centers[c * d + r] + spread * gauss(rng);
+  });
+}
+int cp_normals(uint64_t seed, int64_t count, double* out) {
+  return guard(nullptr, [&] {
+    need(out, "out");
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    for (int64_t k = 0; k < count; ++k) out[k] = gauss(rng);
+  });
+}
+
 int cp_stats_enable(cp_ctx* ctx, int on) {
   return guard(ctx, [&] { ctx->c->stats_on = on != 0; });
 }

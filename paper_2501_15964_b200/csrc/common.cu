@@ -3,6 +3,8 @@
 
 namespace cpb {
 
+unsigned long long g_launches = 0;
+
 Ctx::Ctx(int dev) : device(dev) {
   int count = 0;
   CPB_CUDA(cudaGetDeviceCount(&count));
@@ -31,6 +33,8 @@ Ctx::~Ctx() {
     cudaEventDestroy(p.b);
   }
   for (auto e : event_pool) cudaEventDestroy(e);
+  if (timer_a) cudaEventDestroy(timer_a);
+  if (timer_b) cudaEventDestroy(timer_b);
   ws.clear();
   if (hscal) cudaFreeHost(hscal);
   if (dscal) cudaFree(dscal);

@@ -39,7 +39,15 @@ struct Error : std::runtime_error {
       throw ::cpb::Error(CP_ECUDA, std::string("CUDA error ") + cudaGetErrorString(e_) +    \
                                        " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
   } while (0)
-#define CPB_LAUNCH_CHECK() CPB_CUDA(cudaGetLastError())
+// Every kernel launch of the library is followed by exactly one
+// CPB_LAUNCH_CHECK, which also counts it (cp_launch_count; CUB's internal
+// sort/scan kernels are not counted).
+extern unsigned long long g_launches;
+#define CPB_LAUNCH_CHECK()              \
+  do {                                  \
+    ++::cpb::g_launches;                \
+    CPB_CUDA(cudaGetLastError());       \
+  } while (0)
 
 // ---- device buffers --------------------------------------------------------
 template <class T>
@@ -104,6 +112,7 @@ struct Ctx {
   };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t timer_a = nullptr, timer_b = nullptr;  // cp_timer_start / cp_timer_stop
 
   explicit Ctx(int dev);
   ~Ctx();

@@ -1,0 +1,520 @@
+// Node-CSR gather kernels (see gather.cuh).
+//
+// Work item = (node, feature chunk): one warp owns up to 32*NF consecutive
+// features (lane l holds f = chunk0 + l + 32 k, k < NF) of one node and walks
+// the node's incident edges in ascending id.  Edge metadata (id, other
+// endpoint, per-edge scalars) is fetched 32 edges at a time with one
+// coalesced load per lane and handed out by warp shuffles; feature rows are
+// then loaded 4 edges x NF features at a time (all issued before use).  No
+// block-wide barriers: warps never wait on each other, so a hub node only
+// delays its own warps.  Items are enumerated hubs-first (descending degree).
+// Per-(node, feature) accumulation order = ascending edge id = the reference's
+// scatter order (graph.cpp:140-152), bitwise.
+#include <cstdlib>
+
+#include "gather.cuh"
+
+namespace cpb {
+
+namespace {
+
+constexpr int kEB = 4;  // edges per load batch
+constexpr unsigned kFull = 0xffffffffu;
+
+struct ChunkGeom {
+  int nch;  // chunks per node
+  int nf;   // features per lane
+};
+// Up to 32 * nf_max features per warp (CPB_NFMAX overrides the default 6, tuning only).
+inline ChunkGeom chunk_geom(int64_t d) {
+  static const int nf_max = [] {
+    const char* e = std::getenv("CPB_NFMAX");
+    const int v = e ? std::atoi(e) : 6;
+    return v < 1 ? 1 : (v > 6 ? 6 : v);
+  }();
+  const int nch = static_cast<int>((d + 32 * nf_max - 1) / (32 * nf_max));
+  const int nf = static_cast<int>((d + 32 * nch - 1) / (32 * nch));
+  return {nch, nf};
+}
+
+// Item loop: warp w of the grid takes items w, w + W, ... (static: the
+// per-block partial sums are deterministic).
+#define ITEMS_BEGIN(n, nch)                                                                               \
+  const int lane = threadIdx.x & 31;                                                                      \
+  const int64_t nitems_ = (n) * (nch);                                                                    \
+  for (int64_t it_ = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; it_ < nitems_; \
+       it_ += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {                                      \
+    const int v = order[it_ / (nch)];                                                                     \
+    const int f0 = static_cast<int>(it_ % (nch)) * 32 * NF + lane;                                        \
+    const int p0 = off[v], p1 = off[v + 1];                                                               \
+    const int64_t base = static_cast<int64_t>(v) * d;
+
+#define ITEMS_END }
+
+// ---- Bᵀ-type gathers ------------------------------------------------------------------
+// mode 0: out = sum z;  1: out = A - sum z;  2: out = A + sum (rho U - L)
+template <int NF>
+__global__ void __launch_bounds__(256) k_g_bt(const double* __restrict__ Z, const double* __restrict__ Z2,
+                                              const double* __restrict__ A, double rho, const int* __restrict__ off,
+                                              const int* __restrict__ adj_e, const int* __restrict__ adj_o,
+                                              const int* __restrict__ order, int64_t n, int d, int nch, int mode,
+                                              double* __restrict__ out) {
+  ITEMS_BEGIN(n, nch)
+  double acc[NF];
+#pragma unroll
+  for (int k = 0; k < NF; ++k) acc[k] = 0.0;
+  for (int p = p0; p < p1; p += 32) {
+    const int cnt = min(32, p1 - p);
+    const int my_e = lane < cnt ? adj_e[p + lane] : 0;
+    const int my_o = lane < cnt ? adj_o[p + lane] : 0;
+    for (int u0 = 0; u0 < cnt; u0 += kEB) {
+      int le[kEB];
+      bool pl[kEB];
+#pragma unroll
+      for (int u = 0; u < kEB; ++u) {
+        le[u] = __shfl_sync(kFull, my_e, (u0 + u) & 31);
+        pl[u] = __shfl_sync(kFull, my_o, (u0 + u) & 31) > v;
+      }
+      double x[kEB][NF];
+#pragma unroll
+      for (int u = 0; u < kEB; ++u)
+#pragma unroll
+        for (int k = 0; k < NF; ++k) {
+          const int f = f0 + 32 * k;
+          x[u][k] = 0.0;
+          if (u0 + u < cnt && f < d) {
+            const int64_t i = static_cast<int64_t>(le[u]) * d + f;
+            x[u][k] = (mode == 2) ? rho * __ldcs(Z + i) - __ldcs(Z2 + i) : __ldcs(Z + i);
+          }
+        }
+#pragma unroll
+      for (int u = 0; u < kEB; ++u)
+        if (u0 + u < cnt)
+#pragma unroll
+          for (int k = 0; k < NF; ++k) acc[k] = pl[u] ? acc[k] + x[u][k] : acc[k] - x[u][k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NF; ++k) {
+    const int f = f0 + 32 * k;
+    if (f < d) out[base + f] = (mode == 0) ? acc[k] : (mode == 1 ? A[base + f] - acc[k] : A[base + f] + acc[k]);
+  }
+  ITEMS_END
+}
+
+// ---- (I + rho L) y and its (pAp, pp) block partials ----------------------------------------
+template <int NF>
+__global__ void __launch_bounds__(256) k_g_lap(const double* __restrict__ y, double rho, const int* __restrict__ off,
+                                               const int* __restrict__ adj_o, const int* __restrict__ order, int64_t n,
+                                               int d, int nch, double* __restrict__ out, double* part,
+                                               const int* active) {
+  if (active && !*active) return;
+  __shared__ double sh[32];
+  double s_a = 0.0, s_b = 0.0;
+  ITEMS_BEGIN(n, nch)
+  const double deg = static_cast<double>(p1 - p0);
+  double nb[NF];
+#pragma unroll
+  for (int k = 0; k < NF; ++k) nb[k] = 0.0;
+  for (int p = p0; p < p1; p += 32) {
+    const int cnt = min(32, p1 - p);
+    const int my_o = lane < cnt ? adj_o[p + lane] : 0;
+    for (int u0 = 0; u0 < cnt; u0 += kEB) {
+      int lo[kEB];
+#pragma unroll
+      for (int u = 0; u < kEB; ++u) lo[u] = __shfl_sync(kFull, my_o, (u0 + u) & 31);
+      double x[kEB][NF];
+#pragma unroll
+      for (int u = 0; u < kEB; ++u)
+#pragma unroll
+        for (int k = 0; k < NF; ++k) {
+          const int f = f0 + 32 * k;
+          x[u][k] = (u0 + u < cnt && f < d) ? y[static_cast<int64_t>(lo[u]) * d + f] : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < kEB; ++u)
+#pragma unroll
+        for (int k = 0; k < NF; ++k) nb[k] += x[u][k];
+    }
+  }
+  double a = 0.0, b = 0.0;
+#pragma unroll
+  for (int k = 0; k < NF; ++k) {
+    const int f = f0 + 32 * k;
+    if (f >= d) continue;
+    const double yv = y[base + f];
+    const double o = yv + rho * (deg * yv - nb[k]);
+    out[base + f] = o;
+    a += yv * o;
+    b += yv * yv;
+  }
+  s_a += a;
+  s_b += b;
+  ITEMS_END
+  s_a = block_sum(s_a, sh);
+  s_b = block_sum(s_b, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s_a;
+    part[2 * blockIdx.x + 1] = s_b;
+  }
+}
+
+// ---- gap node terms (objective.cpp:76-88, :100-106) ---------------------------------------
+// part[4b + k]: ||X - A||^2, ||Z Bᵀ||^2, <Z Bᵀ, A>, ||X - A + Z Bᵀ||^2
+template <int NF>
+__global__ void __launch_bounds__(256) k_g_gap(const double* __restrict__ X, const double* __restrict__ A,
+                                               const double* __restrict__ Z, const int* __restrict__ off,
+                                               const int* __restrict__ adj_e, const int* __restrict__ adj_o,
+                                               const int* __restrict__ order, int64_t n, int d, int nch,
+                                               double* part) {
+  __shared__ double sh[32];
+  double s[4] = {0, 0, 0, 0};
+  ITEMS_BEGIN(n, nch)
+  double acc[NF];
+#pragma unroll
+  for (int k = 0; k < NF; ++k) acc[k] = 0.0;
+  for (int p = p0; p < p1; p += 32) {
+    const int cnt = min(32, p1 - p);
+    const int my_e = lane < cnt ? adj_e[p + lane] : 0;
+    const int my_o = lane < cnt ? adj_o[p + lane] : 0;
+    for (int u0 = 0; u0 < cnt; u0 += kEB) {
+      int le[kEB];
+      bool pl[kEB];
+#pragma unroll
+      for (int u = 0; u < kEB; ++u) {
+        le[u] = __shfl_sync(kFull, my_e, (u0 + u) & 31);
+        pl[u] = __shfl_sync(kFull, my_o, (u0 + u) & 31) > v;
+      }
+      double x[kEB][NF];
+#pragma unroll
+      for (int u = 0; u < kEB; ++u)
+#pragma unroll
+        for (int k = 0; k < NF; ++k) {
+          const int f = f0 + 32 * k;
+          x[u][k] = (u0 + u < cnt && f < d) ? __ldcs(Z + static_cast<int64_t>(le[u]) * d + f) : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < kEB; ++u)
+        if (u0 + u < cnt)
+#pragma unroll
+          for (int k = 0; k < NF; ++k) acc[k] = pl[u] ? acc[k] + x[u][k] : acc[k] - x[u][k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NF; ++k) {
+    const int f = f0 + 32 * k;
+    if (f >= d) continue;
+    const double a = A[base + f];
+    const double xa = X[base + f] - a;
+    const double st = xa + acc[k];
+    s[0] += xa * xa;
+    s[1] += acc[k] * acc[k];
+    s[2] += acc[k] * a;
+    s[3] += st * st;
+  }
+  ITEMS_END
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double r = block_sum(s[k], sh);
+    if (threadIdx.x == 0) part[4 * blockIdx.x + k] = r;
+  }
+}
+
+__device__ __forceinline__ double softd(double v, double t) {
+  return static_cast<double>((v > 0.0) - (v < 0.0)) * fmax(fabs(v) - t, 0.0);
+}
+
+// ---- SSNAL gradient + Jacobi diagonal (ssnal.cpp:41-44, :68-82) ---------------------------
+template <int NF>
+__global__ void __launch_bounds__(256) k_g_grad(const double* __restrict__ X, const double* __restrict__ A,
+                                                const double* __restrict__ V, const double* __restrict__ ps,
+                                                const double* __restrict__ jal, const double* __restrict__ jbe,
+                                                const double* __restrict__ thr, const int* __restrict__ off,
+                                                const int* __restrict__ adj_e, const int* __restrict__ adj_o,
+                                                const int* __restrict__ order, int64_t n, int d, int nch,
+                                                double sigma, int q, int want_diag, double* __restrict__ G,
+                                                double* __restrict__ diag, double* part) {
+  __shared__ double sh[32];
+  double s_g = 0.0;
+  ITEMS_BEGIN(n, nch)
+  double ag[NF], ad[NF];
+#pragma unroll
+  for (int k = 0; k < NF; ++k) {
+    ag[k] = 0.0;
+    ad[k] = 1.0;
+  }
+  for (int p = p0; p < p1; p += 32) {
+    const int cnt = min(32, p1 - p);
+    const int my_e = lane < cnt ? adj_e[p + lane] : 0;
+    const int my_o = lane < cnt ? adj_o[p + lane] : 0;
+    const double my_s = lane < cnt ? (q == 2 ? ps[my_e] : thr[my_e]) : 0.0;
+    const double my_a = (lane < cnt && q == 2) ? jal[my_e] : 0.0;
+    const double my_b = (lane < cnt && q == 2) ? jbe[my_e] : 0.0;
+    for (int u0 = 0; u0 < cnt; u0 += kEB) {
+      int le[kEB];
+      bool pl[kEB];
+      double es[kEB], ea[kEB], eb[kEB];
+#pragma unroll
+      for (int u = 0; u < kEB; ++u) {
+        const int src = (u0 + u) & 31;
+        le[u] = __shfl_sync(kFull, my_e, src);
+        pl[u] = __shfl_sync(kFull, my_o, src) > v;
+        es[u] = __shfl_sync(kFull, my_s, src);
+        ea[u] = __shfl_sync(kFull, my_a, src);
+        eb[u] = __shfl_sync(kFull, my_b, src);
+      }
+      double x[kEB][NF];
+#pragma unroll
+      for (int u = 0; u < kEB; ++u)
+#pragma unroll
+        for (int k = 0; k < NF; ++k) {
+          const int f = f0 + 32 * k;
+          x[u][k] = (u0 + u < cnt && f < d) ? __ldcs(V + static_cast<int64_t>(le[u]) * d + f) : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < kEB; ++u) {
+        if (u0 + u >= cnt) continue;
+#pragma unroll
+        for (int k = 0; k < NF; ++k) {
+          const double val = x[u][k];
+          double uu, jd;
+          if (q == 2) {
+            uu = val - es[u] * val;
+            jd = ea[u] + (eb[u] != 0.0 ? eb[u] * val * val : 0.0);
+          } else {
+            uu = val - softd(val, es[u]);
+            jd = fabs(val) > es[u] ? 1.0 : 0.0;
+          }
+          ag[k] = pl[u] ? ag[k] + uu : ag[k] - uu;
+          ad[k] += sigma * (1.0 - jd);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NF; ++k) {
+    const int f = f0 + 32 * k;
+    if (f >= d) continue;
+    const double gv = (X[base + f] - A[base + f]) + sigma * ag[k];
+    G[base + f] = gv;
+    if (want_diag) diag[base + f] = ad[k];
+    s_g += gv * gv;
+  }
+  ITEMS_END
+  s_g = block_sum(s_g, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s_g;
+}
+
+// ---- SSNAL Hessian, pass 1: bc_l = beta_l <v_l, p_i - p_j> (warp per active edge) -----------
+__global__ void __launch_bounds__(256) k_edge_dot(const double* __restrict__ P, const double* __restrict__ V,
+                                                  const double* __restrict__ jbe, const int* __restrict__ ei,
+                                                  const int* __restrict__ ej, int64_t E, int d,
+                                                  double* __restrict__ bc, const int* active) {
+  if (active && !*active) return;
+  const int lane = threadIdx.x & 31;
+  for (int64_t l = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; l < E;
+       l += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const double be = jbe[l];
+    if (be == 0.0) {
+      if (lane == 0) bc[l] = 0.0;
+      continue;
+    }
+    const double* pa = P + static_cast<int64_t>(ei[l]) * d;
+    const double* pb = P + static_cast<int64_t>(ej[l]) * d;
+    const double* vl = V + l * d;
+    double c0 = 0.0, c1 = 0.0;
+    int f = lane;
+    for (; f + 32 < d; f += 64) {
+      const double v0 = __ldcs(vl + f), v1 = __ldcs(vl + f + 32);
+      const double a0 = pa[f], a1 = pa[f + 32], b0 = pb[f], b1 = pb[f + 32];
+      c0 += v0 * (a0 - b0);
+      c1 += v1 * (a1 - b1);
+    }
+    if (f < d) c0 += __ldcs(vl + f) * (pa[f] - pb[f]);
+    const double c = warp_sum(c0 + c1);
+    if (lane == 0) bc[l] = be * c;
+  }
+}
+
+// ---- SSNAL Hessian, pass 2: node gather (ssnal.cpp:56-64) -----------------------------------
+// Ap_v = p_v + sigma sum_l +-(w - (alpha w + bc v)),  w = p_i(l) - p_j(l).
+template <int NF>
+__global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, const double* __restrict__ V,
+                                                const double* __restrict__ jal, const double* __restrict__ bc,
+                                                const double* __restrict__ thr, const int* __restrict__ off,
+                                                const int* __restrict__ adj_e, const int* __restrict__ adj_o,
+                                                const int* __restrict__ order, int64_t n, int d, int nch,
+                                                double sigma, int q, double* __restrict__ Ap, double* part,
+                                                const int* active) {
+  if (active && !*active) return;
+  __shared__ double sh[32];
+  double s_a = 0.0, s_b = 0.0;
+  ITEMS_BEGIN(n, nch)
+  double pv[NF], acc[NF];
+#pragma unroll
+  for (int k = 0; k < NF; ++k) {
+    const int f = f0 + 32 * k;
+    pv[k] = f < d ? P[base + f] : 0.0;
+    acc[k] = 0.0;
+  }
+  for (int p = p0; p < p1; p += 32) {
+    const int cnt = min(32, p1 - p);
+    const int my_e = lane < cnt ? adj_e[p + lane] : 0;
+    const int my_o = lane < cnt ? adj_o[p + lane] : v;
+    const double my_a = lane < cnt ? (q == 2 ? jal[my_e] : thr[my_e]) : 0.0;
+    const double my_b = (lane < cnt && q == 2) ? bc[my_e] : 0.0;
+    for (int u0 = 0; u0 < cnt; u0 += kEB) {
+      int le[kEB], lo[kEB];
+      double ea[kEB], eb[kEB];
+#pragma unroll
+      for (int u = 0; u < kEB; ++u) {
+        const int src = (u0 + u) & 31;
+        le[u] = __shfl_sync(kFull, my_e, src);
+        lo[u] = __shfl_sync(kFull, my_o, src);
+        ea[u] = __shfl_sync(kFull, my_a, src);
+        eb[u] = __shfl_sync(kFull, my_b, src);
+      }
+      double po[kEB][NF], vv[kEB][NF];
+#pragma unroll
+      for (int u = 0; u < kEB; ++u) {
+        const bool ok = u0 + u < cnt;
+        const bool need_v = ok && (q != 2 || eb[u] != 0.0);
+#pragma unroll
+        for (int k = 0; k < NF; ++k) {
+          const int f = f0 + 32 * k;
+          po[u][k] = (ok && f < d) ? __ldg(P + static_cast<int64_t>(lo[u]) * d + f) : 0.0;
+          vv[u][k] = (need_v && f < d) ? __ldcs(V + static_cast<int64_t>(le[u]) * d + f) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kEB; ++u) {
+        if (u0 + u >= cnt) continue;
+        const bool plus = lo[u] > v;
+#pragma unroll
+        for (int k = 0; k < NF; ++k) {
+          const double w = plus ? pv[k] - po[u][k] : po[u][k] - pv[k];
+          double y;
+          if (q == 2)
+            y = (eb[u] != 0.0) ? w - (ea[u] * w + eb[u] * vv[u][k]) : w - ea[u] * w;
+          else
+            y = w - (fabs(vv[u][k]) > ea[u] ? w : 0.0);
+          acc[k] = plus ? acc[k] + y : acc[k] - y;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NF; ++k) {
+    const int f = f0 + 32 * k;
+    if (f >= d) continue;
+    const double o = pv[k] + sigma * acc[k];
+    Ap[base + f] = o;
+    s_a += pv[k] * o;
+    s_b += pv[k] * pv[k];
+  }
+  ITEMS_END
+  s_a = block_sum(s_a, sh);
+  s_b = block_sum(s_b, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s_a;
+    part[2 * blockIdx.x + 1] = s_b;
+  }
+}
+
+#define NF_DISPATCH(nf, KERNEL, ...)           \
+  switch (nf) {                                \
+    case 1: KERNEL<1> __VA_ARGS__; break;      \
+    case 2: KERNEL<2> __VA_ARGS__; break;      \
+    case 3: KERNEL<3> __VA_ARGS__; break;      \
+    case 4: KERNEL<4> __VA_ARGS__; break;      \
+    case 5: KERNEL<5> __VA_ARGS__; break;      \
+    default: KERNEL<6> __VA_ARGS__; break;     \
+  }
+
+}  // namespace
+
+NodeGeom node_geom(Ctx& c, int64_t n, int64_t d) {
+  const ChunkGeom cg = chunk_geom(d);
+  NodeGeom g;
+  g.gx = 256;
+  g.gy = cg.nch;  // chunks per node
+  g.nf = cg.nf;
+  const int64_t warps = n * cg.nch;
+  g.grid = std::max(1, std::min(cdiv(warps, 8), c.sm_count * 8));
+  return g;
+}
+
+#define GEOM                                 \
+  NodeGeom ng = node_geom(c, g.n, d);        \
+  const int di = static_cast<int>(d);        \
+  const int nch = ng.gy;
+
+void gather_bt(Ctx& c, const Graph& g, const double* Z, int64_t d, double* out) {
+  if (g.n == 0 || d == 0) return;
+  GEOM
+  NF_DISPATCH(ng.nf, k_g_bt, <<<ng.grid, 256, 0, c.s>>>(Z, nullptr, nullptr, 0.0, g.off.p, g.adj_e.p, g.adj_o.p,
+                                                         g.order.p, g.n, di, nch, 0, out));
+  CPB_LAUNCH_CHECK();
+}
+
+void gather_a_minus_bt(Ctx& c, const Graph& g, const double* A, const double* Zh, int64_t d, double* Xh) {
+  if (g.n == 0 || d == 0) return;
+  GEOM
+  NF_DISPATCH(ng.nf, k_g_bt, <<<ng.grid, 256, 0, c.s>>>(Zh, nullptr, A, 0.0, g.off.p, g.adj_e.p, g.adj_o.p,
+                                                         g.order.p, g.n, di, nch, 1, Xh));
+  CPB_LAUNCH_CHECK();
+}
+
+void gather_admm_rhs(Ctx& c, const Graph& g, const double* A, const double* U, const double* L, double rho,
+                     int64_t d, double* R) {
+  if (g.n == 0 || d == 0) return;
+  GEOM
+  NF_DISPATCH(ng.nf, k_g_bt, <<<ng.grid, 256, 0, c.s>>>(U, L, A, rho, g.off.p, g.adj_e.p, g.adj_o.p, g.order.p, g.n,
+                                                         di, nch, 2, R));
+  CPB_LAUNCH_CHECK();
+}
+
+int gather_lap(Ctx& c, const Graph& g, const double* y, double rho, int64_t d, double* out, double* part,
+               const int* active) {
+  GEOM
+  NF_DISPATCH(ng.nf, k_g_lap, <<<ng.grid, 256, 0, c.s>>>(y, rho, g.off.p, g.adj_o.p, g.order.p, g.n, di, nch, out,
+                                                          part, active));
+  CPB_LAUNCH_CHECK();
+  return ng.grid;
+}
+
+int gather_gap(Ctx& c, const Graph& g, const double* X, const double* A, const double* Z, int64_t d, double* part) {
+  GEOM
+  NF_DISPATCH(ng.nf, k_g_gap, <<<ng.grid, 256, 0, c.s>>>(X, A, Z, g.off.p, g.adj_e.p, g.adj_o.p, g.order.p, g.n, di,
+                                                          nch, part));
+  CPB_LAUNCH_CHECK();
+  return ng.grid;
+}
+
+int gather_grad_diag(Ctx& c, const Graph& g, const double* X, const double* A, const double* V, const double* ps,
+                     const double* jal, const double* jbe, const double* thr, int64_t d, double sigma, int q,
+                     bool want_diag, double* G, double* diag, double* part) {
+  GEOM
+  NF_DISPATCH(ng.nf, k_g_grad, <<<ng.grid, 256, 0, c.s>>>(X, A, V, ps, jal, jbe, thr, g.off.p, g.adj_e.p, g.adj_o.p,
+                                                           g.order.p, g.n, di, nch, sigma, q, want_diag ? 1 : 0, G,
+                                                           diag, part));
+  CPB_LAUNCH_CHECK();
+  return ng.grid;
+}
+
+int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,
+                  const double* thr, int64_t d, double sigma, int q, double* bc, double* Ap, double* part,
+                  const int* active) {
+  if (q == 2 && g.E > 0) {
+    const int grid = std::max(1, std::min(cdiv(g.E, 8), c.sm_count * 8));
+    k_edge_dot<<<grid, 256, 0, c.s>>>(P, V, jbe, g.ei.p, g.ej.p, g.E, static_cast<int>(d), bc, active);
+    CPB_LAUNCH_CHECK();
+  }
+  GEOM
+  NF_DISPATCH(ng.nf, k_g_hess, <<<ng.grid, 256, 0, c.s>>>(P, V, jal, bc, thr, g.off.p, g.adj_e.p, g.adj_o.p,
+                                                           g.order.p, g.n, di, nch, sigma, q, Ap, part, active));
+  CPB_LAUNCH_CHECK();
+  return ng.grid;
+}
+
+}  // namespace cpb

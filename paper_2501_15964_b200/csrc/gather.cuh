@@ -1,0 +1,47 @@
+// Node-CSR gather kernels: every operator of the form
+//     out_v = f( x_v, sum over incident edges l of v, ascending l, of +-g_l )
+// (Bᵀ, the SSNAL gradient/diagonal/Hessian, the gap's Z Bᵀ, AMA's A - Z Bᵀ,
+// ADMM's right-hand side and the Laplacian).  Accumulation runs in ascending
+// edge id per (node, feature), exactly the order of the reference's scatter
+// loop (graph.cpp:140-152), so sums are bitwise equal to it; there are no
+// atomics.
+//
+// Geometry: d <= 32 -> sub-warp groups of gx = 2^ceil(log2 d) lanes, 256/gx
+// nodes per block; d > 32 -> one node per block, gx = 32 * ceil(d / NF / 32)
+// threads each owning NF features (f = tx + gx k) in registers.  Incident
+// edges are consumed in batches of 8 with all 8 x NF row loads issued before
+// use, so a hub node's latency chain is deg/8 memory round trips, not deg x d/32.
+#pragma once
+
+#include "graph.cuh"
+
+namespace cpb {
+
+struct NodeGeom {
+  int gx, gy, nf, grid;
+};
+NodeGeom node_geom(Ctx& c, int64_t n, int64_t d);
+
+// Bᵀ z (graph.cpp:140-152)
+void gather_bt(Ctx& c, const Graph& g, const double* Z, int64_t d, double* out);
+// Xh = A - Zh Bᵀ (ama.cpp:62-63)
+void gather_a_minus_bt(Ctx& c, const Graph& g, const double* A, const double* Zh, int64_t d, double* Xh);
+// R = A + (rho U - L) Bᵀ (admm.cpp:61)
+void gather_admm_rhs(Ctx& c, const Graph& g, const double* A, const double* U, const double* L, double rho,
+                     int64_t d, double* R);
+// out = y + rho (L y); part[2b] = <y, out>, part[2b+1] = <y, y>  (I + rho L)
+int gather_lap(Ctx& c, const Graph& g, const double* y, double rho, int64_t d, double* out, double* part,
+               const int* active);
+// gap node terms at (X, Z): part[4b + k] = ||X-A||^2, ||ZBᵀ||^2, <ZBᵀ, A>, ||X - A + ZBᵀ||^2
+int gather_gap(Ctx& c, const Graph& g, const double* X, const double* A, const double* Z, int64_t d, double* part);
+// SSNAL gradient and Jacobi diagonal (ssnal.cpp:41-44, :68-82); part[b] = ||G||^2
+int gather_grad_diag(Ctx& c, const Graph& g, const double* X, const double* A, const double* V, const double* ps,
+                     const double* jal, const double* jbe, const double* thr, int64_t d, double sigma, int q,
+                     bool want_diag, double* G, double* diag, double* part);
+// SSNAL Hessian (ssnal.cpp:56-64), two passes: per-edge bc_l = beta_l <v_l, p_i - p_j>,
+// then the node gather; part[2b] = <p, Ap>, part[2b+1] = <p, p>.
+int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,
+                  const double* thr, int64_t d, double sigma, int q, double* bc, double* Ap, double* part,
+                  const int* active);
+
+}  // namespace cpb

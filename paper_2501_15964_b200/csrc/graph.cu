@@ -21,6 +21,7 @@
 #include <cmath>
 #include <random>
 
+#include "gather.cuh"
 #include "graph.cuh"
 
 namespace cpb {
@@ -333,22 +334,6 @@ __global__ void k_incidence(const double* __restrict__ X, const int* __restrict_
     for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = __dsub_rn(a[f], b[f]);
   }
 }
-__global__ void k_incidence_t(const double* __restrict__ Z, const int* __restrict__ off, const int* __restrict__ adj_e,
-                              const int* __restrict__ adj_o, int64_t n, int d, double* __restrict__ out) {
-  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.y) + threadIdx.y; v < n;
-       v += static_cast<int64_t>(gridDim.x) * blockDim.y) {
-    const int p0 = off[v], p1 = off[v + 1];
-    for (int f = threadIdx.x; f < d; f += blockDim.x) {
-      double acc = 0.0;
-      for (int p = p0; p < p1; ++p) {
-        const double z = Z[static_cast<int64_t>(adj_e[p]) * d + f];
-        acc = (adj_o[p] > v) ? __dadd_rn(acc, z) : __dsub_rn(acc, z);
-      }
-      out[v * d + f] = acc;
-    }
-  }
-}
-
 // ---- connected components ------------------------------------------------------------
 __global__ void k_cc_hook(const int* __restrict__ ei, const int* __restrict__ ej, const unsigned char* __restrict__ flag,
                           int E, int* L, int* changed) {
@@ -651,11 +636,7 @@ void incidence_apply_dev(Ctx& c, const Graph& g, const double* X, int64_t d, dou
 }
 
 void incidence_apply_t_dev(Ctx& c, const Graph& g, const double* Z, int64_t d, double* out) {
-  if (g.n == 0) return;
-  RowGeom rg = row_geom(d);
-  k_incidence_t<<<row_grid(c, g.n, rg), dim3(rg.dx, rg.dy), 0, c.s>>>(Z, g.off.p, g.adj_e.p, g.adj_o.p, g.n,
-                                                                      static_cast<int>(d), out);
-  CPB_LAUNCH_CHECK();
+  gather_bt(c, g, Z, d, out);
 }
 
 int64_t components_dev(Ctx& c, const Graph& g, const unsigned char* flag, int* labels) {
@@ -673,6 +654,7 @@ int64_t components_dev(Ctx& c, const Graph& g, const unsigned char* flag, int* l
     for (int iter = 0; iter < 4 * 64 + n; ++iter) {
       CPB_CUDA(cudaMemsetAsync(changed, 0, sizeof(int), c.s));
       k_cc_hook<<<ge, 256, 0, c.s>>>(g.ei.p, g.ej.p, flag, E, L, changed);
+      CPB_LAUNCH_CHECK();
       k_cc_jump<<<gn, 256, 0, c.s>>>(L, n);
       CPB_LAUNCH_CHECK();
       int h = 0;

@@ -12,6 +12,7 @@
 // reference's SSE2 build); the cited reference line is given per kernel.
 #include <cmath>
 
+#include "gather.cuh"
 #include "ops.cuh"
 
 namespace cpb {
@@ -239,126 +240,6 @@ __global__ void k_jac(const double* __restrict__ nv, const double* __restrict__ 
   }
   cnt = block_sum(cnt, sh);
   if (threadIdx.x == 0) part[blockIdx.x] = cnt;
-}
-
-// ---- SSNAL: gradient + Jacobi diagonal (ssnal.cpp:41-44, :68-82) ------------------------
-__global__ void k_grad_diag(const double* __restrict__ X, const double* __restrict__ A, const double* __restrict__ V,
-                            const double* __restrict__ ps, const double* __restrict__ jal,
-                            const double* __restrict__ jbe, const double* __restrict__ thr,
-                            const int* __restrict__ off, const int* __restrict__ adj_e, const int* __restrict__ adj_o,
-                            const int* __restrict__ order, int64_t n, int d, double sigma, int q, int want_diag,
-                            double* __restrict__ G, double* __restrict__ diag, double* part) {
-  __shared__ double sh[32];
-  const unsigned gm = group_mask();
-  double acc = 0.0;
-  ROWS_BEGIN(n) {
-    const int v = order[row_];
-    const int p0 = off[v], p1 = off[v + 1];
-    const int64_t base = static_cast<int64_t>(v) * d;
-    double gg = 0.0;
-    for (int f = threadIdx.x; f < d; f += blockDim.x) {
-      double ag = 0.0, ad = 1.0;
-      for (int p = p0; p < p1; ++p) {
-        const int l = adj_e[p];
-        const double val = V[static_cast<int64_t>(l) * d + f];
-        double u, jd;
-        if (q == Q_L2) {
-          u = val - ps[l] * val;
-          const double be = jbe[l];
-          jd = jal[l] + (be != 0.0 ? be * val * val : 0.0);
-        } else {
-          const double t = thr[l];
-          u = val - soft(val, t);
-          jd = fabs(val) > t ? 1.0 : 0.0;
-        }
-        ag = (adj_o[p] > v) ? ag + u : ag - u;
-        ad += sigma * (1.0 - jd);
-      }
-      const double g = (X[base + f] - A[base + f]) + sigma * ag;
-      G[base + f] = g;
-      if (want_diag) diag[base + f] = ad;
-      gg += g * g;
-    }
-    gg = group_sum(gg, gm);
-    if (threadIdx.x == 0) acc += gg;
-  }
-  acc = block_sum(acc, sh);
-  if (threadIdx.x == 0 && threadIdx.y == 0) part[blockIdx.x] = acc;
-}
-
-// ---- SSNAL: Hessian application (ssnal.cpp:56-64) -------------------------------------
-// Ap_v = p_v + sigma sum_{l ni v} +-(I - M_l)(p_i(l) - p_j(l)), gathered in
-// ascending edge id; the group's running sum lives in shared memory.
-__global__ void k_hess(const double* __restrict__ P, const double* __restrict__ V, const double* __restrict__ jal,
-                       const double* __restrict__ jbe, const double* __restrict__ thr, const int* __restrict__ ei,
-                       const int* __restrict__ ej, const int* __restrict__ off, const int* __restrict__ adj_e,
-                       const int* __restrict__ adj_o, const int* __restrict__ order, int64_t n, int d, double sigma,
-                       int q, double* __restrict__ Ap, double* part, const int* active) {
-  if (active && !*active) return;
-  extern __shared__ double dsm[];
-  __shared__ double sh[32];
-  double* acc = dsm + static_cast<int64_t>(threadIdx.y) * d;
-  const unsigned gm = group_mask();
-  double s_pap = 0.0, s_pp = 0.0;
-  ROWS_BEGIN(n) {
-    const int v = order[row_];
-    const int p0 = off[v], p1 = off[v + 1];
-    for (int f = threadIdx.x; f < d; f += blockDim.x) acc[f] = 0.0;
-    for (int p = p0; p < p1; ++p) {
-      const int l = adj_e[p];
-      const bool plus = adj_o[p] > v;
-      const double* pa = P + static_cast<int64_t>(ei[l]) * d;
-      const double* pb = P + static_cast<int64_t>(ej[l]) * d;
-      const double* vl = V + static_cast<int64_t>(l) * d;
-      if (q == Q_L2) {
-        const double al = jal[l], be = jbe[l];
-        if (be != 0.0) {
-          double c = 0.0;
-          for (int f = threadIdx.x; f < d; f += blockDim.x) c += vl[f] * (pa[f] - pb[f]);
-          const double bc = be * group_sum(c, gm);
-          for (int f = threadIdx.x; f < d; f += blockDim.x) {
-            const double w = pa[f] - pb[f];
-            const double y = w - (al * w + bc * vl[f]);
-            acc[f] = plus ? acc[f] + y : acc[f] - y;
-          }
-        } else if (al != 1.0) {
-          for (int f = threadIdx.x; f < d; f += blockDim.x) {
-            const double w = pa[f] - pb[f];
-            const double y = w - al * w;
-            acc[f] = plus ? acc[f] + y : acc[f] - y;
-          }
-        }
-      } else {
-        const double t = thr[l];
-        for (int f = threadIdx.x; f < d; f += blockDim.x) {
-          const double w = pa[f] - pb[f];
-          const double y = w - (fabs(vl[f]) > t ? w : 0.0);
-          acc[f] = plus ? acc[f] + y : acc[f] - y;
-        }
-      }
-    }
-    const int64_t base = static_cast<int64_t>(v) * d;
-    double a = 0.0, b = 0.0;
-    for (int f = threadIdx.x; f < d; f += blockDim.x) {
-      const double pv = P[base + f];
-      const double o = pv + sigma * acc[f];
-      Ap[base + f] = o;
-      a += pv * o;
-      b += pv * pv;
-    }
-    a = group_sum(a, gm);
-    b = group_sum(b, gm);
-    if (threadIdx.x == 0) {
-      s_pap += a;
-      s_pp += b;
-    }
-  }
-  s_pap = block_sum(s_pap, sh);
-  s_pp = block_sum(s_pp, sh);
-  if (threadIdx.x == 0 && threadIdx.y == 0) {
-    part[2 * blockIdx.x] = s_pap;
-    part[2 * blockIdx.x + 1] = s_pp;
-  }
 }
 
 // ---- PCG (linalg.cpp:143-192) ---------------------------------------------------------
@@ -647,42 +528,6 @@ __global__ void k_gap_edge(const double* __restrict__ X, const double* __restric
   if (threadIdx.x == 0 && threadIdx.y == 0) part[5 * blockIdx.x + 4] = m;
 }
 
-// Node terms: [0] ||X - A||^2, [1] ||Z B^T||^2, [2] <Z B^T, A>, [3] ||X - A + Z B^T||^2
-__global__ void k_gap_node(const double* __restrict__ X, const double* __restrict__ A, const double* __restrict__ Z,
-                           const int* __restrict__ off, const int* __restrict__ adj_e, const int* __restrict__ adj_o,
-                           const int* __restrict__ order, int64_t n, int d, double* part) {
-  __shared__ double sh[32];
-  const unsigned gm = group_mask();
-  double s[4] = {0, 0, 0, 0};
-  ROWS_BEGIN(n) {
-    const int v = order[row_];
-    const int p0 = off[v], p1 = off[v + 1];
-    const int64_t base = static_cast<int64_t>(v) * d;
-    double t[4] = {0, 0, 0, 0};
-    for (int f = threadIdx.x; f < d; f += blockDim.x) {
-      double acc = 0.0;
-      for (int p = p0; p < p1; ++p) {
-        const double z = Z[static_cast<int64_t>(adj_e[p]) * d + f];
-        acc = (adj_o[p] > v) ? acc + z : acc - z;
-      }
-      const double xa = X[base + f] - A[base + f];
-      const double st = xa + acc;
-      t[0] += xa * xa;
-      t[1] += acc * acc;
-      t[2] += acc * A[base + f];
-      t[3] += st * st;
-    }
-    for (int k = 0; k < 4; ++k) {
-      const double r = group_sum(t[k], gm);
-      if (threadIdx.x == 0) s[k] += r;
-    }
-  }
-  for (int k = 0; k < 4; ++k) {
-    const double r = block_sum(s[k], sh);
-    if (threadIdx.x == 0 && threadIdx.y == 0) part[4 * blockIdx.x + k] = r;
-  }
-}
-
 // ---- SSNAL multiplier (ssnal.cpp:183-195, :205) fused with the edge gap terms -----------
 // part per block: [0..3] gap edge terms at the new Z, [4] ||XB - PV||^2, [5] ||XB||^2 (same as [2]),
 // [6] max |Z + sigma XB| (pre-projection), [7] max |Zenv - Zsum|, [8] dual excess
@@ -744,23 +589,6 @@ __global__ void k_mult(const double* __restrict__ X, double* __restrict__ Z, con
 }
 
 // ---- fast AMA (ama.cpp:57-72) -----------------------------------------------------------
-__global__ void k_ama_node(const double* __restrict__ A, const double* __restrict__ Zh, const int* __restrict__ off,
-                           const int* __restrict__ adj_e, const int* __restrict__ adj_o, const int* __restrict__ order,
-                           int64_t n, int d, double* __restrict__ Xh) {
-  ROWS_BEGIN(n) {
-    const int v = order[row_];
-    const int p0 = off[v], p1 = off[v + 1];
-    const int64_t base = static_cast<int64_t>(v) * d;
-    for (int f = threadIdx.x; f < d; f += blockDim.x) {
-      double acc = 0.0;
-      for (int p = p0; p < p1; ++p) {
-        const double z = Zh[static_cast<int64_t>(adj_e[p]) * d + f];
-        acc = (adj_o[p] > v) ? acc + z : acc - z;
-      }
-      Xh[base + f] = A[base + f] - acc;
-    }
-  }
-}
 __global__ void k_ama_edge(const double* __restrict__ Xh, double* __restrict__ Zh, double* __restrict__ Zp,
                            const double* __restrict__ rad, const int* __restrict__ ei, const int* __restrict__ ej,
                            int64_t E, int d, double step, double mom, int q) {
@@ -908,42 +736,22 @@ double grad_diag(const Prob& P, const double* X, const double* V, const double* 
                  const double* jbe, const double* thr, double sigma, double* G, double* diag, bool want_diag) {
   Ctx& c = *P.c;
   const int64_t d = P.d(), n = P.n(), E = P.E();
-  GroupGeom gg = group_geom(c, n, d);
-  double* part = part_buf(c, "grad.part", gg.grid);
+  double* part = part_buf(c, "grad.part", static_cast<size_t>(c.sm_count) * 16);
+  int nb;
   {
     Ctx::Timer tm(&c, "grad_diag", (2.0 * E * d + (want_diag ? 4.0 : 3.0) * n * d) * 8.0);
-    k_grad_diag<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(X, P.A->A.p, V, ps, jal, jbe, thr, P.g->off.p, P.g->adj_e.p,
-                                                         P.g->adj_o.p, P.g->order.p, n, static_cast<int>(d), sigma,
-                                                         P.q, want_diag ? 1 : 0, G, diag, part);
-    CPB_LAUNCH_CHECK();
+    nb = gather_grad_diag(c, *P.g, X, P.A->A.p, V, ps, jal, jbe, thr, d, sigma, P.q, want_diag, G, diag, part);
   }
-  reduce_sum(c, part, gg.grid, c.dscal);
+  reduce_sum(c, part, nb, c.dscal);
   return fetch1(c);
 }
 
 int hess_apply(const Prob& P, const double* p, const double* V, const double* jal, const double* jbe,
                const double* thr, double sigma, double* Ap, double* part, const void* st) {
   Ctx& c = *P.c;
-  const int64_t d = P.d(), n = P.n();
-  GroupGeom gg = group_geom(c, n, d);
-  size_t smem = static_cast<size_t>(gg.gy) * d * sizeof(double);
-  while (smem > 200 * 1024 && gg.gy > 1) {
-    gg.gy >>= 1;
-    smem = static_cast<size_t>(gg.gy) * d * sizeof(double);
-  }
-  if (smem > 200 * 1024) invalid("hessian apply: feature dimension too large");
-  gg.grid = std::max(1, std::min(cdiv(n, gg.gy), c.sm_count * 8));
-  static bool attr_set = false;
-  if (!attr_set) {
-    CPB_CUDA(cudaFuncSetAttribute(k_hess, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_set = true;
-  }
-  k_hess<<<gg.grid, dim3(gg.gx, gg.gy), smem, c.s>>>(p, V, jal, jbe, thr, P.g->ei.p, P.g->ej.p, P.g->off.p,
-                                                     P.g->adj_e.p, P.g->adj_o.p, P.g->order.p, n, static_cast<int>(d),
-                                                     sigma, P.q, Ap, part,
-                                                     st ? &static_cast<const CgState*>(st)->active : nullptr);
-  CPB_LAUNCH_CHECK();
-  return gg.grid;
+  double* bc = c.buf<double>("hess.bc", P.E() + 1);
+  return hess_two_pass(c, *P.g, p, V, jal, jbe, thr, P.d(), sigma, P.q, bc, Ap, part,
+                       st ? &static_cast<const CgState*>(st)->active : nullptr);
 }
 
 const int* cg_active_ptr(const void* st) { return st ? &static_cast<const CgState*>(st)->active : nullptr; }
@@ -958,7 +766,7 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
   const int64_t chunk = (n + nb - 1) / nb;
   double* part_rz = part_buf(c, "pcg.rz", nb);
   double* part_rr = part_buf(c, "pcg.rr", static_cast<size_t>(nb) * d);
-  double* part_h = part_buf(c, "pcg.h", 2 * static_cast<size_t>(c.sm_count) * 8 + 2);
+  double* part_h = part_buf(c, "pcg.h", 2 * static_cast<size_t>(c.sm_count) * 16 + 2);
   double* bn = part_buf(c, "pcg.bn", d);
   CgState* st = reinterpret_cast<CgState*>(c.dscal + 64);
   const int nf = d <= kFeatThreads * 4 ? 4 : (d <= kFeatThreads * 16 ? 16 : 64);
@@ -996,15 +804,21 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
         Ctx::Timer tm(&c, op_name, op_bytes);
         hb = op(w.p, w.Ap, part_h, st);
       }
-      k_pcg_s1<<<1, 256, 0, c.s>>>(st, part_h, hb);
-      CPB_LAUNCH_CHECK();
+      {
+        Ctx::Timer tm(&c, "pcg_s1", 0.0);
+        k_pcg_s1<<<1, 256, 0, c.s>>>(st, part_h, hb);
+        CPB_LAUNCH_CHECK();
+      }
       {
         Ctx::Timer tm(&c, "pcg_update_b", 4.0 * m * 8.0);
         launch_b();
         CPB_LAUNCH_CHECK();
       }
-      k_pcg_s2<<<1, 1024, 0, c.s>>>(st, part_rz, part_rr, nb, di, bn);
-      CPB_LAUNCH_CHECK();
+      {
+        Ctx::Timer tm(&c, "pcg_s2", 0.0);
+        k_pcg_s2<<<1, 1024, 0, c.s>>>(st, part_rz, part_rr, nb, di, bn);
+        CPB_LAUNCH_CHECK();
+      }
       {
         Ctx::Timer tm(&c, "pcg_update_c", 6.0 * m * 8.0);
         k_pcg_c<<<fg, 256, 0, c.s>>>(st, w.r, w.diag, m, w.x, w.p);
@@ -1019,6 +833,8 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
     const int wasted = batch - static_cast<int>(h.it - it_before);
     if (wasted > 0) {
       c.discard_pending(op_name, wasted);
+      c.discard_pending("pcg_s1", wasted);
+      c.discard_pending("pcg_s2", wasted);
       c.discard_pending("pcg_update_b", wasted);
       c.discard_pending("pcg_update_c", wasted);
     }
@@ -1065,15 +881,13 @@ std::vector<double> host_cols(Ctx& c, const double* part, int rows, int cols, co
 GapOut eval_gap(const Prob& P, const double* X, const double* Z) {
   Ctx& c = *P.c;
   const int64_t d = P.d(), n = P.n(), E = P.E();
-  GroupGeom gn = group_geom(c, n, d);
-  double* pn = part_buf(c, "gap.pn", 4 * static_cast<size_t>(gn.grid));
+  double* pn = part_buf(c, "gap.pn", 4 * static_cast<size_t>(c.sm_count) * 16);
+  int nbn;
   {
-    Ctx::Timer tm(&c, "gap_node", (2.0 * E * d + 2.0 * n * d) * 8.0);
-    k_gap_node<<<gn.grid, dim3(gn.gx, gn.gy), 0, c.s>>>(X, P.A->A.p, Z, P.g->off.p, P.g->adj_e.p, P.g->adj_o.p,
-                                                        P.g->order.p, n, static_cast<int>(d), pn);
-    CPB_LAUNCH_CHECK();
+    Ctx::Timer tm(&c, "gap_node", (2.0 * E * d + 3.0 * n * d) * 8.0);
+    nbn = gather_gap(c, *P.g, X, P.A->A.p, Z, d, pn);
   }
-  std::vector<double> h = host_cols(c, pn, gn.grid, 4);
+  std::vector<double> h = host_cols(c, pn, nbn, 4);
   std::vector<double> e(5, 0.0);
   e[4] = -1.0;
   if (E > 0) {
@@ -1134,12 +948,10 @@ double dual_objective_dev(const Prob& P, const double* Z) {
 double kkt_residual_dev(const Prob& P, const double* X, const double* Z) {
   Ctx& c = *P.c;
   const int64_t d = P.d(), n = P.n(), E = P.E();
-  GroupGeom gn = group_geom(c, n, d);
-  double* pn = part_buf(c, "kkt.pn", 4 * static_cast<size_t>(gn.grid));
-  k_gap_node<<<gn.grid, dim3(gn.gx, gn.gy), 0, c.s>>>(X, P.A->A.p, Z, P.g->off.p, P.g->adj_e.p, P.g->adj_o.p,
-                                                      P.g->order.p, n, static_cast<int>(d), pn);
-  CPB_LAUNCH_CHECK();
-  std::vector<double> h = host_cols(c, pn, gn.grid, 4);
+  (void)n;
+  double* pn = part_buf(c, "kkt.pn", 4 * static_cast<size_t>(c.sm_count) * 16);
+  const int nbn = gather_gap(c, *P.g, X, P.A->A.p, Z, d, pn);
+  std::vector<double> h = host_cols(c, pn, nbn, 4);
   const double stat = std::sqrt(h[3]) / (1.0 + data_fro_norm(c, *P.A));
   if (E == 0 || P.gamma == 0.0) return stat;
   GroupGeom ge = group_geom(c, E, d);
@@ -1169,15 +981,13 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
   if (err > 1e-10 * scale) runtime("ssnal: multiplier self-check failed");
   if (excess > 0.0) invalid("dual_objective: Z violates the dual-ball constraint");
   // node terms at (X, new Z)
-  GroupGeom gn = group_geom(c, n, d);
-  double* pn = part_buf(c, "mult.pn", 4 * static_cast<size_t>(gn.grid));
+  double* pn = part_buf(c, "mult.pn", 4 * static_cast<size_t>(c.sm_count) * 16);
+  int nbn;
   {
-    Ctx::Timer tm(&c, "gap_node", (2.0 * E * d + 2.0 * n * d) * 8.0);
-    k_gap_node<<<gn.grid, dim3(gn.gx, gn.gy), 0, c.s>>>(X, P.A->A.p, Z, P.g->off.p, P.g->adj_e.p, P.g->adj_o.p,
-                                                        P.g->order.p, n, static_cast<int>(d), pn);
-    CPB_LAUNCH_CHECK();
+    Ctx::Timer tm(&c, "gap_node", (2.0 * E * d + 3.0 * n * d) * 8.0);
+    nbn = gather_gap(c, *P.g, X, P.A->A.p, Z, d, pn);
   }
-  std::vector<double> h = host_cols(c, pn, gn.grid, 4);
+  std::vector<double> h = host_cols(c, pn, nbn, 4);
   const double normA = data_fro_norm(c, *P.A);
   MultOut o;
   GapOut& g = o.gap;
@@ -1194,12 +1004,7 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
 }
 
 void ama_primal(const Prob& P, const double* Zh, double* Xh) {
-  Ctx& c = *P.c;
-  const int64_t d = P.d(), n = P.n();
-  GroupGeom gn = group_geom(c, n, d);
-  k_ama_node<<<gn.grid, dim3(gn.gx, gn.gy), 0, c.s>>>(P.A->A.p, Zh, P.g->off.p, P.g->adj_e.p, P.g->adj_o.p,
-                                                      P.g->order.p, n, static_cast<int>(d), Xh);
-  CPB_LAUNCH_CHECK();
+  gather_a_minus_bt(*P.c, *P.g, P.A->A.p, Zh, P.d(), Xh);
 }
 void ama_dual_step(const Prob& P, const double* Xh, double* Zh, double* Zprev, double step, double mom) {
   Ctx& c = *P.c;

@@ -360,6 +360,7 @@ int64_t extract_clusters_dev(Ctx& c, const Graph& g, const double* X, int64_t d,
     CPB_CUDA(cudaMemsetAsync(cnt, 0, (K + 1) * sizeof(int), c.s));
     const int gn = std::max(1, std::min(cdiv(n, 256), c.sm_count * 4));
     k_count<<<gn, 256, 0, c.s>>>(labels, static_cast<int>(n), cnt);
+    CPB_LAUNCH_CHECK();
     k_iota2<<<gn, 256, 0, c.s>>>(node, static_cast<int>(n));
     CPB_LAUNCH_CHECK();
     size_t bytes = 0;
