@@ -158,7 +158,7 @@ def barrier(dist):
 
 
 # ---- CPU side (oracle; cpu_baseline leg and --impl reference only) -------------------
-def cpu_estimate(cfg, A, counts, knn_rows=200, reps=1):
+def cpu_estimate(cfg, A, counts, knn_rows=400, reps=2):
     """Extrapolated single-core reference path seconds from a bounded sample."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as orc
@@ -179,7 +179,8 @@ def cpu_estimate(cfg, A, counts, knn_rows=200, reps=1):
     # Graph from the GPU-identical edge set is not needed for unit costs; build a
     # cheap same-size graph: the exact kNN graph costs O(n^2 d) on one core, so
     # use the edge list recorded with the counts.
-    ed = np.load(counts["edges_file"]) if counts.get("edges_file") and os.path.exists(counts["edges_file"]) else None
+    ef = os.path.join(ROOT, counts.get("edges_file", "")) if counts.get("edges_file") else None
+    ed = np.load(ef) if ef and os.path.exists(ef) else None
     if ed is not None:
         g = orc.Graph.from_arrays(n, ed["i"], ed["j"], ed["w"])
     else:  # same degree structure: chain each sample to its k successors inside its cluster
@@ -285,12 +286,13 @@ def run_ours(args, cfg):
     # ---- e2e through the public API with host buffers ------------------------------
     e2e_times = []
     T = cfg["T"]
-    for s in range(max(1, min(args.steps, 2))):
+    for s in range(1 + max(1, min(args.steps, 2))):  # first call untimed: fills the pinned-buffer pool
         t0 = time.perf_counter()
         dA = cp.DataMatrix(A, ctx=ctx)
         g2 = cp.compute_knn_weights(dA, cfg["k"], cfg["phi"])
         res2 = cp.run_path(dA, g2, cfg["q"], sched, cpcfg, keep_solutions=True)
-        e2e_times.append(time.perf_counter() - t0)
+        if s > 0:
+            e2e_times.append(time.perf_counter() - t0)
         del res2
     e2e = allmax(dist, float(np.mean(e2e_times)))
     h2d = cfg["n"] * cfg["d"] * 8
@@ -314,6 +316,10 @@ def run_ours(args, cfg):
                             for gm, s, a in zip(sched.values, res.stats, res.assignments)]}
     if rank == 0 and args.write_counts:
         os.makedirs(os.path.dirname(COUNTS_FILE), exist_ok=True)
+        gi, gj, gw, _ = g.arrays()
+        rel = os.path.join("profiles", f"graph_{args.config}.npz")
+        np.savez_compressed(os.path.join(ROOT, rel), i=gi.astype(np.int32), j=gj.astype(np.int32), w=gw)
+        counts["edges_file"] = rel
         with open(COUNTS_FILE.format(args.config), "w") as f:
             json.dump(counts, f, indent=1)
     cpu = None

@@ -105,6 +105,10 @@ int cp_timer_start(cp_ctx* ctx);
 int cp_timer_stop(cp_ctx* ctx, double* ms);
 /* Evict L2 by writing a buffer larger than it (benchmark hygiene). */
 int cp_flush_l2(cp_ctx* ctx);
+/* Page-locked host buffers: run_path outputs placed in them are copied
+   asynchronously, overlapped with the next gamma's solve. */
+int cp_host_alloc(uint64_t bytes, void** out);
+void cp_host_free(void* p);
 
 /* ---- synthetic inputs (io.cpp:142-165; host code, libstdc++ <random>) -------- */
 /* generate_gaussian_mixture(centers, spread, per_center, seed): centers d x m, out d x (m*per_center). */

@@ -60,6 +60,8 @@ _SIGS = [
     ("cp_timer_start", C.c_int, [VP]),
     ("cp_timer_stop", C.c_int, [VP, D]),
     ("cp_flush_l2", C.c_int, [VP]),
+    ("cp_host_alloc", C.c_int, [C.c_uint64, C.POINTER(VP)]),
+    ("cp_host_free", None, [VP]),
     ("cp_gaussian_mixture", C.c_int, [D, C.c_int64, C.c_int64, C.c_double, C.c_int64, C.c_uint64, D]),
     ("cp_normals", C.c_int, [C.c_uint64, C.c_int64, D]),
     ("cp_data_create", C.c_int, [VP, D, C.c_int64, C.c_int64, C.POINTER(VP)]),

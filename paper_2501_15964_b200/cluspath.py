@@ -117,6 +117,37 @@ def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+class _PinnedBlock:
+    """A page-locked host block (cp_host_alloc) exposed to numpy; returned to
+    the pool when the last array viewing it is released."""
+
+    _pool = {}
+
+    def __init__(self, shape, dtype=np.float64):
+        dtype = np.dtype(dtype)
+        self.nbytes = int(np.prod(shape)) * dtype.itemsize
+        free = _PinnedBlock._pool.get(self.nbytes)
+        if free:
+            self.ptr = free.pop()
+        else:
+            h = C.c_void_p()
+            L.check(L.load().cp_host_alloc(self.nbytes, C.byref(h)))
+            self.ptr = h.value
+        self.__array_interface__ = {"shape": tuple(int(s) for s in shape), "typestr": dtype.str,
+                                    "data": (self.ptr, False), "version": 3}
+
+    def __del__(self):
+        try:
+            _PinnedBlock._pool.setdefault(self.nbytes, []).append(self.ptr)
+        except Exception:
+            pass
+
+
+def pinned_empty(shape, dtype=np.float64):
+    """numpy array in page-locked host memory (fast, asynchronous D2H target)."""
+    return np.asarray(_PinnedBlock(shape, dtype))
+
+
 def _dp(a):
     return a.ctypes.data_as(L.D) if a is not None else None
 
@@ -607,8 +638,8 @@ def run_path(data: DataMatrix, graph: WeightedGraph, norm, schedule: GammaSchedu
     if T == 0:
         raise ValueError("run_path: empty schedule")
     n, d, E = data.n, data.d, graph.edge_count()
-    X = np.empty((T, n, d)) if keep_solutions else None
-    Z = np.empty((T, E, d)) if keep_solutions else None
+    X = pinned_empty((T, n, d)) if keep_solutions else None
+    Z = pinned_empty((T, E, d)) if keep_solutions else None
     lab = np.empty((T, n), np.int64)
     K = np.empty(T, np.int64)
     terms = (L.TerminationC * T)()

@@ -176,6 +176,17 @@ int cp_flush_l2(cp_ctx* ctx) {
   });
 }
 
+int cp_host_alloc(uint64_t bytes, void** out) {
+  return guard(nullptr, [&] {
+    need(out, "out");
+    *out = nullptr;
+    CPB_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable));
+  });
+}
+void cp_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int cp_gaussian_mixture(const double* centers, int64_t d, int64_t m, double spread, int64_t per_center, uint64_t seed,
                         double* out) {
   return guard(nullptr, [&] {

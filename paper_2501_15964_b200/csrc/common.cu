@@ -33,6 +33,10 @@ Ctx::~Ctx() {
     cudaEventDestroy(p.b);
   }
   for (auto e : event_pool) cudaEventDestroy(e);
+  if (cs) {
+    cudaStreamSynchronize(cs);
+    cudaStreamDestroy(cs);
+  }
   if (timer_a) cudaEventDestroy(timer_a);
   if (timer_b) cudaEventDestroy(timer_b);
   ws.clear();

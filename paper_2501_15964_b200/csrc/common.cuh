@@ -113,6 +113,11 @@ struct Ctx {
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
   cudaEvent_t timer_a = nullptr, timer_b = nullptr;  // cp_timer_start / cp_timer_stop
+  cudaStream_t cs = nullptr;                          // device->host copy stream (lazily created)
+  cudaStream_t copy_stream() {
+    if (!cs) CPB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    return cs;
+  }
 
   explicit Ctx(int dev);
   ~Ctx();

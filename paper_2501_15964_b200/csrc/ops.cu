@@ -242,223 +242,6 @@ __global__ void k_jac(const double* __restrict__ nv, const double* __restrict__ 
   if (threadIdx.x == 0) part[blockIdx.x] = cnt;
 }
 
-// ---- PCG (linalg.cpp:143-192) ---------------------------------------------------------
-// Device-resident loop control.  Each iteration is five launches
-//   hess -> s1 -> b -> s2 -> c
-// that all no-op once `active` drops, so the host enqueues iterations in
-// batches and polls the state only between batches.
-struct CgState {
-  double rz, pAp, alpha, beta, relres, tol, pp, rz_next;
-  long long it, maxit;
-  int active, phaseB, phaseC, upd_p, status, pad;
-};
-
-constexpr int kFeatThreads = 256;
-// Feature-major mapping: D1 threads per node row, R rows per pass.
-struct FM {
-  int D1, R, slot, f0;
-  __device__ FM(int d) {
-    D1 = d < kFeatThreads ? d : kFeatThreads;
-    R = kFeatThreads / D1;
-    slot = threadIdx.x / D1;
-    f0 = threadIdx.x % D1;
-  }
-};
-
-// Combine per-thread per-feature partials across slots and store part[b*d + f].
-template <int NF>
-__device__ void fm_store_cols(const FM& fm, const double (&acc)[NF], int d, double* sbuf, double* out) {
-  if (fm.R == 1) {
-#pragma unroll
-    for (int k = 0; k < NF; ++k) {
-      const int f = fm.f0 + fm.D1 * k;
-      if (f < d) out[f] = acc[k];
-    }
-    return;
-  }
-  // d < 256: NF == 1 used
-  sbuf[threadIdx.x] = (fm.slot < fm.R) ? acc[0] : 0.0;
-  __syncthreads();
-  if (fm.slot == 0) {
-    double s = 0.0;
-    for (int r = 0; r < fm.R; ++r) s += sbuf[r * fm.D1 + fm.f0];
-    out[fm.f0] = s;
-  }
-  __syncthreads();
-}
-
-template <int NF>
-__global__ void __launch_bounds__(kFeatThreads) k_pcg_init(const double* __restrict__ rhs, const double* __restrict__ Mx, const double* __restrict__ diag,
-                                                          int64_t n, int d, int64_t chunk, double* __restrict__ x,
-                                                          double* __restrict__ r, double* __restrict__ p,
-                                                          double* part_rz, double* part_bb) {
-  __shared__ double sh[32];
-  __shared__ double sbuf[kFeatThreads];
-  FM fm(d);
-  double acc[NF];
-#pragma unroll
-  for (int k = 0; k < NF; ++k) acc[k] = 0.0;
-  double rz = 0.0;
-  const int64_t v0 = blockIdx.x * chunk, v1 = min(n, v0 + chunk);
-  if (fm.slot < fm.R) {
-    for (int64_t v = v0 + fm.slot; v < v1; v += fm.R) {
-#pragma unroll
-      for (int k = 0; k < NF; ++k) {
-        const int f = fm.f0 + fm.D1 * k;
-        if (f < d) {
-          const int64_t i = v * d + f;
-          const double b = rhs[i];
-          const double rv = Mx ? b - Mx[i] : b;
-          if (!Mx) x[i] = 0.0;
-          r[i] = rv;
-          const double z = rv / diag[i];
-          p[i] = z;
-          rz += rv * z;
-          acc[k] += b * b;
-        }
-      }
-    }
-  }
-  rz = block_sum(rz, sh);
-  if (threadIdx.x == 0) part_rz[blockIdx.x] = rz;
-  fm_store_cols<NF>(fm, acc, d, sbuf, part_bb + static_cast<int64_t>(blockIdx.x) * d);
-}
-
-template <int NF>
-__global__ void __launch_bounds__(kFeatThreads) k_pcg_b(const CgState* __restrict__ st, const double* __restrict__ Ap,
-                                                       const double* __restrict__ diag, int64_t n, int d, int64_t chunk,
-                                                       double* __restrict__ r, double* part_rz, double* part_rr) {
-  if (!st->phaseB) return;
-  __shared__ double sh[32];
-  __shared__ double sbuf[kFeatThreads];
-  const double alpha = st->alpha;
-  FM fm(d);
-  double acc[NF];
-#pragma unroll
-  for (int k = 0; k < NF; ++k) acc[k] = 0.0;
-  double rz = 0.0;
-  const int64_t v0 = blockIdx.x * chunk, v1 = min(n, v0 + chunk);
-  if (fm.slot < fm.R) {
-    for (int64_t v = v0 + fm.slot; v < v1; v += fm.R) {
-#pragma unroll
-      for (int k = 0; k < NF; ++k) {
-        const int f = fm.f0 + fm.D1 * k;
-        if (f < d) {
-          const int64_t i = v * d + f;
-          const double rv = r[i] - alpha * Ap[i];
-          r[i] = rv;
-          rz += rv * (rv / diag[i]);
-          acc[k] += rv * rv;
-        }
-      }
-    }
-  }
-  rz = block_sum(rz, sh);
-  if (threadIdx.x == 0) part_rz[blockIdx.x] = rz;
-  fm_store_cols<NF>(fm, acc, d, sbuf, part_rr + static_cast<int64_t>(blockIdx.x) * d);
-}
-
-// x += alpha p; p = r/diag + beta p (when continuing)
-__global__ void k_pcg_c(const CgState* __restrict__ st, const double* __restrict__ r, const double* __restrict__ diag,
-                        int64_t m, double* __restrict__ x, double* __restrict__ p) {
-  if (!st->phaseC) return;
-  const double alpha = st->alpha, beta = st->beta;
-  const bool upd = st->upd_p != 0;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const double pv = p[i];
-    x[i] = x[i] + alpha * pv;
-    if (upd) p[i] = r[i] / diag[i] + beta * pv;
-  }
-}
-
-// column sums of nb x d partials, then worst relative feature-row residual
-__device__ double pcg_relres(const double* part_rr, int nb, int d, const double* bn, double* sh) {
-  double worst = 0.0;
-  for (int f = threadIdx.x; f < d; f += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += part_rr[static_cast<int64_t>(b) * d + f];
-    const double nb_ = bn[f];
-    worst = fmax(worst, sqrt(s) / (nb_ > 0.0 ? nb_ : 1.0));
-  }
-  return block_max(worst, sh);
-}
-__device__ double sum_part(const double* part, int nb, int stride, double* sh) {
-  double s = 0.0;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) s += part[static_cast<int64_t>(b) * stride];
-  return block_sum(s, sh);
-}
-
-__global__ void k_pcg_s0(CgState* st, const double* part_rz, const double* part_bb, int nb, int d, double tol,
-                         long long maxit, double* bn, int warm) {
-  __shared__ double sh[32];
-  for (int f = threadIdx.x; f < d; f += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += part_bb[static_cast<int64_t>(b) * d + f];
-    bn[f] = sqrt(s);
-  }
-  __syncthreads();
-  const double rel = pcg_relres(part_bb, nb, d, bn, sh);
-  const double rz = sum_part(part_rz, nb, 1, sh);
-  if (threadIdx.x == 0) {
-    st->rz = rz;
-    st->relres = rel;
-    st->tol = tol;
-    st->it = 0;
-    st->maxit = maxit;
-    st->active = (!warm && rel <= tol) ? 0 : 1;
-    st->phaseB = st->phaseC = st->upd_p = 0;
-    st->status = 0;
-  }
-}
-__global__ void k_pcg_s1(CgState* st, const double* part, int nb) {
-  __shared__ double sh[32];
-  if (threadIdx.x == 0) st->phaseC = 0;
-  if (!st->active) {
-    if (threadIdx.x == 0) st->phaseB = 0;
-    return;
-  }
-  const double pAp = sum_part(part, nb, 2, sh);
-  const double pp = sum_part(part + 1, nb, 2, sh);
-  if (threadIdx.x == 0) {
-    st->it += 1;
-    st->pAp = pAp;
-    st->pp = pp;
-    if (pAp <= 0.0) {
-      st->active = 0;
-      st->phaseB = 0;
-      if (pp != 0.0) st->status = 1;  // not positive definite
-    } else {
-      st->alpha = st->rz / pAp;
-      st->phaseB = 1;
-    }
-  }
-}
-__global__ void k_pcg_s2(CgState* st, const double* part_rz, const double* part_rr, int nb, int d,
-                         const double* bn) {
-  __shared__ double sh[32];
-  if (!st->phaseB) {
-    if (threadIdx.x == 0) st->phaseC = 0;
-    return;
-  }
-  const double rel = pcg_relres(part_rr, nb, d, bn, sh);
-  const double rzn = sum_part(part_rz, nb, 1, sh);
-  if (threadIdx.x == 0) {
-    st->phaseB = 0;
-    st->phaseC = 1;
-    st->relres = rel;
-    if (rel <= st->tol || st->it >= st->maxit) {
-      st->active = 0;
-      st->upd_p = 0;
-    } else {
-      st->rz_next = rzn;
-      st->beta = rzn / st->rz;
-      st->rz = rzn;
-      st->upd_p = 1;
-    }
-  }
-}
-
 // ---- objectives / gap (objective.cpp:63-113) ------------------------------------------
 // Edge terms at (X, Z): [0] sum w_l ||XB_l||_q, [1] ||XB - prox_r(XB + Z)||^2,
 // [2] ||XB||^2, [3] ||Z||^2; max dual-ball excess into partmax.
@@ -751,103 +534,7 @@ int hess_apply(const Prob& P, const double* p, const double* V, const double* ja
   Ctx& c = *P.c;
   double* bc = c.buf<double>("hess.bc", P.E() + 1);
   return hess_two_pass(c, *P.g, p, V, jal, jbe, thr, P.d(), sigma, P.q, bc, Ap, part,
-                       st ? &static_cast<const CgState*>(st)->active : nullptr);
-}
-
-const int* cg_active_ptr(const void* st) { return st ? &static_cast<const CgState*>(st)->active : nullptr; }
-
-PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, const char* op_name,
-               const double* rhs, PcgWork w, double tol, int64_t max_iter, bool warm) {
-  const int64_t m = d * n;
-  if (!(tol > 0.0)) invalid("pcg: tol must be positive");
-  if (max_iter < 1) invalid("pcg: max_iter must be >= 1");
-  if (d > 64 * kFeatThreads) invalid("pcg: feature dimension above 16384 is not supported");
-  const int nb = std::max(1, std::min(cdiv(n, 4), c.sm_count * 2));
-  const int64_t chunk = (n + nb - 1) / nb;
-  double* part_rz = part_buf(c, "pcg.rz", nb);
-  double* part_rr = part_buf(c, "pcg.rr", static_cast<size_t>(nb) * d);
-  double* part_h = part_buf(c, "pcg.h", 2 * static_cast<size_t>(c.sm_count) * 16 + 2);
-  double* bn = part_buf(c, "pcg.bn", d);
-  CgState* st = reinterpret_cast<CgState*>(c.dscal + 64);
-  const int nf = d <= kFeatThreads * 4 ? 4 : (d <= kFeatThreads * 16 ? 16 : 64);
-  const double* Mx = nullptr;
-  if (warm) {
-    op(w.x, w.Ap, part_h, nullptr);
-    Mx = w.Ap;
-  }
-  const int di = static_cast<int>(d);
-  if (nf == 4)
-    k_pcg_init<4><<<nb, kFeatThreads, 0, c.s>>>(rhs, Mx, w.diag, n, di, chunk, w.x, w.r, w.p, part_rz, part_rr);
-  else if (nf == 16)
-    k_pcg_init<16><<<nb, kFeatThreads, 0, c.s>>>(rhs, Mx, w.diag, n, di, chunk, w.x, w.r, w.p, part_rz, part_rr);
-  else
-    k_pcg_init<64><<<nb, kFeatThreads, 0, c.s>>>(rhs, Mx, w.diag, n, di, chunk, w.x, w.r, w.p, part_rz, part_rr);
-  CPB_LAUNCH_CHECK();
-  k_pcg_s0<<<1, 1024, 0, c.s>>>(st, part_rz, part_rr, nb, di, tol, max_iter, bn, Mx != nullptr);
-  CPB_LAUNCH_CHECK();
-  auto launch_b = [&]() {
-    if (nf == 4)
-      k_pcg_b<4><<<nb, kFeatThreads, 0, c.s>>>(st, w.Ap, w.diag, n, di, chunk, w.r, part_rz, part_rr);
-    else if (nf == 16)
-      k_pcg_b<16><<<nb, kFeatThreads, 0, c.s>>>(st, w.Ap, w.diag, n, di, chunk, w.r, part_rz, part_rr);
-    else
-      k_pcg_b<64><<<nb, kFeatThreads, 0, c.s>>>(st, w.Ap, w.diag, n, di, chunk, w.r, part_rz, part_rr);
-  };
-  const int fg = flat_grid(c, m);
-  int batch = 4;
-  long long it_before = 0;
-  PcgOut out;
-  for (;;) {
-    for (int b = 0; b < batch; ++b) {
-      int hb;
-      {
-        Ctx::Timer tm(&c, op_name, op_bytes);
-        hb = op(w.p, w.Ap, part_h, st);
-      }
-      {
-        Ctx::Timer tm(&c, "pcg_s1", 0.0);
-        k_pcg_s1<<<1, 256, 0, c.s>>>(st, part_h, hb);
-        CPB_LAUNCH_CHECK();
-      }
-      {
-        Ctx::Timer tm(&c, "pcg_update_b", 4.0 * m * 8.0);
-        launch_b();
-        CPB_LAUNCH_CHECK();
-      }
-      {
-        Ctx::Timer tm(&c, "pcg_s2", 0.0);
-        k_pcg_s2<<<1, 1024, 0, c.s>>>(st, part_rz, part_rr, nb, di, bn);
-        CPB_LAUNCH_CHECK();
-      }
-      {
-        Ctx::Timer tm(&c, "pcg_update_c", 6.0 * m * 8.0);
-        k_pcg_c<<<fg, 256, 0, c.s>>>(st, w.r, w.diag, m, w.x, w.p);
-        CPB_LAUNCH_CHECK();
-      }
-    }
-    CgState h;
-    CPB_CUDA(cudaMemcpyAsync(c.hscal, st, sizeof(CgState), cudaMemcpyDeviceToHost, c.s));
-    c.sync();
-    std::memcpy(&h, c.hscal, sizeof(CgState));
-    // launches after the loop ended were no-ops: drop them from the statistics
-    const int wasted = batch - static_cast<int>(h.it - it_before);
-    if (wasted > 0) {
-      c.discard_pending(op_name, wasted);
-      c.discard_pending("pcg_s1", wasted);
-      c.discard_pending("pcg_s2", wasted);
-      c.discard_pending("pcg_update_b", wasted);
-      c.discard_pending("pcg_update_c", wasted);
-    }
-    it_before = h.it;
-    if (h.status == 1) runtime("pcg: operator is not positive definite (p'Ap <= 0)");
-    if (!h.active) {
-      out.iterations = h.it;
-      out.converged = h.relres <= tol;
-      break;
-    }
-    batch = std::min(batch * 2, 32);
-  }
-  return out;
+                       cg_active_ptr(st));
 }
 
 PcgOut pcg_newton(const Prob& P, const double* V, const double* jal, const double* jbe, const double* thr,

@@ -1,0 +1,288 @@
+// Preconditioned CG on node-shaped d x n blocks (linalg.cpp:143-192), with
+// the loop control on the device.
+//
+// One iteration = operator (Hessian / Laplacian: Ap and <p,Ap>, <p,p> block
+// partials) -> k_cg_b -> k_cg_s2 -> k_cg_c.  Every kernel no-ops once the
+// state's `active` flag drops, so the host enqueues iterations in batches
+// and reads the 80-byte state only between batches.
+//
+//   k_cg_b : every block reduces the operator partials itself (fixed order,
+//            identical in all blocks) to alpha = rz / pAp, then r -= alpha Ap
+//            and the per-feature ||r_f||^2 and <r, r/diag> partials.
+//   k_cg_s2: worst relative feature-row residual (linalg.cpp:128-139) and
+//            beta; decides convergence / max_iter.
+//   k_cg_c : x += alpha p; p = r/diag + beta p.
+//
+// The vector kernels tile (32 features) x (a chunk of rows): per-feature
+// partial sums need no atomics, loads stay coalesced along the feature axis.
+#include "ops.cuh"
+
+namespace cpb {
+
+namespace {
+
+struct CgState {
+  double rz, pAp, alpha, beta, relres, tol, pp, rz_next;
+  long long it, maxit;
+  int active, stepped, phaseC, upd_p, status, pad;
+};
+
+struct Tile {
+  int R, F;           // row chunks, feature chunks (32 wide)
+  int64_t rows_per;   // rows per chunk
+  int blocks() const { return R * F; }
+};
+Tile tile_geom(int64_t n, int64_t d) {
+  Tile t;
+  t.F = static_cast<int>((d + 31) / 32);
+  t.R = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, n / 16)));
+  t.rows_per = (n + t.R - 1) / t.R;
+  return t;
+}
+
+// Fixed-order sum over the linear thread id (1-D or 2-D blocks).
+__device__ __forceinline__ double sum_part(const double* part, int nb, int stride, double* sh) {
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
+  double s = 0.0;
+  for (int b = tid; b < nb; b += nt) s += part[static_cast<int64_t>(b) * stride];
+  return block_sum(s, sh);
+}
+
+// Reduce the 8 row-lanes of a (32 x 8) tile column-wise through shared memory.
+__device__ __forceinline__ double tile_col_sum(double v, double* s8) {
+  s8[threadIdx.y * 32 + threadIdx.x] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.y == 0)
+    for (int y = 0; y < 8; ++y) r += s8[y * 32 + threadIdx.x];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(256) k_cg_init(const double* __restrict__ rhs, const double* __restrict__ Mx,
+                                                 const double* __restrict__ diag, int64_t n, int d, int F,
+                                                 int64_t rows_per, double* __restrict__ x, double* __restrict__ r,
+                                                 double* __restrict__ p, double* part_rz, double* part_bb) {
+  __shared__ double sh[32];
+  __shared__ double s8[256];
+  const int fc = blockIdx.x % F, rc = blockIdx.x / F;
+  const int f = fc * 32 + threadIdx.x;
+  const int64_t r0 = rc * rows_per, r1 = min(n, r0 + rows_per);
+  double rz = 0.0, bb = 0.0;
+  if (f < d) {
+#pragma unroll 4
+    for (int64_t v = r0 + threadIdx.y; v < r1; v += 8) {
+      const int64_t i = v * d + f;
+      const double b = rhs[i];
+      const double rv = Mx ? b - Mx[i] : b;
+      if (!Mx) x[i] = 0.0;
+      r[i] = rv;
+      const double z = rv / diag[i];
+      p[i] = z;
+      rz += rv * z;
+      bb += b * b;
+    }
+  }
+  const double cb = tile_col_sum(bb, s8);
+  if (threadIdx.y == 0 && f < d) part_bb[static_cast<int64_t>(rc) * d + f] = cb;
+  rz = block_sum(rz, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) part_rz[blockIdx.x] = rz;
+}
+
+// Worst relative feature-row residual from R x d column partials.
+__device__ double relres_cols(const double* part, int R, int d, const double* bn, double* sh) {
+  double worst = 0.0;
+  for (int f = threadIdx.x; f < d; f += blockDim.x) {
+    double s = 0.0;
+    for (int rc = 0; rc < R; ++rc) s += part[static_cast<int64_t>(rc) * d + f];
+    const double b = bn[f];
+    worst = fmax(worst, sqrt(s) / (b > 0.0 ? b : 1.0));
+  }
+  return block_max(worst, sh);
+}
+
+__global__ void k_cg_s0(CgState* st, const double* part_rz, int nblk, const double* part_bb, int R, int d,
+                        double tol, long long maxit, double* bn, int warm) {
+  __shared__ double sh[32];
+  for (int f = threadIdx.x; f < d; f += blockDim.x) {
+    double s = 0.0;
+    for (int rc = 0; rc < R; ++rc) s += part_bb[static_cast<int64_t>(rc) * d + f];
+    bn[f] = sqrt(s);
+  }
+  __syncthreads();
+  const double rel = relres_cols(part_bb, R, d, bn, sh);
+  const double rz = sum_part(part_rz, nblk, 1, sh);
+  if (threadIdx.x == 0) {
+    st->rz = rz;
+    st->relres = rel;
+    st->tol = tol;
+    st->it = 0;
+    st->maxit = maxit;
+    st->active = (!warm && rel <= tol) ? 0 : 1;
+    st->stepped = st->phaseC = st->upd_p = 0;
+    st->status = 0;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_cg_b(CgState* st, const double* __restrict__ part_h, int hb,
+                                              const double* __restrict__ Ap, const double* __restrict__ diag,
+                                              int64_t n, int d, int F, int64_t rows_per, double* __restrict__ r,
+                                              double* part_rz, double* part_rr) {
+  __shared__ double sh[32];
+  __shared__ double s8[256];
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0;
+  if (lead) st->phaseC = 0;
+  if (!st->active) return;
+  const double pAp = sum_part(part_h, hb, 2, sh);
+  const double pp = sum_part(part_h + 1, hb, 2, sh);
+  if (pAp <= 0.0) {  // linalg.cpp:172-176: stop (p = 0) or throw (not PD)
+    if (lead) {
+      st->active = 0;
+      st->stepped = 0;
+      if (pp != 0.0) st->status = 1;
+    }
+    return;
+  }
+  const double alpha = st->rz / pAp;
+  if (lead) {
+    st->it += 1;
+    st->pAp = pAp;
+    st->pp = pp;
+    st->alpha = alpha;
+    st->stepped = 1;
+  }
+  const int fc = blockIdx.x % F, rc = blockIdx.x / F;
+  const int f = fc * 32 + threadIdx.x;
+  const int64_t r0 = rc * rows_per, r1 = min(n, r0 + rows_per);
+  double rz = 0.0, rr = 0.0;
+  if (f < d) {
+#pragma unroll 4
+    for (int64_t v = r0 + threadIdx.y; v < r1; v += 8) {
+      const int64_t i = v * d + f;
+      const double rv = r[i] - alpha * Ap[i];
+      r[i] = rv;
+      rz += rv * (rv / diag[i]);
+      rr += rv * rv;
+    }
+  }
+  const double cr = tile_col_sum(rr, s8);
+  if (threadIdx.y == 0 && f < d) part_rr[static_cast<int64_t>(rc) * d + f] = cr;
+  rz = block_sum(rz, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) part_rz[blockIdx.x] = rz;
+}
+
+__global__ void k_cg_s2(CgState* st, const double* part_rz, int nblk, const double* part_rr, int R, int d,
+                        const double* bn) {
+  __shared__ double sh[32];
+  if (!st->stepped) return;
+  const double rel = relres_cols(part_rr, R, d, bn, sh);
+  const double rzn = sum_part(part_rz, nblk, 1, sh);
+  if (threadIdx.x == 0) {
+    st->stepped = 0;
+    st->phaseC = 1;
+    st->relres = rel;
+    if (rel <= st->tol || st->it >= st->maxit) {
+      st->active = 0;
+      st->upd_p = 0;
+    } else {
+      st->rz_next = rzn;
+      st->beta = rzn / st->rz;
+      st->rz = rzn;
+      st->upd_p = 1;
+    }
+  }
+}
+
+// x += alpha p; p = r/diag + beta p (when continuing)
+__global__ void k_cg_c(const CgState* __restrict__ st, const double* __restrict__ r, const double* __restrict__ diag,
+                       int64_t m, double* __restrict__ x, double* __restrict__ p) {
+  if (!st->phaseC) return;
+  const double alpha = st->alpha, beta = st->beta;
+  const bool upd = st->upd_p != 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double pv = p[i];
+    x[i] = x[i] + alpha * pv;
+    if (upd) p[i] = r[i] / diag[i] + beta * pv;
+  }
+}
+
+}  // namespace
+
+const int* cg_active_ptr(const void* st) { return st ? &static_cast<const CgState*>(st)->active : nullptr; }
+
+PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, const char* op_name,
+               const double* rhs, PcgWork w, double tol, int64_t max_iter, bool warm) {
+  const int64_t m = d * n;
+  if (!(tol > 0.0)) invalid("pcg: tol must be positive");
+  if (max_iter < 1) invalid("pcg: max_iter must be >= 1");
+  const Tile tg = tile_geom(n, d);
+  const int nblk = tg.blocks();
+  double* part_rz = c.buf<double>("pcg.rz", nblk + 8);
+  double* part_rr = c.buf<double>("pcg.rr", static_cast<size_t>(tg.R) * d + 8);
+  double* part_h = c.buf<double>("pcg.h", 2 * static_cast<size_t>(c.sm_count) * 16 + 8);
+  double* bn = c.buf<double>("pcg.bn", d + 8);
+  CgState* st = reinterpret_cast<CgState*>(c.dscal + 64);
+  const double* Mx = nullptr;
+  if (warm) {
+    op(w.x, w.Ap, part_h, nullptr);
+    Mx = w.Ap;
+  }
+  const int di = static_cast<int>(d);
+  const dim3 tb(32, 8);
+  k_cg_init<<<nblk, tb, 0, c.s>>>(rhs, Mx, w.diag, n, di, tg.F, tg.rows_per, w.x, w.r, w.p, part_rz, part_rr);
+  CPB_LAUNCH_CHECK();
+  k_cg_s0<<<1, 1024, 0, c.s>>>(st, part_rz, nblk, part_rr, tg.R, di, tol, max_iter, bn, Mx != nullptr);
+  CPB_LAUNCH_CHECK();
+  const int fg = std::max(1, std::min(cdiv(m, 256), c.sm_count * 4));
+  int batch = 4;
+  long long it_before = 0;
+  PcgOut out;
+  for (;;) {
+    for (int b = 0; b < batch; ++b) {
+      int hb;
+      {
+        Ctx::Timer tm(&c, op_name, op_bytes);
+        hb = op(w.p, w.Ap, part_h, st);
+      }
+      {
+        Ctx::Timer tm(&c, "pcg_update_b", 4.0 * m * 8.0);
+        k_cg_b<<<nblk, tb, 0, c.s>>>(st, part_h, hb, w.Ap, w.diag, n, di, tg.F, tg.rows_per, w.r, part_rz, part_rr);
+        CPB_LAUNCH_CHECK();
+      }
+      {
+        Ctx::Timer tm(&c, "pcg_s2", 0.0);
+        k_cg_s2<<<1, 1024, 0, c.s>>>(st, part_rz, nblk, part_rr, tg.R, di, bn);
+        CPB_LAUNCH_CHECK();
+      }
+      {
+        Ctx::Timer tm(&c, "pcg_update_c", 6.0 * m * 8.0);
+        k_cg_c<<<fg, 256, 0, c.s>>>(st, w.r, w.diag, m, w.x, w.p);
+        CPB_LAUNCH_CHECK();
+      }
+    }
+    CgState h;
+    CPB_CUDA(cudaMemcpyAsync(c.hscal, st, sizeof(CgState), cudaMemcpyDeviceToHost, c.s));
+    c.sync();
+    std::memcpy(&h, c.hscal, sizeof(CgState));
+    // launches after the loop ended were no-ops: drop them from the statistics
+    const int wasted = batch - static_cast<int>(h.it - it_before);
+    if (wasted > 0) {
+      c.discard_pending(op_name, wasted);
+      c.discard_pending("pcg_update_b", wasted);
+      c.discard_pending("pcg_s2", wasted);
+      c.discard_pending("pcg_update_c", wasted);
+    }
+    it_before = h.it;
+    if (h.status == 1) runtime("pcg: operator is not positive definite (p'Ap <= 0)");
+    if (!h.active) {
+      out.iterations = h.it;
+      out.converged = h.relres <= tol;
+      break;
+    }
+    batch = std::min(batch * 2, 32);
+  }
+  return out;
+}
+
+}  // namespace cpb

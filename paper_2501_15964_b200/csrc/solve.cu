@@ -403,6 +403,31 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
   std::vector<int> hl(static_cast<size_t>(n));
   SolveCache cache;
   bool warm = false;
+  // Outputs in page-locked host memory (cp_host_alloc / cudaHostRegister)
+  // are filled asynchronously, overlapped with the next gamma's solve.
+  auto pinned = [](const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool async_out = (X_out || Z_out) && pinned(X_out) && pinned(Z_out) && c.copy_stream() != nullptr;
+  cudaStream_t cs = async_out ? c.copy_stream() : nullptr;
+  double* snapX[2] = {nullptr, nullptr};
+  double* snapZ[2] = {nullptr, nullptr};
+  cudaEvent_t snap_ready[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};
+  if (async_out) {
+    for (int s = 0; s < 2; ++s) {
+      snapX[s] = c.buf<double>(s ? "path.sX1" : "path.sX0", m + 1);
+      snapZ[s] = c.buf<double>(s ? "path.sZ1" : "path.sZ0", me + 1);
+      CPB_CUDA(cudaEventCreateWithFlags(&snap_ready[s], cudaEventDisableTiming));
+      CPB_CUDA(cudaEventCreateWithFlags(&copy_done[s], cudaEventDisableTiming));
+      CPB_CUDA(cudaEventRecord(copy_done[s], cs));
+    }
+  }
   for (int64_t t = 0; t < T; ++t) {
     const double gamma = gammas[t];
     if (!(gamma >= 0.0) || !std::isfinite(gamma)) invalid("instance: gamma must be finite and >= 0");
@@ -422,9 +447,31 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
       d2h(c, hl.data(), lab, n * sizeof(int));
       for (int64_t i = 0; i < n; ++i) labels_out[t * n + i] = hl[static_cast<size_t>(i)];
     }
-    if (X_out) d2h(c, X_out + t * m, X, m * sizeof(double));
-    if (Z_out && me) d2h(c, Z_out + t * me, Z, me * sizeof(double));
+    if (async_out) {
+      // Snapshot the solution (D2D) and ship it to pinned host memory on the
+      // copy stream while the next gamma is solved (double-buffered).
+      const int s = static_cast<int>(t & 1);
+      CPB_CUDA(cudaStreamWaitEvent(c.s, copy_done[s], 0));
+      if (X_out) copy_dev(c, snapX[s], X, m);
+      if (Z_out && me) copy_dev(c, snapZ[s], Z, me);
+      CPB_CUDA(cudaEventRecord(snap_ready[s], c.s));
+      CPB_CUDA(cudaStreamWaitEvent(cs, snap_ready[s], 0));
+      if (X_out) CPB_CUDA(cudaMemcpyAsync(X_out + t * m, snapX[s], m * sizeof(double), cudaMemcpyDeviceToHost, cs));
+      if (Z_out && me)
+        CPB_CUDA(cudaMemcpyAsync(Z_out + t * me, snapZ[s], me * sizeof(double), cudaMemcpyDeviceToHost, cs));
+      CPB_CUDA(cudaEventRecord(copy_done[s], cs));
+    } else {
+      if (X_out) d2h(c, X_out + t * m, X, m * sizeof(double));
+      if (Z_out && me) d2h(c, Z_out + t * me, Z, me * sizeof(double));
+    }
     warm = opt.warm_start != 0;
+  }
+  if (async_out) {
+    CPB_CUDA(cudaStreamSynchronize(cs));
+    for (int s = 0; s < 2; ++s) {
+      cudaEventDestroy(snap_ready[s]);
+      cudaEventDestroy(copy_done[s]);
+    }
   }
   c.sync();
 }
