@@ -1,0 +1,671 @@
+// cluspath/b200.hpp — C++ mirror of the reference `cluspath` API
+// (/root/reference/proj/include/cluspath: types.hpp, graph.hpp, prox.hpp,
+// solvers.hpp, path.hpp) implemented over the C-ABI of libcluspath_b200.so
+// (include/cluspath_b200.h).  Same namespace, names, argument meaning and
+// exception types (std::invalid_argument / std::runtime_error), so code written
+// against the reference recompiles against this header; every numeric routine
+// runs on the B200.
+//
+// Differences a caller can see:
+//  * Eigen is not required: `Matrix` is a small owning column-major matrix with
+//    the same memory layout as Eigen::MatrixXd (d x n, one sample per column).
+//  * Host-callback linear algebra (LinearOperator, pcg on user functors,
+//    CholeskyFactor) is not exposed: the solvers run their PCG on the device;
+//    the graph Laplacian's spectral bound is `laplacian_lambda_max`.
+//  * A thread-local device context is used (device 0 unless set_device()).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <utility>
+#include <vector>
+
+#include "cluspath_b200.h"
+
+namespace cluspath {
+
+using Index = std::int64_t;
+
+// ---- types.hpp ---------------------------------------------------------------
+class Matrix {
+ public:
+  Matrix() = default;
+  Matrix(Index rows, Index cols) : r_(rows), c_(cols), v_(static_cast<size_t>(rows * cols), 0.0) {}
+  static Matrix Zero(Index rows, Index cols) { return Matrix(rows, cols); }
+  static Matrix Constant(Index rows, Index cols, double x) {
+    Matrix m(rows, cols);
+    for (auto& e : m.v_) e = x;
+    return m;
+  }
+  Index rows() const { return r_; }
+  Index cols() const { return c_; }
+  Index size() const { return r_ * c_; }
+  double* data() { return v_.data(); }
+  const double* data() const { return v_.data(); }
+  double& operator()(Index r, Index c) { return v_[static_cast<size_t>(c * r_ + r)]; }
+  double operator()(Index r, Index c) const { return v_[static_cast<size_t>(c * r_ + r)]; }
+  double* col(Index c) { return v_.data() + c * r_; }
+  const double* col(Index c) const { return v_.data() + c * r_; }
+  void resize(Index rows, Index cols) {
+    r_ = rows, c_ = cols;
+    v_.assign(static_cast<size_t>(rows * cols), 0.0);
+  }
+  bool allFinite() const {
+    for (double x : v_)
+      if (!std::isfinite(x)) return false;
+    return true;
+  }
+
+ private:
+  Index r_ = 0, c_ = 0;
+  std::vector<double> v_;
+};
+using Vector = std::vector<double>;
+
+namespace detail {
+inline void check(int rc) {
+  if (rc == CP_OK) return;
+  const std::string msg = cp_last_error();
+  if (rc == CP_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+struct CtxHolder {
+  cp_ctx* ctx = nullptr;
+  int device = 0;
+  ~CtxHolder() {
+    if (ctx) cp_ctx_destroy(ctx);
+  }
+};
+inline CtxHolder& holder() {
+  thread_local CtxHolder h;
+  return h;
+}
+inline cp_ctx* ctx() {
+  auto& h = holder();
+  if (!h.ctx) check(cp_ctx_create(h.device, &h.ctx));
+  return h.ctx;
+}
+struct DataDeleter {
+  void operator()(cp_data* p) const { cp_data_destroy(p); }
+};
+struct GraphDeleter {
+  void operator()(cp_graph* p) const { cp_graph_destroy(p); }
+};
+}  // namespace detail
+
+// Select the CUDA device for this thread's subsequent calls.
+inline void set_device(int device) {
+  auto& h = detail::holder();
+  if (h.ctx && h.device != device) {
+    cp_ctx_destroy(h.ctx);
+    h.ctx = nullptr;
+  }
+  h.device = device;
+}
+
+struct DataMatrix {
+  Matrix values;                           // d x n
+  std::vector<std::string> feature_names;  // optional, size d when present
+  Index d() const { return values.rows(); }
+  Index n() const { return values.cols(); }
+};
+
+// make_data_matrix (types.hpp:25-26; graph.cpp:10-23)
+inline DataMatrix make_data_matrix(Matrix values, std::vector<std::string> feature_names = {}) {
+  if (values.rows() < 1 || values.cols() < 1)
+    throw std::invalid_argument("data matrix must have at least one feature and one sample");
+  if (!values.allFinite()) throw std::invalid_argument("data matrix contains non-finite entries");
+  if (!feature_names.empty()) {
+    if (static_cast<Index>(feature_names.size()) != values.rows())
+      throw std::invalid_argument("feature_names size does not match feature count");
+    for (const auto& s : feature_names)
+      if (s.empty()) throw std::invalid_argument("feature_names entries must be non-empty");
+  }
+  return DataMatrix{std::move(values), std::move(feature_names)};
+}
+
+namespace detail {
+inline std::shared_ptr<cp_data> upload(const DataMatrix& data) {
+  cp_data* p = nullptr;
+  check(cp_data_create(ctx(), data.values.data(), data.d(), data.n(), &p));
+  return std::shared_ptr<cp_data>(p, DataDeleter{});
+}
+}  // namespace detail
+
+// ---- graph.hpp ---------------------------------------------------------------
+struct Edge {
+  Index i = 0;
+  Index j = 0;
+  double w = 0.0;
+};
+
+class WeightedGraph {
+ public:
+  WeightedGraph() = default;
+  // Sorts and validates on the device (graph.cpp:25-45).
+  WeightedGraph(Index n, std::vector<Edge> edges) {
+    std::vector<int64_t> i(edges.size()), j(edges.size());
+    std::vector<double> w(edges.size());
+    for (size_t l = 0; l < edges.size(); ++l) i[l] = edges[l].i, j[l] = edges[l].j, w[l] = edges[l].w;
+    cp_graph* g = nullptr;
+    detail::check(cp_graph_from_edges(detail::ctx(), n, i.data(), j.data(), w.data(),
+                                      static_cast<int64_t>(edges.size()), &g));
+    adopt(g);
+  }
+  static WeightedGraph from_handle(cp_graph* g) {
+    WeightedGraph out;
+    out.adopt(g);
+    return out;
+  }
+
+  Index nodes() const { return n_; }
+  Index edge_count() const { return static_cast<Index>(edges_.size()); }
+  const std::vector<Edge>& edges() const { return edges_; }
+  const Edge& edge(Index l) const { return edges_.at(static_cast<size_t>(l)); }
+  std::optional<Index> find_edge(Index i, Index j) const {
+    if (i > j) std::swap(i, j);
+    size_t lo = 0, hi = edges_.size();
+    while (lo < hi) {
+      const size_t mid = (lo + hi) / 2;
+      const Edge& e = edges_[mid];
+      if (e.i < i || (e.i == i && e.j < j)) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < edges_.size() && edges_[lo].i == i && edges_[lo].j == j) return static_cast<Index>(lo);
+    return std::nullopt;
+  }
+  Index degree(Index v) const {
+    if (v < 0 || v >= n_) throw std::invalid_argument("node index out of range");
+    return degree_[static_cast<size_t>(v)];
+  }
+  Index max_degree() const {
+    Index m = 0;
+    for (Index x : degree_) m = std::max(m, x);
+    return m;
+  }
+  Vector weights() const {
+    Vector w(edges_.size());
+    for (size_t l = 0; l < edges_.size(); ++l) w[l] = edges_[l].w;
+    return w;
+  }
+  // kNN squared distances of the edges (NaN for user edge lists).
+  const Vector& squared_distances() const { return d2_; }
+  cp_graph* handle() const { return h_.get(); }
+
+ private:
+  void adopt(cp_graph* g) {
+    h_ = std::shared_ptr<cp_graph>(g, detail::GraphDeleter{});
+    n_ = cp_graph_nodes(g);
+    const Index E = cp_graph_edge_count(g);
+    std::vector<int64_t> i(static_cast<size_t>(E)), j(static_cast<size_t>(E));
+    Vector w(static_cast<size_t>(E));
+    d2_.assign(static_cast<size_t>(E), 0.0);
+    detail::check(cp_graph_export(detail::ctx(), g, i.data(), j.data(), w.data(), d2_.data()));
+    edges_.resize(static_cast<size_t>(E));
+    for (Index l = 0; l < E; ++l) edges_[static_cast<size_t>(l)] = Edge{i[static_cast<size_t>(l)], j[static_cast<size_t>(l)], w[static_cast<size_t>(l)]};
+    std::vector<int64_t> deg(static_cast<size_t>(n_));
+    detail::check(cp_graph_degrees(detail::ctx(), g, deg.data()));
+    degree_.assign(deg.begin(), deg.end());
+  }
+  std::shared_ptr<cp_graph> h_;
+  Index n_ = 0;
+  std::vector<Edge> edges_;
+  std::vector<Index> degree_;
+  Vector d2_;
+};
+
+// compute_knn_weights (graph.hpp:58; graph.cpp:75-114)
+inline WeightedGraph compute_knn_weights(const DataMatrix& data, Index k, double phi) {
+  auto d = detail::upload(data);
+  cp_graph* g = nullptr;
+  detail::check(cp_knn_graph(detail::ctx(), d.get(), k, phi, &g));
+  return WeightedGraph::from_handle(g);
+}
+
+// IncidenceOperator (graph.hpp:62-86)
+class IncidenceOperator {
+ public:
+  explicit IncidenceOperator(const WeightedGraph& g) : graph_(&g) {}
+  Index nodes() const { return graph_->nodes(); }
+  Index edge_count() const { return graph_->edge_count(); }
+  const WeightedGraph& graph() const { return *graph_; }
+  Matrix apply(const Matrix& X) const {
+    Matrix out;
+    apply_into(X, out);
+    return out;
+  }
+  void apply_into(const Matrix& X, Matrix& out) const {
+    out.resize(X.rows(), edge_count());
+    detail::check(cp_incidence_apply(detail::ctx(), graph_->handle(), X.data(), X.rows(), X.cols(), out.data()));
+  }
+  Matrix apply_transpose(const Matrix& Z) const {
+    Matrix out;
+    apply_transpose_into(Z, out);
+    return out;
+  }
+  void apply_transpose_into(const Matrix& Z, Matrix& out) const {
+    out.resize(Z.rows(), nodes());
+    detail::check(cp_incidence_apply_t(detail::ctx(), graph_->handle(), Z.data(), Z.rows(), Z.cols(), out.data()));
+  }
+  // power_iteration(LinearOperator::sparse(laplacian())) (linalg.cpp:194-242)
+  double laplacian_lambda_max(double tol = 1e-9, Index max_iter = 10000) const {
+    double lam = 0.0;
+    detail::check(cp_laplacian_lambda_max(detail::ctx(), graph_->handle(), tol, max_iter, &lam));
+    return lam;
+  }
+
+ private:
+  const WeightedGraph* graph_;
+};
+
+// graph.hpp:90-92
+inline std::vector<Index> connected_components(const WeightedGraph& g) {
+  std::vector<int64_t> lab(static_cast<size_t>(g.nodes()));
+  int64_t K = 0;
+  detail::check(cp_connected_components(detail::ctx(), g.handle(), lab.data(), &K));
+  return std::vector<Index>(lab.begin(), lab.end());
+}
+inline Index component_count(const std::vector<Index>& labels) {
+  Index best = -1;
+  for (Index l : labels) best = std::max(best, l);
+  return best + 1;
+}
+
+// ---- prox.hpp ----------------------------------------------------------------
+enum class PenaltyNorm { l1, l2 };
+inline PenaltyNorm penalty_norm_from_q(int q) {
+  if (q == 1) return PenaltyNorm::l1;
+  if (q == 2) return PenaltyNorm::l2;
+  throw std::invalid_argument("penalty norm exponent must be 1 or 2, got " + std::to_string(q));
+}
+inline int penalty_q(PenaltyNorm norm) { return norm == PenaltyNorm::l1 ? 1 : 2; }
+
+// Columnwise helpers (prox.hpp:28-33), on the device.
+inline void prox_columns_into(const Matrix& V, const Vector& thresholds, PenaltyNorm norm, Matrix& out) {
+  if (static_cast<Index>(thresholds.size()) != V.cols())
+    throw std::invalid_argument("prox_columns: one threshold per column required");
+  out.resize(V.rows(), V.cols());
+  detail::check(cp_prox_columns(detail::ctx(), penalty_q(norm), V.data(), thresholds.data(), V.rows(), V.cols(),
+                                out.data()));
+}
+inline void project_columns_inplace(Matrix& Z, const Vector& radii, PenaltyNorm norm) {
+  if (static_cast<Index>(radii.size()) != Z.cols())
+    throw std::invalid_argument("project_columns: one radius per column required");
+  Matrix out(Z.rows(), Z.cols());
+  detail::check(cp_project_columns(detail::ctx(), penalty_q(norm), Z.data(), radii.data(), Z.rows(), Z.cols(),
+                                   out.data()));
+  Z = std::move(out);
+}
+inline Matrix project_columns(const Matrix& Z, const Vector& radii, PenaltyNorm norm) {
+  Matrix out = Z;
+  project_columns_inplace(out, radii, norm);
+  return out;
+}
+// Single-vector forms (prox.hpp:19-26): one-column device calls.
+inline Vector prox_norm(const Vector& v, double t, PenaltyNorm norm) {
+  Matrix V(static_cast<Index>(v.size()), 1), out;
+  std::memcpy(V.data(), v.data(), v.size() * sizeof(double));
+  prox_columns_into(V, Vector{t}, norm, out);
+  return Vector(out.data(), out.data() + v.size());
+}
+inline Vector project_dual_ball(const Vector& z, double r, PenaltyNorm norm) {
+  Matrix Z(static_cast<Index>(z.size()), 1);
+  std::memcpy(Z.data(), z.data(), z.size() * sizeof(double));
+  project_columns_inplace(Z, Vector{r}, norm);
+  return Vector(Z.data(), Z.data() + z.size());
+}
+// ProxJacobian::diag per column (prox.hpp:38-49).
+inline Matrix prox_jacobian_diag(const Matrix& V, const Vector& thresholds, PenaltyNorm norm) {
+  Matrix out(V.rows(), V.cols());
+  detail::check(cp_prox_jacobian_diag(detail::ctx(), penalty_q(norm), V.data(), thresholds.data(), V.rows(),
+                                      V.cols(), out.data()));
+  return out;
+}
+inline double moreau_check(const Vector& v, double t, PenaltyNorm norm) {
+  const Vector p = prox_norm(v, t, norm), q = project_dual_ball(v, t, norm);
+  double m = 0.0;
+  for (size_t k = 0; k < v.size(); ++k) m = std::max(m, std::abs(p[k] + q[k] - v[k]));
+  return m;
+}
+
+// ---- solvers.hpp -------------------------------------------------------------
+enum class Algorithm { ADMM, FastAMA, SSNAL };
+inline const char* algorithm_name(Algorithm a) {
+  switch (a) {
+    case Algorithm::ADMM: return "admm";
+    case Algorithm::FastAMA: return "ama";
+    case Algorithm::SSNAL: return "ssnal";
+  }
+  return "?";
+}
+inline Algorithm algorithm_from_name(std::string_view name) {
+  if (name == "admm") return Algorithm::ADMM;
+  if (name == "ama" || name == "fast-ama" || name == "fastama") return Algorithm::FastAMA;
+  if (name == "ssnal") return Algorithm::SSNAL;
+  throw std::invalid_argument("unknown solver '" + std::string(name) + "' (expected ssnal, admm or ama)");
+}
+
+struct ProblemInstance {
+  const DataMatrix* data = nullptr;
+  const WeightedGraph* graph = nullptr;
+  IncidenceOperator B;
+  double gamma = 0.0;
+  PenaltyNorm norm = PenaltyNorm::l2;
+  std::shared_ptr<cp_data> dev;  // device copy of A
+
+  ProblemInstance(const DataMatrix& data_, const WeightedGraph& graph_, double gamma_, PenaltyNorm norm_)
+      : data(&data_), graph(&graph_), B(graph_), gamma(gamma_), norm(norm_) {
+    if (data_.n() != graph_.nodes())
+      throw std::invalid_argument("instance: graph has " + std::to_string(graph_.nodes()) + " nodes for " +
+                                  std::to_string(data_.n()) + " samples");
+    if (!(gamma >= 0.0) || !std::isfinite(gamma)) throw std::invalid_argument("instance: gamma must be finite and >= 0");
+    dev = detail::upload(data_);
+  }
+  const Matrix& A() const { return data->values; }
+  Index d() const { return data->d(); }
+  Index n() const { return data->n(); }
+  Index edge_count() const { return graph->edge_count(); }
+  Vector penalty_radii() const {
+    Vector r = graph->weights();
+    for (double& x : r) x *= gamma;
+    return r;
+  }
+};
+
+struct TerminationRecord {
+  double f_primal = 0.0, f_dual = 0.0, gap = 0.0;
+  Index iterations = 0;
+  bool converged = false;
+  double wall_time = 0.0;
+  Index newton = 0, cg = 0, armijo = 0;  // work counters (extension)
+};
+
+struct Solution {
+  Matrix X;
+  Matrix Z;
+  TerminationRecord termination;
+};
+
+struct SolverConfig {
+  Algorithm algorithm = Algorithm::SSNAL;
+  double epsilon = 1e-6;
+  double kkt_factor = 10.0;
+  Index max_iter = 0;
+  std::optional<double> time_limit;
+  double admm_rho = 1.0;
+  double ama_step_safety = 0.99;
+  double ssnal_sigma0 = 1.0;
+  double armijo_mu = 1e-4;
+  double backtrack_beta = 0.5;
+  Index ssnal_newton_max = 50;
+  Index pcg_max_iter = 500;
+  bool collect_trace = false;
+
+  Index resolved_max_iter() const { return max_iter > 0 ? max_iter : (algorithm == Algorithm::SSNAL ? 100 : 20000); }
+  void validate() const {
+    if (time_limit && !(*time_limit > 0.0)) throw std::invalid_argument("config: time_limit must be positive when set");
+    cp_solver_config c = to_c();
+    (void)c;
+  }
+  cp_solver_config to_c() const {
+    cp_solver_config c;
+    cp_solver_config_default(&c);
+    c.algorithm = static_cast<int32_t>(algorithm);
+    c.collect_trace = collect_trace ? 1 : 0;
+    c.epsilon = epsilon;
+    c.kkt_factor = kkt_factor;
+    c.max_iter = max_iter;
+    c.time_limit = time_limit ? *time_limit : 0.0;
+    c.admm_rho = admm_rho;
+    c.ama_step_safety = ama_step_safety;
+    c.ssnal_sigma0 = ssnal_sigma0;
+    c.armijo_mu = armijo_mu;
+    c.backtrack_beta = backtrack_beta;
+    c.ssnal_newton_max = ssnal_newton_max;
+    c.pcg_max_iter = pcg_max_iter;
+    return c;
+  }
+};
+
+namespace detail {
+inline TerminationRecord from_c(const cp_termination& t) {
+  TerminationRecord r;
+  r.f_primal = t.f_primal, r.f_dual = t.f_dual, r.gap = t.gap, r.iterations = t.iterations;
+  r.converged = t.converged != 0, r.wall_time = t.wall_time;
+  r.newton = t.newton, r.cg = t.cg, r.armijo = t.armijo;
+  return r;
+}
+}  // namespace detail
+
+// objectives (solvers.hpp:95-118)
+inline double primal_objective(const ProblemInstance& inst, const Matrix& X) {
+  if (X.rows() != inst.d() || X.cols() != inst.n()) throw std::invalid_argument("primal_objective: X has the wrong shape");
+  double out = 0.0;
+  detail::check(cp_primal_objective(detail::ctx(), inst.dev.get(), inst.graph->handle(), inst.gamma,
+                                    penalty_q(inst.norm), X.data(), &out));
+  return out;
+}
+inline double dual_objective(const ProblemInstance& inst, const Matrix& Z) {
+  if (Z.rows() != inst.d() || Z.cols() != inst.edge_count())
+    throw std::invalid_argument("dual_objective: Z has the wrong shape");
+  double out = 0.0;
+  detail::check(cp_dual_objective(detail::ctx(), inst.dev.get(), inst.graph->handle(), inst.gamma,
+                                  penalty_q(inst.norm), Z.data(), &out));
+  return out;
+}
+inline double duality_gap(double f_p, double f_d) { return std::abs(f_p - f_d) / (1.0 + std::abs(f_p) + std::abs(f_d)); }
+inline Matrix recover_primal(const ProblemInstance& inst, const Matrix& Z) {
+  Matrix T = inst.B.apply_transpose(Z);
+  Matrix X(inst.d(), inst.n());
+  for (Index k = 0; k < X.size(); ++k) X.data()[k] = inst.A().data()[k] - T.data()[k];
+  return X;
+}
+inline double kkt_residual(const ProblemInstance& inst, const Matrix& X, const Matrix& Z) {
+  if (X.rows() != inst.d() || X.cols() != inst.n()) throw std::invalid_argument("kkt_residual: X has the wrong shape");
+  if (Z.rows() != inst.d() || Z.cols() != inst.edge_count())
+    throw std::invalid_argument("kkt_residual: Z has the wrong shape");
+  double out = 0.0;
+  detail::check(cp_kkt_residual(detail::ctx(), inst.dev.get(), inst.graph->handle(), inst.gamma, penalty_q(inst.norm),
+                                X.data(), Z.data(), &out));
+  return out;
+}
+// AL subproblem pieces (solvers.hpp:143-156)
+inline double ssnal_phi_value(const ProblemInstance& inst, const Matrix& Z, double sigma, const Matrix& X) {
+  double out = 0.0;
+  detail::check(cp_ssnal_phi_value(detail::ctx(), inst.dev.get(), inst.graph->handle(), inst.gamma,
+                                   penalty_q(inst.norm), Z.data(), sigma, X.data(), &out));
+  return out;
+}
+inline Matrix ssnal_phi_gradient(const ProblemInstance& inst, const Matrix& Z, double sigma, const Matrix& X) {
+  Matrix out(inst.d(), inst.n());
+  detail::check(cp_ssnal_phi_gradient(detail::ctx(), inst.dev.get(), inst.graph->handle(), inst.gamma,
+                                      penalty_q(inst.norm), Z.data(), sigma, X.data(), out.data()));
+  return out;
+}
+inline Matrix ssnal_hessian_apply(const ProblemInstance& inst, const Matrix& Z, double sigma, const Matrix& X,
+                                  const Matrix& D) {
+  Matrix out(inst.d(), inst.n());
+  detail::check(cp_ssnal_hessian_apply(detail::ctx(), inst.dev.get(), inst.graph->handle(), inst.gamma,
+                                       penalty_q(inst.norm), Z.data(), sigma, X.data(), D.data(), out.data()));
+  return out;
+}
+
+// Per-path state: held by the device context (solvers.hpp:119-123).
+struct SolveCache {};
+
+// solve / solve_* (solvers.hpp:132-141)
+inline Solution solve(const ProblemInstance& inst, const SolverConfig& config, const Solution* warm = nullptr,
+                      SolveCache* = nullptr) {
+  config.validate();
+  cp_solver_config c = config.to_c();
+  Solution sol;
+  sol.X.resize(inst.d(), inst.n());
+  sol.Z.resize(inst.d(), inst.edge_count());
+  cp_termination t;
+  detail::check(cp_solve(detail::ctx(), inst.dev.get(), inst.graph->handle(), inst.gamma, penalty_q(inst.norm), &c,
+                         warm ? warm->X.data() : nullptr, warm ? warm->X.rows() : 0, warm ? warm->X.cols() : 0,
+                         warm ? warm->Z.data() : nullptr, warm ? warm->Z.cols() : 0, sol.X.data(), sol.Z.data(),
+                         &t));
+  sol.termination = detail::from_c(t);
+  return sol;
+}
+inline Solution solve_ssnal(const ProblemInstance& inst, SolverConfig config, const Solution* warm = nullptr,
+                            SolveCache* cache = nullptr) {
+  config.algorithm = Algorithm::SSNAL;
+  return solve(inst, config, warm, cache);
+}
+inline Solution solve_admm(const ProblemInstance& inst, SolverConfig config, const Solution* warm = nullptr,
+                           SolveCache* cache = nullptr) {
+  config.algorithm = Algorithm::ADMM;
+  return solve(inst, config, warm, cache);
+}
+inline Solution solve_fast_ama(const ProblemInstance& inst, SolverConfig config, const Solution* warm = nullptr,
+                               SolveCache* cache = nullptr) {
+  config.algorithm = Algorithm::FastAMA;
+  return solve(inst, config, warm, cache);
+}
+
+// ---- path.hpp ----------------------------------------------------------------
+enum class Spacing { linear, geometric };
+inline const char* spacing_name(Spacing s) { return s == Spacing::linear ? "linear" : "geometric"; }
+inline Spacing spacing_from_name(std::string_view name) {
+  if (name == "linear") return Spacing::linear;
+  if (name == "geometric") return Spacing::geometric;
+  throw std::invalid_argument("unknown spacing '" + std::string(name) + "' (expected linear or geometric)");
+}
+
+struct GammaSchedule {
+  std::vector<double> values;
+  double start = 0.0;
+  double end = 0.0;
+  Index count = 0;
+  Spacing spacing = Spacing::geometric;
+};
+inline GammaSchedule make_schedule(double start, double end, Index count, Spacing spacing) {
+  GammaSchedule s;
+  s.values.assign(static_cast<size_t>(count > 0 ? count : 1), 0.0);
+  detail::check(cp_make_schedule(start, end, count, spacing == Spacing::geometric ? 1 : 0, s.values.data()));
+  s.values.resize(static_cast<size_t>(count));
+  s.start = start, s.end = end, s.count = count, s.spacing = spacing;
+  return s;
+}
+
+struct ClusterAssignment {
+  std::vector<Index> labels;
+  Index K = 0;
+  Matrix centroids;
+};
+inline ClusterAssignment extract_clusters(const Matrix& X, const WeightedGraph& graph, double fuse_tol = 1e-3) {
+  std::vector<int64_t> lab(static_cast<size_t>(X.cols()));
+  int64_t K = 0;
+  Matrix cent(X.rows(), X.cols());
+  detail::check(cp_extract_clusters(detail::ctx(), graph.handle(), X.data(), X.rows(), X.cols(), fuse_tol, lab.data(),
+                                    &K, cent.data()));
+  ClusterAssignment out;
+  out.labels.assign(lab.begin(), lab.end());
+  out.K = K;
+  out.centroids.resize(X.rows(), K);
+  std::memcpy(out.centroids.data(), cent.data(), sizeof(double) * static_cast<size_t>(X.rows() * K));
+  return out;
+}
+inline std::pair<Vector, Vector> two_point_closed_form(const Vector& a1, const Vector& a2, double w, double gamma) {
+  if (a1.size() != a2.size()) throw std::invalid_argument("two_point_closed_form: dimension mismatch");
+  if (!(w > 0.0)) throw std::invalid_argument("two_point_closed_form: weight must be positive");
+  if (!(gamma >= 0.0)) throw std::invalid_argument("two_point_closed_form: gamma must be >= 0");
+  double nc = 0.0;
+  for (size_t k = 0; k < a1.size(); ++k) nc += (a1[k] - a2[k]) * (a1[k] - a2[k]);
+  nc = std::sqrt(nc);
+  if (nc == 0.0) return {a1, a2};
+  const double s = std::min(2.0 * gamma * w / nc, 1.0);
+  Vector x1 = a1, x2 = a2;
+  for (size_t k = 0; k < a1.size(); ++k) {
+    const double c = a1[k] - a2[k];
+    x1[k] = a1[k] - 0.5 * s * c;
+    x2[k] = a2[k] + 0.5 * s * c;
+  }
+  return {x1, x2};
+}
+
+struct PathOptions {
+  bool warm_start = true;
+  bool require_connected = false;
+  double fuse_tol = 1e-3;
+};
+
+struct PathResult {
+  GammaSchedule schedule;
+  std::vector<Solution> solutions;
+  std::vector<ClusterAssignment> assignments;
+  std::vector<TerminationRecord> stats;
+  SolverConfig solver;
+  bool all_converged() const {
+    for (const auto& s : stats)
+      if (!s.converged) return false;
+    return true;
+  }
+};
+
+// run_path (path.hpp:71-73; path.cpp:110-142): the whole sweep on the GPU.
+inline PathResult run_path(const DataMatrix& data, const WeightedGraph& graph, PenaltyNorm norm,
+                           const GammaSchedule& schedule, const SolverConfig& config, const PathOptions& options = {}) {
+  if (schedule.values.empty()) throw std::invalid_argument("run_path: empty schedule");
+  if (data.n() != graph.nodes()) throw std::invalid_argument("run_path: graph size does not match the data");
+  config.validate();
+  auto dev = detail::upload(data);
+  const Index T = static_cast<Index>(schedule.values.size());
+  const Index d = data.d(), n = data.n(), E = graph.edge_count();
+  std::vector<double> X(static_cast<size_t>(T * d * n)), Z(static_cast<size_t>(T * d * E));
+  std::vector<int64_t> lab(static_cast<size_t>(T * n)), K(static_cast<size_t>(T));
+  std::vector<cp_termination> terms(static_cast<size_t>(T));
+  cp_solver_config c = config.to_c();
+  cp_path_options o{options.warm_start ? 1 : 0, options.require_connected ? 1 : 0, options.fuse_tol};
+  detail::check(cp_run_path(detail::ctx(), dev.get(), graph.handle(), penalty_q(norm), schedule.values.data(), T, &c,
+                            &o, X.data(), Z.data(), lab.data(), K.data(), terms.data()));
+  PathResult r;
+  r.schedule = schedule;
+  r.solver = config;
+  for (Index t = 0; t < T; ++t) {
+    Solution s;
+    s.X.resize(d, n);
+    s.Z.resize(d, E);
+    std::memcpy(s.X.data(), X.data() + t * d * n, sizeof(double) * static_cast<size_t>(d * n));
+    if (E) std::memcpy(s.Z.data(), Z.data() + t * d * E, sizeof(double) * static_cast<size_t>(d * E));
+    s.termination = detail::from_c(terms[static_cast<size_t>(t)]);
+    ClusterAssignment a;
+    a.labels.assign(lab.begin() + t * n, lab.begin() + (t + 1) * n);
+    a.K = K[static_cast<size_t>(t)];
+    r.stats.push_back(s.termination);
+    r.assignments.push_back(std::move(a));
+    r.solutions.push_back(std::move(s));
+  }
+  return r;
+}
+
+// generate_gaussian_mixture (io.hpp:41-44; io.cpp:142-165); centers as d-vectors.
+struct SyntheticData {
+  DataMatrix data;
+  std::vector<Index> labels;
+};
+inline SyntheticData generate_gaussian_mixture(const std::vector<Vector>& centers, double spread, Index per_center,
+                                               std::uint64_t seed) {
+  if (centers.empty()) throw std::invalid_argument("mixture needs at least one center");
+  const Index d = static_cast<Index>(centers.front().size()), m = static_cast<Index>(centers.size());
+  for (const auto& c : centers)
+    if (static_cast<Index>(c.size()) != d) throw std::invalid_argument("mixture centers differ in dimension");
+  std::vector<double> C(static_cast<size_t>(d * m));
+  for (Index k = 0; k < m; ++k) std::memcpy(C.data() + k * d, centers[static_cast<size_t>(k)].data(), sizeof(double) * static_cast<size_t>(d));
+  Matrix A(d, m * (per_center > 0 ? per_center : 0));
+  detail::check(cp_gaussian_mixture(C.data(), d, m, spread, per_center, seed, A.data()));
+  SyntheticData s{make_data_matrix(std::move(A)), {}};
+  for (Index k = 0; k < m; ++k)
+    for (Index q = 0; q < per_center; ++q) s.labels.push_back(k);
+  return s;
+}
+
+}  // namespace cluspath

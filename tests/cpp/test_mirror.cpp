@@ -1,0 +1,395 @@
+// C++ parity tests of the drop-in boundary: the reference's own unit-test
+// cases (tests/test_graph.cpp, test_prox.cpp, test_solvers.cpp, test_path.cpp
+// under /root/reference/proj), restated against the C++ mirror
+// include/cluspath/*.hpp, which calls libcluspath_b200.so (sm_100a) through
+// the C-ABI.  Run by tests/test_cpp_mirror.py on a GPU box.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "cluspath/graph.hpp"
+#include "cluspath/path.hpp"
+#include "cluspath/prox.hpp"
+#include "cluspath/solvers.hpp"
+
+using namespace cluspath;
+
+// ---- a very small doctest-like harness ----------------------------------------
+static int g_fail = 0, g_checks = 0;
+static std::vector<std::pair<std::string, std::function<void()>>>& registry() {
+  static std::vector<std::pair<std::string, std::function<void()>>> r;
+  return r;
+}
+struct Reg {
+  Reg(const char* n, std::function<void()> f) { registry().emplace_back(n, std::move(f)); }
+};
+#define CAT2(a, b) a##b
+#define CAT(a, b) CAT2(a, b)
+#define TEST_CASE(name)                                 \
+  static void CAT(tc_, __LINE__)();                     \
+  static Reg CAT(reg_, __LINE__)(name, CAT(tc_, __LINE__)); \
+  static void CAT(tc_, __LINE__)()
+#define CHECK(cond)                                                           \
+  do {                                                                        \
+    ++g_checks;                                                               \
+    if (!(cond)) {                                                            \
+      ++g_fail;                                                               \
+      std::printf("  CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+    }                                                                         \
+  } while (0)
+#define CHECK_THROWS_AS(expr, exc)                                                        \
+  do {                                                                                    \
+    ++g_checks;                                                                           \
+    bool ok_ = false;                                                                     \
+    try {                                                                                 \
+      (void)(expr);                                                                       \
+    } catch (const exc&) {                                                                \
+      ok_ = true;                                                                         \
+    } catch (...) {                                                                       \
+    }                                                                                     \
+    if (!ok_) {                                                                           \
+      ++g_fail;                                                                           \
+      std::printf("  CHECK_THROWS_AS failed %s:%d: %s\n", __FILE__, __LINE__, #expr);   \
+    }                                                                                     \
+  } while (0)
+static bool approx(double a, double b, double rel = 1e-12) { return std::abs(a - b) <= rel * std::max(1.0, std::abs(b)); }
+
+static DataMatrix line_data(std::initializer_list<double> xs) {
+  Matrix A(1, static_cast<Index>(xs.size()));
+  Index c = 0;
+  for (double x : xs) A(0, c++) = x;
+  return make_data_matrix(A);
+}
+static double maxabs_diff(const Matrix& a, const Matrix& b) {
+  double m = 0.0;
+  for (Index k = 0; k < a.size(); ++k) m = std::max(m, std::abs(a.data()[k] - b.data()[k]));
+  return m;
+}
+
+// ---- graph (test_graph.cpp) -----------------------------------------------------------
+TEST_CASE("weighted graph sorts and validates edges") {  // test_graph.cpp:51-77
+  WeightedGraph g(4, {{2, 3, 0.5}, {0, 1, 1.0}, {1, 3, 2.0}});
+  CHECK(g.nodes() == 4 && g.edge_count() == 3);
+  CHECK(g.edge(0).i == 0 && g.edge(0).j == 1 && g.edge(1).i == 1 && g.edge(2).i == 2);
+  CHECK(g.degree(3) == 2 && g.max_degree() == 2);
+  CHECK(g.find_edge(3, 1).has_value() && *g.find_edge(3, 1) == 1);
+  CHECK(!g.find_edge(0, 2).has_value());
+  Vector w = g.weights();
+  CHECK(w[0] == 1.0 && w[1] == 2.0 && w[2] == 0.5);
+  CHECK_THROWS_AS(WeightedGraph(4, {{1, 1, 1.0}}), std::invalid_argument);
+  CHECK_THROWS_AS(WeightedGraph(4, {{3, 1, 1.0}}), std::invalid_argument);
+  CHECK_THROWS_AS(WeightedGraph(4, {{0, 4, 1.0}}), std::invalid_argument);
+  CHECK_THROWS_AS(WeightedGraph(4, {{0, 1, 0.0}}), std::invalid_argument);
+  CHECK_THROWS_AS(WeightedGraph(4, {{0, 1, -2.0}}), std::invalid_argument);
+  CHECK_THROWS_AS(WeightedGraph(4, {{0, 1, 1.0}, {0, 1, 2.0}}), std::invalid_argument);
+}
+
+TEST_CASE("knn graph on a 1-D line, weights, ties, range, underflow") {  // test_graph.cpp:91-138
+  WeightedGraph g = compute_knn_weights(line_data({0.0, 1.0, 3.0}), 1, 0.0);
+  CHECK(g.edge_count() == 2 && g.edge(0).i == 0 && g.edge(0).j == 1 && g.edge(1).i == 1 && g.edge(1).j == 2);
+  CHECK(g.edge(0).w == 1.0 && g.edge(1).w == 1.0);
+  WeightedGraph h = compute_knn_weights(line_data({0.0, 1.0, 3.0}), 1, 0.5);
+  CHECK(approx(h.edge(0).w, 0.6065306597126334, 1e-14) && approx(h.edge(1).w, 0.1353352832366127, 1e-14));
+  Matrix A(2, 5);
+  const double xs[5] = {0.0, 5.0, -5.0, 5.1, -5.1};
+  for (int c = 0; c < 5; ++c) A(0, c) = xs[c];
+  WeightedGraph t = compute_knn_weights(make_data_matrix(A), 1, 0.0);
+  CHECK(t.find_edge(0, 1).has_value() && !t.find_edge(0, 2).has_value());
+  CHECK(t.find_edge(1, 3).has_value() && t.find_edge(2, 4).has_value() && t.edge_count() == 3);
+  CHECK_THROWS_AS(compute_knn_weights(line_data({0.0, 1.0, 3.0}), 0, 0.5), std::invalid_argument);
+  CHECK_THROWS_AS(compute_knn_weights(line_data({0.0, 1.0, 3.0}), 3, 0.5), std::invalid_argument);
+  CHECK(compute_knn_weights(line_data({0.0, 1.0, 3.0}), 2, 0.5).edge_count() == 3);
+  CHECK(compute_knn_weights(line_data({0.0, 1.0}), 1, 1.0).edge_count() == 1);
+  CHECK(compute_knn_weights(line_data({0.0, 1.0}), 1, 1e10).edge_count() == 0);
+}
+
+TEST_CASE("incidence operator and its transpose") {  // test_graph.cpp:140-171
+  WeightedGraph g(3, {{0, 1, 1.0}, {1, 2, 1.0}});
+  IncidenceOperator B(g);
+  Matrix X(1, 3);
+  X(0, 0) = 5, X(0, 1) = 2, X(0, 2) = 9;
+  Matrix XB = B.apply(X);
+  CHECK(XB.rows() == 1 && XB.cols() == 2 && XB(0, 0) == 3.0 && XB(0, 1) == -7.0);
+  std::mt19937_64 rng(11);
+  std::normal_distribution<double> gauss;
+  WeightedGraph g5(5, {{0, 1, 1.0}, {0, 3, 1.0}, {1, 2, 1.0}, {2, 4, 1.0}, {3, 4, 1.0}});
+  IncidenceOperator B5(g5);
+  Matrix X5(3, 5), Z5(3, 5);
+  for (Index k = 0; k < 15; ++k) X5.data()[k] = gauss(rng), Z5.data()[k] = gauss(rng);
+  Matrix xb = B5.apply(X5), zbt = B5.apply_transpose(Z5);
+  double lhs = 0, rhs = 0;
+  for (Index k = 0; k < 15; ++k) lhs += xb.data()[k] * Z5.data()[k], rhs += X5.data()[k] * zbt.data()[k];
+  CHECK(approx(lhs, rhs, 1e-12));
+  for (Index l = 0; l < g5.edge_count(); ++l)
+    for (Index r = 0; r < 3; ++r) CHECK(xb(r, l) == X5(r, g5.edge(l).i) - X5(r, g5.edge(l).j));
+  CHECK_THROWS_AS(B.apply(Matrix(1, 4)), std::invalid_argument);
+}
+
+TEST_CASE("connected components label by first appearance") {  // test_graph.cpp:214-232
+  auto l = connected_components(WeightedGraph(5, {{0, 1, 1.0}, {2, 3, 1.0}}));
+  CHECK((l == std::vector<Index>{0, 0, 1, 1, 2}) && component_count(l) == 3);
+  CHECK((connected_components(WeightedGraph(4, {{2, 3, 1.0}})) == std::vector<Index>{0, 1, 2, 2}));
+  CHECK(component_count(connected_components(WeightedGraph(3, {{0, 1, 1.0}, {1, 2, 1.0}}))) == 1);
+}
+
+// ---- prox (test_prox.cpp) ------------------------------------------------------------------
+TEST_CASE("soft thresholds and projections") {  // test_prox.cpp:45-76
+  Vector p = prox_norm({3, 4}, 1.0, PenaltyNorm::l2);
+  CHECK(approx(p[0], 2.4, 1e-14) && approx(p[1], 3.2, 1e-14));
+  CHECK(prox_norm({3, 4}, 5.0, PenaltyNorm::l2)[0] == 0.0);
+  CHECK((prox_norm({3, -4}, 1.0, PenaltyNorm::l1) == Vector{2.0, -3.0}));
+  Vector q = prox_norm({0.5, -4}, 1.0, PenaltyNorm::l1);
+  CHECK(q[0] == 0.0 && q[1] == -3.0);
+  Vector z = project_dual_ball({6, 8}, 5.0, PenaltyNorm::l2);
+  CHECK(approx(z[0], 3.0, 1e-14) && approx(z[1], 4.0, 1e-14));
+  CHECK((project_dual_ball({3, -4}, 2.0, PenaltyNorm::l1) == Vector{2.0, -2.0}));
+  CHECK_THROWS_AS(prox_norm({1, 1}, -0.5, PenaltyNorm::l2), std::invalid_argument);
+  CHECK_THROWS_AS(penalty_norm_from_q(3), std::invalid_argument);
+}
+
+TEST_CASE("moreau identity holds to machine precision") {  // test_prox.cpp:78-87
+  std::mt19937_64 rng(42);
+  std::uniform_real_distribution<double> tdist(0.0, 3.0);
+  std::normal_distribution<double> g(0.0, 2.0);
+  for (PenaltyNorm norm : {PenaltyNorm::l2, PenaltyNorm::l1})
+    for (int trial = 0; trial < 100; ++trial) {
+      Vector v(1 + rng() % 6);
+      for (double& x : v) x = g(rng);
+      CHECK(moreau_check(v, tdist(rng), norm) <= 1e-12);
+    }
+}
+
+// ---- solvers (test_solvers.cpp) --------------------------------------------------------------
+static DataMatrix five_point() {
+  Matrix A(2, 5);
+  const double a[2][5] = {{0.0, 1.0, -0.8, 0.3, -0.2}, {0.0, 0.2, 0.6, -0.9, 0.5}};
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 5; ++c) A(r, c) = a[r][c];
+  return make_data_matrix(A);
+}
+static WeightedGraph five_graph() {
+  return WeightedGraph(5, {{0, 1, 1.0}, {0, 2, 0.7}, {0, 3, 0.9}, {0, 4, 1.1}, {1, 2, 0.6}, {1, 3, 0.8}, {1, 4, 1.2},
+                           {2, 3, 0.5}, {2, 4, 0.95}, {3, 4, 0.65}});
+}
+
+TEST_CASE("objectives on the two-point example") {  // test_solvers.cpp:108-136
+  DataMatrix data = line_data({0.0, 2.0});
+  WeightedGraph g(2, {{0, 1, 1.0}});
+  ProblemInstance inst(data, g, 0.5, PenaltyNorm::l2);
+  Matrix X(1, 2);
+  X(0, 0) = 0.5, X(0, 1) = 1.5;
+  CHECK(approx(primal_objective(inst, X), 0.75, 1e-14));
+  Matrix Z(1, 1);
+  Z(0, 0) = -0.5;
+  CHECK(approx(dual_objective(inst, Z), 0.75, 1e-14));
+  Matrix rec = recover_primal(inst, Z);
+  CHECK(approx(rec(0, 0), 0.5, 1e-14) && approx(rec(0, 1), 1.5, 1e-14));
+  Matrix Zbad(1, 1);
+  Zbad(0, 0) = -0.6;
+  CHECK_THROWS_AS(dual_objective(inst, Zbad), std::invalid_argument);
+  CHECK_THROWS_AS(ProblemInstance(data, WeightedGraph(3, {{0, 1, 1.0}}), 0.5, PenaltyNorm::l2), std::invalid_argument);
+  CHECK_THROWS_AS(ProblemInstance(data, g, -0.5, PenaltyNorm::l2), std::invalid_argument);
+}
+
+TEST_CASE("every solver reproduces the two-point closed form") {  // test_solvers.cpp:164-197
+  std::mt19937_64 rng(77);
+  std::uniform_real_distribution<double> coord(-2.0, 2.0), wdist(0.5, 2.0), gdist(0.05, 1.5);
+  for (int trial = 0; trial < 6; ++trial) {
+    const Index d = 1 + trial % 3;
+    Vector a1(d), a2(d);
+    for (Index r = 0; r < d; ++r) a1[r] = coord(rng), a2[r] = coord(rng);
+    const double w = wdist(rng), gamma = gdist(rng);
+    Matrix A(d, 2);
+    for (Index r = 0; r < d; ++r) A(r, 0) = a1[r], A(r, 1) = a2[r];
+    DataMatrix data = make_data_matrix(A);
+    WeightedGraph g(2, {{0, 1, w}});
+    ProblemInstance inst(data, g, gamma, PenaltyNorm::l2);
+    auto [x1, x2] = two_point_closed_form(a1, a2, w, gamma);
+    for (Algorithm algo : {Algorithm::ADMM, Algorithm::FastAMA, Algorithm::SSNAL}) {
+      SolverConfig config;
+      config.algorithm = algo;
+      config.epsilon = 1e-8;
+      Solution sol = solve(inst, config);
+      CHECK(sol.termination.converged);
+      for (Index r = 0; r < d; ++r) CHECK(std::abs(sol.X(r, 0) - x1[r]) <= 1e-6 && std::abs(sol.X(r, 1) - x2[r]) <= 1e-6);
+    }
+  }
+}
+
+TEST_CASE("trivial problems, warm starts and shape checks") {  // test_solvers.cpp:199-242
+  DataMatrix data = line_data({1.0, -3.0});
+  WeightedGraph g(2, {{0, 1, 1.0}}), empty(2, {});
+  for (Algorithm algo : {Algorithm::ADMM, Algorithm::FastAMA, Algorithm::SSNAL}) {
+    SolverConfig config;
+    config.algorithm = algo;
+    for (auto* inst : {new ProblemInstance(data, g, 0.0, PenaltyNorm::l2), new ProblemInstance(data, empty, 1.0, PenaltyNorm::l2)}) {
+      Solution sol = solve(*inst, config);
+      CHECK(sol.termination.converged && sol.termination.iterations == 0 && sol.termination.gap == 0.0);
+      CHECK(maxabs_diff(sol.X, data.values) == 0.0);
+      delete inst;
+    }
+    DataMatrix fp = five_point();
+    WeightedGraph fg = five_graph();
+    ProblemInstance inst(fp, fg, 0.15, PenaltyNorm::l2);
+    config.epsilon = 1e-7;
+    Solution cold = solve(inst, config);
+    Solution warm = solve(inst, config, &cold);
+    CHECK(cold.termination.converged && warm.termination.converged && warm.termination.iterations == 0);
+    CHECK(maxabs_diff(warm.X, cold.X) == 0.0);
+    Solution bogus;
+    bogus.X = Matrix(2, 4);
+    bogus.Z = Matrix(2, 10);
+    CHECK_THROWS_AS(solve(inst, config, &bogus), std::invalid_argument);
+  }
+}
+
+TEST_CASE("q = 1 and q = 2 solves agree across solvers (five-point instance)") {  // test_solvers.cpp:244-263, 399-414
+  DataMatrix fp = five_point();
+  WeightedGraph fg = five_graph();
+  for (PenaltyNorm norm : {PenaltyNorm::l2, PenaltyNorm::l1})
+    for (double gamma : {0.05, 0.15, 0.25}) {
+      ProblemInstance inst(fp, fg, gamma, norm);
+      std::vector<double> f;
+      for (Algorithm algo : {Algorithm::ADMM, Algorithm::FastAMA, Algorithm::SSNAL}) {
+        SolverConfig config;
+        config.algorithm = algo;
+        config.epsilon = 1e-9;
+        Solution sol = solve(inst, config);
+        CHECK(sol.termination.converged);
+        const double fp_ = primal_objective(inst, sol.X), fd_ = dual_objective(inst, sol.Z);
+        CHECK(fd_ <= fp_ + 1e-10 * (1.0 + std::abs(fp_)));
+        CHECK(duality_gap(fp_, fd_) <= 1e-9 * (1.0 + 1e-9));
+        CHECK(kkt_residual(inst, sol.X, sol.Z) <= 10 * 1e-9 * (1.0 + 1e-9));
+        f.push_back(fp_);
+      }
+      CHECK(std::abs(f[1] - f[0]) <= 1e-7 * (1 + std::abs(f[0])) && std::abs(f[2] - f[0]) <= 1e-7 * (1 + std::abs(f[0])));
+    }
+}
+
+TEST_CASE("iteration caps and determinism") {  // test_solvers.cpp:318-365
+  DataMatrix fp = five_point();
+  WeightedGraph fg = five_graph();
+  ProblemInstance inst(fp, fg, 0.2, PenaltyNorm::l2);
+  SolverConfig config;
+  config.algorithm = Algorithm::ADMM;
+  config.epsilon = 1e-12;
+  config.max_iter = 3;
+  Solution sol = solve(inst, config);
+  CHECK(!sol.termination.converged && sol.termination.iterations == 3 && sol.termination.gap > 0.0);
+  for (Algorithm algo : {Algorithm::ADMM, Algorithm::FastAMA, Algorithm::SSNAL}) {
+    SolverConfig c;
+    c.algorithm = algo;
+    Solution s1 = solve(inst, c), s2 = solve(inst, c);
+    CHECK(maxabs_diff(s1.X, s2.X) == 0.0 && maxabs_diff(s1.Z, s2.Z) == 0.0);
+    CHECK(s1.termination.iterations == s2.termination.iterations && s1.termination.gap == s2.termination.gap);
+  }
+}
+
+TEST_CASE("augmented lagrangian derivatives match finite differences") {  // test_solvers.cpp:367-397
+  DataMatrix fp = five_point();
+  WeightedGraph fg = five_graph();
+  ProblemInstance inst(fp, fg, 0.3, PenaltyNorm::l2);
+  const double sigma = 1.7, h = 1e-6;
+  std::mt19937_64 rng(55);
+  std::normal_distribution<double> gauss;
+  Matrix Z(2, 10), X(2, 5), D(2, 5);
+  for (Index k = 0; k < 20; ++k) Z.data()[k] = 0.1 * gauss(rng);
+  double dn = 0;
+  for (Index k = 0; k < 10; ++k) X.data()[k] = fp.values.data()[k] + 0.3 * gauss(rng), D.data()[k] = gauss(rng), dn += D.data()[k] * D.data()[k];
+  for (Index k = 0; k < 10; ++k) D.data()[k] /= std::sqrt(dn);
+  Matrix Xp = X, Xm = X;
+  for (Index k = 0; k < 10; ++k) Xp.data()[k] += h * D.data()[k], Xm.data()[k] -= h * D.data()[k];
+  const double fd = (ssnal_phi_value(inst, Z, sigma, Xp) - ssnal_phi_value(inst, Z, sigma, Xm)) / (2 * h);
+  Matrix G = ssnal_phi_gradient(inst, Z, sigma, X);
+  double dir = 0;
+  for (Index k = 0; k < 10; ++k) dir += G.data()[k] * D.data()[k];
+  CHECK(std::abs(fd - dir) <= 1e-5 * std::abs(dir));
+  Matrix Gp = ssnal_phi_gradient(inst, Z, sigma, Xp), Gm = ssnal_phi_gradient(inst, Z, sigma, Xm);
+  Matrix HD = ssnal_hessian_apply(inst, Z, sigma, X, D);
+  double err = 0, nh = 0;
+  for (Index k = 0; k < 10; ++k) {
+    const double e = HD.data()[k] - (Gp.data()[k] - Gm.data()[k]) / (2 * h);
+    err += e * e, nh += HD.data()[k] * HD.data()[k];
+  }
+  CHECK(std::sqrt(err) <= 1e-5 * (1.0 + std::sqrt(nh)));
+}
+
+// ---- path (test_path.cpp) ---------------------------------------------------------------
+TEST_CASE("schedules and cluster extraction") {  // test_path.cpp:32-146
+  GammaSchedule s = make_schedule(1.0, 100.0, 3, Spacing::geometric);
+  CHECK(s.values.size() == 3 && approx(s.values[1], 10.0, 1e-14));
+  CHECK_THROWS_AS(make_schedule(0.5, 0.5, 2, Spacing::linear), std::invalid_argument);
+  CHECK_THROWS_AS(spacing_from_name("log"), std::invalid_argument);
+  WeightedGraph chain(4, {{0, 1, 1.0}, {1, 2, 1.0}, {2, 3, 1.0}});
+  Matrix X(1, 4);
+  X(0, 0) = 0, X(0, 1) = 1, X(0, 2) = 1, X(0, 3) = 3;
+  ClusterAssignment c = extract_clusters(X, chain);
+  CHECK(c.K == 3 && (c.labels == std::vector<Index>{0, 1, 1, 2}) && c.centroids(0, 1) == 1.0);
+  Matrix Y(1, 2);
+  Y(0, 0) = 1000.0, Y(0, 1) = 1000.5;
+  WeightedGraph pair(2, {{0, 1, 1.0}});
+  CHECK(extract_clusters(Y, pair).K == 1 && extract_clusters(Y, pair, 1e-5).K == 2);
+  CHECK_THROWS_AS(extract_clusters(Matrix(1, 3), chain), std::invalid_argument);
+}
+
+TEST_CASE("a two-point path crosses the fusion threshold at the predicted gamma") {  // test_path.cpp:148-170
+  DataMatrix data = line_data({0.0, 2.0});
+  WeightedGraph g(2, {{0, 1, 1.0}});
+  GammaSchedule schedule = make_schedule(0.1, 10.0, 9, Spacing::geometric);
+  SolverConfig config;
+  config.epsilon = 1e-8;
+  PathResult result = run_path(data, g, PenaltyNorm::l2, schedule, config);
+  CHECK(result.solutions.size() == 9 && result.all_converged());
+  for (size_t t = 0; t < 9; ++t) {
+    const double gamma = result.schedule.values[t];
+    CHECK(result.assignments[t].K == (gamma < 1.0 ? 2 : 1));
+    auto [x1, x2] = two_point_closed_form({0.0}, {2.0}, 1.0, gamma);
+    CHECK(std::abs(result.solutions[t].X(0, 0) - x1[0]) <= 1e-6 && std::abs(result.solutions[t].X(0, 1) - x2[0]) <= 1e-6);
+  }
+}
+
+TEST_CASE("warm starts reuse the previous solution; disconnected graphs") {  // test_path.cpp:172-245
+  SyntheticData synth = generate_gaussian_mixture({{-2.0, 0.0}, {2.0, 0.0}}, 0.4, 15, 7);
+  WeightedGraph graph = compute_knn_weights(synth.data, 4, 0.5);
+  GammaSchedule schedule = make_schedule(0.05, 5.0, 12, Spacing::geometric);
+  SolverConfig config;
+  PathOptions cold;
+  cold.warm_start = false;
+  PathResult with = run_path(synth.data, graph, PenaltyNorm::l2, schedule, config);
+  PathResult without = run_path(synth.data, graph, PenaltyNorm::l2, schedule, config, cold);
+  CHECK(with.all_converged() && without.all_converged());
+  Index wt = 0, ct = 0;
+  for (size_t t = 0; t < 12; ++t) wt += with.stats[t].iterations, ct += without.stats[t].iterations;
+  CHECK(wt <= ct);
+  for (size_t t = 0; t < 12; ++t) CHECK(maxabs_diff(with.solutions[t].X, without.solutions[t].X) <= 1e-3);
+  DataMatrix data = line_data({0.0, 1.0, 10.0, 11.0});
+  WeightedGraph g(4, {{0, 1, 1.0}, {2, 3, 1.0}});
+  GammaSchedule s2 = make_schedule(0.5, 1.0, 2, Spacing::geometric);
+  PathOptions opts;
+  opts.require_connected = true;
+  CHECK_THROWS_AS(run_path(data, g, PenaltyNorm::l2, s2, SolverConfig{}, opts), std::runtime_error);
+  opts.require_connected = false;
+  PathResult r = run_path(data, g, PenaltyNorm::l2, s2, SolverConfig{}, opts);
+  CHECK(r.all_converged() && r.assignments.back().K >= 2);
+}
+
+int main() {
+  int failed_cases = 0;
+  for (auto& [name, fn] : registry()) {
+    const int before = g_fail;
+    try {
+      fn();
+    } catch (const std::exception& e) {
+      ++g_fail;
+      std::printf("  unexpected exception: %s\n", e.what());
+    }
+    const bool ok = g_fail == before;
+    failed_cases += ok ? 0 : 1;
+    std::printf("%s  %s\n", ok ? "PASS" : "FAIL", name.c_str());
+  }
+  std::printf("%zu test cases, %d failed; %d checks, %d failed\n", registry().size(), failed_cases, g_checks, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}
