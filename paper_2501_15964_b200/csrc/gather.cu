@@ -322,16 +322,19 @@ __global__ void __launch_bounds__(256) k_edge_dot(const double* __restrict__ P, 
     const double* pa = P + static_cast<int64_t>(ei[l]) * d;
     const double* pb = P + static_cast<int64_t>(ej[l]) * d;
     const double* vl = V + l * d;
-    double c0 = 0.0, c1 = 0.0;
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
     int f = lane;
-    for (; f + 32 < d; f += 64) {
-      const double v0 = __ldcs(vl + f), v1 = __ldcs(vl + f + 32);
-      const double a0 = pa[f], a1 = pa[f + 32], b0 = pb[f], b1 = pb[f + 32];
-      c0 += v0 * (a0 - b0);
-      c1 += v1 * (a1 - b1);
+    for (; f + 96 < d; f += 128) {
+      const double v0 = __ldcs(vl + f), v1 = __ldcs(vl + f + 32), v2 = __ldcs(vl + f + 64), v3 = __ldcs(vl + f + 96);
+      const double a0 = pa[f], a1 = pa[f + 32], a2 = pa[f + 64], a3 = pa[f + 96];
+      const double b0 = pb[f], b1 = pb[f + 32], b2 = pb[f + 64], b3 = pb[f + 96];
+      c0 = __fma_rn(v0, a0 - b0, c0);
+      c1 = __fma_rn(v1, a1 - b1, c1);
+      c2 = __fma_rn(v2, a2 - b2, c2);
+      c3 = __fma_rn(v3, a3 - b3, c3);
     }
-    if (f < d) c0 += __ldcs(vl + f) * (pa[f] - pb[f]);
-    const double c = warp_sum(c0 + c1);
+    for (; f < d; f += 32) c0 = __fma_rn(__ldcs(vl + f), pa[f] - pb[f], c0);
+    const double c = warp_sum((c0 + c1) + (c2 + c3));
     if (lane == 0) bc[l] = be * c;
   }
 }
@@ -351,6 +354,7 @@ __global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, co
   double s_a = 0.0, s_b = 0.0;
   ITEMS_BEGIN(n, nch)
   double pv[NF], acc[NF];
+  double diag_coef = 0.0;  // sum over incident edges of (1 - alpha_l), q = 2
 #pragma unroll
   for (int k = 0; k < NF; ++k) {
     const int f = f0 + 32 * k;
@@ -386,19 +390,33 @@ __global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, co
           vv[u][k] = (need_v && f < d) ? __ldcs(V + static_cast<int64_t>(le[u]) * d + f) : 0.0;
         }
       }
+      if (q == 2) {
+        // Sign-free form: the edge adds (1 - alpha)(p_v - p_o) - s bc v_l to node v
+        // (s = +1 when v is the smaller endpoint); the p_v part is summed as a
+        // scalar, the rest is two FMAs per feature.
 #pragma unroll
-      for (int u = 0; u < kEB; ++u) {
-        if (u0 + u >= cnt) continue;
-        const bool plus = lo[u] > v;
+        for (int u = 0; u < kEB; ++u) {
+          if (u0 + u >= cnt) continue;
+          const double ca = 1.0 - ea[u];
+          const double cb = (lo[u] > v) ? eb[u] : -eb[u];
+          diag_coef += ca;
 #pragma unroll
-        for (int k = 0; k < NF; ++k) {
-          const double w = plus ? pv[k] - po[u][k] : po[u][k] - pv[k];
-          double y;
-          if (q == 2)
-            y = (eb[u] != 0.0) ? w - (ea[u] * w + eb[u] * vv[u][k]) : w - ea[u] * w;
-          else
-            y = w - (fabs(vv[u][k]) > ea[u] ? w : 0.0);
-          acc[k] = plus ? acc[k] + y : acc[k] - y;
+          for (int k = 0; k < NF; ++k) {
+            acc[k] = __fma_rn(-ca, po[u][k], acc[k]);
+            if (cb != 0.0) acc[k] = __fma_rn(-cb, vv[u][k], acc[k]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kEB; ++u) {
+          if (u0 + u >= cnt) continue;
+          const bool plus = lo[u] > v;
+#pragma unroll
+          for (int k = 0; k < NF; ++k) {
+            const double w = plus ? pv[k] - po[u][k] : po[u][k] - pv[k];
+            const double y = w - (fabs(vv[u][k]) > ea[u] ? w : 0.0);
+            acc[k] = plus ? acc[k] + y : acc[k] - y;
+          }
         }
       }
     }
@@ -407,6 +425,7 @@ __global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, co
   for (int k = 0; k < NF; ++k) {
     const int f = f0 + 32 * k;
     if (f >= d) continue;
+    if (q == 2) acc[k] = __fma_rn(diag_coef, pv[k], acc[k]);
     const double o = pv[k] + sigma * acc[k];
     Ap[base + f] = o;
     s_a += pv[k] * o;
@@ -505,6 +524,7 @@ int gather_grad_diag(Ctx& c, const Graph& g, const double* X, const double* A, c
 int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,
                   const double* thr, int64_t d, double sigma, int q, double* bc, double* Ap, double* part,
                   const int* active) {
+  if (q == 2 && g.E > 0 && hess_tma_supported(d)) return hess_tma(c, g, P, V, jal, jbe, d, sigma, Ap, part, active);
   if (q == 2 && g.E > 0) {
     const int grid = std::max(1, std::min(cdiv(g.E, 8), c.sm_count * 8));
     k_edge_dot<<<grid, 256, 0, c.s>>>(P, V, jbe, g.ei.p, g.ej.p, g.E, static_cast<int>(d), bc, active);

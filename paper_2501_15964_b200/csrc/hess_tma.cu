@@ -1,0 +1,335 @@
+// SSNAL Hessian apply (ssnal.cpp:56-64) with TMA-staged rows.
+//
+//   Ap_v = p_v + sigma * sum_{l ni v} +-( w_l - (alpha_l w_l + beta_l <v_l, w_l> v_l) ),
+//   w_l = p_i(l) - p_j(l)
+//
+// Work item = a segment of <= 64 incident edges of one node; one warp owns the
+// node's whole feature row (lane l holds features l + 32 k, k < NK) so the
+// per-edge dot <v_l, w_l> is a warp reduction and V is read once per
+// endpoint (the two-pass edge_dot + gather reads it three times).  Rows
+// p_other and v_l are streamed into a per-warp shared-memory ring by
+// cp.async.bulk (the TMA engine) with mbarrier completion: one lane issues
+// the next stages' copies while the warp computes, so every warp keeps
+// STAGES x 2 rows (2 x 6.3 KB at d = 784) in flight independent of its
+// register budget.  Nodes with more than 64 edges are split into segments
+// whose partial sums a second kernel combines in segment order
+// (deterministic).  Items run in node-id order, so both endpoints of an edge
+// of a clustered graph tend to read v_l within the L2 window.
+#include <cstdlib>
+#include <vector>
+
+#include "gather.cuh"
+#include "ops.cuh"
+
+namespace cpb {
+
+namespace {
+
+constexpr int kSegEdges = 64;
+constexpr int kStages = 2;
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// Per-warp shared memory: a metadata table for the current segment (<= 64
+// edges: id, other endpoint, 1 - alpha, beta) filled with two coalesced
+// rounds at segment start, and a kStages ring of {p_other row, v row}.
+// Per edge, with c = <v_l, p_v - p_o> (sign-free), the edge adds
+//   (1 - alpha)(p_v - p_o) - beta c v_l
+// to node v: one FMA per feature for the dot, two for the update.
+template <int NK>
+__global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, const double* __restrict__ V,
+                                                  const double* __restrict__ jal, const double* __restrict__ jbe,
+                                                  const int* __restrict__ adj_e, const int* __restrict__ adj_o,
+                                                  const int* __restrict__ seg_node, const int* __restrict__ seg_beg,
+                                                  const int* __restrict__ seg_end, const int* __restrict__ seg_slot,
+                                                  int nseg, int d, int dp, double sigma, double* __restrict__ Ap,
+                                                  double* __restrict__ partial, double* part, const int* active) {
+  if (active && !*active) return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ double sh[32];
+  __shared__ uint64_t bars[4][kStages];
+  __shared__ int m_le[4][kSegEdges], m_lo[4][kSegEdges];
+  __shared__ double m_ca[4][kSegEdges], m_be[4][kSegEdges];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* ring = reinterpret_cast<double*>(smraw) + static_cast<size_t>(warp) * kStages * 2 * dp;
+  uint64_t* bar = bars[warp];
+  int* le = m_le[warp];
+  int* lo = m_lo[warp];
+  double* ca = m_ca[warp];
+  double* mb = m_be[warp];
+  if (lane == 0)
+    for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
+  fence_mbar_init();
+  fence_proxy_async();
+  __syncwarp();
+  const unsigned row_bytes = static_cast<unsigned>(d) * 8u;
+  unsigned cnt = 0;  // stages consumed by this warp so far (phase tracking)
+  double s_a = 0.0, s_b = 0.0;
+  auto issue = [&](int q, int st) {  // lane 0: stream edge q's rows into stage st
+    const bool nv = mb[q] != 0.0;
+    mbar_expect_tx(&bar[st], nv ? 2 * row_bytes : row_bytes);
+    bulk_g2s(ring + st * 2 * dp, P + static_cast<int64_t>(lo[q]) * d, row_bytes, &bar[st]);
+    if (nv) bulk_g2s(ring + st * 2 * dp + dp, V + static_cast<int64_t>(le[q]) * d, row_bytes, &bar[st]);
+  };
+  const int wid = blockIdx.x * (blockDim.x >> 5) + warp, nw = gridDim.x * (blockDim.x >> 5);
+  for (int it = wid; it < nseg; it += nw) {
+    const int v = seg_node[it], e0 = seg_beg[it], ne = seg_end[it] - e0, slot = seg_slot[it];
+    const int64_t base = static_cast<int64_t>(v) * d;
+    // segment metadata: coalesced loads, then gathers of alpha / beta
+    for (int q = lane; q < ne; q += 32) {
+      const int l = adj_e[e0 + q];
+      le[q] = l;
+      lo[q] = adj_o[e0 + q];
+      ca[q] = 1.0 - jal[l];
+      mb[q] = jbe[l];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      fence_proxy_async();
+      for (int s = 0; s < kStages && s < ne; ++s) issue(s, (cnt + s) % kStages);
+    }
+    double pv[NK], acc[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+      const int f = lane + 32 * k;
+      pv[k] = f < d ? P[base + f] : 0.0;
+      acc[k] = 0.0;
+    }
+    double dsum = 0.0;
+    for (int q = 0; q < ne; ++q, ++cnt) {
+      const int st = cnt % kStages;
+      const double cq = ca[q], be = mb[q];
+      mbar_wait(&bar[st], (cnt / kStages) & 1u);
+      const double* po = ring + st * 2 * dp;
+      const double* vl = po + dp;
+      dsum += cq;
+      if (be != 0.0) {
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+          const int f = lane + 32 * k;
+          if (f < d) {
+            if (k & 1)
+              c1 = __fma_rn(vl[f], pv[k] - po[f], c1);
+            else
+              c0 = __fma_rn(vl[f], pv[k] - po[f], c0);
+          }
+        }
+        const double bc = be * warp_sum(c0 + c1);
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+          const int f = lane + 32 * k;
+          if (f < d) acc[k] = __fma_rn(-bc, vl[f], __fma_rn(-cq, po[f], acc[k]));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+          const int f = lane + 32 * k;
+          if (f < d) acc[k] = __fma_rn(-cq, po[f], acc[k]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0 && q + kStages < ne) {
+        fence_proxy_async();
+        issue(q + kStages, st);
+      }
+    }
+    __syncwarp();  // metadata table is rewritten by the next segment
+    if (slot < 0) {
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        const int f = lane + 32 * k;
+        if (f >= d) continue;
+        const double o = pv[k] + sigma * __fma_rn(dsum, pv[k], acc[k]);
+        Ap[base + f] = o;
+        a += pv[k] * o;
+        b += pv[k] * pv[k];
+      }
+      s_a += a;
+      s_b += b;
+    } else {
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        const int f = lane + 32 * k;
+        if (f < d) partial[static_cast<int64_t>(slot) * d + f] = __fma_rn(dsum, pv[k], acc[k]);
+      }
+    }
+  }
+  s_a = block_sum(s_a, sh);
+  s_b = block_sum(s_b, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s_a;
+    part[2 * blockIdx.x + 1] = s_b;
+  }
+}
+
+// Hub nodes: Ap = p + sigma * (sum of segment partials, in segment order).
+__global__ void __launch_bounds__(256) k_hess_combine(const double* __restrict__ P, const double* __restrict__ partial,
+                                                      const int* __restrict__ hub_node, const int* __restrict__ hub_slot0,
+                                                      const int* __restrict__ hub_nslots, int nhub, int d, double sigma,
+                                                      double* __restrict__ Ap, double* part, const int* active) {
+  if (active && !*active) return;
+  __shared__ double sh[32];
+  double s_a = 0.0, s_b = 0.0;
+  for (int h = blockIdx.x; h < nhub; h += gridDim.x) {
+    const int v = hub_node[h], s0 = hub_slot0[h], ns = hub_nslots[h];
+    const int64_t base = static_cast<int64_t>(v) * d;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      double acc = 0.0;
+      for (int s = 0; s < ns; ++s) acc += partial[static_cast<int64_t>(s0 + s) * d + f];
+      const double pv = P[base + f];
+      const double o = pv + sigma * acc;
+      Ap[base + f] = o;
+      s_a += pv * o;
+      s_b += pv * pv;
+    }
+  }
+  s_a = block_sum(s_a, sh);
+  s_b = block_sum(s_b, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s_a;
+    part[2 * blockIdx.x + 1] = s_b;
+  }
+}
+
+// Segments per graph (host-built once from the CSR offsets; node-id order).
+struct SegPlan {
+  uint64_t uid = 0;
+  int nseg = 0, nhub = 0, nslots = 0;
+  DBuf<int> node, beg, end, slot, hub_node, hub_slot0, hub_nslots;
+};
+
+SegPlan& seg_plan(Ctx& c, const Graph& g) {
+  static thread_local std::vector<std::unique_ptr<SegPlan>> plans;
+  for (auto& p : plans)
+    if (p->uid == g.uid) return *p;
+  auto p = std::make_unique<SegPlan>();
+  p->uid = g.uid;
+  std::vector<int> off(static_cast<size_t>(g.n + 1));
+  d2h(c, off.data(), g.off.p, off.size() * sizeof(int));
+  std::vector<int> node, beg, end, slot, hn, hs, hc;
+  int slots = 0;
+  for (int v = 0; v < g.n; ++v) {
+    const int a = off[v], b = off[v + 1];
+    if (b - a <= kSegEdges) {
+      node.push_back(v), beg.push_back(a), end.push_back(b), slot.push_back(-1);
+      continue;
+    }
+    hn.push_back(v), hs.push_back(slots);
+    int ns = 0;
+    for (int e = a; e < b; e += kSegEdges, ++ns)
+      node.push_back(v), beg.push_back(e), end.push_back(std::min(b, e + kSegEdges)), slot.push_back(slots + ns);
+    hc.push_back(ns);
+    slots += ns;
+  }
+  auto up = [&](DBuf<int>& buf, const std::vector<int>& h) {
+    buf.resize(h.size() + 1);
+    if (!h.empty()) h2d(c, buf.p, h.data(), h.size() * sizeof(int));
+  };
+  up(p->node, node), up(p->beg, beg), up(p->end, end), up(p->slot, slot);
+  up(p->hub_node, hn), up(p->hub_slot0, hs), up(p->hub_nslots, hc);
+  c.sync();
+  p->nseg = static_cast<int>(node.size());
+  p->nhub = static_cast<int>(hn.size());
+  p->nslots = slots;
+  if (plans.size() > 8) plans.erase(plans.begin());
+  plans.push_back(std::move(p));
+  return *plans.back();
+}
+
+#define NK_DISPATCH(nk, KERNEL, ...)          \
+  switch (nk) {                               \
+    case 2: KERNEL<2> __VA_ARGS__; break;     \
+    case 4: KERNEL<4> __VA_ARGS__; break;     \
+    case 8: KERNEL<8> __VA_ARGS__; break;     \
+    case 16: KERNEL<16> __VA_ARGS__; break;   \
+    case 25: KERNEL<25> __VA_ARGS__; break;   \
+    default: KERNEL<32> __VA_ARGS__; break;   \
+  }
+
+template <int NK>
+void set_smem(int bytes) {
+  CPB_CUDA(cudaFuncSetAttribute(k_hess_tma<NK>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+int nk_bucket(int64_t d) {
+  const int need = static_cast<int>((d + 31) / 32);
+  for (int b : {2, 4, 8, 16, 25, 32})
+    if (need <= b) return b;
+  return 0;
+}
+
+}  // namespace
+
+// Default for even d in [34, 1024] (CPB_TMA_HESS=0 selects the two-pass
+// warp-chunk path, which reads V three times instead of twice).
+bool hess_tma_supported(int64_t d) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("CPB_TMA_HESS");
+    return !(e && e[0] == '0');
+  }();
+  return enabled && d >= 33 && d % 2 == 0 && nk_bucket(d) > 0;
+}
+
+// Returns the number of (pAp, pp) block partials written to `part`.
+int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,
+             int64_t d, double sigma, double* Ap, double* part, const int* active) {
+  SegPlan& sp = seg_plan(c, g);
+  const int nk = nk_bucket(d);
+  const int dp = static_cast<int>((d + 1) / 2 * 2);
+  static const int warps = [] {
+    const char* e = std::getenv("CPB_TMA_WARPS");
+    const int v = e ? std::atoi(e) : 4;
+    return v < 1 ? 1 : (v > 4 ? 4 : v);
+  }();
+  const size_t smem = static_cast<size_t>(warps) * kStages * 2 * dp * sizeof(double);
+  if (smem > 220 * 1024) invalid("hessian: shared-memory ring exceeds 220 KB");
+  NK_DISPATCH(nk, set_smem, (static_cast<int>(smem)));
+  double* partial = c.buf<double>("hess.partial", static_cast<size_t>(sp.nslots) * d + 1);
+  const int grid = std::max(1, std::min(cdiv(sp.nseg, warps), c.sm_count * 2));
+  NK_DISPATCH(nk, k_hess_tma, <<<grid, 32 * warps, smem, c.s>>>(P, V, jal, jbe, g.adj_e.p, g.adj_o.p, sp.node.p,
+                                                                sp.beg.p, sp.end.p, sp.slot.p, sp.nseg,
+                                                                static_cast<int>(d), dp, sigma, Ap, partial, part,
+                                                                active));
+  CPB_LAUNCH_CHECK();
+  int nb = grid;
+  if (sp.nhub > 0) {
+    const int gh = std::max(1, std::min(sp.nhub, c.sm_count * 4));
+    k_hess_combine<<<gh, 256, 0, c.s>>>(P, partial, sp.hub_node.p, sp.hub_slot0.p, sp.hub_nslots.p, sp.nhub,
+                                         static_cast<int>(d), sigma, Ap, part + 2 * grid, active);
+    CPB_LAUNCH_CHECK();
+    nb += gh;
+  }
+  return nb;
+}
+
+}  // namespace cpb

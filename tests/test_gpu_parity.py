@@ -260,6 +260,34 @@ def test_solver_parity_with_oracle(cp, orc, algo, q):
         assert np.array_equal(cp.extract_clusters(sol.X, g).labels, orc.extract_clusters(osol.X, og)[0])
 
 
+@pytest.mark.parametrize("d", [34, 64, 784, 1000])
+def test_hessian_tma_path_matches_oracle(cp, orc, d):
+    """Even d >= 34 takes the TMA-staged single-pass Hessian (hess_tma.cu), including
+    hub nodes split into segments (k = 30 makes degrees > 64)."""
+    A = mixture(orc, 40, d, m=3, seed=5)
+    for k in (6, 30):
+        g, og = check_graph(cp, orc, A, k, 0.5)
+        rng = np.random.default_rng(d + k)
+        inst = cp.ProblemInstance(cp.DataMatrix(A), g, 0.2)
+        X = A + 0.05 * rng.standard_normal(A.shape)
+        Z = orc.project_columns(2, 0.1 * rng.standard_normal((g.edge_count(), d)), 0.2 * og.arrays()[2])
+        D = rng.standard_normal(A.shape)
+        for sigma in (0.7, 5.0):
+            H = cp.ssnal_hessian_apply(inst, Z, sigma, X, D)
+            OH = orc.hessian_apply(A, og, 0.2, 2, Z, sigma, X, D)
+            assert np.linalg.norm(H - OH) <= 1e-13 * np.linalg.norm(OH)
+
+
+def test_ssnal_iteration_path_matches_tma(cp, orc):
+    A = mixture(orc, 30, 40, m=3, seed=4)
+    g, og = check_graph(cp, orc, A, 6, 0.5)
+    sol = cp.solve(cp.ProblemInstance(cp.DataMatrix(A), g, 0.15))
+    osol = orc.solve(A, og, 0.15, 2)
+    t, ot = sol.termination, osol.term
+    assert (t.iterations, t.newton, t.cg, t.armijo) == (ot["iterations"], ot["newton"], ot["cg"], ot["armijo"])
+    assert np.linalg.norm(sol.X - osol.X) <= 1e-10 * np.linalg.norm(osol.X)
+
+
 def test_ssnal_iteration_path_matches(cp, orc):
     A = mixture(orc, 30, 16, m=3, seed=3)
     g, og = check_graph(cp, orc, A, 6, 0.5)
