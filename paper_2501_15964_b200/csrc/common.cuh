@@ -113,6 +113,7 @@ struct Ctx {
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
   cudaEvent_t timer_a = nullptr, timer_b = nullptr;  // cp_timer_start / cp_timer_stop
+  std::map<std::string, int> cg_hint;                 // last PCG iteration count per operator
   cudaStream_t cs = nullptr;                          // device->host copy stream (lazily created)
   cudaStream_t copy_stream() {
     if (!cs) CPB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));

@@ -12,6 +12,7 @@
 // reference's SSE2 build); the cited reference line is given per kernel.
 #include <cmath>
 
+#include "edge.cuh"
 #include "gather.cuh"
 #include "ops.cuh"
 
@@ -180,24 +181,21 @@ __global__ void k_phi_edge(const double* __restrict__ X, const double* __restric
     double env;
     if (q == Q_L2) {
       double ss = 0.0;
+#pragma unroll 4
       for (int f = threadIdx.x; f < d; f += blockDim.x) {
-        const double x = (xa[f] - xb[f]) + z[f] / sigma;
-        v[f] = x;
+        const double x = (xa[f] - xb[f]) + __ldcs(z + f) / sigma;
+        __stcs(v + f, x);
         ss += x * x;
       }
       ss = group_sum(ss, gm);
       const double nvl = sqrt(ss);
       double pn = 0.0, sq = ss;
       if (!(nvl <= t)) {
+        // P = s V with s = 1 - t/||V||: ||P|| = s ||V||, ||P - V||^2 = (s - 1)^2 ||V||^2
+        // (closed forms of the reference's two vector norms, one pass over V).
         const double s = 1.0 - t / nvl;
-        double a = 0.0, b = 0.0;
-        for (int f = threadIdx.x; f < d; f += blockDim.x) {
-          const double p = s * v[f];
-          a += p * p;
-          b += (p - v[f]) * (p - v[f]);
-        }
-        pn = sqrt(group_sum(a, gm));
-        sq = group_sum(b, gm);
+        pn = s * nvl;
+        sq = (s - 1.0) * (s - 1.0) * ss;
       }
       env = rad[row_] * pn + (0.5 * sigma) * sq;
       if (threadIdx.x == 0) nv[row_] = nvl;
@@ -336,21 +334,58 @@ __global__ void k_mult(const double* __restrict__ X, double* __restrict__ Z, con
     mx = fmax(mx, m);
     const double nz = sqrt(group_sum(nn, gm));
     const double sc = rl / nz;
-    double fr = 0.0, e = 0.0;
+    // pass 2: project, self-check, write Z, and the gap's edge sums at the new Z
+    double fr = 0.0, e = 0.0, xb2 = 0.0, zz = 0.0, uu = 0.0, l1 = 0.0, zmax = 0.0, al = 0.0;
+#pragma unroll 2
     for (int f = threadIdx.x; f < d; f += blockDim.x) {
       const double x = xa[f] - xb[f];
       const double zs = z[f] + sigma * x;
       const double zp = (q == Q_L2) ? ((nz <= rl) ? zs : sc * zs) : fmax(fmin(zs, rl), -rl);
-      const double pv = (q == Q_L2) ? sl * v[f] : soft(v[f], tl);
-      const double zenv = sigma * (v[f] - pv);
+      const double vf = __ldcs(v + f);
+      const double pv = (q == Q_L2) ? sl * vf : soft(vf, tl);
+      const double zenv = sigma * (vf - pv);
       e = fmax(e, fabs(zenv - zp));
       z[f] = zp;
       fr += (x - pv) * (x - pv);
+      const double u = x + zp;
+      xb2 += x * x;
+      zz += zp * zp;
+      uu += u * u;
+      l1 += fabs(x);
+      zmax = fmax(zmax, fabs(zp));
+      if (q != Q_L2) {
+        const double ee = x - soft(u, rl);
+        al += ee * ee;
+      }
     }
     err = fmax(err, e);
     fr = group_sum(fr, gm);
+    xb2 = group_sum(xb2, gm);
+    zz = group_sum(zz, gm);
     double t4[4];
-    gap_edge_terms(xa, xb, z, rl, w[row_], d, q, gm, t4, excess);
+    if (q == Q_L2) {
+      const double nu = sqrt(group_sum(uu, gm));
+      if (nu <= rl) {
+        al = xb2;
+      } else {  // pass 3 (objective.cpp:110-111): XB - prox(XB + Z) needs ||XB + Z|| first
+        const double s2 = 1.0 - rl / nu;
+        for (int f = threadIdx.x; f < d; f += blockDim.x) {
+          const double x = xa[f] - xb[f];
+          const double ee = x - s2 * (x + z[f]);
+          al += ee * ee;
+        }
+        al = group_sum(al, gm);
+      }
+      t4[0] = w[row_] * sqrt(xb2);
+      excess = fmax(excess, sqrt(zz) - (rl + 1e-9));
+    } else {
+      al = group_sum(al, gm);
+      t4[0] = w[row_] * group_sum(l1, gm);
+      excess = fmax(excess, group_max(zmax, gm) - (rl + 1e-9));
+    }
+    t4[1] = al;
+    t4[2] = xb2;
+    t4[3] = zz;
     if (threadIdx.x == 0) {
       for (int k = 0; k < 4; ++k) s[k] += t4[k];
       s[4] += fr;
@@ -489,12 +524,17 @@ double eval_phi(const Prob& P, const double* X, const double* D, double alpha, d
   reduce_sum(c, pn, fg, c.dscal);
   if (E > 0) {
     GroupGeom gg = group_geom(c, E, d);
-    double* pe = part_buf(c, "phi.pe", gg.grid);
+    double* pe = part_buf(c, "phi.pe", std::max(gg.grid, edge_grid(c, E)));
+    int nb = gg.grid;
     Ctx::Timer tm(&c, "phi_edge", (2.0 * E * d + n * d + 4.0 * E) * 8.0);
-    k_phi_edge<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, E,
-                                                        static_cast<int>(d), sigma, P.q, V, nv, pe);
-    CPB_LAUNCH_CHECK();
-    reduce_sum(c, pe, gg.grid, c.dscal + 1);
+    if (edge_reg_supported(d)) {
+      nb = phi_edge_reg(c, *P.g, Xe, Z, thr, P.rad, d, sigma, P.q, V, nv, pe);
+    } else {
+      k_phi_edge<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, E,
+                                                          static_cast<int>(d), sigma, P.q, V, nv, pe);
+      CPB_LAUNCH_CHECK();
+    }
+    reduce_sum(c, pe, nb, c.dscal + 1);
   } else {
     fill(c, c.dscal + 1, 1, 0.0);
   }
@@ -655,14 +695,19 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
   Ctx& c = *P.c;
   const int64_t d = P.d(), n = P.n(), E = P.E();
   GroupGeom ge = group_geom(c, E, d);
-  double* pe = part_buf(c, "mult.pe", 9 * static_cast<size_t>(ge.grid));
+  double* pe = part_buf(c, "mult.pe", 9 * static_cast<size_t>(std::max(ge.grid, edge_grid(c, E))));
+  int nb = ge.grid;
   {
     Ctx::Timer tm(&c, "multiplier", (3.0 * E * d + n * d) * 8.0);
-    k_mult<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p, P.g->ej.p, E,
-                                                    static_cast<int>(d), sigma, P.q, pe);
-    CPB_LAUNCH_CHECK();
+    if (edge_reg_supported(d)) {
+      nb = mult_reg(c, *P.g, X, Z, V, ps, thr, P.rad, d, sigma, P.q, pe);
+    } else {
+      k_mult<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p, P.g->ej.p, E,
+                                                      static_cast<int>(d), sigma, P.q, pe);
+      CPB_LAUNCH_CHECK();
+    }
   }
-  std::vector<double> s = host_cols(c, pe, ge.grid, 9, {6, 7, 8});
+  std::vector<double> s = host_cols(c, pe, nb, 9, {6, 7, 8});
   const double mx = s[6], err = s[7], excess = s[8];
   const double scale = 1.0 + mx;
   if (err > 1e-10 * scale) runtime("ssnal: multiplier self-check failed");

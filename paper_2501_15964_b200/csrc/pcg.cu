@@ -15,6 +15,8 @@
 //
 // The vector kernels tile (32 features) x (a chunk of rows): per-feature
 // partial sums need no atomics, loads stay coalesced along the feature axis.
+#include <cstdlib>
+
 #include "ops.cuh"
 
 namespace cpb {
@@ -235,7 +237,12 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
   k_cg_s0<<<1, 1024, 0, c.s>>>(st, part_rz, nblk, part_rr, tg.R, di, tol, max_iter, bn, Mx != nullptr);
   CPB_LAUNCH_CHECK();
   const int fg = std::max(1, std::min(cdiv(m, 256), c.sm_count * 4));
-  int batch = 4;
+  // Batch sizing: the first batch is the previous solve's iteration count
+  // (consecutive Newton systems need similar counts), then small top-ups, so
+  // few no-op iterations are launched past convergence.
+  static const bool doubling = std::getenv("CPB_CG_DOUBLING") != nullptr;  // A/B switch for the batch policy
+  int& hint = c.cg_hint[op_name];
+  int batch = (hint > 0 && !doubling) ? std::max(2, std::min(hint - 1, 64)) : 4;
   long long it_before = 0;
   PcgOut out;
   for (;;) {
@@ -280,8 +287,9 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
       out.converged = h.relres <= tol;
       break;
     }
-    batch = std::min(batch * 2, 32);
+    batch = doubling ? std::min(batch * 2, 32) : (h.it < 8 ? 4 : 2 + static_cast<int>(h.it / 8));
   }
+  hint = static_cast<int>(out.iterations);
   return out;
 }
 
