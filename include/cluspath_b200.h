@@ -98,6 +98,13 @@ int cp_stats_reset(cp_ctx* ctx);
 int cp_stats_get(cp_ctx* ctx, cp_kernel_stat* out, int max_entries, int* count);
 /* Device/library identification: sm major/minor, SM count, kernel build arch. */
 int cp_device_info(cp_ctx* ctx, int* sm_major, int* sm_minor, int* sm_count, int* built_arch);
+/* How the last cp_knn_graph on this context ran: tensor_cores = 1 when the
+ * tcgen05 3xTF32 candidate pass was used, segments = its column segments,
+ * band_rows = rows settled by the second (threshold) tensor-core pass,
+ * exact_rows = rows re-done by the exact FP64 tile kernel, worst_ratio =
+ * max |d2~ - d2| / delta_i over the candidates re-checked (must be < 1). */
+int cp_knn_info(cp_ctx* ctx, int* tensor_cores, int* segments, int64_t* band_rows, int64_t* exact_rows,
+                double* worst_ratio);
 /* Number of library kernel launches so far (process-wide). */
 unsigned long long cp_launch_count(void);
 /* CUDA-event timer on the context's stream; cp_timer_stop waits and returns ms. */

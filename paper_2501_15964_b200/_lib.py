@@ -56,6 +56,8 @@ _SIGS = [
     ("cp_stats_get", C.c_int, [VP, C.POINTER(KernelStatC), C.c_int, C.POINTER(C.c_int)]),
     ("cp_device_info", C.c_int, [VP, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                  C.POINTER(C.c_int)]),
+    ("cp_knn_info", C.c_int, [VP, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int64),
+                              C.POINTER(C.c_int64), D]),
     ("cp_launch_count", C.c_ulonglong, []),
     ("cp_timer_start", C.c_int, [VP]),
     ("cp_timer_stop", C.c_int, [VP, D]),

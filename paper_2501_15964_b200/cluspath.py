@@ -55,6 +55,14 @@ class Context:
         L.check(L.load().cp_device_info(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
         return {"sm": f"{a.value}{b.value}", "sm_count": c.value, "built_arch": d.value}
 
+    def knn_info(self):
+        """How the last compute_knn_weights on this context ran (tensor-core
+        candidate pass, segments, rows re-done exactly, worst |d2~-d2|/bound)."""
+        tc, seg, band, ex, wr = C.c_int(), C.c_int(), C.c_int64(), C.c_int64(), C.c_double()
+        L.check(L.load().cp_knn_info(self._h, C.byref(tc), C.byref(seg), C.byref(band), C.byref(ex), C.byref(wr)))
+        return {"tensor_cores": tc.value, "segments": seg.value, "band_rows": band.value, "exact_rows": ex.value,
+                "worst_ratio": wr.value}
+
     # kernel statistics for roofline accounting
     def stats_enable(self, on=True):
         L.check(L.load().cp_stats_enable(self._h, 1 if on else 0))

@@ -84,9 +84,6 @@ cpb::Prob make_prob(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gam
   return P;
 }
 
-void check_shape(int64_t rows, int64_t cols, int64_t er, int64_t ec, const char* what) {
-  if (rows != er || cols != ec) cpb::invalid(std::string(what) + " has the wrong shape");
-}
 }  // namespace
 
 extern "C" {
@@ -143,6 +140,17 @@ int cp_device_info(cp_ctx* ctx, int* sm_major, int* sm_minor, int* sm_count, int
     if (sm_minor) *sm_minor = ctx->c->sm_minor;
     if (sm_count) *sm_count = ctx->c->sm_count;
     if (built_arch) *built_arch = 100;
+  });
+}
+int cp_knn_info(cp_ctx* ctx, int* tensor_cores, int* segments, int64_t* band_rows, int64_t* exact_rows,
+                double* worst_ratio) {
+  return guard(ctx, [&] {
+    const auto& k = ctx->c->knn_last;
+    if (tensor_cores) *tensor_cores = k.tensor_cores;
+    if (segments) *segments = k.segments;
+    if (band_rows) *band_rows = ctx->c->knn_band_rows;
+    if (exact_rows) *exact_rows = k.overflow_rows;
+    if (worst_ratio) *worst_ratio = k.worst_ratio;
   });
 }
 unsigned long long cp_launch_count(void) { return cpb::g_launches; }
@@ -540,7 +548,7 @@ int cp_solve(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int
     cpb::SolveCache cache;
     cp_termination t = cpb::solve_dev(P, cf, warm, dx, dz, cache);
     if (X) cpb::d2h(c, X, dx, d * n * sizeof(double));
-    if (Z && d * E) cpb::d2h(c, Z, dz, d * E * sizeof(double));
+    if (Z && d > 0 && E > 0) cpb::d2h(c, Z, dz, d * E * sizeof(double));
     if (term) *term = t;
   });
 }

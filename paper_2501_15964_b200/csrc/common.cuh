@@ -114,6 +114,13 @@ struct Ctx {
   std::vector<cudaEvent_t> event_pool;
   cudaEvent_t timer_a = nullptr, timer_b = nullptr;  // cp_timer_start / cp_timer_stop
   std::map<std::string, int> cg_hint;                 // last PCG iteration count per operator
+  struct KnnInfo {
+    int64_t overflow_rows;  // rows re-done by the exact FP64 tile kernel
+    double worst_ratio;     // max |d2~ - d2| / delta_i over re-checked candidates
+    int segments;           // column segments of the tensor-core pass (0 = exact path only)
+    int tensor_cores;       // 1 when the tcgen05 candidate pass ran
+  } knn_last{0, 0.0, 0, 0};
+  int64_t knn_band_rows = 0;  // rows settled by the tensor-core threshold (band) pass
   cudaStream_t cs = nullptr;                          // device->host copy stream (lazily created)
   cudaStream_t copy_stream() {
     if (!cs) CPB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));

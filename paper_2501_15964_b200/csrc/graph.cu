@@ -77,8 +77,11 @@ __device__ __forceinline__ double eigen_finish(double c0, double c1, double c2, 
 
 // One block: KB_M query rows against all n samples, KB_N columns at a time.
 // Thread (tx, ty) of 16 x 16 owns rows {ty, ty+16} x cols {tx + 16 tn}.
+// With `rows` set, block b handles query rows rows[32 b ..] (nq of them):
+// the exact pass for the rows the tensor-core path could not settle.
 __global__ void __launch_bounds__(256) k_knn_topk(const double* __restrict__ A, int n, int d, int e2, int k,
-                                                  double* __restrict__ out_d, int* __restrict__ out_j) {
+                                                  const int* __restrict__ rows, int nq, double* __restrict__ out_d,
+                                                  int* __restrict__ out_j) {
   __shared__ double sA[KB_K][KB_M];
   __shared__ double sB[KB_K][KB_N];
   __shared__ double sD[KB_M][KB_N + 1];
@@ -88,6 +91,7 @@ __global__ void __launch_bounds__(256) k_knn_topk(const double* __restrict__ A, 
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int lane = tid & 31, warp = tid >> 5;
   const int row0 = blockIdx.x * KB_M;
+  auto qrow = [&](int rr) { return row0 + rr < nq ? (rows ? rows[row0 + rr] : row0 + rr) : n; };
 
   for (int p = tid; p < KB_M * KB_LIST; p += 256) {
     sLd[p / KB_LIST][p % KB_LIST] = CUDART_INF;
@@ -106,7 +110,7 @@ __global__ void __launch_bounds__(256) k_knn_topk(const double* __restrict__ A, 
     for (int k0 = 0; k0 < e2; k0 += KB_K) {
       __syncthreads();
       for (int p = tid; p < KB_M * KB_K; p += 256) {
-        const int r = p / KB_K, kk = p % KB_K, gr = row0 + r, gk = k0 + kk;
+        const int r = p / KB_K, kk = p % KB_K, gr = qrow(r), gk = k0 + kk;
         sA[kk][r] = (gr < n && gk < e2) ? A[static_cast<int64_t>(gr) * d + gk] : 0.0;
       }
       for (int p = tid; p < KB_N * KB_K; p += 256) {
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(256) k_knn_topk(const double* __restrict__ A, 
     for (int tm = 0; tm < 2; ++tm)
 #pragma unroll
       for (int tn = 0; tn < 4; ++tn) {
-        const int r = row0 + ty + 16 * tm, cidx = col0 + tx + 16 * tn;
+        const int r = qrow(ty + 16 * tm), cidx = col0 + tx + 16 * tn;
         double dist = CUDART_INF;
         if (r < n && cidx < n)
           dist = eigen_finish(acc[tm][tn][0], acc[tm][tn][1], acc[tm][tn][2], acc[tm][tn][3],
@@ -145,7 +149,7 @@ __global__ void __launch_bounds__(256) k_knn_topk(const double* __restrict__ A, 
     __syncthreads();
     // merge: warp w owns rows 4w..4w+3
     for (int rr = warp * 4; rr < warp * 4 + 4; ++rr) {
-      const int r = row0 + rr;
+      const int r = qrow(rr);
       if (r >= n) continue;
       for (int half = 0; half < 2; ++half) {
         const int cl = lane + 32 * half, j = col0 + cl;
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(256) k_knn_topk(const double* __restrict__ A, 
   }
   __syncthreads();
   for (int p = tid; p < KB_M * k; p += 256) {
-    const int rr = p / k, m = p % k, r = row0 + rr;
+    const int rr = p / k, m = p % k, r = qrow(rr);
     if (r < n) {
       out_d[static_cast<int64_t>(r) * k + m] = sLd[rr][m];
       out_j[static_cast<int64_t>(r) * k + m] = sLj[rr][m];
@@ -553,11 +557,23 @@ std::unique_ptr<Graph> knn_graph(Ctx& c, const Data& A, int64_t k, double phi) {
   int* kj = c.buf<int>("knn.j", NK);
   {
     Ctx::Timer tm(&c, "knn_topk", 0.0);
-    if (k <= KB_LIST) {
+    if (knn_tc_enabled(c, n, d, k)) {
+      int* ovf = c.buf<int>("knn.ovf", n);
+      const int64_t nov = knn_tc(c, A, k, kd, kj, ovf);
+      if (nov > 0) {
+        k_knn_topk<<<cdiv(nov, KB_M), 256, 0, c.s>>>(A.A.p, static_cast<int>(n), static_cast<int>(d), e2,
+                                                      static_cast<int>(k), ovf, static_cast<int>(nov), kd, kj);
+        CPB_LAUNCH_CHECK();
+      }
+    } else if (k <= KB_LIST) {
+      c.knn_last = {0, 0.0, 0, 0};
+      c.knn_band_rows = 0;
       k_knn_topk<<<cdiv(n, KB_M), 256, 0, c.s>>>(A.A.p, static_cast<int>(n), static_cast<int>(d), e2,
-                                                  static_cast<int>(k), kd, kj);
+                                                  static_cast<int>(k), nullptr, static_cast<int>(n), kd, kj);
       CPB_LAUNCH_CHECK();
     } else {
+      c.knn_last = {0, 0.0, 0, 0};
+      c.knn_band_rows = 0;
       const int64_t rows = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(1) << 26) / n));
       auto* keys = c.buf<unsigned long long>("knnf.k", rows * n);
       auto* keys2 = c.buf<unsigned long long>("knnf.k2", rows * n);

@@ -34,6 +34,11 @@ struct Graph {
 std::unique_ptr<Graph> graph_from_edges(Ctx& c, int64_t n, const int64_t* i, const int64_t* j, const double* w,
                                         int64_t E);
 std::unique_ptr<Graph> knn_graph(Ctx& c, const Data& A, int64_t k, double phi);
+// Tensor-core kNN candidates + exact FP64 re-check (knn_tc.cu).  Fills kd/kj
+// (n x k, ascending (d2, j)) for every row it can certify and lists the
+// others in ovf; returns how many (they need the exact tile kernel).
+bool knn_tc_enabled(Ctx& c, int64_t n, int64_t d, int64_t k);
+int64_t knn_tc(Ctx& c, const Data& A, int64_t k, double* kd, int* kj, int* ovf);
 // Builds CSR/order for a graph whose ei/ej/w/d2 (sorted, validated) are set.
 void finalize_graph(Ctx& c, Graph& g);
 

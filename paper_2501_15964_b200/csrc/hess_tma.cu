@@ -27,7 +27,6 @@ namespace {
 
 constexpr int kSegEdges = 64;
 constexpr int kStages = 2;
-constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));

@@ -80,6 +80,61 @@ def test_knn_duplicates_and_ties(cp, orc):
     check_graph(cp, orc, A, 6, 0.5)
 
 
+# ---- tensor-core kNN candidates + exact re-check (knn_tc.cu) ----------------------
+
+def _knn_arrays(cp, A, k, tc):
+    import os
+    old = os.environ.get("CPB_KNN_TC")
+    os.environ["CPB_KNN_TC"] = "1" if tc else "0"
+    try:
+        g = cp.compute_knn_weights(cp.DataMatrix(A), k, 0.5)
+        info = cp.default_context().knn_info()
+    finally:
+        if old is None:
+            del os.environ["CPB_KNN_TC"]
+        else:
+            os.environ["CPB_KNN_TC"] = old
+    return g.arrays(), info
+
+
+@pytest.mark.parametrize("n_per,d,k", [(512, 64, 10), (530, 17, 7), (520, 784, 10), (700, 33, 15)])
+def test_knn_tensor_core_matches_oracle(cp, orc, n_per, d, k):
+    """3xTF32 tcgen05 candidates + FP64 Eigen-order re-check == the oracle, bitwise."""
+    A = mixture(orc, n_per, d)
+    (gi, gj, gw, gd2), info = _knn_arrays(cp, A, k, True)
+    assert info["tensor_cores"] == 1 and 0.0 <= info["worst_ratio"] < 1.0
+    oi, oj, ow, od2 = orc.knn_weights(A, k, 0.5).arrays()
+    assert np.array_equal(gi, oi) and np.array_equal(gj, oj) and np.array_equal(gd2, od2)
+    assert np.max(np.abs(gw - ow) / ow) <= 2 * ULP
+
+
+@pytest.mark.parametrize("n,d,k", [(10000, 784, 10), (4099, 128, 24)])
+def test_knn_tensor_core_matches_exact_kernel(cp, orc, n, d, k):
+    """At C2 size the oracle is slow; the exact FP64 tile kernel (itself pinned
+    to the oracle above) is the reference."""
+    A = mixture(orc, n // 10, d, m=10)
+    (ti, tj, tw, td2), info = _knn_arrays(cp, A, k, True)
+    (ei, ej, ew, ed2), info0 = _knn_arrays(cp, A, k, False)
+    assert info["tensor_cores"] == 1 and info0["tensor_cores"] == 0
+    assert info["worst_ratio"] < 1.0 and info["exact_rows"] == 0
+    assert np.array_equal(ti, ei) and np.array_equal(tj, ej) and np.array_equal(td2, ed2)
+    assert np.array_equal(tw, ew)
+
+
+def test_knn_tensor_core_overflow_rows(cp, orc):
+    """Groups of 40 identical points: a row whose 39 duplicates share one column
+    segment has a full list inside its band, so the threshold pass collects
+    its whole band (groups split across segments are settled by the first
+    re-check)."""
+    base = mixture(orc, 60, 48, m=40)
+    A = np.repeat(base[:60], 40, axis=0)  # 2400 rows, 60 groups of 40 duplicates
+    A = np.concatenate([A, base[60:]], axis=0)
+    (ti, tj, tw, td2), info = _knn_arrays(cp, A, 10, True)
+    assert info["tensor_cores"] == 1 and info["band_rows"] >= 1000 and info["exact_rows"] == 0
+    oi, oj, ow, od2 = orc.knn_weights(A, 10, 0.5).arrays()
+    assert np.array_equal(ti, oi) and np.array_equal(tj, oj) and np.array_equal(td2, od2)
+
+
 def test_data_validation(cp):
     bad = np.ones((3, 2))
     bad[0, 0] = np.inf
