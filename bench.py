@@ -5,7 +5,10 @@ One *step* = one full clustering path on one synthetic Gaussian-mixture input:
 GPU kNN Gaussian-weight graph + 20 warm-started solves (SSNAL by default) +
 per-gamma labels.  Metric: path wall seconds (lower is better), KKT 1e-6.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+Default workload: C3, n=70000 d=784 k=10 (the north-star target; configs[2]
+of BASELINE.json).  c2 (n=10000, configs[1]) and c1 are selectable.
 
 * value  — device-timed (CUDA events on the library stream, max over ranks)
            path seconds with the input already resident in HBM; L2 flushed
@@ -16,8 +19,12 @@ per-gamma labels.  Metric: path wall seconds (lower is better), KKT 1e-6.
 * roofline — the dominant kernel (SSNAL Hessian apply) from the library's
            per-launch CUDA-event statistics during the timed steps:
            algorithmic bytes per launch / event time vs MEASURED_PEAKS hbm_gbs.
+* knn    — the tcgen05 3xTF32 distance contraction: TF32 TFLOP/s executed
+           (3 x 2 n^2 d / time) against half the measured BF16 peak.
+* edge_op_gbps — sum of algorithmic bytes / sum of time over the edge, prox,
+           CG, line-search and KKT kernels.
 * cpu_baseline — the CPU oracle (oracle/, a restatement of the single-threaded
-           reference) on the box's host, bounded sample: kNN of 200 query rows
+           reference) on the box's host, bounded sample: kNN of 400 query rows
            and one call of each SSNAL building block at this config, scaled by
            the GPU path's own iteration counts (which match the oracle's; see
            tests/test_gpu_parity.py::test_ssnal_iteration_path_matches).
@@ -63,6 +70,17 @@ def make_input(cp, cfg):
         centers = (3.0 / np.sqrt(d)) * cp.normals(1001, m * d).reshape(m, d)
         spread = 1.0 / np.sqrt(d)
     return cp.generate_gaussian_mixture(centers, spread, n // m, 42)
+
+
+def _peaks_file():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+PEAKS = _peaks_file()
 
 
 def load_peaks():
@@ -226,8 +244,10 @@ def run_reference(args, cfg):
     vals = []
     sample = ""
     for s in range(args.warmup + args.steps):
-        est, sample, spent = cpu_estimate(cfg, A, counts)
-        if s >= args.warmup:
+        timed = s >= args.warmup
+        # warm-up steps use a smaller sample (untimed); timed steps the bounded one
+        est, sample, spent = cpu_estimate(cfg, A, counts, knn_rows=200 if timed else 40, reps=1)
+        if timed:
             vals.append(est)
     v = float(np.median(vals))
     line = {"metric": "clustering-path wall s (20 gamma, KKT 1e-6)", "value": v, "unit": "s", "impl": "reference",
@@ -310,6 +330,22 @@ def run_ours(args, cfg):
             "per_kernel": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                                "GBps": (v["alg_bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 and v["alg_bytes"] > 0 else None}
                            for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])}}
+    # ---- the dense contraction on the tensor cores (north-star subsystem 1) ----------
+    ki = ctx.knn_info()
+    kg = stats.get("knn_gemm")
+    knn = {"tensor_cores": bool(ki["tensor_cores"]), "segments": ki["segments"], "band_rows": ki["band_rows"],
+           "exact_rows": ki["exact_rows"], "worst_bound_ratio": ki["worst_ratio"],
+           "total_ms": round(stats.get("knn_topk", {"ms": 0.0})["ms"] / max(1, args.steps), 3)}
+    if kg and kg["ms"] > 0:
+        alg = kg["alg_bytes"] / (kg["ms"] / 1e3) / 1e12  # alg_bytes holds 2 n^2 d flops for this kernel
+        tf32_peak = PEAKS.get("bf16_tflops", 2250.0) / 2.0
+        knn.update({"gemm_ms": round(kg["ms"] / kg["launches"], 3), "alg_tflops": round(alg, 1),
+                    "tf32_exec_tflops": round(3 * alg, 1), "bound": "tensor", "peak_tf32_tflops": tf32_peak,
+                    "peak_kind": "MEASURED_PEAKS bf16 burst / 2 (dense TF32 = half of BF16)",
+                    "frac": round(3 * alg / tf32_peak, 3)})
+    edge_ops = {k: v for k, v in stats.items() if v["alg_bytes"] > 0 and not k.startswith("knn")}
+    eb, et = sum(v["alg_bytes"] for v in edge_ops.values()), sum(v["ms"] for v in edge_ops.values())
+    edge_op_gbps = eb / (et / 1e3) / 1e9 if et > 0 else None
     counts = {"algorithm": cfg["algorithm"], "E": E, "gamma_mid": sched.values[len(sched.values) // 2],
               "per_gamma": [{"gamma": gm, "iterations": s.iterations, "newton": s.newton, "cg": s.cg,
                              "armijo": s.armijo, "converged": s.converged, "K": a.K}
@@ -318,7 +354,8 @@ def run_ours(args, cfg):
         os.makedirs(os.path.dirname(COUNTS_FILE), exist_ok=True)
         gi, gj, gw, _ = g.arrays()
         rel = os.path.join("profiles", f"graph_{args.config}.npz")
-        np.savez_compressed(os.path.join(ROOT, rel), i=gi.astype(np.int32), j=gj.astype(np.int32), w=gw)
+        np.savez_compressed(os.path.join(ROOT, rel), i=gi.astype(np.int32), j=gj.astype(np.int32),
+                            w=gw.astype(np.float32))
         counts["edges_file"] = rel
         with open(COUNTS_FILE.format(args.config), "w") as f:
             json.dump(counts, f, indent=1)
@@ -334,6 +371,7 @@ def run_ours(args, cfg):
                 "data": "synthetic", "config": workload_config(args, cfg),
                 "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": int(launches),
+                "knn": knn, "edge_op_gbps": edge_op_gbps,
                 "path": {"E": E, "K": [a.K for a in res.assignments], "converged": all(s.converged for s in res.stats),
                          "outer": [s.iterations for s in res.stats], "newton": sum(s.newton for s in res.stats),
                          "cg": sum(s.cg for s in res.stats), "armijo": sum(s.armijo for s in res.stats),
@@ -348,7 +386,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline sample")
     ap.add_argument("--write-counts", action="store_true", help="record the path counts for the reference arm")

@@ -655,7 +655,9 @@ int64_t knn_tc(Ctx& c, const Data& A, int64_t k, double* kd, int* kj, int* hard)
   const int nq = h[0];
   if (nq > 0) {
     // threshold pass over the rows whose band outgrew a list
-    const int qrb = cdiv(nq, TM), qseg = std::min(2, pick_seg(qrb)), caps = RC_MAX / qseg;
+    // few rows: spread the column sweep over all MAXSEG segments (one CTA each)
+    const int qrb = cdiv(nq, TM), qseg = qrb * 4 <= c.sm_count ? std::min(MAXSEG, ntiles) : pick_seg(qrb);
+    const int caps = RC_MAX;  // per segment; the re-check also caps the row total at RC_MAX
     float* qhi = c.buf<float>("knntc.qhi", static_cast<size_t>(nq) * dp);
     float* qlo = c.buf<float>("knntc.qlo", static_cast<size_t>(nq) * dp);
     float* td = c.buf<float>("knntc.td", static_cast<size_t>(qrb) * TM * qseg * caps);
