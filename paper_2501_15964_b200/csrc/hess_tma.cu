@@ -20,6 +20,7 @@
 
 #include "gather.cuh"
 #include "ops.cuh"
+#include "ptx.cuh"
 
 namespace cpb {
 
@@ -28,34 +29,6 @@ namespace {
 constexpr int kSegEdges = 64;
 constexpr int kStages = 2;
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
 // Per-warp shared memory: a metadata table for the current segment (<= 64
 // edges: id, other endpoint, 1 - alpha, beta) filled with two coalesced
@@ -70,7 +43,8 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
                                                   const int* __restrict__ seg_node, const int* __restrict__ seg_beg,
                                                   const int* __restrict__ seg_end, const int* __restrict__ seg_slot,
                                                   int nseg, int d, int dp, double sigma, double* __restrict__ Ap,
-                                                  double* __restrict__ partial, double* part, const int* active) {
+                                                  double* __restrict__ partial, double* part, const int* active,
+                                                  int evict_v) {
   if (active && !*active) return;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ double sh[32];
@@ -92,11 +66,17 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
   const unsigned row_bytes = static_cast<unsigned>(d) * 8u;
   unsigned cnt = 0;  // stages consumed by this warp so far (phase tracking)
   double s_a = 0.0, s_b = 0.0;
+  const uint64_t vpol = evict_v ? policy_evict_first() : 0;
   auto issue = [&](int q, int st) {  // lane 0: stream edge q's rows into stage st
     const bool nv = mb[q] != 0.0;
     mbar_expect_tx(&bar[st], nv ? 2 * row_bytes : row_bytes);
     bulk_g2s(ring + st * 2 * dp, P + static_cast<int64_t>(lo[q]) * d, row_bytes, &bar[st]);
-    if (nv) bulk_g2s(ring + st * 2 * dp + dp, V + static_cast<int64_t>(le[q]) * d, row_bytes, &bar[st]);
+    if (nv) {
+      if (evict_v)
+        bulk_g2s_hint(ring + st * 2 * dp + dp, V + static_cast<int64_t>(le[q]) * d, row_bytes, &bar[st], vpol);
+      else
+        bulk_g2s(ring + st * 2 * dp + dp, V + static_cast<int64_t>(le[q]) * d, row_bytes, &bar[st]);
+    }
   };
   const int wid = blockIdx.x * (blockDim.x >> 5) + warp, nw = gridDim.x * (blockDim.x >> 5);
   for (int it = wid; it < nseg; it += nw) {
@@ -310,6 +290,13 @@ int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const dou
     const int v = e ? std::atoi(e) : 4;
     return v < 1 ? 1 : (v > 4 ? 4 : v);
   }();
+  // CPB_HESS_VEVICT=1 streams V_l rows with an L2 evict_first policy (to keep
+  // the gathered P rows resident); off by default.
+  static const int vevict_env = [] {
+    const char* e = std::getenv("CPB_HESS_VEVICT");
+    return e ? std::atoi(e) : -1;
+  }();
+  const int evict_v = vevict_env > 0 ? 1 : 0;  // measured neutral-to-worse at C3 (1586 vs 1541 us)
   const size_t smem = static_cast<size_t>(warps) * kStages * 2 * dp * sizeof(double);
   if (smem > 220 * 1024) invalid("hessian: shared-memory ring exceeds 220 KB");
   NK_DISPATCH(nk, set_smem, (static_cast<int>(smem)));
@@ -318,7 +305,7 @@ int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const dou
   NK_DISPATCH(nk, k_hess_tma, <<<grid, 32 * warps, smem, c.s>>>(P, V, jal, jbe, g.adj_e.p, g.adj_o.p, sp.node.p,
                                                                 sp.beg.p, sp.end.p, sp.slot.p, sp.nseg,
                                                                 static_cast<int>(d), dp, sigma, Ap, partial, part,
-                                                                active));
+                                                                active, evict_v));
   CPB_LAUNCH_CHECK();
   int nb = grid;
   if (sp.nhub > 0) {

@@ -15,6 +15,7 @@
 #include "edge.cuh"
 #include "gather.cuh"
 #include "ops.cuh"
+#include "ptx.cuh"
 
 namespace cpb {
 
@@ -326,6 +327,7 @@ __global__ void k_mult(const double* __restrict__ X, double* __restrict__ Z, con
     const double* v = V + row_ * d;
     const double rl = rad[row_], tl = thr[row_], sl = ps[row_];
     double nn = 0.0, m = 0.0;
+#pragma unroll 4
     for (int f = threadIdx.x; f < d; f += blockDim.x) {
       const double zs = z[f] + sigma * (xa[f] - xb[f]);
       nn += zs * zs;
@@ -336,7 +338,7 @@ __global__ void k_mult(const double* __restrict__ X, double* __restrict__ Z, con
     const double sc = rl / nz;
     // pass 2: project, self-check, write Z, and the gap's edge sums at the new Z
     double fr = 0.0, e = 0.0, xb2 = 0.0, zz = 0.0, uu = 0.0, l1 = 0.0, zmax = 0.0, al = 0.0;
-#pragma unroll 2
+#pragma unroll 4
     for (int f = threadIdx.x; f < d; f += blockDim.x) {
       const double x = xa[f] - xb[f];
       const double zs = z[f] + sigma * x;
@@ -369,6 +371,7 @@ __global__ void k_mult(const double* __restrict__ X, double* __restrict__ Z, con
         al = xb2;
       } else {  // pass 3 (objective.cpp:110-111): XB - prox(XB + Z) needs ||XB + Z|| first
         const double s2 = 1.0 - rl / nu;
+#pragma unroll 4
         for (int f = threadIdx.x; f < d; f += blockDim.x) {
           const double x = xa[f] - xb[f];
           const double ee = x - s2 * (x + z[f]);
@@ -404,6 +407,319 @@ __global__ void k_mult(const double* __restrict__ X, double* __restrict__ Z, con
     part[9 * blockIdx.x + 7] = b;
     part[9 * blockIdx.x + 8] = c;
   }
+}
+
+// Shared-memory variant of k_mult for d <= kMultSmemMaxD with 32-lane rows:
+// pass 1 stages x = x_i - x_j and Zsum in the warp's shared-memory rows, so
+// passes 2 and 3 never touch HBM/L2 again (k_mult re-reads the three rows
+// per pass, and at C3 its 60 % L2 hit rate left it latency-bound at ~1.2 TB/s).
+// Each lane reads back only the elements it wrote (f = lane + 32 k), so no
+// synchronisation is needed.  Per-edge arithmetic and per-lane accumulation
+// order are those of k_mult (only the rows-to-block partition of the
+// deterministic block partials differs).
+constexpr int kMultSmemMaxD = 1024, kMultWarps = 4;
+template <int Q>
+__global__ void __launch_bounds__(32 * kMultWarps) k_mult_s(
+    const double* __restrict__ X, double* __restrict__ Z, const double* __restrict__ V, const double* __restrict__ ps,
+    const double* __restrict__ thr, const double* __restrict__ rad, const double* __restrict__ w,
+    const int* __restrict__ ei, const int* __restrict__ ej, int64_t E, int d, double sigma, double* part) {
+  extern __shared__ double srow[];
+  __shared__ double sh[32];
+  double* sx = srow + static_cast<size_t>(threadIdx.y) * 2 * d;
+  double* sz = sx + d;
+  double s[5] = {0, 0, 0, 0, 0}, mx = 0.0, err = 0.0, excess = -1.0;
+  ROWS_BEGIN(E) {
+    const double* xa = X + static_cast<int64_t>(ei[row_]) * d;
+    const double* xb = X + static_cast<int64_t>(ej[row_]) * d;
+    double* z = Z + row_ * d;
+    const double* v = V + row_ * d;
+    const double rl = rad[row_], tl = thr[row_], sl = ps[row_];
+    double nn = 0.0, m = 0.0;
+#pragma unroll 4
+    for (int f = threadIdx.x; f < d; f += 32) {
+      const double x = xa[f] - xb[f];
+      const double zs = z[f] + sigma * x;
+      sx[f] = x;
+      sz[f] = zs;
+      nn += zs * zs;
+      m = fmax(m, fabs(zs));
+    }
+    mx = fmax(mx, m);
+    const double nz = sqrt(warp_sum(nn));
+    const double sc = rl / nz;
+    double fr = 0.0, e = 0.0, xb2 = 0.0, zz = 0.0, uu = 0.0, l1 = 0.0, zmax = 0.0, al = 0.0;
+#pragma unroll 4
+    for (int f = threadIdx.x; f < d; f += 32) {
+      const double x = sx[f];
+      const double zs = sz[f];
+      const double zp = (Q == Q_L2) ? ((nz <= rl) ? zs : sc * zs) : fmax(fmin(zs, rl), -rl);
+      const double vf = __ldcs(v + f);
+      const double pv = (Q == Q_L2) ? sl * vf : soft(vf, tl);
+      const double zenv = sigma * (vf - pv);
+      e = fmax(e, fabs(zenv - zp));
+      z[f] = zp;
+      sz[f] = zp;
+      fr += (x - pv) * (x - pv);
+      const double u = x + zp;
+      xb2 += x * x;
+      zz += zp * zp;
+      if (Q == Q_L2) {
+        uu += u * u;
+      } else {
+        l1 += fabs(x);
+        zmax = fmax(zmax, fabs(zp));
+        const double ee = x - soft(u, rl);
+        al += ee * ee;
+      }
+    }
+    err = fmax(err, e);
+    fr = warp_sum(fr);
+    xb2 = warp_sum(xb2);
+    zz = warp_sum(zz);
+    double t0;
+    if (Q == Q_L2) {
+      const double nu = sqrt(warp_sum(uu));
+      if (nu <= rl) {
+        al = xb2;
+      } else {  // pass 3 (objective.cpp:110-111) from shared memory
+        const double s2 = 1.0 - rl / nu;
+#pragma unroll 4
+        for (int f = threadIdx.x; f < d; f += 32) {
+          const double x = sx[f];
+          const double ee = x - s2 * (x + sz[f]);
+          al += ee * ee;
+        }
+        al = warp_sum(al);
+      }
+      t0 = w[row_] * sqrt(xb2);
+      excess = fmax(excess, sqrt(zz) - (rl + 1e-9));
+    } else {
+      al = warp_sum(al);
+      t0 = w[row_] * warp_sum(l1);
+      excess = fmax(excess, warp_max(zmax) - (rl + 1e-9));
+    }
+    if (threadIdx.x == 0) {
+      s[0] += t0;
+      s[1] += al;
+      s[2] += xb2;
+      s[3] += zz;
+      s[4] += fr;
+    }
+  }
+  for (int k = 0; k < 5; ++k) {
+    const double r = block_sum(s[k], sh);
+    if (threadIdx.x == 0 && threadIdx.y == 0) part[9 * blockIdx.x + k] = r;
+  }
+  const double a = block_max(mx, sh);
+  const double b = block_max(err, sh);
+  const double c = block_max(excess, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    part[9 * blockIdx.x + 5] = 0.0;
+    part[9 * blockIdx.x + 6] = a;
+    part[9 * blockIdx.x + 7] = b;
+    part[9 * blockIdx.x + 8] = c;
+  }
+}
+
+// TMA variant (even d): one lane streams the edge's four rows (x_i, x_j, Z_l,
+// V_l) into the warp's shared-memory slot with cp.async.bulk, so each warp
+// keeps 4 d doubles in flight without spending registers on them; the three
+// passes then run from shared memory (x_i's slot is reused for x, Z_l's for
+// Zsum / the projected Z).  Per-element arithmetic is that of k_mult_s.
+template <int Q>
+__global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
+    const double* __restrict__ X, double* __restrict__ Z, const double* __restrict__ V, const double* __restrict__ ps,
+    const double* __restrict__ thr, const double* __restrict__ rad, const double* __restrict__ w,
+    const int* __restrict__ ei, const int* __restrict__ ej, int64_t E, int d, double sigma, double* part) {
+  extern __shared__ __align__(16) double trow[];
+  __shared__ double sh[32];
+  __shared__ uint64_t bars[kMultWarps];
+  const int lane = threadIdx.x;
+  double* sx = trow + static_cast<size_t>(threadIdx.y) * 4 * d;  // x_i, then x = x_i - x_j
+  double* sb = sx + d;                                            // x_j
+  double* sz = sb + d;                                            // Z_l, then Zsum, then Z_l new
+  double* sv = sz + d;                                            // V_l
+  uint64_t* bar = &bars[threadIdx.y];
+  if (lane == 0) mbar_init(bar, 1);
+  fence_mbar_init();
+  __syncwarp();
+  const unsigned rb = static_cast<unsigned>(d) * 8u;
+  unsigned phase = 0;
+  double s[5] = {0, 0, 0, 0, 0}, mx = 0.0, err = 0.0, excess = -1.0;
+  ROWS_BEGIN(E) {
+    if (lane == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(bar, 4 * rb);
+      bulk_g2s(sx, X + static_cast<int64_t>(ei[row_]) * d, rb, bar);
+      bulk_g2s(sb, X + static_cast<int64_t>(ej[row_]) * d, rb, bar);
+      const uint64_t ef = policy_evict_first();
+      bulk_g2s_hint(sz, Z + row_ * d, rb, bar, ef);
+      bulk_g2s_hint(sv, V + row_ * d, rb, bar, ef);
+    }
+    double* z = Z + row_ * d;
+    const double rl = rad[row_], tl = thr[row_], sl = ps[row_];
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    double nn = 0.0, m = 0.0;
+#pragma unroll 4
+    for (int f = lane; f < d; f += 32) {
+      const double x = sx[f] - sb[f];
+      const double zs = sz[f] + sigma * x;
+      sx[f] = x;
+      sz[f] = zs;
+      nn += zs * zs;
+      m = fmax(m, fabs(zs));
+    }
+    mx = fmax(mx, m);
+    const double nz = sqrt(warp_sum(nn));
+    const double sc = rl / nz;
+    double fr = 0.0, e = 0.0, xb2 = 0.0, zz = 0.0, uu = 0.0, l1 = 0.0, zmax = 0.0, al = 0.0;
+#pragma unroll 4
+    for (int f = lane; f < d; f += 32) {
+      const double x = sx[f];
+      const double zs = sz[f];
+      const double zp = (Q == Q_L2) ? ((nz <= rl) ? zs : sc * zs) : fmax(fmin(zs, rl), -rl);
+      const double vf = sv[f];
+      const double pv = (Q == Q_L2) ? sl * vf : soft(vf, tl);
+      const double zenv = sigma * (vf - pv);
+      e = fmax(e, fabs(zenv - zp));
+      z[f] = zp;
+      sz[f] = zp;
+      fr += (x - pv) * (x - pv);
+      const double u = x + zp;
+      xb2 += x * x;
+      zz += zp * zp;
+      if (Q == Q_L2) {
+        uu += u * u;
+      } else {
+        l1 += fabs(x);
+        zmax = fmax(zmax, fabs(zp));
+        const double ee = x - soft(u, rl);
+        al += ee * ee;
+      }
+    }
+    err = fmax(err, e);
+    fr = warp_sum(fr);
+    xb2 = warp_sum(xb2);
+    zz = warp_sum(zz);
+    double t0;
+    if (Q == Q_L2) {
+      const double nu = sqrt(warp_sum(uu));
+      if (nu <= rl) {
+        al = xb2;
+      } else {  // pass 3 (objective.cpp:110-111) from shared memory
+        const double s2 = 1.0 - rl / nu;
+#pragma unroll 4
+        for (int f = lane; f < d; f += 32) {
+          const double x = sx[f];
+          const double ee = x - s2 * (x + sz[f]);
+          al += ee * ee;
+        }
+        al = warp_sum(al);
+      }
+      t0 = w[row_] * sqrt(xb2);
+      excess = fmax(excess, sqrt(zz) - (rl + 1e-9));
+    } else {
+      al = warp_sum(al);
+      t0 = w[row_] * warp_sum(l1);
+      excess = fmax(excess, warp_max(zmax) - (rl + 1e-9));
+    }
+    if (lane == 0) {
+      s[0] += t0;
+      s[1] += al;
+      s[2] += xb2;
+      s[3] += zz;
+      s[4] += fr;
+    }
+    __syncwarp();  // every lane is done with the slot before lane 0 refills it
+  }
+  for (int k = 0; k < 5; ++k) {
+    const double r = block_sum(s[k], sh);
+    if (threadIdx.x == 0 && threadIdx.y == 0) part[9 * blockIdx.x + k] = r;
+  }
+  const double a = block_max(mx, sh);
+  const double b = block_max(err, sh);
+  const double c = block_max(excess, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    part[9 * blockIdx.x + 5] = 0.0;
+    part[9 * blockIdx.x + 6] = a;
+    part[9 * blockIdx.x + 7] = b;
+    part[9 * blockIdx.x + 8] = c;
+  }
+}
+
+// TMA variant of k_phi_edge (even d, 32-lane rows): x_i, x_j and Z_l are
+// streamed into the warp's shared-memory slot by cp.async.bulk (three rows in
+// flight per warp regardless of registers); V_l is written with streaming
+// stores.  Per-element arithmetic and per-lane order are those of k_phi_edge.
+template <int Q>
+__global__ void __launch_bounds__(32 * kMultWarps) k_phi_edge_t(
+    const double* __restrict__ X, const double* __restrict__ Z, const int* __restrict__ ei,
+    const int* __restrict__ ej, const double* __restrict__ thr, const double* __restrict__ rad, int64_t E, int d,
+    double sigma, double* __restrict__ V, double* __restrict__ nv, double* part) {
+  extern __shared__ __align__(16) double prow[];
+  __shared__ double sh[32];
+  __shared__ uint64_t bars[kMultWarps];
+  const int lane = threadIdx.x;
+  double* sa = prow + static_cast<size_t>(threadIdx.y) * 3 * d;
+  double* sb = sa + d;
+  double* sz = sb + d;
+  uint64_t* bar = &bars[threadIdx.y];
+  if (lane == 0) mbar_init(bar, 1);
+  fence_mbar_init();
+  __syncwarp();
+  const unsigned rb = static_cast<unsigned>(d) * 8u;
+  unsigned phase = 0;
+  double acc = 0.0;
+  ROWS_BEGIN(E) {
+    if (lane == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(bar, 3 * rb);
+      bulk_g2s(sa, X + static_cast<int64_t>(ei[row_]) * d, rb, bar);
+      bulk_g2s(sb, X + static_cast<int64_t>(ej[row_]) * d, rb, bar);
+      bulk_g2s_hint(sz, Z + row_ * d, rb, bar, policy_evict_first());
+    }
+    double* v = V + row_ * d;
+    const double t = thr[row_];
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    double env;
+    if (Q == Q_L2) {
+      double ss = 0.0;
+#pragma unroll 4
+      for (int f = lane; f < d; f += 32) {
+        const double x = (sa[f] - sb[f]) + sz[f] / sigma;
+        __stcs(v + f, x);
+        ss += x * x;
+      }
+      ss = warp_sum(ss);
+      const double nvl = sqrt(ss);
+      double pn = 0.0, sq = ss;
+      if (!(nvl <= t)) {
+        const double sc = 1.0 - t / nvl;
+        pn = sc * nvl;
+        sq = (sc - 1.0) * (sc - 1.0) * ss;
+      }
+      env = rad[row_] * pn + (0.5 * sigma) * sq;
+      if (lane == 0) nv[row_] = nvl;
+    } else {
+      double a = 0.0, b = 0.0;
+#pragma unroll 4
+      for (int f = lane; f < d; f += 32) {
+        const double x = (sa[f] - sb[f]) + sz[f] / sigma;
+        __stcs(v + f, x);
+        const double p = soft(x, t);
+        a += fabs(p);
+        b += (p - x) * (p - x);
+      }
+      env = rad[row_] * warp_sum(a) + (0.5 * sigma) * warp_sum(b);
+      if (lane == 0) nv[row_] = 0.0;
+    }
+    if (lane == 0) acc += env;
+    __syncwarp();
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) part[blockIdx.x] = acc;
 }
 
 // ---- fast AMA (ama.cpp:57-72) -----------------------------------------------------------
@@ -524,11 +840,32 @@ double eval_phi(const Prob& P, const double* X, const double* D, double alpha, d
   reduce_sum(c, pn, fg, c.dscal);
   if (E > 0) {
     GroupGeom gg = group_geom(c, E, d);
-    double* pe = part_buf(c, "phi.pe", std::max(gg.grid, edge_grid(c, E)));
+    double* pe = part_buf(c, "phi.pe", std::max({gg.grid, edge_grid(c, E), c.sm_count * 64}));
     int nb = gg.grid;
     Ctx::Timer tm(&c, "phi_edge", (2.0 * E * d + n * d + 4.0 * E) * 8.0);
     if (edge_reg_supported(d)) {
       nb = phi_edge_reg(c, *P.g, Xe, Z, thr, P.rad, d, sigma, P.q, V, nv, pe);
+    } else if (gg.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1) &&
+               std::getenv("CPB_PHI_NOTMA") == nullptr) {
+      const size_t smem = static_cast<size_t>(kMultWarps) * 3 * d * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        CPB_CUDA(cudaFuncSetAttribute(k_phi_edge_t<Q_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kMultWarps * 3 * kMultSmemMaxD * 8));
+        CPB_CUDA(cudaFuncSetAttribute(k_phi_edge_t<Q_L1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kMultWarps * 3 * kMultSmemMaxD * 8));
+        attr = true;
+      }
+      int per_sm = 0;
+      CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_phi_edge_t<Q_L2>, 32 * kMultWarps, smem));
+      nb = std::max(1, std::min(cdiv(E, kMultWarps), c.sm_count * std::max(1, per_sm)));
+      if (P.q == Q_L2)
+        k_phi_edge_t<Q_L2><<<nb, dim3(32, kMultWarps), smem, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, E,
+                                                                    static_cast<int>(d), sigma, V, nv, pe);
+      else
+        k_phi_edge_t<Q_L1><<<nb, dim3(32, kMultWarps), smem, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, E,
+                                                                    static_cast<int>(d), sigma, V, nv, pe);
+      CPB_LAUNCH_CHECK();
     } else {
       k_phi_edge<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, E,
                                                           static_cast<int>(d), sigma, P.q, V, nv, pe);
@@ -695,12 +1032,53 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
   Ctx& c = *P.c;
   const int64_t d = P.d(), n = P.n(), E = P.E();
   GroupGeom ge = group_geom(c, E, d);
-  double* pe = part_buf(c, "mult.pe", 9 * static_cast<size_t>(std::max(ge.grid, edge_grid(c, E))));
+  double* pe = part_buf(c, "mult.pe", 9 * static_cast<size_t>(std::max({ge.grid, edge_grid(c, E), c.sm_count * 64})));
   int nb = ge.grid;
   {
     Ctx::Timer tm(&c, "multiplier", (3.0 * E * d + n * d) * 8.0);
     if (edge_reg_supported(d)) {
       nb = mult_reg(c, *P.g, X, Z, V, ps, thr, P.rad, d, sigma, P.q, pe);
+    } else if (ge.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1) &&
+               std::getenv("CPB_MULT_NOTMA") == nullptr) {
+      const size_t smem = static_cast<size_t>(kMultWarps) * 4 * d * sizeof(double);
+      static bool attr_t = false;
+      if (!attr_t) {
+        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kMultWarps * 4 * kMultSmemMaxD * 8));
+        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kMultWarps * 4 * kMultSmemMaxD * 8));
+        attr_t = true;
+      }
+      int per_sm = 0;
+      CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mult_t<Q_L2>, 32 * kMultWarps, smem));
+      nb = std::max(1, std::min(cdiv(E, kMultWarps), c.sm_count * std::max(1, per_sm)));
+      if (P.q == Q_L2)
+        k_mult_t<Q_L2><<<nb, dim3(32, kMultWarps), smem, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p,
+                                                                P.g->ej.p, E, static_cast<int>(d), sigma, pe);
+      else
+        k_mult_t<Q_L1><<<nb, dim3(32, kMultWarps), smem, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p,
+                                                                P.g->ej.p, E, static_cast<int>(d), sigma, pe);
+      CPB_LAUNCH_CHECK();
+    } else if (ge.gx == 32 && d <= kMultSmemMaxD && (P.q == Q_L2 || P.q == Q_L1)) {
+      const size_t smem = static_cast<size_t>(kMultWarps) * 2 * d * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        CPB_CUDA(cudaFuncSetAttribute(k_mult_s<Q_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kMultWarps * 2 * kMultSmemMaxD * 8));
+        CPB_CUDA(cudaFuncSetAttribute(k_mult_s<Q_L1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kMultWarps * 2 * kMultSmemMaxD * 8));
+        attr = true;
+      }
+      int per_sm = 0;
+      CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mult_s<Q_L2>, 32 * kMultWarps, smem));
+      nb = std::max(1, std::min(cdiv(E, kMultWarps), c.sm_count * std::max(1, per_sm)));
+      if (P.q == Q_L2)
+        k_mult_s<Q_L2><<<nb, dim3(32, kMultWarps), smem, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p,
+                                                                P.g->ej.p, E, static_cast<int>(d), sigma, pe);
+      else
+        k_mult_s<Q_L1><<<nb, dim3(32, kMultWarps), smem, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p,
+                                                                P.g->ej.p, E, static_cast<int>(d), sigma, pe);
+      CPB_LAUNCH_CHECK();
     } else {
       k_mult<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p, P.g->ej.p, E,
                                                       static_cast<int>(d), sigma, P.q, pe);
