@@ -131,6 +131,20 @@ void cp_data_destroy(cp_data* data);
 /* ---- graph (graph.hpp:23-92) --------------------------------------------- */
 /* compute_knn_weights(data, k, phi) (graph.hpp:58; graph.cpp:75-114) */
 int cp_knn_graph(cp_ctx* ctx, const cp_data* data, int64_t k, double phi, cp_graph** out);
+/* Row-sharded kNN (graph.cpp:79-88 per row).  kd_dev and
+ * kj_dev are DEVICE pointers to n x k arrays (double, int32): the k nearest
+ * (d2, j) of every row in [r0, r1), ascending by (d2, j), are written at
+ * their global row positions; other rows are untouched.  Bit-identical to the
+ * rows cp_knn_graph computes, whatever the row range. */
+int cp_knn_rows(cp_ctx* ctx, const cp_data* data, int64_t k, int64_t r0, int64_t r1, double* kd_dev,
+                int32_t* kj_dev);
+/* The graph from complete per-row lists (DEVICE pointers, n x k): union of
+ * (min, max) pairs, sorted, unique, w = exp(-phi d2) (graph.cpp:89-111). */
+int cp_graph_from_knn(cp_ctx* ctx, int64_t n, int64_t k, double phi, const double* kd_dev, const int32_t* kj_dev,
+                      cp_graph** out);
+/* Host-only: the query rows [r0, r1) of `rank` among `nranks` for the
+ * row-sharded kNN: ceil(n / nranks) rows per rank, the last rank short. */
+int cp_shard_rows(int64_t n, int nranks, int rank, int64_t* r0, int64_t* r1);
 /* WeightedGraph(n, edges): sorts and validates (graph.hpp:29-31; graph.cpp:25-45) */
 int cp_graph_from_edges(cp_ctx* ctx, int64_t n, const int64_t* i, const int64_t* j, const double* w, int64_t E,
                         cp_graph** out);

@@ -356,6 +356,34 @@ int orc_mixture(const double* centers, int64_t d, int64_t m, double spread, int6
     put(gaussian_mixture(c, spread, per_center, seed), out);
   });
 }
+// Per-row k nearest (d2, j) lists of rows [r0, r1) (graph.cpp:79-88): all j != i,
+// partial_sort of (dist, j) pairs; kd/kj are (r1 - r0) x k, row-major.
+int orc_knn_rows(const double* A, int64_t d, int64_t n, int64_t k, int64_t r0, int64_t r1, double* kd,
+                 int64_t* kj) {
+  return guard([&] {
+    if (k < 1 || k > n - 1 || r0 < 0 || r1 > n || r0 > r1) throw std::invalid_argument("orc_knn_rows: bad range");
+    Mat Am = wrap(A, d, n);
+    std::vector<std::pair<double, Index>> cand;
+    for (Index i = r0; i < r1; ++i) {
+      cand.clear();
+      for (Index j = 0; j < n; ++j) {
+        if (j == i) continue;
+        const double* x = Am.col(i);
+        const double* y = Am.col(j);
+        cand.emplace_back(esum(d, [&](Index r) {
+                            const double t = x[r] - y[r];
+                            return t * t;
+                          }),
+                          j);
+      }
+      std::partial_sort(cand.begin(), cand.begin() + k, cand.end());
+      for (Index m = 0; m < k; ++m) {
+        kd[(i - r0) * k + m] = cand[static_cast<size_t>(m)].first;
+        kj[(i - r0) * k + m] = cand[static_cast<size_t>(m)].second;
+      }
+    }
+  });
+}
 // ---- CPU-baseline unit costs (bench.py cpu_baseline / --impl reference) ----------
 // Seconds for the kNN of the first `rows` samples against all n (graph.cpp:90-103).
 int orc_time_knn_rows(const double* A, int64_t d, int64_t n, int64_t k, int64_t rows, double* seconds) {

@@ -402,6 +402,16 @@ def gaussian_mixture(centers, spread, per_center, seed):
     return out
 
 
+def knn_rows(A, k, r0, r1):
+    """Per-row k nearest (d2, j) of rows [r0, r1) (graph.cpp:79-88)."""
+    A = _f64(A)
+    n, d = A.shape
+    kd = np.zeros((r1 - r0, k))
+    kj = np.zeros((r1 - r0, k), dtype=np.int64)
+    _check(lib().orc_knn_rows(_dp(A), _ci(d), _ci(n), _ci(k), _ci(r0), _ci(r1), _dp(kd), _ip(kj)))
+    return kd, kj
+
+
 def time_knn_rows(A, k, rows):
     """Seconds for the reference kNN of the first `rows` samples (graph.cpp:90-103)."""
     A = _f64(A)

@@ -11,10 +11,10 @@ mirror of the reference API.
 from .cluspath import (Algorithm, ClusterAssignment, Context, DataMatrix, GammaSchedule, IncidenceOperator,
                        PathOptions, PathResult, PenaltyNorm, ProblemInstance, Solution, SolverConfig, Spacing,
                        TerminationRecord, WeightedGraph, algorithm_from_name, algorithm_name, component_count,
-                       compute_knn_weights, connected_components, default_context, dual_objective, duality_gap,
-                       extract_clusters, flush_l2, generate_gaussian_mixture, kkt_residual, launch_count,
+                       compute_knn_weights, compute_knn_weights_sharded, connected_components, default_context, dual_objective, duality_gap,
+                       extract_clusters, flush_l2, gather_row_lists, knn_rows_into, generate_gaussian_mixture, kkt_residual, launch_count,
                        make_data_matrix, make_schedule, normals, penalty_norm_from_q, timer_start, timer_stop,
-                       primal_objective, project_columns, prox_columns, prox_jacobian_diag, recover_primal, run_path,
+                       primal_objective, project_columns, shard_rows, prox_columns, prox_jacobian_diag, recover_primal, run_path,
                        solve, ssnal_hessian_apply, ssnal_phi_gradient, ssnal_phi_value, two_point_closed_form)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -69,6 +69,9 @@ _SIGS = [
     ("cp_data_create", C.c_int, [VP, D, C.c_int64, C.c_int64, C.POINTER(VP)]),
     ("cp_data_destroy", None, [VP]),
     ("cp_knn_graph", C.c_int, [VP, VP, C.c_int64, C.c_double, C.POINTER(VP)]),
+    ("cp_knn_rows", C.c_int, [VP, VP, C.c_int64, C.c_int64, C.c_int64, VP, VP]),
+    ("cp_graph_from_knn", C.c_int, [VP, C.c_int64, C.c_int64, C.c_double, VP, VP, C.POINTER(VP)]),
+    ("cp_shard_rows", C.c_int, [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("cp_graph_from_edges", C.c_int, [VP, C.c_int64, I64, I64, D, C.c_int64, C.POINTER(VP)]),
     ("cp_graph_destroy", None, [VP]),
     ("cp_graph_nodes", C.c_int64, [VP]),

@@ -299,6 +299,76 @@ def compute_knn_weights(data: DataMatrix, k: int, phi: float) -> WeightedGraph:
     return WeightedGraph(ctx=data.ctx, _handle=h)
 
 
+def shard_rows(n: int, nranks: int, rank: int):
+    """Query rows [r0, r1) of `rank` in the row-sharded kNN (cp_shard_rows)."""
+    r0, r1 = C.c_int64(), C.c_int64()
+    L.check(L.load().cp_shard_rows(int(n), int(nranks), int(rank), C.byref(r0), C.byref(r1)))
+    return r0.value, r1.value
+
+
+def knn_rows_into(data: DataMatrix, k: int, r0: int, r1: int, kd, kj) -> None:
+    """cp_knn_rows: rows [r0, r1) of the per-row kNN lists into the CUDA
+    tensors kd (n x k float64) and kj (n x k int32) at their global rows."""
+    n = data.n
+    if kd.shape[0] < n or kj.shape[0] < n or kd.shape[1] != k or kj.shape[1] != k or not kd.is_cuda or not kj.is_cuda:
+        raise ValueError("knn_rows_into: kd / kj must be CUDA tensors of at least n x k")
+    if str(kd.dtype) != "torch.float64" or str(kj.dtype) != "torch.int32" or not kd.is_contiguous() \
+            or not kj.is_contiguous():
+        raise ValueError("knn_rows_into: kd must be contiguous float64 and kj contiguous int32")
+    L.check(L.load().cp_knn_rows(data.ctx._h, data._h, int(k), int(r0), int(r1), C.c_void_p(kd.data_ptr()),
+                                 C.c_void_p(kj.data_ptr())))
+
+
+def gather_row_lists(n: int, k: int, rows_fn, device, group=None):
+    """Row-sharded kNN lists: this rank fills its rows with
+    ``rows_fn(r0, r1, kd, kj)`` (kd, kj: (n_pad, k) float64 / int32 tensors on
+    `device`), then every rank receives every rank's equal-size row chunk
+    through torch.distributed (NCCL over NVLink on GPUs, gloo on CPU).
+    Returns the complete (n, k) lists, identical on every rank."""
+    import torch
+    import torch.distributed as dist
+    P = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    chunk = -(-n // P)
+    kd = torch.zeros((chunk * P, k), dtype=torch.float64, device=device)
+    kj = torch.zeros((chunk * P, k), dtype=torch.int32, device=device)
+    r0, r1 = shard_rows(n, P, rank)
+    if r1 > r0:
+        rows_fn(r0, r1, kd, kj)
+    if P > 1:
+        mine_d = kd[rank * chunk:(rank + 1) * chunk].contiguous()
+        mine_j = kj[rank * chunk:(rank + 1) * chunk].contiguous()
+        outs_d = [torch.empty_like(mine_d) for _ in range(P)]
+        outs_j = [torch.empty_like(mine_j) for _ in range(P)]
+        dist.all_gather(outs_d, mine_d, group=group)
+        dist.all_gather(outs_j, mine_j, group=group)
+        kd = torch.cat(outs_d)
+        kj = torch.cat(outs_j)
+    return kd[:n], kj[:n]
+
+
+def compute_knn_weights_sharded(data: DataMatrix, k: int, phi: float, group=None) -> WeightedGraph:
+    """compute_knn_weights with the n^2 d distance work split by query-row
+    blocks over the ranks of `group` (one process per GPU, NCCL all-gather of
+    the n x k lists); every rank returns the same graph, bit-identical to
+    compute_knn_weights on one GPU."""
+    import torch
+    n = data.n
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def rows_fn(r0, r1, kd, kj):
+        torch.cuda.synchronize(dev)
+        knn_rows_into(data, k, r0, r1, kd, kj)
+
+    kd, kj = gather_row_lists(n, int(k), rows_fn, dev, group)
+    kd, kj = kd.contiguous(), kj.contiguous()
+    torch.cuda.synchronize(dev)
+    h = C.c_void_p()
+    L.check(L.load().cp_graph_from_knn(data.ctx._h, n, int(k), float(phi), C.c_void_p(kd.data_ptr()),
+                                       C.c_void_p(kj.data_ptr()), C.byref(h)))
+    return WeightedGraph(ctx=data.ctx, _handle=h)
+
+
 class IncidenceOperator:
     """IncidenceOperator (graph.hpp:62-86): X B and Z B^T on the GPU."""
 

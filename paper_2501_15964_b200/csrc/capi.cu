@@ -283,6 +283,39 @@ int cp_knn_graph(cp_ctx* ctx, const cp_data* data, int64_t k, double phi, cp_gra
     *out = g.release();
   });
 }
+int cp_knn_rows(cp_ctx* ctx, const cp_data* data, int64_t k, int64_t r0, int64_t r1, double* kd_dev,
+                int32_t* kj_dev) {
+  return guard(ctx, [&] {
+    need(data, "data");
+    need(kd_dev, "kd");
+    need(kj_dev, "kj");
+    cpb::knn_validate(data->d, k, 0.0);
+    cpb::knn_rows_dev(*ctx->c, data->d, k, r0, r1, kd_dev, kj_dev);
+    ctx->c->sync();
+  });
+}
+int cp_graph_from_knn(cp_ctx* ctx, int64_t n, int64_t k, double phi, const double* kd_dev, const int32_t* kj_dev,
+                      cp_graph** out) {
+  return guard(ctx, [&] {
+    need(kd_dev, "kd");
+    need(kj_dev, "kj");
+    need(out, "out");
+    if (n < 2) cpb::invalid("graph from kNN lists: n must be >= 2");
+    auto g = std::make_unique<cp_graph>();
+    g->g = cpb::graph_from_knn_dev(*ctx->c, n, k, phi, kd_dev, kj_dev);
+    *out = g.release();
+  });
+}
+int cp_shard_rows(int64_t n, int nranks, int rank, int64_t* r0, int64_t* r1) {
+  if (n < 0 || nranks < 1 || rank < 0 || rank >= nranks || !r0 || !r1) {
+    g_err = "cp_shard_rows: invalid arguments";
+    return CP_EINVAL;
+  }
+  const int64_t chunk = (n + nranks - 1) / nranks;
+  *r0 = std::min<int64_t>(n, chunk * rank);
+  *r1 = std::min<int64_t>(n, chunk * (rank + 1));
+  return CP_OK;
+}
 int cp_graph_from_edges(cp_ctx* ctx, int64_t n, const int64_t* i, const int64_t* j, const double* w, int64_t E,
                         cp_graph** out) {
   return guard(ctx, [&] {

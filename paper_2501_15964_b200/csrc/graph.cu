@@ -80,8 +80,8 @@ __device__ __forceinline__ double eigen_finish(double c0, double c1, double c2, 
 // With `rows` set, block b handles query rows rows[32 b ..] (nq of them):
 // the exact pass for the rows the tensor-core path could not settle.
 __global__ void __launch_bounds__(256) k_knn_topk(const double* __restrict__ A, int n, int d, int e2, int k,
-                                                  const int* __restrict__ rows, int nq, double* __restrict__ out_d,
-                                                  int* __restrict__ out_j) {
+                                                  const int* __restrict__ rows, int row_base, int nq,
+                                                  double* __restrict__ out_d, int* __restrict__ out_j) {
   __shared__ double sA[KB_K][KB_M];
   __shared__ double sB[KB_K][KB_N];
   __shared__ double sD[KB_M][KB_N + 1];
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(256) k_knn_topk(const double* __restrict__ A, 
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int lane = tid & 31, warp = tid >> 5;
   const int row0 = blockIdx.x * KB_M;
-  auto qrow = [&](int rr) { return row0 + rr < nq ? (rows ? rows[row0 + rr] : row0 + rr) : n; };
+  auto qrow = [&](int rr) { return row0 + rr < nq ? (rows ? rows[row0 + rr] : row_base + row0 + rr) : n; };
 
   for (int p = tid; p < KB_M * KB_LIST; p += 256) {
     sLd[p / KB_LIST][p % KB_LIST] = CUDART_INF;
@@ -237,6 +237,16 @@ __global__ void k_knn_take(const unsigned long long* __restrict__ keys, const in
 __global__ void k_seg_offsets(int* off, int rows, int n) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t <= rows) off[t] = t * n;
+}
+
+__global__ void k_check_lists(const double* __restrict__ kd, const int* __restrict__ kj, int n, int k, int* bad) {
+  const int64_t total = static_cast<int64_t>(n) * k;
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < total;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = kj[p], i = static_cast<int>(p / k);
+    const double v = kd[p];
+    if (j < 0 || j >= n || j == i || !(v >= 0.0) || !isfinite(v)) *bad = 1;
+  }
 }
 
 // (min, max) pair keys carrying the squared distance.
@@ -544,59 +554,91 @@ std::unique_ptr<Graph> graph_from_edges(Ctx& c, int64_t n, const int64_t* i, con
   return g;
 }
 
-std::unique_ptr<Graph> knn_graph(Ctx& c, const Data& A, int64_t k, double phi) {
-  const int64_t n = A.n, d = A.d;
+void knn_validate(const Data& A, int64_t k, double phi) {
+  const int64_t n = A.n;
   if (k < 1 || k > n - 1)
     invalid("compute_knn_weights: k must satisfy 1 <= k <= n-1, got k=" + std::to_string(k) +
             " with n=" + std::to_string(n));
   if (!(phi >= 0.0) || !std::isfinite(phi)) invalid("compute_knn_weights: phi must be finite and nonnegative");
   if (n >= (1ll << 31) - 1 || n * k >= (1ll << 31) - 1) invalid("compute_knn_weights: problem too large");
+}
+
+// The k nearest (d2, j) of every query row in [r0, r1), ascending (graph.cpp:79-88),
+// into kd/kj at the global row positions (n x k arrays).
+void knn_rows_dev(Ctx& c, const Data& A, int64_t k, int64_t r0, int64_t r1, double* kd, int* kj) {
+  const int64_t n = A.n, d = A.d;
+  if (r0 < 0 || r1 > n || r0 > r1) invalid("knn rows: row range out of bounds");
+  if (r0 == r1) return;
   const int e2 = d >= 4 ? static_cast<int>((d / 4) * 4) : 0;
-  const int64_t NK = n * k;
+  Ctx::Timer tm(&c, "knn_topk", 0.0);
+  if (knn_tc_enabled(c, n, d, k)) {
+    int* ovf = c.buf<int>("knn.ovf", n);
+    const int64_t nov = knn_tc(c, A, k, r0, r1, kd, kj, ovf);
+    if (nov > 0) {
+      k_knn_topk<<<cdiv(nov, KB_M), 256, 0, c.s>>>(A.A.p, static_cast<int>(n), static_cast<int>(d), e2,
+                                                    static_cast<int>(k), ovf, 0, static_cast<int>(nov), kd, kj);
+      CPB_LAUNCH_CHECK();
+    }
+  } else if (k <= KB_LIST) {
+    c.knn_last = {0, 0.0, 0, 0};
+    c.knn_band_rows = 0;
+    k_knn_topk<<<cdiv(r1 - r0, KB_M), 256, 0, c.s>>>(A.A.p, static_cast<int>(n), static_cast<int>(d), e2,
+                                                      static_cast<int>(k), nullptr, static_cast<int>(r0),
+                                                      static_cast<int>(r1 - r0), kd, kj);
+    CPB_LAUNCH_CHECK();
+  } else {
+    c.knn_last = {0, 0.0, 0, 0};
+    c.knn_band_rows = 0;
+    const int64_t rows = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(1) << 26) / n));
+    auto* keys = c.buf<unsigned long long>("knnf.k", rows * n);
+    auto* keys2 = c.buf<unsigned long long>("knnf.k2", rows * n);
+    int* vals = c.buf<int>("knnf.v", rows * n);
+    int* vals2 = c.buf<int>("knnf.v2", rows * n);
+    int* segoff = c.buf<int>("knnf.off", rows + 1);
+    for (int64_t q0 = r0; q0 < r1; q0 += rows) {
+      const int rr = static_cast<int>(std::min(rows, r1 - q0));
+      const int64_t m = static_cast<int64_t>(rr) * n;
+      k_knn_rows<<<std::min(cdiv(m, 256), c.sm_count * 16), 256, 0, c.s>>>(
+          A.A.p, static_cast<int>(n), static_cast<int>(d), e2, static_cast<int>(q0), rr, keys, vals);
+      CPB_LAUNCH_CHECK();
+      k_seg_offsets<<<cdiv(rr + 1, 256), 256, 0, c.s>>>(segoff, rr, static_cast<int>(n));
+      CPB_LAUNCH_CHECK();
+      cub_call(c, "knnf.sort", [&](void* t, size_t& b) {
+        return cub::DeviceSegmentedRadixSort::SortPairs(t, b, keys, keys2, vals, vals2, static_cast<int>(m), rr,
+                                                        segoff, segoff + 1, 0, 64, c.s);
+      });
+      k_knn_take<<<std::min(cdiv(static_cast<int64_t>(rr) * k, 256), c.sm_count * 8), 256, 0, c.s>>>(
+          keys2, vals2, static_cast<int>(n), static_cast<int>(q0), rr, static_cast<int>(k), kd, kj);
+      CPB_LAUNCH_CHECK();
+    }
+  }
+}
+
+std::unique_ptr<Graph> knn_graph(Ctx& c, const Data& A, int64_t k, double phi) {
+  knn_validate(A, k, phi);
+  const int64_t n = A.n, NK = n * k;
   double* kd = c.buf<double>("knn.d", NK);
   int* kj = c.buf<int>("knn.j", NK);
-  {
-    Ctx::Timer tm(&c, "knn_topk", 0.0);
-    if (knn_tc_enabled(c, n, d, k)) {
-      int* ovf = c.buf<int>("knn.ovf", n);
-      const int64_t nov = knn_tc(c, A, k, kd, kj, ovf);
-      if (nov > 0) {
-        k_knn_topk<<<cdiv(nov, KB_M), 256, 0, c.s>>>(A.A.p, static_cast<int>(n), static_cast<int>(d), e2,
-                                                      static_cast<int>(k), ovf, static_cast<int>(nov), kd, kj);
-        CPB_LAUNCH_CHECK();
-      }
-    } else if (k <= KB_LIST) {
-      c.knn_last = {0, 0.0, 0, 0};
-      c.knn_band_rows = 0;
-      k_knn_topk<<<cdiv(n, KB_M), 256, 0, c.s>>>(A.A.p, static_cast<int>(n), static_cast<int>(d), e2,
-                                                  static_cast<int>(k), nullptr, static_cast<int>(n), kd, kj);
-      CPB_LAUNCH_CHECK();
-    } else {
-      c.knn_last = {0, 0.0, 0, 0};
-      c.knn_band_rows = 0;
-      const int64_t rows = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(1) << 26) / n));
-      auto* keys = c.buf<unsigned long long>("knnf.k", rows * n);
-      auto* keys2 = c.buf<unsigned long long>("knnf.k2", rows * n);
-      int* vals = c.buf<int>("knnf.v", rows * n);
-      int* vals2 = c.buf<int>("knnf.v2", rows * n);
-      int* segoff = c.buf<int>("knnf.off", rows + 1);
-      for (int64_t r0 = 0; r0 < n; r0 += rows) {
-        const int rr = static_cast<int>(std::min(rows, n - r0));
-        const int64_t m = static_cast<int64_t>(rr) * n;
-        k_knn_rows<<<std::min(cdiv(m, 256), c.sm_count * 16), 256, 0, c.s>>>(
-            A.A.p, static_cast<int>(n), static_cast<int>(d), e2, static_cast<int>(r0), rr, keys, vals);
-        CPB_LAUNCH_CHECK();
-        k_seg_offsets<<<cdiv(rr + 1, 256), 256, 0, c.s>>>(segoff, rr, static_cast<int>(n));
-        CPB_LAUNCH_CHECK();
-        cub_call(c, "knnf.sort", [&](void* t, size_t& b) {
-          return cub::DeviceSegmentedRadixSort::SortPairs(t, b, keys, keys2, vals, vals2, static_cast<int>(m), rr,
-                                                          segoff, segoff + 1, 0, 64, c.s);
-        });
-        k_knn_take<<<std::min(cdiv(static_cast<int64_t>(rr) * k, 256), c.sm_count * 8), 256, 0, c.s>>>(
-            keys2, vals2, static_cast<int>(n), static_cast<int>(r0), rr, static_cast<int>(k), kd, kj);
-        CPB_LAUNCH_CHECK();
-      }
-    }
+  knn_rows_dev(c, A, k, 0, n, kd, kj);
+  return graph_from_knn_dev(c, n, k, phi, kd, kj);
+}
+
+// Union of the per-row lists as (min, max) pairs, sorted and unique, with
+// w = exp(-phi d2), dropping underflowed weights (graph.cpp:89-111).
+std::unique_ptr<Graph> graph_from_knn_dev(Ctx& c, int64_t n, int64_t k, double phi, const double* kd, const int* kj) {
+  if (!(phi >= 0.0) || !std::isfinite(phi)) invalid("compute_knn_weights: phi must be finite and nonnegative");
+  if (k < 1 || k > n - 1 || n >= (1ll << 31) - 1 || n * k >= (1ll << 31) - 1)
+    invalid("compute_knn_weights: bad list shape");
+  const int64_t NK = n * k;
+  {  // every entry must be a neighbour id != its row with a finite d2 >= 0
+    int* bad = c.buf<int>("knn.bad", 1);
+    CPB_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.s));
+    k_check_lists<<<std::min(cdiv(NK, 256), c.sm_count * 8), 256, 0, c.s>>>(kd, kj, static_cast<int>(n),
+                                                                             static_cast<int>(k), bad);
+    CPB_LAUNCH_CHECK();
+    int hb = 0;
+    d2h(c, &hb, bad, sizeof(int));
+    if (hb) invalid("graph from kNN lists: entry out of range, self-loop or non-finite distance");
   }
   // union of (min, max) pairs, sorted and unique, with weights
   auto* key = c.buf<unsigned long long>("knn.key", NK);

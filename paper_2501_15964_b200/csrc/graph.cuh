@@ -38,7 +38,12 @@ std::unique_ptr<Graph> knn_graph(Ctx& c, const Data& A, int64_t k, double phi);
 // (n x k, ascending (d2, j)) for every row it can certify and lists the
 // others in ovf; returns how many (they need the exact tile kernel).
 bool knn_tc_enabled(Ctx& c, int64_t n, int64_t d, int64_t k);
-int64_t knn_tc(Ctx& c, const Data& A, int64_t k, double* kd, int* kj, int* ovf);
+int64_t knn_tc(Ctx& c, const Data& A, int64_t k, int64_t r0, int64_t r1, double* kd, int* kj, int* ovf);
+// Row-sharded kNN: each rank fills rows [r0, r1) of the n x k
+// lists, the lists are all-gathered, and every rank builds the same graph.
+void knn_validate(const Data& A, int64_t k, double phi);
+void knn_rows_dev(Ctx& c, const Data& A, int64_t k, int64_t r0, int64_t r1, double* kd, int* kj);
+std::unique_ptr<Graph> graph_from_knn_dev(Ctx& c, int64_t n, int64_t k, double phi, const double* kd, const int* kj);
 // Builds CSR/order for a graph whose ei/ej/w/d2 (sorted, validated) are set.
 void finalize_graph(Ctx& c, Graph& g);
 

@@ -134,7 +134,7 @@ template <bool THRESH>
 __global__ void __launch_bounds__(192, 1)
     k_knn_tc(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
              const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
-             const float* __restrict__ n32, int n, int kblocks, int ntiles, int nseg, float* __restrict__ cd,
+             const float* __restrict__ n32, int rbase, int n, int kblocks, int ntiles, int nseg, float* __restrict__ cd,
              int* __restrict__ cj, const int* __restrict__ qrows, const float* __restrict__ qlim, int nq, int caps,
              int* __restrict__ ccount) {
   extern __shared__ unsigned char smem_raw[];
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row0 = blockIdx.x * TM, seg = blockIdx.y;
+  const int row0 = rbase + blockIdx.x * TM, seg = blockIdx.y;
   const int t0 = static_cast<int>(static_cast<int64_t>(ntiles) * seg / nseg);
   const int t1 = static_cast<int>(static_cast<int64_t>(ntiles) * (seg + 1) / nseg);
 
@@ -220,7 +220,8 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ===== epilogue: thread t owns query row row0 + t (TMEM lane t) =====
+    // ===== epilogue: thread t owns query row row0 + t (TMEM lane t); LIST mode
+    // rows are [rbase, n), THRESH mode local rows index qrows =====
     const int t = threadIdx.x, lr = row0 + t;
     int row;
     float lim = CUDART_INF_F;
@@ -399,8 +400,8 @@ __device__ __forceinline__ void flush_worst(float wmax, float* worst) {
 // to the exact tile kernel (hard).
 __global__ void __launch_bounds__(RC_WARPS * 32)
     k_knn_recheck(const double* __restrict__ A, const float* __restrict__ cd, const int* __restrict__ cj,
-                  const double* __restrict__ n64, const double* __restrict__ max_n2, int n, int d, int e2, int k,
-                  int nseg, double* __restrict__ kd, int* __restrict__ kj, int* __restrict__ cnts,
+                  const double* __restrict__ n64, const double* __restrict__ max_n2, int r0, int n, int d, int e2,
+                  int k, int nseg, double* __restrict__ kd, int* __restrict__ kj, int* __restrict__ cnts,
                   int* __restrict__ ovf, float* __restrict__ ovf_lim, int* __restrict__ hard,
                   float* __restrict__ worst) {
   static_assert(KC == 32, "one list entry per lane and segment");
@@ -410,7 +411,7 @@ __global__ void __launch_bounds__(RC_WARPS * 32)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const double M = sqrt(*max_n2);
   float wmax = 0.0f;
-  for (int row = blockIdx.x * RC_WARPS + w; row < n; row += gridDim.x * RC_WARPS) {
+  for (int row = r0 + blockIdx.x * RC_WARPS + w; row < n; row += gridDim.x * RC_WARPS) {
     float v[MAXSEG];
     int j[MAXSEG];
 #pragma unroll
@@ -569,10 +570,11 @@ bool knn_tc_enabled(Ctx& c, int64_t n, int64_t d, int64_t k) {
   return c.sm_major == 10 && d >= 16 && n >= 2048 && k <= KC - 8 && n < (int64_t(1) << 30) / MAXSEG;
 }
 
-int64_t knn_tc(Ctx& c, const Data& A, int64_t k, double* kd, int* kj, int* hard) {
+int64_t knn_tc(Ctx& c, const Data& A, int64_t k, int64_t r0_, int64_t r1_, double* kd, int* kj, int* hard) {
   const int n = static_cast<int>(A.n), d = static_cast<int>(A.d);
+  const int r0 = static_cast<int>(r0_), r1 = static_cast<int>(r1_);
   const int dp = (d + 3) & ~3, e2 = (d / 4) * 4;
-  const int ntiles = cdiv(n, TN), nrb = cdiv(n, TM), kblocks = cdiv(dp, TK);
+  const int ntiles = cdiv(n, TN), nrb = cdiv(r1 - r0, TM), kblocks = cdiv(dp, TK);
   const int npad = ntiles * TN;
   // column segments so that blocks * nseg fills the SMs (one CTA per SM)
   auto pick_seg = [&](int blocks0) {
@@ -614,8 +616,8 @@ int64_t knn_tc(Ctx& c, const Data& A, int64_t k, double* kd, int* kj, int* hard)
   }
   {
     // "bytes" of the dense contraction = its algorithmic flops 2 n^2 d (reported as TFLOP/s)
-    Ctx::Timer tm(&c, "knn_gemm", 2.0 * static_cast<double>(n) * n * d);
-    k_knn_tc<false><<<dim3(nrb, nseg), 192, SMEM_BYTES, c.s>>>(mhi, mlo, mhi, mlo, n32, n, kblocks, ntiles, nseg, cd,
+    Ctx::Timer tm(&c, "knn_gemm", 2.0 * static_cast<double>(r1 - r0) * n * d);
+    k_knn_tc<false><<<dim3(nrb, nseg), 192, SMEM_BYTES, c.s>>>(mhi, mlo, mhi, mlo, n32, r0, r1, kblocks, ntiles, nseg, cd,
                                                                cj, nullptr, nullptr, 0, KC, nullptr);
     CPB_LAUNCH_CHECK();
   }
@@ -623,8 +625,8 @@ int64_t knn_tc(Ctx& c, const Data& A, int64_t k, double* kd, int* kj, int* hard)
   CPB_CUDA(cudaMemsetAsync(worst, 0, sizeof(float), c.s));
   {
     Ctx::Timer tm(&c, "knn_recheck", 0.0);
-    k_knn_recheck<<<std::min(cdiv(n, RC_WARPS), c.sm_count * 8), RC_WARPS * 32, 0, c.s>>>(
-        A.A.p, cd, cj, n64, mx, n, d, e2, static_cast<int>(k), nseg, kd, kj, cnts, ovf, ovf_lim, hard, worst);
+    k_knn_recheck<<<std::min(cdiv(r1 - r0, RC_WARPS), c.sm_count * 8), RC_WARPS * 32, 0, c.s>>>(
+        A.A.p, cd, cj, n64, mx, r0, r1, d, e2, static_cast<int>(k), nseg, kd, kj, cnts, ovf, ovf_lim, hard, worst);
     CPB_LAUNCH_CHECK();
   }
   int h[2] = {0, 0};
@@ -647,7 +649,7 @@ int64_t knn_tc(Ctx& c, const Data& A, int64_t k, double* kd, int* kj, int* hard)
     CUtensorMap qmh, qml;
     make_map(&qmh, qhi, dp, nq);
     make_map(&qml, qlo, dp, nq);
-    k_knn_tc<true><<<dim3(qrb, qseg), 192, SMEM_BYTES, c.s>>>(qmh, qml, mhi, mlo, n32, n, kblocks, ntiles, qseg, td,
+    k_knn_tc<true><<<dim3(qrb, qseg), 192, SMEM_BYTES, c.s>>>(qmh, qml, mhi, mlo, n32, 0, n, kblocks, ntiles, qseg, td,
                                                               tj, ovf, ovf_lim, nq, caps, tc);
     CPB_LAUNCH_CHECK();
     k_knn_recheck_t<<<std::min(cdiv(nq, RC_WARPS), c.sm_count * 8), RC_WARPS * 32, 0, c.s>>>(

@@ -135,6 +135,37 @@ def test_knn_tensor_core_overflow_rows(cp, orc):
     assert np.array_equal(ti, oi) and np.array_equal(tj, oj) and np.array_equal(td2, od2)
 
 
+@pytest.mark.parametrize("n_per,d,k,tc", [(1000, 64, 10, True), (60, 5, 4, False), (700, 33, 40, False)])
+def test_knn_rows_sharded_bitwise(cp, orc, n_per, d, k, tc):
+    """Row blocks computed separately (as the ranks of the sharded kNN do) and
+    assembled give the single-call graph bit for bit."""
+    import torch
+    A = mixture(orc, n_per, d)
+    n = len(A)
+    data = cp.DataMatrix(A)
+    g1 = cp.compute_knn_weights(data, k, 0.5)
+    assert cp.default_context().knn_info()["tensor_cores"] == int(tc)
+    kd = torch.zeros((n, k), dtype=torch.float64, device="cuda")
+    kj = torch.zeros((n, k), dtype=torch.int32, device="cuda")
+    for r in range(3):
+        r0, r1 = cp.shard_rows(n, 3, r)
+        cp.knn_rows_into(data, k, r0, r1, kd, kj)
+    od, oj = orc.knn_rows(A, k, 0, min(n, 64))
+    assert np.array_equal(kd[:64].cpu().numpy(), od) and np.array_equal(kj[:64].cpu().numpy(), oj)
+    g2 = cp.compute_knn_weights_sharded(data, k, 0.5)  # world 1: one block, same assembly path
+    for g in (g2,):
+        for a, b in zip(g.arrays(), g1.arrays()):
+            assert np.array_equal(a, b)
+    bad = kj.clone()
+    bad[5, 0] = 5  # self loop
+    import ctypes as C
+    from paper_2501_15964_b200 import _lib as L
+    h = C.c_void_p()
+    rc = L.load().cp_graph_from_knn(cp.default_context()._h, n, k, 0.5, C.c_void_p(kd.data_ptr()),
+                                    C.c_void_p(bad.data_ptr()), C.byref(h))
+    assert rc == 1
+
+
 def test_data_validation(cp):
     bad = np.ones((3, 2))
     bad[0, 0] = np.inf
