@@ -39,10 +39,11 @@ Mat wrap(const double* p, Index r, Index c) {
 void put(const Mat& m, double* p) {
   if (m.size()) std::memcpy(p, m.v.data(), sizeof(double) * static_cast<size_t>(m.size()));
 }
-Norm nq(int q) {
+Norm nq(int q) {  // 0 encodes q = infinity (no reference counterpart)
+  if (q == 0) return Norm::linf;
   if (q == 1) return Norm::l1;
   if (q == 2) return Norm::l2;
-  throw std::invalid_argument("penalty norm exponent must be 1 or 2, got " + std::to_string(q));
+  throw std::invalid_argument("penalty norm exponent must be 1, 2 or 0 (infinity), got " + std::to_string(q));
 }
 
 }  // namespace

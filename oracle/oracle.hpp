@@ -124,7 +124,17 @@ std::vector<Index> connected_components(const Graph& g);  // graph.cpp:169-196
 Index component_count(const std::vector<Index>& labels);
 
 // ---- prox (prox.hpp, prox.cpp) ---------------------------------------------
-enum class Norm { l1 = 1, l2 = 2 };
+// linf (q = infinity) has no reference implementation (prox.cpp:17-21 rejects
+// it): parity unpinned; the math restated here is SURVEY.md §8(c):
+//   prox_{t||.||inf}(v) = v - Pi_{B1(t)}(v) = clamp(v, -theta, theta),
+//   Pi_{B1(t)}(v)       = sign(v) max(|v| - theta, 0) when ||v||_1 > t,
+// theta from the sort-based l1-ball threshold; outside the ball the Clarke
+// Jacobian element of the projection is diag(1_S) - s_S s_S^T / |S|.
+enum class Norm { linf = 0, l1 = 1, l2 = 2 };
+// l1-ball projection threshold: theta >= 0 with sum max(|v| - theta, 0) = t
+// when ||v||_1 > t (sorted |v|, largest feasible support), else -1; *count =
+// #{|v_i| > theta}.
+double l1_theta(const double* v, Index n, double t, Index* count);
 double norm_value(const double* v, Index n, Norm q);
 double dual_norm_value(const double* v, Index n, Norm q);
 void prox_norm_into(const double* v, Index n, double t, Norm q, double* out);
@@ -135,7 +145,9 @@ struct ProxJac {
   Norm q = Norm::l2;
   double alpha = 0.0, beta = 0.0;
   std::vector<double> dir;     // q=2 rank-one direction
-  std::vector<char> active;    // q=1 mask
+  std::vector<char> active;    // q=1 mask; q=inf support S = {|v| > theta}
+  double theta = -1.0;         // q=inf: l1-ball threshold (< 0: v inside the ball)
+  Index support = 0;           // q=inf: |S|
   void apply(const double* w, Index n, double* out) const;
   double diag(Index r) const;
 };

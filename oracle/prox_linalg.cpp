@@ -3,7 +3,9 @@
 // block PCG, power iteration, the ADMM factor) of the reference.
 #include "oracle.hpp"
 
+#include <algorithm>
 #include <deque>
+#include <functional>
 
 namespace oracle {
 
@@ -14,12 +16,38 @@ void check_t(double t, const char* what) {
 double sgn(double x) { return static_cast<double>((x > 0.0) - (x < 0.0)); }  // Eigen's sign()
 }  // namespace
 
-// prox.cpp:25-31
+// prox.cpp:25-31 (+ q = inf: ||.||_inf with dual ||.||_1)
 double norm_value(const double* v, Index n, Norm q) {
+  if (q == Norm::linf) return max_abs(v, n);
   return q == Norm::l1 ? esum(n, [&](Index k) { return std::abs(v[k]); }) : norm2(v, n);
 }
 double dual_norm_value(const double* v, Index n, Norm q) {
+  if (q == Norm::linf) return esum(n, [&](Index k) { return std::abs(v[k]); });
   return q == Norm::l1 ? max_abs(v, n) : norm2(v, n);
+}
+
+double l1_theta(const double* v, Index n, double t, Index* count) {
+  double s1 = 0.0;
+  for (Index k = 0; k < n; ++k) s1 += std::abs(v[k]);
+  if (!(s1 > t)) {
+    if (count) *count = 0;
+    return -1.0;
+  }
+  std::vector<double> u(static_cast<size_t>(n));
+  for (Index k = 0; k < n; ++k) u[static_cast<size_t>(k)] = std::abs(v[k]);
+  std::sort(u.begin(), u.end(), std::greater<double>());
+  double cs = 0.0, theta = u[0] - t;  // support of one element when no larger support is feasible
+  for (Index j = 0; j < n; ++j) {
+    cs += u[static_cast<size_t>(j)];
+    const double th = (cs - t) / static_cast<double>(j + 1);
+    if (u[static_cast<size_t>(j)] - th > 0.0) theta = th;
+  }
+  if (count) {
+    Index c = 0;
+    for (Index k = 0; k < n; ++k) c += std::abs(v[k]) > theta ? 1 : 0;
+    *count = c;
+  }
+  return theta;
 }
 
 // prox.cpp:33-45
@@ -33,6 +61,9 @@ void prox_norm_into(const double* v, Index n, double t, Norm q, double* out) {
       const double s = 1.0 - t / nv;
       for (Index k = 0; k < n; ++k) out[k] = s * v[k];
     }
+  } else if (q == Norm::linf) {
+    const double th = l1_theta(v, n, t, nullptr);
+    for (Index k = 0; k < n; ++k) out[k] = th < 0.0 ? 0.0 : std::max(std::min(v[k], th), -th);
   } else {
     for (Index k = 0; k < n; ++k) out[k] = sgn(v[k]) * std::max(std::abs(v[k]) - t, 0.0);
   }
@@ -49,6 +80,9 @@ void project_dual_ball_into(const double* z, Index n, double r, Norm q, double* 
       const double s = r / nz;
       for (Index k = 0; k < n; ++k) out[k] = s * z[k];
     }
+  } else if (q == Norm::linf) {
+    const double th = l1_theta(z, n, r, nullptr);
+    for (Index k = 0; k < n; ++k) out[k] = th < 0.0 ? z[k] : sgn(z[k]) * std::max(std::abs(z[k]) - th, 0.0);
   } else {
     for (Index k = 0; k < n; ++k) out[k] = std::max(std::min(z[k], r), -r);
   }
@@ -80,10 +114,26 @@ void ProxJac::apply(const double* w, Index n, double* out) const {
     return;
   }
   if (static_cast<Index>(active.size()) != n) throw std::invalid_argument("ProxJacobian::apply: size mismatch");
+  if (q == Norm::linf) {  // M = I - (diag(1_S) - s s^T / |S|), or 0 inside the ball
+    if (theta < 0.0) {
+      for (Index k = 0; k < n; ++k) out[k] = 0.0;
+      return;
+    }
+    double c = 0.0;
+    for (Index k = 0; k < n; ++k) c += dir[static_cast<size_t>(k)] * w[k];
+    const double b = support > 0 ? c / static_cast<double>(support) : 0.0;
+    for (Index k = 0; k < n; ++k)
+      out[k] = active[static_cast<size_t>(k)] ? b * dir[static_cast<size_t>(k)] : w[k];
+    return;
+  }
   for (Index k = 0; k < n; ++k) out[k] = active[static_cast<size_t>(k)] ? w[k] : 0.0;
 }
 double ProxJac::diag(Index r) const {
   if (q == Norm::l2) return alpha + (beta != 0.0 ? beta * dir[static_cast<size_t>(r)] * dir[static_cast<size_t>(r)] : 0.0);
+  if (q == Norm::linf) {
+    if (theta < 0.0) return 0.0;
+    return active[static_cast<size_t>(r)] ? 1.0 / static_cast<double>(support) : 1.0;
+  }
   return active[static_cast<size_t>(r)] ? 1.0 : 0.0;
 }
 
@@ -104,6 +154,16 @@ ProxJac prox_jacobian(const double* v, Index n, double t, Norm q) {
       J.beta = t / (nv * nv * nv);
       J.dir.assign(v, v + n);
     }
+  } else if (q == Norm::linf) {
+    J.theta = l1_theta(v, n, t, &J.support);
+    J.active.assign(static_cast<size_t>(n), 0);
+    J.dir.assign(static_cast<size_t>(n), 0.0);
+    if (J.theta >= 0.0)
+      for (Index k = 0; k < n; ++k)
+        if (std::abs(v[k]) > J.theta) {
+          J.active[static_cast<size_t>(k)] = 1;
+          J.dir[static_cast<size_t>(k)] = sgn(v[k]);
+        }
   } else {
     J.active.resize(static_cast<size_t>(n));
     for (Index k = 0; k < n; ++k) J.active[static_cast<size_t>(k)] = std::abs(v[k]) > t;
