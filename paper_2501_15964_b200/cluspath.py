@@ -16,6 +16,7 @@ from __future__ import annotations
 import bisect
 import ctypes as C
 import enum
+import math
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -422,16 +423,31 @@ def component_count(labels) -> int:
 # ---- prox.hpp ----------------------------------------------------------------
 
 class PenaltyNorm(enum.IntEnum):
+    """prox.hpp:8 PenaltyNorm{l1, l2}, extended with linf (q = infinity, code 0;
+    no reference counterpart)."""
+    linf = 0
     l1 = 1
     l2 = 2
 
 
-def penalty_norm_from_q(q: int) -> PenaltyNorm:
+def penalty_norm_from_q(q) -> PenaltyNorm:
+    """q in {1, 2} as the reference (prox.cpp:17-21), plus q = inf / "inf"."""
     if q == 1:
         return PenaltyNorm.l1
     if q == 2:
         return PenaltyNorm.l2
-    raise ValueError(f"penalty norm exponent must be 1 or 2, got {q}")
+    if (isinstance(q, float) and math.isinf(q) and q > 0) or (isinstance(q, str) and q.lower() in ("inf", "linf")):
+        return PenaltyNorm.linf
+    raise ValueError(f"penalty norm exponent must be 1, 2 or inf, got {q}")
+
+
+def _qcode(norm) -> int:
+    """C-ABI code of a penalty norm: PenaltyNorm / 0, 1, 2 / inf / "inf"."""
+    if isinstance(norm, PenaltyNorm):
+        return int(norm)
+    if isinstance(norm, (int, np.integer)) and int(norm) in (0, 1, 2):
+        return int(norm)
+    return int(penalty_norm_from_q(norm))
 
 
 def _cols_call(fn, q, V, t, ctx):
@@ -449,17 +465,17 @@ def _cols_call(fn, q, V, t, ctx):
 
 def prox_columns(V, thresholds, norm=PenaltyNorm.l2, ctx=None):
     """prox_columns_into (prox.cpp:73-80): per-column prox of t_l ||.||_q."""
-    return _cols_call(L.load().cp_prox_columns, int(norm), V, thresholds, ctx)
+    return _cols_call(L.load().cp_prox_columns, _qcode(norm), V, thresholds, ctx)
 
 
 def project_columns(Z, radii, norm=PenaltyNorm.l2, ctx=None):
     """project_columns (prox.cpp:82-93): per-column dual-ball projection."""
-    return _cols_call(L.load().cp_project_columns, int(norm), Z, radii, ctx)
+    return _cols_call(L.load().cp_project_columns, _qcode(norm), Z, radii, ctx)
 
 
 def prox_jacobian_diag(V, thresholds, norm=PenaltyNorm.l2, ctx=None):
     """ProxJacobian::diag per column (prox.cpp:106-132)."""
-    return _cols_call(L.load().cp_prox_jacobian_diag, int(norm), V, thresholds, ctx)
+    return _cols_call(L.load().cp_prox_jacobian_diag, _qcode(norm), V, thresholds, ctx)
 
 
 # ---- solvers.hpp ---------------------------------------------------------------
@@ -550,7 +566,7 @@ class ProblemInstance:
             raise ValueError(f"instance: graph has {graph.nodes()} nodes for {data.n} samples")
         if not (gamma >= 0.0) or not np.isfinite(gamma):
             raise ValueError("instance: gamma must be finite and >= 0")
-        self.data, self.graph, self.gamma, self.norm = data, graph, float(gamma), int(norm)
+        self.data, self.graph, self.gamma, self.norm = data, graph, float(gamma), _qcode(norm)
         self.B = IncidenceOperator(graph)
 
     def penalty_radii(self):
@@ -723,7 +739,7 @@ def run_path(data: DataMatrix, graph: WeightedGraph, norm, schedule: GammaSchedu
     terms = (L.TerminationC * T)()
     cfg = config.to_c()
     opt = L.PathOptionsC(int(options.warm_start), int(options.require_connected), float(options.fuse_tol))
-    L.check(L.load().cp_run_path(data.ctx._h, data._h, graph._h, int(norm), _dp(gam), T, C.byref(cfg), C.byref(opt),
+    L.check(L.load().cp_run_path(data.ctx._h, data._h, graph._h, _qcode(norm), _dp(gam), T, C.byref(cfg), C.byref(opt),
                                  _dp(X), _dp(Z), _ip(lab), _ip(K), terms))
     stats = [TerminationRecord.from_c(t) for t in terms]
     sols = [Solution(X[t] if X is not None else None, Z[t] if Z is not None else None, stats[t]) for t in range(T)]

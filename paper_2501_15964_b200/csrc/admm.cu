@@ -10,6 +10,7 @@
 
 #include "gather.cuh"
 #include "solve.cuh"
+#include "linf.cuh"
 
 namespace cpb {
 
@@ -55,7 +56,7 @@ __global__ void k_admm_edge(const double* __restrict__ X, double* __restrict__ U
     double* lam = L + row_ * d;
     double* zc = Zc + row_ * d;
     const double rl = rad[row_], tl = rl / rho;
-    if (q == 2) {
+    if (q == Q_L2) {
       double vv = 0.0;
       for (int f = threadIdx.x; f < d; f += blockDim.x) {
         const double v = (xa[f] - xb[f]) + lam[f] / rho;
@@ -76,6 +77,17 @@ __global__ void k_admm_edge(const double* __restrict__ X, double* __restrict__ U
       const double nl = sqrt(group_sum(ll, gm));
       const double sc = rl / nl;
       for (int f = threadIdx.x; f < d; f += blockDim.x) zc[f] = (nl <= rl) ? lam[f] : sc * lam[f];
+    } else if (q == Q_LINF) {
+      int cnt;
+      const double thv = linf_theta([&](int f) { return (xa[f] - xb[f]) + lam[f] / rho; }, d, tl, gm, &cnt);
+      for (int f = threadIdx.x; f < d; f += blockDim.x) {
+        const double x = xa[f] - xb[f];
+        const double un = thv < 0.0 ? 0.0 : clampd(x + lam[f] / rho, thv);
+        u[f] = un;
+        lam[f] = lam[f] + rho * (x - un);
+      }
+      const double thl = linf_theta([&](int f) { return lam[f]; }, d, rl, gm, &cnt);
+      for (int f = threadIdx.x; f < d; f += blockDim.x) zc[f] = thl < 0.0 ? lam[f] : soft(lam[f], thl);
     } else {
       for (int f = threadIdx.x; f < d; f += blockDim.x) {
         const double x = xa[f] - xb[f];

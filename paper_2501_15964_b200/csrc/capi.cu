@@ -49,7 +49,8 @@ void need(const void* p, const char* what) {
   if (!p) cpb::invalid(std::string(what) + " must not be null");
 }
 void check_q(int q) {
-  if (q != 1 && q != 2) cpb::invalid("penalty norm exponent must be 1 or 2, got " + std::to_string(q));
+  if (q != 0 && q != 1 && q != 2)
+    cpb::invalid("penalty norm exponent must be 1, 2 or 0 (infinity), got " + std::to_string(q));
 }
 
 double* upload(cpb::Ctx& c, const char* name, const double* h, int64_t count) {
@@ -503,7 +504,7 @@ double phi_at(cpb::Prob& P, const double* Z, double sigma, const double* X, doub
   double* dz = upload(c, "api.z", Z, d * E);
   *thr = c.buf<double>("api.thr", E + 1);
   *V = c.buf<double>("api.V", d * E + 1);
-  *nv = c.buf<double>("api.nv", E + 1);
+  *nv = c.buf<double>("api.nv", 2 * E + 1);
   cpb::make_thr(c, E, P.rad, sigma, *thr);
   const double zz = cpb::dot_dev(c, dz, dz, d * E);
   return cpb::eval_phi(P, *dx, nullptr, 0.0, nullptr, dz, sigma, *thr, zz, *V, *nv);

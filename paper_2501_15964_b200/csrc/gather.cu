@@ -247,9 +247,10 @@ __global__ void __launch_bounds__(256) k_g_grad(const double* __restrict__ X, co
     const int cnt = min(32, p1 - p);
     const int my_e = lane < cnt ? adj_e[p + lane] : 0;
     const int my_o = lane < cnt ? adj_o[p + lane] : 0;
-    const double my_s = lane < cnt ? (q == 2 ? ps[my_e] : thr[my_e]) : 0.0;
+    // q = 0 (infinity): ps = theta, jbe = 1/|S| (k_jac)
+    const double my_s = lane < cnt ? ((q == 2 || q == 0) ? ps[my_e] : thr[my_e]) : 0.0;
     const double my_a = (lane < cnt && q == 2) ? jal[my_e] : 0.0;
-    const double my_b = (lane < cnt && q == 2) ? jbe[my_e] : 0.0;
+    const double my_b = (lane < cnt && (q == 2 || q == 0)) ? jbe[my_e] : 0.0;
     for (int u0 = 0; u0 < cnt; u0 += kEB) {
       int le[kEB];
       bool pl[kEB];
@@ -281,6 +282,10 @@ __global__ void __launch_bounds__(256) k_g_grad(const double* __restrict__ X, co
           if (q == 2) {
             uu = val - es[u] * val;
             jd = ea[u] + (eb[u] != 0.0 ? eb[u] * val * val : 0.0);
+          } else if (q == 0) {  // V - clamp(V, theta); diag M = 1/|S| on S, 1 off S, 0 inside
+            const double th = es[u];
+            uu = th < 0.0 ? val : softd(val, th);
+            jd = th < 0.0 ? 0.0 : (fabs(val) > th ? eb[u] : 1.0);
           } else {
             uu = val - softd(val, es[u]);
             jd = fabs(val) > es[u] ? 1.0 : 0.0;
@@ -339,6 +344,34 @@ __global__ void __launch_bounds__(256) k_edge_dot(const double* __restrict__ P, 
   }
 }
 
+// q = infinity: bc_l = <s_S, p_i - p_j> / |S| over S = {|v_f| > theta_l}
+// (zero inside the ball, where (I - M) = I).
+__global__ void __launch_bounds__(256) k_edge_dot_inf(const double* __restrict__ P, const double* __restrict__ V,
+                                                      const double* __restrict__ jal, const double* __restrict__ jbe,
+                                                      const int* __restrict__ ei, const int* __restrict__ ej,
+                                                      int64_t E, int d, double* __restrict__ bc, const int* active) {
+  if (active && !*active) return;
+  const int lane = threadIdx.x & 31;
+  for (int64_t l = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; l < E;
+       l += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const double th = jal[l], be = jbe[l];
+    if (th < 0.0 || be == 0.0) {
+      if (lane == 0) bc[l] = 0.0;
+      continue;
+    }
+    const double* pa = P + static_cast<int64_t>(ei[l]) * d;
+    const double* pb = P + static_cast<int64_t>(ej[l]) * d;
+    const double* vl = V + l * d;
+    double c = 0.0;
+    for (int f = lane; f < d; f += 32) {
+      const double vf = vl[f];
+      if (fabs(vf) > th) c += vf > 0.0 ? pa[f] - pb[f] : pb[f] - pa[f];
+    }
+    c = warp_sum(c);
+    if (lane == 0) bc[l] = be * c;
+  }
+}
+
 // ---- SSNAL Hessian, pass 2: node gather (ssnal.cpp:56-64) -----------------------------------
 // Ap_v = p_v + sigma sum_l +-(w - (alpha w + bc v)),  w = p_i(l) - p_j(l).
 template <int NF>
@@ -365,8 +398,8 @@ __global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, co
     const int cnt = min(32, p1 - p);
     const int my_e = lane < cnt ? adj_e[p + lane] : 0;
     const int my_o = lane < cnt ? adj_o[p + lane] : v;
-    const double my_a = lane < cnt ? (q == 2 ? jal[my_e] : thr[my_e]) : 0.0;
-    const double my_b = (lane < cnt && q == 2) ? bc[my_e] : 0.0;
+    const double my_a = lane < cnt ? ((q == 2 || q == 0) ? jal[my_e] : thr[my_e]) : 0.0;
+    const double my_b = (lane < cnt && (q == 2 || q == 0)) ? bc[my_e] : 0.0;
     for (int u0 = 0; u0 < cnt; u0 += kEB) {
       int le[kEB], lo[kEB];
       double ea[kEB], eb[kEB];
@@ -404,6 +437,20 @@ __global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, co
           for (int k = 0; k < NF; ++k) {
             acc[k] = __fma_rn(-ca, po[u][k], acc[k]);
             if (cb != 0.0) acc[k] = __fma_rn(-cb, vv[u][k], acc[k]);
+          }
+        }
+      } else if (q == 0) {  // (I - M) w = 1_S (w - s bc), identity inside the ball
+#pragma unroll
+        for (int u = 0; u < kEB; ++u) {
+          if (u0 + u >= cnt) continue;
+          const bool plus = lo[u] > v;
+          const double th = ea[u];
+#pragma unroll
+          for (int k = 0; k < NF; ++k) {
+            const double w = plus ? pv[k] - po[u][k] : po[u][k] - pv[k];
+            const double vf = vv[u][k];
+            const double y = th < 0.0 ? w : (fabs(vf) > th ? w - (vf > 0.0 ? eb[u] : -eb[u]) : 0.0);
+            acc[k] = plus ? acc[k] + y : acc[k] - y;
           }
         }
       } else {
@@ -528,6 +575,10 @@ int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, cons
   if (q == 2 && g.E > 0) {
     const int grid = std::max(1, std::min(cdiv(g.E, 8), c.sm_count * 8));
     k_edge_dot<<<grid, 256, 0, c.s>>>(P, V, jbe, g.ei.p, g.ej.p, g.E, static_cast<int>(d), bc, active);
+    CPB_LAUNCH_CHECK();
+  } else if (q == 0 && g.E > 0) {
+    const int grid = std::max(1, std::min(cdiv(g.E, 8), c.sm_count * 8));
+    k_edge_dot_inf<<<grid, 256, 0, c.s>>>(P, V, jal, jbe, g.ei.p, g.ej.p, g.E, static_cast<int>(d), bc, active);
     CPB_LAUNCH_CHECK();
   }
   GEOM

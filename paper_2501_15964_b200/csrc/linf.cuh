@@ -1,0 +1,60 @@
+// q = infinity building blocks (no reference counterpart: prox.cpp:17-21
+// accepts q in {1, 2} only; the math is SURVEY.md §8(c), restated in
+// oracle/prox_linalg.cpp l1_theta):
+//   prox_{t||.||inf}(v) = clamp(v, -theta, theta)        (0 when ||v||_1 <= t)
+//   Pi_{B1(r)}(z)       = sign(z) max(|z| - theta_r, 0)  (z when ||z||_1 <= r)
+//   (I - M)             = diag(1_S) - s_S s_S^T / |S|    (I inside the ball)
+// with theta the l1-ball projection threshold and S = {|v_f| > theta}.
+#pragma once
+
+#include "common.cuh"
+
+namespace cpb {
+
+// theta >= 0 with sum_f max(|v_f| - theta, 0) = t when ||v||_1 > t, else -1;
+// *cnt = |S|.  Michelot's fixed point: theta_0 = (||v||_1 - t) / d on the full
+// support, then theta <- (sum_{|v| > theta} |v| - t) / #{|v| > theta} until the
+// support stops shrinking (monotone; at most d + 1 passes, a handful in
+// practice).  For t = 0 the support empties at theta = max |v| (prox = v).
+// `val(f)` yields element f; one pass over the row per iteration by the
+// group's lanes (group_sum over blockDim.x <= 32 lanes, see common.cuh).
+template <class F>
+__device__ __forceinline__ double linf_theta(F val, int d, double t, unsigned gm, int* cnt) {
+  double s1 = 0.0;
+  for (int f = threadIdx.x; f < d; f += blockDim.x) s1 += fabs(val(f));
+  s1 = group_sum(s1, gm);
+  if (!(s1 > t)) {
+    *cnt = 0;
+    return -1.0;
+  }
+  double theta = (s1 - t) / static_cast<double>(d);
+  int support = d;
+  for (;;) {
+    double s = 0.0, c = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double a = fabs(val(f));
+      if (a > theta) {
+        s += a;
+        c += 1.0;
+      }
+    }
+    s = group_sum(s, gm);
+    c = group_sum(c, gm);
+    const int ci = static_cast<int>(c);
+    if (ci == 0) {
+      support = 0;
+      break;
+    }
+    const double nt = (s - t) / c;
+    const bool same = ci == support;
+    theta = nt;
+    support = ci;
+    if (same) break;
+  }
+  *cnt = support;
+  return theta;
+}
+
+__device__ __forceinline__ double clampd(double v, double th) { return fmax(fmin(v, th), -th); }
+
+}  // namespace cpb

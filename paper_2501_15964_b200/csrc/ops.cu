@@ -16,6 +16,7 @@
 #include "gather.cuh"
 #include "ops.cuh"
 #include "ptx.cuh"
+#include "linf.cuh"
 
 namespace cpb {
 
@@ -115,6 +116,10 @@ __global__ void k_prox_cols(int q, const double* __restrict__ V, const double* _
       const double nv = sqrt(group_sum(ss, gm));
       const double s = 1.0 - tl / nv;
       for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = (nv <= tl) ? 0.0 : s * v[f];
+    } else if (q == Q_LINF) {
+      int cnt;
+      const double th = linf_theta([&](int f) { return v[f]; }, d, tl, gm, &cnt);
+      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = th < 0.0 ? 0.0 : clampd(v[f], th);
     } else {
       for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = soft(v[f], tl);
     }
@@ -133,6 +138,10 @@ __global__ void k_project_cols(int q, const double* __restrict__ Z, const double
       const double nz = sqrt(group_sum(ss, gm));
       const double s = rl / nz;
       for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = (nz <= rl) ? z[f] : s * z[f];
+    } else if (q == Q_LINF) {
+      int cnt;
+      const double th = linf_theta([&](int f) { return z[f]; }, d, rl, gm, &cnt);
+      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = th < 0.0 ? z[f] : soft(z[f], th);
     } else {
       for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = fmax(fmin(z[f], rl), -rl);
     }
@@ -157,6 +166,11 @@ __global__ void k_jac_diag_cols(int q, const double* __restrict__ V, const doubl
         be = tl / (nv * nv * nv);
       }
       for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = al + (be != 0.0 ? be * v[f] * v[f] : 0.0);
+    } else if (q == Q_LINF) {  // diag of M = I - (diag(1_S) - s s^T / |S|); 0 inside the ball
+      int cnt;
+      const double th = linf_theta([&](int f) { return v[f]; }, d, tl, gm, &cnt);
+      const double b = cnt > 0 ? 1.0 / cnt : 0.0;
+      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = th < 0.0 ? 0.0 : (fabs(v[f]) > th ? b : 1.0);
     } else {
       for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = fabs(v[f]) > tl ? 1.0 : 0.0;
     }
@@ -200,6 +214,21 @@ __global__ void k_phi_edge(const double* __restrict__ X, const double* __restric
       }
       env = rad[row_] * pn + (0.5 * sigma) * sq;
       if (threadIdx.x == 0) nv[row_] = nvl;
+    } else if (q == Q_LINF) {
+      // P = clamp(V, theta): ||P||_inf = theta, ||P - V||^2 = sum soft(V, theta)^2
+      for (int f = threadIdx.x; f < d; f += blockDim.x) v[f] = (xa[f] - xb[f]) + z[f] / sigma;
+      int cnt;
+      const double th = linf_theta([&](int f) { return v[f]; }, d, t, gm, &cnt);
+      double sq = 0.0;
+      for (int f = threadIdx.x; f < d; f += blockDim.x) {
+        const double r = th < 0.0 ? v[f] : soft(v[f], th);
+        sq += r * r;
+      }
+      env = rad[row_] * (th < 0.0 ? 0.0 : th) + (0.5 * sigma) * group_sum(sq, gm);
+      if (threadIdx.x == 0) {
+        nv[row_] = th;
+        nv[E + row_] = cnt;
+      }
     } else {
       double a = 0.0, b = 0.0;
       for (int f = threadIdx.x; f < d; f += blockDim.x) {
@@ -233,6 +262,12 @@ __global__ void k_jac(const double* __restrict__ nv, const double* __restrict__ 
       jal[l] = (t == 0.0) ? 1.0 : s;
       jbe[l] = be;
       cnt += (be != 0.0) ? 1.0 : 0.0;
+    } else if (q == Q_LINF) {  // nv = (theta, |S|) from the phi edge pass
+      const double th = nv[l], sc = nv[E + l];
+      ps[l] = th;
+      jal[l] = th;
+      jbe[l] = (th >= 0.0 && sc > 0.0) ? 1.0 / sc : 0.0;
+      cnt += 1.0;
     } else {
       cnt += 1.0;
     }
@@ -246,6 +281,30 @@ __global__ void k_jac(const double* __restrict__ nv, const double* __restrict__ 
 // [2] ||XB||^2, [3] ||Z||^2; max dual-ball excess into partmax.
 __device__ __forceinline__ void gap_edge_terms(const double* xa, const double* xb, const double* z, double rl,
                                                double wl, int d, int q, unsigned gm, double* t4, double& excess) {
+  if (q == Q_LINF) {  // ||XB_l||_inf, prox_{r||.||inf}(XB + Z) = clamp at theta_r, dual norm l1
+    double xb2 = 0.0, zz = 0.0, xm = 0.0, z1 = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double x = xa[f] - xb[f];
+      xb2 += x * x;
+      zz += z[f] * z[f];
+      xm = fmax(xm, fabs(x));
+      z1 += fabs(z[f]);
+    }
+    int cnt;
+    const double th = linf_theta([&](int f) { return (xa[f] - xb[f]) + z[f]; }, d, rl, gm, &cnt);
+    double al = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double x = xa[f] - xb[f];
+      const double e = x - (th < 0.0 ? 0.0 : clampd(x + z[f], th));
+      al += e * e;
+    }
+    t4[0] = wl * group_max(xm, gm);
+    t4[1] = group_sum(al, gm);
+    t4[2] = group_sum(xb2, gm);
+    t4[3] = group_sum(zz, gm);
+    excess = fmax(excess, group_sum(z1, gm) - (rl + 1e-9));
+    return;
+  }
   double xb2 = 0.0, zz = 0.0, uu = 0.0, l1 = 0.0, zmax = 0.0;
   for (int f = threadIdx.x; f < d; f += blockDim.x) {
     const double x = xa[f] - xb[f];
@@ -391,6 +450,81 @@ __global__ void k_mult(const double* __restrict__ X, double* __restrict__ Z, con
     t4[3] = zz;
     if (threadIdx.x == 0) {
       for (int k = 0; k < 4; ++k) s[k] += t4[k];
+      s[4] += fr;
+    }
+  }
+  for (int k = 0; k < 5; ++k) {
+    const double r = block_sum(s[k], sh);
+    if (threadIdx.x == 0 && threadIdx.y == 0) part[9 * blockIdx.x + k] = r;
+  }
+  const double a = block_max(mx, sh);
+  const double b = block_max(err, sh);
+  const double c = block_max(excess, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    part[9 * blockIdx.x + 5] = 0.0;
+    part[9 * blockIdx.x + 6] = a;
+    part[9 * blockIdx.x + 7] = b;
+    part[9 * blockIdx.x + 8] = c;
+  }
+}
+
+// q = infinity multiplier (ssnal.cpp:183-206 with the l1 dual ball): Zsum =
+// Pi_{B1(r)}(Z + sigma XB) at its own threshold, the self-check against
+// Zenv = sigma (V - clamp(V, theta_v)) (theta_v = ps from the phi pass), and
+// the gap's edge terms at the new Z (prox_{r||.||inf}(XB + Z) needs a third
+// threshold).  Same part layout as k_mult.
+__global__ void k_mult_inf(const double* __restrict__ X, double* __restrict__ Z, const double* __restrict__ V,
+                           const double* __restrict__ ps, const double* __restrict__ rad,
+                           const double* __restrict__ w, const int* __restrict__ ei, const int* __restrict__ ej,
+                           int64_t E, int d, double sigma, double* part) {
+  __shared__ double sh[32];
+  const unsigned gm = group_mask();
+  double s[5] = {0, 0, 0, 0, 0}, mx = 0.0, err = 0.0, excess = -1.0;
+  ROWS_BEGIN(E) {
+    const double* xa = X + static_cast<int64_t>(ei[row_]) * d;
+    const double* xb = X + static_cast<int64_t>(ej[row_]) * d;
+    double* z = Z + row_ * d;
+    const double* v = V + row_ * d;
+    const double rl = rad[row_], thv = ps[row_];
+    double m = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) m = fmax(m, fabs(z[f] + sigma * (xa[f] - xb[f])));
+    mx = fmax(mx, m);
+    int cnt;
+    const double thz = linf_theta([&](int f) { return z[f] + sigma * (xa[f] - xb[f]); }, d, rl, gm, &cnt);
+    double fr = 0.0, e = 0.0, xb2 = 0.0, zz = 0.0, xm = 0.0, z1 = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double x = xa[f] - xb[f];
+      const double zs = z[f] + sigma * x;
+      const double zp = thz < 0.0 ? zs : soft(zs, thz);
+      const double vf = v[f];
+      const double pv = thv < 0.0 ? 0.0 : clampd(vf, thv);
+      e = fmax(e, fabs(sigma * (vf - pv) - zp));
+      z[f] = zp;
+      fr += (x - pv) * (x - pv);
+      xb2 += x * x;
+      zz += zp * zp;
+      xm = fmax(xm, fabs(x));
+      z1 += fabs(zp);
+    }
+    err = fmax(err, e);
+    const double thu = linf_theta([&](int f) { return (xa[f] - xb[f]) + z[f]; }, d, rl, gm, &cnt);
+    double al = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double x = xa[f] - xb[f];
+      const double ee = x - (thu < 0.0 ? 0.0 : clampd(x + z[f], thu));
+      al += ee * ee;
+    }
+    al = group_sum(al, gm);
+    fr = group_sum(fr, gm);
+    xb2 = group_sum(xb2, gm);
+    zz = group_sum(zz, gm);
+    const double pen = w[row_] * group_max(xm, gm);
+    excess = fmax(excess, group_sum(z1, gm) - (rl + 1e-9));
+    if (threadIdx.x == 0) {
+      s[0] += pen;
+      s[1] += al;
+      s[2] += xb2;
+      s[3] += zz;
       s[4] += fr;
     }
   }
@@ -733,6 +867,18 @@ __global__ void k_ama_edge(const double* __restrict__ Xh, double* __restrict__ Z
     double* zh = Zh + row_ * d;
     double* zp = Zp + row_ * d;
     const double rl = rad[row_];
+    if (q == Q_LINF) {
+      int cnt;
+      const double th = linf_theta([&](int f) { return zh[f] + step * (xa[f] - xb[f]); }, d, rl, gm, &cnt);
+      for (int f = threadIdx.x; f < d; f += blockDim.x) {
+        const double zn = zh[f] + step * (xa[f] - xb[f]);
+        const double zpr = th < 0.0 ? zn : soft(zn, th);
+        const double old = zp[f];
+        zh[f] = zpr + mom * (zpr - old);
+        zp[f] = zpr;
+      }
+      continue;
+    }
     double nn = 0.0;
     if (q == Q_L2) {
       for (int f = threadIdx.x; f < d; f += blockDim.x) {
@@ -843,7 +989,7 @@ double eval_phi(const Prob& P, const double* X, const double* D, double alpha, d
     double* pe = part_buf(c, "phi.pe", std::max({gg.grid, edge_grid(c, E), c.sm_count * 64}));
     int nb = gg.grid;
     Ctx::Timer tm(&c, "phi_edge", (2.0 * E * d + n * d + 4.0 * E) * 8.0);
-    if (edge_reg_supported(d)) {
+    if (edge_reg_supported(d) && P.q != Q_LINF) {
       nb = phi_edge_reg(c, *P.g, Xe, Z, thr, P.rad, d, sigma, P.q, V, nv, pe);
     } else if (gg.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1) &&
                std::getenv("CPB_PHI_NOTMA") == nullptr) {
@@ -1036,7 +1182,11 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
   int nb = ge.grid;
   {
     Ctx::Timer tm(&c, "multiplier", (3.0 * E * d + n * d) * 8.0);
-    if (edge_reg_supported(d)) {
+    if (P.q == Q_LINF) {
+      k_mult_inf<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, V, ps, P.rad, P.g->w.p, P.g->ei.p, P.g->ej.p, E,
+                                                          static_cast<int>(d), sigma, pe);
+      CPB_LAUNCH_CHECK();
+    } else if (edge_reg_supported(d)) {
       nb = mult_reg(c, *P.g, X, Z, V, ps, thr, P.rad, d, sigma, P.q, pe);
     } else if (ge.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1) &&
                std::getenv("CPB_MULT_NOTMA") == nullptr) {

@@ -10,7 +10,7 @@
 
 namespace cpb {
 
-enum { Q_L1 = 1, Q_L2 = 2 };
+enum { Q_LINF = 0, Q_L1 = 1, Q_L2 = 2 };  // Q_LINF: q = infinity (no reference counterpart)
 
 // One penalty level on one (data, graph) pair: ProblemInstance (solvers.hpp:26-43).
 struct Prob {

@@ -73,8 +73,8 @@ cp_termination ssnal(Prob& P, const cp_solver_config& cfg, bool warm, double* Xo
   double* Z = Zout;
   double* V = c.buf<double>("s.V", me);
   double* Vt = c.buf<double>("s.Vt", me);
-  double* nv = c.buf<double>("s.nv", E);
-  double* nvt = c.buf<double>("s.nvt", E);
+  double* nv = c.buf<double>("s.nv", 2 * E);  // q = inf keeps (theta, |S|) per edge
+  double* nvt = c.buf<double>("s.nvt", 2 * E);
   double* thr = c.buf<double>("s.thr", E);
   double* ps = c.buf<double>("s.ps", E);
   double* jal = c.buf<double>("s.jal", E);
@@ -387,7 +387,7 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
                   int64_t* labels_out, int64_t* K_out, cp_termination* terms_out) {
   if (T < 1) invalid("run_path: empty schedule");
   if (A.n != g.n) invalid("run_path: graph size does not match the data");
-  if (q != 1 && q != 2) invalid("penalty norm exponent must be 1 or 2, got " + std::to_string(q));
+  if (q != 0 && q != 1 && q != 2) invalid("penalty norm exponent must be 1, 2 or 0 (infinity), got " + std::to_string(q));
   validate_config(cfg);
   if (opt.require_connected) {
     int* lab = c.buf<int>("path.lab0", g.n + 1);

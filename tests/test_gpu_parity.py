@@ -254,6 +254,32 @@ def test_prox_project_jacobian(cp, orc, q):
         cp.prox_columns(np.ones((1, 2)), [0.5], 3)
 
 
+def test_prox_project_jacobian_linf(cp, orc):
+    """q = infinity (code 0): no reference; parity against the oracle's sort-based
+    l1-ball threshold (the GPU uses Michelot's fixed point)."""
+    rng = np.random.default_rng(4242)
+    for d in (1, 2, 3, 33, 784, 3072):
+        V = rng.normal(0, 2.0, (50, d))
+        l1 = np.abs(V).sum(axis=1)
+        t = rng.uniform(0, 1.2, 50) * l1
+        t[0] = 0.0
+        t[1] = l1[1]  # boundary of the l1 ball
+        t[2] = 2.0 * l1[2]  # inside
+        tol = 1e-13 * (1.0 + l1[:, None])
+        p = cp.prox_columns(V, t, float("inf"))
+        op = orc.prox_columns(0, V, t)
+        assert np.all(np.abs(p - op) <= tol)
+        z = cp.project_columns(V, t, "inf")
+        oz = orc.project_columns(0, V, t)
+        assert np.all(np.abs(z - oz) <= tol)
+        assert np.max(np.abs(p + z - V)) <= 1e-12 * max(1.0, np.max(np.abs(V)))  # Moreau
+        assert np.array_equal(p[0], V[0]) and np.all(p[2] == 0) and np.array_equal(z[2], V[2])
+        jd = cp.prox_jacobian_diag(V, t, cp.PenaltyNorm.linf)
+        ojd = np.stack([orc.prox_jacobian_diag(0, V[l], t[l]) for l in range(50)])
+        keep = np.arange(50) != 1
+        assert np.allclose(jd[keep], ojd[keep], rtol=1e-13, atol=1e-15)
+
+
 # ---- objectives and AL pieces (test_solvers.cpp:108-136, 367-397) ---------------------
 
 FIVE_A = np.array([[0.0, 0.0], [1.0, 0.2], [-0.8, 0.6], [0.3, -0.9], [-0.2, 0.5]])
@@ -275,7 +301,7 @@ def test_objectives_two_point(cp):
         cp.ProblemInstance(data, g, -0.5)
 
 
-@pytest.mark.parametrize("q", [1, 2])
+@pytest.mark.parametrize("q", [1, 2, 0])
 def test_objectives_and_al_match_oracle(cp, orc, q):
     A = mixture(orc, 30, 11)
     g, og = check_graph(cp, orc, A, 6, 0.5)
@@ -332,7 +358,7 @@ def test_trivial_and_warm(cp, algo):
 
 
 @pytest.mark.parametrize("algo", ALGOS)
-@pytest.mark.parametrize("q", [2, 1])
+@pytest.mark.parametrize("q", [2, 1, 0])
 def test_solver_parity_with_oracle(cp, orc, algo, q):
     """Same instance, same algorithm: X within 1e-6 relative Frobenius, labels equal."""
     A = mixture(orc, 25, 4, m=3, seed=9)
@@ -439,6 +465,20 @@ def test_path_parity(cp, orc, algo):
         assert np.linalg.norm(res.solutions[t].X - ores["X"][t]) <= 1e-6 * np.linalg.norm(ores["X"][t])
         assert np.array_equal(res.assignments[t].labels, ores["labels"][t])
         assert res.assignments[t].K == ores["K"][t]
+
+
+def test_path_parity_linf(cp, orc):
+    """Warm-started SSNAL path with q = infinity (C4's prox variant): every X
+    within 1e-6 relative Frobenius of the oracle path and identical labels."""
+    A = mixture(orc, 20, 8, m=4, seed=5)
+    g, og = check_graph(cp, orc, A, 6, 0.5)
+    sched = cp.make_schedule(0.01, 3.0, 8)
+    res = cp.run_path(cp.DataMatrix(A), g, float("inf"), sched, cp.SolverConfig())
+    ores = orc.run_path(A, og, 0, sched.values, orc.config("ssnal"))
+    for t in range(len(sched.values)):
+        assert res.stats[t].converged == bool(ores["terms"][t]["converged"])
+        assert np.linalg.norm(res.solutions[t].X - ores["X"][t]) <= 1e-6 * np.linalg.norm(ores["X"][t])
+        assert np.array_equal(res.assignments[t].labels, ores["labels"][t])
 
 
 def test_path_validation(cp):
