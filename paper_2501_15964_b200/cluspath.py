@@ -723,8 +723,11 @@ class PathResult:
 
 
 def run_path(data: DataMatrix, graph: WeightedGraph, norm, schedule: GammaSchedule, config: Optional[SolverConfig] = None,
-             options: Optional[PathOptions] = None, keep_solutions: bool = True) -> PathResult:
-    """run_path (path.cpp:110-142): warm-started gamma sweep, all on the GPU."""
+             options: Optional[PathOptions] = None, keep_solutions: bool = True, keep_z: bool = True) -> PathResult:
+    """run_path (path.cpp:110-142): warm-started gamma sweep, all on the GPU.
+    keep_solutions=False returns labels and records only; keep_z=False keeps
+    every X(gamma) but not the E x d multipliers (their host copy is the
+    dominant cost of a large path: 20 x E x d doubles)."""
     config = config or SolverConfig()
     options = options or PathOptions()
     gam = _f64(schedule.values)
@@ -733,7 +736,7 @@ def run_path(data: DataMatrix, graph: WeightedGraph, norm, schedule: GammaSchedu
         raise ValueError("run_path: empty schedule")
     n, d, E = data.n, data.d, graph.edge_count()
     X = pinned_empty((T, n, d)) if keep_solutions else None
-    Z = pinned_empty((T, E, d)) if keep_solutions else None
+    Z = pinned_empty((T, E, d)) if keep_solutions and keep_z else None
     lab = np.empty((T, n), np.int64)
     K = np.empty(T, np.int64)
     terms = (L.TerminationC * T)()

@@ -269,14 +269,17 @@ int nk_bucket(int64_t d) {
 
 }  // namespace
 
-// Default for even d in [34, 1024] (CPB_TMA_HESS=0 selects the two-pass
-// warp-chunk path, which reads V three times instead of twice).
+// Default for even d in [256, 1024]: below that the per-edge rows are too
+// short for a two-deep ring to cover the copy latency (C5, d = 64: 17.4 ms vs
+// 9.7 ms for the two-pass warp-chunk path).  CPB_TMA_HESS=0 disables it,
+// CPB_TMA_HESS=1 forces it for every even d in [34, 1024].
 bool hess_tma_supported(int64_t d) {
-  static const bool enabled = [] {
+  static const int mode = [] {
     const char* e = std::getenv("CPB_TMA_HESS");
-    return !(e && e[0] == '0');
+    return e ? (e[0] == '0' ? 0 : 2) : 1;
   }();
-  return enabled && d >= 33 && d % 2 == 0 && nk_bucket(d) > 0;
+  if (mode == 0 || d < 33 || d % 2 != 0 || nk_bucket(d) == 0) return false;
+  return mode == 2 || d >= 256;
 }
 
 // Returns the number of (pAp, pp) block partials written to `part`.

@@ -422,7 +422,7 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
   if (async_out) {
     for (int s = 0; s < 2; ++s) {
       snapX[s] = c.buf<double>(s ? "path.sX1" : "path.sX0", m + 1);
-      snapZ[s] = c.buf<double>(s ? "path.sZ1" : "path.sZ0", me + 1);
+      if (Z_out) snapZ[s] = c.buf<double>(s ? "path.sZ1" : "path.sZ0", me + 1);
       CPB_CUDA(cudaEventCreateWithFlags(&snap_ready[s], cudaEventDisableTiming));
       CPB_CUDA(cudaEventCreateWithFlags(&copy_done[s], cudaEventDisableTiming));
       CPB_CUDA(cudaEventRecord(copy_done[s], cs));

@@ -372,10 +372,11 @@ def test_solver_parity_with_oracle(cp, orc, algo, q):
         assert np.array_equal(cp.extract_clusters(sol.X, g).labels, orc.extract_clusters(osol.X, og)[0])
 
 
-@pytest.mark.parametrize("d", [34, 64, 784, 1000])
+@pytest.mark.parametrize("d", [34, 64, 256, 784, 1000])
 def test_hessian_tma_path_matches_oracle(cp, orc, d):
-    """Even d >= 34 takes the TMA-staged single-pass Hessian (hess_tma.cu), including
-    hub nodes split into segments (k = 30 makes degrees > 64)."""
+    """Even d >= 256 takes the TMA-staged single-pass Hessian (hess_tma.cu),
+    including hub nodes split into segments (k = 30 makes degrees > 64); d = 34
+    and 64 the two-pass warp-chunk path."""
     A = mixture(orc, 40, d, m=3, seed=5)
     for k in (6, 30):
         g, og = check_graph(cp, orc, A, k, 0.5)
