@@ -15,7 +15,9 @@
 //  * A thread-local device context is used (device 0 unless set_device()).
 #pragma once
 
+#include <charconv>
 #include <cmath>
+#include <fstream>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -278,13 +280,16 @@ inline Index component_count(const std::vector<Index>& labels) {
 }
 
 // ---- prox.hpp ----------------------------------------------------------------
-enum class PenaltyNorm { l1, l2 };
+// prox.hpp:8 PenaltyNorm{l1, l2}, extended with linf (q = infinity; no
+// reference counterpart, C-ABI code 0).  penalty_norm_from_q keeps the
+// reference's q in {1, 2}; linf is selected by name.
+enum class PenaltyNorm { l1, l2, linf };
 inline PenaltyNorm penalty_norm_from_q(int q) {
   if (q == 1) return PenaltyNorm::l1;
   if (q == 2) return PenaltyNorm::l2;
   throw std::invalid_argument("penalty norm exponent must be 1 or 2, got " + std::to_string(q));
 }
-inline int penalty_q(PenaltyNorm norm) { return norm == PenaltyNorm::l1 ? 1 : 2; }
+inline int penalty_q(PenaltyNorm norm) { return norm == PenaltyNorm::l1 ? 1 : (norm == PenaltyNorm::l2 ? 2 : 0); }
 
 // Columnwise helpers (prox.hpp:28-33), on the device.
 inline void prox_columns_into(const Matrix& V, const Vector& thresholds, PenaltyNorm norm, Matrix& out) {
@@ -645,6 +650,148 @@ inline PathResult run_path(const DataMatrix& data, const WeightedGraph& graph, P
     r.solutions.push_back(std::move(s));
   }
   return r;
+}
+
+// ---- output formats (io.cpp:14-18, 120-140; path.cpp:144-177) ------------------
+inline std::string format_double(double value) {
+  char buf[64];
+  auto res = std::to_chars(buf, buf + sizeof(buf), value);
+  return std::string(buf, res.ptr);
+}
+inline void write_matrix_csv(const std::string& path, const Matrix& M) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw std::runtime_error("cannot open '" + path + "' for writing");
+  for (Index r = 0; r < M.rows(); ++r) {
+    for (Index c = 0; c < M.cols(); ++c) {
+      if (c) out << ',';
+      out << format_double(M(r, c));
+    }
+    out << '\n';
+  }
+  if (!out) throw std::runtime_error("write to '" + path + "' failed");
+}
+inline void export_graph_csv(const std::string& path, const WeightedGraph& graph) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw std::runtime_error("cannot open '" + path + "' for writing");
+  out << "i,j,w\n";
+  for (const Edge& e : graph.edges()) out << e.i << ',' << e.j << ',' << format_double(e.w) << '\n';
+  if (!out) throw std::runtime_error("write to '" + path + "' failed");
+}
+// JSON with the reference's document shape and keys in nlohmann::json's order
+// (std::map: sorted); numbers in std::to_chars shortest form.
+inline std::string path_result_to_json(const PathResult& result, int indent = 2) {
+  std::string o;
+  auto nl = [&](int level) {
+    if (indent >= 0) {
+      o += '\n';
+      o.append(static_cast<size_t>(indent * level), ' ');
+    }
+  };
+  auto num = [&](double v) {
+    if (!std::isfinite(v)) {
+      o += "null";
+      return;
+    }
+    std::string s = format_double(v);
+    o += s;
+  };
+  auto key = [&](const char* k, int level, bool first) {
+    if (!first) o += ',';
+    nl(level);
+    o += '"';
+    o += k;
+    o += indent >= 0 ? "\": " : "\":";
+  };
+  o += '{';
+  key("per_gamma", 1, true);
+  o += '[';
+  for (size_t t = 0; t < result.stats.size(); ++t) {
+    const TerminationRecord& rec = result.stats[t];
+    const ClusterAssignment& asg = result.assignments[t];
+    if (t) o += ',';
+    nl(2);
+    o += '{';
+    key("K", 3, true);
+    o += std::to_string(asg.K);
+    key("converged", 3, false);
+    o += rec.converged ? "true" : "false";
+    key("f_d", 3, false);
+    num(rec.f_dual);
+    key("f_p", 3, false);
+    num(rec.f_primal);
+    key("gamma", 3, false);
+    num(result.schedule.values[t]);
+    key("gap", 3, false);
+    num(rec.gap);
+    key("iterations", 3, false);
+    o += std::to_string(rec.iterations);
+    key("labels", 3, false);
+    o += '[';
+    for (size_t i = 0; i < asg.labels.size(); ++i) {
+      if (i) o += ',';
+      nl(4);
+      o += std::to_string(asg.labels[i]);
+    }
+    if (!asg.labels.empty()) nl(3);
+    o += ']';
+    key("wall_time_s", 3, false);
+    num(rec.wall_time);
+    nl(2);
+    o += '}';
+  }
+  if (!result.stats.empty()) nl(1);
+  o += ']';
+  key("schedule", 1, false);
+  o += '{';
+  key("count", 2, true);
+  o += std::to_string(result.schedule.count);
+  key("end", 2, false);
+  num(result.schedule.end);
+  key("spacing", 2, false);
+  o += '"';
+  o += spacing_name(result.schedule.spacing);
+  o += '"';
+  key("start", 2, false);
+  num(result.schedule.start);
+  key("values", 2, false);
+  o += '[';
+  for (size_t i = 0; i < result.schedule.values.size(); ++i) {
+    if (i) o += ',';
+    nl(3);
+    num(result.schedule.values[i]);
+  }
+  if (!result.schedule.values.empty()) nl(2);
+  o += ']';
+  nl(1);
+  o += '}';
+  key("solver", 1, false);
+  o += '{';
+  const SolverConfig& c = result.solver;
+  key("admm_rho", 2, true);
+  num(c.admm_rho);
+  key("algorithm", 2, false);
+  o += '"';
+  o += algorithm_name(c.algorithm);
+  o += '"';
+  key("ama_step_safety", 2, false);
+  num(c.ama_step_safety);
+  key("epsilon", 2, false);
+  num(c.epsilon);
+  key("kkt_factor", 2, false);
+  num(c.kkt_factor);
+  key("max_iter", 2, false);
+  o += std::to_string(c.resolved_max_iter());
+  key("ssnal_sigma0", 2, false);
+  num(c.ssnal_sigma0);
+  if (c.time_limit) {
+    key("time_limit", 2, false);
+    num(*c.time_limit);
+  }
+  nl(1);
+  o += '}';
+  nl(0);
+  o += '}';
+  return o;
 }
 
 // generate_gaussian_mixture (io.hpp:41-44; io.cpp:142-165); centers as d-vectors.

@@ -17,4 +17,6 @@ from .cluspath import (Algorithm, ClusterAssignment, Context, DataMatrix, GammaS
                        primal_objective, project_columns, shard_rows, prox_columns, prox_jacobian_diag, recover_primal, run_path,
                        solve, ssnal_hessian_apply, ssnal_phi_gradient, ssnal_phi_value, two_point_closed_form)
 
+from .io import export_graph_csv, format_double, path_result_to_json, write_matrix_csv
+
 __all__ = [n for n in dir() if not n.startswith("_")]

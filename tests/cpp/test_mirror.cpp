@@ -376,6 +376,46 @@ TEST_CASE("warm starts reuse the previous solution; disconnected graphs") {  // 
   CHECK(r.all_converged() && r.assignments.back().K >= 2);
 }
 
+TEST_CASE("path JSON and CSV outputs") {  // test_path.cpp:243-270, test_io.cpp:197-203
+  DataMatrix data = line_data({0.0, 2.0});
+  WeightedGraph g(2, {{0, 1, 1.0}});
+  GammaSchedule s = make_schedule(0.5, 2.0, 3, Spacing::geometric);
+  SolverConfig cfg;
+  cfg.epsilon = 1e-8;
+  PathResult r = run_path(data, g, PenaltyNorm::l2, s, cfg);
+  const std::string j = path_result_to_json(r);
+  CHECK(j.find("\"spacing\": \"geometric\"") != std::string::npos);
+  CHECK(j.find("\"algorithm\": \"ssnal\"") != std::string::npos);
+  CHECK(j.find("\"epsilon\": 1e-08") != std::string::npos);
+  CHECK(j.find("\"max_iter\": 100") != std::string::npos);
+  CHECK(j.find("\"wall_time_s\"") != std::string::npos && j.find("\"f_p\"") != std::string::npos);
+  std::FILE* f = std::fopen("_build/path.json", "wb");
+  if (f) {
+    std::fputs(j.c_str(), f);
+    std::fclose(f);
+  }
+  WeightedGraph h(3, {{0, 1, 0.5}, {1, 2, 2.0}});
+  export_graph_csv("_build/g.csv", h);
+  std::FILE* in = std::fopen("_build/g.csv", "rb");
+  char buf[64] = {0};
+  const size_t got = in ? std::fread(buf, 1, sizeof(buf) - 1, in) : 0;
+  if (in) std::fclose(in);
+  CHECK(std::string(buf, got) == "i,j,w\n0,1,0.5\n1,2,2\n");
+  CHECK(format_double(1e5) == "1e+05" && format_double(2.0) == "2" && format_double(0.001) == "0.001");
+}
+
+TEST_CASE("q = infinity through the mirror") {  // no reference counterpart
+  Matrix V(3, 1);
+  V(0, 0) = 3.0;
+  V(1, 0) = -1.0;
+  V(2, 0) = 0.5;
+  Matrix P;
+  prox_columns_into(V, {1.0}, PenaltyNorm::linf, P);
+  CHECK(P(0, 0) == 2.0 && P(1, 0) == -1.0 && P(2, 0) == 0.5);
+  Matrix Zp = project_columns(V, {1.0}, PenaltyNorm::linf);
+  CHECK(Zp(0, 0) == 1.0 && Zp(1, 0) == 0.0 && Zp(2, 0) == 0.0);
+}
+
 int main() {
   int failed_cases = 0;
   for (auto& [name, fn] : registry()) {

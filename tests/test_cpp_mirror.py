@@ -21,7 +21,7 @@ def test_cpp_mirror_compiles():
 @pytest.mark.gpu
 def test_cpp_mirror_parity():
     exe = build()
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600, cwd=CPP)
     print(r.stdout[-4000:])
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert "0 failed; " in r.stdout
