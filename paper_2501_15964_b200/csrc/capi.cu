@@ -16,9 +16,13 @@ struct cp_ctx {
 };
 struct cp_data {
   cpb::Data d;
+  cudaStream_t s = nullptr;  // stream of the creating context (stream-ordered frees)
+  int device = 0;
 };
 struct cp_graph {
   std::unique_ptr<cpb::Graph> g;
+  cudaStream_t s = nullptr;
+  int device = 0;
 };
 
 namespace {
@@ -28,6 +32,7 @@ template <class F>
 int guard(cp_ctx* ctx, F f) {
   try {
     if (ctx && ctx->c) cudaSetDevice(ctx->c->device);
+    cpb::StreamScope scope(ctx && ctx->c ? ctx->c->s : nullptr);
     f();
     return CP_OK;
   } catch (const cpb::Error& e) {
@@ -258,6 +263,8 @@ int cp_data_create(cp_ctx* ctx, const double* A, int64_t d, int64_t n, cp_data**
     need(A, "A");
     cpb::Ctx& c = *ctx->c;
     auto p = std::make_unique<cp_data>();
+    p->s = ctx->c->s;
+    p->device = ctx->c->device;
     p->d.d = d;
     p->d.n = n;
     p->d.A.resize(d * n);
@@ -272,7 +279,12 @@ int cp_data_create(cp_ctx* ctx, const double* A, int64_t d, int64_t n, cp_data**
     *out = p.release();
   });
 }
-void cp_data_destroy(cp_data* data) { delete data; }
+void cp_data_destroy(cp_data* data) {
+  if (!data) return;
+  cudaSetDevice(data->device);
+  cpb::StreamScope scope(data->s);
+  delete data;
+}
 
 // ---- graph --------------------------------------------------------------------
 int cp_knn_graph(cp_ctx* ctx, const cp_data* data, int64_t k, double phi, cp_graph** out) {
@@ -280,6 +292,8 @@ int cp_knn_graph(cp_ctx* ctx, const cp_data* data, int64_t k, double phi, cp_gra
     need(data, "data");
     need(out, "out");
     auto g = std::make_unique<cp_graph>();
+    g->s = ctx->c->s;
+    g->device = ctx->c->device;
     g->g = cpb::knn_graph(*ctx->c, data->d, k, phi);
     *out = g.release();
   });
@@ -303,6 +317,8 @@ int cp_graph_from_knn(cp_ctx* ctx, int64_t n, int64_t k, double phi, const doubl
     need(out, "out");
     if (n < 2) cpb::invalid("graph from kNN lists: n must be >= 2");
     auto g = std::make_unique<cp_graph>();
+    g->s = ctx->c->s;
+    g->device = ctx->c->device;
     g->g = cpb::graph_from_knn_dev(*ctx->c, n, k, phi, kd_dev, kj_dev);
     *out = g.release();
   });
@@ -328,11 +344,18 @@ int cp_graph_from_edges(cp_ctx* ctx, int64_t n, const int64_t* i, const int64_t*
       need(w, "w");
     }
     auto g = std::make_unique<cp_graph>();
+    g->s = ctx->c->s;
+    g->device = ctx->c->device;
     g->g = cpb::graph_from_edges(*ctx->c, n, i, j, w, E);
     *out = g.release();
   });
 }
-void cp_graph_destroy(cp_graph* g) { delete g; }
+void cp_graph_destroy(cp_graph* g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  cpb::StreamScope scope(g->s);
+  delete g;
+}
 int64_t cp_graph_nodes(const cp_graph* g) { return g ? g->g->n : 0; }
 int64_t cp_graph_edge_count(const cp_graph* g) { return g ? g->g->E : 0; }
 int cp_graph_export(cp_ctx* ctx, const cp_graph* g, int64_t* i, int64_t* j, double* w, double* d2) {

@@ -1,7 +1,105 @@
 // Context, statistics and the fixed-order reduction kernels (see common.cuh).
 #include "common.cuh"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+
 namespace cpb {
+
+thread_local cudaStream_t tl_stream = nullptr;
+
+void trace(const char* tag) {
+  static const bool on = std::getenv("CPB_TRACE") != nullptr;
+  if (!on) return;
+  static auto last = std::chrono::steady_clock::now();
+  const auto now = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[cpb] %s +%.3f ms\n", tag, std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
+}
+
+namespace {
+struct Block {
+  void* p;
+  cudaEvent_t ready;  // recorded on the freeing stream (null: no pending work known)
+};
+std::mutex g_cache_mu;
+std::map<std::pair<int, size_t>, std::vector<Block>>& cache() {
+  static auto* m = new std::map<std::pair<int, size_t>, std::vector<Block>>();  // outlives static dtors
+  return *m;
+}
+}  // namespace
+
+void* dev_alloc(size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Block b{nullptr, nullptr};
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto& m = cache();
+    auto it = m.lower_bound({dev, bytes});
+    if (it != m.end() && it->first.first == dev && it->first.second <= 2 * bytes && !it->second.empty()) {
+      b = it->second.back();
+      it->second.pop_back();
+      if (it->second.empty()) m.erase(it);
+    }
+  }
+  if (b.p) {
+    if (b.ready) {
+      if (tl_stream)
+        cudaStreamWaitEvent(tl_stream, b.ready, 0);
+      else
+        cudaEventSynchronize(b.ready);
+      cudaEventDestroy(b.ready);
+    }
+    return b.p;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {  // out of memory: return the cache to CUDA and retry once
+    cudaGetLastError();
+    dev_cache_trim();
+    CPB_CUDA(cudaMalloc(&p, bytes));
+  }
+  return p;
+}
+void dev_free(void* p, size_t bytes) {
+  if (!p) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Block b{p, nullptr};
+  if (tl_stream && cudaEventCreateWithFlags(&b.ready, cudaEventDisableTiming) == cudaSuccess) {
+    if (cudaEventRecord(b.ready, tl_stream) != cudaSuccess) {
+      cudaGetLastError();
+      cudaEventDestroy(b.ready);
+      b.ready = nullptr;
+    }
+  } else {
+    cudaGetLastError();
+    b.ready = nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  cache()[{dev, bytes}].push_back(b);
+}
+void dev_cache_trim() {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& kv : cache()) {
+    cudaSetDevice(kv.first.first);
+    for (auto& b : kv.second) {
+      if (b.ready) {
+        cudaEventSynchronize(b.ready);
+        cudaEventDestroy(b.ready);
+      }
+      cudaFree(b.p);
+    }
+  }
+  cache().clear();
+  cudaSetDevice(cur);
+}
 
 unsigned long long g_launches = 0;
 

@@ -50,6 +50,25 @@ extern unsigned long long g_launches;
   } while (0)
 
 // ---- device buffers --------------------------------------------------------
+// Caching device allocator: freed blocks are kept in a per-device, size-keyed
+// free list and handed back to later requests of up to 2x smaller size, so
+// rebuilding a graph or re-growing a workspace never calls cudaFree (which
+// synchronises the device) or cudaMalloc in steady state (C3 path steps
+// varied 2.5-3.7 s with cudaFree in the graph rebuild, 2.49 s without).
+// Stream ordering: a free records an event on the freeing thread's current
+// library stream (tl_stream, set by the C-ABI for the call's context); a
+// reuse makes its own stream wait on that event, so a block is never touched
+// before the work of another context that used it has finished.
+extern thread_local cudaStream_t tl_stream;
+struct StreamScope {  // sets tl_stream for the current thread
+  cudaStream_t prev;
+  explicit StreamScope(cudaStream_t s) : prev(tl_stream) { tl_stream = s; }
+  ~StreamScope() { tl_stream = prev; }
+};
+void* dev_alloc(size_t bytes);
+void dev_free(void* p, size_t bytes);
+void dev_cache_trim();
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -69,7 +88,7 @@ struct DBuf {
   }
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) dev_free(p, n * sizeof(T));
     p = nullptr, n = 0;
   }
   // Grow-only (contents are not preserved on growth).
@@ -77,7 +96,7 @@ struct DBuf {
     if (count <= n && p) return;
     release();
     if (count == 0) count = 1;
-    CPB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    p = static_cast<T*>(dev_alloc(count * sizeof(T)));
     n = count;
   }
   T* get() const { return p; }
@@ -218,6 +237,10 @@ __device__ __forceinline__ double group_max(double v, unsigned m) {
   for (int o = blockDim.x >> 1; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(m, v, o, blockDim.x));
   return v;
 }
+
+// CPB_TRACE=1: host wall-clock trace lines "[cpb] <tag> +<ms since previous>"
+// on stderr (diagnostics for host-side stalls; off by default).
+void trace(const char* tag);
 
 // Host helpers implemented in common.cu.
 // Deterministic sum of `count` doubles at `src` into dst[0] (one block).

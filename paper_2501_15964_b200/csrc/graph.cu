@@ -514,6 +514,7 @@ std::unique_ptr<Graph> graph_from_edges(Ctx& c, int64_t n, const int64_t* i, con
   g->n = n;
   g->E = E;
   g->ei.resize(E);
+  trace("graph buffers allocated");
   g->ej.resize(E);
   g->w.resize(E);
   g->d2.resize(E);
@@ -617,10 +618,14 @@ void knn_rows_dev(Ctx& c, const Data& A, int64_t k, int64_t r0, int64_t r1, doub
 std::unique_ptr<Graph> knn_graph(Ctx& c, const Data& A, int64_t k, double phi) {
   knn_validate(A, k, phi);
   const int64_t n = A.n, NK = n * k;
+  trace("knn_graph begin");
   double* kd = c.buf<double>("knn.d", NK);
   int* kj = c.buf<int>("knn.j", NK);
   knn_rows_dev(c, A, k, 0, n, kd, kj);
-  return graph_from_knn_dev(c, n, k, phi, kd, kj);
+  trace("knn rows enqueued");
+  auto g = graph_from_knn_dev(c, n, k, phi, kd, kj);
+  trace("knn graph built");
+  return g;
 }
 
 // Union of the per-row lists as (min, max) pairs, sorted and unique, with
@@ -664,6 +669,7 @@ std::unique_ptr<Graph> graph_from_knn_dev(Ctx& c, int64_t n, int64_t k, double p
   });
   int E = 0;
   d2h(c, &E, nsel, sizeof(int));
+  trace("knn pairs selected (synced)");
   auto g = std::make_unique<Graph>();
   g->n = n;
   g->E = E;

@@ -630,7 +630,9 @@ int64_t knn_tc(Ctx& c, const Data& A, int64_t k, int64_t r0_, int64_t r1_, doubl
     CPB_LAUNCH_CHECK();
   }
   int h[2] = {0, 0};
+  trace("knn_tc enqueued");
   d2h(c, h, cnts, 2 * sizeof(int));
+  trace("knn_tc recheck synced");
   const int nq = h[0];
   if (nq > 0) {
     // threshold pass over the rows whose band outgrew a list

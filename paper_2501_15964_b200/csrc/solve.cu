@@ -465,6 +465,7 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
       if (Z_out && me) d2h(c, Z_out + t * me, Z, me * sizeof(double));
     }
     warm = opt.warm_start != 0;
+    trace("path gamma done");
   }
   if (async_out) {
     CPB_CUDA(cudaStreamSynchronize(cs));
