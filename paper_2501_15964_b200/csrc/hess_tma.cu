@@ -16,6 +16,7 @@
 // (deterministic).  Items run in node-id order, so both endpoints of an edge
 // of a clustered graph tend to read v_l within the L2 window.
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "gather.cuh"
@@ -200,7 +201,11 @@ __global__ void __launch_bounds__(256) k_hess_combine(const double* __restrict__
   }
 }
 
-// Segments per graph (host-built once from the CSR offsets; node-id order).
+// Segments per graph (host-built once from the CSR).  Items run in a
+// breadth-first (Cuthill-McKee-like) node order by default, so the nodes in
+// flight at any time are graph neighbours of each other and the second
+// endpoint's read of V_l and the gathered p rows tend to hit L2
+// (CPB_HESS_ORDER=id keeps node-id order).
 struct SegPlan {
   uint64_t uid = 0;
   int nseg = 0, nhub = 0, nslots = 0;
@@ -215,9 +220,34 @@ SegPlan& seg_plan(Ctx& c, const Graph& g) {
   p->uid = g.uid;
   std::vector<int> off(static_cast<size_t>(g.n + 1));
   d2h(c, off.data(), g.off.p, off.size() * sizeof(int));
+  std::vector<int> seq(static_cast<size_t>(g.n));
+  static const bool bfs = [] {
+    const char* e = std::getenv("CPB_HESS_ORDER");
+    return !(e && std::string(e) == "id");
+  }();
+  if (bfs && g.E > 0) {
+    std::vector<int> adj(static_cast<size_t>(2 * g.E));
+    d2h(c, adj.data(), g.adj_o.p, adj.size() * sizeof(int));
+    std::vector<char> seen(static_cast<size_t>(g.n), 0);
+    size_t head = 0, tail = 0;
+    for (int s0 = 0; s0 < g.n; ++s0) {
+      if (seen[s0]) continue;
+      seen[s0] = 1;
+      seq[tail++] = s0;
+      while (head < tail) {
+        const int v = seq[head++];
+        for (int e = off[v]; e < off[v + 1]; ++e) {
+          const int o = adj[static_cast<size_t>(e)];
+          if (!seen[o]) seen[o] = 1, seq[tail++] = o;
+        }
+      }
+    }
+  } else {
+    for (int v = 0; v < g.n; ++v) seq[v] = v;
+  }
   std::vector<int> node, beg, end, slot, hn, hs, hc;
   int slots = 0;
-  for (int v = 0; v < g.n; ++v) {
+  for (int v : seq) {
     const int a = off[v], b = off[v + 1];
     if (b - a <= kSegEdges) {
       node.push_back(v), beg.push_back(a), end.push_back(b), slot.push_back(-1);
