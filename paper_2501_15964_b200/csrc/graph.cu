@@ -503,7 +503,49 @@ void finalize_graph(Ctx& c, Graph& g) {
     CPB_CUDA(cudaMemcpyAsync(&md, degs, sizeof(int), cudaMemcpyDeviceToHost, c.s));
     c.sync();
     g.max_degree = md;
+    locality_order(c, g);
   }
+}
+
+// Gather work order: hubs (degree > 4x the mean) first for load balance, then
+// every other node in breadth-first order, so the nodes in flight together
+// are graph neighbours and their gathered rows (and each edge's row, read by
+// both endpoints) tend to be L2 hits (CPB_GATHER_ORDER=degree keeps the plain
+// degree-descending order).
+void locality_order(Ctx& c, Graph& g) {
+  static const bool bfs = [] {
+    const char* e = std::getenv("CPB_GATHER_ORDER");
+    return !(e && std::string(e) == "degree");
+  }();
+  const int n = static_cast<int>(g.n);
+  if (!bfs || g.E == 0 || n < 2) return;
+  std::vector<int> off(static_cast<size_t>(n) + 1), adj(static_cast<size_t>(2 * g.E));
+  d2h(c, off.data(), g.off.p, off.size() * sizeof(int));
+  d2h(c, adj.data(), g.adj_o.p, adj.size() * sizeof(int));
+  const double mean = 2.0 * static_cast<double>(g.E) / n;
+  auto hub = [&](int v) { return off[v + 1] - off[v] > 4.0 * mean + 16; };
+  std::vector<int> bfs_seq(static_cast<size_t>(n));
+  std::vector<char> seen(static_cast<size_t>(n), 0);
+  size_t head = 0, tail = 0;
+  for (int s0 = 0; s0 < n; ++s0) {
+    if (seen[s0]) continue;
+    seen[s0] = 1;
+    bfs_seq[tail++] = s0;
+    while (head < tail) {
+      const int v = bfs_seq[head++];
+      for (int e = off[v]; e < off[v + 1]; ++e) {
+        const int o = adj[static_cast<size_t>(e)];
+        if (!seen[o]) seen[o] = 1, bfs_seq[tail++] = o;
+      }
+    }
+  }
+  std::vector<int> seq;
+  seq.reserve(static_cast<size_t>(n));
+  for (int v : bfs_seq)
+    if (hub(v)) seq.push_back(v);
+  for (int v : bfs_seq)
+    if (!hub(v)) seq.push_back(v);
+  h2d(c, g.order.p, seq.data(), seq.size() * sizeof(int));
 }
 
 std::unique_ptr<Graph> graph_from_edges(Ctx& c, int64_t n, const int64_t* i, const int64_t* j, const double* w,

@@ -46,6 +46,8 @@ void knn_rows_dev(Ctx& c, const Data& A, int64_t k, int64_t r0, int64_t r1, doub
 std::unique_ptr<Graph> graph_from_knn_dev(Ctx& c, int64_t n, int64_t k, double phi, const double* kd, const int* kj);
 // Builds CSR/order for a graph whose ei/ej/w/d2 (sorted, validated) are set.
 void finalize_graph(Ctx& c, Graph& g);
+// Replaces g.order (degree-descending) by hubs-first breadth-first order.
+void locality_order(Ctx& c, Graph& g);
 
 // Incidence operator on device arrays (row layouts as above).
 void incidence_apply_dev(Ctx& c, const Graph& g, const double* X, int64_t d, double* out);
