@@ -28,12 +28,12 @@ namespace cpb {
 namespace {
 
 constexpr int kSegEdges = 64;
-constexpr int kStages = 2;
+constexpr int kMaxStages = 8;  // ring depth per warp: 2 at d = 784, up to 8 for short rows
 
 
 // Per-warp shared memory: a metadata table for the current segment (<= 64
 // edges: id, other endpoint, 1 - alpha, beta) filled with two coalesced
-// rounds at segment start, and a kStages ring of {p_other row, v row}.
+// rounds at segment start, and an S-deep ring of {p_other row, v row}.
 // Per edge, with c = <v_l, p_v - p_o> (sign-free), the edge adds
 //   (1 - alpha)(p_v - p_o) - beta c v_l
 // to node v: one FMA per feature for the dot, two for the update.
@@ -45,22 +45,22 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
                                                   const int* __restrict__ seg_end, const int* __restrict__ seg_slot,
                                                   int nseg, int d, int dp, double sigma, double* __restrict__ Ap,
                                                   double* __restrict__ partial, double* part, const int* active,
-                                                  int evict_v) {
+                                                  int evict_v, int S) {
   if (active && !*active) return;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ double sh[32];
-  __shared__ uint64_t bars[4][kStages];
+  __shared__ uint64_t bars[4][kMaxStages];
   __shared__ int m_le[4][kSegEdges], m_lo[4][kSegEdges];
   __shared__ double m_ca[4][kSegEdges], m_be[4][kSegEdges];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* ring = reinterpret_cast<double*>(smraw) + static_cast<size_t>(warp) * kStages * 2 * dp;
+  double* ring = reinterpret_cast<double*>(smraw) + static_cast<size_t>(warp) * S * 2 * dp;
   uint64_t* bar = bars[warp];
   int* le = m_le[warp];
   int* lo = m_lo[warp];
   double* ca = m_ca[warp];
   double* mb = m_be[warp];
   if (lane == 0)
-    for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
   fence_mbar_init();
   fence_proxy_async();
   __syncwarp();
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
     __syncwarp();
     if (lane == 0) {
       fence_proxy_async();
-      for (int s = 0; s < kStages && s < ne; ++s) issue(s, (cnt + s) % kStages);
+      for (int s = 0; s < S && s < ne; ++s) issue(s, (cnt + s) % S);
     }
     double pv[NK], acc[NK];
 #pragma unroll
@@ -105,9 +105,9 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
     }
     double dsum = 0.0;
     for (int q = 0; q < ne; ++q, ++cnt) {
-      const int st = cnt % kStages;
+      const int st = cnt % S;
       const double cq = ca[q], be = mb[q];
-      mbar_wait(&bar[st], (cnt / kStages) & 1u);
+      mbar_wait(&bar[st], (cnt / S) & 1u);
       const double* po = ring + st * 2 * dp;
       const double* vl = po + dp;
       dsum += cq;
@@ -137,9 +137,9 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
         }
       }
       __syncwarp();
-      if (lane == 0 && q + kStages < ne) {
+      if (lane == 0 && q + S < ne) {
         fence_proxy_async();
-        issue(q + kStages, st);
+        issue(q + S, st);
       }
     }
     __syncwarp();  // metadata table is rewritten by the next segment
@@ -330,7 +330,14 @@ int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const dou
     return e ? std::atoi(e) : -1;
   }();
   const int evict_v = vevict_env > 0 ? 1 : 0;  // measured neutral-to-worse at C3 (1586 vs 1541 us)
-  const size_t smem = static_cast<size_t>(warps) * kStages * 2 * dp * sizeof(double);
+  // ring depth: as many stages as fit ~25 KB per warp (2 at d = 784, 8 at d <= 195)
+  static const int s_env = [] {
+    const char* e = std::getenv("CPB_HESS_STAGES");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int S = s_env > 0 ? std::min(s_env, kMaxStages)
+                          : std::max(2, std::min(kMaxStages, static_cast<int>((25 * 1024) / (2 * dp * 8))));
+  const size_t smem = static_cast<size_t>(warps) * S * 2 * dp * sizeof(double);
   if (smem > 220 * 1024) invalid("hessian: shared-memory ring exceeds 220 KB");
   NK_DISPATCH(nk, set_smem, (static_cast<int>(smem)));
   double* partial = c.buf<double>("hess.partial", static_cast<size_t>(sp.nslots) * d + 1);
@@ -338,7 +345,7 @@ int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const dou
   NK_DISPATCH(nk, k_hess_tma, <<<grid, 32 * warps, smem, c.s>>>(P, V, jal, jbe, g.adj_e.p, g.adj_o.p, sp.node.p,
                                                                 sp.beg.p, sp.end.p, sp.slot.p, sp.nseg,
                                                                 static_cast<int>(d), dp, sigma, Ap, partial, part,
-                                                                active, evict_v));
+                                                                active, evict_v, S));
   CPB_LAUNCH_CHECK();
   int nb = grid;
   if (sp.nhub > 0) {

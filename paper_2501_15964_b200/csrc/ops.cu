@@ -552,6 +552,18 @@ __global__ void k_mult_inf(const double* __restrict__ X, double* __restrict__ Z,
 // order are those of k_mult (only the rows-to-block partition of the
 // deterministic block partials differs).
 constexpr int kMultSmemMaxD = 1024, kMultWarps = 4;
+// Ring depth of the TMA edge kernels: as many edges in flight per warp as fit
+// ~24 KB (1 at d = 784, where 8 warps per SM already keep ~150 KB in flight;
+// 8 for rows of <= 96 doubles, e.g. C5's d = 64).
+constexpr int kEdgeMaxStages = 8;
+inline int edge_stages(int64_t d, int rows) {
+  static const int env = [] {
+    const char* e = std::getenv("CPB_EDGE_STAGES");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env > 0) return std::min(env, kEdgeMaxStages);
+  return std::max(1, std::min(kEdgeMaxStages, static_cast<int>((24 * 1024) / (rows * d * 8))));
+}
 template <int Q>
 __global__ void __launch_bounds__(32 * kMultWarps) k_mult_s(
     const double* __restrict__ X, double* __restrict__ Z, const double* __restrict__ V, const double* __restrict__ ps,
@@ -664,36 +676,45 @@ template <int Q>
 __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
     const double* __restrict__ X, double* __restrict__ Z, const double* __restrict__ V, const double* __restrict__ ps,
     const double* __restrict__ thr, const double* __restrict__ rad, const double* __restrict__ w,
-    const int* __restrict__ ei, const int* __restrict__ ej, int64_t E, int d, double sigma, double* part) {
+    const int* __restrict__ ei, const int* __restrict__ ej, int64_t E, int d, double sigma, double* part, int S) {
   extern __shared__ __align__(16) double trow[];
   __shared__ double sh[32];
-  __shared__ uint64_t bars[kMultWarps];
+  __shared__ uint64_t bars[kMultWarps][kEdgeMaxStages];
   const int lane = threadIdx.x;
-  double* sx = trow + static_cast<size_t>(threadIdx.y) * 4 * d;  // x_i, then x = x_i - x_j
-  double* sb = sx + d;                                            // x_j
-  double* sz = sb + d;                                            // Z_l, then Zsum, then Z_l new
-  double* sv = sz + d;                                            // V_l
-  uint64_t* bar = &bars[threadIdx.y];
-  if (lane == 0) mbar_init(bar, 1);
+  uint64_t* bar = bars[threadIdx.y];
+  if (lane == 0)
+    for (int q = 0; q < S; ++q) mbar_init(&bar[q], 1);
   fence_mbar_init();
   __syncwarp();
   const unsigned rb = static_cast<unsigned>(d) * 8u;
-  unsigned phase = 0;
+  const int64_t wid = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * blockDim.y;
+  const int64_t cnt = wid < E ? (E - wid + nw - 1) / nw : 0;  // this warp's edges: wid + e nw
+  auto slot = [&](int64_t e) { return trow + (static_cast<size_t>(threadIdx.y) * S + e % S) * 4 * d; };
+  auto issue = [&](int64_t e) {  // lane 0: x_i, x_j, Z_l, V_l of edge wid + e nw into its slot
+    const int64_t l = wid + e * nw;
+    double* sx = slot(e);
+    uint64_t* b = &bar[e % S];
+    fence_proxy_async();
+    mbar_expect_tx(b, 4 * rb);
+    bulk_g2s(sx, X + static_cast<int64_t>(ei[l]) * d, rb, b);
+    bulk_g2s(sx + d, X + static_cast<int64_t>(ej[l]) * d, rb, b);
+    const uint64_t ef = policy_evict_first();
+    bulk_g2s_hint(sx + 2 * d, Z + l * d, rb, b, ef);
+    bulk_g2s_hint(sx + 3 * d, V + l * d, rb, b, ef);
+  };
+  if (lane == 0)
+    for (int64_t e = 0; e < S && e < cnt; ++e) issue(e);
   double s[5] = {0, 0, 0, 0, 0}, mx = 0.0, err = 0.0, excess = -1.0;
-  ROWS_BEGIN(E) {
-    if (lane == 0) {
-      fence_proxy_async();
-      mbar_expect_tx(bar, 4 * rb);
-      bulk_g2s(sx, X + static_cast<int64_t>(ei[row_]) * d, rb, bar);
-      bulk_g2s(sb, X + static_cast<int64_t>(ej[row_]) * d, rb, bar);
-      const uint64_t ef = policy_evict_first();
-      bulk_g2s_hint(sz, Z + row_ * d, rb, bar, ef);
-      bulk_g2s_hint(sv, V + row_ * d, rb, bar, ef);
-    }
+  for (int64_t it = 0; it < cnt; ++it) {
+    const int64_t row_ = wid + it * nw;
+    double* sx = slot(it);  // x_i, then x = x_i - x_j
+    double* sb = sx + d;   // x_j
+    double* sz = sb + d;   // Z_l, then Zsum, then Z_l new
+    double* sv = sz + d;   // V_l
     double* z = Z + row_ * d;
     const double rl = rad[row_], tl = thr[row_], sl = ps[row_];
-    mbar_wait(bar, phase);
-    phase ^= 1u;
+    mbar_wait(&bar[it % S], static_cast<unsigned>((it / S) & 1));
     double nn = 0.0, m = 0.0;
 #pragma unroll 4
     for (int f = lane; f < d; f += 32) {
@@ -766,6 +787,7 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
       s[4] += fr;
     }
     __syncwarp();  // every lane is done with the slot before lane 0 refills it
+    if (lane == 0 && it + S < cnt) issue(it + S);
   }
   for (int k = 0; k < 5; ++k) {
     const double r = block_sum(s[k], sh);
@@ -790,33 +812,42 @@ template <int Q>
 __global__ void __launch_bounds__(32 * kMultWarps) k_phi_edge_t(
     const double* __restrict__ X, const double* __restrict__ Z, const int* __restrict__ ei,
     const int* __restrict__ ej, const double* __restrict__ thr, const double* __restrict__ rad, int64_t E, int d,
-    double sigma, double* __restrict__ V, double* __restrict__ nv, double* part) {
+    double sigma, double* __restrict__ V, double* __restrict__ nv, double* part, int S) {
   extern __shared__ __align__(16) double prow[];
   __shared__ double sh[32];
-  __shared__ uint64_t bars[kMultWarps];
+  __shared__ uint64_t bars[kMultWarps][kEdgeMaxStages];
   const int lane = threadIdx.x;
-  double* sa = prow + static_cast<size_t>(threadIdx.y) * 3 * d;
-  double* sb = sa + d;
-  double* sz = sb + d;
-  uint64_t* bar = &bars[threadIdx.y];
-  if (lane == 0) mbar_init(bar, 1);
+  uint64_t* bar = bars[threadIdx.y];
+  if (lane == 0)
+    for (int q = 0; q < S; ++q) mbar_init(&bar[q], 1);
   fence_mbar_init();
   __syncwarp();
   const unsigned rb = static_cast<unsigned>(d) * 8u;
-  unsigned phase = 0;
+  const int64_t wid = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * blockDim.y;
+  const int64_t cnt = wid < E ? (E - wid + nw - 1) / nw : 0;
+  auto slot = [&](int64_t e) { return prow + (static_cast<size_t>(threadIdx.y) * S + e % S) * 3 * d; };
+  auto issue = [&](int64_t e) {
+    const int64_t l = wid + e * nw;
+    double* sa = slot(e);
+    uint64_t* b = &bar[e % S];
+    fence_proxy_async();
+    mbar_expect_tx(b, 3 * rb);
+    bulk_g2s(sa, X + static_cast<int64_t>(ei[l]) * d, rb, b);
+    bulk_g2s(sa + d, X + static_cast<int64_t>(ej[l]) * d, rb, b);
+    bulk_g2s_hint(sa + 2 * d, Z + l * d, rb, b, policy_evict_first());
+  };
+  if (lane == 0)
+    for (int64_t e = 0; e < S && e < cnt; ++e) issue(e);
   double acc = 0.0;
-  ROWS_BEGIN(E) {
-    if (lane == 0) {
-      fence_proxy_async();
-      mbar_expect_tx(bar, 3 * rb);
-      bulk_g2s(sa, X + static_cast<int64_t>(ei[row_]) * d, rb, bar);
-      bulk_g2s(sb, X + static_cast<int64_t>(ej[row_]) * d, rb, bar);
-      bulk_g2s_hint(sz, Z + row_ * d, rb, bar, policy_evict_first());
-    }
+  for (int64_t e = 0; e < cnt; ++e) {
+    const int64_t row_ = wid + e * nw;
+    double* sa = slot(e);
+    double* sb = sa + d;
+    double* sz = sb + d;
     double* v = V + row_ * d;
     const double t = thr[row_];
-    mbar_wait(bar, phase);
-    phase ^= 1u;
+    mbar_wait(&bar[e % S], static_cast<unsigned>((e / S) & 1));
     double env;
     if (Q == Q_L2) {
       double ss = 0.0;
@@ -851,6 +882,7 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_phi_edge_t(
     }
     if (lane == 0) acc += env;
     __syncwarp();
+    if (lane == 0 && e + S < cnt) issue(e + S);
   }
   acc = block_sum(acc, sh);
   if (threadIdx.x == 0 && threadIdx.y == 0) part[blockIdx.x] = acc;
@@ -993,13 +1025,12 @@ double eval_phi(const Prob& P, const double* X, const double* D, double alpha, d
       nb = phi_edge_reg(c, *P.g, Xe, Z, thr, P.rad, d, sigma, P.q, V, nv, pe);
     } else if (gg.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1) &&
                std::getenv("CPB_PHI_NOTMA") == nullptr) {
-      const size_t smem = static_cast<size_t>(kMultWarps) * 3 * d * sizeof(double);
+      const int S = edge_stages(d, 3);
+      const size_t smem = static_cast<size_t>(kMultWarps) * S * 3 * d * sizeof(double);
       static bool attr = false;
       if (!attr) {
-        CPB_CUDA(cudaFuncSetAttribute(k_phi_edge_t<Q_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kMultWarps * 3 * kMultSmemMaxD * 8));
-        CPB_CUDA(cudaFuncSetAttribute(k_phi_edge_t<Q_L1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kMultWarps * 3 * kMultSmemMaxD * 8));
+        CPB_CUDA(cudaFuncSetAttribute(k_phi_edge_t<Q_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CPB_CUDA(cudaFuncSetAttribute(k_phi_edge_t<Q_L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         attr = true;
       }
       int per_sm = 0;
@@ -1007,10 +1038,10 @@ double eval_phi(const Prob& P, const double* X, const double* D, double alpha, d
       nb = std::max(1, std::min(cdiv(E, kMultWarps), c.sm_count * std::max(1, per_sm)));
       if (P.q == Q_L2)
         k_phi_edge_t<Q_L2><<<nb, dim3(32, kMultWarps), smem, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, E,
-                                                                    static_cast<int>(d), sigma, V, nv, pe);
+                                                                    static_cast<int>(d), sigma, V, nv, pe, S);
       else
         k_phi_edge_t<Q_L1><<<nb, dim3(32, kMultWarps), smem, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, E,
-                                                                    static_cast<int>(d), sigma, V, nv, pe);
+                                                                    static_cast<int>(d), sigma, V, nv, pe, S);
       CPB_LAUNCH_CHECK();
     } else {
       k_phi_edge<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, E,
@@ -1190,13 +1221,12 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
       nb = mult_reg(c, *P.g, X, Z, V, ps, thr, P.rad, d, sigma, P.q, pe);
     } else if (ge.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1) &&
                std::getenv("CPB_MULT_NOTMA") == nullptr) {
-      const size_t smem = static_cast<size_t>(kMultWarps) * 4 * d * sizeof(double);
+      const int S = edge_stages(d, 4);
+      const size_t smem = static_cast<size_t>(kMultWarps) * S * 4 * d * sizeof(double);
       static bool attr_t = false;
       if (!attr_t) {
-        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kMultWarps * 4 * kMultSmemMaxD * 8));
-        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kMultWarps * 4 * kMultSmemMaxD * 8));
+        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         attr_t = true;
       }
       int per_sm = 0;
@@ -1204,10 +1234,10 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
       nb = std::max(1, std::min(cdiv(E, kMultWarps), c.sm_count * std::max(1, per_sm)));
       if (P.q == Q_L2)
         k_mult_t<Q_L2><<<nb, dim3(32, kMultWarps), smem, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p,
-                                                                P.g->ej.p, E, static_cast<int>(d), sigma, pe);
+                                                                P.g->ej.p, E, static_cast<int>(d), sigma, pe, S);
       else
         k_mult_t<Q_L1><<<nb, dim3(32, kMultWarps), smem, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p,
-                                                                P.g->ej.p, E, static_cast<int>(d), sigma, pe);
+                                                                P.g->ej.p, E, static_cast<int>(d), sigma, pe, S);
       CPB_LAUNCH_CHECK();
     } else if (ge.gx == 32 && d <= kMultSmemMaxD && (P.q == Q_L2 || P.q == Q_L1)) {
       const size_t smem = static_cast<size_t>(kMultWarps) * 2 * d * sizeof(double);

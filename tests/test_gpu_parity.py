@@ -468,6 +468,21 @@ def test_path_parity(cp, orc, algo):
         assert res.assignments[t].K == ores["K"][t]
 
 
+@pytest.mark.parametrize("d", [64, 96])
+def test_edge_ring_wraps_match_oracle(cp, orc, d):
+    """Short rows run the TMA edge kernels with an 8-deep per-warp ring; with
+    ~20k edges every warp wraps its ring several times."""
+    A = mixture(orc, 750, d, m=4, seed=21)
+    g, og = check_graph(cp, orc, A, 10, 0.5)
+    assert g.edge_count() > 15000
+    gamma = 0.05
+    sol = cp.solve(cp.ProblemInstance(cp.DataMatrix(A), g, gamma, 2), cp.SolverConfig())
+    osol = orc.solve(A, og, gamma, 2, orc.config("ssnal"))
+    assert sol.termination.converged == bool(osol.term["converged"])
+    assert np.linalg.norm(sol.X - osol.X) <= 1e-6 * np.linalg.norm(osol.X)
+    assert sol.termination.cg == osol.term["cg"] and sol.termination.newton == osol.term["newton"]
+
+
 def test_path_parity_linf(cp, orc):
     """Warm-started SSNAL path with q = infinity (C4's prox variant): every X
     within 1e-6 relative Frobenius of the oracle path and identical labels."""
