@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
   fence_proxy_async();
   __syncwarp();
   const unsigned row_bytes = static_cast<unsigned>(d) * 8u;
-  unsigned cnt = 0;  // stages consumed by this warp so far (phase tracking)
+  int cst = 0;        // next ring slot to consume
+  unsigned cph = 0;   // its mbarrier phase parity
   double s_a = 0.0, s_b = 0.0;
   const uint64_t vpol = evict_v ? policy_evict_first() : 0;
   auto issue = [&](int q, int st) {  // lane 0: stream edge q's rows into stage st
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
     __syncwarp();
     if (lane == 0) {
       fence_proxy_async();
-      for (int s = 0; s < S && s < ne; ++s) issue(s, (cnt + s) % S);
+      for (int s = 0, t = cst; s < S && s < ne; ++s, t = (t + 1 == S) ? 0 : t + 1) issue(s, t);
     }
     double pv[NK], acc[NK];
 #pragma unroll
@@ -104,10 +105,11 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
       acc[k] = 0.0;
     }
     double dsum = 0.0;
-    for (int q = 0; q < ne; ++q, ++cnt) {
-      const int st = cnt % S;
+    for (int q = 0; q < ne; ++q) {
+      const int st = cst;
       const double cq = ca[q], be = mb[q];
-      mbar_wait(&bar[st], (cnt / S) & 1u);
+      mbar_wait(&bar[st], cph);
+      if (++cst == S) cst = 0, cph ^= 1u;
       const double* po = ring + st * 2 * dp;
       const double* vl = po + dp;
       dsum += cq;
@@ -330,13 +332,13 @@ int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const dou
     return e ? std::atoi(e) : -1;
   }();
   const int evict_v = vevict_env > 0 ? 1 : 0;  // measured neutral-to-worse at C3 (1586 vs 1541 us)
-  // ring depth: as many stages as fit ~25 KB per warp (2 at d = 784, 8 at d <= 195)
+  // ring depth: 2 (deeper rings measured slower: C5 with 8 stages 38.8 vs 17.4 ms);
+  // CPB_HESS_STAGES overrides
   static const int s_env = [] {
     const char* e = std::getenv("CPB_HESS_STAGES");
     return e ? std::atoi(e) : 0;
   }();
-  const int S = s_env > 0 ? std::min(s_env, kMaxStages)
-                          : std::max(2, std::min(kMaxStages, static_cast<int>((25 * 1024) / (2 * dp * 8))));
+  const int S = s_env > 0 ? std::min(s_env, kMaxStages) : 2;
   const size_t smem = static_cast<size_t>(warps) * S * 2 * dp * sizeof(double);
   if (smem > 220 * 1024) invalid("hessian: shared-memory ring exceeds 220 KB");
   NK_DISPATCH(nk, set_smem, (static_cast<int>(smem)));

@@ -552,17 +552,18 @@ __global__ void k_mult_inf(const double* __restrict__ X, double* __restrict__ Z,
 // order are those of k_mult (only the rows-to-block partition of the
 // deterministic block partials differs).
 constexpr int kMultSmemMaxD = 1024, kMultWarps = 4;
-// Ring depth of the TMA edge kernels: as many edges in flight per warp as fit
-// ~24 KB (1 at d = 784, where 8 warps per SM already keep ~150 KB in flight;
-// 8 for rows of <= 96 doubles, e.g. C5's d = 64).
+// Ring depth of the TMA edge kernels (edges in flight per warp).  One stage
+// by default: at d = 784 eight warps per SM already keep ~150 KB in flight,
+// and deeper rings measured slower for short rows (C5, d = 64: phi 14.3 vs
+// 6.4 ms, multiplier 23.5 vs 11.6 ms at 8 stages).  CPB_EDGE_STAGES overrides.
 constexpr int kEdgeMaxStages = 8;
 inline int edge_stages(int64_t d, int rows) {
+  (void)d, (void)rows;
   static const int env = [] {
     const char* e = std::getenv("CPB_EDGE_STAGES");
     return e ? std::atoi(e) : 0;
   }();
-  if (env > 0) return std::min(env, kEdgeMaxStages);
-  return std::max(1, std::min(kEdgeMaxStages, static_cast<int>((24 * 1024) / (rows * d * 8))));
+  return env > 0 ? std::min(env, kEdgeMaxStages) : 1;
 }
 template <int Q>
 __global__ void __launch_bounds__(32 * kMultWarps) k_mult_s(
@@ -690,11 +691,11 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
   const int64_t wid = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * blockDim.y;
   const int64_t cnt = wid < E ? (E - wid + nw - 1) / nw : 0;  // this warp's edges: wid + e nw
-  auto slot = [&](int64_t e) { return trow + (static_cast<size_t>(threadIdx.y) * S + e % S) * 4 * d; };
-  auto issue = [&](int64_t e) {  // lane 0: x_i, x_j, Z_l, V_l of edge wid + e nw into its slot
+  double* const base = trow + static_cast<size_t>(threadIdx.y) * S * 4 * d;
+  auto issue = [&](int64_t e, int q) {  // lane 0: x_i, x_j, Z_l, V_l of edge wid + e nw into slot q
     const int64_t l = wid + e * nw;
-    double* sx = slot(e);
-    uint64_t* b = &bar[e % S];
+    double* sx = base + static_cast<size_t>(q) * 4 * d;
+    uint64_t* b = &bar[q];
     fence_proxy_async();
     mbar_expect_tx(b, 4 * rb);
     bulk_g2s(sx, X + static_cast<int64_t>(ei[l]) * d, rb, b);
@@ -704,17 +705,19 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
     bulk_g2s_hint(sx + 3 * d, V + l * d, rb, b, ef);
   };
   if (lane == 0)
-    for (int64_t e = 0; e < S && e < cnt; ++e) issue(e);
+    for (int q = 0; q < S && q < cnt; ++q) issue(q, q);
   double s[5] = {0, 0, 0, 0, 0}, mx = 0.0, err = 0.0, excess = -1.0;
+  int q = 0;
+  unsigned ph = 0;
   for (int64_t it = 0; it < cnt; ++it) {
     const int64_t row_ = wid + it * nw;
-    double* sx = slot(it);  // x_i, then x = x_i - x_j
+    double* sx = base + static_cast<size_t>(q) * 4 * d;  // x_i, then x = x_i - x_j
     double* sb = sx + d;   // x_j
     double* sz = sb + d;   // Z_l, then Zsum, then Z_l new
     double* sv = sz + d;   // V_l
     double* z = Z + row_ * d;
     const double rl = rad[row_], tl = thr[row_], sl = ps[row_];
-    mbar_wait(&bar[it % S], static_cast<unsigned>((it / S) & 1));
+    mbar_wait(&bar[q], ph);
     double nn = 0.0, m = 0.0;
 #pragma unroll 4
     for (int f = lane; f < d; f += 32) {
@@ -787,7 +790,8 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
       s[4] += fr;
     }
     __syncwarp();  // every lane is done with the slot before lane 0 refills it
-    if (lane == 0 && it + S < cnt) issue(it + S);
+    if (lane == 0 && it + S < cnt) issue(it + S, q);
+    if (++q == S) q = 0, ph ^= 1u;
   }
   for (int k = 0; k < 5; ++k) {
     const double r = block_sum(s[k], sh);
@@ -826,11 +830,11 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_phi_edge_t(
   const int64_t wid = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * blockDim.y;
   const int64_t cnt = wid < E ? (E - wid + nw - 1) / nw : 0;
-  auto slot = [&](int64_t e) { return prow + (static_cast<size_t>(threadIdx.y) * S + e % S) * 3 * d; };
-  auto issue = [&](int64_t e) {
+  double* const base = prow + static_cast<size_t>(threadIdx.y) * S * 3 * d;
+  auto issue = [&](int64_t e, int q) {
     const int64_t l = wid + e * nw;
-    double* sa = slot(e);
-    uint64_t* b = &bar[e % S];
+    double* sa = base + static_cast<size_t>(q) * 3 * d;
+    uint64_t* b = &bar[q];
     fence_proxy_async();
     mbar_expect_tx(b, 3 * rb);
     bulk_g2s(sa, X + static_cast<int64_t>(ei[l]) * d, rb, b);
@@ -838,16 +842,18 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_phi_edge_t(
     bulk_g2s_hint(sa + 2 * d, Z + l * d, rb, b, policy_evict_first());
   };
   if (lane == 0)
-    for (int64_t e = 0; e < S && e < cnt; ++e) issue(e);
+    for (int q = 0; q < S && q < cnt; ++q) issue(q, q);
   double acc = 0.0;
+  int q = 0;
+  unsigned ph = 0;
   for (int64_t e = 0; e < cnt; ++e) {
     const int64_t row_ = wid + e * nw;
-    double* sa = slot(e);
+    double* sa = base + static_cast<size_t>(q) * 3 * d;
     double* sb = sa + d;
     double* sz = sb + d;
     double* v = V + row_ * d;
     const double t = thr[row_];
-    mbar_wait(&bar[e % S], static_cast<unsigned>((e / S) & 1));
+    mbar_wait(&bar[q], ph);
     double env;
     if (Q == Q_L2) {
       double ss = 0.0;
@@ -882,7 +888,8 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_phi_edge_t(
     }
     if (lane == 0) acc += env;
     __syncwarp();
-    if (lane == 0 && e + S < cnt) issue(e + S);
+    if (lane == 0 && e + S < cnt) issue(e + S, q);
+    if (++q == S) q = 0, ph ^= 1u;
   }
   acc = block_sum(acc, sh);
   if (threadIdx.x == 0 && threadIdx.y == 0) part[blockIdx.x] = acc;
