@@ -244,28 +244,47 @@ __global__ void __launch_bounds__(192, 1)
         uint32_t r[32];
         tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(b * TN + ch * 32), r);
         const int cb = tt * TN + ch * 32;
+        // branch-free common path: the chunk's 32 column norms as 8 broadcast
+        // float4 loads, 32 d2~ values, one candidate bit mask; the (rare)
+        // insertions then run over the set bits with static register indices
+        const float4* nj4 = reinterpret_cast<const float4*>(n32 + cb);
+        float d2v[32];
 #pragma unroll
-        for (int v = 0; v < 32; ++v) {
-          const int col = cb + v;
-          const float d2 = (ni + __ldg(n32 + col)) - 2.0f * __uint_as_float(r[v]);
-          if (THRESH) {
-            if (d2 <= lim && col != row) {
+        for (int u = 0; u < 8; ++u) {
+          const float4 q4 = __ldg(nj4 + u);
+          d2v[4 * u + 0] = (ni + q4.x) - 2.0f * __uint_as_float(r[4 * u + 0]);
+          d2v[4 * u + 1] = (ni + q4.y) - 2.0f * __uint_as_float(r[4 * u + 1]);
+          d2v[4 * u + 2] = (ni + q4.z) - 2.0f * __uint_as_float(r[4 * u + 2]);
+          d2v[4 * u + 3] = (ni + q4.w) - 2.0f * __uint_as_float(r[4 * u + 3]);
+        }
+        unsigned m = 0;
+#pragma unroll
+        for (int v = 0; v < 32; ++v) m |= ((THRESH ? d2v[v] <= lim : d2v[v] < thr) ? 1u : 0u) << v;
+        const int self = row - cb;
+        if (self >= 0 && self < 32) m &= ~(1u << self);
+        if (m) {
+#pragma unroll
+          for (int v = 0; v < 32; ++v) {
+            if (!((m >> v) & 1u)) continue;
+            const float d2 = d2v[v];
+            const int col = cb + v;
+            if (THRESH) {
               if (cnt < caps) {
                 cd[tbase + cnt] = d2;
                 cj[tbase + cnt] = col;
               }
               ++cnt;
-            }
-          } else if (d2 < thr && col != row) {
-            const int pos = cnt < KC ? cnt++ : maxpos;
-            Ld[pos * TM + t] = d2;
-            Lj[pos * TM + t] = col;
-            if (cnt == KC) {
-              thr = Ld[t];
-              maxpos = 0;
-              for (int q = 1; q < KC; ++q) {
-                const float x = Ld[q * TM + t];
-                if (x > thr) thr = x, maxpos = q;
+            } else if (d2 < thr) {  // thr may have dropped since the mask was taken
+              const int pos = cnt < KC ? cnt++ : maxpos;
+              Ld[pos * TM + t] = d2;
+              Lj[pos * TM + t] = col;
+              if (cnt == KC) {
+                thr = Ld[t];
+                maxpos = 0;
+                for (int q = 1; q < KC; ++q) {
+                  const float x = Ld[q * TM + t];
+                  if (x > thr) thr = x, maxpos = q;
+                }
               }
             }
           }
