@@ -80,6 +80,18 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// tcgen05.ld without the wait (the caller issues tmem_wait_ld before use).
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
@@ -239,10 +251,16 @@ __global__ void __launch_bounds__(192, 1)
       const int b = lt & 1;
       mbar_wait(&tfull[b], (lt >> 1) & 1);
       tc_fence_after();
+      const uint32_t tbuf = tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(b * TN);
+      uint32_t rn[32];
+      tmem_ld32(tbuf, rn);
 #pragma unroll 1
       for (int ch = 0; ch < TN / 32; ++ch) {
         uint32_t r[32];
-        tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(b * TN + ch * 32), r);
+#pragma unroll
+        for (int v = 0; v < 32; ++v) r[v] = rn[v];
+        // the next chunk's accumulator load overlaps this chunk's processing
+        if (ch + 1 < TN / 32) tmem_ld32_nowait(tbuf + static_cast<uint32_t>((ch + 1) * 32), rn);
         const int cb = tt * TN + ch * 32;
         // branch-free common path: the chunk's 32 column norms as 8 broadcast
         // float4 loads, 32 d2~ values, one candidate bit mask; the (rare)
@@ -263,10 +281,15 @@ __global__ void __launch_bounds__(192, 1)
         const int self = row - cb;
         if (self >= 0 && self < 32) m &= ~(1u << self);
         if (m) {
+          // rare path, kept small for the instruction cache: spill the chunk
+          // to a local array once and walk the set bits
+          float dl[32];
 #pragma unroll
-          for (int v = 0; v < 32; ++v) {
-            if (!((m >> v) & 1u)) continue;
-            const float d2 = d2v[v];
+          for (int v = 0; v < 32; ++v) dl[v] = d2v[v];
+          while (m) {
+            const int v = __ffs(m) - 1;
+            m &= m - 1;
+            const float d2 = dl[v];
             const int col = cb + v;
             if (THRESH) {
               if (cnt < caps) {
@@ -289,6 +312,7 @@ __global__ void __launch_bounds__(192, 1)
             }
           }
         }
+        tmem_wait_ld();  // the prefetched chunk is in rn
       }
       tc_fence_before();
       mbar_arrive(&tempty[b]);
