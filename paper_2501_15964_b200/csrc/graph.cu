@@ -349,14 +349,36 @@ __global__ void k_incidence(const double* __restrict__ X, const int* __restrict_
   }
 }
 // ---- connected components ------------------------------------------------------------
-__global__ void k_cc_hook(const int* __restrict__ ei, const int* __restrict__ ej, const unsigned char* __restrict__ flag,
-                          int E, int* L, int* changed) {
+// Lock-free union-find over the flagged edges in one pass (ECL-CC style):
+// find with path halving, then link the larger root under the smaller with
+// CAS, retrying on contention.  A root is only ever linked under a smaller
+// root, so each component ends rooted at its smallest node whatever the
+// interleaving: the labels are deterministic.
+__device__ __forceinline__ int cc_find(int* L, int x) {
+  int y = __ldcg(L + x);  // L2 (coherent) reads: other threads relink concurrently
+  while (y != x) {
+    const int z = __ldcg(L + y);
+    if (z != y) L[x] = z;  // path halving (benign race: z is an ancestor)
+    x = y;
+    y = z;
+  }
+  return x;
+}
+__global__ void k_cc_union(const int* __restrict__ ei, const int* __restrict__ ej,
+                           const unsigned char* __restrict__ flag, int E, int* L) {
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < E; l += gridDim.x * blockDim.x) {
     if (flag && !flag[l]) continue;
-    const int a = L[ei[l]], b = L[ej[l]];
-    if (a != b) {
-      atomicMin(L + max(a, b), min(a, b));
-      *changed = 1;
+    int u = cc_find(L, ei[l]), v = cc_find(L, ej[l]);
+    while (u != v) {
+      if (u > v) {
+        const int t = u;
+        u = v;
+        v = t;
+      }
+      const int old = atomicCAS(L + v, v, u);  // v is (was) a root: hang it under u
+      if (old == v) break;
+      v = cc_find(L, old);
+      u = cc_find(L, u);
     }
   }
 }
@@ -750,22 +772,15 @@ int64_t components_dev(Ctx& c, const Graph& g, const unsigned char* flag, int* l
   int* L = c.buf<int>("cc.L", n);
   int* root = c.buf<int>("cc.root", n + 1);
   int* rank = c.buf<int>("cc.rank", n + 1);
-  int* changed = c.buf<int>("cc.changed", 1);
   const int gn = std::max(1, std::min(cdiv(n, 256), c.sm_count * 8));
   const int ge = std::max(1, std::min(cdiv(E, 256), c.sm_count * 8));
   k_iota<<<gn, 256, 0, c.s>>>(L, n);
   CPB_LAUNCH_CHECK();
   if (E > 0) {
-    for (int iter = 0; iter < 4 * 64 + n; ++iter) {
-      CPB_CUDA(cudaMemsetAsync(changed, 0, sizeof(int), c.s));
-      k_cc_hook<<<ge, 256, 0, c.s>>>(g.ei.p, g.ej.p, flag, E, L, changed);
-      CPB_LAUNCH_CHECK();
-      k_cc_jump<<<gn, 256, 0, c.s>>>(L, n);
-      CPB_LAUNCH_CHECK();
-      int h = 0;
-      d2h(c, &h, changed, sizeof(int));
-      if (!h) break;
-    }
+    k_cc_union<<<ge, 256, 0, c.s>>>(g.ei.p, g.ej.p, flag, E, L);
+    CPB_LAUNCH_CHECK();
+    k_cc_jump<<<gn, 256, 0, c.s>>>(L, n);
+    CPB_LAUNCH_CHECK();
   }
   k_cc_roots<<<gn, 256, 0, c.s>>>(L, n, root);
   CPB_CUDA(cudaMemsetAsync(root + n, 0, sizeof(int), c.s));
