@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_s(
 // keeps 4 d doubles in flight without spending registers on them; the three
 // passes then run from shared memory (x_i's slot is reused for x, Z_l's for
 // Zsum / the projected Z).  Per-element arithmetic is that of k_mult_s.
-template <int Q>
+template <int Q, bool VS>
 __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
     const double* __restrict__ X, double* __restrict__ Z, const double* __restrict__ V, const double* __restrict__ ps,
     const double* __restrict__ thr, const double* __restrict__ rad, const double* __restrict__ w,
@@ -691,18 +691,19 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
   const int64_t wid = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * blockDim.y;
   const int64_t cnt = wid < E ? (E - wid + nw - 1) / nw : 0;  // this warp's edges: wid + e nw
-  double* const base = trow + static_cast<size_t>(threadIdx.y) * S * 4 * d;
+  constexpr int NR = VS ? 4 : 3;  // staged rows per edge (V_l staged or streamed)
+  double* const base = trow + static_cast<size_t>(threadIdx.y) * S * NR * d;
   auto issue = [&](int64_t e, int q) {  // lane 0: x_i, x_j, Z_l, V_l of edge wid + e nw into slot q
     const int64_t l = wid + e * nw;
-    double* sx = base + static_cast<size_t>(q) * 4 * d;
+    double* sx = base + static_cast<size_t>(q) * NR * d;
     uint64_t* b = &bar[q];
     fence_proxy_async();
-    mbar_expect_tx(b, 4 * rb);
+    mbar_expect_tx(b, NR * rb);
     bulk_g2s(sx, X + static_cast<int64_t>(ei[l]) * d, rb, b);
     bulk_g2s(sx + d, X + static_cast<int64_t>(ej[l]) * d, rb, b);
     const uint64_t ef = policy_evict_first();
     bulk_g2s_hint(sx + 2 * d, Z + l * d, rb, b, ef);
-    bulk_g2s_hint(sx + 3 * d, V + l * d, rb, b, ef);
+    if (VS) bulk_g2s_hint(sx + 3 * d, V + l * d, rb, b, ef);
   };
   if (lane == 0)
     for (int q = 0; q < S && q < cnt; ++q) issue(q, q);
@@ -711,10 +712,10 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
   unsigned ph = 0;
   for (int64_t it = 0; it < cnt; ++it) {
     const int64_t row_ = wid + it * nw;
-    double* sx = base + static_cast<size_t>(q) * 4 * d;  // x_i, then x = x_i - x_j
+    double* sx = base + static_cast<size_t>(q) * NR * d;  // x_i, then x = x_i - x_j
     double* sb = sx + d;   // x_j
     double* sz = sb + d;   // Z_l, then Zsum, then Z_l new
-    double* sv = sz + d;   // V_l
+    const double* sv = VS ? sz + d : V + row_ * d;  // V_l (staged, or streamed from HBM)
     double* z = Z + row_ * d;
     const double rl = rad[row_], tl = thr[row_], sl = ps[row_];
     mbar_wait(&bar[q], ph);
@@ -737,7 +738,7 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
       const double x = sx[f];
       const double zs = sz[f];
       const double zp = (Q == Q_L2) ? ((nz <= rl) ? zs : sc * zs) : fmax(fmin(zs, rl), -rl);
-      const double vf = sv[f];
+      const double vf = VS ? sv[f] : __ldcs(sv + f);
       const double pv = (Q == Q_L2) ? sl * vf : soft(vf, tl);
       const double zenv = sigma * (vf - pv);
       e = fmax(e, fabs(zenv - zp));
@@ -1228,23 +1229,40 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
       nb = mult_reg(c, *P.g, X, Z, V, ps, thr, P.rad, d, sigma, P.q, pe);
     } else if (ge.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1) &&
                std::getenv("CPB_MULT_NOTMA") == nullptr) {
-      const int S = edge_stages(d, 4);
-      const size_t smem = static_cast<size_t>(kMultWarps) * S * 4 * d * sizeof(double);
+      // V_l staged with the other rows (default) or streamed from HBM in pass 2
+      // (CPB_MULT_VSTAGE=0: 3 staged rows, more warps per SM — measured slower,
+      // 4.42 vs 3.46 ms at C3)
+      static const bool vstage = [] {
+        const char* e = std::getenv("CPB_MULT_VSTAGE");
+        return !(e && e[0] == '0');
+      }();
+      const int NR = vstage ? 4 : 3;
+      const int S = edge_stages(d, NR);
+      const size_t smem = static_cast<size_t>(kMultWarps) * S * NR * d * sizeof(double);
       static bool attr_t = false;
       if (!attr_t) {
-        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         attr_t = true;
       }
       int per_sm = 0;
-      CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mult_t<Q_L2>, 32 * kMultWarps, smem));
+      CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mult_t<Q_L2, false>, 32 * kMultWarps, smem));
       nb = std::max(1, std::min(cdiv(E, kMultWarps), c.sm_count * std::max(1, per_sm)));
-      if (P.q == Q_L2)
-        k_mult_t<Q_L2><<<nb, dim3(32, kMultWarps), smem, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p,
-                                                                P.g->ej.p, E, static_cast<int>(d), sigma, pe, S);
+      const dim3 blk(32, kMultWarps);
+      const int di = static_cast<int>(d);
+      const int* ei = P.g->ei.p;
+      const int* ej = P.g->ej.p;
+      const double* wl = P.g->w.p;
+      if (P.q == Q_L2 && vstage)
+        k_mult_t<Q_L2, true><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, E, di, sigma, pe, S);
+      else if (P.q == Q_L2)
+        k_mult_t<Q_L2, false><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, E, di, sigma, pe, S);
+      else if (vstage)
+        k_mult_t<Q_L1, true><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, E, di, sigma, pe, S);
       else
-        k_mult_t<Q_L1><<<nb, dim3(32, kMultWarps), smem, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p,
-                                                                P.g->ej.p, E, static_cast<int>(d), sigma, pe, S);
+        k_mult_t<Q_L1, false><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, E, di, sigma, pe, S);
       CPB_LAUNCH_CHECK();
     } else if (ge.gx == 32 && d <= kMultSmemMaxD && (P.q == Q_L2 || P.q == Q_L1)) {
       const size_t smem = static_cast<size_t>(kMultWarps) * 2 * d * sizeof(double);
