@@ -32,9 +32,10 @@ of BASELINE.json).  c2 (n=10000, configs[1]) and c1 are selectable.
 
 Multi-GPU (N > 1, one process per GPU under torchrun, NCCL): the kNN is
 sharded by query-row blocks with an all-gather of the per-row lists (every
-rank then builds the bit-identical graph); the 20-gamma solve is replicated
-on every rank (the node/edge-partitioned solver with halo exchange is not
-built yet), so "scaling" is "strong" on one fixed path.
+rank then builds the bit-identical graph), and every SSNAL Newton system's PCG
+(~75 % of the C3 path) is node-partitioned (each rank applies the Hessian and
+updates the vectors for its rows; block partials all-reduced, p all-gathered);
+the remaining per-Newton work is replicated.  "scaling": "strong" (one path).
 """
 from __future__ import annotations
 
@@ -273,13 +274,16 @@ def workload_config(args, cfg):
             "n": cfg["n"], "d": cfg["d"], "k": cfg["k"], "T": cfg["T"], "solver": cfg["algorithm"],
             "l2": "flushed between steps (512 MB write); edge arrays > L2",
             "parallelism": ("kNN query rows sharded over the ranks (NCCL all-gather of the n x k lists); "
-                            "20-gamma solver replicated on every rank") if args.gpus > 1 else "single"}
+                            "each Newton system's PCG node-partitioned (NCCL all-reduce of partials, all-gather "
+                            "of p); the rest of the path replicated") if args.gpus > 1 else "single"}
 
 
 def run_ours(args, cfg):
     world, rank, local, dist = dist_setup()
     import paper_2501_15964_b200 as cp
     ctx = cp.default_context(local)
+    if world > 1:
+        cp.init_comm_from_torch(ctx)  # NCCL communicator: node-partitioned Newton PCG
     A = make_input(cp, cfg)
     cpcfg = cp.SolverConfig(algorithm=cp.algorithm_from_name(cfg["algorithm"]))
     sched = cp.make_schedule(cfg["gamma"][0], cfg["gamma"][1], cfg["T"])

@@ -142,6 +142,16 @@ int cp_knn_rows(cp_ctx* ctx, const cp_data* data, int64_t k, int64_t r0, int64_t
  * (min, max) pairs, sorted, unique, w = exp(-phi d2) (graph.cpp:89-111). */
 int cp_graph_from_knn(cp_ctx* ctx, int64_t n, int64_t k, double phi, const double* kd_dev, const int32_t* kj_dev,
                       cp_graph** out);
+/* Multi-GPU (one process per GPU): rank 0 creates a 128-byte
+ * NCCL unique id, the caller distributes it (e.g. torch.distributed), and every
+ * rank attaches a communicator to its context.  With a communicator, each SSNAL
+ * Newton system's PCG is node-partitioned over the ranks (rows
+ * [r ceil(n/P), (r+1) ceil(n/P))): Hessian applies and vector updates cover the
+ * rank's rows, block partials are all-reduced and p / x all-gathered over
+ * NVLink; the rest of the path is replicated.  nranks = 1 runs the same code
+ * path on one GPU.  libnccl.so.2 is loaded at run time (CP_ENCCL if absent). */
+int cp_nccl_unique_id(char out[128]);
+int cp_ctx_set_comm(cp_ctx* ctx, int nranks, int rank, const char id[128]);
 /* Host-only: the query rows [r0, r1) of `rank` among `nranks` for the
  * row-sharded kNN: ceil(n / nranks) rows per rank, the last rank short. */
 int cp_shard_rows(int64_t n, int nranks, int rank, int64_t* r0, int64_t* r1);

@@ -12,7 +12,7 @@ from .cluspath import (Algorithm, ClusterAssignment, Context, DataMatrix, GammaS
                        PathOptions, PathResult, PenaltyNorm, ProblemInstance, Solution, SolverConfig, Spacing,
                        TerminationRecord, WeightedGraph, algorithm_from_name, algorithm_name, component_count,
                        compute_knn_weights, compute_knn_weights_sharded, connected_components, default_context, dual_objective, duality_gap,
-                       extract_clusters, flush_l2, gather_row_lists, knn_rows_into, generate_gaussian_mixture, kkt_residual, launch_count,
+                       extract_clusters, flush_l2, gather_row_lists, init_comm_from_torch, knn_rows_into, nccl_unique_id, generate_gaussian_mixture, kkt_residual, launch_count,
                        make_data_matrix, make_schedule, normals, penalty_norm_from_q, timer_start, timer_stop,
                        primal_objective, project_columns, shard_rows, prox_columns, prox_jacobian_diag, recover_primal, run_path,
                        solve, ssnal_hessian_apply, ssnal_phi_gradient, ssnal_phi_value, two_point_closed_form)

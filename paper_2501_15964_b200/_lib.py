@@ -72,6 +72,8 @@ _SIGS = [
     ("cp_knn_rows", C.c_int, [VP, VP, C.c_int64, C.c_int64, C.c_int64, VP, VP]),
     ("cp_graph_from_knn", C.c_int, [VP, C.c_int64, C.c_int64, C.c_double, VP, VP, C.POINTER(VP)]),
     ("cp_shard_rows", C.c_int, [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("cp_nccl_unique_id", C.c_int, [C.c_char_p]),
+    ("cp_ctx_set_comm", C.c_int, [VP, C.c_int, C.c_int, C.c_char_p]),
     ("cp_graph_from_edges", C.c_int, [VP, C.c_int64, I64, I64, D, C.c_int64, C.POINTER(VP)]),
     ("cp_graph_destroy", None, [VP]),
     ("cp_graph_nodes", C.c_int64, [VP]),

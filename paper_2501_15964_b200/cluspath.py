@@ -56,6 +56,13 @@ class Context:
         L.check(L.load().cp_device_info(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
         return {"sm": f"{a.value}{b.value}", "sm_count": c.value, "built_arch": d.value}
 
+    def set_comm(self, nranks: int, rank: int, unique_id: bytes):
+        """Attach an NCCL communicator (cp_ctx_set_comm): the SSNAL Newton
+        systems' PCG is then node-partitioned over the ranks."""
+        if len(unique_id) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        L.check(L.load().cp_ctx_set_comm(self._h, int(nranks), int(rank), C.c_char_p(bytes(unique_id))))
+
     def knn_info(self):
         """How the last compute_knn_weights on this context ran (tensor-core
         candidate pass, segments, rows re-done exactly, worst |d2~-d2|/bound)."""
@@ -298,6 +305,24 @@ def compute_knn_weights(data: DataMatrix, k: int, phi: float) -> WeightedGraph:
     h = C.c_void_p()
     L.check(L.load().cp_knn_graph(data.ctx._h, data._h, int(k), float(phi), C.byref(h)))
     return WeightedGraph(ctx=data.ctx, _handle=h)
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (cp_nccl_unique_id)."""
+    buf = C.create_string_buffer(128)
+    L.check(L.load().cp_nccl_unique_id(buf))
+    return buf.raw
+
+
+def init_comm_from_torch(ctx: "Context", group=None) -> None:
+    """One process per GPU: rank 0 creates the NCCL id, torch.distributed
+    broadcasts it, every rank attaches the communicator to its context."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    ctx.set_comm(world, rank, obj[0])
 
 
 def shard_rows(n: int, nranks: int, rank: int):

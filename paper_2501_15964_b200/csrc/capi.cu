@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.cuh"
 #include "solve.cuh"
 
 struct cp_ctx {
@@ -321,6 +322,18 @@ int cp_graph_from_knn(cp_ctx* ctx, int64_t n, int64_t k, double phi, const doubl
     g->device = ctx->c->device;
     g->g = cpb::graph_from_knn_dev(*ctx->c, n, k, phi, kd_dev, kj_dev);
     *out = g.release();
+  });
+}
+int cp_nccl_unique_id(char out[128]) {
+  return guard(nullptr, [&] {
+    need(out, "out");
+    cpb::comm_unique_id(out);
+  });
+}
+int cp_ctx_set_comm(cp_ctx* ctx, int nranks, int rank, const char id[128]) {
+  return guard(ctx, [&] {
+    need(id, "id");
+    cpb::comm_init(*ctx->c, nranks, rank, id);
   });
 }
 int cp_shard_rows(int64_t n, int nranks, int rank, int64_t* r0, int64_t* r1) {

@@ -1,5 +1,6 @@
 // Context, statistics and the fixed-order reduction kernels (see common.cuh).
 #include "common.cuh"
+#include "comm.cuh"
 
 #include <chrono>
 #include <cstdio>

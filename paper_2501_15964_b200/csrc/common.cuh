@@ -140,6 +140,11 @@ struct Ctx {
     int tensor_cores;       // 1 when the tcgen05 candidate pass ran
   } knn_last{0, 0.0, 0, 0};
   int64_t knn_band_rows = 0;  // rows settled by the tensor-core threshold (band) pass
+  // Multi-GPU: the NCCL communicator (comm.cuh) and, while the partitioned PCG
+  // runs, the node rows [own_v0, own_v1) this rank's Hessian applies cover
+  // (own_v1 < 0: every node).
+  std::unique_ptr<struct Comm> comm;
+  int64_t own_v0 = 0, own_v1 = -1;
   cudaStream_t cs = nullptr;                          // device->host copy stream (lazily created)
   cudaStream_t copy_stream() {
     if (!cs) CPB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));

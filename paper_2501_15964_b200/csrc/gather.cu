@@ -568,6 +568,32 @@ int gather_grad_diag(Ctx& c, const Graph& g, const double* X, const double* A, c
   return ng.grid;
 }
 
+// Partitioned PCG (c.own_v1 >= 0): the gather visits only this rank's nodes,
+// in the graph's degree order; cached per (graph, range).
+struct OwnOrder {
+  uint64_t uid = 0;
+  int64_t v0 = 0, v1 = -1, count = 0;
+  DBuf<int> order;
+};
+const OwnOrder& own_order(Ctx& c, const Graph& g) {
+  static thread_local std::vector<std::unique_ptr<OwnOrder>> cache;
+  for (auto& o : cache)
+    if (o->uid == g.uid && o->v0 == c.own_v0 && o->v1 == c.own_v1) return *o;
+  auto o = std::make_unique<OwnOrder>();
+  o->uid = g.uid, o->v0 = c.own_v0, o->v1 = c.own_v1;
+  std::vector<int> all(static_cast<size_t>(g.n)), mine;
+  if (g.n) d2h(c, all.data(), g.order.p, all.size() * sizeof(int));
+  for (int v : all)
+    if (v >= c.own_v0 && v < c.own_v1) mine.push_back(v);
+  o->count = static_cast<int64_t>(mine.size());
+  o->order.resize(mine.size() + 1);
+  if (!mine.empty()) h2d(c, o->order.p, mine.data(), mine.size() * sizeof(int));
+  c.sync();
+  if (cache.size() > 8) cache.erase(cache.begin());
+  cache.push_back(std::move(o));
+  return *cache.back();
+}
+
 int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,
                   const double* thr, int64_t d, double sigma, int q, double* bc, double* Ap, double* part,
                   const int* active) {
@@ -582,10 +608,17 @@ int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, cons
     CPB_LAUNCH_CHECK();
   }
   GEOM
-  NF_DISPATCH(ng.nf, k_g_hess, <<<ng.grid, 256, 0, c.s>>>(P, V, jal, bc, thr, g.off.p, g.adj_e.p, g.adj_o.p,
-                                                           g.order.p, g.n, di, nch, sigma, q, Ap, part, active));
+  const int* ord = g.order.p;
+  int64_t items = g.n;
+  int grid = ng.grid;
+  if (c.own_v1 >= 0) {  // partitioned PCG: this rank's nodes, the same grid on every rank
+    const OwnOrder& o = own_order(c, g);
+    ord = o.order.p, items = o.count, grid = c.sm_count * 8;
+  }
+  NF_DISPATCH(ng.nf, k_g_hess, <<<grid, 256, 0, c.s>>>(P, V, jal, bc, thr, g.off.p, g.adj_e.p, g.adj_o.p, ord,
+                                                        items, di, nch, sigma, q, Ap, part, active));
   CPB_LAUNCH_CHECK();
-  return ng.grid;
+  return grid;
 }
 
 }  // namespace cpb

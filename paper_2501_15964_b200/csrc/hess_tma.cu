@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(256) k_hess_combine(const double* __restrict__
 // (CPB_HESS_ORDER=id keeps node-id order).
 struct SegPlan {
   uint64_t uid = 0;
+  int64_t v0 = 0, v1 = -1;  // node range the items cover (v1 < 0: all nodes)
   int nseg = 0, nhub = 0, nslots = 0;
   DBuf<int> node, beg, end, slot, hub_node, hub_slot0, hub_nslots;
 };
@@ -217,9 +218,11 @@ struct SegPlan {
 SegPlan& seg_plan(Ctx& c, const Graph& g) {
   static thread_local std::vector<std::unique_ptr<SegPlan>> plans;
   for (auto& p : plans)
-    if (p->uid == g.uid) return *p;
+    if (p->uid == g.uid && p->v0 == c.own_v0 && p->v1 == c.own_v1) return *p;
   auto p = std::make_unique<SegPlan>();
   p->uid = g.uid;
+  p->v0 = c.own_v0;
+  p->v1 = c.own_v1;
   std::vector<int> off(static_cast<size_t>(g.n + 1));
   d2h(c, off.data(), g.off.p, off.size() * sizeof(int));
   std::vector<int> seq(static_cast<size_t>(g.n));
@@ -250,6 +253,7 @@ SegPlan& seg_plan(Ctx& c, const Graph& g) {
   std::vector<int> node, beg, end, slot, hn, hs, hc;
   int slots = 0;
   for (int v : seq) {
+    if (c.own_v1 >= 0 && (v < c.own_v0 || v >= c.own_v1)) continue;  // another rank's node
     const int a = off[v], b = off[v + 1];
     if (b - a <= kSegEdges) {
       node.push_back(v), beg.push_back(a), end.push_back(b), slot.push_back(-1);
@@ -343,15 +347,17 @@ int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const dou
   if (smem > 220 * 1024) invalid("hessian: shared-memory ring exceeds 220 KB");
   NK_DISPATCH(nk, set_smem, (static_cast<int>(smem)));
   double* partial = c.buf<double>("hess.partial", static_cast<size_t>(sp.nslots) * d + 1);
-  const int grid = std::max(1, std::min(cdiv(sp.nseg, warps), c.sm_count * 2));
+  // partitioned PCG: every rank launches the same grid so the partial tables line up
+  const bool parted = c.own_v1 >= 0;
+  const int grid = parted ? c.sm_count * 2 : std::max(1, std::min(cdiv(sp.nseg, warps), c.sm_count * 2));
   NK_DISPATCH(nk, k_hess_tma, <<<grid, 32 * warps, smem, c.s>>>(P, V, jal, jbe, g.adj_e.p, g.adj_o.p, sp.node.p,
                                                                 sp.beg.p, sp.end.p, sp.slot.p, sp.nseg,
                                                                 static_cast<int>(d), dp, sigma, Ap, partial, part,
                                                                 active, evict_v, S));
   CPB_LAUNCH_CHECK();
   int nb = grid;
-  if (sp.nhub > 0) {
-    const int gh = std::max(1, std::min(sp.nhub, c.sm_count * 4));
+  if (sp.nhub > 0 || parted) {
+    const int gh = parted ? c.sm_count * 4 : std::max(1, std::min(sp.nhub, c.sm_count * 4));
     k_hess_combine<<<gh, 256, 0, c.s>>>(P, partial, sp.hub_node.p, sp.hub_slot0.p, sp.hub_nslots.p, sp.nhub,
                                          static_cast<int>(d), sigma, Ap, part + 2 * grid, active);
     CPB_LAUNCH_CHECK();

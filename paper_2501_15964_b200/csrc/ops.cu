@@ -16,6 +16,7 @@
 #include "gather.cuh"
 #include "ops.cuh"
 #include "ptx.cuh"
+#include "comm.cuh"
 #include "linf.cuh"
 
 namespace cpb {
@@ -1108,7 +1109,11 @@ PcgOut pcg_newton(const Prob& P, const double* V, const double* jal, const doubl
   PcgOp op = [&](const double* p, double* Ap, double* part, const void* st) {
     return hess_apply(P, p, V, jal, jbe, thr, sigma, Ap, part, st);
   };
-  return pcg_dev(*P.c, n, d, op, hess_bytes, "hess_apply", rhs, w, tol, max_iter, false);
+  // with a communicator the Newton system is node-partitioned over the ranks
+  // (everything outside the PCG stays replicated: identical on every rank)
+  const bool dist = P.c->comm != nullptr;
+  const double op_b = dist ? hess_bytes / P.c->comm->nranks : hess_bytes;
+  return pcg_dev(*P.c, n, d, op, op_b, "hess_apply", rhs, w, tol, max_iter, false, dist);
 }
 
 // Sum (and max) the columns of a (rows x cols) block-partial table on the host,

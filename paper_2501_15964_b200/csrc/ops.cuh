@@ -67,8 +67,12 @@ struct PcgOut {
 // block); returns the block count.  `cg_state` lets it no-op after the loop ends.
 using PcgOp = std::function<int(const double* p, double* Ap, double* part, const void* cg_state)>;
 // Generic device PCG (x0 = 0, or x0 = w.x when warm) on node-shaped d x n blocks.
+// dist: node-partitioned over the context's communicator (comm.cuh) — each
+// rank updates its own rows, the operator covers them (c.own_v0/own_v1), the
+// block partials are all-reduced and p (then x) all-gathered; the work
+// buffers must hold P * ceil(n / P) rows.
 PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, const char* op_name,
-               const double* rhs, PcgWork w, double tol, int64_t max_iter, bool warm);
+               const double* rhs, PcgWork w, double tol, int64_t max_iter, bool warm, bool dist = false);
 PcgOut pcg_newton(const Prob& P, const double* V, const double* jal, const double* jbe, const double* thr,
                   double sigma, const double* rhs, PcgWork w, double tol, int64_t max_iter, int64_t n_active);
 

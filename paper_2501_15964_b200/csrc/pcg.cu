@@ -17,6 +17,7 @@
 // partial sums need no atomics, loads stay coalesced along the feature axis.
 #include <cstdlib>
 
+#include "comm.cuh"
 #include "ops.cuh"
 
 namespace cpb {
@@ -214,11 +215,23 @@ __global__ void k_cg_c(const CgState* __restrict__ st, const double* __restrict_
 const int* cg_active_ptr(const void* st) { return st ? &static_cast<const CgState*>(st)->active : nullptr; }
 
 PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, const char* op_name,
-               const double* rhs, PcgWork w, double tol, int64_t max_iter, bool warm) {
-  const int64_t m = d * n;
+               const double* rhs, PcgWork w, double tol, int64_t max_iter, bool warm, bool dist) {
   if (!(tol > 0.0)) invalid("pcg: tol must be positive");
   if (max_iter < 1) invalid("pcg: max_iter must be >= 1");
-  const Tile tg = tile_geom(n, d);
+  dist = dist && c.comm != nullptr;
+  // this rank's rows [v0, v0 + nown) (all of them without a communicator)
+  const int64_t chunk = dist ? c.comm->chunk(n) : n;
+  const int64_t v0 = dist ? c.comm->v0(n) : 0;
+  const int64_t nown = dist ? c.comm->v1(n) - v0 : n;
+  const int64_t m = d * nown, off = v0 * d;
+  struct OwnScope {  // the operator covers this rank's nodes while the PCG runs
+    Ctx& c;
+    OwnScope(Ctx& c_, bool on, int64_t a, int64_t b) : c(c_) {
+      if (on) c.own_v0 = a, c.own_v1 = b;
+    }
+    ~OwnScope() { c.own_v0 = 0, c.own_v1 = -1; }
+  } own(c, dist, v0, v0 + nown);
+  const Tile tg = tile_geom(chunk, d);  // identical on every rank: partial tables line up
   const int nblk = tg.blocks();
   double* part_rz = c.buf<double>("pcg.rz", nblk + 8);
   double* part_rr = c.buf<double>("pcg.rr", static_cast<size_t>(tg.R) * d + 8);
@@ -232,8 +245,14 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
   }
   const int di = static_cast<int>(d);
   const dim3 tb(32, 8);
-  k_cg_init<<<nblk, tb, 0, c.s>>>(rhs, Mx, w.diag, n, di, tg.F, tg.rows_per, w.x, w.r, w.p, part_rz, part_rr);
+  k_cg_init<<<nblk, tb, 0, c.s>>>(rhs + off, Mx ? Mx + off : nullptr, w.diag + off, nown, di, tg.F, tg.rows_per,
+                                  w.x + off, w.r + off, w.p + off, part_rz, part_rr);
   CPB_LAUNCH_CHECK();
+  if (dist) {
+    comm_allreduce_sum(c, part_rz, nblk);
+    comm_allreduce_sum(c, part_rr, static_cast<size_t>(tg.R) * d);
+    comm_allgather(c, w.p, static_cast<size_t>(chunk * d));
+  }
   k_cg_s0<<<1, 1024, 0, c.s>>>(st, part_rz, nblk, part_rr, tg.R, di, tol, max_iter, bn, Mx != nullptr);
   CPB_LAUNCH_CHECK();
   const int fg = std::max(1, std::min(cdiv(m, 256), c.sm_count * 4));
@@ -252,10 +271,16 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
         Ctx::Timer tm(&c, op_name, op_bytes);
         hb = op(w.p, w.Ap, part_h, st);
       }
+      if (dist) comm_allreduce_sum(c, part_h, 2 * static_cast<size_t>(hb));
       {
         Ctx::Timer tm(&c, "pcg_update_b", 4.0 * m * 8.0);
-        k_cg_b<<<nblk, tb, 0, c.s>>>(st, part_h, hb, w.Ap, w.diag, n, di, tg.F, tg.rows_per, w.r, part_rz, part_rr);
+        k_cg_b<<<nblk, tb, 0, c.s>>>(st, part_h, hb, w.Ap + off, w.diag + off, nown, di, tg.F, tg.rows_per,
+                                      w.r + off, part_rz, part_rr);
         CPB_LAUNCH_CHECK();
+      }
+      if (dist) {
+        comm_allreduce_sum(c, part_rz, nblk);
+        comm_allreduce_sum(c, part_rr, static_cast<size_t>(tg.R) * d);
       }
       {
         Ctx::Timer tm(&c, "pcg_s2", 0.0);
@@ -264,9 +289,10 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
       }
       {
         Ctx::Timer tm(&c, "pcg_update_c", 6.0 * m * 8.0);
-        k_cg_c<<<fg, 256, 0, c.s>>>(st, w.r, w.diag, m, w.x, w.p);
+        k_cg_c<<<fg, 256, 0, c.s>>>(st, w.r + off, w.diag + off, m, w.x + off, w.p + off);
         CPB_LAUNCH_CHECK();
       }
+      if (dist) comm_allgather(c, w.p, static_cast<size_t>(chunk * d));
     }
     CgState h;
     CPB_CUDA(cudaMemcpyAsync(c.hscal, st, sizeof(CgState), cudaMemcpyDeviceToHost, c.s));
@@ -288,6 +314,10 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
       break;
     }
     batch = doubling ? std::min(batch * 2, 32) : (h.it < 8 ? 4 : 2 + static_cast<int>(h.it / 8));
+  }
+  if (dist) {
+    comm_allgather(c, w.x, static_cast<size_t>(chunk * d));
+    c.sync();
   }
   hint = static_cast<int>(out.iterations);
   return out;

@@ -5,6 +5,7 @@
 
 #include <cub/cub.cuh>
 
+#include "comm.cuh"
 #include "solve.cuh"
 
 namespace cpb {
@@ -80,8 +81,11 @@ cp_termination ssnal(Prob& P, const cp_solver_config& cfg, bool warm, double* Xo
   double* jal = c.buf<double>("s.jal", E);
   double* jbe = c.buf<double>("s.jbe", E);
   double* G = c.buf<double>("s.G", m);
-  PcgWork w{c.buf<double>("s.D", m), c.buf<double>("s.r", m), c.buf<double>("s.p", m), c.buf<double>("s.Ap", m),
-            c.buf<double>("s.diag", m)};
+  // PCG work arrays hold P * ceil(n / P) rows when the Newton systems are
+  // node-partitioned (in-place all-gathers of each rank's chunk)
+  const int64_t mpad = c.comm ? c.comm->chunk(n) * c.comm->nranks * d : m;
+  PcgWork w{c.buf<double>("s.D", mpad), c.buf<double>("s.r", mpad), c.buf<double>("s.p", mpad),
+            c.buf<double>("s.Ap", mpad), c.buf<double>("s.diag", mpad)};
   double* Xb = c.buf<double>("s.Xb", m);
   double* Zb = c.buf<double>("s.Zb", me);
   copy_dev(c, X, Xout, m);

@@ -483,6 +483,26 @@ def test_edge_ring_wraps_match_oracle(cp, orc, d):
     assert sol.termination.cg == osol.term["cg"] and sol.termination.newton == osol.term["newton"]
 
 
+@pytest.mark.parametrize("d,k", [(64, 8), (300, 8)])
+def test_partitioned_pcg_single_rank(cp, orc, d, k):
+    """The node-partitioned PCG (NCCL communicator attached; one rank) through
+    both Hessian paths (two-pass for d < 256, TMA for d >= 256): same solution
+    as the oracle within 1e-6 and identical labels."""
+    ctx = cp.Context(0)
+    ctx.set_comm(1, 0, cp.nccl_unique_id())
+    A = mixture(orc, 150, d, m=4, seed=31)
+    data = cp.DataMatrix(A, ctx=ctx)
+    g = cp.compute_knn_weights(data, k, 0.5)
+    og = orc.knn_weights(A, k, 0.5)
+    for gamma in (0.05, 0.2):
+        sol = cp.solve(cp.ProblemInstance(data, g, gamma, 2), cp.SolverConfig())
+        osol = orc.solve(A, og, gamma, 2, orc.config("ssnal"))
+        assert sol.termination.converged and bool(osol.term["converged"])
+        assert sol.termination.cg > 0
+        assert np.linalg.norm(sol.X - osol.X) <= 1e-6 * np.linalg.norm(osol.X)
+        assert np.array_equal(cp.extract_clusters(sol.X, g).labels, orc.extract_clusters(osol.X, og)[0])
+
+
 def test_path_parity_linf(cp, orc):
     """Warm-started SSNAL path with q = infinity (C4's prox variant): every X
     within 1e-6 relative Frobenius of the oracle path and identical labels."""
