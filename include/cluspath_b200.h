@@ -152,6 +152,13 @@ int cp_graph_from_knn(cp_ctx* ctx, int64_t n, int64_t k, double phi, const doubl
  * path on one GPU.  libnccl.so.2 is loaded at run time (CP_ENCCL if absent). */
 int cp_nccl_unique_id(char out[128]);
 int cp_ctx_set_comm(cp_ctx* ctx, int nranks, int rank, const char id[128]);
+/* In-process group of nranks contexts driven by nranks host threads (the same
+ * partitioned code path without NCCL, e.g. several ranks tested on one GPU:
+ * collectives meet at host barriers, no kernel waits on another rank). */
+typedef struct cp_local_group cp_local_group;
+int cp_local_group_create(int nranks, cp_local_group** out);
+void cp_local_group_destroy(cp_local_group* g);
+int cp_ctx_set_local_comm(cp_ctx* ctx, cp_local_group* g, int rank);
 /* Host-only: the query rows [r0, r1) of `rank` among `nranks` for the
  * row-sharded kNN: ceil(n / nranks) rows per rank, the last rank short. */
 int cp_shard_rows(int64_t n, int nranks, int rank, int64_t* r0, int64_t* r1);

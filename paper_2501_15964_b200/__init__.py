@@ -8,7 +8,7 @@ path.  All numerics run in hand-written sm_100a CUDA (libcluspath_b200.so)
 behind the C-ABI of include/cluspath_b200.h; this package is the host-side
 mirror of the reference API.
 """
-from .cluspath import (Algorithm, ClusterAssignment, Context, DataMatrix, GammaSchedule, IncidenceOperator,
+from .cluspath import (Algorithm, ClusterAssignment, Context, DataMatrix, GammaSchedule, IncidenceOperator, LocalGroup,
                        PathOptions, PathResult, PenaltyNorm, ProblemInstance, Solution, SolverConfig, Spacing,
                        TerminationRecord, WeightedGraph, algorithm_from_name, algorithm_name, component_count,
                        compute_knn_weights, compute_knn_weights_sharded, connected_components, default_context, dual_objective, duality_gap,

@@ -74,6 +74,9 @@ _SIGS = [
     ("cp_shard_rows", C.c_int, [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("cp_nccl_unique_id", C.c_int, [C.c_char_p]),
     ("cp_ctx_set_comm", C.c_int, [VP, C.c_int, C.c_int, C.c_char_p]),
+    ("cp_local_group_create", C.c_int, [C.c_int, C.POINTER(VP)]),
+    ("cp_local_group_destroy", None, [VP]),
+    ("cp_ctx_set_local_comm", C.c_int, [VP, VP, C.c_int]),
     ("cp_graph_from_edges", C.c_int, [VP, C.c_int64, I64, I64, D, C.c_int64, C.POINTER(VP)]),
     ("cp_graph_destroy", None, [VP]),
     ("cp_graph_nodes", C.c_int64, [VP]),

@@ -63,6 +63,11 @@ class Context:
             raise ValueError("NCCL unique id must be 128 bytes")
         L.check(L.load().cp_ctx_set_comm(self._h, int(nranks), int(rank), C.c_char_p(bytes(unique_id))))
 
+    def set_local_comm(self, group: "LocalGroup", rank: int):
+        """Join an in-process group (cp_ctx_set_local_comm): the partitioned
+        path with several ranks in one process (one host thread per rank)."""
+        L.check(L.load().cp_ctx_set_local_comm(self._h, group._h, int(rank)))
+
     def knn_info(self):
         """How the last compute_knn_weights on this context ran (tensor-core
         candidate pass, segments, rows re-done exactly, worst |d2~-d2|/bound)."""
@@ -305,6 +310,23 @@ def compute_knn_weights(data: DataMatrix, k: int, phi: float) -> WeightedGraph:
     h = C.c_void_p()
     L.check(L.load().cp_knn_graph(data.ctx._h, data._h, int(k), float(phi), C.byref(h)))
     return WeightedGraph(ctx=data.ctx, _handle=h)
+
+
+class LocalGroup:
+    """In-process rank group (cp_local_group): collectives meet at host
+    barriers, so several ranks can share one GPU without any kernel waiting
+    on another rank."""
+
+    def __init__(self, nranks: int):
+        h = C.c_void_p()
+        L.check(L.load().cp_local_group_create(int(nranks), C.byref(h)))
+        self._h = h
+        self.nranks = int(nranks)
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and L._lib is not None:
+            L._lib.cp_local_group_destroy(self._h)
+            self._h = None
 
 
 def nccl_unique_id() -> bytes:

@@ -336,6 +336,19 @@ int cp_ctx_set_comm(cp_ctx* ctx, int nranks, int rank, const char id[128]) {
     cpb::comm_init(*ctx->c, nranks, rank, id);
   });
 }
+int cp_local_group_create(int nranks, cp_local_group** out) {
+  return guard(nullptr, [&] {
+    need(out, "out");
+    *out = reinterpret_cast<cp_local_group*>(cpb::local_group_create(nranks));
+  });
+}
+void cp_local_group_destroy(cp_local_group* g) { cpb::local_group_destroy(reinterpret_cast<cpb::LocalGroup*>(g)); }
+int cp_ctx_set_local_comm(cp_ctx* ctx, cp_local_group* g, int rank) {
+  return guard(ctx, [&] {
+    need(g, "group");
+    cpb::comm_init_local(*ctx->c, reinterpret_cast<cpb::LocalGroup*>(g), rank);
+  });
+}
 int cp_shard_rows(int64_t n, int nranks, int rank, int64_t* r0, int64_t* r1) {
   if (n < 0 || nranks < 1 || rank < 0 || rank >= nranks || !r0 || !r1) {
     g_err = "cp_shard_rows: invalid arguments";

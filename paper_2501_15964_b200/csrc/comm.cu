@@ -2,7 +2,9 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <condition_variable>
 #include <mutex>
+#include <vector>
 
 #include "comm.cuh"
 
@@ -45,6 +47,37 @@ void check(ncclResult_t r, const char* what) {
 
 }  // namespace
 
+struct LocalGroup {
+  int n = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long gen = 0;
+  std::vector<double*> ptrs;
+  std::vector<std::vector<double>> host;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const unsigned long long g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+LocalGroup* local_group_create(int nranks) {
+  if (nranks < 1) invalid("local group: nranks must be >= 1");
+  auto* g = new LocalGroup();
+  g->n = nranks;
+  g->ptrs.assign(static_cast<size_t>(nranks), nullptr);
+  g->host.resize(static_cast<size_t>(nranks));
+  return g;
+}
+void local_group_destroy(LocalGroup* g) { delete g; }
+
 Comm::~Comm() {
   if (nccl) {
     try {
@@ -74,14 +107,48 @@ void comm_init(Ctx& c, int nranks, int rank, const char id[128]) {
   c.comm = std::move(cm);
 }
 
+void comm_init_local(Ctx& c, LocalGroup* g, int rank) {
+  if (!g || rank < 0 || rank >= g->n) invalid("communicator: rank out of range");
+  auto cm = std::make_unique<Comm>();
+  cm->local = g;
+  cm->rank = rank;
+  cm->nranks = g->n;
+  c.comm = std::move(cm);
+}
+
 void comm_allreduce_sum(Ctx& c, double* buf, size_t count) {
   if (!c.comm || count == 0) return;
+  if (LocalGroup* g = c.comm->local) {  // host sum in rank order: identical on every rank
+    const int r = c.comm->rank;
+    g->host[r].resize(count);
+    d2h(c, g->host[r].data(), buf, count * sizeof(double));
+    g->barrier();
+    std::vector<double> sum(count, 0.0);
+    for (int q = 0; q < g->n; ++q)
+      for (size_t i = 0; i < count; ++i) sum[i] += g->host[q][i];
+    g->barrier();  // nobody refills its host slot before every rank has read it
+    h2d(c, buf, sum.data(), count * sizeof(double));
+    return;
+  }
   check(nccl().allreduce(buf, buf, count, ncclFloat64, ncclSum, static_cast<ncclComm_t>(c.comm->nccl), c.s),
         "ncclAllReduce");
 }
 
 void comm_allgather(Ctx& c, double* base, size_t chunk_elems) {
   if (!c.comm || chunk_elems == 0) return;
+  if (LocalGroup* g = c.comm->local) {  // device-to-device copies of the other ranks' chunks
+    const int r = c.comm->rank;
+    c.sync();
+    g->ptrs[r] = base;
+    g->barrier();
+    for (int q = 0; q < g->n; ++q)
+      if (q != r)
+        CPB_CUDA(cudaMemcpyAsync(base + q * chunk_elems, g->ptrs[q] + q * chunk_elems, chunk_elems * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, c.s));
+    c.sync();
+    g->barrier();  // every rank has copied before anyone writes its chunk again
+    return;
+  }
   check(nccl().allgather(base + static_cast<size_t>(c.comm->rank) * chunk_elems, base, chunk_elems, ncclFloat64,
                          static_cast<ncclComm_t>(c.comm->nccl), c.s),
         "ncclAllGather");

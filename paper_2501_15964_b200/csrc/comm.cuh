@@ -14,8 +14,16 @@
 
 namespace cpb {
 
+// In-process group: P contexts driven by P host threads (tests on one GPU).
+// Collectives synchronise the ranks' streams and meet at a host barrier; no
+// kernel ever waits on another rank, so ranks sharing a GPU cannot deadlock.
+struct LocalGroup;
+LocalGroup* local_group_create(int nranks);
+void local_group_destroy(LocalGroup* g);
+
 struct Comm {
-  void* nccl = nullptr;  // ncclComm_t
+  void* nccl = nullptr;         // ncclComm_t
+  LocalGroup* local = nullptr;  // or an in-process group
   int rank = 0, nranks = 1;
   ~Comm();
   int64_t chunk(int64_t n) const { return (n + nranks - 1) / nranks; }
@@ -26,6 +34,7 @@ struct Comm {
 // 128-byte NCCL unique id (rank 0 creates it, the caller distributes it).
 void comm_unique_id(char out[128]);
 void comm_init(Ctx& c, int nranks, int rank, const char id[128]);
+void comm_init_local(Ctx& c, LocalGroup* g, int rank);
 // In-place sum over the ranks of `count` doubles on the context stream.
 void comm_allreduce_sum(Ctx& c, double* buf, size_t count);
 // In-place all-gather: rank r's `chunk_elems` doubles at base + r * chunk_elems.

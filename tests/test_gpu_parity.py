@@ -503,6 +503,47 @@ def test_partitioned_pcg_single_rank(cp, orc, d, k):
         assert np.array_equal(cp.extract_clusters(sol.X, g).labels, orc.extract_clusters(osol.X, og)[0])
 
 
+@pytest.mark.parametrize("nranks,d", [(2, 64), (3, 300), (4, 784)])
+def test_partitioned_path_multi_rank(cp, orc, nranks, d):
+    """P ranks in one process (one host thread and context each, in-process
+    group): the node-partitioned Newton PCG of a warm-started path matches the
+    single-context path within 1e-6 at every gamma with identical labels, and
+    every rank returns the same result bit for bit."""
+    import threading
+    A = mixture(orc, 90, d, m=4, seed=41)
+    g0 = cp.compute_knn_weights(cp.DataMatrix(A), 8, 0.5)
+    sched = cp.make_schedule(0.02, 2.0, 6)
+    ref = cp.run_path(cp.DataMatrix(A), g0, 2, sched, cp.SolverConfig())
+    group = cp.LocalGroup(nranks)
+    ctxs = [cp.Context(0) for _ in range(nranks)]
+    for r, c in enumerate(ctxs):
+        c.set_local_comm(group, r)
+    datas = [cp.DataMatrix(A, ctx=c) for c in ctxs]
+    graphs = [cp.compute_knn_weights(dm, 8, 0.5) for dm in datas]
+    out, errs = [None] * nranks, []
+
+    def work(r):
+        try:
+            out[r] = cp.run_path(datas[r], graphs[r], 2, sched, cp.SolverConfig())
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(300)
+    assert not errs, errs
+    for t in range(len(sched.values)):
+        X0 = ref.solutions[t].X
+        for r in range(nranks):
+            assert np.linalg.norm(out[r].solutions[t].X - X0) <= 1e-6 * np.linalg.norm(X0)
+            assert np.array_equal(out[r].assignments[t].labels, ref.assignments[t].labels)
+            assert np.array_equal(out[r].solutions[t].X, out[0].solutions[t].X)
+        assert out[0].stats[t].converged
+    assert sum(s.cg for s in out[0].stats) > 0
+
+
 def test_path_parity_linf(cp, orc):
     """Warm-started SSNAL path with q = infinity (C4's prox variant): every X
     within 1e-6 relative Frobenius of the oracle path and identical labels."""
