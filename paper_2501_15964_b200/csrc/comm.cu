@@ -2,6 +2,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <condition_variable>
 #include <mutex>
 #include <vector>
@@ -19,6 +20,9 @@ struct Nccl {
   decltype(&ncclAllReduce) allreduce = nullptr;
   decltype(&ncclAllGather) allgather = nullptr;
   decltype(&ncclGetErrorString) errstr = nullptr;
+  decltype(&ncclBroadcast) bcast = nullptr;
+  decltype(&ncclGroupStart) gstart = nullptr;
+  decltype(&ncclGroupEnd) gend = nullptr;
 };
 
 const Nccl& nccl() {
@@ -34,8 +38,11 @@ const Nccl& nccl() {
     n.allreduce = reinterpret_cast<decltype(n.allreduce)>(dlsym(h, "ncclAllReduce"));
     n.allgather = reinterpret_cast<decltype(n.allgather)>(dlsym(h, "ncclAllGather"));
     n.errstr = reinterpret_cast<decltype(n.errstr)>(dlsym(h, "ncclGetErrorString"));
+    n.bcast = reinterpret_cast<decltype(n.bcast)>(dlsym(h, "ncclBroadcast"));
+    n.gstart = reinterpret_cast<decltype(n.gstart)>(dlsym(h, "ncclGroupStart"));
+    n.gend = reinterpret_cast<decltype(n.gend)>(dlsym(h, "ncclGroupEnd"));
   });
-  if (!n.get_id || !n.init || !n.destroy || !n.allreduce || !n.allgather)
+  if (!n.get_id || !n.init || !n.destroy || !n.allreduce || !n.allgather || !n.bcast || !n.gstart || !n.gend)
     throw Error(CP_ENCCL, "NCCL (libnccl.so.2) is not available in this process");
   return n;
 }
@@ -132,6 +139,65 @@ void comm_allreduce_sum(Ctx& c, double* buf, size_t count) {
   }
   check(nccl().allreduce(buf, buf, count, ncclFloat64, ncclSum, static_cast<ncclComm_t>(c.comm->nccl), c.s),
         "ncclAllReduce");
+}
+
+void comm_allreduce_max(Ctx& c, double* buf, size_t count) {
+  if (!c.comm || count == 0) return;
+  if (LocalGroup* g = c.comm->local) {
+    const int r = c.comm->rank;
+    g->host[r].resize(count);
+    d2h(c, g->host[r].data(), buf, count * sizeof(double));
+    g->barrier();
+    std::vector<double> mx(g->host[0]);
+    for (int q = 1; q < g->n; ++q)
+      for (size_t i = 0; i < count; ++i) mx[i] = std::max(mx[i], g->host[q][i]);
+    g->barrier();
+    h2d(c, buf, mx.data(), count * sizeof(double));
+    return;
+  }
+  check(nccl().allreduce(buf, buf, count, ncclFloat64, ncclMax, static_cast<ncclComm_t>(c.comm->nccl), c.s),
+        "ncclAllReduce(max)");
+}
+
+void comm_allreduce_host(Ctx& c, std::vector<double>& v, const std::vector<int>& max_cols) {
+  if (!c.comm || v.empty()) return;
+  const size_t k = v.size();
+  std::vector<double> buf(2 * k, 0.0);
+  for (size_t i = 0; i < k; ++i) buf[i] = v[i], buf[k + i] = -1e300;
+  for (int mcol : max_cols) buf[k + mcol] = v[static_cast<size_t>(mcol)], buf[static_cast<size_t>(mcol)] = 0.0;
+  double* d = c.buf<double>("comm.host", 2 * k);
+  h2d(c, d, buf.data(), 2 * k * sizeof(double));
+  comm_allreduce_sum(c, d, k);
+  comm_allreduce_max(c, d + k, k);
+  d2h(c, buf.data(), d, 2 * k * sizeof(double));
+  for (size_t i = 0; i < k; ++i) v[i] = buf[i];
+  for (int mcol : max_cols) v[static_cast<size_t>(mcol)] = buf[k + mcol];
+}
+
+void comm_allgatherv_rows(Ctx& c, double* base, const std::vector<int64_t>& row0, const std::vector<int64_t>& rows,
+                          int64_t d) {
+  if (!c.comm) return;
+  if (LocalGroup* g = c.comm->local) {
+    const int r = c.comm->rank;
+    c.sync();
+    g->ptrs[r] = base;
+    g->barrier();
+    for (int q = 0; q < g->n; ++q)
+      if (q != r && rows[q] > 0)
+        CPB_CUDA(cudaMemcpyAsync(base + row0[q] * d, g->ptrs[q] + row0[q] * d, rows[q] * d * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, c.s));
+    c.sync();
+    g->barrier();
+    return;
+  }
+  const Nccl& n = nccl();
+  check(n.gstart(), "ncclGroupStart");
+  for (int q = 0; q < c.comm->nranks; ++q)
+    if (rows[q] > 0)
+      check(n.bcast(base + row0[q] * d, base + row0[q] * d, static_cast<size_t>(rows[q] * d), ncclFloat64, q,
+                    static_cast<ncclComm_t>(c.comm->nccl), c.s),
+            "ncclBroadcast");
+  check(n.gend(), "ncclGroupEnd");
 }
 
 void comm_allgather(Ctx& c, double* base, size_t chunk_elems) {

@@ -12,6 +12,8 @@
 
 #include "common.cuh"
 
+#include <vector>
+
 namespace cpb {
 
 // In-process group: P contexts driven by P host threads (tests on one GPU).
@@ -39,5 +41,12 @@ void comm_init_local(Ctx& c, LocalGroup* g, int rank);
 void comm_allreduce_sum(Ctx& c, double* buf, size_t count);
 // In-place all-gather: rank r's `chunk_elems` doubles at base + r * chunk_elems.
 void comm_allgather(Ctx& c, double* base, size_t chunk_elems);
+// In-place max over the ranks.
+void comm_allreduce_max(Ctx& c, double* buf, size_t count);
+// In-place all-gather of variable row ranges: rank q owns rows [row0[q], row0[q] + rows[q]) of width d.
+void comm_allgatherv_rows(Ctx& c, double* base, const std::vector<int64_t>& row0, const std::vector<int64_t>& rows,
+                          int64_t d);
+// Host values: sums except the entries in max_cols, which are maxed.
+void comm_allreduce_host(Ctx& c, std::vector<double>& v, const std::vector<int>& max_cols = {});
 
 }  // namespace cpb

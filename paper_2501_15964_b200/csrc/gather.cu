@@ -12,6 +12,9 @@
 // scatter order (graph.cpp:140-152), bitwise.
 #include <cstdlib>
 
+#include <algorithm>
+
+#include "comm.cuh"
 #include "gather.cuh"
 
 namespace cpb {
@@ -515,6 +518,81 @@ NodeGeom node_geom(Ctx& c, int64_t n, int64_t d) {
   const int di = static_cast<int>(d);        \
   const int nch = ng.gy;
 
+// Partitioned PCG (c.own_v1 >= 0): the gather visits only this rank's nodes,
+// in the graph's degree order; cached per (graph, range).
+struct OwnOrder {
+  uint64_t uid = 0;
+  int64_t v0 = 0, v1 = -1, count = 0;
+  DBuf<int> order;
+};
+const OwnOrder& own_order(Ctx& c, const Graph& g) {
+  static thread_local std::vector<std::unique_ptr<OwnOrder>> cache;
+  for (auto& o : cache)
+    if (o->uid == g.uid && o->v0 == c.own_v0 && o->v1 == c.own_v1) return *o;
+  auto o = std::make_unique<OwnOrder>();
+  o->uid = g.uid, o->v0 = c.own_v0, o->v1 = c.own_v1;
+  std::vector<int> all(static_cast<size_t>(g.n)), mine;
+  if (g.n) d2h(c, all.data(), g.order.p, all.size() * sizeof(int));
+  for (int v : all)
+    if (v >= c.own_v0 && v < c.own_v1) mine.push_back(v);
+  o->count = static_cast<int64_t>(mine.size());
+  o->order.resize(mine.size() + 1);
+  if (!mine.empty()) h2d(c, o->order.p, mine.data(), mine.size() * sizeof(int));
+  c.sync();
+  if (cache.size() > 8) cache.erase(cache.begin());
+  cache.push_back(std::move(o));
+  return *cache.back();
+}
+
+// Work items of the node gathers: every node, or this rank's in a partitioned solve.
+struct Items {
+  const int* order;
+  int64_t count;
+};
+Items node_items(Ctx& c, const Graph& g) {
+  if (c.own_v1 < 0) return {g.order.p, g.n};
+  const OwnOrder& o = own_order(c, g);
+  return {o.order.p, o.count};
+}
+
+const EdgePart& edge_part(Ctx& c, const Graph& g) {
+  static thread_local std::vector<std::unique_ptr<EdgePart>> cache;
+  const int P = c.comm ? c.comm->nranks : 1;
+  for (auto& e : cache)
+    if (e->uid == g.uid && e->v0 == c.own_v0 && e->v1 == c.own_v1 && e->nranks == P) return *e;
+  auto e = std::make_unique<EdgePart>();
+  e->uid = g.uid, e->v0 = c.own_v0, e->v1 = c.own_v1, e->nranks = P;
+  std::vector<int> ei(static_cast<size_t>(g.E)), ej(static_cast<size_t>(g.E));
+  if (g.E) {
+    d2h(c, ei.data(), g.ei.p, ei.size() * sizeof(int));
+    d2h(c, ej.data(), g.ej.p, ej.size() * sizeof(int));
+  }
+  auto first_at_least = [&](int64_t v) {  // edges are sorted by (i, j): the owned ones are contiguous
+    return static_cast<int64_t>(std::lower_bound(ei.begin(), ei.end(), static_cast<int>(std::min<int64_t>(v, g.n))) -
+                                ei.begin());
+  };
+  const int64_t chunk = (g.n + P - 1) / P;
+  for (int q = 0; q < P; ++q) {
+    const int64_t a = first_at_least(std::min<int64_t>(g.n, chunk * q));
+    const int64_t b = first_at_least(std::min<int64_t>(g.n, chunk * (q + 1)));
+    e->row0.push_back(a);
+    e->rows.push_back(b - a);
+  }
+  e->e0 = first_at_least(c.own_v0);
+  e->e1 = first_at_least(c.own_v1);
+  std::vector<int> ghost;  // edges into an owned node from a lower-id node of another rank
+  for (int64_t l = 0; l < e->e0; ++l)
+    if (ej[static_cast<size_t>(l)] >= c.own_v0 && ej[static_cast<size_t>(l)] < c.own_v1)
+      ghost.push_back(static_cast<int>(l));
+  e->nghost = static_cast<int64_t>(ghost.size());
+  e->ghost.resize(ghost.size() + 1);
+  if (!ghost.empty()) h2d(c, e->ghost.p, ghost.data(), ghost.size() * sizeof(int));
+  c.sync();
+  if (cache.size() > 8) cache.erase(cache.begin());
+  cache.push_back(std::move(e));
+  return *cache.back();
+}
+
 void gather_bt(Ctx& c, const Graph& g, const double* Z, int64_t d, double* out) {
   if (g.n == 0 || d == 0) return;
   GEOM
@@ -551,8 +629,9 @@ int gather_lap(Ctx& c, const Graph& g, const double* y, double rho, int64_t d, d
 
 int gather_gap(Ctx& c, const Graph& g, const double* X, const double* A, const double* Z, int64_t d, double* part) {
   GEOM
-  NF_DISPATCH(ng.nf, k_g_gap, <<<ng.grid, 256, 0, c.s>>>(X, A, Z, g.off.p, g.adj_e.p, g.adj_o.p, g.order.p, g.n, di,
-                                                          nch, part));
+  const Items it = node_items(c, g);
+  NF_DISPATCH(ng.nf, k_g_gap, <<<ng.grid, 256, 0, c.s>>>(X, A, Z, g.off.p, g.adj_e.p, g.adj_o.p, it.order, it.count,
+                                                          di, nch, part));
   CPB_LAUNCH_CHECK();
   return ng.grid;
 }
@@ -561,37 +640,12 @@ int gather_grad_diag(Ctx& c, const Graph& g, const double* X, const double* A, c
                      const double* jal, const double* jbe, const double* thr, int64_t d, double sigma, int q,
                      bool want_diag, double* G, double* diag, double* part) {
   GEOM
+  const Items it = node_items(c, g);
   NF_DISPATCH(ng.nf, k_g_grad, <<<ng.grid, 256, 0, c.s>>>(X, A, V, ps, jal, jbe, thr, g.off.p, g.adj_e.p, g.adj_o.p,
-                                                           g.order.p, g.n, di, nch, sigma, q, want_diag ? 1 : 0, G,
-                                                           diag, part));
+                                                           it.order, it.count, di, nch, sigma, q, want_diag ? 1 : 0,
+                                                           G, diag, part));
   CPB_LAUNCH_CHECK();
   return ng.grid;
-}
-
-// Partitioned PCG (c.own_v1 >= 0): the gather visits only this rank's nodes,
-// in the graph's degree order; cached per (graph, range).
-struct OwnOrder {
-  uint64_t uid = 0;
-  int64_t v0 = 0, v1 = -1, count = 0;
-  DBuf<int> order;
-};
-const OwnOrder& own_order(Ctx& c, const Graph& g) {
-  static thread_local std::vector<std::unique_ptr<OwnOrder>> cache;
-  for (auto& o : cache)
-    if (o->uid == g.uid && o->v0 == c.own_v0 && o->v1 == c.own_v1) return *o;
-  auto o = std::make_unique<OwnOrder>();
-  o->uid = g.uid, o->v0 = c.own_v0, o->v1 = c.own_v1;
-  std::vector<int> all(static_cast<size_t>(g.n)), mine;
-  if (g.n) d2h(c, all.data(), g.order.p, all.size() * sizeof(int));
-  for (int v : all)
-    if (v >= c.own_v0 && v < c.own_v1) mine.push_back(v);
-  o->count = static_cast<int64_t>(mine.size());
-  o->order.resize(mine.size() + 1);
-  if (!mine.empty()) h2d(c, o->order.p, mine.data(), mine.size() * sizeof(int));
-  c.sync();
-  if (cache.size() > 8) cache.erase(cache.begin());
-  cache.push_back(std::move(o));
-  return *cache.back();
 }
 
 int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,

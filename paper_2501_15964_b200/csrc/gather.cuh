@@ -44,6 +44,20 @@ int gather_grad_diag(Ctx& c, const Graph& g, const double* X, const double* A, c
 bool hess_tma_supported(int64_t d);
 int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,
              int64_t d, double sigma, double* Ap, double* part, const int* active);
+// Edge ownership in a partitioned solve (c.own range): this rank's owned edges
+// are the contiguous ids [e0, e1) (smaller endpoint owned); ghost edges enter an
+// owned node from another rank's node (computed redundantly, never summed);
+// row0/rows: every rank's owned range (to assemble full edge arrays).
+struct EdgePart {
+  uint64_t uid = 0;
+  int64_t v0 = 0, v1 = -1;
+  int nranks = 1;
+  int64_t e0 = 0, e1 = 0, nghost = 0;
+  DBuf<int> ghost;
+  std::vector<int64_t> row0, rows;
+};
+const EdgePart& edge_part(Ctx& c, const Graph& g);
+
 int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,
                   const double* thr, int64_t d, double sigma, int q, double* bc, double* Ap, double* part,
                   const int* active);

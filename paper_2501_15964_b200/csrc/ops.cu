@@ -44,6 +44,16 @@ __device__ __forceinline__ double soft(double v, double t) { return sgnd(v) * fm
   for (int64_t row_ = blockIdx.x * static_cast<int64_t>(blockDim.y) + threadIdx.y; row_ < (rows); \
        row_ += static_cast<int64_t>(gridDim.x) * blockDim.y)
 
+// A node-partitioned SSNAL solve is running on this context (solve.cu sets the
+// owned node range for the whole solve when a communicator is attached).
+inline bool partitioned(const Ctx& c) { return c.comm && c.own_v1 >= 0; }
+
+// Edge rows of an EdgeSel, one group (blockDim.x lanes) per edge.
+#define EDGES_BEGIN(sel)                                                                                    \
+  for (int64_t i_ = blockIdx.x * static_cast<int64_t>(blockDim.y) + threadIdx.y; i_ < (sel).count;       \
+       i_ += static_cast<int64_t>(gridDim.x) * blockDim.y)                                                 \
+    if (const int64_t row_ = (sel).at(i_); true)
+
 // ---- flat vector kernels ----------------------------------------------------------
 __global__ void k_scale(const double* __restrict__ x, double s, int64_t m, double* __restrict__ out) {
   for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
@@ -183,12 +193,12 @@ __global__ void k_jac_diag_cols(int q, const double* __restrict__ V, const doubl
 //   sum_l gamma w_l ||P_l||_q + sigma/2 ||P_l - V_l||^2.
 __global__ void k_phi_edge(const double* __restrict__ X, const double* __restrict__ Z, const int* __restrict__ ei,
                            const int* __restrict__ ej, const double* __restrict__ thr, const double* __restrict__ rad,
-                           int64_t E, int d, double sigma, int q, double* __restrict__ V, double* __restrict__ nv,
-                           double* part) {
+                           EdgeSel sel, int d, double sigma, int q, double* __restrict__ V, double* __restrict__ nv,
+                           double* __restrict__ nvc, double* part) {
   __shared__ double sh[32];
   const unsigned gm = group_mask();
   double acc = 0.0;
-  ROWS_BEGIN(E) {
+  EDGES_BEGIN(sel) {
     const double* xa = X + static_cast<int64_t>(ei[row_]) * d;
     const double* xb = X + static_cast<int64_t>(ej[row_]) * d;
     const double* z = Z + row_ * d;
@@ -228,7 +238,7 @@ __global__ void k_phi_edge(const double* __restrict__ X, const double* __restric
       env = rad[row_] * (th < 0.0 ? 0.0 : th) + (0.5 * sigma) * group_sum(sq, gm);
       if (threadIdx.x == 0) {
         nv[row_] = th;
-        nv[E + row_] = cnt;
+        nvc[row_] = cnt;
       }
     } else {
       double a = 0.0, b = 0.0;
@@ -351,11 +361,11 @@ __device__ __forceinline__ void gap_edge_terms(const double* xa, const double* x
 
 __global__ void k_gap_edge(const double* __restrict__ X, const double* __restrict__ Z, const int* __restrict__ ei,
                            const int* __restrict__ ej, const double* __restrict__ rad, const double* __restrict__ w,
-                           int64_t E, int d, int q, double* part) {
+                           EdgeSel sel, int d, int q, double* part) {
   __shared__ double sh[32];
   const unsigned gm = group_mask();
   double s[4] = {0, 0, 0, 0}, excess = -1.0;
-  ROWS_BEGIN(E) {
+  EDGES_BEGIN(sel) {
     double t4[4];
     gap_edge_terms(X + static_cast<int64_t>(ei[row_]) * d, X + static_cast<int64_t>(ej[row_]) * d, Z + row_ * d,
                    rad[row_], w[row_], d, q, gm, t4, excess);
@@ -375,12 +385,12 @@ __global__ void k_gap_edge(const double* __restrict__ X, const double* __restric
 // [6] max |Z + sigma XB| (pre-projection), [7] max |Zenv - Zsum|, [8] dual excess
 __global__ void k_mult(const double* __restrict__ X, double* __restrict__ Z, const double* __restrict__ V,
                        const double* __restrict__ ps, const double* __restrict__ thr, const double* __restrict__ rad,
-                       const double* __restrict__ w, const int* __restrict__ ei, const int* __restrict__ ej, int64_t E,
+                       const double* __restrict__ w, const int* __restrict__ ei, const int* __restrict__ ej, EdgeSel sel,
                        int d, double sigma, int q, double* part) {
   __shared__ double sh[32];
   const unsigned gm = group_mask();
   double s[5] = {0, 0, 0, 0, 0}, mx = 0.0, err = 0.0, excess = -1.0;
-  ROWS_BEGIN(E) {
+  EDGES_BEGIN(sel) {
     const double* xa = X + static_cast<int64_t>(ei[row_]) * d;
     const double* xb = X + static_cast<int64_t>(ej[row_]) * d;
     double* z = Z + row_ * d;
@@ -477,11 +487,11 @@ __global__ void k_mult(const double* __restrict__ X, double* __restrict__ Z, con
 __global__ void k_mult_inf(const double* __restrict__ X, double* __restrict__ Z, const double* __restrict__ V,
                            const double* __restrict__ ps, const double* __restrict__ rad,
                            const double* __restrict__ w, const int* __restrict__ ei, const int* __restrict__ ej,
-                           int64_t E, int d, double sigma, double* part) {
+                           EdgeSel sel, int d, double sigma, double* part) {
   __shared__ double sh[32];
   const unsigned gm = group_mask();
   double s[5] = {0, 0, 0, 0, 0}, mx = 0.0, err = 0.0, excess = -1.0;
-  ROWS_BEGIN(E) {
+  EDGES_BEGIN(sel) {
     const double* xa = X + static_cast<int64_t>(ei[row_]) * d;
     const double* xb = X + static_cast<int64_t>(ej[row_]) * d;
     double* z = Z + row_ * d;
@@ -570,13 +580,13 @@ template <int Q>
 __global__ void __launch_bounds__(32 * kMultWarps) k_mult_s(
     const double* __restrict__ X, double* __restrict__ Z, const double* __restrict__ V, const double* __restrict__ ps,
     const double* __restrict__ thr, const double* __restrict__ rad, const double* __restrict__ w,
-    const int* __restrict__ ei, const int* __restrict__ ej, int64_t E, int d, double sigma, double* part) {
+    const int* __restrict__ ei, const int* __restrict__ ej, EdgeSel sel, int d, double sigma, double* part) {
   extern __shared__ double srow[];
   __shared__ double sh[32];
   double* sx = srow + static_cast<size_t>(threadIdx.y) * 2 * d;
   double* sz = sx + d;
   double s[5] = {0, 0, 0, 0, 0}, mx = 0.0, err = 0.0, excess = -1.0;
-  ROWS_BEGIN(E) {
+  EDGES_BEGIN(sel) {
     const double* xa = X + static_cast<int64_t>(ei[row_]) * d;
     const double* xb = X + static_cast<int64_t>(ej[row_]) * d;
     double* z = Z + row_ * d;
@@ -678,7 +688,7 @@ template <int Q, bool VS>
 __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
     const double* __restrict__ X, double* __restrict__ Z, const double* __restrict__ V, const double* __restrict__ ps,
     const double* __restrict__ thr, const double* __restrict__ rad, const double* __restrict__ w,
-    const int* __restrict__ ei, const int* __restrict__ ej, int64_t E, int d, double sigma, double* part, int S) {
+    const int* __restrict__ ei, const int* __restrict__ ej, EdgeSel sel, int d, double sigma, double* part, int S) {
   extern __shared__ __align__(16) double trow[];
   __shared__ double sh[32];
   __shared__ uint64_t bars[kMultWarps][kEdgeMaxStages];
@@ -691,11 +701,11 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
   const unsigned rb = static_cast<unsigned>(d) * 8u;
   const int64_t wid = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * blockDim.y;
-  const int64_t cnt = wid < E ? (E - wid + nw - 1) / nw : 0;  // this warp's edges: wid + e nw
+  const int64_t cnt = wid < sel.count ? (sel.count - wid + nw - 1) / nw : 0;  // this warp's edges: wid + e nw
   constexpr int NR = VS ? 4 : 3;  // staged rows per edge (V_l staged or streamed)
   double* const base = trow + static_cast<size_t>(threadIdx.y) * S * NR * d;
   auto issue = [&](int64_t e, int q) {  // lane 0: x_i, x_j, Z_l, V_l of edge wid + e nw into slot q
-    const int64_t l = wid + e * nw;
+    const int64_t l = sel.at(wid + e * nw);
     double* sx = base + static_cast<size_t>(q) * NR * d;
     uint64_t* b = &bar[q];
     fence_proxy_async();
@@ -712,7 +722,7 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
   int q = 0;
   unsigned ph = 0;
   for (int64_t it = 0; it < cnt; ++it) {
-    const int64_t row_ = wid + it * nw;
+    const int64_t row_ = sel.at(wid + it * nw);
     double* sx = base + static_cast<size_t>(q) * NR * d;  // x_i, then x = x_i - x_j
     double* sb = sx + d;   // x_j
     double* sz = sb + d;   // Z_l, then Zsum, then Z_l new
@@ -817,7 +827,7 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
 template <int Q>
 __global__ void __launch_bounds__(32 * kMultWarps) k_phi_edge_t(
     const double* __restrict__ X, const double* __restrict__ Z, const int* __restrict__ ei,
-    const int* __restrict__ ej, const double* __restrict__ thr, const double* __restrict__ rad, int64_t E, int d,
+    const int* __restrict__ ej, const double* __restrict__ thr, const double* __restrict__ rad, EdgeSel sel, int d,
     double sigma, double* __restrict__ V, double* __restrict__ nv, double* part, int S) {
   extern __shared__ __align__(16) double prow[];
   __shared__ double sh[32];
@@ -831,10 +841,10 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_phi_edge_t(
   const unsigned rb = static_cast<unsigned>(d) * 8u;
   const int64_t wid = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * blockDim.y;
-  const int64_t cnt = wid < E ? (E - wid + nw - 1) / nw : 0;
+  const int64_t cnt = wid < sel.count ? (sel.count - wid + nw - 1) / nw : 0;
   double* const base = prow + static_cast<size_t>(threadIdx.y) * S * 3 * d;
   auto issue = [&](int64_t e, int q) {
-    const int64_t l = wid + e * nw;
+    const int64_t l = sel.at(wid + e * nw);
     double* sa = base + static_cast<size_t>(q) * 3 * d;
     uint64_t* b = &bar[q];
     fence_proxy_async();
@@ -849,7 +859,7 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_phi_edge_t(
   int q = 0;
   unsigned ph = 0;
   for (int64_t e = 0; e < cnt; ++e) {
-    const int64_t row_ = wid + e * nw;
+    const int64_t row_ = sel.at(wid + e * nw);
     double* sa = base + static_cast<size_t>(q) * 3 * d;
     double* sb = sa + d;
     double* sz = sb + d;
@@ -1026,38 +1036,50 @@ double eval_phi(const Prob& P, const double* X, const double* D, double alpha, d
   }
   reduce_sum(c, pn, fg, c.dscal);
   if (E > 0) {
-    GroupGeom gg = group_geom(c, E, d);
-    double* pe = part_buf(c, "phi.pe", std::max({gg.grid, edge_grid(c, E), c.sm_count * 64}));
-    int nb = gg.grid;
-    Ctx::Timer tm(&c, "phi_edge", (2.0 * E * d + n * d + 4.0 * E) * 8.0);
-    if (edge_reg_supported(d) && P.q != Q_LINF) {
-      nb = phi_edge_reg(c, *P.g, Xe, Z, thr, P.rad, d, sigma, P.q, V, nv, pe);
-    } else if (gg.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1) &&
-               std::getenv("CPB_PHI_NOTMA") == nullptr) {
-      const int S = edge_stages(d, 3);
-      const size_t smem = static_cast<size_t>(kMultWarps) * S * 3 * d * sizeof(double);
-      static bool attr = false;
-      if (!attr) {
-        CPB_CUDA(cudaFuncSetAttribute(k_phi_edge_t<Q_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        CPB_CUDA(cudaFuncSetAttribute(k_phi_edge_t<Q_L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        attr = true;
+    // one launch over an edge selection; returns the number of block partials in pe_
+    auto run = [&](EdgeSel sel, double* pe_) -> int {
+      GroupGeom gg = group_geom(c, sel.count, d);
+      int nb = gg.grid;
+      if (edge_reg_supported(d) && P.q != Q_LINF && sel.list == nullptr && sel.e0 == 0 && sel.count == E) {
+        nb = phi_edge_reg(c, *P.g, Xe, Z, thr, P.rad, d, sigma, P.q, V, nv, pe_);
+      } else if (gg.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1) &&
+                 std::getenv("CPB_PHI_NOTMA") == nullptr) {
+        const int S = edge_stages(d, 3);
+        const size_t smem = static_cast<size_t>(kMultWarps) * S * 3 * d * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+          CPB_CUDA(cudaFuncSetAttribute(k_phi_edge_t<Q_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+          CPB_CUDA(cudaFuncSetAttribute(k_phi_edge_t<Q_L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+          attr = true;
+        }
+        int per_sm = 0;
+        CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_phi_edge_t<Q_L2>, 32 * kMultWarps, smem));
+        nb = std::max(1, std::min(cdiv(sel.count, kMultWarps), c.sm_count * std::max(1, per_sm)));
+        if (P.q == Q_L2)
+          k_phi_edge_t<Q_L2><<<nb, dim3(32, kMultWarps), smem, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, sel,
+                                                                      static_cast<int>(d), sigma, V, nv, pe_, S);
+        else
+          k_phi_edge_t<Q_L1><<<nb, dim3(32, kMultWarps), smem, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, sel,
+                                                                      static_cast<int>(d), sigma, V, nv, pe_, S);
+        CPB_LAUNCH_CHECK();
+      } else {
+        k_phi_edge<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, sel,
+                                                            static_cast<int>(d), sigma, P.q, V, nv, nv + E, pe_);
+        CPB_LAUNCH_CHECK();
       }
-      int per_sm = 0;
-      CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_phi_edge_t<Q_L2>, 32 * kMultWarps, smem));
-      nb = std::max(1, std::min(cdiv(E, kMultWarps), c.sm_count * std::max(1, per_sm)));
-      if (P.q == Q_L2)
-        k_phi_edge_t<Q_L2><<<nb, dim3(32, kMultWarps), smem, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, E,
-                                                                    static_cast<int>(d), sigma, V, nv, pe, S);
-      else
-        k_phi_edge_t<Q_L1><<<nb, dim3(32, kMultWarps), smem, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, E,
-                                                                    static_cast<int>(d), sigma, V, nv, pe, S);
-      CPB_LAUNCH_CHECK();
-    } else {
-      k_phi_edge<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, E,
-                                                          static_cast<int>(d), sigma, P.q, V, nv, pe);
-      CPB_LAUNCH_CHECK();
+      return nb;
+    };
+    const size_t pe_n = std::max({group_geom(c, E, d).grid, edge_grid(c, E), c.sm_count * 64});
+    double* pe = part_buf(c, "phi.pe", pe_n);
+    Ctx::Timer tm(&c, "phi_edge", (2.0 * E * d + n * d + 4.0 * E) * 8.0);
+    if (!partitioned(c)) {
+      reduce_sum(c, pe, run(EdgeSel{nullptr, 0, E}, pe), c.dscal + 1);
+    } else {  // owned edges (summed) + ghost edges (their V feeds this rank's gathers)
+      const EdgePart& ep = edge_part(c, *P.g);
+      reduce_sum(c, pe, run(EdgeSel{nullptr, ep.e0, ep.e1 - ep.e0}, pe), c.dscal + 1);
+      if (ep.nghost) run(EdgeSel{ep.ghost.p, 0, ep.nghost}, part_buf(c, "phi.pg", pe_n));
+      comm_allreduce_sum(c, c.dscal + 1, 1);
     }
-    reduce_sum(c, pe, nb, c.dscal + 1);
   } else {
     fill(c, c.dscal + 1, 1, 0.0);
   }
@@ -1089,6 +1111,7 @@ double grad_diag(const Prob& P, const double* X, const double* V, const double* 
     nb = gather_grad_diag(c, *P.g, X, P.A->A.p, V, ps, jal, jbe, thr, d, sigma, P.q, want_diag, G, diag, part);
   }
   reduce_sum(c, part, nb, c.dscal);
+  if (partitioned(c)) comm_allreduce_sum(c, c.dscal, 1);  // ||G||^2 over every rank's rows
   return fetch1(c);
 }
 
@@ -1142,18 +1165,25 @@ GapOut eval_gap(const Prob& P, const double* X, const double* Z) {
     nbn = gather_gap(c, *P.g, X, P.A->A.p, Z, d, pn);
   }
   std::vector<double> h = host_cols(c, pn, nbn, 4);
+  if (partitioned(c)) comm_allreduce_host(c, h);
   std::vector<double> e(5, 0.0);
   e[4] = -1.0;
   if (E > 0) {
-    GroupGeom ge = group_geom(c, E, d);
+    EdgeSel sel{nullptr, 0, E};
+    if (partitioned(c)) {
+      const EdgePart& ep = edge_part(c, *P.g);
+      sel = EdgeSel{nullptr, ep.e0, ep.e1 - ep.e0};
+    }
+    GroupGeom ge = group_geom(c, sel.count, d);
     double* pe = part_buf(c, "gap.pe", 5 * static_cast<size_t>(ge.grid));
     {
       Ctx::Timer tm(&c, "gap_edge", (E * d + n * d) * 8.0);
-      k_gap_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, E,
+      k_gap_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, sel,
                                                           static_cast<int>(d), P.q, pe);
       CPB_LAUNCH_CHECK();
     }
     e = host_cols(c, pe, ge.grid, 5, {4});
+    if (partitioned(c)) comm_allreduce_host(c, e, {4});
   }
   if (e[4] > 0.0) invalid("dual_objective: Z violates the dual-ball constraint");
   const double normA = data_fro_norm(c, *P.A);
@@ -1187,7 +1217,7 @@ double primal_objective_dev(const Prob& P, const double* X) {
   CPB_CUDA(cudaMemsetAsync(Z0, 0, static_cast<size_t>(E) * d * sizeof(double), c.s));
   GroupGeom ge = group_geom(c, E, d);
   double* pe = part_buf(c, "po.pe", 5 * static_cast<size_t>(ge.grid));
-  k_gap_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z0, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, E,
+  k_gap_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z0, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, EdgeSel{nullptr, 0, E},
                                                       static_cast<int>(d), P.q, pe);
   CPB_LAUNCH_CHECK();
   std::vector<double> e = host_cols(c, pe, ge.grid, 5, {4});
@@ -1210,7 +1240,7 @@ double kkt_residual_dev(const Prob& P, const double* X, const double* Z) {
   if (E == 0 || P.gamma == 0.0) return stat;
   GroupGeom ge = group_geom(c, E, d);
   double* pe = part_buf(c, "kkt.pe", 5 * static_cast<size_t>(ge.grid));
-  k_gap_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, E,
+  k_gap_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, EdgeSel{nullptr, 0, E},
                                                       static_cast<int>(d), P.q, pe);
   CPB_LAUNCH_CHECK();
   std::vector<double> e = host_cols(c, pe, ge.grid, 5, {4});
@@ -1221,16 +1251,18 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
                          const double* thr, double sigma) {
   Ctx& c = *P.c;
   const int64_t d = P.d(), n = P.n(), E = P.E();
-  GroupGeom ge = group_geom(c, E, d);
-  double* pe = part_buf(c, "mult.pe", 9 * static_cast<size_t>(std::max({ge.grid, edge_grid(c, E), c.sm_count * 64})));
-  int nb = ge.grid;
-  {
-    Ctx::Timer tm(&c, "multiplier", (3.0 * E * d + n * d) * 8.0);
+  const size_t pe_n = 9 * static_cast<size_t>(std::max({group_geom(c, E, d).grid, edge_grid(c, E), c.sm_count * 64}));
+  double* pe = part_buf(c, "mult.pe", pe_n);
+  // one launch over an edge selection; returns the number of 9-wide block partials
+  auto run = [&](EdgeSel sel, double* pe) -> int {
+    GroupGeom ge = group_geom(c, sel.count, d);
+    int nb = ge.grid;
+    const bool full = sel.list == nullptr && sel.e0 == 0 && sel.count == E;
     if (P.q == Q_LINF) {
-      k_mult_inf<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, V, ps, P.rad, P.g->w.p, P.g->ei.p, P.g->ej.p, E,
+      k_mult_inf<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, V, ps, P.rad, P.g->w.p, P.g->ei.p, P.g->ej.p, sel,
                                                           static_cast<int>(d), sigma, pe);
       CPB_LAUNCH_CHECK();
-    } else if (edge_reg_supported(d)) {
+    } else if (edge_reg_supported(d) && full) {
       nb = mult_reg(c, *P.g, X, Z, V, ps, thr, P.rad, d, sigma, P.q, pe);
     } else if (ge.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1) &&
                std::getenv("CPB_MULT_NOTMA") == nullptr) {
@@ -1254,20 +1286,20 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
       }
       int per_sm = 0;
       CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mult_t<Q_L2, false>, 32 * kMultWarps, smem));
-      nb = std::max(1, std::min(cdiv(E, kMultWarps), c.sm_count * std::max(1, per_sm)));
+      nb = std::max(1, std::min(cdiv(sel.count, kMultWarps), c.sm_count * std::max(1, per_sm)));
       const dim3 blk(32, kMultWarps);
       const int di = static_cast<int>(d);
       const int* ei = P.g->ei.p;
       const int* ej = P.g->ej.p;
       const double* wl = P.g->w.p;
       if (P.q == Q_L2 && vstage)
-        k_mult_t<Q_L2, true><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, E, di, sigma, pe, S);
+        k_mult_t<Q_L2, true><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, sel, di, sigma, pe, S);
       else if (P.q == Q_L2)
-        k_mult_t<Q_L2, false><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, E, di, sigma, pe, S);
+        k_mult_t<Q_L2, false><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, sel, di, sigma, pe, S);
       else if (vstage)
-        k_mult_t<Q_L1, true><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, E, di, sigma, pe, S);
+        k_mult_t<Q_L1, true><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, sel, di, sigma, pe, S);
       else
-        k_mult_t<Q_L1, false><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, E, di, sigma, pe, S);
+        k_mult_t<Q_L1, false><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, sel, di, sigma, pe, S);
       CPB_LAUNCH_CHECK();
     } else if (ge.gx == 32 && d <= kMultSmemMaxD && (P.q == Q_L2 || P.q == Q_L1)) {
       const size_t smem = static_cast<size_t>(kMultWarps) * 2 * d * sizeof(double);
@@ -1281,21 +1313,34 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
       }
       int per_sm = 0;
       CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mult_s<Q_L2>, 32 * kMultWarps, smem));
-      nb = std::max(1, std::min(cdiv(E, kMultWarps), c.sm_count * std::max(1, per_sm)));
+      nb = std::max(1, std::min(cdiv(sel.count, kMultWarps), c.sm_count * std::max(1, per_sm)));
       if (P.q == Q_L2)
         k_mult_s<Q_L2><<<nb, dim3(32, kMultWarps), smem, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p,
-                                                                P.g->ej.p, E, static_cast<int>(d), sigma, pe);
+                                                                P.g->ej.p, sel, static_cast<int>(d), sigma, pe);
       else
         k_mult_s<Q_L1><<<nb, dim3(32, kMultWarps), smem, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p,
-                                                                P.g->ej.p, E, static_cast<int>(d), sigma, pe);
+                                                                P.g->ej.p, sel, static_cast<int>(d), sigma, pe);
       CPB_LAUNCH_CHECK();
     } else {
-      k_mult<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p, P.g->ej.p, E,
+      k_mult<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, V, ps, thr, P.rad, P.g->w.p, P.g->ei.p, P.g->ej.p, sel,
                                                       static_cast<int>(d), sigma, P.q, pe);
       CPB_LAUNCH_CHECK();
     }
+    return nb;
+  };
+  int nb;
+  {
+    Ctx::Timer tm(&c, "multiplier", (3.0 * E * d + n * d) * 8.0);
+    if (!partitioned(c)) {
+      nb = run(EdgeSel{nullptr, 0, E}, pe);
+    } else {  // ghost edges first (updated, never summed), then the owned range
+      const EdgePart& ep = edge_part(c, *P.g);
+      if (ep.nghost) run(EdgeSel{ep.ghost.p, 0, ep.nghost}, part_buf(c, "mult.pg", pe_n));
+      nb = run(EdgeSel{nullptr, ep.e0, ep.e1 - ep.e0}, pe);
+    }
   }
   std::vector<double> s = host_cols(c, pe, nb, 9, {6, 7, 8});
+  if (partitioned(c)) comm_allreduce_host(c, s, {6, 7, 8});
   const double mx = s[6], err = s[7], excess = s[8];
   const double scale = 1.0 + mx;
   if (err > 1e-10 * scale) runtime("ssnal: multiplier self-check failed");
@@ -1308,6 +1353,7 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
     nbn = gather_gap(c, *P.g, X, P.A->A.p, Z, d, pn);
   }
   std::vector<double> h = host_cols(c, pn, nbn, 4);
+  if (partitioned(c)) comm_allreduce_host(c, h);
   const double normA = data_fro_norm(c, *P.A);
   MultOut o;
   GapOut& g = o.gap;

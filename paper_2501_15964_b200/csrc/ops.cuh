@@ -25,6 +25,14 @@ struct Prob {
   int64_t E() const { return g->E; }
 };
 
+// A set of edges for the edge passes: the contiguous range [e0, e0 + count),
+// or list[0 .. count) when list is set (a partitioned solve's ghost edges).
+struct EdgeSel {
+  const int* list = nullptr;
+  int64_t e0 = 0, count = 0;
+  __host__ __device__ int64_t at(int64_t i) const { return list ? static_cast<int64_t>(list[i]) : e0 + i; }
+};
+
 void make_radii(Ctx& c, const Graph& g, double gamma, double* rad);
 void make_thr(Ctx& c, int64_t E, const double* rad, double sigma, double* thr);
 

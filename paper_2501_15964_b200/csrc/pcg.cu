@@ -226,10 +226,11 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
   const int64_t m = d * nown, off = v0 * d;
   struct OwnScope {  // the operator covers this rank's nodes while the PCG runs
     Ctx& c;
-    OwnScope(Ctx& c_, bool on, int64_t a, int64_t b) : c(c_) {
+    int64_t p0, p1;
+    OwnScope(Ctx& c_, bool on, int64_t a, int64_t b) : c(c_), p0(c_.own_v0), p1(c_.own_v1) {
       if (on) c.own_v0 = a, c.own_v1 = b;
     }
-    ~OwnScope() { c.own_v0 = 0, c.own_v1 = -1; }
+    ~OwnScope() { c.own_v0 = p0, c.own_v1 = p1; }
   } own(c, dist, v0, v0 + nown);
   const Tile tg = tile_geom(chunk, d);  // identical on every rank: partial tables line up
   const int nblk = tg.blocks();

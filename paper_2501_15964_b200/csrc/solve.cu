@@ -6,6 +6,7 @@
 #include <cub/cub.cuh>
 
 #include "comm.cuh"
+#include "gather.cuh"
 #include "solve.cuh"
 
 namespace cpb {
@@ -64,6 +65,33 @@ cp_termination ssnal(Prob& P, const cp_solver_config& cfg, bool warm, double* Xo
   Ctx& c = *P.c;
   const auto t0 = Clock::now();
   const int64_t d = P.d(), n = P.n(), E = P.E(), m = d * n, me = d * E;
+  // With a communicator the solve is node-partitioned: this
+  // rank owns nodes [v0, v1) and the edges whose smaller endpoint it owns; node
+  // arrays X, D stay full (replicated / all-gathered), edge passes and node
+  // gathers cover the owned part (+ ghost edges), sums are all-reduced.
+  struct PartScope {
+    Ctx& c;
+    PartScope(Ctx& c_, int64_t n_) : c(c_) {
+      if (c.comm) c.own_v0 = c.comm->v0(n_), c.own_v1 = c.comm->v1(n_);
+    }
+    ~PartScope() { c.own_v0 = 0, c.own_v1 = -1; }
+  } part_scope(c, n);
+  const bool parted = c.comm != nullptr;
+  const int64_t ov0 = parted ? c.own_v0 * d : 0, om = parted ? (c.own_v1 - c.own_v0) * d : m;
+  auto pdot = [&](const double* a, const double* b) {  // <a, b> over the owned rows, all-reduced
+    double v = dot_dev(c, a + ov0, b + ov0, om);
+    if (parted) {
+      std::vector<double> t{v};
+      comm_allreduce_host(c, t);
+      v = t[0];
+    }
+    return v;
+  };
+  auto assemble_z = [&](double* Zfull) {  // every rank's owned edge rows -> full Z on every rank
+    if (!parted || E == 0) return;
+    const EdgePart& ep = edge_part(c, *P.g);
+    comm_allgatherv_rows(c, Zfull, ep.row0, ep.rows, d);
+  };
   initial_point(P, warm, Xout, Zout);
   {
     GapOut s0 = eval_gap(P, Xout, Zout);
@@ -114,9 +142,10 @@ cp_termination ssnal(Prob& P, const cp_solver_config& cfg, bool warm, double* Xo
       cnt.cg += dir.iterations;
       cnt.hess_apply += dir.iterations;
       double* D = w.x;
-      double descent = dot_dev(c, G, D, m);
+      double descent = pdot(G, D);
       if (!(descent < 0.0)) {  // inexact CG returned a non-descent direction (ssnal.cpp:166-170)
-        neg_dev(c, D, G, m);
+        neg_dev(c, D + ov0, G + ov0, om);
+        if (parted) comm_allgather(c, D, static_cast<size_t>(c.comm->chunk(n) * d));
         descent = -gnorm * gnorm;
       }
       double alpha = 1.0, trial = 0.0;
@@ -144,6 +173,7 @@ cp_termination ssnal(Prob& P, const cp_solver_config& cfg, bool warm, double* Xo
     zz = mo.zz;
     if (accepts(mo.gap, cfg)) {
       copy_dev(c, Xout, X, m);
+      assemble_z(Zout);
       cp_termination t = finish(mo.gap, k, true, since(t0));
       t.newton = cnt.newton, t.cg = cnt.cg, t.armijo = cnt.armijo, t.hess_apply = cnt.hess_apply;
       return t;
@@ -156,6 +186,7 @@ cp_termination ssnal(Prob& P, const cp_solver_config& cfg, bool warm, double* Xo
   }
   copy_dev(c, Xout, Xb, m);
   copy_dev(c, Zout, Zb, me);
+  assemble_z(Zout);
   cp_termination t = finish(best.s, done, false, since(t0));
   t.newton = cnt.newton, t.cg = cnt.cg, t.armijo = cnt.armijo, t.hess_apply = cnt.hess_apply;
   return t;
