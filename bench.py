@@ -32,10 +32,11 @@ of BASELINE.json).  c2 (n=10000, configs[1]) and c1 are selectable.
 
 Multi-GPU (N > 1, one process per GPU under torchrun, NCCL): the kNN is
 sharded by query-row blocks with an all-gather of the per-row lists (every
-rank then builds the bit-identical graph), and every SSNAL Newton system's PCG
-(~75 % of the C3 path) is node-partitioned (each rank applies the Hessian and
-updates the vectors for its rows; block partials all-reduced, p all-gathered);
-the remaining per-Newton work is replicated.  "scaling": "strong" (one path).
+rank then builds the bit-identical graph), and the SSNAL solves are node-
+partitioned (each rank owns a node range and the edges it starts: edge passes,
+node gathers, Hessian applies and PCG vector updates cover the owned part; sums
+are all-reduced, p / D all-gathered, Z assembled after each solve).  Labels and
+the graph build stay replicated.  "scaling": "strong" (one path).
 """
 from __future__ import annotations
 
@@ -274,8 +275,8 @@ def workload_config(args, cfg):
             "n": cfg["n"], "d": cfg["d"], "k": cfg["k"], "T": cfg["T"], "solver": cfg["algorithm"],
             "l2": "flushed between steps (512 MB write); edge arrays > L2",
             "parallelism": ("kNN query rows sharded over the ranks (NCCL all-gather of the n x k lists); "
-                            "each Newton system's PCG node-partitioned (NCCL all-reduce of partials, all-gather "
-                            "of p); the rest of the path replicated") if args.gpus > 1 else "single"}
+                            "SSNAL node-partitioned: owned nodes / owned+ghost edges per rank, NCCL all-reduce "
+                            "of sums, all-gather of p and D, Z assembled per gamma") if args.gpus > 1 else "single"}
 
 
 def run_ours(args, cfg):
