@@ -290,7 +290,7 @@ def run_ours(args, cfg):
     sched = cp.make_schedule(cfg["gamma"][0], cfg["gamma"][1], cfg["T"])
     data = cp.DataMatrix(A, ctx=ctx)
 
-    knn = cp.compute_knn_weights_sharded if world > 1 else cp.compute_knn_weights
+    knn = cp.compute_knn_weights  # row-sharded over the communicator's ranks when world > 1
 
     def step():
         g = knn(data, cfg["k"], cfg["phi"])

@@ -200,6 +200,27 @@ void comm_allgatherv_rows(Ctx& c, double* base, const std::vector<int64_t>& row0
   check(n.gend(), "ncclGroupEnd");
 }
 
+void comm_allgather_bytes(Ctx& c, void* base_, size_t chunk_bytes) {
+  if (!c.comm || chunk_bytes == 0) return;
+  char* base = static_cast<char*>(base_);
+  if (LocalGroup* g = c.comm->local) {
+    const int r = c.comm->rank;
+    c.sync();
+    g->ptrs[r] = reinterpret_cast<double*>(base);
+    g->barrier();
+    for (int q = 0; q < g->n; ++q)
+      if (q != r)
+        CPB_CUDA(cudaMemcpyAsync(base + q * chunk_bytes, reinterpret_cast<char*>(g->ptrs[q]) + q * chunk_bytes,
+                                 chunk_bytes, cudaMemcpyDeviceToDevice, c.s));
+    c.sync();
+    g->barrier();
+    return;
+  }
+  check(nccl().allgather(base + static_cast<size_t>(c.comm->rank) * chunk_bytes, base, chunk_bytes, ncclChar,
+                         static_cast<ncclComm_t>(c.comm->nccl), c.s),
+        "ncclAllGather(bytes)");
+}
+
 void comm_allgather(Ctx& c, double* base, size_t chunk_elems) {
   if (!c.comm || chunk_elems == 0) return;
   if (LocalGroup* g = c.comm->local) {  // device-to-device copies of the other ranks' chunks

@@ -41,6 +41,8 @@ void comm_init_local(Ctx& c, LocalGroup* g, int rank);
 void comm_allreduce_sum(Ctx& c, double* buf, size_t count);
 // In-place all-gather: rank r's `chunk_elems` doubles at base + r * chunk_elems.
 void comm_allgather(Ctx& c, double* base, size_t chunk_elems);
+// In-place all-gather of raw bytes (rank r's chunk at base + r * chunk_bytes).
+void comm_allgather_bytes(Ctx& c, void* base, size_t chunk_bytes);
 // In-place max over the ranks.
 void comm_allreduce_max(Ctx& c, double* buf, size_t count);
 // In-place all-gather of variable row ranges: rank q owns rows [row0[q], row0[q] + rows[q]) of width d.

@@ -21,6 +21,7 @@
 #include <cmath>
 #include <random>
 
+#include "comm.cuh"
 #include "gather.cuh"
 #include "graph.cuh"
 
@@ -682,6 +683,17 @@ std::unique_ptr<Graph> knn_graph(Ctx& c, const Data& A, int64_t k, double phi) {
   knn_validate(A, k, phi);
   const int64_t n = A.n, NK = n * k;
   trace("knn_graph begin");
+  if (c.comm && c.comm->nranks > 1) {
+    // Row-sharded: this rank's query rows, then an in-place
+    // all-gather of the padded n x k lists; every rank builds the same graph.
+    const int64_t chunk = c.comm->chunk(n), P = c.comm->nranks;
+    double* kd = c.buf<double>("knn.d", chunk * P * k);
+    int* kj = c.buf<int>("knn.j", chunk * P * k);
+    knn_rows_dev(c, A, k, c.comm->v0(n), c.comm->v1(n), kd, kj);
+    comm_allgather_bytes(c, kd, static_cast<size_t>(chunk * k) * sizeof(double));
+    comm_allgather_bytes(c, kj, static_cast<size_t>(chunk * k) * sizeof(int));
+    return graph_from_knn_dev(c, n, k, phi, kd, kj);
+  }
   double* kd = c.buf<double>("knn.d", NK);
   int* kj = c.buf<int>("knn.j", NK);
   knn_rows_dev(c, A, k, 0, n, kd, kj);

@@ -519,11 +519,11 @@ def test_partitioned_path_multi_rank(cp, orc, nranks, d):
     for r, c in enumerate(ctxs):
         c.set_local_comm(group, r)
     datas = [cp.DataMatrix(A, ctx=c) for c in ctxs]
-    graphs = [cp.compute_knn_weights(dm, 8, 0.5) for dm in datas]
-    out, errs = [None] * nranks, []
+    out, errs, graphs = [None] * nranks, [], [None] * nranks
 
     def work(r):
-        try:
+        try:  # the kNN is row-sharded across the group too (cp_knn_graph with a communicator)
+            graphs[r] = cp.compute_knn_weights(datas[r], 8, 0.5)
             out[r] = cp.run_path(datas[r], graphs[r], 2, sched, cp.SolverConfig())
         except Exception as e:  # noqa: BLE001
             errs.append(e)
@@ -534,6 +534,9 @@ def test_partitioned_path_multi_rank(cp, orc, nranks, d):
     for t in th:
         t.join(300)
     assert not errs, errs
+    for r in range(nranks):
+        for a_, b_ in zip(graphs[r].arrays(), g0.arrays()):
+            assert np.array_equal(a_, b_)
     for t in range(len(sched.values)):
         X0 = ref.solutions[t].X
         for r in range(nranks):
