@@ -23,6 +23,8 @@ struct Nccl {
   decltype(&ncclBroadcast) bcast = nullptr;
   decltype(&ncclGroupStart) gstart = nullptr;
   decltype(&ncclGroupEnd) gend = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
 };
 
 const Nccl& nccl() {
@@ -41,8 +43,11 @@ const Nccl& nccl() {
     n.bcast = reinterpret_cast<decltype(n.bcast)>(dlsym(h, "ncclBroadcast"));
     n.gstart = reinterpret_cast<decltype(n.gstart)>(dlsym(h, "ncclGroupStart"));
     n.gend = reinterpret_cast<decltype(n.gend)>(dlsym(h, "ncclGroupEnd"));
+    n.send = reinterpret_cast<decltype(n.send)>(dlsym(h, "ncclSend"));
+    n.recv = reinterpret_cast<decltype(n.recv)>(dlsym(h, "ncclRecv"));
   });
-  if (!n.get_id || !n.init || !n.destroy || !n.allreduce || !n.allgather || !n.bcast || !n.gstart || !n.gend)
+  if (!n.get_id || !n.init || !n.destroy || !n.allreduce || !n.allgather || !n.bcast || !n.gstart || !n.gend ||
+      !n.send || !n.recv)
     throw Error(CP_ENCCL, "NCCL (libnccl.so.2) is not available in this process");
   return n;
 }
@@ -61,6 +66,7 @@ struct LocalGroup {
   int arrived = 0;
   unsigned long long gen = 0;
   std::vector<double*> ptrs;
+  std::vector<const std::vector<int64_t>*> offs;
   std::vector<std::vector<double>> host;
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
@@ -80,6 +86,7 @@ LocalGroup* local_group_create(int nranks) {
   auto* g = new LocalGroup();
   g->n = nranks;
   g->ptrs.assign(static_cast<size_t>(nranks), nullptr);
+  g->offs.assign(static_cast<size_t>(nranks), nullptr);
   g->host.resize(static_cast<size_t>(nranks));
   return g;
 }
@@ -197,6 +204,39 @@ void comm_allgatherv_rows(Ctx& c, double* base, const std::vector<int64_t>& row0
       check(n.bcast(base + row0[q] * d, base + row0[q] * d, static_cast<size_t>(rows[q] * d), ncclFloat64, q,
                     static_cast<ncclComm_t>(c.comm->nccl), c.s),
             "ncclBroadcast");
+  check(n.gend(), "ncclGroupEnd");
+}
+
+void comm_exchange(Ctx& c, const double* sbuf, const std::vector<int64_t>& send_off, double* rbuf,
+                   const std::vector<int64_t>& recv_off, int64_t d) {
+  if (!c.comm || c.comm->nranks == 1) return;
+  const int r = c.comm->rank, P = c.comm->nranks;
+  if (LocalGroup* g = c.comm->local) {  // pull my segment of every peer's send buffer
+    c.sync();
+    g->ptrs[r] = const_cast<double*>(sbuf);
+    g->offs[r] = &send_off;
+    g->barrier();
+    for (int q = 0; q < P; ++q) {
+      if (q == r) continue;
+      const int64_t rows = recv_off[q + 1] - recv_off[q];
+      if (rows == 0) continue;
+      const int64_t at = (*g->offs[q])[r];  // peer q's rows destined to me start here
+      CPB_CUDA(cudaMemcpyAsync(rbuf + recv_off[q] * d, g->ptrs[q] + at * d, rows * d * sizeof(double),
+                               cudaMemcpyDeviceToDevice, c.s));
+    }
+    c.sync();
+    g->barrier();
+    return;
+  }
+  const Nccl& n = nccl();
+  ncclComm_t cm = static_cast<ncclComm_t>(c.comm->nccl);
+  check(n.gstart(), "ncclGroupStart");
+  for (int q = 0; q < P; ++q) {
+    if (q == r) continue;
+    const int64_t ns = send_off[q + 1] - send_off[q], nr = recv_off[q + 1] - recv_off[q];
+    if (ns) check(n.send(sbuf + send_off[q] * d, static_cast<size_t>(ns * d), ncclFloat64, q, cm, c.s), "ncclSend");
+    if (nr) check(n.recv(rbuf + recv_off[q] * d, static_cast<size_t>(nr * d), ncclFloat64, q, cm, c.s), "ncclRecv");
+  }
   check(n.gend(), "ncclGroupEnd");
 }
 

@@ -43,6 +43,10 @@ void comm_allreduce_sum(Ctx& c, double* buf, size_t count);
 void comm_allgather(Ctx& c, double* base, size_t chunk_elems);
 // In-place all-gather of raw bytes (rank r's chunk at base + r * chunk_bytes).
 void comm_allgather_bytes(Ctx& c, void* base, size_t chunk_bytes);
+// Point-to-point exchange: rows [send_off[s], send_off[s+1]) of sbuf go to
+// rank s, rows [recv_off[s], recv_off[s+1]) of rbuf come from rank s (width d).
+void comm_exchange(Ctx& c, const double* sbuf, const std::vector<int64_t>& send_off, double* rbuf,
+                   const std::vector<int64_t>& recv_off, int64_t d);
 // In-place max over the ranks.
 void comm_allreduce_max(Ctx& c, double* buf, size_t count);
 // In-place all-gather of variable row ranges: rank q owns rows [row0[q], row0[q] + rows[q]) of width d.

@@ -555,6 +555,91 @@ Items node_items(Ctx& c, const Graph& g) {
   return {o.order.p, o.count};
 }
 
+const HaloPlan& halo_plan(Ctx& c, const Graph& g) {
+  static thread_local std::vector<std::unique_ptr<HaloPlan>> cache;
+  const int P = c.comm ? c.comm->nranks : 1;
+  for (auto& h : cache)
+    if (h->uid == g.uid && h->v0 == c.own_v0 && h->v1 == c.own_v1 && h->nranks == P) return *h;
+  auto h = std::make_unique<HaloPlan>();
+  h->uid = g.uid, h->v0 = c.own_v0, h->v1 = c.own_v1, h->nranks = P;
+  const int64_t n = g.n, chunk = (n + P - 1) / P;
+  auto owner = [&](int v) { return static_cast<int>(v / chunk); };
+  std::vector<int> off(static_cast<size_t>(n) + 1), adj(static_cast<size_t>(2 * g.E));
+  d2h(c, off.data(), g.off.p, off.size() * sizeof(int));
+  if (g.E) d2h(c, adj.data(), g.adj_o.p, adj.size() * sizeof(int));
+  const int me = c.comm ? c.comm->rank : 0;
+  std::vector<std::vector<int>> send(static_cast<size_t>(P)), recv(static_cast<size_t>(P));
+  for (int64_t v = c.own_v0; v < c.own_v1; ++v)
+    for (int e = off[v]; e < off[v + 1]; ++e) {
+      const int o = adj[static_cast<size_t>(e)], s = owner(o);
+      if (s == me) continue;
+      send[static_cast<size_t>(s)].push_back(static_cast<int>(v));  // s gathers v
+      recv[static_cast<size_t>(s)].push_back(o);                     // this rank gathers o
+    }
+  std::vector<int> si, ri;
+  h->send_off.push_back(0);
+  h->recv_off.push_back(0);
+  for (int s = 0; s < P; ++s) {
+    auto& a = send[static_cast<size_t>(s)];
+    auto& b = recv[static_cast<size_t>(s)];
+    std::sort(a.begin(), a.end());
+    a.erase(std::unique(a.begin(), a.end()), a.end());
+    std::sort(b.begin(), b.end());
+    b.erase(std::unique(b.begin(), b.end()), b.end());
+    si.insert(si.end(), a.begin(), a.end());
+    ri.insert(ri.end(), b.begin(), b.end());
+    h->send_off.push_back(static_cast<int64_t>(si.size()));
+    h->recv_off.push_back(static_cast<int64_t>(ri.size()));
+  }
+  h->nsend = static_cast<int64_t>(si.size());
+  h->nrecv = static_cast<int64_t>(ri.size());
+  h->send_idx.resize(si.size() + 1);
+  h->recv_idx.resize(ri.size() + 1);
+  if (!si.empty()) h2d(c, h->send_idx.p, si.data(), si.size() * sizeof(int));
+  if (!ri.empty()) h2d(c, h->recv_idx.p, ri.data(), ri.size() * sizeof(int));
+  c.sync();
+  if (cache.size() > 8) cache.erase(cache.begin());
+  cache.push_back(std::move(h));
+  return *cache.back();
+}
+
+__global__ void k_rows_pack(const double* __restrict__ src, const int* __restrict__ idx, int64_t rows, int d,
+                            double* __restrict__ dst) {
+  const int64_t total = rows * d;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = t / d, f = t % d;
+    dst[t] = src[static_cast<int64_t>(idx[r]) * d + f];
+  }
+}
+__global__ void k_rows_unpack(const double* __restrict__ src, const int* __restrict__ idx, int64_t rows, int d,
+                              double* __restrict__ dst) {
+  const int64_t total = rows * d;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = t / d, f = t % d;
+    dst[static_cast<int64_t>(idx[r]) * d + f] = src[t];
+  }
+}
+
+void halo_exchange(Ctx& c, const Graph& g, double* p, int64_t d) {
+  if (!c.comm || c.comm->nranks == 1) return;
+  const HaloPlan& h = halo_plan(c, g);
+  double* sbuf = c.buf<double>("halo.send", static_cast<size_t>(h.nsend * d) + 1);
+  double* rbuf = c.buf<double>("halo.recv", static_cast<size_t>(h.nrecv * d) + 1);
+  if (h.nsend) {
+    k_rows_pack<<<std::max(1, std::min(cdiv(h.nsend * d, 256), c.sm_count * 8)), 256, 0, c.s>>>(
+        p, h.send_idx.p, h.nsend, static_cast<int>(d), sbuf);
+    CPB_LAUNCH_CHECK();
+  }
+  comm_exchange(c, sbuf, h.send_off, rbuf, h.recv_off, d);
+  if (h.nrecv) {
+    k_rows_unpack<<<std::max(1, std::min(cdiv(h.nrecv * d, 256), c.sm_count * 8)), 256, 0, c.s>>>(
+        rbuf, h.recv_idx.p, h.nrecv, static_cast<int>(d), p);
+    CPB_LAUNCH_CHECK();
+  }
+}
+
 const EdgePart& edge_part(Ctx& c, const Graph& g) {
   static thread_local std::vector<std::unique_ptr<EdgePart>> cache;
   const int P = c.comm ? c.comm->nranks : 1;

@@ -58,6 +58,22 @@ struct EdgePart {
 };
 const EdgePart& edge_part(Ctx& c, const Graph& g);
 
+// Halo plan of a partitioned solve: for every other rank s, the owned nodes
+// this rank sends to s (those adjacent to s's nodes) and the nodes of s it
+// receives (s's nodes adjacent to this rank's), both in ascending id, so the
+// two sides agree without negotiation (the graph is replicated).
+struct HaloPlan {
+  uint64_t uid = 0;
+  int64_t v0 = 0, v1 = -1;
+  int nranks = 1;
+  std::vector<int64_t> send_off, recv_off;  // per rank, prefix offsets (size nranks + 1)
+  DBuf<int> send_idx, recv_idx;
+  int64_t nsend = 0, nrecv = 0;
+};
+const HaloPlan& halo_plan(Ctx& c, const Graph& g);
+// p's halo rows <- the owning ranks' rows (p is a full-size node array).
+void halo_exchange(Ctx& c, const Graph& g, double* p, int64_t d);
+
 int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,
                   const double* thr, int64_t d, double sigma, int q, double* bc, double* Ap, double* part,
                   const int* active);

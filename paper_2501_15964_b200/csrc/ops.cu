@@ -1136,7 +1136,7 @@ PcgOut pcg_newton(const Prob& P, const double* V, const double* jal, const doubl
   // (everything outside the PCG stays replicated: identical on every rank)
   const bool dist = P.c->comm != nullptr;
   const double op_b = dist ? hess_bytes / P.c->comm->nranks : hess_bytes;
-  return pcg_dev(*P.c, n, d, op, op_b, "hess_apply", rhs, w, tol, max_iter, false, dist);
+  return pcg_dev(*P.c, n, d, op, op_b, "hess_apply", rhs, w, tol, max_iter, false, dist, P.g);
 }
 
 // Sum (and max) the columns of a (rows x cols) block-partial table on the host,

@@ -80,7 +80,8 @@ using PcgOp = std::function<int(const double* p, double* Ap, double* part, const
 // block partials are all-reduced and p (then x) all-gathered; the work
 // buffers must hold P * ceil(n / P) rows.
 PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, const char* op_name,
-               const double* rhs, PcgWork w, double tol, int64_t max_iter, bool warm, bool dist = false);
+               const double* rhs, PcgWork w, double tol, int64_t max_iter, bool warm, bool dist = false,
+               const Graph* halo = nullptr);  // dist: refresh p by halo exchange over this graph (else all-gather)
 PcgOut pcg_newton(const Prob& P, const double* V, const double* jal, const double* jbe, const double* thr,
                   double sigma, const double* rhs, PcgWork w, double tol, int64_t max_iter, int64_t n_active);
 

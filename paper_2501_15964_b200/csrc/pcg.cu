@@ -18,6 +18,7 @@
 #include <cstdlib>
 
 #include "comm.cuh"
+#include "gather.cuh"
 #include "ops.cuh"
 
 namespace cpb {
@@ -215,7 +216,8 @@ __global__ void k_cg_c(const CgState* __restrict__ st, const double* __restrict_
 const int* cg_active_ptr(const void* st) { return st ? &static_cast<const CgState*>(st)->active : nullptr; }
 
 PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, const char* op_name,
-               const double* rhs, PcgWork w, double tol, int64_t max_iter, bool warm, bool dist) {
+               const double* rhs, PcgWork w, double tol, int64_t max_iter, bool warm, bool dist,
+               const Graph* halo) {
   if (!(tol > 0.0)) invalid("pcg: tol must be positive");
   if (max_iter < 1) invalid("pcg: max_iter must be >= 1");
   dist = dist && c.comm != nullptr;
@@ -233,6 +235,14 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
     ~OwnScope() { c.own_v0 = p0, c.own_v1 = p1; }
   } own(c, dist, v0, v0 + nown);
   const Tile tg = tile_geom(chunk, d);  // identical on every rank: partial tables line up
+  // p rows other ranks own: only the halo the operator gathers (ascending-id
+  // plans both sides derive from the replicated graph), or the whole chunk
+  auto refresh_p = [&] {
+    if (halo)
+      halo_exchange(c, *halo, w.p, d);
+    else
+      comm_allgather(c, w.p, static_cast<size_t>(chunk * d));
+  };
   const int nblk = tg.blocks();
   double* part_rz = c.buf<double>("pcg.rz", nblk + 8);
   double* part_rr = c.buf<double>("pcg.rr", static_cast<size_t>(tg.R) * d + 8);
@@ -252,7 +262,7 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
   if (dist) {
     comm_allreduce_sum(c, part_rz, nblk);
     comm_allreduce_sum(c, part_rr, static_cast<size_t>(tg.R) * d);
-    comm_allgather(c, w.p, static_cast<size_t>(chunk * d));
+    refresh_p();
   }
   k_cg_s0<<<1, 1024, 0, c.s>>>(st, part_rz, nblk, part_rr, tg.R, di, tol, max_iter, bn, Mx != nullptr);
   CPB_LAUNCH_CHECK();
@@ -293,7 +303,7 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
         k_cg_c<<<fg, 256, 0, c.s>>>(st, w.r + off, w.diag + off, m, w.x + off, w.p + off);
         CPB_LAUNCH_CHECK();
       }
-      if (dist) comm_allgather(c, w.p, static_cast<size_t>(chunk * d));
+      if (dist) refresh_p();
     }
     CgState h;
     CPB_CUDA(cudaMemcpyAsync(c.hscal, st, sizeof(CgState), cudaMemcpyDeviceToHost, c.s));
