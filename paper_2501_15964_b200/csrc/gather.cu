@@ -316,12 +316,13 @@ __global__ void __launch_bounds__(256) k_g_grad(const double* __restrict__ X, co
 // ---- SSNAL Hessian, pass 1: bc_l = beta_l <v_l, p_i - p_j> (warp per active edge) -----------
 __global__ void __launch_bounds__(256) k_edge_dot(const double* __restrict__ P, const double* __restrict__ V,
                                                   const double* __restrict__ jbe, const int* __restrict__ ei,
-                                                  const int* __restrict__ ej, int64_t E, int d,
+                                                  const int* __restrict__ ej, const int* __restrict__ elist, int64_t e0, int64_t E, int d,
                                                   double* __restrict__ bc, const int* active) {
   if (active && !*active) return;
   const int lane = threadIdx.x & 31;
-  for (int64_t l = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; l < E;
-       l += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+  for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; i < E;
+       i += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t l = elist ? static_cast<int64_t>(elist[i]) : e0 + i;  // an edge selection (see EdgeSel)
     const double be = jbe[l];
     if (be == 0.0) {
       if (lane == 0) bc[l] = 0.0;
@@ -352,11 +353,12 @@ __global__ void __launch_bounds__(256) k_edge_dot(const double* __restrict__ P, 
 __global__ void __launch_bounds__(256) k_edge_dot_inf(const double* __restrict__ P, const double* __restrict__ V,
                                                       const double* __restrict__ jal, const double* __restrict__ jbe,
                                                       const int* __restrict__ ei, const int* __restrict__ ej,
-                                                      int64_t E, int d, double* __restrict__ bc, const int* active) {
+                                                      const int* __restrict__ elist, int64_t e0, int64_t E, int d, double* __restrict__ bc, const int* active) {
   if (active && !*active) return;
   const int lane = threadIdx.x & 31;
-  for (int64_t l = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; l < E;
-       l += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+  for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; i < E;
+       i += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t l = elist ? static_cast<int64_t>(elist[i]) : e0 + i;  // an edge selection (see EdgeSel)
     const double th = jal[l], be = jbe[l];
     if (th < 0.0 || be == 0.0) {
       if (lane == 0) bc[l] = 0.0;
@@ -737,14 +739,25 @@ int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, cons
                   const double* thr, int64_t d, double sigma, int q, double* bc, double* Ap, double* part,
                   const int* active) {
   if (q == 2 && g.E > 0 && hess_tma_supported(d)) return hess_tma(c, g, P, V, jal, jbe, d, sigma, Ap, part, active);
-  if (q == 2 && g.E > 0) {
-    const int grid = std::max(1, std::min(cdiv(g.E, 8), c.sm_count * 8));
-    k_edge_dot<<<grid, 256, 0, c.s>>>(P, V, jbe, g.ei.p, g.ej.p, g.E, static_cast<int>(d), bc, active);
-    CPB_LAUNCH_CHECK();
-  } else if (q == 0 && g.E > 0) {
-    const int grid = std::max(1, std::min(cdiv(g.E, 8), c.sm_count * 8));
-    k_edge_dot_inf<<<grid, 256, 0, c.s>>>(P, V, jal, jbe, g.ei.p, g.ej.p, g.E, static_cast<int>(d), bc, active);
-    CPB_LAUNCH_CHECK();
+  if ((q == 2 || q == 0) && g.E > 0) {
+    // per-edge dots: every edge, or in a partitioned solve this rank's owned + ghost edges
+    auto dots = [&](const int* list, int64_t e0, int64_t cnt) {
+      if (cnt == 0) return;
+      const int grid = std::max(1, std::min(cdiv(cnt, 8), c.sm_count * 8));
+      if (q == 2)
+        k_edge_dot<<<grid, 256, 0, c.s>>>(P, V, jbe, g.ei.p, g.ej.p, list, e0, cnt, static_cast<int>(d), bc, active);
+      else
+        k_edge_dot_inf<<<grid, 256, 0, c.s>>>(P, V, jal, jbe, g.ei.p, g.ej.p, list, e0, cnt, static_cast<int>(d), bc,
+                                              active);
+      CPB_LAUNCH_CHECK();
+    };
+    if (c.comm && c.own_v1 >= 0) {
+      const EdgePart& ep = edge_part(c, g);
+      dots(nullptr, ep.e0, ep.e1 - ep.e0);
+      dots(ep.ghost.p, 0, ep.nghost);
+    } else {
+      dots(nullptr, 0, g.E);
+    }
   }
   GEOM
   const int* ord = g.order.p;
