@@ -329,7 +329,8 @@ def run_ours(args, cfg):
         t0 = time.perf_counter()
         dA = cp.DataMatrix(A, ctx=ctx)
         g2 = knn(dA, cfg["k"], cfg["phi"])
-        res2 = cp.run_path(dA, g2, cfg["q"], sched, cpcfg, keep_solutions=True, keep_z=keep_z)
+        # one copy of the path's outputs comes back to the host: rank 0's (every rank holds the same)
+        res2 = cp.run_path(dA, g2, cfg["q"], sched, cpcfg, keep_solutions=(rank == 0), keep_z=keep_z)
         if s > 0:
             e2e_times.append(time.perf_counter() - t0)
         del res2
