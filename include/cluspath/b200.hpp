@@ -231,6 +231,23 @@ inline WeightedGraph compute_knn_weights(const DataMatrix& data, Index k, double
 }
 
 // IncidenceOperator (graph.hpp:62-86)
+// Compressed-column sparse matrix (the layout of Eigen::SparseMatrix<double>).
+struct SparseMatrix {
+  Index rows_ = 0, cols_ = 0;
+  std::vector<int64_t> colptr, rowidx;
+  std::vector<double> values;
+  Index rows() const { return rows_; }
+  Index cols() const { return cols_; }
+  Index nonZeros() const { return static_cast<Index>(values.size()); }
+  Matrix toDense() const {
+    Matrix M(rows_, cols_);
+    for (Index c = 0; c < cols_; ++c)
+      for (int64_t q = colptr[static_cast<size_t>(c)]; q < colptr[static_cast<size_t>(c) + 1]; ++q)
+        M(rowidx[static_cast<size_t>(q)], c) = values[static_cast<size_t>(q)];
+    return M;
+  }
+};
+
 class IncidenceOperator {
  public:
   explicit IncidenceOperator(const WeightedGraph& g) : graph_(&g) {}
@@ -254,6 +271,19 @@ class IncidenceOperator {
   void apply_transpose_into(const Matrix& Z, Matrix& out) const {
     out.resize(Z.rows(), nodes());
     detail::check(cp_incidence_apply_t(detail::ctx(), graph_->handle(), Z.data(), Z.rows(), Z.cols(), out.data()));
+  }
+  // laplacian() (graph.hpp:82): B B^T in compressed columns, built on the device.
+  SparseMatrix laplacian() const {
+    SparseMatrix L;
+    L.rows_ = L.cols_ = graph_->nodes();
+    int64_t nnz = 0;
+    detail::check(cp_graph_laplacian(detail::ctx(), graph_->handle(), nullptr, nullptr, nullptr, &nnz));
+    L.colptr.resize(static_cast<size_t>(L.cols_ + 1));
+    L.rowidx.resize(static_cast<size_t>(nnz));
+    L.values.resize(static_cast<size_t>(nnz));
+    detail::check(cp_graph_laplacian(detail::ctx(), graph_->handle(), L.colptr.data(), L.rowidx.data(),
+                                     L.values.data(), &nnz));
+    return L;
   }
   // power_iteration(LinearOperator::sparse(laplacian())) (linalg.cpp:194-242)
   double laplacian_lambda_max(double tol = 1e-9, Index max_iter = 10000) const {

@@ -178,6 +178,12 @@ int cp_incidence_apply(cp_ctx* ctx, const cp_graph* g, const double* X, int64_t 
 /* IncidenceOperator::apply_transpose_into: Z (d x |E|) -> Z B^T (d x n) (graph.hpp:74-75; graph.cpp:140-152) */
 int cp_incidence_apply_t(cp_ctx* ctx, const cp_graph* g, const double* Z, int64_t d, int64_t E, double* out);
 /* connected_components + component_count (graph.hpp:90-92; graph.cpp:169-202) */
+/* IncidenceOperator::laplacian (graph.hpp:82; graph.cpp:154-167): B B^T
+ * (weights do not enter) as compressed columns, n x n.  Call with colptr = NULL
+ * to get *nnz, then with colptr (n + 1), rowidx (nnz) and values (nnz); rows are
+ * ascending within each column (Eigen's compressed layout). */
+int cp_graph_laplacian(cp_ctx* ctx, const cp_graph* g, int64_t* colptr, int64_t* rowidx, double* values,
+                       int64_t* nnz);
 int cp_connected_components(cp_ctx* ctx, const cp_graph* g, int64_t* labels, int64_t* K);
 /* power_iteration(LinearOperator::sparse(B.laplacian())) (linalg.hpp:84-85; linalg.cpp:194-242) */
 int cp_laplacian_lambda_max(cp_ctx* ctx, const cp_graph* g, double tol, int64_t max_iter, double* lambda);

@@ -70,6 +70,8 @@ _SIGS = [
     ("cp_data_destroy", None, [VP]),
     ("cp_knn_graph", C.c_int, [VP, VP, C.c_int64, C.c_double, C.POINTER(VP)]),
     ("cp_knn_rows", C.c_int, [VP, VP, C.c_int64, C.c_int64, C.c_int64, VP, VP]),
+    ("cp_graph_laplacian", C.c_int, [VP, VP, C.POINTER(C.c_int64), C.POINTER(C.c_int64), D,
+                                     C.POINTER(C.c_int64)]),
     ("cp_graph_from_knn", C.c_int, [VP, C.c_int64, C.c_int64, C.c_double, VP, VP, C.POINTER(VP)]),
     ("cp_shard_rows", C.c_int, [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("cp_nccl_unique_id", C.c_int, [C.c_char_p]),

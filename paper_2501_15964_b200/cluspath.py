@@ -447,6 +447,20 @@ class IncidenceOperator:
                                               _dp(out)))
         return out
 
+    def laplacian(self):
+        """IncidenceOperator::laplacian (graph.cpp:154-167): B B^T as a
+        scipy.sparse.csc_matrix, built on the GPU."""
+        import scipy.sparse as sp
+        n = self.graph.nodes()
+        nnz = C.c_int64()
+        h = self.graph.ctx._h
+        L.check(L.load().cp_graph_laplacian(h, self.graph._h, None, None, None, C.byref(nnz)))
+        colptr = np.empty(n + 1, np.int64)
+        rows = np.empty(max(1, nnz.value), np.int64)
+        vals = np.empty(max(1, nnz.value))
+        L.check(L.load().cp_graph_laplacian(h, self.graph._h, _ip(colptr), _ip(rows), _dp(vals), C.byref(nnz)))
+        return sp.csc_matrix((vals[:nnz.value], rows[:nnz.value], colptr), shape=(n, n))
+
     def laplacian_lambda_max(self, tol=1e-9, max_iter=10000):
         """power_iteration(LinearOperator::sparse(laplacian())) (linalg.cpp:194-242)."""
         out = C.c_double()

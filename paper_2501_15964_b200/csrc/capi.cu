@@ -299,6 +299,14 @@ int cp_knn_graph(cp_ctx* ctx, const cp_data* data, int64_t k, double phi, cp_gra
     *out = g.release();
   });
 }
+int cp_graph_laplacian(cp_ctx* ctx, const cp_graph* g, int64_t* colptr, int64_t* rowidx, double* values,
+                       int64_t* nnz) {
+  return guard(ctx, [&] {
+    need(g, "graph");
+    const int64_t z = cpb::laplacian_csc(*ctx->c, *g->g, colptr, rowidx, values);
+    if (nnz) *nnz = z;
+  });
+}
 int cp_knn_rows(cp_ctx* ctx, const cp_data* data, int64_t k, int64_t r0, int64_t r1, double* kd_dev,
                 int32_t* kj_dev) {
   return guard(ctx, [&] {

@@ -805,6 +805,66 @@ int64_t components_dev(Ctx& c, const Graph& g, const unsigned char* flag, int* l
   return K;
 }
 
+// IncidenceOperator::laplacian (graph.cpp:154-167): B B^T, unweighted, in
+// compressed-column form.  Column v holds the neighbours below v (-1), the
+// degree on the diagonal, then the neighbours above v (-1): the CSR's
+// incident edges are in ascending edge id = ascending neighbour order.
+// Isolated nodes have an empty column (the reference adds no triplet).
+__global__ void k_lap_colcount(const int* __restrict__ off, int n, long long* __restrict__ cnt) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const int deg = off[v + 1] - off[v];
+    cnt[v] = deg + (deg > 0 ? 1 : 0);
+  }
+}
+__global__ void k_lap_fill(const int* __restrict__ off, const int* __restrict__ adj_o, int n,
+                           const long long* __restrict__ colptr, long long* __restrict__ row,
+                           double* __restrict__ val) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const int a = off[v], b = off[v + 1];
+    if (a == b) continue;
+    long long q = colptr[v];
+    bool diag = false;
+    for (int e = a; e < b; ++e) {
+      const int o = adj_o[e];
+      if (!diag && o > v) {
+        row[q] = v, val[q] = static_cast<double>(b - a), ++q;
+        diag = true;
+      }
+      row[q] = o, val[q] = -1.0, ++q;
+    }
+    if (!diag) row[q] = v, val[q] = static_cast<double>(b - a);
+  }
+}
+
+int64_t laplacian_csc(Ctx& c, const Graph& g, int64_t* colptr, int64_t* rowidx, double* values) {
+  const int n = static_cast<int>(g.n);
+  long long* cnt = c.buf<long long>("lap.cnt", n + 1);
+  long long* cp = c.buf<long long>("lap.cp", n + 1);
+  CPB_CUDA(cudaMemsetAsync(cnt + n, 0, sizeof(long long), c.s));
+  const int gn = std::max(1, std::min(cdiv(n, 256), c.sm_count * 8));
+  if (n > 0) {
+    k_lap_colcount<<<gn, 256, 0, c.s>>>(g.off.p, n, cnt);
+    CPB_LAUNCH_CHECK();
+  }
+  cub_call(c, "lap.scan", [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, cnt, cp, n + 1, c.s); });
+  long long nnz = 0;
+  d2h(c, &nnz, cp + n, sizeof(long long));
+  if (!colptr) return nnz;
+  long long* row = c.buf<long long>("lap.row", static_cast<size_t>(nnz) + 1);
+  double* val = c.buf<double>("lap.val", static_cast<size_t>(nnz) + 1);
+  if (n > 0) {
+    k_lap_fill<<<gn, 256, 0, c.s>>>(g.off.p, g.adj_o.p, n, cp, row, val);
+    CPB_LAUNCH_CHECK();
+  }
+  static_assert(sizeof(long long) == sizeof(int64_t), "int64");
+  d2h(c, colptr, cp, (n + 1) * sizeof(int64_t));
+  if (nnz) {
+    if (rowidx) d2h(c, rowidx, row, nnz * sizeof(int64_t));
+    if (values) d2h(c, values, val, nnz * sizeof(double));
+  }
+  return nnz;
+}
+
 double laplacian_lambda_max(Ctx& c, const Graph& g, double tol, int64_t max_iter) {
   if (!(tol > 0.0)) invalid("power_iteration: tol must be positive");
   if (max_iter < 1) invalid("power_iteration: max_iter must be >= 1");

@@ -57,6 +57,10 @@ void incidence_apply_t_dev(Ctx& c, const Graph& g, const double* Z, int64_t d, d
 // is null).  labels: rank of each component's smallest node (graph.cpp:169-196).
 int64_t components_dev(Ctx& c, const Graph& g, const unsigned char* flag, int* labels);
 
+// IncidenceOperator::laplacian (graph.cpp:154-167) in CSC form (host outputs;
+// colptr null: only the nonzero count is returned).
+int64_t laplacian_csc(Ctx& c, const Graph& g, int64_t* colptr, int64_t* rowidx, double* values);
+
 // power_iteration on L = B B^T (linalg.cpp:194-242).
 double laplacian_lambda_max(Ctx& c, const Graph& g, double tol, int64_t max_iter);
 

@@ -404,6 +404,22 @@ TEST_CASE("path JSON and CSV outputs") {  // test_path.cpp:243-270, test_io.cpp:
   CHECK(format_double(1e5) == "1e+05" && format_double(2.0) == "2" && format_double(0.001) == "0.001");
 }
 
+TEST_CASE("laplacian of the path and complete graphs") {  // test_graph.cpp:173-185
+  WeightedGraph path3(3, {{0, 1, 0.7}, {1, 2, 0.2}});
+  Matrix Lp = IncidenceOperator(path3).laplacian().toDense();
+  const double ep[9] = {1, -1, 0, -1, 2, -1, 0, -1, 1};
+  bool ok = true;
+  for (Index r = 0; r < 3; ++r)
+    for (Index c = 0; c < 3; ++c) ok = ok && Lp(r, c) == ep[r * 3 + c];
+  CHECK(ok);
+  WeightedGraph k3(3, {{0, 1, 1.0}, {0, 2, 1.0}, {1, 2, 1.0}});
+  SparseMatrix Lc = IncidenceOperator(k3).laplacian();
+  CHECK(Lc.nonZeros() == 9 && Lc.toDense()(0, 0) == 2.0 && Lc.toDense()(2, 1) == -1.0);
+  WeightedGraph iso(4, {{0, 2, 1.0}});
+  SparseMatrix Li = IncidenceOperator(iso).laplacian();
+  CHECK(Li.nonZeros() == 4 && Li.colptr[1] == Li.colptr[2]);  // node 1 isolated: empty column
+}
+
 TEST_CASE("q = infinity through the mirror") {  // no reference counterpart
   Matrix V(3, 1);
   V(0, 0) = 3.0;

@@ -202,6 +202,21 @@ def test_incidence_bitwise(cp, orc):
         cp.IncidenceOperator(g3).apply_transpose(np.zeros((3, 1)))
 
 
+def test_laplacian_csc(cp, orc):  # test_graph.cpp:173-210
+    p3 = cp.IncidenceOperator(cp.WeightedGraph(3, [(0, 1, 0.7), (1, 2, 0.2)])).laplacian().toarray()
+    assert np.array_equal(p3, [[1, -1, 0], [-1, 2, -1], [0, -1, 1]])
+    rng = np.random.default_rng(3)
+    n = 40
+    edges = sorted({(i, j) for i in range(n) for j in range(i + 1, n) if rng.random() < 0.15} | {(0, 1)})
+    g = cp.WeightedGraph(n + 2, [(i, j, 0.5 + rng.random()) for i, j in edges])  # two isolated nodes
+    L = cp.IncidenceOperator(g).laplacian()
+    B = np.zeros((n + 2, len(edges)))
+    for l, (i, j) in enumerate(edges):
+        B[i, l], B[j, l] = 1.0, -1.0
+    assert np.array_equal(L.toarray(), B @ B.T)
+    assert L.nnz == 2 * len(edges) + n and L.has_sorted_indices
+
+
 def test_connected_components(cp, orc):
     assert cp.connected_components(cp.WeightedGraph(5, [(0, 1, 1.0), (2, 3, 1.0)])).tolist() == [0, 0, 1, 1, 2]
     assert cp.connected_components(cp.WeightedGraph(4, [(2, 3, 1.0)])).tolist() == [0, 1, 2, 2]
