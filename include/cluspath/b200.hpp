@@ -362,6 +362,33 @@ inline Matrix prox_jacobian_diag(const Matrix& V, const Vector& thresholds, Pena
                                       V.cols(), out.data()));
   return out;
 }
+// prox_jacobian (prox.hpp:38-54): the structured Jacobian of prox_{t||.||} at v;
+// apply / diag evaluate on the device (cp_prox_jacobian_apply / _diag).
+struct ProxJacobian {
+  Vector v;
+  double t = 0.0;
+  PenaltyNorm norm = PenaltyNorm::l2;
+  Vector apply(const Vector& w) const {
+    if (w.size() != v.size()) throw std::invalid_argument("ProxJacobian::apply: size mismatch");
+    Vector out(v.size());
+    const double tt[1] = {t};
+    detail::check(cp_prox_jacobian_apply(detail::ctx(), penalty_q(norm), v.data(), tt, w.data(),
+                                         static_cast<int64_t>(v.size()), 1, out.data()));
+    return out;
+  }
+  double diag(Index r) const {
+    Vector out(v.size());
+    const double tt[1] = {t};
+    detail::check(cp_prox_jacobian_diag(detail::ctx(), penalty_q(norm), v.data(), tt,
+                                        static_cast<int64_t>(v.size()), 1, out.data()));
+    return out[static_cast<size_t>(r)];
+  }
+};
+inline ProxJacobian prox_jacobian(const Vector& v, double t, PenaltyNorm norm) {
+  if (!(t >= 0.0) || !std::isfinite(t)) throw std::invalid_argument("prox_jacobian: threshold must be finite and >= 0");
+  return ProxJacobian{v, t, norm};
+}
+
 inline double moreau_check(const Vector& v, double t, PenaltyNorm norm) {
   const Vector p = prox_norm(v, t, norm), q = project_dual_ball(v, t, norm);
   double m = 0.0;

@@ -195,6 +195,10 @@ int cp_prox_columns(cp_ctx* ctx, int q, const double* V, const double* threshold
 /* project_columns (prox.hpp:30-31; prox.cpp:82-93) */
 int cp_project_columns(cp_ctx* ctx, int q, const double* Z, const double* radii, int64_t d, int64_t E, double* out);
 /* ProxJacobian::diag for every column (prox.hpp:38-49; prox.cpp:106-132): out d x E */
+/* ProxJacobian::apply (prox.hpp:38-47; prox.cpp:95-132) column-wise: out_l =
+ * M_l W_l, M_l the structured Jacobian of prox_{t_l ||.||_q} at V_l. */
+int cp_prox_jacobian_apply(cp_ctx* ctx, int q, const double* V, const double* thresholds, const double* W,
+                           int64_t d, int64_t E, double* out);
 int cp_prox_jacobian_diag(cp_ctx* ctx, int q, const double* V, const double* thresholds, int64_t d, int64_t E,
                           double* out);
 

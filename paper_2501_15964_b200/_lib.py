@@ -91,6 +91,7 @@ _SIGS = [
     ("cp_laplacian_lambda_max", C.c_int, [VP, VP, C.c_double, C.c_int64, D]),
     ("cp_prox_columns", C.c_int, [VP, C.c_int, D, D, C.c_int64, C.c_int64, D]),
     ("cp_project_columns", C.c_int, [VP, C.c_int, D, D, C.c_int64, C.c_int64, D]),
+    ("cp_prox_jacobian_apply", C.c_int, [VP, C.c_int, D, D, D, C.c_int64, C.c_int64, D]),
     ("cp_prox_jacobian_diag", C.c_int, [VP, C.c_int, D, D, C.c_int64, C.c_int64, D]),
     ("cp_primal_objective", C.c_int, [VP, VP, VP, C.c_double, C.c_int, D, D]),
     ("cp_dual_objective", C.c_int, [VP, VP, VP, C.c_double, C.c_int, D, D]),

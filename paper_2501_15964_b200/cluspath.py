@@ -534,6 +534,46 @@ def project_columns(Z, radii, norm=PenaltyNorm.l2, ctx=None):
     return _cols_call(L.load().cp_project_columns, _qcode(norm), Z, radii, ctx)
 
 
+def prox_jacobian_apply(V, thresholds, W, norm=PenaltyNorm.l2, ctx=None):
+    """Columnwise M_l W_l with M_l = Jacobian of prox at V_l (prox.cpp:95-132), on the GPU."""
+    ctx = ctx or default_context()
+    V, W = _f64(V), _f64(W)
+    if V.shape != W.shape or V.ndim != 2:
+        raise ValueError("prox_jacobian_apply: V and W must have the same (E, d) shape")
+    t = _f64(thresholds)
+    out = np.empty_like(V)
+    L.check(L.load().cp_prox_jacobian_apply(ctx._h, _qcode(norm), _dp(V), _dp(t), _dp(W), V.shape[1], V.shape[0],
+                                            _dp(out)))
+    return out
+
+
+class ProxJacobian:
+    """prox_jacobian(v, t, norm) (prox.hpp:38-47): apply(w) and diag(r) of the
+    structured Jacobian of prox_{t||.||} at v, evaluated on the GPU."""
+
+    def __init__(self, v, t, norm=PenaltyNorm.l2, ctx=None):
+        self.v = _f64(v).reshape(-1)
+        self.t = float(t)
+        self.norm = norm
+        self.ctx = ctx
+
+    def apply(self, w):
+        w = _f64(w).reshape(-1)
+        if w.shape != self.v.shape:
+            raise ValueError("ProxJacobian::apply: size mismatch")
+        return prox_jacobian_apply(self.v[None, :], [self.t], w[None, :], self.norm, self.ctx)[0]
+
+    def diag(self, r=None):
+        dg = prox_jacobian_diag(self.v[None, :], [self.t], self.norm, self.ctx)[0]
+        return dg if r is None else dg[r]
+
+
+def prox_jacobian(v, t, norm=PenaltyNorm.l2, ctx=None) -> ProxJacobian:
+    if not (t >= 0) or not math.isfinite(t):
+        raise ValueError("prox_jacobian: threshold must be finite and >= 0")
+    return ProxJacobian(v, t, norm, ctx)
+
+
 def prox_jacobian_diag(V, thresholds, norm=PenaltyNorm.l2, ctx=None):
     """ProxJacobian::diag per column (prox.cpp:106-132)."""
     return _cols_call(L.load().cp_prox_jacobian_diag, _qcode(norm), V, thresholds, ctx)

@@ -514,6 +514,15 @@ int cp_project_columns(cp_ctx* ctx, int q, const double* Z, const double* radii,
     cpb::project_columns_dev(c, q, v, t, d, E, o);
   });
 }
+int cp_prox_jacobian_apply(cp_ctx* ctx, int q, const double* V, const double* thresholds, const double* W,
+                           int64_t d, int64_t E, double* out) {
+  return columns_call(ctx, q, V, thresholds, d, E, out, "prox_jacobian",
+                      [&](cpb::Ctx& c, double* v, double* t, double* o) {
+                        need(W, "W");
+                        double* w = upload(c, "api.w", W, d * E);
+                        cpb::prox_jacobian_apply_dev(c, q, v, t, w, d, E, o);
+                      });
+}
 int cp_prox_jacobian_diag(cp_ctx* ctx, int q, const double* V, const double* thresholds, int64_t d, int64_t E,
                           double* out) {
   return columns_call(ctx, q, V, thresholds, d, E, out, "prox_jacobian",

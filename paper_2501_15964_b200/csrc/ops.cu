@@ -188,6 +188,45 @@ __global__ void k_jac_diag_cols(int q, const double* __restrict__ V, const doubl
   }
 }
 
+// ProxJacobian::apply (prox.cpp:95-104, :112-132) column-wise: out_l = M_l w_l
+// with M_l the structured Jacobian of prox_{t_l ||.||} at v_l.
+__global__ void k_jac_apply_cols(int q, const double* __restrict__ V, const double* __restrict__ t,
+                                 const double* __restrict__ W, int64_t E, int d, double* __restrict__ out) {
+  const unsigned gm = group_mask();
+  ROWS_BEGIN(E) {
+    const double* v = V + row_ * d;
+    const double* w = W + row_ * d;
+    double* o = out + row_ * d;
+    const double tl = t[row_];
+    if (q == Q_L2) {  // alpha w + beta <v, w> v outside the ball, 0 at/inside the kink, w at t = 0
+      double ss = 0.0, vw = 0.0;
+      for (int f = threadIdx.x; f < d; f += blockDim.x) ss += v[f] * v[f], vw += v[f] * w[f];
+      const double nv = sqrt(group_sum(ss, gm));
+      vw = group_sum(vw, gm);
+      double al = 0.0, be = 0.0;
+      if (tl == 0.0) {
+        al = 1.0;
+      } else if (nv > tl) {
+        al = 1.0 - tl / nv;
+        be = tl / (nv * nv * nv);
+      }
+      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = al * w[f] + (be != 0.0 ? be * vw * v[f] : 0.0);
+    } else if (q == Q_LINF) {  // w - (1_S w - s <s, w> / |S|); 0 inside the l1 ball
+      int cnt;
+      const double th = linf_theta([&](int f) { return v[f]; }, d, tl, gm, &cnt);
+      double sw = 0.0;
+      for (int f = threadIdx.x; f < d; f += blockDim.x)
+        if (th >= 0.0 && fabs(v[f]) > th) sw += (v[f] > 0.0 ? w[f] : -w[f]);
+      sw = group_sum(sw, gm);
+      const double b = cnt > 0 ? sw / cnt : 0.0;
+      for (int f = threadIdx.x; f < d; f += blockDim.x)
+        o[f] = th < 0.0 ? 0.0 : (fabs(v[f]) > th ? (v[f] > 0.0 ? b : -b) : w[f]);
+    } else {  // strict |v_r| > t mask
+      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = fabs(v[f]) > tl ? w[f] : 0.0;
+    }
+  }
+}
+
 // ---- SSNAL: phi edge pass (ssnal.cpp:24-39) -------------------------------------------
 // V = X B + Z / sigma (write), nv = ||V_l||, envelope partial
 //   sum_l gamma w_l ||P_l||_q + sigma/2 ||P_l - V_l||^2.
@@ -1015,6 +1054,14 @@ void project_columns_dev(Ctx& c, int q, const double* Z, const double* r, int64_
   k_project_cols<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(q, Z, r, E, static_cast<int>(d), out);
   CPB_LAUNCH_CHECK();
 }
+void prox_jacobian_apply_dev(Ctx& c, int q, const double* V, const double* t, const double* W, int64_t d, int64_t E,
+                             double* out) {
+  if (E == 0) return;
+  GroupGeom gg = group_geom(c, E, d);
+  k_jac_apply_cols<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(q, V, t, W, E, static_cast<int>(d), out);
+  CPB_LAUNCH_CHECK();
+}
+
 void prox_jacobian_diag_dev(Ctx& c, int q, const double* V, const double* t, int64_t d, int64_t E, double* out) {
   if (E == 0) return;
   GroupGeom gg = group_geom(c, E, d);

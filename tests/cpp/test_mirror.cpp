@@ -420,6 +420,16 @@ TEST_CASE("laplacian of the path and complete graphs") {  // test_graph.cpp:173-
   CHECK(Li.nonZeros() == 4 && Li.colptr[1] == Li.colptr[2]);  // node 1 isolated: empty column
 }
 
+TEST_CASE("prox jacobian structure") {  // test_prox.cpp:146-170
+  ProxJacobian J = prox_jacobian(Vector{3.0, 4.0}, 1.0, PenaltyNorm::l2);
+  CHECK(approx(J.diag(0), 0.8 + 9.0 / 125.0, 1e-14));
+  Vector y = J.apply(Vector{1.0, 0.0});
+  CHECK(approx(y[0], 0.8 + 9.0 / 125.0, 1e-14) && approx(y[1], 12.0 / 125.0, 1e-14));
+  Vector z = prox_jacobian(Vector{3.0, 4.0}, 5.0, PenaltyNorm::l2).apply(Vector{1.0, 2.0});
+  CHECK(z[0] == 0.0 && z[1] == 0.0);
+  CHECK_THROWS_AS(prox_jacobian(Vector{1.0}, -1.0, PenaltyNorm::l1), std::invalid_argument);
+}
+
 TEST_CASE("q = infinity through the mirror") {  // no reference counterpart
   Matrix V(3, 1);
   V(0, 0) = 3.0;

@@ -269,6 +269,27 @@ def test_prox_project_jacobian(cp, orc, q):
         cp.prox_columns(np.ones((1, 2)), [0.5], 3)
 
 
+@pytest.mark.parametrize("q", [1, 2, 0])
+def test_prox_jacobian_apply(cp, orc, q):  # test_prox.cpp:124-188 (q = 0: infinity)
+    rng = np.random.default_rng(70 + q)
+    for d in (1, 3, 33, 300):
+        V = rng.normal(0, 2.0, (40, d))
+        base = np.abs(V).sum(axis=1) if q == 0 else (np.linalg.norm(V, axis=1) if q == 2 else np.abs(V).max(axis=1))
+        t = rng.uniform(0.05, 1.2, 40) * base
+        t[0] = 0.0
+        W = rng.normal(0, 1.0, (40, d))
+        out = cp.prox_jacobian_apply(V, t, W, q)
+        for l in range(40):
+            J, _, _ = orc.prox_jacobian(q, V[l], t[l])
+            assert np.allclose(out[l], J @ W[l], rtol=1e-12, atol=1e-12)
+    J = cp.prox_jacobian([3.0, 4.0], 1.0)  # test_prox.cpp:146-170
+    assert J.diag(0) == pytest.approx(0.8 + 9.0 / 125.0)
+    assert np.allclose(J.apply([1.0, 0.0]), [0.8 + 9.0 / 125.0, 12.0 / 125.0])
+    assert np.all(cp.prox_jacobian([3.0, 4.0], 5.0).apply([1.0, 2.0]) == 0)  # kink -> zero map
+    with pytest.raises(ValueError):
+        cp.prox_jacobian([1.0], -1.0)
+
+
 def test_prox_project_jacobian_linf(cp, orc):
     """q = infinity (code 0): no reference; parity against the oracle's sort-based
     l1-ball threshold (the GPU uses Michelot's fixed point)."""
