@@ -332,6 +332,29 @@ __global__ void __launch_bounds__(256) k_edge_dot(const double* __restrict__ P, 
     const double* pb = P + static_cast<int64_t>(ej[l]) * d;
     const double* vl = V + l * d;
     double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+    if ((d & 1) == 0) {  // even d: 16-byte loads of feature pairs, two pairs per lane in flight
+      const int h = d >> 1;
+      const double2* v2 = reinterpret_cast<const double2*>(vl);
+      const double2* a2 = reinterpret_cast<const double2*>(pa);
+      const double2* b2 = reinterpret_cast<const double2*>(pb);
+      int k = lane;
+      for (; k + 32 < h; k += 64) {
+        const double2 v0 = __ldcs(v2 + k), v1 = __ldcs(v2 + k + 32);
+        const double2 x0 = a2[k], x1 = a2[k + 32], y0 = b2[k], y1 = b2[k + 32];
+        c0 = __fma_rn(v0.x, x0.x - y0.x, c0);
+        c1 = __fma_rn(v0.y, x0.y - y0.y, c1);
+        c2 = __fma_rn(v1.x, x1.x - y1.x, c2);
+        c3 = __fma_rn(v1.y, x1.y - y1.y, c3);
+      }
+      if (k < h) {
+        const double2 v0 = __ldcs(v2 + k), x0 = a2[k], y0 = b2[k];
+        c0 = __fma_rn(v0.x, x0.x - y0.x, c0);
+        c1 = __fma_rn(v0.y, x0.y - y0.y, c1);
+      }
+      const double c = warp_sum((c0 + c1) + (c2 + c3));
+      if (lane == 0) bc[l] = be * c;
+      continue;
+    }
     int f = lane;
     for (; f + 96 < d; f += 128) {
       const double v0 = __ldcs(vl + f), v1 = __ldcs(vl + f + 32), v2 = __ldcs(vl + f + 64), v3 = __ldcs(vl + f + 96);

@@ -15,7 +15,9 @@
 // whose partial sums a second kernel combines in segment order
 // (deterministic).  Items run in node-id order, so both endpoints of an edge
 // of a clustered graph tend to read v_l within the L2 window.
+#include <algorithm>
 #include <cstdlib>
+#include <queue>
 #include <string>
 #include <vector>
 
@@ -34,9 +36,12 @@ constexpr int kMaxStages = 8;  // ring depth per warp: 2 at d = 784, up to 8 for
 // Per-warp shared memory: a metadata table for the current segment (<= 64
 // edges: id, other endpoint, 1 - alpha, beta) filled with two coalesced
 // rounds at segment start, and an S-deep ring of {p_other row, v row}.
-// Per edge, with c = <v_l, p_v - p_o> (sign-free), the edge adds
-//   (1 - alpha)(p_v - p_o) - beta c v_l
-// to node v: one FMA per feature for the dot, two for the update.
+// Per edge, with w = p_v - p_o and c = <v_l, w> (sign-free), the edge adds
+//   (1 - alpha) w - beta c v_l
+// to node v: one FMA per feature for the dot, two for the update (w is kept
+// in registers, so the update reads only v_l back from shared memory).  An
+// edge with beta = 0 (prox zero) adds (1 - alpha)(p_v - p_o): its p_v part is
+// folded into one final FMA.
 template <int NK>
 __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, const double* __restrict__ V,
                                                   const double* __restrict__ jal, const double* __restrict__ jbe,
@@ -45,7 +50,7 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
                                                   const int* __restrict__ seg_end, const int* __restrict__ seg_slot,
                                                   int nseg, int d, int dp, double sigma, double* __restrict__ Ap,
                                                   double* __restrict__ partial, double* part, const int* active,
-                                                  int evict_v, int S) {
+                                                  int evict_v, int S, const int* __restrict__ wrange) {
   if (active && !*active) return;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ double sh[32];
@@ -68,20 +73,28 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
   int cst = 0;        // next ring slot to consume
   unsigned cph = 0;   // its mbarrier phase parity
   double s_a = 0.0, s_b = 0.0;
-  const uint64_t vpol = evict_v ? policy_evict_first() : 0;
+  // evict_v bit 0: V_l rows evict_first; bit 1: gathered p rows evict_last
+  const uint64_t vpol = (evict_v & 1) ? policy_evict_first() : 0;
+  const uint64_t ppol = (evict_v & 2) ? policy_evict_last() : 0;
   auto issue = [&](int q, int st) {  // lane 0: stream edge q's rows into stage st
     const bool nv = mb[q] != 0.0;
     mbar_expect_tx(&bar[st], nv ? 2 * row_bytes : row_bytes);
-    bulk_g2s(ring + st * 2 * dp, P + static_cast<int64_t>(lo[q]) * d, row_bytes, &bar[st]);
+    if (evict_v & 2)
+      bulk_g2s_hint(ring + st * 2 * dp, P + static_cast<int64_t>(lo[q]) * d, row_bytes, &bar[st], ppol);
+    else
+      bulk_g2s(ring + st * 2 * dp, P + static_cast<int64_t>(lo[q]) * d, row_bytes, &bar[st]);
     if (nv) {
-      if (evict_v)
+      if (evict_v & 1)
         bulk_g2s_hint(ring + st * 2 * dp + dp, V + static_cast<int64_t>(le[q]) * d, row_bytes, &bar[st], vpol);
       else
         bulk_g2s(ring + st * 2 * dp + dp, V + static_cast<int64_t>(le[q]) * d, row_bytes, &bar[st]);
     }
   };
   const int wid = blockIdx.x * (blockDim.x >> 5) + warp, nw = gridDim.x * (blockDim.x >> 5);
-  for (int it = wid; it < nseg; it += nw) {
+  // each warp walks its balanced item list (wrange: offsets, then items) or, without it, every nw-th item
+  const int j0 = wrange ? wrange[wid] : wid, j1 = wrange ? wrange[wid + 1] : nseg, jstep = wrange ? 1 : nw;
+  for (int j = j0; j < j1; j += jstep) {
+    const int it = wrange ? wrange[j] : j;
     const int v = seg_node[it], e0 = seg_beg[it], ne = seg_end[it] - e0, slot = seg_slot[it];
     const int64_t base = static_cast<int64_t>(v) * d;
     // segment metadata: coalesced loads, then gathers of alpha / beta
@@ -94,7 +107,6 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
     }
     __syncwarp();
     if (lane == 0) {
-      fence_proxy_async();
       for (int s = 0, t = cst; s < S && s < ne; ++s, t = (t + 1 == S) ? 0 : t + 1) issue(s, t);
     }
     double pv[NK], acc[NK];
@@ -112,37 +124,39 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
       if (++cst == S) cst = 0, cph ^= 1u;
       const double* po = ring + st * 2 * dp;
       const double* vl = po + dp;
-      dsum += cq;
       if (be != 0.0) {
-        double c0 = 0.0, c1 = 0.0;
+        // w = p_v - p_o stays in registers: the update re-reads only v_l
+        double w[NK];
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
 #pragma unroll
         for (int k = 0; k < NK; ++k) {
           const int f = lane + 32 * k;
+          w[k] = f < d ? pv[k] - po[f] : 0.0;
           if (f < d) {
-            if (k & 1)
-              c1 = __fma_rn(vl[f], pv[k] - po[f], c1);
-            else
-              c0 = __fma_rn(vl[f], pv[k] - po[f], c0);
+            if ((k & 3) == 0) c0 = __fma_rn(vl[f], w[k], c0);
+            if ((k & 3) == 1) c1 = __fma_rn(vl[f], w[k], c1);
+            if ((k & 3) == 2) c2 = __fma_rn(vl[f], w[k], c2);
+            if ((k & 3) == 3) c3 = __fma_rn(vl[f], w[k], c3);
           }
         }
-        const double bc = be * warp_sum(c0 + c1);
+        const double bc = be * warp_sum((c0 + c1) + (c2 + c3));
 #pragma unroll
         for (int k = 0; k < NK; ++k) {
           const int f = lane + 32 * k;
-          if (f < d) acc[k] = __fma_rn(-bc, vl[f], __fma_rn(-cq, po[f], acc[k]));
+          if (f < d) acc[k] = __fma_rn(cq, w[k], __fma_rn(-bc, vl[f], acc[k]));
         }
       } else {
+        dsum += cq;
 #pragma unroll
         for (int k = 0; k < NK; ++k) {
           const int f = lane + 32 * k;
           if (f < d) acc[k] = __fma_rn(-cq, po[f], acc[k]);
         }
       }
+      // the warp's reads of this slot are ordered before the refill by the
+      // warp barrier (only reads: no generic->async proxy fence is needed)
       __syncwarp();
-      if (lane == 0 && q + S < ne) {
-        fence_proxy_async();
-        issue(q + S, st);
-      }
+      if (lane == 0 && q + S < ne) issue(q + S, st);
     }
     __syncwarp();  // metadata table is rewritten by the next segment
     if (slot < 0) {
@@ -213,7 +227,49 @@ struct SegPlan {
   int64_t v0 = 0, v1 = -1;  // node range the items cover (v1 < 0: all nodes)
   int nseg = 0, nhub = 0, nslots = 0;
   DBuf<int> node, beg, end, slot, hub_node, hub_slot0, hub_nslots;
+  std::vector<int64_t> cost_prefix;  // per-item cost prefix (edges + fixed overhead)
+  int split_nw = 0;                  // warp count `wrange` was cut for
+  DBuf<int> wrange;  // nw + 1 list offsets, then the items of every warp's list
 };
+
+// Per-warp item lists: the items are taken in windows of nw consecutive
+// (breadth-first) items, so all warps work on neighbouring nodes at the same
+// time (L2 reuse of V_l and the gathered p rows, as with round-robin), and
+// inside each window the largest items go to the least-loaded warps so the
+// warps finish together (round-robin left the longest warp ~15 % behind).
+const int* warp_ranges(Ctx& c, SegPlan& p, int nw) {
+  if (p.split_nw == nw) return p.wrange.p;
+  std::vector<std::vector<int>> lists(static_cast<size_t>(nw));
+  using Load = std::pair<int64_t, int>;
+  std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+  for (int w = 0; w < nw; ++w) heap.push({0, w});
+  std::vector<int> win;
+  for (int w0 = 0; w0 < p.nseg; w0 += nw) {
+    const int w1 = std::min(p.nseg, w0 + nw);
+    win.clear();
+    for (int it = w0; it < w1; ++it) win.push_back(it);
+    auto cost = [&](int it) { return p.cost_prefix[it + 1] - p.cost_prefix[it]; };
+    std::stable_sort(win.begin(), win.end(), [&](int a, int b) { return cost(a) > cost(b); });
+    for (int it : win) {
+      Load l = heap.top();
+      heap.pop();
+      lists[static_cast<size_t>(l.second)].push_back(it);
+      heap.push({l.first + cost(it), l.second});
+    }
+  }
+  std::vector<int> flat(static_cast<size_t>(nw) + 1 + p.nseg);
+  int pos = nw + 1;
+  for (int w = 0; w < nw; ++w) {
+    flat[static_cast<size_t>(w)] = pos;
+    for (int it : lists[static_cast<size_t>(w)]) flat[static_cast<size_t>(pos++)] = it;
+  }
+  flat[static_cast<size_t>(nw)] = pos;
+  p.wrange.resize(flat.size());
+  h2d(c, p.wrange.p, flat.data(), flat.size() * sizeof(int));
+  c.sync();
+  p.split_nw = nw;
+  return p.wrange.p;
+}
 
 SegPlan& seg_plan(Ctx& c, const Graph& g) {
   static thread_local std::vector<std::unique_ptr<SegPlan>> plans;
@@ -274,6 +330,8 @@ SegPlan& seg_plan(Ctx& c, const Graph& g) {
   up(p->hub_node, hn), up(p->hub_slot0, hs), up(p->hub_nslots, hc);
   c.sync();
   p->nseg = static_cast<int>(node.size());
+  p->cost_prefix.assign(node.size() + 1, 0);
+  for (size_t i = 0; i < node.size(); ++i) p->cost_prefix[i + 1] = p->cost_prefix[i] + (end[i] - beg[i]) + 4;
   p->nhub = static_cast<int>(hn.size());
   p->nslots = slots;
   if (plans.size() > 8) plans.erase(plans.begin());
@@ -335,7 +393,7 @@ int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const dou
     const char* e = std::getenv("CPB_HESS_VEVICT");
     return e ? std::atoi(e) : -1;
   }();
-  const int evict_v = vevict_env > 0 ? 1 : 0;  // measured neutral-to-worse at C3 (1586 vs 1541 us)
+  const int evict_v = vevict_env > 0 ? (vevict_env & 3) : 0;  // measured neutral-to-worse at C3 (1586 vs 1541 us)
   // ring depth: 2 (deeper rings measured slower: C5 with 8 stages 38.8 vs 17.4 ms);
   // CPB_HESS_STAGES overrides
   static const int s_env = [] {
@@ -350,10 +408,15 @@ int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const dou
   // partitioned PCG: every rank launches the same grid so the partial tables line up
   const bool parted = c.own_v1 >= 0;
   const int grid = parted ? c.sm_count * 2 : std::max(1, std::min(cdiv(sp.nseg, warps), c.sm_count * 2));
+  static const bool rr = [] {
+    const char* e = std::getenv("CPB_HESS_SPLIT");
+    return e && std::string(e) == "rr";
+  }();
+  const int* wr = rr ? nullptr : warp_ranges(c, sp, grid * warps);
   NK_DISPATCH(nk, k_hess_tma, <<<grid, 32 * warps, smem, c.s>>>(P, V, jal, jbe, g.adj_e.p, g.adj_o.p, sp.node.p,
                                                                 sp.beg.p, sp.end.p, sp.slot.p, sp.nseg,
                                                                 static_cast<int>(d), dp, sigma, Ap, partial, part,
-                                                                active, evict_v, S));
+                                                                active, evict_v, S, wr));
   CPB_LAUNCH_CHECK();
   int nb = grid;
   if (sp.nhub > 0 || parted) {
