@@ -13,9 +13,13 @@
 #include <cstdlib>
 
 #include <algorithm>
+#include <memory>
+#include <string>
+#include <vector>
 
 #include "comm.cuh"
 #include "gather.cuh"
+#include "graph.cuh"
 
 namespace cpb {
 
@@ -515,6 +519,130 @@ __global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, co
   }
 }
 
+
+// ---- single-pass Hessian for short rows (q = 2, even d <= 256) --------------------------
+// One warp per node; lane l holds the feature pairs 2(l + 32k), k < NP, as
+// double2.  Per batch of kEB incident edges it loads p_other and v_l (16-byte
+// loads, all in flight together), forms the kEB dots <v_l, p_v - p_o> with
+// interleaved butterfly reductions and adds (1 - alpha) w - beta c v_l.  This
+// replaces the two-pass path (k_edge_dot + k_g_hess), which read V three times
+// and gathered every p row four times, by one pass that reads V once per
+// endpoint.
+template <int NP>
+__global__ void __launch_bounds__(256, NP == 1 ? 2 : 1) k_hess_warp(const double* __restrict__ P, const double* __restrict__ V,
+                                                   const double* __restrict__ jal, const double* __restrict__ jbe,
+                                                   const int* __restrict__ off, const int* __restrict__ adj_e,
+                                                   const int* __restrict__ adj_o, const int* __restrict__ order,
+                                                   int64_t n, int d, double sigma, double* __restrict__ Ap,
+                                                   double* part, const int* active, const int* __restrict__ wl) {
+  if (active && !*active) return;
+  __shared__ double sh[32];
+  const int lane = threadIdx.x & 31;
+  const int h = d >> 1;  // double2 per row
+  // node lists per warp (wl: offsets, then node ids) or a grid-stride walk of `order`
+  const int64_t wid = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t j0 = wl ? wl[wid] : wid, j1 = wl ? wl[wid + 1] : n, jstep = wl ? 1 : nwarps;
+  const double2* P2 = reinterpret_cast<const double2*>(P);
+  const double2* V2 = reinterpret_cast<const double2*>(V);
+  double s_a = 0.0, s_b = 0.0;
+  for (int64_t jt = j0; jt < j1; jt += jstep) {
+    const int v = wl ? wl[jt] : order[jt];
+    const int p0 = off[v], p1 = off[v + 1];
+    const int64_t base = static_cast<int64_t>(v) * h;
+    double2 pv[NP], acc[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const int j = lane + 32 * k;
+      pv[k] = j < h ? P2[base + j] : make_double2(0.0, 0.0);
+      acc[k] = make_double2(0.0, 0.0);
+    }
+    double dsum = 0.0;  // sum of (1 - alpha) over edges with beta = 0 (their p_v part)
+    for (int p = p0; p < p1; p += 32) {
+      const int cnt = min(32, p1 - p);
+      const int my_e = lane < cnt ? adj_e[p + lane] : 0;
+      const int my_o = lane < cnt ? adj_o[p + lane] : v;
+      const double my_a = lane < cnt ? 1.0 - jal[my_e] : 0.0;
+      const double my_b = lane < cnt ? jbe[my_e] : 0.0;
+      for (int u0 = 0; u0 < cnt; u0 += kEB) {
+        int le[kEB], lo[kEB];
+        double ca[kEB], be[kEB];
+#pragma unroll
+        for (int u = 0; u < kEB; ++u) {
+          const int src = (u0 + u) & 31;
+          le[u] = __shfl_sync(kFull, my_e, src);
+          lo[u] = __shfl_sync(kFull, my_o, src);
+          ca[u] = __shfl_sync(kFull, my_a, src);
+          be[u] = __shfl_sync(kFull, my_b, src);
+        }
+        double2 po[kEB][NP], vv[kEB][NP];
+#pragma unroll
+        for (int u = 0; u < kEB; ++u) {
+          const bool ok = u0 + u < cnt;
+          const bool nv = ok && be[u] != 0.0;
+#pragma unroll
+          for (int k = 0; k < NP; ++k) {
+            const int j = lane + 32 * k;
+            po[u][k] = (ok && j < h) ? __ldg(P2 + static_cast<int64_t>(lo[u]) * h + j) : make_double2(0.0, 0.0);
+            vv[u][k] = (nv && j < h) ? __ldcs(V2 + static_cast<int64_t>(le[u]) * h + j) : make_double2(0.0, 0.0);
+          }
+        }
+        double cu[kEB];
+#pragma unroll
+        for (int u = 0; u < kEB; ++u) {
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < NP; ++k) {
+            c0 = __fma_rn(vv[u][k].x, pv[k].x - po[u][k].x, c0);
+            c1 = __fma_rn(vv[u][k].y, pv[k].y - po[u][k].y, c1);
+          }
+          cu[u] = c0 + c1;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int u = 0; u < kEB; ++u) cu[u] += __shfl_xor_sync(kFull, cu[u], o);
+#pragma unroll
+        for (int u = 0; u < kEB; ++u) {
+          if (u0 + u >= cnt) continue;
+          if (be[u] != 0.0) {
+            const double bc = be[u] * cu[u];
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+              acc[k].x = __fma_rn(ca[u], pv[k].x - po[u][k].x, __fma_rn(-bc, vv[u][k].x, acc[k].x));
+              acc[k].y = __fma_rn(ca[u], pv[k].y - po[u][k].y, __fma_rn(-bc, vv[u][k].y, acc[k].y));
+            }
+          } else {
+            dsum += ca[u];
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+              acc[k].x = __fma_rn(-ca[u], po[u][k].x, acc[k].x);
+              acc[k].y = __fma_rn(-ca[u], po[u][k].y, acc[k].y);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const int j = lane + 32 * k;
+      if (j >= h) continue;
+      double2 o;
+      o.x = pv[k].x + sigma * __fma_rn(dsum, pv[k].x, acc[k].x);
+      o.y = pv[k].y + sigma * __fma_rn(dsum, pv[k].y, acc[k].y);
+      reinterpret_cast<double2*>(Ap)[base + j] = o;
+      s_a += pv[k].x * o.x + pv[k].y * o.y;
+      s_b += pv[k].x * pv[k].x + pv[k].y * pv[k].y;
+    }
+  }
+  s_a = block_sum(s_a, sh);
+  s_b = block_sum(s_b, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s_a;
+    part[2 * blockIdx.x + 1] = s_b;
+  }
+}
+
 #define NF_DISPATCH(nf, KERNEL, ...)           \
   switch (nf) {                                \
     case 1: KERNEL<1> __VA_ARGS__; break;      \
@@ -758,10 +886,78 @@ int gather_grad_diag(Ctx& c, const Graph& g, const double* X, const double* A, c
   return ng.grid;
 }
 
+// Optional work lists of the single-pass short-row Hessian
+// (CPB_HESS_WARP_ORDER=bfs): breadth-first node order (this rank's nodes when
+// partitioned) cut by lpt_lists into windows of one node per warp, cost =
+// degree + 4, cached per (graph, node range, warps).  Measured 2x slower than
+// the default grid-stride walk of the degree-descending order at C5 (13.3 vs
+// 7.0 ms): the concurrently processed breadth-first window shares its
+// neighbours, so many warps gather the same rows at once.
+struct WarpNodeLists {
+  uint64_t uid = 0;
+  int64_t v0 = 0, v1 = -1;
+  int nw = 0;
+  DBuf<int> flat;
+};
+const int* warp_node_lists(Ctx& c, const Graph& g, int nw) {
+  static const bool on = [] {
+    const char* e = std::getenv("CPB_HESS_WARP_ORDER");
+    return e && std::string(e) == "bfs";
+  }();
+  if (!on) return nullptr;
+  static thread_local std::vector<std::unique_ptr<WarpNodeLists>> cache;
+  for (auto& w : cache)
+    if (w->uid == g.uid && w->v0 == c.own_v0 && w->v1 == c.own_v1 && w->nw == nw) return w->flat.p;
+  auto w = std::make_unique<WarpNodeLists>();
+  w->uid = g.uid, w->v0 = c.own_v0, w->v1 = c.own_v1, w->nw = nw;
+  std::vector<int> off;
+  const std::vector<int> seq_all = bfs_sequence(c, g, &off);
+  std::vector<int> seq;
+  seq.reserve(seq_all.size());
+  for (int v : seq_all)
+    if (c.own_v1 < 0 || (v >= c.own_v0 && v < c.own_v1)) seq.push_back(v);
+  std::vector<int64_t> cost(seq.size());
+  for (size_t i = 0; i < seq.size(); ++i) cost[i] = off[seq[i] + 1] - off[seq[i]] + 4;
+  std::vector<int> flat = lpt_lists(cost, nw, nw);
+  for (size_t j = static_cast<size_t>(nw) + 1; j < flat.size(); ++j) flat[j] = seq[static_cast<size_t>(flat[j])];
+  w->flat.resize(flat.size());
+  h2d(c, w->flat.p, flat.data(), flat.size() * sizeof(int));
+  c.sync();
+  if (cache.size() > 8) cache.erase(cache.begin());
+  cache.push_back(std::move(w));
+  return cache.back()->flat.p;
+}
+
 int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,
                   const double* thr, int64_t d, double sigma, int q, double* bc, double* Ap, double* part,
                   const int* active) {
   if (q == 2 && g.E > 0 && hess_tma_supported(d)) return hess_tma(c, g, P, V, jal, jbe, d, sigma, Ap, part, active);
+  static const bool warp_hess = [] {  // CPB_HESS_WARP=0 keeps the two-pass path for short rows
+    const char* e = std::getenv("CPB_HESS_WARP");
+    return !(e && e[0] == '0');
+  }();
+  if (q == 2 && g.E > 0 && warp_hess && d % 2 == 0 && d <= 192) {
+    const int np = static_cast<int>((d / 2 + 31) / 32);
+    const int* ord = g.order.p;
+    int64_t items = g.n;
+    int grid = std::max(1, std::min(cdiv(g.n, 8), c.sm_count * 8));
+    if (c.own_v1 >= 0) {  // partitioned PCG: this rank's nodes, the same grid on every rank
+      const OwnOrder& o = own_order(c, g);
+      ord = o.order.p, items = o.count, grid = c.sm_count * 8;
+    }
+    const int* wl = warp_node_lists(c, g, grid * 8);
+    const int di = static_cast<int>(d);
+    switch (np) {
+      case 1: k_hess_warp<1><<<grid, 256, 0, c.s>>>(P, V, jal, jbe, g.off.p, g.adj_e.p, g.adj_o.p, ord, items, di,
+                                                   sigma, Ap, part, active, wl); break;
+      case 2: k_hess_warp<2><<<grid, 256, 0, c.s>>>(P, V, jal, jbe, g.off.p, g.adj_e.p, g.adj_o.p, ord, items, di,
+                                                   sigma, Ap, part, active, wl); break;
+      default: k_hess_warp<3><<<grid, 256, 0, c.s>>>(P, V, jal, jbe, g.off.p, g.adj_e.p, g.adj_o.p, ord, items, di,
+                                                    sigma, Ap, part, active, wl); break;
+    }
+    CPB_LAUNCH_CHECK();
+    return grid;
+  }
   if ((q == 2 || q == 0) && g.E > 0) {
     // per-edge dots: every edge, or in a partitioned solve this rank's owned + ghost edges
     auto dots = [&](const int* list, int64_t e0, int64_t cnt) {

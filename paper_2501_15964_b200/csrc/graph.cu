@@ -18,8 +18,11 @@
 #include <cub/cub.cuh>
 #include <math_constants.h>
 
+#include <algorithm>
 #include <cmath>
+#include <queue>
 #include <random>
+#include <vector>
 
 #include "comm.cuh"
 #include "gather.cuh"
@@ -534,6 +537,65 @@ void finalize_graph(Ctx& c, Graph& g) {
 // mean) first, then breadth-first.  Measured slower than the default
 // degree-descending order (C5 Hessian 13.6 vs 9.7 ms, C3 gap 1.39 vs 1.30 ms,
 // plus the host BFS), so it is off by default.
+// Breadth-first node sequence over all components (lowest unvisited id
+// starts the next one), with the CSR offsets copied to the host on the way.
+std::vector<int> bfs_sequence(Ctx& c, const Graph& g, std::vector<int>* off_out) {
+  const int n = static_cast<int>(g.n);
+  std::vector<int> off(static_cast<size_t>(n) + 1), adj(static_cast<size_t>(2 * g.E));
+  d2h(c, off.data(), g.off.p, off.size() * sizeof(int));
+  if (g.E > 0) d2h(c, adj.data(), g.adj_o.p, adj.size() * sizeof(int));
+  std::vector<int> seq(static_cast<size_t>(n));
+  std::vector<char> seen(static_cast<size_t>(n), 0);
+  size_t head = 0, tail = 0;
+  for (int s0 = 0; s0 < n; ++s0) {
+    if (seen[s0]) continue;
+    seen[s0] = 1;
+    seq[tail++] = s0;
+    while (head < tail) {
+      const int v = seq[head++];
+      for (int e = off[v]; e < off[v + 1]; ++e) {
+        const int o = adj[static_cast<size_t>(e)];
+        if (!seen[o]) seen[o] = 1, seq[tail++] = o;
+      }
+    }
+  }
+  if (off_out) *off_out = std::move(off);
+  return seq;
+}
+
+// Windowed longest-processing-time assignment: items (in the given order) are
+// cut into windows of `win` consecutive items; inside each window the largest
+// items go to the least-loaded of the nw warps.  Returns nw + 1 offsets
+// followed by every warp's item list (items keep their window order).
+std::vector<int> lpt_lists(const std::vector<int64_t>& cost, int nw, int win) {
+  const int m = static_cast<int>(cost.size());
+  std::vector<std::vector<int>> lists(static_cast<size_t>(nw));
+  using Load = std::pair<int64_t, int>;
+  std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+  for (int w = 0; w < nw; ++w) heap.push({0, w});
+  std::vector<int> wv;
+  for (int w0 = 0; w0 < m; w0 += win) {
+    const int w1 = std::min(m, w0 + win);
+    wv.clear();
+    for (int it = w0; it < w1; ++it) wv.push_back(it);
+    std::stable_sort(wv.begin(), wv.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    for (int it : wv) {
+      Load l = heap.top();
+      heap.pop();
+      lists[static_cast<size_t>(l.second)].push_back(it);
+      heap.push({l.first + cost[it], l.second});
+    }
+  }
+  std::vector<int> flat(static_cast<size_t>(nw) + 1 + m);
+  int pos = nw + 1;
+  for (int w = 0; w < nw; ++w) {
+    flat[static_cast<size_t>(w)] = pos;
+    for (int it : lists[static_cast<size_t>(w)]) flat[static_cast<size_t>(pos++)] = it;
+  }
+  flat[static_cast<size_t>(nw)] = pos;
+  return flat;
+}
+
 void locality_order(Ctx& c, Graph& g) {
   static const bool bfs = [] {
     const char* e = std::getenv("CPB_GATHER_ORDER");
@@ -541,26 +603,10 @@ void locality_order(Ctx& c, Graph& g) {
   }();
   const int n = static_cast<int>(g.n);
   if (!bfs || g.E == 0 || n < 2) return;
-  std::vector<int> off(static_cast<size_t>(n) + 1), adj(static_cast<size_t>(2 * g.E));
-  d2h(c, off.data(), g.off.p, off.size() * sizeof(int));
-  d2h(c, adj.data(), g.adj_o.p, adj.size() * sizeof(int));
+  std::vector<int> off;
+  const std::vector<int> bfs_seq = bfs_sequence(c, g, &off);
   const double mean = 2.0 * static_cast<double>(g.E) / n;
   auto hub = [&](int v) { return off[v + 1] - off[v] > 4.0 * mean + 16; };
-  std::vector<int> bfs_seq(static_cast<size_t>(n));
-  std::vector<char> seen(static_cast<size_t>(n), 0);
-  size_t head = 0, tail = 0;
-  for (int s0 = 0; s0 < n; ++s0) {
-    if (seen[s0]) continue;
-    seen[s0] = 1;
-    bfs_seq[tail++] = s0;
-    while (head < tail) {
-      const int v = bfs_seq[head++];
-      for (int e = off[v]; e < off[v + 1]; ++e) {
-        const int o = adj[static_cast<size_t>(e)];
-        if (!seen[o]) seen[o] = 1, bfs_seq[tail++] = o;
-      }
-    }
-  }
   std::vector<int> seq;
   seq.reserve(static_cast<size_t>(n));
   for (int v : bfs_seq)

@@ -13,6 +13,8 @@
 //   order    int32[n]       nodes by descending degree (work scheduling only)
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace cpb {
@@ -48,6 +50,8 @@ std::unique_ptr<Graph> graph_from_knn_dev(Ctx& c, int64_t n, int64_t k, double p
 void finalize_graph(Ctx& c, Graph& g);
 // Replaces g.order (degree-descending) by hubs-first breadth-first order.
 void locality_order(Ctx& c, Graph& g);
+std::vector<int> bfs_sequence(Ctx& c, const Graph& g, std::vector<int>* off_out);
+std::vector<int> lpt_lists(const std::vector<int64_t>& cost, int nw, int win);
 
 // Incidence operator on device arrays (row layouts as above).
 void incidence_apply_dev(Ctx& c, const Graph& g, const double* X, int64_t d, double* out);
