@@ -900,25 +900,46 @@ struct WarpNodeLists {
   DBuf<int> flat;
 };
 const int* warp_node_lists(Ctx& c, const Graph& g, int nw) {
-  static const bool on = [] {
+  static const int mode = [] {  // 0 off, 1 bfs + LPT windows, 2 node id + LPT windows, 3 bfs round-robin
     const char* e = std::getenv("CPB_HESS_WARP_ORDER");
-    return e && std::string(e) == "bfs";
+    if (!e) return 0;
+    const std::string v(e);
+    return v == "bfs" ? 1 : (v == "id" ? 2 : (v == "bfsrr" ? 3 : 0));
   }();
-  if (!on) return nullptr;
+  if (mode == 0) return nullptr;
   static thread_local std::vector<std::unique_ptr<WarpNodeLists>> cache;
   for (auto& w : cache)
     if (w->uid == g.uid && w->v0 == c.own_v0 && w->v1 == c.own_v1 && w->nw == nw) return w->flat.p;
   auto w = std::make_unique<WarpNodeLists>();
   w->uid = g.uid, w->v0 = c.own_v0, w->v1 = c.own_v1, w->nw = nw;
-  std::vector<int> off;
-  const std::vector<int> seq_all = bfs_sequence(c, g, &off);
+  std::vector<int> off, seq_all;
+  if (mode == 2) {
+    off.resize(static_cast<size_t>(g.n) + 1);
+    d2h(c, off.data(), g.off.p, off.size() * sizeof(int));
+    seq_all.resize(static_cast<size_t>(g.n));
+    for (int v = 0; v < g.n; ++v) seq_all[static_cast<size_t>(v)] = v;
+  } else {
+    seq_all = bfs_sequence(c, g, &off);
+  }
   std::vector<int> seq;
   seq.reserve(seq_all.size());
   for (int v : seq_all)
     if (c.own_v1 < 0 || (v >= c.own_v0 && v < c.own_v1)) seq.push_back(v);
   std::vector<int64_t> cost(seq.size());
   for (size_t i = 0; i < seq.size(); ++i) cost[i] = off[seq[i] + 1] - off[seq[i]] + 4;
-  std::vector<int> flat = lpt_lists(cost, nw, nw);
+  std::vector<int> flat;
+  if (mode == 3) {  // round-robin: warp w takes items w, w + nw, ...
+    flat.resize(static_cast<size_t>(nw) + 1 + seq.size());
+    size_t pos = static_cast<size_t>(nw) + 1;
+    for (int w = 0; w < nw; ++w) {
+      flat[static_cast<size_t>(w)] = static_cast<int>(pos);
+      for (size_t i = static_cast<size_t>(w); i < seq.size(); i += static_cast<size_t>(nw))
+        flat[pos++] = static_cast<int>(i);
+    }
+    flat[static_cast<size_t>(nw)] = static_cast<int>(pos);
+  } else {
+    flat = lpt_lists(cost, nw, nw);
+  }
   for (size_t j = static_cast<size_t>(nw) + 1; j < flat.size(); ++j) flat[j] = seq[static_cast<size_t>(flat[j])];
   w->flat.resize(flat.size());
   h2d(c, w->flat.p, flat.data(), flat.size() * sizeof(int));
