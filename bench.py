@@ -343,8 +343,17 @@ def run_ours(args, cfg):
     hs = stats.get("hess_apply", top[1])
     achieved = hs["alg_bytes"] / (hs["ms"] / 1e3) / 1e9 if hs["ms"] > 0 else 0.0
     total_ms = sum(v["ms"] for v in stats.values())
+    traffic = None
+    try:  # one ncu --set full capture of this config's Hessian (profiles/ncu_traffic_r01.json)
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")) as f:
+            traffic = json.load(f).get(args.config)
+    except Exception:
+        traffic = None
     roof = {"bound": "hbm", "kernel": "hess_apply", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
-            "unit": "GB/s", "frac": achieved / peak if peak else None, "traffic": None,
+            "unit": "GB/s", "frac": achieved / peak if peak else None,
+            "traffic": traffic["dram_bytes"] if traffic else None,
+            "traffic_launch": ({k: traffic[k] for k in ("kernel", "launch", "alg_bytes", "duration_ms", "source")}
+                               if traffic else None),
             "launches": hs["launches"], "avg_launch_us": 1e3 * hs["ms"] / max(1, hs["launches"]),
             "share_of_timed_kernels": hs["ms"] / total_ms if total_ms else None,
             "per_kernel": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
