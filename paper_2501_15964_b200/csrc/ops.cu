@@ -603,17 +603,19 @@ __global__ void k_mult_inf(const double* __restrict__ X, double* __restrict__ Z,
 // deterministic block partials differs).
 constexpr int kMultSmemMaxD = 1024, kMultWarps = 4;
 // Ring depth of the TMA edge kernels (edges in flight per warp).  One stage
-// by default: at d = 784 eight warps per SM already keep ~150 KB in flight,
-// and deeper rings measured slower for short rows (C5, d = 64: phi 14.3 vs
-// 6.4 ms, multiplier 23.5 vs 11.6 ms at 8 stages).  CPB_EDGE_STAGES overrides.
+// for long rows: at d = 784 eight warps per SM already keep ~150 KB in
+// flight, and two stages halve the warps per SM (C3 phi 230 -> 511 ms,
+// multiplier 187 -> 294 ms per 10 gammas).  Two stages for short rows (C5,
+// d = 64: phi 242 -> 230 ms, multiplier 201 -> 197 ms); eight were much
+// slower (phi 14.3 vs 6.4 ms per launch).  CPB_EDGE_STAGES overrides.
 constexpr int kEdgeMaxStages = 8;
 inline int edge_stages(int64_t d, int rows) {
-  (void)d, (void)rows;
+  (void)rows;
   static const int env = [] {
     const char* e = std::getenv("CPB_EDGE_STAGES");
     return e ? std::atoi(e) : 0;
   }();
-  return env > 0 ? std::min(env, kEdgeMaxStages) : 1;
+  return env > 0 ? std::min(env, kEdgeMaxStages) : (d <= 128 ? 2 : 1);
 }
 template <int Q>
 __global__ void __launch_bounds__(32 * kMultWarps) k_mult_s(
