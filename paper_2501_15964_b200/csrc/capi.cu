@@ -195,7 +195,7 @@ int cp_host_alloc(uint64_t bytes, void** out) {
   return guard(nullptr, [&] {
     need(out, "out");
     *out = nullptr;
-    CPB_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable));
+    CPB_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable | cudaHostAllocMapped));
   });
 }
 void cp_host_free(void* p) {

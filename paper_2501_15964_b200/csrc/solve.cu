@@ -1,7 +1,9 @@
 // Solver drivers and the path engine (see solve.cuh).
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <limits>
+#include <string>
 
 #include <cub/cub.cuh>
 
@@ -190,6 +192,24 @@ cp_termination ssnal(Prob& P, const cp_solver_config& cfg, bool warm, double* Xo
   cp_termination t = finish(best.s, done, false, since(t0));
   t.newton = cnt.newton, t.cg = cnt.cg, t.armijo = cnt.armijo, t.hess_apply = cnt.hess_apply;
   return t;
+}
+
+// Device -> host copy by the SMs through mapped pinned memory.  The path's
+// per-gamma snapshots (4.4 GB at C3) used to go through the D2H copy engine,
+// whose FIFO then held every small state read of the next solve (PCG state,
+// gap partials, labels) behind the big copy, so the solve and the copies
+// serialised (C3: 2.24 s solve + 1.63 s copies).  A few CTAs on the copy
+// stream stream the snapshot over the host link instead, leaving the copy
+// engine to the solver's reads.
+__global__ void __launch_bounds__(256) k_to_host(const double* __restrict__ src, double* dst, int64_t n) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    const double a = __ldcs(src + i), b = __ldcs(src + i + stride), c = __ldcs(src + i + 2 * stride),
+                 d = __ldcs(src + i + 3 * stride);
+    dst[i] = a, dst[i + stride] = b, dst[i + 2 * stride] = c, dst[i + 3 * stride] = d;
+  }
+  for (; i < n; i += stride) dst[i] = __ldcs(src + i);
 }
 
 // ---- fast AMA (ama.cpp:17-89) ---------------------------------------------------------
@@ -451,6 +471,30 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
   };
   const bool async_out = (X_out || Z_out) && pinned(X_out) && pinned(Z_out) && c.copy_stream() != nullptr;
   cudaStream_t cs = async_out ? c.copy_stream() : nullptr;
+  // device views of mapped pinned outputs (cp_host_alloc maps them): the SMs ship the snapshots
+  auto mapped = [&](double* h) -> double* {
+    if (!h || !async_out) return nullptr;
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, h, 0) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return static_cast<double*>(dp);
+  };
+  static const int d2h_mode = [] {  // CPB_D2H=engine keeps cudaMemcpyAsync on the copy engine
+    const char* e = std::getenv("CPB_D2H");
+    return e && std::string(e) == "engine" ? 0 : 1;
+  }();
+  double* mX = d2h_mode ? mapped(X_out) : nullptr;
+  double* mZ = d2h_mode ? mapped(Z_out) : nullptr;
+  // CTAs of the copy kernel: enough to fill the ~57 GB/s link, few enough to
+  // leave the SMs to the solver (C3 e2e: 2 -> 4.53 s, 4 -> 3.24, 6 -> 3.26,
+  // 8 -> 3.28, 16 -> 3.48, 32 -> 3.69; copy engine 3.88 s)
+  static const int d2h_ctas = [] {
+    const char* e = std::getenv("CPB_D2H_CTAS");
+    const int v = e ? std::atoi(e) : 6;
+    return v < 1 ? 1 : v;
+  }();
   double* snapX[2] = {nullptr, nullptr};
   double* snapZ[2] = {nullptr, nullptr};
   cudaEvent_t snap_ready[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};
@@ -491,9 +535,16 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
       if (Z_out && me) copy_dev(c, snapZ[s], Z, me);
       CPB_CUDA(cudaEventRecord(snap_ready[s], c.s));
       CPB_CUDA(cudaStreamWaitEvent(cs, snap_ready[s], 0));
-      if (X_out) CPB_CUDA(cudaMemcpyAsync(X_out + t * m, snapX[s], m * sizeof(double), cudaMemcpyDeviceToHost, cs));
-      if (Z_out && me)
-        CPB_CUDA(cudaMemcpyAsync(Z_out + t * me, snapZ[s], me * sizeof(double), cudaMemcpyDeviceToHost, cs));
+      auto ship = [&](double* host, double* mapped, const double* snap, int64_t cnt) {
+        if (mapped) {
+          k_to_host<<<d2h_ctas, 256, 0, cs>>>(snap, mapped, cnt);
+          CPB_LAUNCH_CHECK();
+        } else {
+          CPB_CUDA(cudaMemcpyAsync(host, snap, cnt * sizeof(double), cudaMemcpyDeviceToHost, cs));
+        }
+      };
+      if (X_out) ship(X_out + t * m, mX ? mX + t * m : nullptr, snapX[s], m);
+      if (Z_out && me) ship(Z_out + t * me, mZ ? mZ + t * me : nullptr, snapZ[s], me);
       CPB_CUDA(cudaEventRecord(copy_done[s], cs));
     } else {
       if (X_out) d2h(c, X_out + t * m, X, m * sizeof(double));
