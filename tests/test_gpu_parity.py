@@ -408,11 +408,12 @@ def test_solver_parity_with_oracle(cp, orc, algo, q):
         assert np.array_equal(cp.extract_clusters(sol.X, g).labels, orc.extract_clusters(osol.X, og)[0])
 
 
-@pytest.mark.parametrize("d", [34, 64, 256, 784, 1000])
+@pytest.mark.parametrize("d", [2, 33, 34, 64, 100, 130, 192, 194, 256, 784, 1000])
 def test_hessian_tma_path_matches_oracle(cp, orc, d):
     """Even d >= 256 takes the TMA-staged single-pass Hessian (hess_tma.cu),
-    including hub nodes split into segments (k = 30 makes degrees > 64); d = 34
-    and 64 the two-pass warp-chunk path."""
+    including hub nodes split into segments (k = 30 makes degrees > 64); even
+    d <= 192 the single-pass warp Hessian (k_hess_warp, 1/2/3 double2 pairs per
+    lane: d = 2..64 / 100 / 130..192); odd d and 194 the two-pass path."""
     A = mixture(orc, 40, d, m=3, seed=5)
     for k in (6, 30):
         g, og = check_graph(cp, orc, A, k, 0.5)
