@@ -464,6 +464,23 @@ def test_iteration_cap(cp):
     assert not sol.termination.converged and sol.termination.iterations == 3 and sol.termination.gap > 0
 
 
+@pytest.mark.parametrize("d", [16, 300])
+def test_ssnal_best_iterate_when_capped(cp, orc, d):
+    """A capped, non-converged SSNAL solve returns the best-gap iterate
+    (solver_util.hpp:70-100): X and Z equal the oracle's."""
+    A = mixture(orc, 25, d, m=3, seed=6)
+    g, og = check_graph(cp, orc, A, 6, 0.5)
+    inst = cp.ProblemInstance(cp.DataMatrix(A), g, 0.3)
+    for cap in (1, 2, 3):
+        sol = cp.solve(inst, cp.SolverConfig(epsilon=1e-14, max_iter=cap))
+        osol = orc.solve(A, og, 0.3, 2, orc.config("ssnal", epsilon=1e-14, max_iter=cap))
+        assert not sol.termination.converged and not osol.term["converged"]
+        assert sol.termination.iterations == osol.term["iterations"] == cap
+        assert np.linalg.norm(sol.X - osol.X) <= 1e-10 * np.linalg.norm(osol.X)
+        assert np.linalg.norm(sol.Z - osol.Z) <= 1e-10 * max(np.linalg.norm(osol.Z), 1e-300)
+        assert sol.termination.gap == pytest.approx(osol.term["gap"], rel=1e-8)
+
+
 # ---- path (test_path.cpp) ------------------------------------------------------------------
 
 def test_schedule_and_clusters(cp):
