@@ -951,7 +951,8 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_phi_edge_t(
 // ---- fast AMA (ama.cpp:57-72) -----------------------------------------------------------
 __global__ void k_ama_edge(const double* __restrict__ Xh, double* __restrict__ Zh, double* __restrict__ Zp,
                            const double* __restrict__ rad, const int* __restrict__ ei, const int* __restrict__ ej,
-                           int64_t E, int d, double step, double mom, int q) {
+                           int64_t E, int d, double step, double mom, int q, const double* __restrict__ momp) {
+  if (momp) mom = *momp;  // graph-launched blocks read the momentum the block's k_ama_mom wrote
   const unsigned gm = group_mask();
   ROWS_BEGIN(E) {
     const double* xa = Xh + static_cast<int64_t>(ei[row_]) * d;
@@ -1190,6 +1191,19 @@ PcgOut pcg_newton(const Prob& P, const double* V, const double* jal, const doubl
 
 // Sum (and max) the columns of a (rows x cols) block-partial table on the host,
 // in block order: deterministic and cheap (rows <= 8 x SM count).
+// Column sums (or maxima for max_cols) of a host copy of a rows x cols block-partial table.
+std::vector<double> reduce_cols(const double* all, int rows, int cols, const std::vector<int>& max_cols = {}) {
+  std::vector<double> out(cols, 0.0);
+  for (int k : max_cols) out[k] = -1e300;
+  for (int b = 0; b < rows; ++b)
+    for (int k = 0; k < cols; ++k) {
+      const double x = all[static_cast<size_t>(b) * cols + k];
+      bool is_max = false;
+      for (int mk : max_cols) is_max |= (mk == k);
+      out[k] = is_max ? std::max(out[k], x) : out[k] + x;
+    }
+  return out;
+}
 std::vector<double> host_cols(Ctx& c, const double* part, int rows, int cols, const std::vector<int>& max_cols = {}) {
   std::vector<double> all(static_cast<size_t>(rows) * cols), out(cols, 0.0);
   d2h(c, all.data(), part, all.size() * sizeof(double));
@@ -1207,31 +1221,36 @@ std::vector<double> host_cols(Ctx& c, const double* part, int rows, int cols, co
 GapOut eval_gap(const Prob& P, const double* X, const double* Z) {
   Ctx& c = *P.c;
   const int64_t d = P.d(), n = P.n(), E = P.E();
-  double* pn = part_buf(c, "gap.pn", 4 * static_cast<size_t>(c.sm_count) * 16);
+  // node partials [nbn x 4] and edge partials [grid x 5] share one buffer: both kernels are
+  // enqueued first and one D2H brings both tables back (one host round trip per gap check)
+  EdgeSel sel{nullptr, 0, E};
+  if (E > 0 && partitioned(c)) {
+    const EdgePart& ep = edge_part(c, *P.g);
+    sel = EdgeSel{nullptr, ep.e0, ep.e1 - ep.e0};
+  }
+  GroupGeom ge = group_geom(c, sel.count, d);
+  const size_t node_cap = 4 * static_cast<size_t>(c.sm_count) * 16;  // gather_gap: <= 8 * SMs blocks x 4
+  double* pn = part_buf(c, "gap.pp", node_cap + 5 * static_cast<size_t>(ge.grid));
   int nbn;
   {
     Ctx::Timer tm(&c, "gap_node", (2.0 * E * d + 3.0 * n * d) * 8.0);
     nbn = gather_gap(c, *P.g, X, P.A->A.p, Z, d, pn);
   }
-  std::vector<double> h = host_cols(c, pn, nbn, 4);
+  double* pe = pn + 4 * static_cast<size_t>(nbn);
+  if (E > 0) {
+    Ctx::Timer tm(&c, "gap_edge", (E * d + n * d) * 8.0);
+    k_gap_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, sel,
+                                                        static_cast<int>(d), P.q, pe);
+    CPB_LAUNCH_CHECK();
+  }
+  std::vector<double> all(4 * static_cast<size_t>(nbn) + (E > 0 ? 5 * static_cast<size_t>(ge.grid) : 0));
+  d2h(c, all.data(), pn, all.size() * sizeof(double));
+  std::vector<double> h = reduce_cols(all.data(), nbn, 4);
   if (partitioned(c)) comm_allreduce_host(c, h);
   std::vector<double> e(5, 0.0);
   e[4] = -1.0;
   if (E > 0) {
-    EdgeSel sel{nullptr, 0, E};
-    if (partitioned(c)) {
-      const EdgePart& ep = edge_part(c, *P.g);
-      sel = EdgeSel{nullptr, ep.e0, ep.e1 - ep.e0};
-    }
-    GroupGeom ge = group_geom(c, sel.count, d);
-    double* pe = part_buf(c, "gap.pe", 5 * static_cast<size_t>(ge.grid));
-    {
-      Ctx::Timer tm(&c, "gap_edge", (E * d + n * d) * 8.0);
-      k_gap_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, sel,
-                                                          static_cast<int>(d), P.q, pe);
-      CPB_LAUNCH_CHECK();
-    }
-    e = host_cols(c, pe, ge.grid, 5, {4});
+    e = reduce_cols(all.data() + 4 * static_cast<size_t>(nbn), ge.grid, 5, {4});
     if (partitioned(c)) comm_allreduce_host(c, e, {4});
   }
   if (e[4] > 0.0) invalid("dual_objective: Z violates the dual-ball constraint");
@@ -1421,12 +1440,35 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
 void ama_primal(const Prob& P, const double* Zh, double* Xh) {
   gather_a_minus_bt(*P.c, *P.g, P.A->A.p, Zh, P.d(), Xh);
 }
-void ama_dual_step(const Prob& P, const double* Xh, double* Zh, double* Zprev, double step, double mom) {
+void ama_dual_step(const Prob& P, const double* Xh, double* Zh, double* Zprev, double step, double mom,
+                   const double* momp) {
   Ctx& c = *P.c;
   const int64_t d = P.d(), E = P.E();
   GroupGeom ge = group_geom(c, E, d);
   k_ama_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(Xh, Zh, Zprev, P.rad, P.g->ei.p, P.g->ej.p, E,
-                                                      static_cast<int>(d), step, mom, P.q);
+                                                      static_cast<int>(d), step, mom, P.q, momp);
+  CPB_LAUNCH_CHECK();
+}
+
+// Nesterov momenta of `cnt` consecutive AMA iterations (ama.cpp:66-70): t' = (1 + sqrt(1 + 4t^2)) / 2,
+// mom = (t - 1) / t'.  tm[cnt] carries t across blocks.  Same operation order as the host loop and
+// -fmad=false, so the values are bitwise the host's.
+__global__ void k_ama_mom(double* tm, int cnt) {
+  double t = tm[cnt];
+  for (int j = 0; j < cnt; ++j) {
+    const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+    tm[j] = (t - 1.0) / tn;
+    t = tn;
+  }
+  tm[cnt] = t;
+}
+__global__ void k_set1(double* p, double v) { *p = v; }
+void ama_momenta(const Prob& P, double* tm, int cnt) {
+  k_ama_mom<<<1, 1, 0, P.c->s>>>(tm, cnt);
+  CPB_LAUNCH_CHECK();
+}
+void ama_set_t(const Prob& P, double* tm, int cnt, double t) {
+  k_set1<<<1, 1, 0, P.c->s>>>(tm + cnt, t);
   CPB_LAUNCH_CHECK();
 }
 

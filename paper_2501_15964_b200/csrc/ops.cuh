@@ -109,7 +109,10 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
 // Xh = A - Zhat B^T
 void ama_primal(const Prob& P, const double* Zh, double* Xh);
 // Znew = Pi(Zhat + step Xh B); Zhat = Znew + mom (Znew - Zprev); Zprev = Znew
-void ama_dual_step(const Prob& P, const double* Xh, double* Zh, double* Zprev, double step, double mom);
+void ama_dual_step(const Prob& P, const double* Xh, double* Zh, double* Zprev, double step, double mom,
+                   const double* momp = nullptr);
+void ama_momenta(const Prob& P, double* tm, int cnt);             // tm[0..cnt) = momenta, tm[cnt] = t
+void ama_set_t(const Prob& P, double* tm, int cnt, double t);
 
 // The `active` flag of a PCG state (nullptr when none): operators no-op on it.
 const int* cg_active_ptr(const void* cg_state);

@@ -213,6 +213,42 @@ __global__ void __launch_bounds__(256) k_to_host(const double* __restrict__ src,
 }
 
 // ---- fast AMA (ama.cpp:17-89) ---------------------------------------------------------
+// One captured CUDA graph (instantiated once, relaunched); counts its kernels into g_launches
+// per launch so gpu_launches stays the number of kernels that ran.
+struct GraphExec {
+  cudaGraphExec_t exec = nullptr;
+  unsigned long long kernels = 0;
+  template <class F>
+  void capture(cudaStream_t s, F&& body) {
+    cudaGraph_t g = nullptr;
+    const unsigned long long l0 = g_launches;
+    CPB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try {
+      body();
+    } catch (...) {
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    CPB_CUDA(cudaStreamEndCapture(s, &g));
+    kernels = g_launches - l0;
+    g_launches = l0;
+    const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    CPB_CUDA(e);
+  }
+  void launch(cudaStream_t s) {
+    CPB_CUDA(cudaGraphLaunch(exec, s));
+    g_launches += kernels;
+  }
+  GraphExec() = default;
+  GraphExec(const GraphExec&) = delete;
+  GraphExec& operator=(const GraphExec&) = delete;
+  ~GraphExec() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
 cp_termination fast_ama(Prob& P, const cp_solver_config& cfg, bool warm, double* Xout, double* Zout,
                         SolveCache& cache) {
   Ctx& c = *P.c;
@@ -244,7 +280,37 @@ cp_termination fast_ama(Prob& P, const cp_solver_config& cfg, bool warm, double*
   Best best;
   const int64_t max_iter = resolved_max_iter(cfg);
   int64_t k = 0;
+  // From k = 10 on, the 10 iterations between two gap checks are one CUDA graph launch
+  // (k_ama_mom + 10 x (B^T gather, edge step)): same kernels, same arguments, the momenta
+  // computed on the device bitwise like the host's.  C1-sized paths are launch-bound.
+  constexpr int kBlk = 10;
+  double* tm = c.buf<double>("a.tm", kBlk + 1);
+  GraphExec blk;
   while (k < max_iter) {
+    if (k >= kBlk && k % kBlk == 0 && k + kBlk <= max_iter) {
+      if (!blk.exec) {
+        ama_set_t(P, tm, kBlk, t);
+        blk.capture(c.s, [&] {
+          ama_momenta(P, tm, kBlk);
+          for (int j = 0; j < kBlk; ++j) {
+            ama_primal(P, Zh, Xh);
+            ama_dual_step(P, Xh, Zh, Zp, step, 0.0, tm + j);
+          }
+        });
+      }
+      blk.launch(c.s);
+      for (int j = 0; j < kBlk; ++j) t = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));  // host copy of t
+      k += kBlk;
+      ama_primal(P, Zp, Xout);  // X = A - Znew B^T (recover_primal)
+      GapOut s = eval_gap(P, Xout, Zp);
+      if (accepts(s, cfg)) {
+        copy_dev(c, Zout, Zp, me);
+        return finish(s, k, true, since(t0));
+      }
+      best.offer(c, s, Xout, Zp, Xb, Zb, m, me);
+      if (cfg.time_limit > 0.0 && since(t0) > cfg.time_limit) break;
+      continue;
+    }
     ++k;
     ama_primal(P, Zh, Xh);
     const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));

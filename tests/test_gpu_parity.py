@@ -522,6 +522,25 @@ def test_path_parity(cp, orc, algo):
         assert res.assignments[t].K == ores["K"][t]
 
 
+@pytest.mark.parametrize("q", [2, 1, 0])
+def test_ama_graph_blocks_match_oracle(cp, orc, q):
+    """Fast AMA runs its 10-iteration blocks between gap checks as one CUDA graph with the
+    Nesterov momenta computed on the device: long solves (hundreds of blocks) must keep the
+    oracle's iteration counts and X to near round-off."""
+    A = circle(orc, 30)
+    g, og = check_graph(cp, orc, A, 10, 0.5)
+    sched = cp.make_schedule(0.01, 10.0, 6)
+    cfg = cp.SolverConfig(algorithm=cp.Algorithm.FastAMA)
+    res = cp.run_path(cp.DataMatrix(A), g, q, sched, cfg)
+    ores = orc.run_path(A, og, q, sched.values, orc.config("ama"))
+    assert sum(res.stats[t].iterations for t in range(len(sched.values))) > 200
+    for t in range(len(sched.values)):
+        assert res.stats[t].iterations == ores["terms"][t]["iterations"]
+        assert res.stats[t].converged == bool(ores["terms"][t]["converged"])
+        assert np.linalg.norm(res.solutions[t].X - ores["X"][t]) <= 1e-10 * np.linalg.norm(ores["X"][t])
+        assert np.array_equal(res.assignments[t].labels, ores["labels"][t])
+
+
 @pytest.mark.parametrize("d", [64, 96])
 def test_edge_ring_wraps_match_oracle(cp, orc, d):
     """Short rows run the TMA edge kernels with an 8-deep per-warp ring; with
