@@ -18,6 +18,8 @@
 #include "ptx.cuh"
 #include "comm.cuh"
 #include "linf.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace cpb {
 
@@ -949,46 +951,150 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_phi_edge_t(
 }
 
 // ---- fast AMA (ama.cpp:57-72) -----------------------------------------------------------
+// One edge row of the dual step: z~ = Zh_l + step (x_i - x_j), Z+ = proj_{dual ball}(z~),
+// Zh_l = Z+ + mom (Z+ - Zp_l), Zp_l = Z+.  Loads bypass L1 (__ldcg): the fused block kernel
+// below reads rows other SMs wrote before its grid barrier.
+__device__ __forceinline__ void ama_edge_row(int64_t row, const double* __restrict__ Xh, double* __restrict__ Zh,
+                                             double* __restrict__ Zp, int ia, int ib, double rl, int d, double step,
+                                             double mom, int q, unsigned gm) {
+  const double* xa = Xh + static_cast<int64_t>(ia) * d;
+  const double* xb = Xh + static_cast<int64_t>(ib) * d;
+  double* zh = Zh + row * d;
+  double* zp = Zp + row * d;
+  if (q == Q_LINF) {
+    int cnt;
+    const double th =
+        linf_theta([&](int f) { return __ldcg(zh + f) + step * (__ldcg(xa + f) - __ldcg(xb + f)); }, d, rl, gm, &cnt);
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double zn = __ldcg(zh + f) + step * (__ldcg(xa + f) - __ldcg(xb + f));
+      const double zpr = th < 0.0 ? zn : soft(zn, th);
+      const double old = __ldcg(zp + f);
+      zh[f] = zpr + mom * (zpr - old);
+      zp[f] = zpr;
+    }
+    return;
+  }
+  double nn = 0.0;
+  if (q == Q_L2) {
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double zn = __ldcg(zh + f) + step * (__ldcg(xa + f) - __ldcg(xb + f));
+      nn += zn * zn;
+    }
+  }
+  const double nz = sqrt(group_sum(nn, gm));
+  const double sc = rl / nz;
+  for (int f = threadIdx.x; f < d; f += blockDim.x) {
+    const double zn = __ldcg(zh + f) + step * (__ldcg(xa + f) - __ldcg(xb + f));
+    const double zpr = (q == Q_L2) ? ((nz <= rl) ? zn : sc * zn) : fmax(fmin(zn, rl), -rl);
+    const double old = __ldcg(zp + f);
+    zh[f] = zpr + mom * (zpr - old);
+    zp[f] = zpr;
+  }
+}
+
 __global__ void k_ama_edge(const double* __restrict__ Xh, double* __restrict__ Zh, double* __restrict__ Zp,
                            const double* __restrict__ rad, const int* __restrict__ ei, const int* __restrict__ ej,
                            int64_t E, int d, double step, double mom, int q, const double* __restrict__ momp) {
   if (momp) mom = *momp;  // graph-launched blocks read the momentum the block's k_ama_mom wrote
   const unsigned gm = group_mask();
-  ROWS_BEGIN(E) {
-    const double* xa = Xh + static_cast<int64_t>(ei[row_]) * d;
-    const double* xb = Xh + static_cast<int64_t>(ej[row_]) * d;
-    double* zh = Zh + row_ * d;
-    double* zp = Zp + row_ * d;
-    const double rl = rad[row_];
-    if (q == Q_LINF) {
-      int cnt;
-      const double th = linf_theta([&](int f) { return zh[f] + step * (xa[f] - xb[f]); }, d, rl, gm, &cnt);
-      for (int f = threadIdx.x; f < d; f += blockDim.x) {
-        const double zn = zh[f] + step * (xa[f] - xb[f]);
-        const double zpr = th < 0.0 ? zn : soft(zn, th);
-        const double old = zp[f];
-        zh[f] = zpr + mom * (zpr - old);
-        zp[f] = zpr;
-      }
-      continue;
-    }
-    double nn = 0.0;
-    if (q == Q_L2) {
-      for (int f = threadIdx.x; f < d; f += blockDim.x) {
-        const double zn = zh[f] + step * (xa[f] - xb[f]);
-        nn += zn * zn;
-      }
-    }
-    const double nz = sqrt(group_sum(nn, gm));
-    const double sc = rl / nz;
-    for (int f = threadIdx.x; f < d; f += blockDim.x) {
-      const double zn = zh[f] + step * (xa[f] - xb[f]);
-      const double zpr = (q == Q_L2) ? ((nz <= rl) ? zn : sc * zn) : fmax(fmin(zn, rl), -rl);
-      const double old = zp[f];
-      zh[f] = zpr + mom * (zpr - old);
-      zp[f] = zpr;
+  ROWS_BEGIN(E) { ama_edge_row(row_, Xh, Zh, Zp, ei[row_], ej[row_], rad[row_], d, step, mom, q, gm); }
+}
+
+// Fused block of `cnt` AMA iterations for small problems (d <= 32), one cooperative launch:
+// per iteration X^ = A - Z^ B^T (node-CSR gather, incident edges in ascending id: k_g_bt mode
+// 1's exact order), grid barrier, the edge step with the iteration's Nesterov momentum
+// (computed per thread from tm[cnt] exactly like the host loop), grid barrier; finally
+// X = A - Z B^T of the new iterate (recover_primal).  Bitwise the same as the per-kernel loop;
+// replaces 2 cnt + 1 launches by one (C1: n = 1000, d = 2, launch-bound).
+__global__ void __launch_bounds__(256) k_ama_block(const double* __restrict__ A, double* Xh, double* Zh, double* Zp,
+                                                   double* Xout, const double* __restrict__ rad,
+                                                   const int* __restrict__ ei, const int* __restrict__ ej,
+                                                   const int* __restrict__ off, const int* __restrict__ adj_e,
+                                                   const int* __restrict__ adj_o, const int* __restrict__ order,
+                                                   int64_t n, int64_t E, int d, double step, int q, double* tm,
+                                                   int cnt) {
+  cg::grid_group grid = cg::this_grid();
+  const unsigned gm = group_mask();
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const int lane = tid & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * 256 + tid) >> 5, nw = static_cast<int64_t>(gridDim.x) * 8;
+  double t = __ldcg(tm + cnt);
+  // When every warp owns at most one node and every group at most one edge for the whole
+  // kernel (C1), the node's incident edge ids / sides and the edge's endpoints stay in
+  // registers, so an iteration's loads are all independent (one L2 latency per phase).
+  const bool one_node = nw >= n;
+  const int64_t row0 = blockIdx.x * static_cast<int64_t>(blockDim.y) + threadIdx.y;
+  const bool one_row = static_cast<int64_t>(gridDim.x) * blockDim.y >= E;
+  int my_v = -1, my_deg = 0, my_e = 0, my_o = 0;
+  if (one_node && w0 < n) {
+    my_v = order[w0];
+    const int p0 = off[my_v];
+    my_deg = off[my_v + 1] - p0;
+    if (my_deg <= 32 && lane < my_deg) {
+      my_e = adj_e[p0 + lane];
+      my_o = adj_o[p0 + lane];
     }
   }
+  int r_a = 0, r_b = 0;
+  double r_l = 0.0;
+  if (one_row && row0 < E) {
+    r_a = ei[row0];
+    r_b = ej[row0];
+    r_l = rad[row0];
+  }
+  for (int j = 0;; ++j) {
+    const bool last = j == cnt;
+    const double* Zs = last ? Zp : Zh;
+    double* Xd = last ? Xout : Xh;
+    if (one_node && my_deg <= 32) {
+      if (my_v >= 0) {  // warp-uniform
+        double acc = 0.0;
+        for (int u0 = 0; u0 < my_deg; u0 += 8) {
+          double x[8];
+          bool pl[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = __shfl_sync(0xffffffffu, my_e, (u0 + u) & 31);
+            pl[u] = __shfl_sync(0xffffffffu, my_o, (u0 + u) & 31) > my_v;
+            x[u] = (u0 + u < my_deg && lane < d) ? __ldcg(Zs + static_cast<int64_t>(e) * d + lane) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (u0 + u < my_deg) acc = pl[u] ? acc + x[u] : acc - x[u];
+        }
+        if (lane < d) {
+          const int64_t i = static_cast<int64_t>(my_v) * d + lane;
+          Xd[i] = A[i] - acc;
+        }
+      }
+    } else
+    for (int64_t it = w0; it < n; it += nw) {
+      const int v = order[it];
+      if (lane < d) {
+        const int p0 = off[v], p1 = off[v + 1];
+        double acc = 0.0;
+        for (int p = p0; p < p1; ++p) {
+          const double x = __ldcg(Zs + static_cast<int64_t>(adj_e[p]) * d + lane);
+          acc = adj_o[p] > v ? acc + x : acc - x;
+        }
+        const int64_t i = static_cast<int64_t>(v) * d + lane;
+        Xd[i] = A[i] - acc;
+      }
+    }
+    if (last) break;
+    grid.sync();
+    const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+    const double mom = (t - 1.0) / tn;
+    t = tn;
+    if (one_row) {
+      if (row0 < E) ama_edge_row(row0, Xh, Zh, Zp, r_a, r_b, r_l, d, step, mom, q, gm);
+    } else {
+      for (int64_t row = row0; row < E; row += static_cast<int64_t>(gridDim.x) * blockDim.y)
+        ama_edge_row(row, Xh, Zh, Zp, ei[row], ej[row], rad[row], d, step, mom, q, gm);
+    }
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && tid == 0) tm[cnt] = t;
 }
 
 // ---- host helpers ----------------------------------------------------------------------------
@@ -1466,6 +1572,33 @@ __global__ void k_set1(double* p, double v) { *p = v; }
 void ama_momenta(const Prob& P, double* tm, int cnt) {
   k_ama_mom<<<1, 1, 0, P.c->s>>>(tm, cnt);
   CPB_LAUNCH_CHECK();
+}
+bool ama_block_fused(const Prob& P, double* Xh, double* Zh, double* Zp, double* Xout, double step,
+                     double* tm, int cnt) {
+  Ctx& c = *P.c;
+  const int64_t d = P.d(), n = P.n(), E = P.E();
+  static const bool enabled = [] {
+    const char* e = std::getenv("CPB_AMA_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  if (!enabled || d > 32 || E > (1 << 18) || n > (1 << 17) || partitioned(c)) return false;
+  GroupGeom ge = group_geom(c, E, d);
+  static int occ = -1;
+  if (occ < 0) CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ama_block, 256, 0));
+  if (occ < 1) return false;
+  const int64_t want = std::max<int64_t>(cdiv(n, 8), cdiv(E, ge.gy));
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(c.sm_count))));
+  const double* A = P.A->A.p;
+  const int *ei = P.g->ei.p, *ej = P.g->ej.p, *off = P.g->off.p, *ae = P.g->adj_e.p, *ao = P.g->adj_o.p,
+            *ord = P.g->order.p;
+  const double* rad = P.rad;
+  int dd = static_cast<int>(d), qq = P.q;
+  void* args[] = {(void*)&A,   (void*)&Xh,  (void*)&Zh, (void*)&Zp, (void*)&Xout, (void*)&rad, (void*)&ei,
+                  (void*)&ej,  (void*)&off, (void*)&ae, (void*)&ao, (void*)&ord,  (void*)&n,   (void*)&E,
+                  (void*)&dd,  (void*)&step, (void*)&qq, (void*)&tm, (void*)&cnt};
+  CPB_CUDA(cudaLaunchCooperativeKernel((const void*)k_ama_block, dim3(grid), dim3(ge.gx, ge.gy), args, 0, c.s));
+  CPB_LAUNCH_CHECK();
+  return true;
 }
 void ama_set_t(const Prob& P, double* tm, int cnt, double t) {
   k_set1<<<1, 1, 0, P.c->s>>>(tm + cnt, t);

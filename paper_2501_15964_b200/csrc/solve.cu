@@ -286,22 +286,28 @@ cp_termination fast_ama(Prob& P, const cp_solver_config& cfg, bool warm, double*
   constexpr int kBlk = 10;
   double* tm = c.buf<double>("a.tm", kBlk + 1);
   GraphExec blk;
+  bool t_on_device = false;
   while (k < max_iter) {
     if (k >= kBlk && k % kBlk == 0 && k + kBlk <= max_iter) {
-      if (!blk.exec) {
+      if (!t_on_device) {
         ama_set_t(P, tm, kBlk, t);
-        blk.capture(c.s, [&] {
-          ama_momenta(P, tm, kBlk);
-          for (int j = 0; j < kBlk; ++j) {
-            ama_primal(P, Zh, Xh);
-            ama_dual_step(P, Xh, Zh, Zp, step, 0.0, tm + j);
-          }
-        });
+        t_on_device = true;
       }
-      blk.launch(c.s);
+      // small problems: the whole block + recover_primal is one cooperative kernel
+      if (!ama_block_fused(P, Xh, Zh, Zp, Xout, step, tm, kBlk)) {
+        if (!blk.exec)
+          blk.capture(c.s, [&] {
+            ama_momenta(P, tm, kBlk);
+            for (int j = 0; j < kBlk; ++j) {
+              ama_primal(P, Zh, Xh);
+              ama_dual_step(P, Xh, Zh, Zp, step, 0.0, tm + j);
+            }
+          });
+        blk.launch(c.s);
+        ama_primal(P, Zp, Xout);  // X = A - Znew B^T (recover_primal)
+      }
       for (int j = 0; j < kBlk; ++j) t = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));  // host copy of t
       k += kBlk;
-      ama_primal(P, Zp, Xout);  // X = A - Znew B^T (recover_primal)
       GapOut s = eval_gap(P, Xout, Zp);
       if (accepts(s, cfg)) {
         copy_dev(c, Zout, Zp, me);
