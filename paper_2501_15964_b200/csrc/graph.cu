@@ -405,50 +405,84 @@ __global__ void k_cc_label(const int* __restrict__ L, const int* __restrict__ ra
 }
 
 // ---- Laplacian power iteration -------------------------------------------------------------
-// y_v = sum over column order of L's column-major CSC (SparseDenseProduct.h):
-// neighbours ascending with the degree term at position v.
-__device__ __forceinline__ void lap_apply(const int* __restrict__ off, const int* __restrict__ adj_o,
-                                          const double* __restrict__ x, double* __restrict__ y, int n) {
-  for (int v = threadIdx.x; v < n; v += blockDim.x) {
-    const int p0 = off[v], p1 = off[v + 1];
-    const double deg = static_cast<double>(p1 - p0);
-    double acc = 0.0;
-    bool diag_done = (p1 == p0);
-    for (int p = p0; p < p1; ++p) {
-      const int u = adj_o[p];
-      if (!diag_done && u > v) {
-        acc = __dadd_rn(acc, __dmul_rn(deg, x[v]));
-        diag_done = true;
-      }
-      acc = __dsub_rn(acc, x[u]);
-    }
-    if (!diag_done) acc = __dadd_rn(acc, __dmul_rn(deg, x[v]));
-    y[v] = acc;
-  }
-}
+// w = L v in the column order of L's column-major CSC (SparseDenseProduct.h): neighbours
+// ascending with the degree term at position v (fused into k_power below).
 __device__ double blk_dot(const double* a, const double* b, int n, double* sh) {
   double s = 0.0;
   for (int v = threadIdx.x; v < n; v += blockDim.x) s = __dadd_rn(s, __dmul_rn(a[v], b[v]));
   return block_sum(s, sh);
 }
+// Two block sums in one barrier round; each value is reduced by exactly block_sum's tree.
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* sh /* 64 */) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = (blockDim.x + 31) >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  __syncthreads();
+  if (lane == 0) {
+    sh[wid] = a;
+    sh[32 + wid] = b;
+  }
+  __syncthreads();
+  double ta = (tid < nw) ? sh[tid] : 0.0, tb = (tid < nw) ? sh[32 + tid] : 0.0;
+  if (wid == 0) {
+    ta = warp_sum(ta);
+    tb = warp_sum(tb);
+  }
+  if (tid == 0) {
+    sh[0] = ta;
+    sh[32] = tb;
+  }
+  __syncthreads();
+  a = sh[0];
+  b = sh[32];
+  __syncthreads();
+}
+// power_iteration (linalg.cpp:194-242) for one probe per block.  Each thread forms w = L v for
+// its nodes and accumulates <w, w> and <v, w> in the same per-thread order as blk_dot, so the
+// fused pass reduces bitwise like the separate dots did.
 __global__ void __launch_bounds__(1024) k_power(const int* __restrict__ off, const int* __restrict__ adj_o,
                                                 const double* __restrict__ start, int n, double tol, long long max_iter,
                                                 double* v, double* w, double* out) {
-  __shared__ double sh[32];
+  // one block per probe (linalg.cpp:206-216 runs them one after another; they are independent)
+  start += static_cast<int64_t>(blockIdx.x) * n;
+  v += static_cast<int64_t>(blockIdx.x) * n;
+  w += static_cast<int64_t>(blockIdx.x) * n;
+  out += 2 * blockIdx.x;
+  __shared__ double sh[64];
   const double ns = sqrt(blk_dot(start, start, n, sh));
   for (int t = threadIdx.x; t < n; t += blockDim.x) v[t] = __ddiv_rn(start[t], ns);
   __syncthreads();
   double prev = 0.0, est = 0.0;
   int dead = 0;
   for (long long it = 1; it <= max_iter; ++it) {
-    lap_apply(off, adj_o, v, w, n);
-    __syncthreads();
-    const double nw = sqrt(blk_dot(w, w, n, sh));
+    double sww = 0.0, svw = 0.0;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      const int p0 = off[t], p1 = off[t + 1];
+      const double deg = static_cast<double>(p1 - p0);
+      const double xv = v[t];
+      double acc = 0.0;
+      bool diag_done = (p1 == p0);
+#pragma unroll 4
+      for (int p = p0; p < p1; ++p) {
+        const int u = adj_o[p];
+        if (!diag_done && u > t) {
+          acc = __dadd_rn(acc, __dmul_rn(deg, xv));
+          diag_done = true;
+        }
+        acc = __dsub_rn(acc, v[u]);
+      }
+      if (!diag_done) acc = __dadd_rn(acc, __dmul_rn(deg, xv));
+      w[t] = acc;
+      sww = __dadd_rn(sww, __dmul_rn(acc, acc));
+      svw = __dadd_rn(svw, __dmul_rn(xv, acc));
+    }
+    block_sum2(sww, svw, sh);
+    const double nw = sqrt(sww);
     if (nw <= 1e-300) {
       dead = 1;
       break;
     }
-    const double lam = blk_dot(v, w, n, sh);
+    const double lam = svw;
     est = lam;
     for (int t = threadIdx.x; t < n; t += blockDim.x) v[t] = __ddiv_rn(w[t], nw);
     __syncthreads();
@@ -926,19 +960,20 @@ double laplacian_lambda_max(Ctx& c, const Graph& g, double tol, int64_t max_iter
   }
   starts[2 * n] = 1.0;
   double* ds = c.buf<double>("pw.start", 3 * n);
-  double* v = c.buf<double>("pw.v", n);
-  double* w = c.buf<double>("pw.w", n);
+  double* v = c.buf<double>("pw.v", 3 * n);
+  double* w = c.buf<double>("pw.w", 3 * n);
   h2d(c, ds, starts.data(), starts.size() * sizeof(double));
+  // the three probes run concurrently, one block each
+  k_power<<<3, 1024, 0, c.s>>>(g.off.p, g.adj_o.p, ds, static_cast<int>(n), tol, max_iter, v, w, c.dscal);
+  CPB_LAUNCH_CHECK();
+  double out[6];
+  c.fetch(0, 6, out);
   double best = 0.0;
   bool any = false;
   for (int s = 0; s < 3; ++s) {
-    k_power<<<1, 1024, 0, c.s>>>(g.off.p, g.adj_o.p, ds + s * n, static_cast<int>(n), tol, max_iter, v, w, c.dscal);
-    CPB_LAUNCH_CHECK();
-    double out[2];
-    c.fetch(0, 2, out);
-    if (out[1] == 0.0) {
+    if (out[2 * s + 1] == 0.0) {
       any = true;
-      best = std::max(best, out[0]);
+      best = std::max(best, out[2 * s]);
     }
   }
   return any ? best : 0.0;
