@@ -1003,7 +1003,7 @@ __global__ void k_ama_edge(const double* __restrict__ Xh, double* __restrict__ Z
 // Fused block of `cnt` AMA iterations for small problems (d <= 32), one cooperative launch:
 // per iteration X^ = A - Z^ B^T (node-CSR gather, incident edges in ascending id: k_g_bt mode
 // 1's exact order), grid barrier, the edge step with the iteration's Nesterov momentum
-// (computed per thread from tm[cnt] exactly like the host loop), grid barrier; finally
+// (computed per thread from t0 exactly like the host loop), grid barrier; finally
 // X = A - Z B^T of the new iterate (recover_primal).  Bitwise the same as the per-kernel loop;
 // replaces 2 cnt + 1 launches by one (C1: n = 1000, d = 2, launch-bound).
 __global__ void __launch_bounds__(256) k_ama_block(const double* __restrict__ A, double* Xh, double* Zh, double* Zp,
@@ -1011,14 +1011,14 @@ __global__ void __launch_bounds__(256) k_ama_block(const double* __restrict__ A,
                                                    const int* __restrict__ ei, const int* __restrict__ ej,
                                                    const int* __restrict__ off, const int* __restrict__ adj_e,
                                                    const int* __restrict__ adj_o, const int* __restrict__ order,
-                                                   int64_t n, int64_t E, int d, double step, int q, double* tm,
+                                                   int64_t n, int64_t E, int d, double step, int q, double t0,
                                                    int cnt) {
   cg::grid_group grid = cg::this_grid();
   const unsigned gm = group_mask();
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const int lane = tid & 31;
   const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * 256 + tid) >> 5, nw = static_cast<int64_t>(gridDim.x) * 8;
-  double t = __ldcg(tm + cnt);
+  double t = t0;
   // When every warp owns at most one node and every group at most one edge for the whole
   // kernel (C1), the node's incident edge ids / sides and the edge's endpoints stay in
   // registers, so an iteration's loads are all independent (one L2 latency per phase).
@@ -1094,7 +1094,6 @@ __global__ void __launch_bounds__(256) k_ama_block(const double* __restrict__ A,
     }
     grid.sync();
   }
-  if (blockIdx.x == 0 && tid == 0) tm[cnt] = t;
 }
 
 // ---- host helpers ----------------------------------------------------------------------------
@@ -1573,8 +1572,8 @@ void ama_momenta(const Prob& P, double* tm, int cnt) {
   k_ama_mom<<<1, 1, 0, P.c->s>>>(tm, cnt);
   CPB_LAUNCH_CHECK();
 }
-bool ama_block_fused(const Prob& P, double* Xh, double* Zh, double* Zp, double* Xout, double step,
-                     double* tm, int cnt) {
+bool ama_block_fused(const Prob& P, double* Xh, double* Zh, double* Zp, double* Xout, double step, double t0,
+                     int cnt) {
   Ctx& c = *P.c;
   const int64_t d = P.d(), n = P.n(), E = P.E();
   static const bool enabled = [] {
@@ -1595,7 +1594,7 @@ bool ama_block_fused(const Prob& P, double* Xh, double* Zh, double* Zp, double* 
   int dd = static_cast<int>(d), qq = P.q;
   void* args[] = {(void*)&A,   (void*)&Xh,  (void*)&Zh, (void*)&Zp, (void*)&Xout, (void*)&rad, (void*)&ei,
                   (void*)&ej,  (void*)&off, (void*)&ae, (void*)&ao, (void*)&ord,  (void*)&n,   (void*)&E,
-                  (void*)&dd,  (void*)&step, (void*)&qq, (void*)&tm, (void*)&cnt};
+                  (void*)&dd,  (void*)&step, (void*)&qq, (void*)&t0, (void*)&cnt};
   CPB_CUDA(cudaLaunchCooperativeKernel((const void*)k_ama_block, dim3(grid), dim3(ge.gx, ge.gy), args, 0, c.s));
   CPB_LAUNCH_CHECK();
   return true;

@@ -115,8 +115,8 @@ void ama_momenta(const Prob& P, double* tm, int cnt);             // tm[0..cnt) 
 void ama_set_t(const Prob& P, double* tm, int cnt, double t);
 // cnt AMA iterations + recover_primal into Xout as one cooperative kernel (small d, E);
 // false = not applicable (caller runs the per-kernel / graph path)
-bool ama_block_fused(const Prob& P, double* Xh, double* Zh, double* Zp, double* Xout, double step,
-                     double* tm, int cnt);
+bool ama_block_fused(const Prob& P, double* Xh, double* Zh, double* Zp, double* Xout, double step, double t0,
+                     int cnt);
 
 // The `active` flag of a PCG state (nullptr when none): operators no-op on it.
 const int* cg_active_ptr(const void* cg_state);

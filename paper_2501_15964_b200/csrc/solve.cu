@@ -280,57 +280,50 @@ cp_termination fast_ama(Prob& P, const cp_solver_config& cfg, bool warm, double*
   Best best;
   const int64_t max_iter = resolved_max_iter(cfg);
   int64_t k = 0;
-  // From k = 10 on, the 10 iterations between two gap checks are one CUDA graph launch
-  // (k_ama_mom + 10 x (B^T gather, edge step)): same kernels, same arguments, the momenta
-  // computed on the device bitwise like the host's.  C1-sized paths are launch-bound.
+  // Between two gap checks: small problems run the block as one cooperative kernel
+  // (k_ama_block); otherwise every full 10-iteration block is one CUDA graph launch
+  // (k_ama_mom + 10 x (B^T gather, edge step)) with the momenta computed on the device bitwise
+  // like the host's, its t seeded once (graph blocks are consecutive).  Time limit checked
+  // per block.
   constexpr int kBlk = 10;
   double* tm = c.buf<double>("a.tm", kBlk + 1);
   GraphExec blk;
-  bool t_on_device = false;
   while (k < max_iter) {
-    if (k >= kBlk && k % kBlk == 0 && k + kBlk <= max_iter) {
-      if (!t_on_device) {
+    // the iterations up to the next gap check (ama.cpp: k == 1, every 10th, the last)
+    const int64_t next = (k == 0) ? 1 : std::min<int64_t>((k / kBlk + 1) * kBlk, max_iter);
+    const int cnt = static_cast<int>(next - k);
+    if (ama_block_fused(P, Xh, Zh, Zp, Xout, step, t, cnt)) {  // small problems: one cooperative kernel
+      for (int j = 0; j < cnt; ++j) t = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));  // host copy of t
+    } else if (cnt == kBlk) {
+      if (!blk.exec) {
         ama_set_t(P, tm, kBlk, t);
-        t_on_device = true;
+        blk.capture(c.s, [&] {
+          ama_momenta(P, tm, kBlk);
+          for (int j = 0; j < kBlk; ++j) {
+            ama_primal(P, Zh, Xh);
+            ama_dual_step(P, Xh, Zh, Zp, step, 0.0, tm + j);
+          }
+        });
       }
-      // small problems: the whole block + recover_primal is one cooperative kernel
-      if (!ama_block_fused(P, Xh, Zh, Zp, Xout, step, tm, kBlk)) {
-        if (!blk.exec)
-          blk.capture(c.s, [&] {
-            ama_momenta(P, tm, kBlk);
-            for (int j = 0; j < kBlk; ++j) {
-              ama_primal(P, Zh, Xh);
-              ama_dual_step(P, Xh, Zh, Zp, step, 0.0, tm + j);
-            }
-          });
-        blk.launch(c.s);
-        ama_primal(P, Zp, Xout);  // X = A - Znew B^T (recover_primal)
-      }
+      blk.launch(c.s);
       for (int j = 0; j < kBlk; ++j) t = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));  // host copy of t
-      k += kBlk;
-      GapOut s = eval_gap(P, Xout, Zp);
-      if (accepts(s, cfg)) {
-        copy_dev(c, Zout, Zp, me);
-        return finish(s, k, true, since(t0));
-      }
-      best.offer(c, s, Xout, Zp, Xb, Zb, m, me);
-      if (cfg.time_limit > 0.0 && since(t0) > cfg.time_limit) break;
-      continue;
-    }
-    ++k;
-    ama_primal(P, Zh, Xh);
-    const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));
-    ama_dual_step(P, Xh, Zh, Zp, step, (t - 1.0) / tn);
-    t = tn;
-    if (k == 1 || k % 10 == 0 || k == max_iter) {
       ama_primal(P, Zp, Xout);  // X = A - Znew B^T (recover_primal)
-      GapOut s = eval_gap(P, Xout, Zp);
-      if (accepts(s, cfg)) {
-        copy_dev(c, Zout, Zp, me);
-        return finish(s, k, true, since(t0));
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        ama_primal(P, Zh, Xh);
+        const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));
+        ama_dual_step(P, Xh, Zh, Zp, step, (t - 1.0) / tn);
+        t = tn;
       }
-      best.offer(c, s, Xout, Zp, Xb, Zb, m, me);
+      ama_primal(P, Zp, Xout);  // X = A - Znew B^T (recover_primal)
     }
+    k = next;
+    GapOut s = eval_gap(P, Xout, Zp);
+    if (accepts(s, cfg)) {
+      copy_dev(c, Zout, Zp, me);
+      return finish(s, k, true, since(t0));
+    }
+    best.offer(c, s, Xout, Zp, Xb, Zb, m, me);
     if (cfg.time_limit > 0.0 && since(t0) > cfg.time_limit) break;
   }
   copy_dev(c, Xout, Xb, m);
