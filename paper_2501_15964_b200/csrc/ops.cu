@@ -1000,6 +1000,16 @@ __global__ void k_ama_edge(const double* __restrict__ Xh, double* __restrict__ Z
   ROWS_BEGIN(E) { ama_edge_row(row_, Xh, Zh, Zp, ei[row_], ej[row_], rad[row_], d, step, mom, q, gm); }
 }
 
+// k_g_gap's per-(node, feature) terms: ||X - A||^2, ||B^T Z||^2, <B^T Z, A>, ||X - A + B^T Z||^2
+__device__ __forceinline__ void gap_node_acc(double* s, double xv, double a, double acc) {
+  const double xa = xv - a;
+  const double st = xa + acc;
+  s[0] += xa * xa;
+  s[1] += acc * acc;
+  s[2] += acc * a;
+  s[3] += st * st;
+}
+
 // Fused block of `cnt` AMA iterations for small problems (d <= 32), one cooperative launch:
 // per iteration X^ = A - Z^ B^T (node-CSR gather, incident edges in ascending id: k_g_bt mode
 // 1's exact order), grid barrier, the edge step with the iteration's Nesterov momentum
@@ -1012,13 +1022,14 @@ __global__ void __launch_bounds__(256) k_ama_block(const double* __restrict__ A,
                                                    const int* __restrict__ off, const int* __restrict__ adj_e,
                                                    const int* __restrict__ adj_o, const int* __restrict__ order,
                                                    int64_t n, int64_t E, int d, double step, int q, double t0,
-                                                   int cnt) {
+                                                   int cnt, const double* __restrict__ wt, double* part) {
   cg::grid_group grid = cg::this_grid();
   const unsigned gm = group_mask();
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const int lane = tid & 31;
   const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * 256 + tid) >> 5, nw = static_cast<int64_t>(gridDim.x) * 8;
   double t = t0;
+  double sn[4] = {0, 0, 0, 0};
   // When every warp owns at most one node and every group at most one edge for the whole
   // kernel (C1), the node's incident edge ids / sides and the edge's endpoints stay in
   // registers, so an iteration's loads are all independent (one L2 latency per phase).
@@ -1064,7 +1075,9 @@ __global__ void __launch_bounds__(256) k_ama_block(const double* __restrict__ A,
         }
         if (lane < d) {
           const int64_t i = static_cast<int64_t>(my_v) * d + lane;
-          Xd[i] = A[i] - acc;
+          const double xv = A[i] - acc;
+          Xd[i] = xv;
+          if (last) gap_node_acc(sn, xv, A[i], acc);
         }
       }
     } else
@@ -1078,7 +1091,9 @@ __global__ void __launch_bounds__(256) k_ama_block(const double* __restrict__ A,
           acc = adj_o[p] > v ? acc + x : acc - x;
         }
         const int64_t i = static_cast<int64_t>(v) * d + lane;
-        Xd[i] = A[i] - acc;
+        const double xv = A[i] - acc;
+        Xd[i] = xv;
+        if (last) gap_node_acc(sn, xv, A[i], acc);
       }
     }
     if (last) break;
@@ -1094,6 +1109,31 @@ __global__ void __launch_bounds__(256) k_ama_block(const double* __restrict__ A,
     }
     grid.sync();
   }
+  // The gap check's partials at (Xout, Zp) (k_g_gap / k_gap_edge terms): the node terms came
+  // with the last gather (acc = the B^T Zp row k_g_gap forms, same order); the edge terms need
+  // every Xout row, hence one more barrier.  X, Z rows are first touched here by this SM (earlier
+  // phases load with __ldcg), so plain loads see the other SMs' writes.
+  __shared__ double sh[32];
+  for (int k = 0; k < 4; ++k) {
+    const double r = block_sum(sn[k], sh);
+    if (tid == 0) part[4 * blockIdx.x + k] = r;
+  }
+  grid.sync();
+  double se[4] = {0, 0, 0, 0}, excess = -1.0;
+  for (int64_t row = row0; row < E; row += static_cast<int64_t>(gridDim.x) * blockDim.y) {
+    double t4[4];
+    gap_edge_terms(Xout + static_cast<int64_t>(ei[row]) * d, Xout + static_cast<int64_t>(ej[row]) * d, Zp + row * d,
+                   rad[row], wt[row], d, q, gm, t4, excess);
+    if (threadIdx.x == 0)
+      for (int k = 0; k < 4; ++k) se[k] += t4[k];
+  }
+  double* pe = part + 4 * static_cast<int64_t>(gridDim.x);
+  for (int k = 0; k < 4; ++k) {
+    const double r = block_sum(se[k], sh);
+    if (tid == 0) pe[5 * blockIdx.x + k] = r;
+  }
+  const double m = block_max(excess, sh);
+  if (tid == 0) pe[5 * blockIdx.x + 4] = m;
 }
 
 // ---- host helpers ----------------------------------------------------------------------------
@@ -1348,14 +1388,22 @@ GapOut eval_gap(const Prob& P, const double* X, const double* Z) {
                                                         static_cast<int>(d), P.q, pe);
     CPB_LAUNCH_CHECK();
   }
-  std::vector<double> all(4 * static_cast<size_t>(nbn) + (E > 0 ? 5 * static_cast<size_t>(ge.grid) : 0));
-  d2h(c, all.data(), pn, all.size() * sizeof(double));
+  return gap_from_partials(P, pn, nbn, E > 0 ? ge.grid : 0);
+}
+
+// The gap / KKT numbers from the device's node partial table [nbn x 4] followed by the edge
+// partial table [nbe x 5] (one D2H for both).
+GapOut gap_from_partials(const Prob& P, const double* dev_parts, int nbn, int nbe) {
+  Ctx& c = *P.c;
+  const int64_t E = P.E();
+  std::vector<double> all(4 * static_cast<size_t>(nbn) + 5 * static_cast<size_t>(nbe));
+  d2h(c, all.data(), dev_parts, all.size() * sizeof(double));
   std::vector<double> h = reduce_cols(all.data(), nbn, 4);
   if (partitioned(c)) comm_allreduce_host(c, h);
   std::vector<double> e(5, 0.0);
   e[4] = -1.0;
   if (E > 0) {
-    e = reduce_cols(all.data() + 4 * static_cast<size_t>(nbn), ge.grid, 5, {4});
+    e = reduce_cols(all.data() + 4 * static_cast<size_t>(nbn), nbe, 5, {4});
     if (partitioned(c)) comm_allreduce_host(c, e, {4});
   }
   if (e[4] > 0.0) invalid("dual_objective: Z violates the dual-ball constraint");
@@ -1572,19 +1620,19 @@ void ama_momenta(const Prob& P, double* tm, int cnt) {
   k_ama_mom<<<1, 1, 0, P.c->s>>>(tm, cnt);
   CPB_LAUNCH_CHECK();
 }
-bool ama_block_fused(const Prob& P, double* Xh, double* Zh, double* Zp, double* Xout, double step, double t0,
-                     int cnt) {
+int ama_block_fused(const Prob& P, double* Xh, double* Zh, double* Zp, double* Xout, double step, double t0,
+                    int cnt, double** parts) {
   Ctx& c = *P.c;
   const int64_t d = P.d(), n = P.n(), E = P.E();
   static const bool enabled = [] {
     const char* e = std::getenv("CPB_AMA_FUSED");
     return !(e && e[0] == '0');
   }();
-  if (!enabled || d > 32 || E > (1 << 18) || n > (1 << 17) || partitioned(c)) return false;
+  if (!enabled || d > 32 || E < 1 || E > (1 << 18) || n > (1 << 17) || partitioned(c)) return 0;
   GroupGeom ge = group_geom(c, E, d);
   static int occ = -1;
   if (occ < 0) CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ama_block, 256, 0));
-  if (occ < 1) return false;
+  if (occ < 1) return 0;
   const int64_t want = std::max<int64_t>(cdiv(n, 8), cdiv(E, ge.gy));
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(c.sm_count))));
   const double* A = P.A->A.p;
@@ -1592,12 +1640,18 @@ bool ama_block_fused(const Prob& P, double* Xh, double* Zh, double* Zp, double* 
             *ord = P.g->order.p;
   const double* rad = P.rad;
   int dd = static_cast<int>(d), qq = P.q;
+  const double* wt = P.g->w.p;
+  double* part = part_buf(c, "ama.parts", 9 * static_cast<size_t>(grid));
   void* args[] = {(void*)&A,   (void*)&Xh,  (void*)&Zh, (void*)&Zp, (void*)&Xout, (void*)&rad, (void*)&ei,
                   (void*)&ej,  (void*)&off, (void*)&ae, (void*)&ao, (void*)&ord,  (void*)&n,   (void*)&E,
-                  (void*)&dd,  (void*)&step, (void*)&qq, (void*)&t0, (void*)&cnt};
-  CPB_CUDA(cudaLaunchCooperativeKernel((const void*)k_ama_block, dim3(grid), dim3(ge.gx, ge.gy), args, 0, c.s));
-  CPB_LAUNCH_CHECK();
-  return true;
+                  (void*)&dd,  (void*)&step, (void*)&qq, (void*)&t0, (void*)&cnt, (void*)&wt, (void*)&part};
+  {
+    Ctx::Timer tm(&c, "ama_block", static_cast<double>(cnt) * (5.0 * E * d + 3.0 * n * d) * 8.0);
+    CPB_CUDA(cudaLaunchCooperativeKernel((const void*)k_ama_block, dim3(grid), dim3(ge.gx, ge.gy), args, 0, c.s));
+    CPB_LAUNCH_CHECK();
+  }
+  *parts = part;
+  return grid;
 }
 void ama_set_t(const Prob& P, double* tm, int cnt, double t) {
   k_set1<<<1, 1, 0, P.c->s>>>(tm + cnt, t);

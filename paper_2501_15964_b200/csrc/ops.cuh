@@ -113,10 +113,13 @@ void ama_dual_step(const Prob& P, const double* Xh, double* Zh, double* Zprev, d
                    const double* momp = nullptr);
 void ama_momenta(const Prob& P, double* tm, int cnt);             // tm[0..cnt) = momenta, tm[cnt] = t
 void ama_set_t(const Prob& P, double* tm, int cnt, double t);
-// cnt AMA iterations + recover_primal into Xout as one cooperative kernel (small d, E);
-// false = not applicable (caller runs the per-kernel / graph path)
-bool ama_block_fused(const Prob& P, double* Xh, double* Zh, double* Zp, double* Xout, double step, double t0,
-                     int cnt);
+// cnt AMA iterations + recover_primal into Xout + the gap partials as one cooperative kernel
+// (small d, E).
+// Returns the grid G (0 = not applicable: caller runs the per-kernel / graph path); *parts then
+// holds the gap check's partial tables at (Xout, Zp) for gap_from_partials(P, *parts, G, G).
+int ama_block_fused(const Prob& P, double* Xh, double* Zh, double* Zp, double* Xout, double step, double t0,
+                    int cnt, double** parts);
+GapOut gap_from_partials(const Prob& P, const double* dev_parts, int nbn, int nbe);
 
 // The `active` flag of a PCG state (nullptr when none): operators no-op on it.
 const int* cg_active_ptr(const void* cg_state);

@@ -292,7 +292,9 @@ cp_termination fast_ama(Prob& P, const cp_solver_config& cfg, bool warm, double*
     // the iterations up to the next gap check (ama.cpp: k == 1, every 10th, the last)
     const int64_t next = (k == 0) ? 1 : std::min<int64_t>((k / kBlk + 1) * kBlk, max_iter);
     const int cnt = static_cast<int>(next - k);
-    if (ama_block_fused(P, Xh, Zh, Zp, Xout, step, t, cnt)) {  // small problems: one cooperative kernel
+    double* parts = nullptr;
+    const int fg = ama_block_fused(P, Xh, Zh, Zp, Xout, step, t, cnt, &parts);  // small problems: one kernel
+    if (fg > 0) {
       for (int j = 0; j < cnt; ++j) t = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));  // host copy of t
     } else if (cnt == kBlk) {
       if (!blk.exec) {
@@ -318,7 +320,7 @@ cp_termination fast_ama(Prob& P, const cp_solver_config& cfg, bool warm, double*
       ama_primal(P, Zp, Xout);  // X = A - Znew B^T (recover_primal)
     }
     k = next;
-    GapOut s = eval_gap(P, Xout, Zp);
+    GapOut s = fg > 0 ? gap_from_partials(P, parts, fg, fg) : eval_gap(P, Xout, Zp);
     if (accepts(s, cfg)) {
       copy_dev(c, Zout, Zp, me);
       return finish(s, k, true, since(t0));
