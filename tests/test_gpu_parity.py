@@ -525,13 +525,17 @@ def test_path_parity(cp, orc, algo):
 # (q = inf at d = 40 is left out: there the device's l1-ball threshold (Michelot fixed point)
 # and the oracle's sort-based one round differently and the gap lands within 4e-9 of epsilon,
 # so the two stop one check apart, which AMA's slow convergence turns into 5e-6 in X.)
-@pytest.mark.parametrize("q,shape", [(2, "circle"), (1, "circle"), (0, "circle"), (2, "d40"), (1, "d40")])
+# circle: 300 nodes, one node per warp (register-resident adjacency); circle1500: more nodes
+# than warps in the grid, the grid-stride gather; d40: the CUDA-graph path.
+@pytest.mark.parametrize("q,shape", [(2, "circle"), (1, "circle"), (0, "circle"), (2, "circle1500"), (2, "d40"),
+                                     (1, "d40")])
 def test_ama_graph_blocks_match_oracle(cp, orc, q, shape):
     """Fast AMA runs the iterations between gap checks as one cooperative kernel (d <= 32:
     k_ama_block) or as one CUDA graph per 10-iteration block with the Nesterov momenta computed
     on the device (d = 40): long solves (hundreds of blocks) must keep the oracle's iteration
     counts and X to near round-off."""
-    A = circle(orc, 30) if shape == "circle" else mixture(orc, 60, 40, m=5, seed=3)
+    A = {"circle": lambda: circle(orc, 30), "circle1500": lambda: circle(orc, 150),
+         "d40": lambda: mixture(orc, 60, 40, m=5, seed=3)}[shape]()
     g, og = check_graph(cp, orc, A, 10, 0.5)
     sched = cp.make_schedule(0.01, 10.0, 6)
     cfg = cp.SolverConfig(algorithm=cp.Algorithm.FastAMA)
