@@ -442,11 +442,17 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* sh /* 6
 // fused pass reduces bitwise like the separate dots did.
 __global__ void __launch_bounds__(1024) k_power(const int* __restrict__ off, const int* __restrict__ adj_o,
                                                 const double* __restrict__ start, int n, double tol, long long max_iter,
-                                                double* v, double* w, double* out) {
+                                                double* v, double* w, double* out, int in_smem) {
   // one block per probe (linalg.cpp:206-216 runs them one after another; they are independent)
+  extern __shared__ double smvw[];
   start += static_cast<int64_t>(blockIdx.x) * n;
-  v += static_cast<int64_t>(blockIdx.x) * n;
-  w += static_cast<int64_t>(blockIdx.x) * n;
+  if (in_smem) {  // small graphs: the iterate and L v live in shared memory
+    v = smvw;
+    w = smvw + n;
+  } else {
+    v += static_cast<int64_t>(blockIdx.x) * n;
+    w += static_cast<int64_t>(blockIdx.x) * n;
+  }
   out += 2 * blockIdx.x;
   __shared__ double sh[64];
   const double ns = sqrt(blk_dot(start, start, n, sh));
@@ -964,7 +970,15 @@ double laplacian_lambda_max(Ctx& c, const Graph& g, double tol, int64_t max_iter
   double* w = c.buf<double>("pw.w", 3 * n);
   h2d(c, ds, starts.data(), starts.size() * sizeof(double));
   // the three probes run concurrently, one block each
-  k_power<<<3, 1024, 0, c.s>>>(g.off.p, g.adj_o.p, ds, static_cast<int>(n), tol, max_iter, v, w, c.dscal);
+  const size_t smem = 2 * static_cast<size_t>(n) * sizeof(double);
+  const int in_smem = smem <= 200 * 1024;
+  static bool attr = false;
+  if (in_smem && !attr) {
+    CPB_CUDA(cudaFuncSetAttribute(k_power, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  k_power<<<3, 1024, in_smem ? smem : 0, c.s>>>(g.off.p, g.adj_o.p, ds, static_cast<int>(n), tol, max_iter, v, w,
+                                                c.dscal, in_smem);
   CPB_LAUNCH_CHECK();
   double out[6];
   c.fetch(0, 6, out);
