@@ -84,6 +84,21 @@ inline double norm2(const double* x, Index n) { return std::sqrt(sq_norm(x, n));
 inline double dotp(const double* x, const double* y, Index n) {
   return esum(n, [&](Index k) { return x[k] * y[k]; });
 }
+// ---- optional host threads (checker runs at C3-C5 sizes only) ---------------
+// ORC_THREADS (default 1: the reference is single-threaded, and the CPU
+// baselines time one thread).  par_ranges splits an index range whose
+// iterations are independent into contiguous chunks; every output element is
+// produced by exactly the sequential loop's arithmetic, and global reductions
+// stay sequential in Eigen's order, so results are bitwise those of one thread
+// (node-partitioned scatters keep the ascending-edge order per node).
+int threads();
+void par_ranges(Index n, const std::function<void(Index, Index)>& f);
+template <class F>
+inline void par_for(Index n, F f) {
+  par_ranges(n, [&](Index lo, Index hi) {
+    for (Index k = lo; k < hi; ++k) f(k);
+  });
+}
 inline double max_abs(const double* x, Index n) {
   double m = 0.0;
   for (Index k = 0; k < n; ++k) m = std::max(m, std::abs(x[k]));

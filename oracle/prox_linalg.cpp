@@ -92,15 +92,17 @@ void project_dual_ball_into(const double* z, Index n, double r, Norm q, double* 
 void prox_columns_into(const Mat& V, const std::vector<double>& t, Norm q, Mat& out) {
   if (static_cast<Index>(t.size()) != V.cols) throw std::invalid_argument("prox_columns: one threshold per column required");
   out = Mat(V.rows, V.cols);
-  for (Index l = 0; l < V.cols; ++l) prox_norm_into(V.col(l), V.rows, t[static_cast<size_t>(l)], q, out.col(l));
+  par_for(V.cols, [&](Index l) { prox_norm_into(V.col(l), V.rows, t[static_cast<size_t>(l)], q, out.col(l)); });
 }
 void project_columns_inplace(Mat& Z, const std::vector<double>& r, Norm q) {
   if (static_cast<Index>(r.size()) != Z.cols) throw std::invalid_argument("project_columns: one radius per column required");
-  std::vector<double> tmp(static_cast<size_t>(Z.rows));
-  for (Index l = 0; l < Z.cols; ++l) {
-    project_dual_ball_into(Z.col(l), Z.rows, r[static_cast<size_t>(l)], q, tmp.data());
-    std::copy(tmp.begin(), tmp.end(), Z.col(l));
-  }
+  par_ranges(Z.cols, [&](Index lo, Index hi) {
+    std::vector<double> tmp(static_cast<size_t>(Z.rows));
+    for (Index l = lo; l < hi; ++l) {
+      project_dual_ball_into(Z.col(l), Z.rows, r[static_cast<size_t>(l)], q, tmp.data());
+      std::copy(tmp.begin(), tmp.end(), Z.col(l));
+    }
+  });
 }
 
 // prox.cpp:95-110
@@ -233,7 +235,7 @@ LinOp op_jacobi(const Mat& diag) {
   op.fn = [diag](const Mat& x) {
     if (x.cols != diag.cols) throw std::invalid_argument("jacobi: operand shape mismatch");
     Mat y(x.rows, x.cols);
-    for (Index k = 0; k < x.size(); ++k) y.v[static_cast<size_t>(k)] = x.v[static_cast<size_t>(k)] / diag.v[static_cast<size_t>(k)];
+    par_for(x.size(), [&](Index k) { y.v[static_cast<size_t>(k)] = x.v[static_cast<size_t>(k)] / diag.v[static_cast<size_t>(k)]; });
     return y;
   };
   return op;
@@ -260,12 +262,14 @@ double relres(const Mat& r, const Mat& b) {
     const double nb = norm2(b.v.data(), b.size());
     return norm2(r.v.data(), r.size()) / (nb > 0.0 ? nb : 1.0);
   }
-  double worst = 0.0;
-  for (Index i = 0; i < b.rows; ++i) {
+  std::vector<double> rel(static_cast<size_t>(b.rows));
+  par_for(b.rows, [&](Index i) {
     const double nb = std::sqrt(ssum(b.cols, [&](Index c) { return b(i, c) * b(i, c); }));
     const double nr = std::sqrt(ssum(r.cols, [&](Index c) { return r(i, c) * r(i, c); }));
-    worst = std::max(worst, nr / (nb > 0.0 ? nb : 1.0));
-  }
+    rel[static_cast<size_t>(i)] = nr / (nb > 0.0 ? nb : 1.0);
+  });
+  double worst = 0.0;
+  for (double x : rel) worst = std::max(worst, x);
   return worst;
 }
 double fdot(const Mat& a, const Mat& b) { return dotp(a.v.data(), b.v.data(), a.size()); }
@@ -298,13 +302,15 @@ PcgOut pcg(const LinOp& op, const Mat& rhs, const LinOp* pre, double tol, Index 
       throw std::runtime_error("pcg: operator is not positive definite (p'Ap <= 0)");
     }
     const double alpha = rz / pAp;
-    for (Index k = 0; k < p.size(); ++k) res.x.v[static_cast<size_t>(k)] += alpha * p.v[static_cast<size_t>(k)];
-    for (Index k = 0; k < p.size(); ++k) r.v[static_cast<size_t>(k)] -= alpha * Ap.v[static_cast<size_t>(k)];
+    par_for(p.size(), [&](Index k) {
+      res.x.v[static_cast<size_t>(k)] += alpha * p.v[static_cast<size_t>(k)];
+      r.v[static_cast<size_t>(k)] -= alpha * Ap.v[static_cast<size_t>(k)];
+    });
     if (relres(r, rhs) <= tol) break;
     z = precond(r);
     const double rz_next = fdot(r, z);
     const double beta = rz_next / rz;
-    for (Index k = 0; k < p.size(); ++k) p.v[static_cast<size_t>(k)] = z.v[static_cast<size_t>(k)] + beta * p.v[static_cast<size_t>(k)];
+    par_for(p.size(), [&](Index k) { p.v[static_cast<size_t>(k)] = z.v[static_cast<size_t>(k)] + beta * p.v[static_cast<size_t>(k)]; });
     rz = rz_next;
   }
   res.iterations = it;

@@ -39,12 +39,32 @@ std::vector<double> Instance::radii() const {
 namespace {
 Mat sub(const Mat& a, const Mat& b) {
   Mat o(a.rows, a.cols);
-  for (Index k = 0; k < a.size(); ++k) o.v[static_cast<size_t>(k)] = a.v[static_cast<size_t>(k)] - b.v[static_cast<size_t>(k)];
+  par_for(a.size(), [&](Index k) { o.v[static_cast<size_t>(k)] = a.v[static_cast<size_t>(k)] - b.v[static_cast<size_t>(k)]; });
   return o;
 }
 double sqn(const Mat& a) { return sq_norm(a.v.data(), a.size()); }
 double fro(const Mat& a) { return std::sqrt(sqn(a)); }
-double maxabs(const Mat& a) { return max_abs(a.v.data(), a.size()); }
+// max is exact in any order
+double maxabs(const Mat& a) {
+  const Index T = threads();
+  std::vector<double> part(static_cast<size_t>(T), 0.0);
+  par_ranges(a.size(), [&](Index lo, Index hi) {
+    const Index t = a.size() ? lo * T / a.size() : 0;
+    part[static_cast<size_t>(std::min(t, T - 1))] = max_abs(a.v.data() + lo, hi - lo);
+  });
+  double m = 0.0;
+  for (double x : part) m = std::max(m, x);
+  return m;
+}
+// per-column terms in parallel, summed sequentially in ascending l
+template <class F>
+double colsum(Index E, F term) {
+  std::vector<double> t(static_cast<size_t>(E));
+  par_for(E, [&](Index l) { t[static_cast<size_t>(l)] = term(l); });
+  double acc = 0.0;
+  for (double x : t) acc += x;
+  return acc;
+}
 }  // namespace
 
 // objective.cpp:63-74
@@ -54,19 +74,21 @@ double primal_objective(const Instance& in, const Mat& X) {
   if (in.E() == 0 || in.gamma == 0.0) return value;
   Mat D;
   incidence_apply(*in.g, X, D);
-  double pen = 0.0;
-  for (Index l = 0; l < D.cols; ++l) pen += in.g->edges[static_cast<size_t>(l)].w * norm_value(D.col(l), D.rows, in.q);
+  const double pen = colsum(D.cols, [&](Index l) { return in.g->edges[static_cast<size_t>(l)].w * norm_value(D.col(l), D.rows, in.q); });
   return value + in.gamma * pen;
 }
 
 // objective.cpp:76-88
 double dual_objective(const Instance& in, const Mat& Z) {
   if (Z.rows != in.d() || Z.cols != in.E()) throw std::invalid_argument("dual_objective: Z has the wrong shape");
-  for (Index l = 0; l < Z.cols; ++l) {
+  std::vector<char> bad(static_cast<size_t>(Z.cols), 0);
+  par_for(Z.cols, [&](Index l) {
     const double radius = in.gamma * in.g->edges[static_cast<size_t>(l)].w;
-    if (dual_norm_value(Z.col(l), Z.rows, in.q) > radius + 1e-9)
+    bad[static_cast<size_t>(l)] = dual_norm_value(Z.col(l), Z.rows, in.q) > radius + 1e-9;
+  });
+  for (Index l = 0; l < Z.cols; ++l)
+    if (bad[static_cast<size_t>(l)])
       throw std::invalid_argument("dual_objective: Z violates the dual-ball constraint on edge " + std::to_string(l));
-  }
   Mat ZBt;
   incidence_apply_t(*in.g, Z, ZBt);
   return -0.5 * sqn(ZBt) + dotp(ZBt.v.data(), in.A->v.data(), ZBt.size());
@@ -88,14 +110,15 @@ double kkt_residual(const Instance& in, const Mat& X, const Mat& Z) {
   Mat ZBt;
   incidence_apply_t(*in.g, Z, ZBt);
   Mat S(X.rows, X.cols);
-  for (Index k = 0; k < S.size(); ++k)
+  par_for(S.size(), [&](Index k) {
     S.v[static_cast<size_t>(k)] = X.v[static_cast<size_t>(k)] - in.A->v[static_cast<size_t>(k)] + ZBt.v[static_cast<size_t>(k)];
+  });
   const double stat = fro(S) / (1.0 + fro(*in.A));
   if (in.E() == 0 || in.gamma == 0.0) return stat;
   Mat XB, P;
   incidence_apply(*in.g, X, XB);
   Mat W(XB.rows, XB.cols);
-  for (Index k = 0; k < W.size(); ++k) W.v[static_cast<size_t>(k)] = XB.v[static_cast<size_t>(k)] + Z.v[static_cast<size_t>(k)];
+  par_for(W.size(), [&](Index k) { W.v[static_cast<size_t>(k)] = XB.v[static_cast<size_t>(k)] + Z.v[static_cast<size_t>(k)]; });
   prox_columns_into(W, in.radii(), in.q, P);
   const double align = fro(sub(XB, P)) / (1.0 + fro(XB) + fro(Z));
   return std::max(stat, align);
@@ -170,16 +193,15 @@ struct Phi {
 Phi eval_phi(const Instance& in, const Mat& Z, double sigma, const std::vector<double>& thr, const Mat& X) {
   Phi e;
   incidence_apply(*in.g, X, e.V);
-  for (Index k = 0; k < e.V.size(); ++k) e.V.v[static_cast<size_t>(k)] += Z.v[static_cast<size_t>(k)] / sigma;
+  par_for(e.V.size(), [&](Index k) { e.V.v[static_cast<size_t>(k)] += Z.v[static_cast<size_t>(k)] / sigma; });
   prox_columns_into(e.V, thr, in.q, e.PV);
-  double env = 0.0;
   const Index d = e.V.rows;
-  std::vector<double> diff(static_cast<size_t>(d));
-  for (Index l = 0; l < e.V.cols; ++l) {
+  const double env = colsum(e.V.cols, [&](Index l) {
+    std::vector<double> diff(static_cast<size_t>(d));
     const double w = in.g->edges[static_cast<size_t>(l)].w;
     for (Index r = 0; r < d; ++r) diff[static_cast<size_t>(r)] = e.PV(r, l) - e.V(r, l);
-    env += in.gamma * w * norm_value(e.PV.col(l), d, in.q) + 0.5 * sigma * sq_norm(diff.data(), d);
-  }
+    return in.gamma * w * norm_value(e.PV.col(l), d, in.q) + 0.5 * sigma * sq_norm(diff.data(), d);
+  });
   e.value = 0.5 * sqn(sub(X, *in.A)) + env - sqn(Z) / (2.0 * sigma);
   return e;
 }
@@ -187,40 +209,47 @@ Mat phi_grad(const Instance& in, double sigma, const Mat& X, const Phi& e) {
   Mat T, U = sub(e.V, e.PV);
   incidence_apply_t(*in.g, U, T);
   Mat G(X.rows, X.cols);
-  for (Index k = 0; k < G.size(); ++k)
+  par_for(G.size(), [&](Index k) {
     G.v[static_cast<size_t>(k)] = X.v[static_cast<size_t>(k)] - in.A->v[static_cast<size_t>(k)] + sigma * T.v[static_cast<size_t>(k)];
+  });
   return G;
 }
 std::vector<ProxJac> edge_jacobians(const Instance& in, const Mat& V, const std::vector<double>& thr) {
-  std::vector<ProxJac> J;
-  J.reserve(static_cast<size_t>(V.cols));
-  for (Index l = 0; l < V.cols; ++l) J.push_back(prox_jacobian(V.col(l), V.rows, thr[static_cast<size_t>(l)], in.q));
+  std::vector<ProxJac> J(static_cast<size_t>(V.cols));
+  par_for(V.cols, [&](Index l) { J[static_cast<size_t>(l)] = prox_jacobian(V.col(l), V.rows, thr[static_cast<size_t>(l)], in.q); });
   return J;
 }
 Mat hess_apply(const Instance& in, double sigma, const Mat& D, const std::vector<ProxJac>& J) {
   Mat W;
   incidence_apply(*in.g, D, W);
-  std::vector<double> jw(static_cast<size_t>(W.rows));
-  for (Index l = 0; l < W.cols; ++l) {
-    J[static_cast<size_t>(l)].apply(W.col(l), W.rows, jw.data());
-    for (Index r = 0; r < W.rows; ++r) W(r, l) = W(r, l) - jw[static_cast<size_t>(r)];
-  }
+  par_ranges(W.cols, [&](Index lo, Index hi) {
+    std::vector<double> jw(static_cast<size_t>(W.rows));
+    for (Index l = lo; l < hi; ++l) {
+      J[static_cast<size_t>(l)].apply(W.col(l), W.rows, jw.data());
+      for (Index r = 0; r < W.rows; ++r) W(r, l) = W(r, l) - jw[static_cast<size_t>(r)];
+    }
+  });
   Mat T;
   incidence_apply_t(*in.g, W, T);
   Mat H(D.rows, D.cols);
-  for (Index k = 0; k < H.size(); ++k) H.v[static_cast<size_t>(k)] = D.v[static_cast<size_t>(k)] + sigma * T.v[static_cast<size_t>(k)];
+  par_for(H.size(), [&](Index k) { H.v[static_cast<size_t>(k)] = D.v[static_cast<size_t>(k)] + sigma * T.v[static_cast<size_t>(k)]; });
   return H;
 }
 Mat hess_diag(const Instance& in, double sigma, const std::vector<ProxJac>& J) {
   Mat g(in.d(), in.n(), 1.0);
-  for (Index l = 0; l < in.E(); ++l) {
-    const Edge& e = in.g->edges[static_cast<size_t>(l)];
-    for (Index r = 0; r < in.d(); ++r) {
-      const double c = sigma * (1.0 - J[static_cast<size_t>(l)].diag(r));
-      g(r, e.i) += c;
-      g(r, e.j) += c;
+  // node ranges per thread, ascending l within each (the sequential order per node)
+  par_ranges(in.n(), [&](Index lo, Index hi) {
+    for (Index l = 0; l < in.E(); ++l) {
+      const Edge& e = in.g->edges[static_cast<size_t>(l)];
+      const bool in_i = e.i >= lo && e.i < hi, in_j = e.j >= lo && e.j < hi;
+      if (!in_i && !in_j) continue;
+      for (Index r = 0; r < in.d(); ++r) {
+        const double c = sigma * (1.0 - J[static_cast<size_t>(l)].diag(r));
+        if (in_i) g(r, e.i) += c;
+        if (in_j) g(r, e.j) += c;
+      }
     }
-  }
+  });
   return g;
 }
 std::vector<double> thresholds(const Instance& in, double sigma) {
@@ -283,7 +312,7 @@ Solution solve_ssnal(const Instance& in, const Config& c, const Solution* warm, 
       LinOp pre = op_jacobi(hess_diag(in, sigma, J));
       const double cg_tol = std::min(0.1, std::sqrt(gnorm));
       Mat rhs(G.rows, G.cols);
-      for (Index q = 0; q < G.size(); ++q) rhs.v[static_cast<size_t>(q)] = -G.v[static_cast<size_t>(q)];
+      par_for(G.size(), [&](Index q) { rhs.v[static_cast<size_t>(q)] = -G.v[static_cast<size_t>(q)]; });
       PcgOut dir = pcg(H, rhs, &pre, std::max(cg_tol, 1e-12), c.pcg_max_iter);
       cnt.cg += dir.iterations;
       Mat D = std::move(dir.x);
@@ -296,23 +325,23 @@ Solution solve_ssnal(const Instance& in, const Config& c, const Solution* warm, 
       Phi trial;
       Mat Xt(d, n);
       for (int bt = 0; bt < 60; ++bt) {
-        for (Index q = 0; q < X.size(); ++q) Xt.v[static_cast<size_t>(q)] = X.v[static_cast<size_t>(q)] + alpha * D.v[static_cast<size_t>(q)];
+        par_for(X.size(), [&](Index q) { Xt.v[static_cast<size_t>(q)] = X.v[static_cast<size_t>(q)] + alpha * D.v[static_cast<size_t>(q)]; });
         trial = eval_phi(in, Z, sigma, thr, Xt);
         ++cnt.armijo;
         if (trial.value <= e.value + c.armijo_mu * alpha * descent) break;
         alpha *= c.backtrack_beta;
       }
-      for (Index q = 0; q < X.size(); ++q) X.v[static_cast<size_t>(q)] += alpha * D.v[static_cast<size_t>(q)];
+      par_for(X.size(), [&](Index q) { X.v[static_cast<size_t>(q)] += alpha * D.v[static_cast<size_t>(q)]; });
       e = std::move(trial);
     }
     Mat XB;
     incidence_apply(*in.g, X, XB);
     {
       Mat Zenv(d, in.E()), Zsum(d, in.E());
-      for (Index q = 0; q < Zenv.size(); ++q) {
+      par_for(Zenv.size(), [&](Index q) {
         Zenv.v[static_cast<size_t>(q)] = sigma * (e.V.v[static_cast<size_t>(q)] - e.PV.v[static_cast<size_t>(q)]);
         Zsum.v[static_cast<size_t>(q)] = Z.v[static_cast<size_t>(q)] + sigma * XB.v[static_cast<size_t>(q)];
-      }
+      });
       const double scale = 1.0 + maxabs(Zsum);
       project_columns_inplace(Zsum, radii, in.q);
       if (maxabs(sub(Zenv, Zsum)) > 1e-10 * scale) throw std::runtime_error("ssnal: multiplier self-check failed");
