@@ -143,12 +143,12 @@ Index component_count(const std::vector<Index>& labels);
 // it): parity unpinned; the math restated here is SURVEY.md §8(c):
 //   prox_{t||.||inf}(v) = v - Pi_{B1(t)}(v) = clamp(v, -theta, theta),
 //   Pi_{B1(t)}(v)       = sign(v) max(|v| - theta, 0) when ||v||_1 > t,
-// theta from the sort-based l1-ball threshold; outside the ball the Clarke
+// theta the l1-ball threshold (Michelot's fixed point in the device's 32-lane
+// summation order, prox_linalg.cpp); outside the ball the Clarke
 // Jacobian element of the projection is diag(1_S) - s_S s_S^T / |S|.
 enum class Norm { linf = 0, l1 = 1, l2 = 2 };
 // l1-ball projection threshold: theta >= 0 with sum max(|v| - theta, 0) = t
-// when ||v||_1 > t (sorted |v|, largest feasible support), else -1; *count =
-// #{|v_i| > theta}.
+// when ||v||_1 > t, else -1; *count = |S| of the converged support.
 double l1_theta(const double* v, Index n, double t, Index* count);
 double norm_value(const double* v, Index n, Norm q);
 double dual_norm_value(const double* v, Index n, Norm q);

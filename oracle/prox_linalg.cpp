@@ -26,27 +26,64 @@ double dual_norm_value(const double* v, Index n, Norm q) {
   return q == Norm::l1 ? max_abs(v, n) : norm2(v, n);
 }
 
+// The l1-ball threshold by Michelot's fixed point, with every sum in the
+// "32-lane" order the device uses (linf.cuh, group_sum over lane-strided
+// partials): element k goes to partial k mod 32 in increasing k, then the
+// partials meet in an xor butterfly (16, 8, 4, 2, 1).  Same algorithm and same
+// rounding on both sides, so theta, S and everything derived from them are
+// bitwise equal to the device's (no reference exists for q = inf; the
+// bisection / sort-based checks in tests/test_linf_oracle.py pin the math).
+namespace {
+template <class F>
+double lane32_sum(Index n, F f) {  // f(k, &x) -> include?
+  double p[32] = {0.0};
+  for (Index k = 0; k < n; ++k) {
+    double x;
+    if (f(k, &x)) p[k & 31] += x;
+  }
+  for (int o = 16; o >= 1; o >>= 1) {
+    double q[32];
+    for (int v = 0; v < 32; ++v) q[v] = p[v] + p[v ^ o];
+    for (int v = 0; v < 32; ++v) p[v] = q[v];
+  }
+  return p[0];
+}
+}  // namespace
+
 double l1_theta(const double* v, Index n, double t, Index* count) {
-  double s1 = 0.0;
-  for (Index k = 0; k < n; ++k) s1 += std::abs(v[k]);
+  const double s1 = lane32_sum(n, [&](Index k, double* x) {
+    *x = std::abs(v[k]);
+    return true;
+  });
   if (!(s1 > t)) {
     if (count) *count = 0;
     return -1.0;
   }
-  std::vector<double> u(static_cast<size_t>(n));
-  for (Index k = 0; k < n; ++k) u[static_cast<size_t>(k)] = std::abs(v[k]);
-  std::sort(u.begin(), u.end(), std::greater<double>());
-  double cs = 0.0, theta = u[0] - t;  // support of one element when no larger support is feasible
-  for (Index j = 0; j < n; ++j) {
-    cs += u[static_cast<size_t>(j)];
-    const double th = (cs - t) / static_cast<double>(j + 1);
-    if (u[static_cast<size_t>(j)] - th > 0.0) theta = th;
-  }
-  if (count) {
+  double theta = (s1 - t) / static_cast<double>(n);
+  Index support = n;
+  // the support shrinks strictly on every pass that continues, so this ends
+  // within n passes; a pass whose support does not shrink (the fixed point,
+  // or a rounding-induced regrowth) keeps the previous theta
+  for (;;) {
     Index c = 0;
-    for (Index k = 0; k < n; ++k) c += std::abs(v[k]) > theta ? 1 : 0;
-    *count = c;
+    const double th = theta;
+    const double s = lane32_sum(n, [&](Index k, double* x) {
+      *x = std::abs(v[k]);
+      if (*x > th) {
+        ++c;
+        return true;
+      }
+      return false;
+    });
+    if (c == 0) {
+      support = 0;
+      break;
+    }
+    if (c >= support) break;
+    theta = (s - t) / static_cast<double>(c);
+    support = c;
   }
+  if (count) *count = support;
   return theta;
 }
 

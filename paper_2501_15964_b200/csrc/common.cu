@@ -7,10 +7,21 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <set>
+#include <string>
 
 namespace cpb {
 
 thread_local cudaStream_t tl_stream = nullptr;
+
+bool first_on_device(const char* tag) {
+  static std::mutex mu;
+  static std::set<std::pair<int, std::string>> seen;
+  int dev = 0;
+  CPB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  return seen.emplace(dev, tag).second;
+}
 
 void trace(const char* tag) {
   static const bool on = std::getenv("CPB_TRACE") != nullptr;

@@ -247,6 +247,11 @@ __device__ __forceinline__ double group_max(double v, unsigned m) {
 // on stderr (diagnostics for host-side stalls; off by default).
 void trace(const char* tag);
 
+// True the first time `tag` is seen for the calling thread's current device
+// (kernel attributes such as the >48 KB shared-memory opt-in are per device;
+// thread-safe, so in-process ranks on several devices each set their own).
+bool first_on_device(const char* tag);
+
 // Host helpers implemented in common.cu.
 // Deterministic sum of `count` doubles at `src` into dst[0] (one block).
 void reduce_sum(Ctx& c, const double* src, int64_t count, double* dst);

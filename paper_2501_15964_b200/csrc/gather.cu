@@ -32,13 +32,9 @@ struct ChunkGeom {
   int nch;  // chunks per node
   int nf;   // features per lane
 };
-// Up to 32 * nf_max features per warp (CPB_NFMAX overrides the default 6, tuning only).
+// Up to 32 * 6 features per warp.
 inline ChunkGeom chunk_geom(int64_t d) {
-  static const int nf_max = [] {
-    const char* e = std::getenv("CPB_NFMAX");
-    const int v = e ? std::atoi(e) : 6;
-    return v < 1 ? 1 : (v > 6 ? 6 : v);
-  }();
+  constexpr int nf_max = 6;
   const int nch = static_cast<int>((d + 32 * nf_max - 1) / (32 * nf_max));
   const int nf = static_cast<int>((d + 32 * nch - 1) / (32 * nch));
   return {nch, nf};
@@ -886,78 +882,11 @@ int gather_grad_diag(Ctx& c, const Graph& g, const double* X, const double* A, c
   return ng.grid;
 }
 
-// Optional work lists of the single-pass short-row Hessian
-// (CPB_HESS_WARP_ORDER=bfs): breadth-first node order (this rank's nodes when
-// partitioned) cut by lpt_lists into windows of one node per warp, cost =
-// degree + 4, cached per (graph, node range, warps).  Measured 2x slower than
-// the default grid-stride walk of the degree-descending order at C5 (13.3 vs
-// 7.0 ms): the concurrently processed breadth-first window shares its
-// neighbours, so many warps gather the same rows at once.
-struct WarpNodeLists {
-  uint64_t uid = 0;
-  int64_t v0 = 0, v1 = -1;
-  int nw = 0;
-  DBuf<int> flat;
-};
-const int* warp_node_lists(Ctx& c, const Graph& g, int nw) {
-  static const int mode = [] {  // 0 off, 1 bfs + LPT windows, 2 node id + LPT windows, 3 bfs round-robin
-    const char* e = std::getenv("CPB_HESS_WARP_ORDER");
-    if (!e) return 0;
-    const std::string v(e);
-    return v == "bfs" ? 1 : (v == "id" ? 2 : (v == "bfsrr" ? 3 : 0));
-  }();
-  if (mode == 0) return nullptr;
-  static thread_local std::vector<std::unique_ptr<WarpNodeLists>> cache;
-  for (auto& w : cache)
-    if (w->uid == g.uid && w->v0 == c.own_v0 && w->v1 == c.own_v1 && w->nw == nw) return w->flat.p;
-  auto w = std::make_unique<WarpNodeLists>();
-  w->uid = g.uid, w->v0 = c.own_v0, w->v1 = c.own_v1, w->nw = nw;
-  std::vector<int> off, seq_all;
-  if (mode == 2) {
-    off.resize(static_cast<size_t>(g.n) + 1);
-    d2h(c, off.data(), g.off.p, off.size() * sizeof(int));
-    seq_all.resize(static_cast<size_t>(g.n));
-    for (int v = 0; v < g.n; ++v) seq_all[static_cast<size_t>(v)] = v;
-  } else {
-    seq_all = bfs_sequence(c, g, &off);
-  }
-  std::vector<int> seq;
-  seq.reserve(seq_all.size());
-  for (int v : seq_all)
-    if (c.own_v1 < 0 || (v >= c.own_v0 && v < c.own_v1)) seq.push_back(v);
-  std::vector<int64_t> cost(seq.size());
-  for (size_t i = 0; i < seq.size(); ++i) cost[i] = off[seq[i] + 1] - off[seq[i]] + 4;
-  std::vector<int> flat;
-  if (mode == 3) {  // round-robin: warp w takes items w, w + nw, ...
-    flat.resize(static_cast<size_t>(nw) + 1 + seq.size());
-    size_t pos = static_cast<size_t>(nw) + 1;
-    for (int w = 0; w < nw; ++w) {
-      flat[static_cast<size_t>(w)] = static_cast<int>(pos);
-      for (size_t i = static_cast<size_t>(w); i < seq.size(); i += static_cast<size_t>(nw))
-        flat[pos++] = static_cast<int>(i);
-    }
-    flat[static_cast<size_t>(nw)] = static_cast<int>(pos);
-  } else {
-    flat = lpt_lists(cost, nw, nw);
-  }
-  for (size_t j = static_cast<size_t>(nw) + 1; j < flat.size(); ++j) flat[j] = seq[static_cast<size_t>(flat[j])];
-  w->flat.resize(flat.size());
-  h2d(c, w->flat.p, flat.data(), flat.size() * sizeof(int));
-  c.sync();
-  if (cache.size() > 8) cache.erase(cache.begin());
-  cache.push_back(std::move(w));
-  return cache.back()->flat.p;
-}
-
 int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,
                   const double* thr, int64_t d, double sigma, int q, double* bc, double* Ap, double* part,
                   const int* active) {
   if (q == 2 && g.E > 0 && hess_tma_supported(d)) return hess_tma(c, g, P, V, jal, jbe, d, sigma, Ap, part, active);
-  static const bool warp_hess = [] {  // CPB_HESS_WARP=0 keeps the two-pass path for short rows
-    const char* e = std::getenv("CPB_HESS_WARP");
-    return !(e && e[0] == '0');
-  }();
-  if (q == 2 && g.E > 0 && warp_hess && d % 2 == 0 && d <= 192) {
+  if (q == 2 && g.E > 0 && d % 2 == 0 && d <= 192) {
     const int np = static_cast<int>((d / 2 + 31) / 32);
     const int* ord = g.order.p;
     int64_t items = g.n;
@@ -966,7 +895,7 @@ int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, cons
       const OwnOrder& o = own_order(c, g);
       ord = o.order.p, items = o.count, grid = c.sm_count * 8;
     }
-    const int* wl = warp_node_lists(c, g, grid * 8);
+    const int* wl = nullptr;  // degree-descending grid-stride walk (node lists measured 1.5-2x slower at C5)
     const int di = static_cast<int>(d);
     switch (np) {
       case 1: k_hess_warp<1><<<grid, 256, 0, c.s>>>(P, V, jal, jbe, g.off.p, g.adj_e.p, g.adj_o.p, ord, items, di,

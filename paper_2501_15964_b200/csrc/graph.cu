@@ -569,14 +569,9 @@ void finalize_graph(Ctx& c, Graph& g) {
     CPB_CUDA(cudaMemcpyAsync(&md, degs, sizeof(int), cudaMemcpyDeviceToHost, c.s));
     c.sync();
     g.max_degree = md;
-    locality_order(c, g);
   }
 }
 
-// Optional gather work order (CPB_GATHER_ORDER=bfs): hubs (degree > 4x the
-// mean) first, then breadth-first.  Measured slower than the default
-// degree-descending order (C5 Hessian 13.6 vs 9.7 ms, C3 gap 1.39 vs 1.30 ms,
-// plus the host BFS), so it is off by default.
 // Breadth-first node sequence over all components (lowest unvisited id
 // starts the next one), with the CSR offsets copied to the host on the way.
 std::vector<int> bfs_sequence(Ctx& c, const Graph& g, std::vector<int>* off_out) {
@@ -634,26 +629,6 @@ std::vector<int> lpt_lists(const std::vector<int64_t>& cost, int nw, int win) {
   }
   flat[static_cast<size_t>(nw)] = pos;
   return flat;
-}
-
-void locality_order(Ctx& c, Graph& g) {
-  static const bool bfs = [] {
-    const char* e = std::getenv("CPB_GATHER_ORDER");
-    return e && std::string(e) == "bfs";
-  }();
-  const int n = static_cast<int>(g.n);
-  if (!bfs || g.E == 0 || n < 2) return;
-  std::vector<int> off;
-  const std::vector<int> bfs_seq = bfs_sequence(c, g, &off);
-  const double mean = 2.0 * static_cast<double>(g.E) / n;
-  auto hub = [&](int v) { return off[v + 1] - off[v] > 4.0 * mean + 16; };
-  std::vector<int> seq;
-  seq.reserve(static_cast<size_t>(n));
-  for (int v : bfs_seq)
-    if (hub(v)) seq.push_back(v);
-  for (int v : bfs_seq)
-    if (!hub(v)) seq.push_back(v);
-  h2d(c, g.order.p, seq.data(), seq.size() * sizeof(int));
 }
 
 std::unique_ptr<Graph> graph_from_edges(Ctx& c, int64_t n, const int64_t* i, const int64_t* j, const double* w,
@@ -972,11 +947,8 @@ double laplacian_lambda_max(Ctx& c, const Graph& g, double tol, int64_t max_iter
   // the three probes run concurrently, one block each
   const size_t smem = 2 * static_cast<size_t>(n) * sizeof(double);
   const int in_smem = smem <= 200 * 1024;
-  static bool attr = false;
-  if (in_smem && !attr) {
+  if (in_smem && first_on_device("k_power.smem"))
     CPB_CUDA(cudaFuncSetAttribute(k_power, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
   k_power<<<3, 1024, in_smem ? smem : 0, c.s>>>(g.off.p, g.adj_o.p, ds, static_cast<int>(n), tol, max_iter, v, w,
                                                 c.dscal, in_smem);
   CPB_LAUNCH_CHECK();

@@ -48,8 +48,6 @@ void knn_rows_dev(Ctx& c, const Data& A, int64_t k, int64_t r0, int64_t r1, doub
 std::unique_ptr<Graph> graph_from_knn_dev(Ctx& c, int64_t n, int64_t k, double phi, const double* kd, const int* kj);
 // Builds CSR/order for a graph whose ei/ej/w/d2 (sorted, validated) are set.
 void finalize_graph(Ctx& c, Graph& g);
-// Replaces g.order (degree-descending) by hubs-first breadth-first order.
-void locality_order(Ctx& c, Graph& g);
 std::vector<int> bfs_sequence(Ctx& c, const Graph& g, std::vector<int>* off_out);
 std::vector<int> lpt_lists(const std::vector<int64_t>& cost, int nw, int win);
 

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
                                                   const int* __restrict__ seg_end, const int* __restrict__ seg_slot,
                                                   int nseg, int d, int dp, double sigma, double* __restrict__ Ap,
                                                   double* __restrict__ partial, double* part, const int* active,
-                                                  int evict_v, int S, const int* __restrict__ wrange) {
+                                                  int S, const int* __restrict__ wrange) {
   if (active && !*active) return;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ double sh[32];
@@ -74,22 +74,11 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
   int cst = 0;        // next ring slot to consume
   unsigned cph = 0;   // its mbarrier phase parity
   double s_a = 0.0, s_b = 0.0;
-  // evict_v bit 0: V_l rows evict_first; bit 1: gathered p rows evict_last
-  const uint64_t vpol = (evict_v & 1) ? policy_evict_first() : 0;
-  const uint64_t ppol = (evict_v & 2) ? policy_evict_last() : 0;
   auto issue = [&](int q, int st) {  // lane 0: stream edge q's rows into stage st
     const bool nv = mb[q] != 0.0;
     mbar_expect_tx(&bar[st], nv ? 2 * row_bytes : row_bytes);
-    if (evict_v & 2)
-      bulk_g2s_hint(ring + st * 2 * dp, P + static_cast<int64_t>(lo[q]) * d, row_bytes, &bar[st], ppol);
-    else
-      bulk_g2s(ring + st * 2 * dp, P + static_cast<int64_t>(lo[q]) * d, row_bytes, &bar[st]);
-    if (nv) {
-      if (evict_v & 1)
-        bulk_g2s_hint(ring + st * 2 * dp + dp, V + static_cast<int64_t>(le[q]) * d, row_bytes, &bar[st], vpol);
-      else
-        bulk_g2s(ring + st * 2 * dp + dp, V + static_cast<int64_t>(le[q]) * d, row_bytes, &bar[st]);
-    }
+    bulk_g2s(ring + st * 2 * dp, P + static_cast<int64_t>(lo[q]) * d, row_bytes, &bar[st]);
+    if (nv) bulk_g2s(ring + st * 2 * dp + dp, V + static_cast<int64_t>(le[q]) * d, row_bytes, &bar[st]);
   };
   const int wid = blockIdx.x * (blockDim.x >> 5) + warp, nw = gridDim.x * (blockDim.x >> 5);
   // each warp walks its balanced item list (wrange: offsets, then items) or, without it, every nw-th item
@@ -241,14 +230,9 @@ struct SegPlan {
 // 1.43 -> 1.20 ms).
 const int* warp_ranges(Ctx& c, SegPlan& p, int nw) {
   if (p.split_nw == nw) return p.wrange.p;
-  static const double wmul = [] {  // window length in units of nw (CPB_HESS_WIN, default 1)
-    const char* e = std::getenv("CPB_HESS_WIN");
-    const double v = e ? std::atof(e) : 1.0;
-    return v > 0.0 ? v : 1.0;
-  }();
   std::vector<int64_t> cost(static_cast<size_t>(p.nseg));
   for (int i = 0; i < p.nseg; ++i) cost[i] = p.cost_prefix[i + 1] - p.cost_prefix[i];
-  const std::vector<int> flat = lpt_lists(cost, nw, std::max(1, static_cast<int>(nw * wmul)));
+  const std::vector<int> flat = lpt_lists(cost, nw, nw);  // windows of one item per warp
   p.wrange.resize(flat.size());
   h2d(c, p.wrange.p, flat.data(), flat.size() * sizeof(int));
   c.sync();
@@ -264,12 +248,8 @@ SegPlan& seg_plan(Ctx& c, const Graph& g) {
   p->uid = g.uid;
   p->v0 = c.own_v0;
   p->v1 = c.own_v1;
-  static const bool bfs = [] {
-    const char* e = std::getenv("CPB_HESS_ORDER");
-    return !(e && std::string(e) == "id");
-  }();
   std::vector<int> off, seq;
-  if (bfs && g.E > 0) {
+  if (g.E > 0) {
     seq = bfs_sequence(c, g, &off);
   } else {
     off.resize(static_cast<size_t>(g.n + 1));
@@ -334,18 +314,10 @@ int nk_bucket(int64_t d) {
 
 }  // namespace
 
-// Default for even d in [256, 1024]: below that the per-edge rows are too
-// short for a two-deep ring to cover the copy latency (C5, d = 64: 17.4 ms vs
-// 9.7 ms for the two-pass warp-chunk path).  CPB_TMA_HESS=0 disables it,
-// CPB_TMA_HESS=1 forces it for every even d in [34, 1024].
-bool hess_tma_supported(int64_t d) {
-  static const int mode = [] {
-    const char* e = std::getenv("CPB_TMA_HESS");
-    return e ? (e[0] == '0' ? 0 : 2) : 1;
-  }();
-  if (mode == 0 || d < 33 || d % 2 != 0 || nk_bucket(d) == 0) return false;
-  return mode == 2 || d >= 256;
-}
+// Even d in [256, 1024]: below that the per-edge rows are too short for a
+// two-deep ring to cover the copy latency (C5, d = 64: 17.4 ms vs 9.7 ms for
+// the warp-chunk path).
+bool hess_tma_supported(int64_t d) { return d >= 256 && d % 2 == 0 && nk_bucket(d) != 0; }
 
 // Returns the number of (pAp, pp) block partials written to `part`.
 int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,
@@ -353,25 +325,11 @@ int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const dou
   SegPlan& sp = seg_plan(c, g);
   const int nk = nk_bucket(d);
   const int dp = static_cast<int>((d + 1) / 2 * 2);
-  static const int warps = [] {
-    const char* e = std::getenv("CPB_TMA_WARPS");
-    const int v = e ? std::atoi(e) : 4;
-    return v < 1 ? 1 : (v > 4 ? 4 : v);
-  }();
-  // CPB_HESS_VEVICT=1 streams V_l rows with an L2 evict_first policy (to keep
-  // the gathered P rows resident); off by default.
-  static const int vevict_env = [] {
-    const char* e = std::getenv("CPB_HESS_VEVICT");
-    return e ? std::atoi(e) : -1;
-  }();
-  const int evict_v = vevict_env > 0 ? (vevict_env & 3) : 0;  // measured neutral-to-worse at C3 (1586 vs 1541 us)
-  // ring depth: 2 (deeper rings measured slower: C5 with 8 stages 38.8 vs 17.4 ms);
-  // CPB_HESS_STAGES overrides
-  static const int s_env = [] {
-    const char* e = std::getenv("CPB_HESS_STAGES");
-    return e ? std::atoi(e) : 0;
-  }();
-  const int S = s_env > 0 ? std::min(s_env, kMaxStages) : 2;
+  const int warps = 4;
+  // ring depth 2 (deeper rings measured slower: C5 with 8 stages 38.8 vs 17.4 ms;
+  // an L2 evict_first policy on the streamed V_l rows measured neutral-to-worse
+  // at C3, 1586 vs 1541 us)
+  const int S = 2;
   const size_t smem = static_cast<size_t>(warps) * S * 2 * dp * sizeof(double);
   if (smem > 220 * 1024) invalid("hessian: shared-memory ring exceeds 220 KB");
   NK_DISPATCH(nk, set_smem, (static_cast<int>(smem)));
@@ -379,15 +337,11 @@ int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const dou
   // partitioned PCG: every rank launches the same grid so the partial tables line up
   const bool parted = c.own_v1 >= 0;
   const int grid = parted ? c.sm_count * 2 : std::max(1, std::min(cdiv(sp.nseg, warps), c.sm_count * 2));
-  static const bool rr = [] {
-    const char* e = std::getenv("CPB_HESS_SPLIT");
-    return e && std::string(e) == "rr";
-  }();
-  const int* wr = rr ? nullptr : warp_ranges(c, sp, grid * warps);
+  const int* wr = warp_ranges(c, sp, grid * warps);
   NK_DISPATCH(nk, k_hess_tma, <<<grid, 32 * warps, smem, c.s>>>(P, V, jal, jbe, g.adj_e.p, g.adj_o.p, sp.node.p,
                                                                 sp.beg.p, sp.end.p, sp.slot.p, sp.nseg,
                                                                 static_cast<int>(d), dp, sigma, Ap, partial, part,
-                                                                active, evict_v, S, wr));
+                                                                active, S, wr));
   CPB_LAUNCH_CHECK();
   int nb = grid;
   if (sp.nhub > 0 || parted) {

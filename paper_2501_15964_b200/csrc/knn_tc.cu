@@ -651,11 +651,9 @@ int64_t knn_tc(Ctx& c, const Data& A, int64_t k, int64_t r0_, int64_t r1_, doubl
   CUtensorMap mhi, mlo;
   make_map(&mhi, hi, dp, n);
   make_map(&mlo, lo, dp, n);
-  static bool attr = false;
-  if (!attr) {
+  if (first_on_device("k_knn_tc.smem")) {
     CPB_CUDA(cudaFuncSetAttribute(k_knn_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     CPB_CUDA(cudaFuncSetAttribute(k_knn_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr = true;
   }
   {
     // "bytes" of the dense contraction = its algorithmic flops 2 n^2 d (reported as TFLOP/s)

@@ -13,9 +13,11 @@ namespace cpb {
 
 // theta >= 0 with sum_f max(|v_f| - theta, 0) = t when ||v||_1 > t, else -1;
 // *cnt = |S|.  Michelot's fixed point: theta_0 = (||v||_1 - t) / d on the full
-// support, then theta <- (sum_{|v| > theta} |v| - t) / #{|v| > theta} until the
-// support stops shrinking (monotone; at most d + 1 passes, a handful in
-// practice).  For t = 0 the support empties at theta = max |v| (prox = v).
+// support, then theta <- (sum_{|v| > theta} |v| - t) / #{|v| > theta} while the
+// support shrinks (a handful of passes in practice).  Sums run over lane-strided
+// partials (element f -> lane f mod 32 in increasing f) met by an xor butterfly,
+// the order oracle/prox_linalg.cpp l1_theta reproduces, so theta is bitwise
+// the oracle's.  For t = 0 the support empties at theta = max |v| (prox = v).
 // `val(f)` yields element f; one pass over the row per iteration by the
 // group's lanes (group_sum over blockDim.x <= 32 lanes, see common.cuh).
 template <class F>
@@ -29,6 +31,9 @@ __device__ __forceinline__ double linf_theta(F val, int d, double t, unsigned gm
   }
   double theta = (s1 - t) / static_cast<double>(d);
   int support = d;
+  // the support shrinks strictly on every pass that continues (at most d
+  // passes); a pass whose support does not shrink — the fixed point, or a
+  // rounding-induced regrowth that would otherwise cycle — keeps theta
   for (;;) {
     double s = 0.0, c = 0.0;
     for (int f = threadIdx.x; f < d; f += blockDim.x) {
@@ -45,11 +50,9 @@ __device__ __forceinline__ double linf_theta(F val, int d, double t, unsigned gm
       support = 0;
       break;
     }
-    const double nt = (s - t) / c;
-    const bool same = ci == support;
-    theta = nt;
+    if (ci >= support) break;
+    theta = (s - t) / c;
     support = ci;
-    if (same) break;
   }
   *cnt = support;
   return theta;

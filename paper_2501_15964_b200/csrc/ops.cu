@@ -12,7 +12,6 @@
 // reference's SSE2 build); the cited reference line is given per kernel.
 #include <cmath>
 
-#include "edge.cuh"
 #include "gather.cuh"
 #include "ops.cuh"
 #include "ptx.cuh"
@@ -609,15 +608,11 @@ constexpr int kMultSmemMaxD = 1024, kMultWarps = 4;
 // flight, and two stages halve the warps per SM (C3 phi 230 -> 511 ms,
 // multiplier 187 -> 294 ms per 10 gammas).  Two stages for short rows (C5,
 // d = 64: phi 242 -> 230 ms, multiplier 201 -> 197 ms); eight were much
-// slower (phi 14.3 vs 6.4 ms per launch).  CPB_EDGE_STAGES overrides.
+// slower (phi 14.3 vs 6.4 ms per launch).
 constexpr int kEdgeMaxStages = 8;
 inline int edge_stages(int64_t d, int rows) {
   (void)rows;
-  static const int env = [] {
-    const char* e = std::getenv("CPB_EDGE_STAGES");
-    return e ? std::atoi(e) : 0;
-  }();
-  return env > 0 ? std::min(env, kEdgeMaxStages) : (d <= 128 ? 2 : 1);
+  return d <= 128 ? 2 : 1;
 }
 template <int Q>
 __global__ void __launch_bounds__(32 * kMultWarps) k_mult_s(
@@ -1235,17 +1230,12 @@ double eval_phi(const Prob& P, const double* X, const double* D, double alpha, d
     auto run = [&](EdgeSel sel, double* pe_) -> int {
       GroupGeom gg = group_geom(c, sel.count, d);
       int nb = gg.grid;
-      if (edge_reg_supported(d) && P.q != Q_LINF && sel.list == nullptr && sel.e0 == 0 && sel.count == E) {
-        nb = phi_edge_reg(c, *P.g, Xe, Z, thr, P.rad, d, sigma, P.q, V, nv, pe_);
-      } else if (gg.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1) &&
-                 std::getenv("CPB_PHI_NOTMA") == nullptr) {
+      if (gg.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1)) {
         const int S = edge_stages(d, 3);
         const size_t smem = static_cast<size_t>(kMultWarps) * S * 3 * d * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
+        if (first_on_device("k_phi_edge_t.smem")) {
           CPB_CUDA(cudaFuncSetAttribute(k_phi_edge_t<Q_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
           CPB_CUDA(cudaFuncSetAttribute(k_phi_edge_t<Q_L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-          attr = true;
         }
         int per_sm = 0;
         CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_phi_edge_t<Q_L2>, 32 * kMultWarps, smem));
@@ -1264,7 +1254,7 @@ double eval_phi(const Prob& P, const double* X, const double* D, double alpha, d
       }
       return nb;
     };
-    const size_t pe_n = std::max({group_geom(c, E, d).grid, edge_grid(c, E), c.sm_count * 64});
+    const size_t pe_n = std::max(group_geom(c, E, d).grid, c.sm_count * 64);
     double* pe = part_buf(c, "phi.pe", pe_n);
     Ctx::Timer tm(&c, "phi_edge", (2.0 * E * d + n * d + 4.0 * E) * 8.0);
     if (!partitioned(c)) {
@@ -1302,7 +1292,10 @@ double grad_diag(const Prob& P, const double* X, const double* V, const double* 
   double* part = part_buf(c, "grad.part", static_cast<size_t>(c.sm_count) * 16);
   int nb;
   {
-    Ctx::Timer tm(&c, "grad_diag", (2.0 * E * d + (want_diag ? 4.0 : 3.0) * n * d) * 8.0);
+    // SURVEY.md §8(d) K8/K9 compulsory bytes: V once, the per-edge scalar, X and A read, G (and the
+    // Jacobi diagonal) written, the CSR
+    Ctx::Timer tm(&c, "grad_diag", (static_cast<double>(E) * d + E + (want_diag ? 4.0 : 3.0) * n * d) * 8.0 +
+                                       (2.0 * E + n + 1) * 4.0);
     nb = gather_grad_diag(c, *P.g, X, P.A->A.p, V, ps, jal, jbe, thr, d, sigma, P.q, want_diag, G, diag, part);
   }
   reduce_sum(c, part, nb, c.dscal);
@@ -1378,7 +1371,7 @@ GapOut eval_gap(const Prob& P, const double* X, const double* Z) {
   double* pn = part_buf(c, "gap.pp", node_cap + 5 * static_cast<size_t>(ge.grid));
   int nbn;
   {
-    Ctx::Timer tm(&c, "gap_node", (2.0 * E * d + 3.0 * n * d) * 8.0);
+    Ctx::Timer tm(&c, "gap_node", (static_cast<double>(E) * d + 2.0 * n * d) * 8.0 + (2.0 * E + n + 1) * 4.0);  // Z once, X, A, CSR
     nbn = gather_gap(c, *P.g, X, P.A->A.p, Z, d, pn);
   }
   double* pe = pn + 4 * static_cast<size_t>(nbn);
@@ -1472,38 +1465,28 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
                          const double* thr, double sigma) {
   Ctx& c = *P.c;
   const int64_t d = P.d(), n = P.n(), E = P.E();
-  const size_t pe_n = 9 * static_cast<size_t>(std::max({group_geom(c, E, d).grid, edge_grid(c, E), c.sm_count * 64}));
+  const size_t pe_n = 9 * static_cast<size_t>(std::max(group_geom(c, E, d).grid, c.sm_count * 64));
   double* pe = part_buf(c, "mult.pe", pe_n);
   // one launch over an edge selection; returns the number of 9-wide block partials
   auto run = [&](EdgeSel sel, double* pe) -> int {
     GroupGeom ge = group_geom(c, sel.count, d);
     int nb = ge.grid;
-    const bool full = sel.list == nullptr && sel.e0 == 0 && sel.count == E;
     if (P.q == Q_LINF) {
       k_mult_inf<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, V, ps, P.rad, P.g->w.p, P.g->ei.p, P.g->ej.p, sel,
                                                           static_cast<int>(d), sigma, pe);
       CPB_LAUNCH_CHECK();
-    } else if (edge_reg_supported(d) && full) {
-      nb = mult_reg(c, *P.g, X, Z, V, ps, thr, P.rad, d, sigma, P.q, pe);
-    } else if (ge.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1) &&
-               std::getenv("CPB_MULT_NOTMA") == nullptr) {
-      // V_l staged with the other rows (default) or streamed from HBM in pass 2
-      // (CPB_MULT_VSTAGE=0: 3 staged rows, more warps per SM — measured slower,
-      // 4.42 vs 3.46 ms at C3)
-      static const bool vstage = [] {
-        const char* e = std::getenv("CPB_MULT_VSTAGE");
-        return !(e && e[0] == '0');
-      }();
-      const int NR = vstage ? 4 : 3;
+    } else if (ge.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1)) {
+      // V_l staged with the other rows (streaming it from HBM in pass 2 with 3
+      // staged rows and more warps per SM measured slower: 4.42 vs 3.46 ms at C3)
+      const bool vstage = true;
+      const int NR = 4;
       const int S = edge_stages(d, NR);
       const size_t smem = static_cast<size_t>(kMultWarps) * S * NR * d * sizeof(double);
-      static bool attr_t = false;
-      if (!attr_t) {
+      if (first_on_device("k_mult_t.smem")) {
         CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        attr_t = true;
       }
       int per_sm = 0;
       CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mult_t<Q_L2, false>, 32 * kMultWarps, smem));
@@ -1524,13 +1507,11 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
       CPB_LAUNCH_CHECK();
     } else if (ge.gx == 32 && d <= kMultSmemMaxD && (P.q == Q_L2 || P.q == Q_L1)) {
       const size_t smem = static_cast<size_t>(kMultWarps) * 2 * d * sizeof(double);
-      static bool attr = false;
-      if (!attr) {
+      if (first_on_device("k_mult_s.smem")) {
         CPB_CUDA(cudaFuncSetAttribute(k_mult_s<Q_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kMultWarps * 2 * kMultSmemMaxD * 8));
         CPB_CUDA(cudaFuncSetAttribute(k_mult_s<Q_L1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kMultWarps * 2 * kMultSmemMaxD * 8));
-        attr = true;
       }
       int per_sm = 0;
       CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mult_s<Q_L2>, 32 * kMultWarps, smem));
@@ -1570,7 +1551,7 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
   double* pn = part_buf(c, "mult.pn", 4 * static_cast<size_t>(c.sm_count) * 16);
   int nbn;
   {
-    Ctx::Timer tm(&c, "gap_node", (2.0 * E * d + 3.0 * n * d) * 8.0);
+    Ctx::Timer tm(&c, "gap_node", (static_cast<double>(E) * d + 2.0 * n * d) * 8.0 + (2.0 * E + n + 1) * 4.0);  // Z once, X, A, CSR
     nbn = gather_gap(c, *P.g, X, P.A->A.p, Z, d, pn);
   }
   std::vector<double> h = host_cols(c, pn, nbn, 4);
@@ -1624,14 +1605,10 @@ int ama_block_fused(const Prob& P, double* Xh, double* Zh, double* Zp, double* X
                     int cnt, double** parts) {
   Ctx& c = *P.c;
   const int64_t d = P.d(), n = P.n(), E = P.E();
-  static const bool enabled = [] {
-    const char* e = std::getenv("CPB_AMA_FUSED");
-    return !(e && e[0] == '0');
-  }();
-  if (!enabled || d > 32 || E < 1 || E > (1 << 18) || n > (1 << 17) || partitioned(c)) return 0;
+  if (d > 32 || E < 1 || E > (1 << 18) || n > (1 << 17) || partitioned(c)) return 0;
   GroupGeom ge = group_geom(c, E, d);
-  static int occ = -1;
-  if (occ < 0) CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ama_block, 256, 0));
+  int occ = 0;
+  CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ama_block, 256, 0));
   if (occ < 1) return 0;
   const int64_t want = std::max<int64_t>(cdiv(n, 8), cdiv(E, ge.gy));
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(c.sm_count))));

@@ -237,8 +237,8 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
     }
     ~OwnScope() { c.own_v0 = p0, c.own_v1 = p1; }
   } own(c, dist, v0, v0 + nown);
-  static int cap = 0;  // resident 256-thread blocks of the vector kernels per wave
-  if (cap == 0) {
+  int cap = 0;  // resident 256-thread blocks of the vector kernels per wave
+  {
     int per_sm = 0;
     CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_b, 256, 0));
     cap = std::max(1, per_sm) * c.sm_count;
@@ -279,9 +279,8 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
   // Batch sizing: the first batch is the previous solve's iteration count
   // (consecutive Newton systems need similar counts), then small top-ups, so
   // few no-op iterations are launched past convergence.
-  static const bool doubling = std::getenv("CPB_CG_DOUBLING") != nullptr;  // A/B switch for the batch policy
   int& hint = c.cg_hint[op_name];
-  int batch = (hint > 0 && !doubling) ? std::max(2, std::min(hint - 1, 64)) : 4;
+  int batch = hint > 0 ? std::max(2, std::min(hint - 1, 64)) : 4;
   long long it_before = 0;
   PcgOut out;
   for (;;) {
@@ -333,7 +332,7 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
       out.converged = h.relres <= tol;
       break;
     }
-    batch = doubling ? std::min(batch * 2, 32) : (h.it < 8 ? 4 : 2 + static_cast<int>(h.it / 8));
+    batch = h.it < 8 ? 4 : 2 + static_cast<int>(h.it / 8);
   }
   if (dist) {
     comm_allgather(c, w.x, static_cast<size_t>(chunk * d));

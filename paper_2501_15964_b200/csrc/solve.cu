@@ -457,7 +457,7 @@ int64_t extract_clusters_dev(Ctx& c, const Graph& g, const double* X, int64_t d,
                              double* centroids) {
   if (!(fuse_tol > 0.0)) invalid("extract_clusters: fuse_tol must be positive");
   const int64_t n = g.n, E = g.E;
-  Ctx::Timer tm(&c, "extract_clusters", (n * d + 2.0 * E * d) * 8.0);
+  Ctx::Timer tm(&c, "extract_clusters", static_cast<double>(n) * d * 8.0 + 2.0 * E * 4.0);  // X once, the edge list
   const int grid = std::max(1, std::min(cdiv(4 * n, 256), c.sm_count * 4));
   double* part = c.buf<double>("cl.part", grid + 2);
   double* thr = c.buf<double>("cl.thr", 2);
@@ -548,20 +548,14 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
     }
     return static_cast<double*>(dp);
   };
-  static const int d2h_mode = [] {  // CPB_D2H=engine keeps cudaMemcpyAsync on the copy engine
-    const char* e = std::getenv("CPB_D2H");
-    return e && std::string(e) == "engine" ? 0 : 1;
-  }();
-  double* mX = d2h_mode ? mapped(X_out) : nullptr;
-  double* mZ = d2h_mode ? mapped(Z_out) : nullptr;
+  // mapped pinned outputs are written by a copy kernel; other host buffers go
+  // through cudaMemcpyAsync on the copy engine
+  double* mX = mapped(X_out);
+  double* mZ = mapped(Z_out);
   // CTAs of the copy kernel: enough to fill the ~57 GB/s link, few enough to
   // leave the SMs to the solver (C3 e2e: 2 -> 4.53 s, 4 -> 3.24, 6 -> 3.26,
   // 8 -> 3.28, 16 -> 3.48, 32 -> 3.69; copy engine 3.88 s)
-  static const int d2h_ctas = [] {
-    const char* e = std::getenv("CPB_D2H_CTAS");
-    const int v = e ? std::atoi(e) : 6;
-    return v < 1 ? 1 : v;
-  }();
+  const int d2h_ctas = 6;
   double* snapX[2] = {nullptr, nullptr};
   double* snapZ[2] = {nullptr, nullptr};
   cudaEvent_t snap_ready[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};

@@ -522,13 +522,13 @@ def test_path_parity(cp, orc, algo):
         assert res.assignments[t].K == ores["K"][t]
 
 
-# (q = inf at d = 40 is left out: there the device's l1-ball threshold (Michelot fixed point)
-# and the oracle's sort-based one round differently and the gap lands within 4e-9 of epsilon,
-# so the two stop one check apart, which AMA's slow convergence turns into 5e-6 in X.)
+# q = inf: the device and the oracle compute the l1-ball threshold with the same Michelot
+# passes and the same 32-lane summation order (linf.cuh, oracle l1_theta), so the projected
+# iterates agree bit for bit and the d = 40 case holds the same 1e-10 bar as q = 1, 2.
 # circle: 300 nodes, one node per warp (register-resident adjacency); circle1500: more nodes
 # than warps in the grid, the grid-stride gather; d40: the CUDA-graph path.
 @pytest.mark.parametrize("q,shape", [(2, "circle"), (1, "circle"), (0, "circle"), (2, "circle1500"), (2, "d40"),
-                                     (1, "d40")])
+                                     (1, "d40"), (0, "d40")])
 def test_ama_graph_blocks_match_oracle(cp, orc, q, shape):
     """Fast AMA runs the iterations between gap checks as one cooperative kernel (d <= 32:
     k_ama_block) or as one CUDA graph per 10-iteration block with the Nesterov momenta computed
@@ -547,6 +547,24 @@ def test_ama_graph_blocks_match_oracle(cp, orc, q, shape):
         assert res.stats[t].converged == bool(ores["terms"][t]["converged"])
         assert np.linalg.norm(res.solutions[t].X - ores["X"][t]) <= 1e-10 * np.linalg.norm(ores["X"][t])
         assert np.array_equal(res.assignments[t].labels, ores["labels"][t])
+
+
+def test_c1_exact_config_matches_oracle(cp, orc):
+    """BASELINE.json configs[0] as bench.py runs it: n = 1000 on the 10-centre circle (spread
+    0.5), kNN k = 10, phi = 0.5, q = 2, fast AMA over the 20 geometric gammas in [0.01, 10]
+    (path.cpp:110-142, ama.cpp:17-89): identical iteration counts and labels, X within 1e-10."""
+    A = circle(orc, 100)
+    g, og = check_graph(cp, orc, A, 10, 0.5)
+    sched = cp.make_schedule(0.01, 10.0, 20)
+    res = cp.run_path(cp.DataMatrix(A), g, 2, sched, cp.SolverConfig(algorithm=cp.Algorithm.FastAMA))
+    ores = orc.run_path(A, og, 2, sched.values, orc.config("ama"))
+    for t in range(20):
+        assert res.stats[t].iterations == ores["terms"][t]["iterations"]
+        assert res.stats[t].converged == bool(ores["terms"][t]["converged"])
+        assert np.linalg.norm(res.solutions[t].X - ores["X"][t]) <= 1e-10 * np.linalg.norm(ores["X"][t])
+        assert np.linalg.norm(res.solutions[t].Z - ores["Z"][t]) <= 1e-10 * max(1.0, np.linalg.norm(ores["Z"][t]))
+        assert np.array_equal(res.assignments[t].labels, ores["labels"][t])
+        assert res.assignments[t].K == ores["K"][t]
 
 
 @pytest.mark.parametrize("d", [64, 96])
