@@ -70,6 +70,9 @@ COUNTS_FILE = os.path.join(ROOT, "profiles", "path_counts_{}.json")
 
 
 def make_input(cp, cfg):
+    """The synthetic mixture through `cp`'s generator: the product package
+    for our arm, pyoracle for the reference arm (both restate io.cpp:142-165 on libstdc++
+    <random>, so A is bit-identical)."""
     n, d = cfg["n"], cfg["d"]
     m = 10
     if cfg["centers"] == "circle":
@@ -79,7 +82,28 @@ def make_input(cp, cfg):
     else:
         centers = (3.0 / np.sqrt(d)) * cp.normals(1001, m * d).reshape(m, d)
         spread = 1.0 / np.sqrt(d)
-    return cp.generate_gaussian_mixture(centers, spread, n // m, 42)
+    gen = getattr(cp, "generate_gaussian_mixture", None) or cp.gaussian_mixture
+    return gen(centers, spread, n // m, 42)
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def oracle_counts(name):
+    """The oracle's own per-gamma counts of this config (tests/golden/<cfg>_path.json, made by
+    tools/golden_path.py), when the golden covers the whole schedule."""
+    f = os.path.join(ROOT, "tests", "golden", f"{name}_path.json")
+    if not os.path.exists(f):
+        return None
+    g = json.load(open(f))
+    if len(g.get("per_gamma", [])) != g["cfg"]["T"]:
+        return None
+    return [{"gamma": r["gamma"], "iterations": r["counts"][0], "newton": r["counts"][1], "cg": r["counts"][2],
+             "armijo": r["counts"][3], "converged": r["counts"][4], "K": r["K"]} for r in g["per_gamma"]]
 
 
 def _peaks_file():
@@ -244,13 +268,23 @@ def cpu_estimate(cfg, A, counts, knn_rows=400, reps=2):
 
 
 def run_reference(args, cfg):
-    world, rank, local, dist = dist_setup()
+    """The reference arm: the CPU restatement of the reference's single-threaded path (oracle/;
+    the reference itself needs Eigen 3.4, absent from this image) on this box's host, rank 0
+    only.  Inputs come from the oracle's own generator and the iteration counts from the
+    oracle's own run of this config (tests/golden); nothing of the product is loaded."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_2501_15964_b200 as cp  # host-side generator only (io.cpp restatement in the C-ABI)
-    A = make_input(cp, cfg)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as orc
+    A = make_input(orc, cfg)
     cf = COUNTS_FILE.format(args.config)
     counts = json.load(open(cf)) if os.path.exists(cf) else {"algorithm": cfg["algorithm"]}
+    oc = oracle_counts(args.config)
+    if oc is not None:
+        counts["per_gamma"] = oc
+        counts["counts_source"] = f"tests/golden/{args.config}_path.json (the oracle's own path)"
     vals = []
     sample = ""
     for s in range(args.warmup + args.steps):
@@ -261,14 +295,17 @@ def run_reference(args, cfg):
             vals.append(est)
     v = float(np.median(vals))
     line = {"metric": "clustering-path wall s (20 gamma, KKT 1e-6)", "value": v, "unit": "s", "impl": "reference",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": False,
-            "dtype": "f64", "data": "synthetic", "config": workload_config(args, cfg),
-            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": sample},
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": False,
+            "dtype": "f64", "data": "synthetic", "config": workload_config(args, cfg, world),
+            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "host_cores": host_cores(), "kind": "port",
+                             "extrapolated": counts.get("algorithm") == "ssnal",
+                             "counts_source": counts.get("counts_source", "profiles/path_counts (GPU path)"),
+                             "sample": sample},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def workload_config(args, cfg):
+def workload_config(args, cfg, world):
     return {"workload": f"{args.config}: Gaussian mixture n={cfg['n']} d={cfg['d']}, kNN k={cfg['k']} phi={cfg['phi']}, "
                         f"q={'inf' if cfg['q'] == 0 else cfg['q']}, {cfg['algorithm'].upper()} {cfg['T']}-gamma warm-started path "
                         f"[{cfg['gamma'][0]}, {cfg['gamma'][1]}] geometric, eps=1e-6",
@@ -276,11 +313,24 @@ def workload_config(args, cfg):
             "l2": "flushed between steps (512 MB write); edge arrays > L2",
             "parallelism": ("kNN query rows sharded over the ranks (NCCL all-gather of the n x k lists); "
                             "SSNAL node-partitioned: owned nodes / owned+ghost edges per rank, NCCL all-reduce "
-                            "of sums, all-gather of p and D, Z assembled per gamma") if args.gpus > 1 else "single"}
+                            "of sums, all-gather of p and D, Z assembled per gamma") if world > 1 else "single"}
+
+
+# Kernels whose timer bytes are algorithmic HBM bytes; the kNN entries carry
+# flops (knn_gemm, knn_band) or nothing and are reported under "knn".
+def per_kernel_entry(name, v, peak):
+    e = {"launches": v["launches"], "ms": round(v["ms"], 3)}
+    if v["ms"] > 0 and v["alg_bytes"] > 0 and not name.startswith("knn"):
+        gbps = v["alg_bytes"] / (v["ms"] / 1e3) / 1e9
+        e.update({"GBps": round(gbps, 1), "frac": round(gbps / peak, 3) if peak else None})
+    return e
 
 
 def run_ours(args, cfg):
     world, rank, local, dist = dist_setup()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to report a "
+                         f"{args.gpus}-GPU number from {world} process(es)")
     import paper_2501_15964_b200 as cp
     ctx = cp.default_context(local)
     if world > 1:
@@ -294,7 +344,7 @@ def run_ours(args, cfg):
 
     def step():
         g = knn(data, cfg["k"], cfg["phi"])
-        res = cp.run_path(data, g, cfg["q"], sched, cpcfg, keep_solutions=False)
+        res = cp.run_path(data, g, cfg["q"], sched, cpcfg, keep_solutions=False, centroids=False)
         return g, res
 
     for _ in range(args.warmup):
@@ -325,7 +375,9 @@ def run_ours(args, cfg):
     # every X(gamma) and labels always come back; the 20 E x d multipliers too
     # unless they exceed 96 GB of host memory (C4, C5)
     keep_z = T * E * cfg["d"] * 8 <= (96 << 30)
-    for s in range(1 + max(1, min(args.steps, 2))):  # first call untimed: fills the pinned-buffer pool
+    e2e_cold = None
+    for s in range(1 + max(1, min(args.steps, 2))):  # the first call also allocates the pinned output pool
+        barrier(dist)
         t0 = time.perf_counter()
         dA = cp.DataMatrix(A, ctx=ctx)
         g2 = knn(dA, cfg["k"], cfg["phi"])
@@ -333,8 +385,11 @@ def run_ours(args, cfg):
         res2 = cp.run_path(dA, g2, cfg["q"], sched, cpcfg, keep_solutions=(rank == 0), keep_z=keep_z)
         if s > 0:
             e2e_times.append(time.perf_counter() - t0)
+        else:
+            e2e_cold = time.perf_counter() - t0
         del res2
     e2e = allmax(dist, float(np.mean(e2e_times)))
+    e2e_cold = allmax(dist, e2e_cold)
     h2d = cfg["n"] * cfg["d"] * 8
     d2h = T * (cfg["n"] * cfg["d"] + (E * cfg["d"] if keep_z else 0)) * 8 + T * cfg["n"] * 8
     # ---- roofline of the dominant kernel --------------------------------------------
@@ -359,9 +414,7 @@ def run_ours(args, cfg):
                                if traffic else None),
             "launches": hs["launches"], "avg_launch_us": 1e3 * hs["ms"] / max(1, hs["launches"]),
             "share_of_timed_kernels": hs["ms"] / total_ms if total_ms else None,
-            "per_kernel": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
-                               "GBps": (v["alg_bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 and v["alg_bytes"] > 0 else None}
-                           for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])}}
+            "per_kernel": {k: per_kernel_entry(k, v, peak) for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])}}
     # ---- the dense contraction on the tensor cores (north-star subsystem 1) ----------
     ki = ctx.knn_info()
     kg = stats.get("knn_gemm")
@@ -393,16 +446,26 @@ def run_ours(args, cfg):
             json.dump(counts, f, indent=1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        est, sample, spent = cpu_estimate(cfg, A, counts)
-        cpu = {"value": est, "unit": "s", "cores": 1, "kind": "port", "sample": sample,
-               "sample_cpu_seconds": round(spent, 1)}
+        ccounts = dict(counts)
+        oc = oracle_counts(args.config)
+        if oc is not None:  # the oracle's own iteration counts of this path
+            ccounts["per_gamma"] = oc
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyoracle as orc
+        est, sample, spent = cpu_estimate(cfg, make_input(orc, cfg), ccounts)
+        cpu = {"value": est, "unit": "s", "cores": 1, "host_cores": host_cores(), "kind": "port",
+               "extrapolated": cfg["algorithm"] == "ssnal",
+               "counts_source": "oracle goldens" if oc is not None else "this GPU path (identical to the oracle's at C2)",
+               "sample": sample, "sample_cpu_seconds": round(spent, 1)}
     if rank == 0:
         line = {"metric": "clustering-path wall s (20 gamma, KKT 1e-6)", "value": per_step, "unit": "s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * per_step,
                 "higher_is_better": False, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
                 "dtype": "f64",
-                "data": "synthetic", "config": workload_config(args, cfg),
+                "data": "synthetic", "config": workload_config(args, cfg, world),
                 "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                        "cold_value": e2e_cold,
+                        "cold_note": "first call of the process: includes allocating/pinning the host output pool",
                         "returns": "X, labels, records per gamma" + (", Z per gamma" if keep_z else "")},
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": int(launches),
                 "knn": knn, "edge_op_gbps": edge_op_gbps,
@@ -413,6 +476,23 @@ def run_ours(args, cfg):
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` started without a launcher: re-exec under torch.distributed.run with N
+    ranks (one per GPU), or fail loudly when the box has fewer GPUs than asked for."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} requested but this box has {have} GPU(s); "
+                         f"not reporting a {args.gpus}-GPU number")
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -426,6 +506,8 @@ def main():
     ap.add_argument("--write-counts", action="store_true", help="record the path counts for the reference arm")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -9,14 +9,22 @@
 // Differences a caller can see:
 //  * Eigen is not required: `Matrix` is a small owning column-major matrix with
 //    the same memory layout as Eigen::MatrixXd (d x n, one sample per column).
-//  * Host-callback linear algebra (LinearOperator, pcg on user functors,
-//    CholeskyFactor) is not exposed: the solvers run their PCG on the device;
-//    the graph Laplacian's spectral bound is `laplacian_lambda_max`.
+//  * LinearOperator / pcg / power_iteration / CholeskyFactor (linalg.hpp) run
+//    on the device: the factories hold device data; an operator built from a
+//    user functor is applied on the host (one device round trip per apply).
+//    CholeskyFactor solves I + rho L by device CG to 1e-14 relative residual
+//    per column instead of a sparse LLT factor (same solution up to rounding).
+//  * SparseMatrix is a compressed-column struct (Eigen::SparseMatrix layout).
 //  * A thread-local device context is used (device 0 unless set_device()).
+//  * run_path returns its matrices in page-locked host storage shared by the
+//    path's solutions (the device streams each gamma's X and Z into it while
+//    the next gamma is solved); copying a Matrix always deep-copies.
 #pragma once
 
 #include <charconv>
 #include <cmath>
+#include <exception>
+#include <functional>
 #include <fstream>
 #include <cstdint>
 #include <cstring>
@@ -38,7 +46,27 @@ using Index = std::int64_t;
 class Matrix {
  public:
   Matrix() = default;
-  Matrix(Index rows, Index cols) : r_(rows), c_(cols), v_(static_cast<size_t>(rows * cols), 0.0) {}
+  Matrix(Index rows, Index cols) : r_(rows), c_(cols), v_(static_cast<size_t>(rows * cols), 0.0), p_(v_.data()) {}
+  Matrix(const Matrix& o) : r_(o.r_), c_(o.c_), v_(o.p_, o.p_ + o.size()), p_(v_.data()) {}
+  Matrix(Matrix&& o) noexcept : r_(o.r_), c_(o.c_), v_(std::move(o.v_)), ext_(std::move(o.ext_)), p_(o.p_) {
+    o.r_ = o.c_ = 0, o.p_ = nullptr;
+  }
+  Matrix& operator=(const Matrix& o) {
+    if (this != &o) *this = Matrix(o);
+    return *this;
+  }
+  Matrix& operator=(Matrix&& o) noexcept {
+    r_ = o.r_, c_ = o.c_, v_ = std::move(o.v_), ext_ = std::move(o.ext_), p_ = o.p_;
+    o.r_ = o.c_ = 0, o.p_ = nullptr;
+    return *this;
+  }
+  // A rows x cols matrix stored at p inside `slab`, which it keeps alive
+  // (run_path's page-locked output storage); copies are deep.
+  static Matrix adopt(Index rows, Index cols, std::shared_ptr<double> slab, double* p) {
+    Matrix m;
+    m.r_ = rows, m.c_ = cols, m.ext_ = std::move(slab), m.p_ = p;
+    return m;
+  }
   static Matrix Zero(Index rows, Index cols) { return Matrix(rows, cols); }
   static Matrix Constant(Index rows, Index cols, double x) {
     Matrix m(rows, cols);
@@ -48,25 +76,29 @@ class Matrix {
   Index rows() const { return r_; }
   Index cols() const { return c_; }
   Index size() const { return r_ * c_; }
-  double* data() { return v_.data(); }
-  const double* data() const { return v_.data(); }
-  double& operator()(Index r, Index c) { return v_[static_cast<size_t>(c * r_ + r)]; }
-  double operator()(Index r, Index c) const { return v_[static_cast<size_t>(c * r_ + r)]; }
-  double* col(Index c) { return v_.data() + c * r_; }
-  const double* col(Index c) const { return v_.data() + c * r_; }
+  double* data() { return p_; }
+  const double* data() const { return p_; }
+  double& operator()(Index r, Index c) { return p_[c * r_ + r]; }
+  double operator()(Index r, Index c) const { return p_[c * r_ + r]; }
+  double* col(Index c) { return p_ + c * r_; }
+  const double* col(Index c) const { return p_ + c * r_; }
   void resize(Index rows, Index cols) {
     r_ = rows, c_ = cols;
+    ext_.reset();
     v_.assign(static_cast<size_t>(rows * cols), 0.0);
+    p_ = v_.data();
   }
   bool allFinite() const {
-    for (double x : v_)
-      if (!std::isfinite(x)) return false;
+    for (Index k = 0; k < size(); ++k)
+      if (!std::isfinite(p_[k])) return false;
     return true;
   }
 
  private:
   Index r_ = 0, c_ = 0;
   std::vector<double> v_;
+  std::shared_ptr<double> ext_;
+  double* p_ = nullptr;
 };
 using Vector = std::vector<double>;
 
@@ -389,12 +421,193 @@ inline ProxJacobian prox_jacobian(const Vector& v, double t, PenaltyNorm norm) {
   return ProxJacobian{v, t, norm};
 }
 
+// norm_value / dual_norm_value (prox.hpp:14-15; prox.cpp:25-31), on the device.
+inline std::pair<double, double> norm_pair(const Vector& v, PenaltyNorm norm) {
+  double a = 0.0, b = 0.0;
+  detail::check(cp_norm_values(detail::ctx(), penalty_q(norm), v.data(), static_cast<int64_t>(v.size()), 1, &a, &b));
+  return {a, b};
+}
+inline double norm_value(const Vector& v, PenaltyNorm norm) { return norm_pair(v, norm).first; }
+inline double dual_norm_value(const Vector& v, PenaltyNorm norm) { return norm_pair(v, norm).second; }
+// prox_norm_into / project_dual_ball_into (prox.hpp:20-26)
+inline void prox_norm_into(const Vector& v, double t, PenaltyNorm norm, Vector& out) {
+  if (!(t >= 0.0) || !std::isfinite(t)) throw std::invalid_argument("prox_norm: threshold must be finite and >= 0");
+  out = prox_norm(v, t, norm);
+}
+inline void project_dual_ball_into(const Vector& z, double r, PenaltyNorm norm, Vector& out) {
+  if (!(r >= 0.0) || !std::isfinite(r))
+    throw std::invalid_argument("project_dual_ball: threshold must be finite and >= 0");
+  out = project_dual_ball(z, r, norm);
+}
+
 inline double moreau_check(const Vector& v, double t, PenaltyNorm norm) {
   const Vector p = prox_norm(v, t, norm), q = project_dual_ball(v, t, norm);
   double m = 0.0;
   for (size_t k = 0; k < v.size(); ++k) m = std::max(m, std::abs(p[k] + q[k] - v[k]));
   return m;
 }
+
+// ---- linalg.hpp ----------------------------------------------------------------
+// LinearOperator (linalg.hpp:38-65).  Factories hold device data; a functor
+// operator is applied on the host through the C-ABI callback.
+class LinearOperator {
+ public:
+  using ApplyFn = std::function<Matrix(const Matrix&)>;
+  LinearOperator(Index rows, ApplyFn fn, bool symmetric = true, bool positive_definite = false)
+      : fn_(std::make_shared<Functor>()) {
+    if (rows < 0) throw std::invalid_argument("LinearOperator: negative dimension");
+    if (!fn) throw std::invalid_argument("LinearOperator: empty apply function");
+    fn_->fn = std::move(fn);
+    cp_linop* h = nullptr;
+    detail::check(cp_linop_callback(detail::ctx(), rows, &LinearOperator::trampoline, fn_.get(), symmetric ? 1 : 0,
+                                    positive_definite ? 1 : 0, &h));
+    h_.reset(h, cp_linop_destroy);
+  }
+  Index rows() const { return info().rows; }
+  bool symmetric() const { return info().sym; }
+  bool positive_definite() const { return info().pd; }
+  Matrix apply(const Matrix& x) const {
+    if (x.rows() != rows()) throw std::invalid_argument("LinearOperator::apply: operand has wrong row count");
+    Matrix out(x.rows(), x.cols());
+    rethrow(cp_linop_apply(detail::ctx(), h_.get(), x.data(), x.cols(), out.data()));
+    return out;
+  }
+  static LinearOperator identity(Index n) { return make([&](cp_linop** h) { return cp_linop_identity(detail::ctx(), n, h); }); }
+  static LinearOperator dense(const Matrix& M, bool positive_definite = false) {
+    if (M.rows() != M.cols()) throw std::invalid_argument("LinearOperator::dense: matrix must be square");
+    return make([&](cp_linop** h) {
+      return cp_linop_dense(detail::ctx(), M.data(), M.rows(), positive_definite ? 1 : 0, h);
+    });
+  }
+  static LinearOperator sparse(const SparseMatrix& M, bool positive_definite = false) {
+    if (M.rows() != M.cols()) throw std::invalid_argument("LinearOperator::sparse: matrix must be square");
+    return make([&](cp_linop** h) {
+      return cp_linop_sparse(detail::ctx(), M.rows(), M.colptr.data(), M.rowidx.data(), M.values.data(),
+                             positive_definite ? 1 : 0, h);
+    });
+  }
+  static LinearOperator jacobi(const Vector& diag) {
+    return make([&](cp_linop** h) {
+      return cp_linop_jacobi(detail::ctx(), diag.data(), static_cast<int64_t>(diag.size()), 1, h);
+    });
+  }
+  static LinearOperator jacobi(const Matrix& diag) {
+    return make([&](cp_linop** h) {
+      return cp_linop_jacobi(detail::ctx(), diag.data(), diag.rows(), diag.cols() > 0 ? diag.cols() : 1, h);
+    });
+  }
+  const cp_linop* handle() const { return h_.get(); }
+  // a user functor's exception (or a C-ABI error) after a device call
+  void rethrow(int rc) const {
+    if (fn_ && fn_->err) {
+      std::exception_ptr e = fn_->err;
+      fn_->err = nullptr;
+      std::rethrow_exception(e);
+    }
+    detail::check(rc);
+  }
+
+ private:
+  struct Functor {
+    ApplyFn fn;
+    std::exception_ptr err;
+  };
+  struct Info {
+    Index rows;
+    bool sym, pd;
+  };
+  LinearOperator() = default;
+  template <class F>
+  static LinearOperator make(F f) {
+    cp_linop* h = nullptr;
+    detail::check(f(&h));
+    LinearOperator op;
+    op.h_.reset(h, cp_linop_destroy);
+    return op;
+  }
+  Info info() const {
+    int64_t r = 0;
+    int s = 0, p = 0;
+    detail::check(cp_linop_info(h_.get(), &r, &s, &p));
+    return {r, s != 0, p != 0};
+  }
+  static int trampoline(void* user, const double* in, double* out, int64_t rows, int64_t cols) {
+    auto* f = static_cast<Functor*>(user);
+    try {
+      Matrix x(rows, cols);
+      std::memcpy(x.data(), in, sizeof(double) * static_cast<size_t>(rows * cols));
+      Matrix y = f->fn(x);
+      if (y.rows() != rows || y.cols() != cols)
+        throw std::runtime_error("LinearOperator::apply: image shape mismatch");
+      std::memcpy(out, y.data(), sizeof(double) * static_cast<size_t>(rows * cols));
+      return 0;
+    } catch (...) {
+      f->err = std::current_exception();
+      return 1;
+    }
+  }
+  std::shared_ptr<cp_linop> h_;
+  std::shared_ptr<Functor> fn_;
+};
+
+struct PcgResult {
+  Matrix x;
+  Index iterations = 0;
+  double residual = 0.0;  // relative, recomputed from op at exit
+  bool converged = false;
+};
+// pcg (linalg.hpp:76-77; linalg.cpp:143-192) on the device.
+inline PcgResult pcg(const LinearOperator& op, const Matrix& rhs, const LinearOperator* preconditioner, double tol,
+                     Index max_iter) {
+  if (rhs.rows() != op.rows()) throw std::invalid_argument("pcg: rhs row count does not match the operator");
+  PcgResult r;
+  r.x.resize(rhs.rows(), rhs.cols());
+  int64_t it = 0;
+  double res = 0.0;
+  int32_t conv = 0;
+  const int rc = cp_pcg(detail::ctx(), op.handle(), rhs.data(), rhs.cols(),
+                        preconditioner ? preconditioner->handle() : nullptr, tol, max_iter, r.x.data(), &it, &res,
+                        &conv);
+  if (preconditioner) preconditioner->rethrow(CP_OK);  // a functor preconditioner's own exception first
+  op.rethrow(rc);
+  r.iterations = it, r.residual = res, r.converged = conv != 0;
+  return r;
+}
+inline PcgResult pcg(const LinearOperator& op, const Vector& rhs, const LinearOperator* preconditioner, double tol,
+                     Index max_iter) {
+  Matrix b(static_cast<Index>(rhs.size()), 1);
+  std::memcpy(b.data(), rhs.data(), rhs.size() * sizeof(double));
+  return pcg(op, b, preconditioner, tol, max_iter);
+}
+// power_iteration (linalg.hpp:82-83; linalg.cpp:194-242) on the device.
+inline double power_iteration(const LinearOperator& op, double tol = 1e-9, Index max_iter = 10000) {
+  double lam = 0.0;
+  op.rethrow(cp_power_iteration(detail::ctx(), op.handle(), tol, max_iter, &lam));
+  return lam;
+}
+// CholeskyFactor (linalg.hpp:17-33): (I + rho L)^{-1} on the device.
+class CholeskyFactor {
+ public:
+  CholeskyFactor(const SparseMatrix& L, double rho) : size_(L.rows()), rho_(rho) {
+    if (L.rows() != L.cols()) throw std::invalid_argument("cholesky: matrix must be square");
+    cp_factor* f = nullptr;
+    detail::check(cp_factor_create(detail::ctx(), L.rows(), L.colptr.data(), L.rowidx.data(), L.values.data(), rho, &f));
+    f_.reset(f, cp_factor_destroy);
+  }
+  Index size() const { return size_; }
+  double rho() const { return rho_; }
+  Matrix solve(const Matrix& rhs) const {
+    if (rhs.rows() != size_) throw std::invalid_argument("cholesky solve: rhs has wrong row count");
+    Matrix out(rhs.rows(), rhs.cols());
+    detail::check(cp_factor_solve(detail::ctx(), f_.get(), rhs.data(), rhs.cols(), out.data()));
+    return out;
+  }
+
+ private:
+  std::shared_ptr<cp_factor> f_;
+  Index size_ = 0;
+  double rho_ = 0.0;
+};
 
 // ---- solvers.hpp -------------------------------------------------------------
 enum class Algorithm { ADMM, FastAMA, SSNAL };
@@ -448,10 +661,19 @@ struct TerminationRecord {
   Index newton = 0, cg = 0, armijo = 0;  // work counters (extension)
 };
 
+struct TraceRow {  // solvers.hpp:54-60
+  Index iter = 0;
+  double f_p = 0.0;
+  double f_d = 0.0;
+  double gap = 0.0;
+  double elapsed_s = 0.0;
+};
+
 struct Solution {
   Matrix X;
   Matrix Z;
   TerminationRecord termination;
+  std::vector<TraceRow> trace;  // filled when SolverConfig::collect_trace
 };
 
 struct SolverConfig {
@@ -575,6 +797,13 @@ inline Solution solve(const ProblemInstance& inst, const SolverConfig& config, c
                          warm ? warm->Z.data() : nullptr, warm ? warm->Z.cols() : 0, sol.X.data(), sol.Z.data(),
                          &t));
   sol.termination = detail::from_c(t);
+  if (config.collect_trace) {
+    int64_t cnt = 0;
+    detail::check(cp_last_trace(detail::ctx(), nullptr, 0, &cnt));
+    std::vector<cp_trace_row> rows(static_cast<size_t>(cnt));
+    detail::check(cp_last_trace(detail::ctx(), rows.data(), cnt, &cnt));
+    for (const auto& r : rows) sol.trace.push_back(TraceRow{r.iter, r.f_p, r.f_d, r.gap, r.elapsed_s});
+  }
   return sol;
 }
 inline Solution solve_ssnal(const ProblemInstance& inst, SolverConfig config, const Solution* warm = nullptr,
@@ -674,6 +903,9 @@ struct PathResult {
 };
 
 // run_path (path.hpp:71-73; path.cpp:110-142): the whole sweep on the GPU.
+// X(gamma) and Z(gamma) land in one page-locked host slab shared by the
+// returned matrices (streamed by the device while the next gamma is solved);
+// centroids and trace rows arrive through the C-ABI path sink.
 inline PathResult run_path(const DataMatrix& data, const WeightedGraph& graph, PenaltyNorm norm,
                            const GammaSchedule& schedule, const SolverConfig& config, const PathOptions& options = {}) {
   if (schedule.values.empty()) throw std::invalid_argument("run_path: empty schedule");
@@ -682,26 +914,51 @@ inline PathResult run_path(const DataMatrix& data, const WeightedGraph& graph, P
   auto dev = detail::upload(data);
   const Index T = static_cast<Index>(schedule.values.size());
   const Index d = data.d(), n = data.n(), E = graph.edge_count();
-  std::vector<double> X(static_cast<size_t>(T * d * n)), Z(static_cast<size_t>(T * d * E));
+  const size_t mx = static_cast<size_t>(d * n), mz = static_cast<size_t>(d * E);
+  void* raw = nullptr;
+  detail::check(cp_host_alloc(static_cast<uint64_t>(T) * (mx + mz) * sizeof(double) + 8, &raw));
+  std::shared_ptr<double> slab(static_cast<double*>(raw), [](double* p) { cp_host_free(p); });
+  double* X = slab.get();
+  double* Z = X + static_cast<size_t>(T) * mx;
   std::vector<int64_t> lab(static_cast<size_t>(T * n)), K(static_cast<size_t>(T));
   std::vector<cp_termination> terms(static_cast<size_t>(T));
   cp_solver_config c = config.to_c();
   cp_path_options o{options.warm_start ? 1 : 0, options.require_connected ? 1 : 0, options.fuse_tol};
-  detail::check(cp_run_path(detail::ctx(), dev.get(), graph.handle(), penalty_q(norm), schedule.values.data(), T, &c,
-                            &o, X.data(), Z.data(), lab.data(), K.data(), terms.data()));
+  struct Sink {
+    std::vector<Matrix> cent;
+    std::vector<std::vector<TraceRow>> trace;
+  } sk;
+  sk.cent.resize(static_cast<size_t>(T));
+  sk.trace.resize(static_cast<size_t>(T));
+  cp_path_sink sink;
+  sink.user = &sk;
+  sink.centroids = [](void* u, int64_t t, int64_t k, int64_t dd, const double* cent) {
+    Matrix m(dd, k);
+    if (k) std::memcpy(m.data(), cent, sizeof(double) * static_cast<size_t>(dd * k));
+    static_cast<Sink*>(u)->cent[static_cast<size_t>(t)] = std::move(m);
+  };
+  sink.trace = [](void* u, int64_t t, const cp_trace_row* rows, int64_t cnt) {
+    auto& tr = static_cast<Sink*>(u)->trace[static_cast<size_t>(t)];
+    for (int64_t k = 0; k < cnt; ++k)
+      tr.push_back(TraceRow{rows[k].iter, rows[k].f_p, rows[k].f_d, rows[k].gap, rows[k].elapsed_s});
+  };
+  sink.skip_identity = 1;  // K = n: centroids = X (filled below from the returned X)
+  detail::check(cp_run_path_ex(detail::ctx(), dev.get(), graph.handle(), penalty_q(norm), schedule.values.data(), T,
+                               &c, &o, X, Z, lab.data(), K.data(), terms.data(), &sink));
   PathResult r;
   r.schedule = schedule;
   r.solver = config;
   for (Index t = 0; t < T; ++t) {
     Solution s;
-    s.X.resize(d, n);
-    s.Z.resize(d, E);
-    std::memcpy(s.X.data(), X.data() + t * d * n, sizeof(double) * static_cast<size_t>(d * n));
-    if (E) std::memcpy(s.Z.data(), Z.data() + t * d * E, sizeof(double) * static_cast<size_t>(d * E));
+    s.X = Matrix::adopt(d, n, slab, X + static_cast<size_t>(t) * mx);
+    s.Z = Matrix::adopt(d, E, slab, Z + static_cast<size_t>(t) * mz);
     s.termination = detail::from_c(terms[static_cast<size_t>(t)]);
+    s.trace = std::move(sk.trace[static_cast<size_t>(t)]);
     ClusterAssignment a;
     a.labels.assign(lab.begin() + t * n, lab.begin() + (t + 1) * n);
     a.K = K[static_cast<size_t>(t)];
+    a.centroids = a.K == n && sk.cent[static_cast<size_t>(t)].size() == 0 && n > 0 ? s.X
+                                                                                  : std::move(sk.cent[static_cast<size_t>(t)]);
     r.stats.push_back(s.termination);
     r.assignments.push_back(std::move(a));
     r.solutions.push_back(std::move(s));

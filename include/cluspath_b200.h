@@ -47,7 +47,7 @@ typedef struct cp_graph cp_graph; /* device-resident WeightedGraph (graph.hpp:23
 /* SolverConfig (solvers.hpp:72-93); cp_solver_config_default fills the reference defaults. */
 typedef struct cp_solver_config {
   int32_t algorithm;      /* 0 ADMM, 1 FastAMA, 2 SSNAL (solvers.hpp:15) */
-  int32_t collect_trace;  /* accepted, ignored (trace rows are host-side diagnostics) */
+  int32_t collect_trace;  /* 1: record a cp_trace_row per gap evaluation (cp_last_trace, cp_path_sink) */
   double epsilon;         /* 1e-6 */
   double kkt_factor;      /* 10 */
   int64_t max_iter;       /* 0 -> 100 outer (SSNAL) or 20000 (ADMM, AMA) */
@@ -69,6 +69,12 @@ typedef struct cp_termination {
   double wall_time;
   int64_t newton, cg, armijo, hess_apply; /* counters (not in the reference record) */
 } cp_termination;
+
+/* TraceRow (solvers.hpp:54-60): one row per gap evaluation when collect_trace. */
+typedef struct cp_trace_row {
+  int64_t iter;
+  double f_p, f_d, gap, elapsed_s;
+} cp_trace_row;
 
 /* PathOptions (path.hpp:51-55). */
 typedef struct cp_path_options {
@@ -223,6 +229,46 @@ int cp_solve(cp_ctx* ctx, const cp_data* A, const cp_graph* g, double gamma, int
              const double* warmX, int64_t warm_d, int64_t warm_n, const double* warmZ, int64_t warm_E, double* X,
              double* Z, cp_termination* term);
 
+/* Solution::trace (solvers.hpp:54-66) of the most recent cp_solve on this
+ * context (empty unless cfg->collect_trace).  Call with rows = NULL for *count. */
+int cp_last_trace(cp_ctx* ctx, cp_trace_row* rows, int64_t max_rows, int64_t* count);
+
+/* ---- linalg (linalg.hpp:17-87) --------------------------------------------- */
+/* LinearOperator (linalg.hpp:38-65).  The operand is a rows x cols column-major
+ * block; device-resident for the factory kinds.  A host callback
+ * (LinearOperator(rows, fn, symmetric, positive_definite)) receives host
+ * buffers and returns 0 on success; each apply is one device round trip. */
+typedef struct cp_linop cp_linop;
+typedef int (*cp_apply_fn)(void* user, const double* in, double* out, int64_t rows, int64_t cols);
+int cp_linop_identity(cp_ctx* ctx, int64_t n, cp_linop** out);                             /* linalg.hpp:53 */
+int cp_linop_dense(cp_ctx* ctx, const double* M, int64_t n, int positive_definite, cp_linop** out); /* :54 */
+/* n x n compressed columns (Eigen::SparseMatrix<double> layout, int64 indices) (linalg.hpp:55-56) */
+int cp_linop_sparse(cp_ctx* ctx, int64_t n, const int64_t* colptr, const int64_t* rowidx, const double* values,
+                    int positive_definite, cp_linop** out);
+/* jacobi(Vector diag) when cols = 1, jacobi(Matrix diag) otherwise (linalg.hpp:60-61) */
+int cp_linop_jacobi(cp_ctx* ctx, const double* diag, int64_t rows, int64_t cols, cp_linop** out);
+int cp_linop_callback(cp_ctx* ctx, int64_t rows, cp_apply_fn fn, void* user, int symmetric, int positive_definite,
+                      cp_linop** out); /* linalg.hpp:45-46 */
+int cp_linop_info(const cp_linop* op, int64_t* rows, int* symmetric, int* positive_definite);
+void cp_linop_destroy(cp_linop* op);
+int cp_linop_apply(cp_ctx* ctx, const cp_linop* op, const double* X, int64_t cols, double* out); /* :51 */
+/* pcg(op, rhs, preconditioner, tol, max_iter) (linalg.hpp:76-77; linalg.cpp:143-192).
+ * rhs / x: rows x cols host buffers; pre nullable (identity). */
+int cp_pcg(cp_ctx* ctx, const cp_linop* op, const double* rhs, int64_t cols, const cp_linop* pre, double tol,
+           int64_t max_iter, double* x, int64_t* iterations, double* residual, int32_t* converged);
+/* power_iteration(op, tol, max_iter) (linalg.hpp:82-83; linalg.cpp:194-242) */
+int cp_power_iteration(cp_ctx* ctx, const cp_linop* op, double tol, int64_t max_iter, double* lambda);
+/* CholeskyFactor(L, rho) / solve(rhs) (linalg.hpp:17-33; linalg.cpp:32-54): M = I + rho L,
+ * L n x n compressed columns; solve returns M^{-1} rhs (rows n, cols columns) to 1e-14
+ * relative residual per column (device CG in place of the sparse factor). */
+typedef struct cp_factor cp_factor;
+int cp_factor_create(cp_ctx* ctx, int64_t n, const int64_t* colptr, const int64_t* rowidx, const double* values,
+                     double rho, cp_factor** out);
+int cp_factor_solve(cp_ctx* ctx, const cp_factor* f, const double* rhs, int64_t cols, double* out);
+void cp_factor_destroy(cp_factor* f);
+/* norm_value / dual_norm_value (prox.hpp:14-15; prox.cpp:25-31) of every column of a d x cols block */
+int cp_norm_values(cp_ctx* ctx, int q, const double* V, int64_t d, int64_t cols, double* norm, double* dual);
+
 /* ---- path (path.hpp:26-78) ------------------------------------------------ */
 /* make_schedule(start, end, count, spacing) (path.hpp:26; path.cpp:21-58); spacing 0 linear, 1 geometric */
 int cp_make_schedule(double start, double end, int64_t count, int geometric, double* out);
@@ -234,6 +280,21 @@ int cp_extract_clusters(cp_ctx* ctx, const cp_graph* g, const double* X, int64_t
 int cp_run_path(cp_ctx* ctx, const cp_data* A, const cp_graph* g, int q, const double* gammas, int64_t T,
                 const cp_solver_config* cfg, const cp_path_options* opt, double* X_out, double* Z_out,
                 int64_t* labels_out, int64_t* K_out, cp_termination* terms_out);
+/* Per-gamma callbacks of cp_run_path_ex (all nullable), called on the calling
+ * thread in gamma order: the d x K centroids of ClusterAssignment (path.hpp:30-34,
+ * filled by path.cpp:135; host memory valid during the call) and the solver's
+ * trace rows (Solution::trace, when cfg->collect_trace). */
+typedef struct cp_path_sink {
+  void* user;
+  void (*centroids)(void* user, int64_t t, int64_t K, int64_t d, const double* centroids);
+  void (*trace)(void* user, int64_t t, const cp_trace_row* rows, int64_t count);
+  /* 1: skip the centroids call when K = n (every node its own cluster, labels 0..n-1 and
+     centroids = X bitwise); a caller that keeps X(gamma) reuses it instead of a d x n copy */
+  int32_t skip_identity;
+} cp_path_sink;
+int cp_run_path_ex(cp_ctx* ctx, const cp_data* A, const cp_graph* g, int q, const double* gammas, int64_t T,
+                   const cp_solver_config* cfg, const cp_path_options* opt, double* X_out, double* Z_out,
+                   int64_t* labels_out, int64_t* K_out, cp_termination* terms_out, const cp_path_sink* sink);
 
 #ifdef __cplusplus
 }

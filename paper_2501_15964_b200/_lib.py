@@ -39,6 +39,21 @@ class PathOptionsC(C.Structure):
     _fields_ = [("warm_start", C.c_int32), ("require_connected", C.c_int32), ("fuse_tol", C.c_double)]
 
 
+class TraceRowC(C.Structure):
+    """cp_trace_row (TraceRow, solvers.hpp:54-60)."""
+    _fields_ = [("iter", C.c_int64), ("f_p", C.c_double), ("f_d", C.c_double), ("gap", C.c_double),
+                ("elapsed_s", C.c_double)]
+
+
+APPLY_FN = C.CFUNCTYPE(C.c_int, VP, D, D, C.c_int64, C.c_int64)
+CENT_FN = C.CFUNCTYPE(None, VP, C.c_int64, C.c_int64, C.c_int64, D)
+TRACE_FN = C.CFUNCTYPE(None, VP, C.c_int64, C.POINTER(TraceRowC), C.c_int64)
+
+
+class PathSinkC(C.Structure):
+    _fields_ = [("user", VP), ("centroids", CENT_FN), ("trace", TRACE_FN), ("skip_identity", C.c_int32)]
+
+
 class KernelStatC(C.Structure):
     _fields_ = [("name", C.c_char * 40), ("launches", C.c_int64), ("ms", C.c_double), ("alg_bytes", C.c_double)]
 
@@ -105,6 +120,24 @@ _SIGS = [
     ("cp_extract_clusters", C.c_int, [VP, VP, D, C.c_int64, C.c_int64, C.c_double, I64, I64, D]),
     ("cp_run_path", C.c_int, [VP, VP, VP, C.c_int, D, C.c_int64, C.POINTER(SolverConfigC),
                               C.POINTER(PathOptionsC), D, D, I64, I64, C.POINTER(TerminationC)]),
+    ("cp_run_path_ex", C.c_int, [VP, VP, VP, C.c_int, D, C.c_int64, C.POINTER(SolverConfigC),
+                                 C.POINTER(PathOptionsC), D, D, I64, I64, C.POINTER(TerminationC),
+                                 C.POINTER(PathSinkC)]),
+    ("cp_last_trace", C.c_int, [VP, C.POINTER(TraceRowC), C.c_int64, I64]),
+    ("cp_linop_identity", C.c_int, [VP, C.c_int64, C.POINTER(VP)]),
+    ("cp_linop_dense", C.c_int, [VP, D, C.c_int64, C.c_int, C.POINTER(VP)]),
+    ("cp_linop_sparse", C.c_int, [VP, C.c_int64, I64, I64, D, C.c_int, C.POINTER(VP)]),
+    ("cp_linop_jacobi", C.c_int, [VP, D, C.c_int64, C.c_int64, C.POINTER(VP)]),
+    ("cp_linop_callback", C.c_int, [VP, C.c_int64, APPLY_FN, VP, C.c_int, C.c_int, C.POINTER(VP)]),
+    ("cp_linop_info", C.c_int, [VP, I64, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("cp_linop_destroy", None, [VP]),
+    ("cp_linop_apply", C.c_int, [VP, VP, D, C.c_int64, D]),
+    ("cp_pcg", C.c_int, [VP, VP, D, C.c_int64, VP, C.c_double, C.c_int64, D, I64, D, C.POINTER(C.c_int32)]),
+    ("cp_power_iteration", C.c_int, [VP, VP, C.c_double, C.c_int64, D]),
+    ("cp_factor_create", C.c_int, [VP, C.c_int64, I64, I64, D, C.c_double, C.POINTER(VP)]),
+    ("cp_factor_solve", C.c_int, [VP, VP, D, C.c_int64, D]),
+    ("cp_factor_destroy", None, [VP]),
+    ("cp_norm_values", C.c_int, [VP, C.c_int, D, C.c_int64, C.c_int64, D, D]),
 ]
 
 EXPORTED = [s[0] for s in _SIGS]

@@ -579,6 +579,246 @@ def prox_jacobian_diag(V, thresholds, norm=PenaltyNorm.l2, ctx=None):
     return _cols_call(L.load().cp_prox_jacobian_diag, _qcode(norm), V, thresholds, ctx)
 
 
+def norm_value(v, norm=PenaltyNorm.l2, ctx=None) -> float:
+    """norm_value (prox.hpp:14; prox.cpp:25-31): ||v||_q on the GPU."""
+    return _norms(v, norm, ctx)[0]
+
+
+def dual_norm_value(v, norm=PenaltyNorm.l2, ctx=None) -> float:
+    """dual_norm_value (prox.hpp:15; prox.cpp:25-31): ||v||_q' on the GPU."""
+    return _norms(v, norm, ctx)[1]
+
+
+def _norms(v, norm, ctx):
+    v = _f64(v).reshape(-1)
+    ctx = ctx or default_context()
+    a, b = C.c_double(), C.c_double()
+    L.check(L.load().cp_norm_values(ctx._h, _qcode(norm), _dp(v), len(v), 1, C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def prox_norm(v, t, norm=PenaltyNorm.l2, ctx=None):
+    """prox_norm (prox.hpp:19-21): prox_{t ||.||_q}(v)."""
+    if not (t >= 0) or not math.isfinite(t):
+        raise ValueError("prox_norm: threshold must be finite and >= 0")
+    return prox_columns(_f64(v).reshape(1, -1), [t], norm, ctx)[0]
+
+
+def prox_norm_into(v, t, norm, out, ctx=None):
+    """prox_norm_into (prox.hpp:20-21): writes prox_{t ||.||_q}(v) into `out`."""
+    out[...] = prox_norm(v, t, norm, ctx).reshape(np.shape(out))
+
+
+def project_dual_ball(z, r, norm=PenaltyNorm.l2, ctx=None):
+    """project_dual_ball (prox.hpp:24-26): projection onto {||.||_q' <= r}."""
+    if not (r >= 0) or not math.isfinite(r):
+        raise ValueError("project_dual_ball: threshold must be finite and >= 0")
+    return project_columns(_f64(z).reshape(1, -1), [r], norm, ctx)[0]
+
+
+def project_dual_ball_into(z, r, norm, out, ctx=None):
+    """project_dual_ball_into (prox.hpp:25-26)."""
+    out[...] = project_dual_ball(z, r, norm, ctx).reshape(np.shape(out))
+
+
+def moreau_check(v, t, norm=PenaltyNorm.l2, ctx=None) -> float:
+    """moreau_check (prox.hpp:51-54): ||prox(v) + Pi(v) - v||_inf."""
+    v = _f64(v).reshape(-1)
+    return float(np.max(np.abs(prox_norm(v, t, norm, ctx) + project_dual_ball(v, t, norm, ctx) - v), initial=0.0))
+
+
+# ---- linalg.hpp (linalg.hpp:17-87) ----------------------------------------------
+# Operands are (rows,) vectors or (rows, cols) blocks in the reference's own
+# orientation (Eigen d x k), passed column-major to the device.
+
+def _fblock(x, rows=None):
+    x = np.asarray(x, dtype=np.float64)
+    vec = x.ndim == 1
+    x2 = x.reshape(-1, 1) if vec else x
+    if x2.ndim != 2:
+        raise ValueError("operand must be a vector or a matrix")
+    return np.asfortranarray(x2), vec
+
+
+class LinearOperator:
+    """LinearOperator (linalg.hpp:38-65).  LinearOperator(rows, fn) wraps a
+    Python callable (host round trip per apply); the static factories build
+    device-resident operators."""
+
+    def __init__(self, rows, fn=None, symmetric=True, positive_definite=False, ctx=None, _handle=None):
+        self.ctx = ctx or default_context()
+        self._h = None
+        self._keep = None
+        if _handle is not None:
+            self._h = _handle
+            return
+        if fn is None:
+            raise ValueError("LinearOperator: empty apply function")
+        self._err = None
+
+        def tramp(user, xin, xout, r, c):
+            try:
+                X = np.ctypeslib.as_array(xin, shape=(int(c) * int(r),)).reshape((int(r), int(c)), order="F")
+                Y = np.asarray(fn(X.copy(order="F") if c > 1 else X[:, 0].copy()), dtype=np.float64)
+                Y = Y.reshape((int(r), int(c)), order="F") if Y.ndim == 1 else Y
+                if Y.shape != (int(r), int(c)):
+                    raise RuntimeError("LinearOperator::apply: image shape mismatch")
+                np.ctypeslib.as_array(xout, shape=(int(c) * int(r),))[:] = Y.reshape(-1, order="F")
+                return 0
+            except Exception as e:  # noqa: BLE001 — re-raised by the caller after the C call returns
+                self._err = e
+                return 1
+
+        self._keep = L.APPLY_FN(tramp)
+        h = C.c_void_p()
+        L.check(L.load().cp_linop_callback(self.ctx._h, int(rows), self._keep, None, int(bool(symmetric)),
+                                           int(bool(positive_definite)), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and L._lib is not None:
+            L._lib.cp_linop_destroy(self._h)
+            self._h = None
+
+    def _info(self):
+        r, s, p = C.c_int64(), C.c_int(), C.c_int()
+        L.check(L.load().cp_linop_info(self._h, C.byref(r), C.byref(s), C.byref(p)))
+        return r.value, bool(s.value), bool(p.value)
+
+    def rows(self):
+        return self._info()[0]
+
+    def symmetric(self):
+        return self._info()[1]
+
+    def positive_definite(self):
+        return self._info()[2]
+
+    def _raise_callback(self, rc):
+        err = getattr(self, "_err", None)
+        if rc != 0 and err is not None:
+            self._err = None
+            raise err
+        L.check(rc)
+
+    def apply(self, x):
+        X, vec = _fblock(x)
+        if X.shape[0] != self.rows():
+            raise ValueError("LinearOperator::apply: operand has wrong row count")
+        out = np.empty(X.shape, order="F")
+        self._raise_callback(L.load().cp_linop_apply(self.ctx._h, self._h, _dp(X), X.shape[1], _dp(out)))
+        return out[:, 0].copy() if vec else out
+
+    @staticmethod
+    def _make(fn, ctx, *args):
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        L.check(fn(ctx._h, *args, C.byref(h)))
+        return LinearOperator(0, ctx=ctx, _handle=h)
+
+    @staticmethod
+    def identity(n, ctx=None):
+        return LinearOperator._make(L.load().cp_linop_identity, ctx, int(n))
+
+    @staticmethod
+    def dense(M, positive_definite=False, ctx=None):
+        M = np.asarray(M, dtype=np.float64)
+        if M.ndim != 2 or M.shape[0] != M.shape[1]:
+            raise ValueError("LinearOperator::dense: matrix must be square")
+        M = np.asfortranarray(M)
+        return LinearOperator._make(L.load().cp_linop_dense, ctx, _dp(M), M.shape[0], int(bool(positive_definite)))
+
+    @staticmethod
+    def sparse(M, positive_definite=False, ctx=None):
+        import scipy.sparse as sp
+        M = sp.csc_matrix(M)
+        if M.shape[0] != M.shape[1]:
+            raise ValueError("LinearOperator::sparse: matrix must be square")
+        cp_ = np.ascontiguousarray(M.indptr, dtype=np.int64)
+        ri = np.ascontiguousarray(M.indices, dtype=np.int64)
+        va = np.ascontiguousarray(M.data, dtype=np.float64)
+        return LinearOperator._make(L.load().cp_linop_sparse, ctx, M.shape[0], _ip(cp_), _ip(ri), _dp(va),
+                                    int(bool(positive_definite)))
+
+    @staticmethod
+    def jacobi(diag, ctx=None):
+        """jacobi(Vector) for a 1-D diagonal, jacobi(Matrix) for a 2-D block."""
+        D, vec = _fblock(diag)
+        return LinearOperator._make(L.load().cp_linop_jacobi, ctx, _dp(D), D.shape[0], D.shape[1])
+
+
+@dataclass
+class PcgResult:
+    """PcgResult (linalg.hpp:67-72)."""
+    x: np.ndarray
+    iterations: int = 0
+    residual: float = 0.0
+    converged: bool = False
+
+
+def pcg(op: LinearOperator, rhs, preconditioner: Optional[LinearOperator] = None, tol: float = 1e-10,
+        max_iter: int = 1000) -> PcgResult:
+    """pcg (linalg.hpp:76-77; linalg.cpp:143-192) on the GPU."""
+    B, vec = _fblock(rhs)
+    if B.shape[0] != op.rows():
+        raise ValueError("pcg: rhs row count does not match the operator")
+    x = np.empty(B.shape, order="F")
+    it, res, conv = C.c_int64(), C.c_double(), C.c_int32()
+    rc = L.load().cp_pcg(op.ctx._h, op._h, _dp(B), B.shape[1], preconditioner._h if preconditioner else None,
+                         float(tol), int(max_iter), _dp(x), C.byref(it), C.byref(res), C.byref(conv))
+    for o in (op, preconditioner):
+        if o is not None and getattr(o, "_err", None) is not None:
+            o._raise_callback(rc)
+    L.check(rc)
+    return PcgResult(x[:, 0].copy() if vec else x, it.value, res.value, bool(conv.value))
+
+
+def power_iteration(op: LinearOperator, tol: float = 1e-9, max_iter: int = 10000) -> float:
+    """power_iteration (linalg.hpp:82-83; linalg.cpp:194-242) on the GPU."""
+    out = C.c_double()
+    op._raise_callback(L.load().cp_power_iteration(op.ctx._h, op._h, float(tol), int(max_iter), C.byref(out)))
+    return out.value
+
+
+class CholeskyFactor:
+    """CholeskyFactor(L, rho) (linalg.hpp:17-33): solve() returns (I + rho L)^{-1} rhs,
+    computed on the GPU by Jacobi-preconditioned CG to 1e-14 relative residual per column."""
+
+    def __init__(self, Lap, rho, ctx=None):
+        import scipy.sparse as sp
+        self.ctx = ctx or default_context()
+        Lc = sp.csc_matrix(Lap)
+        if Lc.shape[0] != Lc.shape[1]:
+            raise ValueError("cholesky: matrix must be square")
+        self._n, self._rho = Lc.shape[0], float(rho)
+        cp_ = np.ascontiguousarray(Lc.indptr, dtype=np.int64)
+        ri = np.ascontiguousarray(Lc.indices, dtype=np.int64)
+        va = np.ascontiguousarray(Lc.data, dtype=np.float64)
+        h = C.c_void_p()
+        self._h = None
+        L.check(L.load().cp_factor_create(self.ctx._h, self._n, _ip(cp_), _ip(ri), _dp(va), float(rho), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and L._lib is not None:
+            L._lib.cp_factor_destroy(self._h)
+            self._h = None
+
+    def size(self):
+        return self._n
+
+    def rho(self):
+        return self._rho
+
+    def solve(self, rhs):
+        B, vec = _fblock(rhs)
+        if B.shape[0] != self._n:
+            raise ValueError("cholesky solve: rhs has wrong row count")
+        out = np.empty(B.shape, order="F")
+        L.check(L.load().cp_factor_solve(self.ctx._h, self._h, _dp(B), B.shape[1], _dp(out)))
+        return out[:, 0].copy() if vec else out
+
+
 # ---- solvers.hpp ---------------------------------------------------------------
 
 class Algorithm(enum.IntEnum):
@@ -653,10 +893,25 @@ class TerminationRecord:
 
 
 @dataclass
+class TraceRow:
+    """TraceRow (solvers.hpp:54-60)."""
+    iter: int = 0
+    f_p: float = 0.0
+    f_d: float = 0.0
+    gap: float = 0.0
+    elapsed_s: float = 0.0
+
+
+def _trace_rows(rows, count):
+    return [TraceRow(rows[k].iter, rows[k].f_p, rows[k].f_d, rows[k].gap, rows[k].elapsed_s) for k in range(count)]
+
+
+@dataclass
 class Solution:
     X: np.ndarray
     Z: np.ndarray
     termination: TerminationRecord = field(default_factory=TerminationRecord)
+    trace: List[TraceRow] = field(default_factory=list)  # filled when SolverConfig.collect_trace
 
 
 class ProblemInstance:
@@ -759,7 +1014,14 @@ def solve(inst: ProblemInstance, config: Optional[SolverConfig] = None, warm: Op
         wshape = (wx.shape[1], wx.shape[0], wz.shape[0])
     L.check(L.load().cp_solve(*inst._args(), C.byref(cfg), _dp(wx), wshape[0], wshape[1], _dp(wz), wshape[2], _dp(X),
                               _dp(Z), C.byref(t)))
-    return Solution(X, Z, TerminationRecord.from_c(t))
+    trace = []
+    if config.collect_trace:
+        cnt = C.c_int64()
+        L.check(L.load().cp_last_trace(inst.data.ctx._h, None, 0, C.byref(cnt)))
+        rows = (L.TraceRowC * max(1, cnt.value))()
+        L.check(L.load().cp_last_trace(inst.data.ctx._h, rows, cnt.value, C.byref(cnt)))
+        trace = _trace_rows(rows, cnt.value)
+    return Solution(X, Z, TerminationRecord.from_c(t), trace)
 
 
 # ---- path.hpp --------------------------------------------------------------------
@@ -824,11 +1086,13 @@ class PathResult:
 
 
 def run_path(data: DataMatrix, graph: WeightedGraph, norm, schedule: GammaSchedule, config: Optional[SolverConfig] = None,
-             options: Optional[PathOptions] = None, keep_solutions: bool = True, keep_z: bool = True) -> PathResult:
+             options: Optional[PathOptions] = None, keep_solutions: bool = True, keep_z: bool = True,
+             centroids: bool = True) -> PathResult:
     """run_path (path.cpp:110-142): warm-started gamma sweep, all on the GPU.
     keep_solutions=False returns labels and records only; keep_z=False keeps
     every X(gamma) but not the E x d multipliers (their host copy is the
-    dominant cost of a large path: 20 x E x d doubles)."""
+    dominant cost of a large path: 20 x E x d doubles).  centroids=False skips
+    ClusterAssignment.centroids (path.cpp:135; one d x K D2H per gamma)."""
     config = config or SolverConfig()
     options = options or PathOptions()
     gam = _f64(schedule.values)
@@ -843,11 +1107,28 @@ def run_path(data: DataMatrix, graph: WeightedGraph, norm, schedule: GammaSchedu
     terms = (L.TerminationC * T)()
     cfg = config.to_c()
     opt = L.PathOptionsC(int(options.warm_start), int(options.require_connected), float(options.fuse_tol))
-    L.check(L.load().cp_run_path(data.ctx._h, data._h, graph._h, _qcode(norm), _dp(gam), T, C.byref(cfg), C.byref(opt),
-                                 _dp(X), _dp(Z), _ip(lab), _ip(K), terms))
+    cents = [None] * T
+    traces = [[] for _ in range(T)]
+
+    def on_cent(user, t, k, dd, ptr):  # ClusterAssignment::centroids, d x K -> (K, d) rows
+        cents[t] = np.ctypeslib.as_array(ptr, shape=(int(k) * int(dd),)).reshape(int(k), int(dd)).copy() \
+            if k > 0 else np.empty((0, int(dd)))
+
+    def on_trace(user, t, rows, cnt):
+        traces[t] = _trace_rows(rows, int(cnt))
+
+    sink = L.PathSinkC(None, L.CENT_FN(on_cent) if centroids else L.CENT_FN(),
+                       L.TRACE_FN(on_trace) if config.collect_trace else L.TRACE_FN(), int(X is not None))
+    L.check(L.load().cp_run_path_ex(data.ctx._h, data._h, graph._h, _qcode(norm), _dp(gam), T, C.byref(cfg),
+                                    C.byref(opt), _dp(X), _dp(Z), _ip(lab), _ip(K), terms, C.byref(sink)))
     stats = [TerminationRecord.from_c(t) for t in terms]
-    sols = [Solution(X[t] if X is not None else None, Z[t] if Z is not None else None, stats[t]) for t in range(T)]
-    asg = [ClusterAssignment(lab[t], int(K[t]), None) for t in range(T)]
+    sols = [Solution(X[t] if X is not None else None, Z[t] if Z is not None else None, stats[t], traces[t])
+            for t in range(T)]
+    if centroids and X is not None:  # K = n: every node its own cluster, centroids = X (skip_identity)
+        for t in range(T):
+            if cents[t] is None and int(K[t]) == n:
+                cents[t] = X[t]
+    asg = [ClusterAssignment(lab[t], int(K[t]), cents[t]) for t in range(T)]
     return PathResult(schedule, sols, asg, stats, config)
 
 

@@ -124,6 +124,7 @@ cp_termination admm_solve(Prob& P, const cp_solver_config& cfg, bool warm, doubl
   }
   {
     GapOut s0 = eval_gap(P, Xout, Zout);
+    trace_gap(c, cfg, 0, s0, since(t0));
     if (s0.gap <= cfg.epsilon && s0.kkt <= cfg.kkt_factor * cfg.epsilon) return fin(s0, 0, true);
   }
   const double rho = cfg.admm_rho;
@@ -158,6 +159,7 @@ cp_termination admm_solve(Prob& P, const cp_solver_config& cfg, bool warm, doubl
                                                          static_cast<int>(d), rho, P.q);
     CPB_LAUNCH_CHECK();
     GapOut s = eval_gap(P, X, Zc);
+    trace_gap(c, cfg, k, s, since(t0));
     if (s.gap <= cfg.epsilon && s.kkt <= cfg.kkt_factor * cfg.epsilon) {
       copy_dev(c, Zout, Zc, me);
       return fin(s, k, true);

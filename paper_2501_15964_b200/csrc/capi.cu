@@ -5,11 +5,13 @@
 // without a CUDA device cp_ctx_create fails with CP_ERUNTIME.
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <random>
 #include <string>
 #include <vector>
 
 #include "comm.cuh"
+#include "linalg.cuh"
 #include "solve.cuh"
 
 struct cp_ctx {
@@ -23,6 +25,16 @@ struct cp_data {
 struct cp_graph {
   std::unique_ptr<cpb::Graph> g;
   cudaStream_t s = nullptr;
+  int device = 0;
+};
+struct cp_linop {
+  cpb::LinOp op;
+  int device = 0;
+};
+struct cp_factor {
+  cpb::LinOp M;    // I + rho L (CSR rows)
+  cpb::LinOp pre;  // Jacobi diagonal of M
+  double rho = 0.0;
   int device = 0;
 };
 
@@ -702,6 +714,12 @@ int cp_extract_clusters(cp_ctx* ctx, const cp_graph* g, const double* X, int64_t
 int cp_run_path(cp_ctx* ctx, const cp_data* A, const cp_graph* g, int q, const double* gammas, int64_t T,
                 const cp_solver_config* cfg, const cp_path_options* opt, double* X_out, double* Z_out,
                 int64_t* labels_out, int64_t* K_out, cp_termination* terms_out) {
+  return cp_run_path_ex(ctx, A, g, q, gammas, T, cfg, opt, X_out, Z_out, labels_out, K_out, terms_out, nullptr);
+}
+
+int cp_run_path_ex(cp_ctx* ctx, const cp_data* A, const cp_graph* g, int q, const double* gammas, int64_t T,
+                   const cp_solver_config* cfg, const cp_path_options* opt, double* X_out, double* Z_out,
+                   int64_t* labels_out, int64_t* K_out, cp_termination* terms_out, const cp_path_sink* sink) {
   return guard(ctx, [&] {
     need(A, "data");
     need(g, "graph");
@@ -712,7 +730,233 @@ int cp_run_path(cp_ctx* ctx, const cp_data* A, const cp_graph* g, int q, const d
     cp_path_options defo;
     cp_path_options_default(&defo);
     cpb::run_path_dev(*ctx->c, const_cast<cpb::Data&>(A->d), *g->g, q, gammas, T, cfg ? *cfg : defc,
-                      opt ? *opt : defo, X_out, Z_out, labels_out, K_out, terms_out);
+                      opt ? *opt : defo, X_out, Z_out, labels_out, K_out, terms_out, sink);
+  });
+}
+
+int cp_last_trace(cp_ctx* ctx, cp_trace_row* rows, int64_t max_rows, int64_t* count) {
+  return guard(ctx, [&] {
+    need(ctx, "ctx");
+    const auto& tr = ctx->c->trace;
+    if (count) *count = static_cast<int64_t>(tr.size());
+    if (rows)
+      for (size_t k = 0; k < tr.size() && static_cast<int64_t>(k) < max_rows; ++k) rows[k] = tr[k];
+  });
+}
+
+// ---- linalg (linalg.hpp:17-87) --------------------------------------------------------
+}  // extern "C"
+namespace {
+template <class F>
+int make_linop(cp_ctx* ctx, cp_linop** out, F fill) {
+  return guard(ctx, [&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    auto h = std::make_unique<cp_linop>();
+    h->device = ctx->c->device;
+    fill(h->op);
+    *out = h.release();
+  });
+}
+void check_op(cp_ctx* ctx, const cp_linop* op) {
+  need(ctx, "ctx");
+  need(op, "operator");
+  if (op->device != ctx->c->device) cpb::invalid("operator belongs to another device");
+}
+}  // namespace
+extern "C" {
+
+int cp_linop_identity(cp_ctx* ctx, int64_t n, cp_linop** out) {
+  return make_linop(ctx, out, [&](cpb::LinOp& op) {
+    if (n < 0) cpb::invalid("LinearOperator: negative dimension");
+    op.kind = cpb::LinOp::Identity;
+    op.n = n;
+    op.symmetric = op.positive_definite = true;
+  });
+}
+int cp_linop_dense(cp_ctx* ctx, const double* M, int64_t n, int positive_definite, cp_linop** out) {
+  return make_linop(ctx, out, [&](cpb::LinOp& op) {
+    if (n < 0) cpb::invalid("LinearOperator::dense: matrix must be square");
+    if (n > 0) need(M, "M");
+    // symmetric flag as linalg.cpp:82-84: ||M - M^T||_inf-entry <= 1e-12 (1 + ||M||_inf-entry)
+    double asym = 0.0, scale = 0.0;
+    for (int64_t r = 0; r < n; ++r)
+      for (int64_t c = 0; c < n; ++c) {
+        asym = std::max(asym, std::abs(M[c * n + r] - M[r * n + c]));
+        scale = std::max(scale, std::abs(M[c * n + r]));
+      }
+    op.kind = cpb::LinOp::Dense;
+    op.n = n;
+    op.symmetric = asym <= 1e-12 * (1.0 + scale);
+    op.positive_definite = positive_definite != 0;
+    op.vals.resize(static_cast<size_t>(n * n) + 1);
+    if (n > 0) cpb::h2d(*ctx->c, op.vals.p, M, static_cast<size_t>(n * n) * sizeof(double));
+    ctx->c->sync();
+  });
+}
+int cp_linop_sparse(cp_ctx* ctx, int64_t n, const int64_t* colptr, const int64_t* rowidx, const double* values,
+                    int positive_definite, cp_linop** out) {
+  return make_linop(ctx, out, [&](cpb::LinOp& op) {
+    need(colptr, "colptr");
+    cpb::linop_set_sparse(*ctx->c, op, n, colptr, rowidx, values, 1.0, 0.0);
+    op.symmetric = true;
+    op.positive_definite = positive_definite != 0;
+  });
+}
+int cp_linop_jacobi(cp_ctx* ctx, const double* diag, int64_t rows, int64_t cols, cp_linop** out) {
+  return make_linop(ctx, out, [&](cpb::LinOp& op) {
+    if (rows < 0 || cols < 1) cpb::invalid("jacobi: bad diagonal shape");
+    const int64_t m = rows * cols;
+    if (m > 0) need(diag, "diag");
+    for (int64_t k = 0; k < m; ++k)
+      if (!(diag[k] > 0.0)) cpb::invalid("jacobi: diagonal must be positive");
+    op.kind = cpb::LinOp::Jacobi;
+    op.n = rows;
+    op.jcols = cols;
+    op.symmetric = op.positive_definite = true;
+    op.vals.resize(static_cast<size_t>(m) + 1);
+    if (m > 0) cpb::h2d(*ctx->c, op.vals.p, diag, static_cast<size_t>(m) * sizeof(double));
+    ctx->c->sync();
+  });
+}
+int cp_linop_callback(cp_ctx* ctx, int64_t rows, cp_apply_fn fn, void* user, int symmetric, int positive_definite,
+                      cp_linop** out) {
+  return make_linop(ctx, out, [&](cpb::LinOp& op) {
+    if (rows < 0) cpb::invalid("LinearOperator: negative dimension");
+    if (!fn) cpb::invalid("LinearOperator: empty apply function");
+    op.kind = cpb::LinOp::Callback;
+    op.n = rows;
+    op.fn = fn;
+    op.user = user;
+    op.symmetric = symmetric != 0;
+    op.positive_definite = positive_definite != 0;
+  });
+}
+int cp_linop_info(const cp_linop* op, int64_t* rows, int* symmetric, int* positive_definite) {
+  return guard(nullptr, [&] {
+    need(op, "operator");
+    if (rows) *rows = op->op.n;
+    if (symmetric) *symmetric = op->op.symmetric;
+    if (positive_definite) *positive_definite = op->op.positive_definite;
+  });
+}
+void cp_linop_destroy(cp_linop* op) {
+  if (!op) return;
+  cudaSetDevice(op->device);
+  delete op;
+}
+int cp_linop_apply(cp_ctx* ctx, const cp_linop* op, const double* X, int64_t cols, double* out) {
+  return guard(ctx, [&] {
+    check_op(ctx, op);
+    if (cols < 0) cpb::invalid("LinearOperator::apply: operand has wrong row count");
+    cpb::Ctx& c = *ctx->c;
+    const int64_t m = op->op.n * cols;
+    double* dx = upload(c, "la.x", X, m);
+    double* dy = c.buf<double>("la.y", m + 1);
+    cpb::linop_apply(c, op->op, dx, cols, dy);
+    cpb::d2h(c, out, dy, m * sizeof(double));
+  });
+}
+int cp_pcg(cp_ctx* ctx, const cp_linop* op, const double* rhs, int64_t cols, const cp_linop* pre, double tol,
+           int64_t max_iter, double* x, int64_t* iterations, double* residual, int32_t* converged) {
+  return guard(ctx, [&] {
+    check_op(ctx, op);
+    if (pre) check_op(ctx, pre);
+    if (cols < 0) cpb::invalid("pcg: rhs row count does not match the operator");
+    cpb::Ctx& c = *ctx->c;
+    const int64_t m = op->op.n * cols;
+    double* db = upload(c, "la.b", rhs, m);
+    double* dx = c.buf<double>("la.xo", m + 1);
+    const cpb::PcgResultDev r = cpb::pcg_generic(c, op->op, db, cols, pre ? &pre->op : nullptr, tol, max_iter, dx);
+    if (x) cpb::d2h(c, x, dx, m * sizeof(double));
+    if (iterations) *iterations = r.iterations;
+    if (residual) *residual = r.residual;
+    if (converged) *converged = r.converged ? 1 : 0;
+  });
+}
+int cp_power_iteration(cp_ctx* ctx, const cp_linop* op, double tol, int64_t max_iter, double* lambda) {
+  return guard(ctx, [&] {
+    check_op(ctx, op);
+    need(lambda, "lambda");
+    *lambda = cpb::power_generic(*ctx->c, op->op, tol, max_iter);
+  });
+}
+int cp_factor_create(cp_ctx* ctx, int64_t n, const int64_t* colptr, const int64_t* rowidx, const double* values,
+                     double rho, cp_factor** out) {
+  return guard(ctx, [&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    need(colptr, "colptr");
+    if (!(rho > 0.0) || !std::isfinite(rho)) cpb::invalid("cholesky: rho must be positive and finite");
+    if (n < 0) cpb::invalid("cholesky: matrix must be square");
+    // check_square_symmetric (linalg.cpp:14-28): max |L^T - L| <= 1e-12 (1 + max |L|)
+    std::map<std::pair<int64_t, int64_t>, double> ent;
+    double scale = 0.0;
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t q = colptr[j]; q < colptr[j + 1]; ++q) {
+        if (rowidx[q] < 0 || rowidx[q] >= n) cpb::invalid("cholesky: row index out of range");
+        ent[{rowidx[q], j}] += values[q];
+        scale = std::max(scale, std::abs(values[q]));
+      }
+    double asym = 0.0;
+    for (const auto& [rc, v] : ent) {
+      auto it = ent.find({rc.second, rc.first});
+      asym = std::max(asym, std::abs(v - (it == ent.end() ? 0.0 : it->second)));
+    }
+    if (asym > 1e-12 * (1.0 + scale)) cpb::invalid("cholesky: matrix is not symmetric");
+    auto f = std::make_unique<cp_factor>();
+    f->device = ctx->c->device;
+    f->rho = rho;
+    cpb::Ctx& c = *ctx->c;
+    cpb::linop_set_sparse(c, f->M, n, colptr, rowidx, values, rho, 1.0);  // M = I + rho L (linalg.cpp:40-42)
+    std::vector<double> dg(static_cast<size_t>(n), 1.0);
+    for (const auto& [rc, v] : ent)
+      if (rc.first == rc.second) dg[static_cast<size_t>(rc.first)] += rho * v;
+    for (double x : dg)
+      if (!(x > 0.0)) cpb::runtime("cholesky: factorization of I + rho*L failed");
+    f->pre.kind = cpb::LinOp::Jacobi;
+    f->pre.n = n;
+    f->pre.vals.resize(static_cast<size_t>(n) + 1);
+    if (n > 0) cpb::h2d(c, f->pre.vals.p, dg.data(), static_cast<size_t>(n) * sizeof(double));
+    c.sync();
+    *out = f.release();
+  });
+}
+int cp_factor_solve(cp_ctx* ctx, const cp_factor* f, const double* rhs, int64_t cols, double* out) {
+  return guard(ctx, [&] {
+    need(ctx, "ctx");
+    need(f, "factor");
+    if (f->device != ctx->c->device) cpb::invalid("factor belongs to another device");
+    if (cols < 0) cpb::invalid("cholesky solve: rhs has wrong row count");
+    cpb::Ctx& c = *ctx->c;
+    const int64_t n = f->M.n, m = n * cols;
+    double* db = upload(c, "fa.b", rhs, m);
+    double* dx = c.buf<double>("fa.x", m + 1);
+    const cpb::PcgResultDev r = cpb::pcg_generic(c, f->M, db, cols, &f->pre, 1e-14, 20 * n + 100, dx, 1);
+    if (!r.converged && r.residual > 1e-10) cpb::runtime("cholesky: solve of I + rho*L did not converge");
+    cpb::d2h(c, out, dx, m * sizeof(double));
+  });
+}
+void cp_factor_destroy(cp_factor* f) {
+  if (!f) return;
+  cudaSetDevice(f->device);
+  delete f;
+}
+int cp_norm_values(cp_ctx* ctx, int q, const double* V, int64_t d, int64_t cols, double* norm, double* dual) {
+  return guard(ctx, [&] {
+    need(ctx, "ctx");
+    check_q(q);
+    if (d < 0 || cols < 0) cpb::invalid("norm_value: bad shape");
+    cpb::Ctx& c = *ctx->c;
+    double* dv = upload(c, "nv.v", V, d * cols);
+    double* dn = c.buf<double>("nv.n", 2 * cols + 2);
+    cpb::norm_values_dev(c, q, dv, d, cols, dn, dn + cols);
+    std::vector<double> h(static_cast<size_t>(2 * cols));
+    if (cols) cpb::d2h(c, h.data(), dn, 2 * cols * sizeof(double));
+    for (int64_t k = 0; k < cols; ++k) {
+      if (norm) norm[k] = h[static_cast<size_t>(k)];
+      if (dual) dual[k] = h[static_cast<size_t>(cols + k)];
+    }
   });
 }
 

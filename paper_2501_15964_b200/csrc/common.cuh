@@ -133,6 +133,7 @@ struct Ctx {
   std::vector<cudaEvent_t> event_pool;
   cudaEvent_t timer_a = nullptr, timer_b = nullptr;  // cp_timer_start / cp_timer_stop
   std::map<std::string, int> cg_hint;                 // last PCG iteration count per operator
+  std::vector<cp_trace_row> trace;                    // Solution::trace of the current / last solve
   struct KnnInfo {
     int64_t overflow_rows;  // rows re-done by the exact FP64 tile kernel
     double worst_ratio;     // max |d2~ - d2| / delta_i over re-checked candidates

@@ -407,39 +407,57 @@ __global__ void k_cc_label(const int* __restrict__ L, const int* __restrict__ ra
 // ---- Laplacian power iteration -------------------------------------------------------------
 // w = L v in the column order of L's column-major CSC (SparseDenseProduct.h): neighbours
 // ascending with the degree term at position v (fused into k_power below).
-__device__ double blk_dot(const double* a, const double* b, int n, double* sh) {
-  double s = 0.0;
-  for (int v = threadIdx.x; v < n; v += blockDim.x) s = __dadd_rn(s, __dmul_rn(a[v], b[v]));
-  return block_sum(s, sh);
+// Sums of a[k] * b[k] in Eigen 3.4's SSE2 reduction order (Redux.h, LinearVectorizedTraversal
+// with Packet2d; the oracle's esum): four stride-4 chains, P0 += P1, the leftover packet,
+// predux, the odd tail.  Chains c = 0..3 run on four threads (sequential by nature); `slot`
+// selects a 4-double area of `sh`; thread `lead` returns the result, all others 0.  Bitwise
+// the reference's norm / dot, so lambda_max (and AMA's step 0.99 / lambda_max) is too.
+__device__ double eigen_dot(const double* a, const double* b, int n, double* sh, int lead) {
+  const int c = threadIdx.x - lead;
+  const int e2 = (n / 4) * 4;
+  if (c >= 0 && c < 4 && n >= 4) {
+    double p = __dmul_rn(a[c], b[c]);
+#pragma unroll 8
+    for (int k = c + 4; k < e2; k += 4) p = __dadd_rn(p, __dmul_rn(a[k], b[k]));
+    sh[c] = p;
+  }
+  __syncthreads();
+  double res = 0.0;
+  if (c == 0) {
+    auto f = [&](int k) { return __dmul_rn(a[k], b[k]); };
+    if (n < 2) {
+      res = n == 1 ? f(0) : 0.0;
+    } else {
+      double p00 = f(0), p01 = f(1);
+      if (n >= 4) {
+        p00 = __dadd_rn(sh[0], sh[2]);
+        p01 = __dadd_rn(sh[1], sh[3]);
+        if ((n / 2) * 2 > e2) {
+          p00 = __dadd_rn(p00, f(e2));
+          p01 = __dadd_rn(p01, f(e2 + 1));
+        }
+      }
+      res = __dadd_rn(p00, p01);
+      if (n & 1) res = __dadd_rn(res, f(n - 1));
+    }
+  }
+  return res;
 }
-// Two block sums in one barrier round; each value is reduced by exactly block_sum's tree.
-__device__ __forceinline__ void block_sum2(double& a, double& b, double* sh /* 64 */) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = (blockDim.x + 31) >> 5;
-  a = warp_sum(a);
-  b = warp_sum(b);
+// <w, w> and <v, w> at once: chains on threads 0-3 and 32-35, one barrier round.
+__device__ __forceinline__ void eigen_dots2(const double* v, const double* w, int n, double* sh /* 64 */,
+                                            double& sww, double& svw) {
+  const double a = eigen_dot(w, w, n, sh, 0);  // threads 0..3
+  const double b = eigen_dot(v, w, n, sh + 32, 32);  // threads 32..35 (their own barrier round)
+  if (threadIdx.x == 0) sh[8] = a;
+  if (threadIdx.x == 32) sh[40] = b;
   __syncthreads();
-  if (lane == 0) {
-    sh[wid] = a;
-    sh[32 + wid] = b;
-  }
-  __syncthreads();
-  double ta = (tid < nw) ? sh[tid] : 0.0, tb = (tid < nw) ? sh[32 + tid] : 0.0;
-  if (wid == 0) {
-    ta = warp_sum(ta);
-    tb = warp_sum(tb);
-  }
-  if (tid == 0) {
-    sh[0] = ta;
-    sh[32] = tb;
-  }
-  __syncthreads();
-  a = sh[0];
-  b = sh[32];
+  sww = sh[8];
+  svw = sh[40];
   __syncthreads();
 }
-// power_iteration (linalg.cpp:194-242) for one probe per block.  Each thread forms w = L v for
-// its nodes and accumulates <w, w> and <v, w> in the same per-thread order as blk_dot, so the
-// fused pass reduces bitwise like the separate dots did.
+// power_iteration (linalg.cpp:194-242) for one probe per block: w = L v in the column order of
+// L's column-major CSC (SparseDenseProduct.h: neighbours ascending with the degree term at
+// position v), then the two dots in Eigen's order.
 __global__ void __launch_bounds__(1024) k_power(const int* __restrict__ off, const int* __restrict__ adj_o,
                                                 const double* __restrict__ start, int n, double tol, long long max_iter,
                                                 double* v, double* w, double* out, int in_smem) {
@@ -455,13 +473,16 @@ __global__ void __launch_bounds__(1024) k_power(const int* __restrict__ off, con
   }
   out += 2 * blockIdx.x;
   __shared__ double sh[64];
-  const double ns = sqrt(blk_dot(start, start, n, sh));
+  const double ns0 = eigen_dot(start, start, n, sh, 0);
+  if (threadIdx.x == 0) sh[8] = ns0;
+  __syncthreads();
+  const double ns = sqrt(sh[8]);
+  __syncthreads();
   for (int t = threadIdx.x; t < n; t += blockDim.x) v[t] = __ddiv_rn(start[t], ns);
   __syncthreads();
   double prev = 0.0, est = 0.0;
   int dead = 0;
   for (long long it = 1; it <= max_iter; ++it) {
-    double sww = 0.0, svw = 0.0;
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
       const int p0 = off[t], p1 = off[t + 1];
       const double deg = static_cast<double>(p1 - p0);
@@ -479,10 +500,10 @@ __global__ void __launch_bounds__(1024) k_power(const int* __restrict__ off, con
       }
       if (!diag_done) acc = __dadd_rn(acc, __dmul_rn(deg, xv));
       w[t] = acc;
-      sww = __dadd_rn(sww, __dmul_rn(acc, acc));
-      svw = __dadd_rn(svw, __dmul_rn(xv, acc));
     }
-    block_sum2(sww, svw, sh);
+    __syncthreads();
+    double sww, svw;
+    eigen_dots2(v, w, n, sh, sww, svw);
     const double nw = sqrt(sww);
     if (nw <= 1e-300) {
       dead = 1;

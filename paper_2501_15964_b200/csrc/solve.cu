@@ -97,6 +97,7 @@ cp_termination ssnal(Prob& P, const cp_solver_config& cfg, bool warm, double* Xo
   initial_point(P, warm, Xout, Zout);
   {
     GapOut s0 = eval_gap(P, Xout, Zout);
+    trace_gap(c, cfg, 0, s0, since(t0));
     if (accepts(s0, cfg)) return finish(s0, 0, true, since(t0));
   }
   double* X = c.buf<double>("s.X", m);
@@ -173,6 +174,7 @@ cp_termination ssnal(Prob& P, const cp_solver_config& cfg, bool warm, double* Xo
     jac_params(P, nv, thr, ps, jal, jbe);  // prox scale at the last accepted V
     MultOut mo = ssnal_multiplier(P, X, Z, V, ps, thr, sigma);
     zz = mo.zz;
+    trace_gap(c, cfg, k, mo.gap, since(t0));
     if (accepts(mo.gap, cfg)) {
       copy_dev(c, Xout, X, m);
       assemble_z(Zout);
@@ -257,6 +259,7 @@ cp_termination fast_ama(Prob& P, const cp_solver_config& cfg, bool warm, double*
   initial_point(P, warm, Xout, Zout);
   {
     GapOut s0 = eval_gap(P, Xout, Zout);
+    trace_gap(c, cfg, 0, s0, since(t0));
     if (accepts(s0, cfg)) return finish(s0, 0, true, since(t0));
   }
   double lmax;
@@ -321,6 +324,7 @@ cp_termination fast_ama(Prob& P, const cp_solver_config& cfg, bool warm, double*
     }
     k = next;
     GapOut s = fg > 0 ? gap_from_partials(P, parts, fg, fg) : eval_gap(P, Xout, Zp);
+    trace_gap(c, cfg, k, s, since(t0));
     if (accepts(s, cfg)) {
       copy_dev(c, Zout, Zp, me);
       return finish(s, k, true, since(t0));
@@ -359,6 +363,7 @@ cp_termination admm_solve(Prob& P, const cp_solver_config& cfg, bool warm, doubl
 cp_termination solve_dev(Prob& P, const cp_solver_config& cfg, bool warm, double* X, double* Z, SolveCache& cache) {
   validate_config(cfg);
   Ctx& c = *P.c;
+  c.trace.clear();
   const int64_t m = P.d() * P.n();
   // trivial_solution (solver_util.hpp:44-51)
   if (!(P.gamma > 0.0) || P.E() == 0) {
@@ -506,11 +511,15 @@ int64_t extract_clusters_dev(Ctx& c, const Graph& g, const double* X, int64_t d,
 
 void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, int64_t T,
                   const cp_solver_config& cfg, const cp_path_options& opt, double* X_out, double* Z_out,
-                  int64_t* labels_out, int64_t* K_out, cp_termination* terms_out) {
+                  int64_t* labels_out, int64_t* K_out, cp_termination* terms_out, const cp_path_sink* sink) {
   if (T < 1) invalid("run_path: empty schedule");
   if (A.n != g.n) invalid("run_path: graph size does not match the data");
   if (q != 0 && q != 1 && q != 2) invalid("penalty norm exponent must be 1, 2 or 0 (infinity), got " + std::to_string(q));
   validate_config(cfg);
+  // every gamma is validated before any work starts (ProblemInstance, objective.cpp:26-33), so
+  // a bad value never leaves the caller's outputs half written
+  for (int64_t t = 0; t < T; ++t)
+    if (!(gammas[t] >= 0.0) || !std::isfinite(gammas[t])) invalid("instance: gamma must be finite and >= 0");
   if (opt.require_connected) {
     int* lab = c.buf<int>("path.lab0", g.n + 1);
     const int64_t comps = components_dev(c, g, nullptr, lab);
@@ -558,7 +567,25 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
   const int d2h_ctas = 6;
   double* snapX[2] = {nullptr, nullptr};
   double* snapZ[2] = {nullptr, nullptr};
-  cudaEvent_t snap_ready[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};
+  // The copy stream may still be writing the caller's buffers when a solve
+  // throws: drain it and release the events on every exit.
+  struct AsyncGuard {
+    cudaStream_t cs = nullptr;
+    cudaEvent_t snap_ready[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};
+    ~AsyncGuard() {
+      if (cs) cudaStreamSynchronize(cs);
+      for (int s = 0; s < 2; ++s) {
+        if (snap_ready[s]) cudaEventDestroy(snap_ready[s]);
+        if (copy_done[s]) cudaEventDestroy(copy_done[s]);
+      }
+    }
+  } ag;
+  ag.cs = cs;
+  cudaEvent_t* snap_ready = ag.snap_ready;
+  cudaEvent_t* copy_done = ag.copy_done;
+  double* cent = nullptr;
+  std::vector<double> hcent;
+  if (sink && sink->centroids) cent = c.buf<double>("path.cent", m + 1);
   if (async_out) {
     for (int s = 0; s < 2; ++s) {
       snapX[s] = c.buf<double>(s ? "path.sX1" : "path.sX0", m + 1);
@@ -570,7 +597,6 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
   }
   for (int64_t t = 0; t < T; ++t) {
     const double gamma = gammas[t];
-    if (!(gamma >= 0.0) || !std::isfinite(gamma)) invalid("instance: gamma must be finite and >= 0");
     Prob P;
     P.c = &c;
     P.A = &A;
@@ -580,7 +606,13 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
     P.rad = rad;
     make_radii(c, g, gamma, rad);
     cp_termination term = solve_dev(P, cfg, warm, X, Z, cache);
-    const int64_t K = extract_clusters_dev(c, g, X, d, opt.fuse_tol, lab, nullptr);
+    if (sink && sink->trace) sink->trace(sink->user, t, c.trace.data(), static_cast<int64_t>(c.trace.size()));
+    const int64_t K = extract_clusters_dev(c, g, X, d, opt.fuse_tol, lab, cent);
+    if (cent && !(sink->skip_identity && K == n)) {  // ClusterAssignment::centroids (path.cpp:135)
+      hcent.resize(static_cast<size_t>(K * d));
+      d2h(c, hcent.data(), cent, K * d * sizeof(double));
+      sink->centroids(sink->user, t, K, d, hcent.data());
+    }
     if (terms_out) terms_out[t] = term;
     if (K_out) K_out[t] = K;
     if (labels_out) {
@@ -614,13 +646,7 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
     warm = opt.warm_start != 0;
     trace("path gamma done");
   }
-  if (async_out) {
-    CPB_CUDA(cudaStreamSynchronize(cs));
-    for (int s = 0; s < 2; ++s) {
-      cudaEventDestroy(snap_ready[s]);
-      cudaEventDestroy(copy_done[s]);
-    }
-  }
+  if (async_out) CPB_CUDA(cudaStreamSynchronize(cs));
   c.sync();
 }
 

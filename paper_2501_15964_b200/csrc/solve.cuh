@@ -15,6 +15,10 @@ struct SolveCache {
 };
 
 void validate_config(const cp_solver_config& c);  // objective.cpp:43-61
+// TraceRow (solvers.hpp:54-60) after a gap evaluation, when collect_trace
+inline void trace_gap(Ctx& c, const cp_solver_config& cfg, int64_t k, const GapOut& g, double elapsed) {
+  if (cfg.collect_trace) c.trace.push_back(cp_trace_row{k, g.fp, g.fd, g.gap, elapsed});
+}
 int64_t resolved_max_iter(const cp_solver_config& c);
 
 // Solve one instance.  X (d x n) and Z (d x E) are device buffers; when `warm`
@@ -28,8 +32,9 @@ int64_t extract_clusters_dev(Ctx& c, const Graph& g, const double* X, int64_t d,
                              double* centroids);
 
 // run_path (path.cpp:110-142).  Outputs are host buffers (nullable).
+// sink (nullable): per-gamma centroids (host d x K) and trace rows.
 void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, int64_t T,
                   const cp_solver_config& cfg, const cp_path_options& opt, double* X_out, double* Z_out,
-                  int64_t* labels_out, int64_t* K_out, cp_termination* terms_out);
+                  int64_t* labels_out, int64_t* K_out, cp_termination* terms_out, const cp_path_sink* sink = nullptr);
 
 }  // namespace cpb

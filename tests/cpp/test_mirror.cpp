@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "cluspath/graph.hpp"
+#include "cluspath/linalg.hpp"
 #include "cluspath/path.hpp"
 #include "cluspath/prox.hpp"
 #include "cluspath/solvers.hpp"
@@ -440,6 +441,321 @@ TEST_CASE("q = infinity through the mirror") {  // no reference counterpart (SUR
   CHECK(P(0, 0) == 2.0 && P(1, 0) == -1.0 && P(2, 0) == 0.5);
   Matrix Zp = project_columns(V, {1.0}, PenaltyNorm::linf);
   CHECK(Zp(0, 0) == 1.0 && Zp(1, 0) == 0.0 && Zp(2, 0) == 0.0);
+}
+
+// ---- linalg (test_linalg.cpp) ------------------------------------------------------------
+// Small dense helpers standing in for the Eigen calls of the reference tests.
+static Matrix matmul(const Matrix& A, const Matrix& B) {
+  Matrix C(A.rows(), B.cols());
+  for (Index c = 0; c < B.cols(); ++c)
+    for (Index k = 0; k < A.cols(); ++k)
+      for (Index r = 0; r < A.rows(); ++r) C(r, c) += A(r, k) * B(k, c);
+  return C;
+}
+static Matrix dense_solve(Matrix M, Matrix B) {  // Gaussian elimination with partial pivoting
+  const Index n = M.rows();
+  for (Index k = 0; k < n; ++k) {
+    Index p = k;
+    for (Index r = k + 1; r < n; ++r)
+      if (std::abs(M(r, k)) > std::abs(M(p, k))) p = r;
+    for (Index c = 0; c < n; ++c) std::swap(M(k, c), M(p, c));
+    for (Index c = 0; c < B.cols(); ++c) std::swap(B(k, c), B(p, c));
+    for (Index r = k + 1; r < n; ++r) {
+      const double f = M(r, k) / M(k, k);
+      for (Index c = k; c < n; ++c) M(r, c) -= f * M(k, c);
+      for (Index c = 0; c < B.cols(); ++c) B(r, c) -= f * B(k, c);
+    }
+  }
+  for (Index k = n - 1; k >= 0; --k)
+    for (Index c = 0; c < B.cols(); ++c) {
+      double s = B(k, c);
+      for (Index j = k + 1; j < n; ++j) s -= M(k, j) * B(j, c);
+      B(k, c) = s / M(k, k);
+    }
+  return B;
+}
+static double sym_lambda_max(Matrix A) {  // cyclic Jacobi eigenvalue sweeps
+  const Index n = A.rows();
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (Index p = 0; p < n; ++p)
+      for (Index q = p + 1; q < n; ++q) off += A(p, q) * A(p, q);
+    if (off < 1e-30) break;
+    for (Index p = 0; p < n; ++p)
+      for (Index q = p + 1; q < n; ++q) {
+        if (std::abs(A(p, q)) < 1e-300) continue;
+        const double th = 0.5 * std::atan2(2.0 * A(p, q), A(q, q) - A(p, p));
+        const double c = std::cos(th), s = std::sin(th);
+        for (Index k = 0; k < n; ++k) {
+          const double akp = A(k, p), akq = A(k, q);
+          A(k, p) = c * akp - s * akq;
+          A(k, q) = s * akp + c * akq;
+        }
+        for (Index k = 0; k < n; ++k) {
+          const double apk = A(p, k), aqk = A(q, k);
+          A(p, k) = c * apk - s * aqk;
+          A(q, k) = s * apk + c * aqk;
+        }
+      }
+  }
+  double m = A(0, 0);
+  for (Index k = 1; k < n; ++k) m = std::max(m, A(k, k));
+  return m;
+}
+static Matrix random_spd(std::mt19937_64& rng, Index n) {  // test_linalg.cpp:23-31
+  std::normal_distribution<double> gauss;
+  Matrix G(n, n);
+  for (Index r = 0; r < n; ++r)
+    for (Index c = 0; c < n; ++c) G(r, c) = gauss(rng);
+  Matrix M(n, n);
+  for (Index r = 0; r < n; ++r)
+    for (Index c = 0; c < n; ++c) {
+      double s = 0.0;
+      for (Index k = 0; k < n; ++k) s += G(r, k) * G(c, k);
+      M(r, c) = s;
+    }
+  for (Index k = 0; k < n; ++k) M(k, k) += 0.5;
+  return M;
+}
+static SparseMatrix path3_laplacian() {
+  WeightedGraph g(3, {{0, 1, 1.0}, {1, 2, 1.0}});
+  return IncidenceOperator(g).laplacian();
+}
+static double maxabs(const Matrix& a) {
+  double m = 0.0;
+  for (Index k = 0; k < a.size(); ++k) m = std::max(m, std::abs(a.data()[k]));
+  return m;
+}
+
+TEST_CASE("cholesky factor of I + rho L on the 3-path") {  // test_linalg.cpp:35-45
+  CholeskyFactor factor(path3_laplacian(), 1.0);
+  CHECK(factor.size() == 3);
+  CHECK(factor.rho() == 1.0);
+  Matrix rhs = Matrix::Zero(3, 1);
+  rhs(0, 0) = 1.0;
+  Matrix x = factor.solve(rhs);
+  CHECK(approx(x(0, 0), 0.625, 1e-14));
+  CHECK(approx(x(1, 0), 0.25, 1e-14));
+  CHECK(approx(x(2, 0), 0.125, 1e-14));
+}
+
+TEST_CASE("cholesky solve residual on random laplacians") {  // test_linalg.cpp:47-70
+  std::mt19937_64 rng(17);
+  std::uniform_real_distribution<double> unif(0.2, 3.0);
+  for (int trial = 0; trial < 10; ++trial) {
+    const Index n = 4 + static_cast<Index>(rng() % 12);
+    std::vector<Edge> edges;
+    for (Index i = 0; i + 1 < n; ++i) edges.push_back({i, i + 1, 1.0});
+    for (Index i = 0; i < n; ++i)
+      for (Index j = i + 2; j < n; ++j)
+        if ((rng() & 3u) == 0u) edges.push_back({i, j, 1.0});
+    WeightedGraph g(n, edges);
+    const double rho = unif(rng);
+    CholeskyFactor factor(IncidenceOperator(g).laplacian(), rho);
+    Matrix M = IncidenceOperator(g).laplacian().toDense();
+    for (Index k = 0; k < M.size(); ++k) M.data()[k] *= rho;
+    for (Index k = 0; k < n; ++k) M(k, k) += 1.0;
+    Matrix rhs(n, 3);
+    std::normal_distribution<double> gauss;
+    for (Index r = 0; r < n; ++r)
+      for (Index c = 0; c < 3; ++c) rhs(r, c) = gauss(rng);
+    Matrix x = factor.solve(rhs);
+    Matrix res = matmul(M, x);
+    for (Index k = 0; k < res.size(); ++k) res.data()[k] -= rhs.data()[k];
+    CHECK(maxabs(res) <= 1e-10 * (1.0 + maxabs(rhs)));
+  }
+}
+
+TEST_CASE("cholesky rejects invalid input") {  // test_linalg.cpp:72-78
+  CHECK_THROWS_AS(CholeskyFactor(path3_laplacian(), -1.0), std::invalid_argument);
+  SparseMatrix asym;
+  asym.rows_ = asym.cols_ = 2;
+  asym.colptr = {0, 0, 1};
+  asym.rowidx = {0};
+  asym.values = {1.0};  // (0, 1) only: not symmetric
+  CHECK_THROWS_AS(CholeskyFactor(asym, 1.0), std::invalid_argument);
+}
+
+TEST_CASE("linear operator factories agree with dense arithmetic") {  // test_linalg.cpp:80-110
+  std::mt19937_64 rng(3);
+  Matrix M = random_spd(rng, 5);
+  LinearOperator dense = LinearOperator::dense(M, true);
+  CHECK(dense.rows() == 5);
+  CHECK(dense.symmetric());
+  CHECK(dense.positive_definite());
+  SparseMatrix S;
+  S.rows_ = S.cols_ = 5;
+  S.colptr.push_back(0);
+  for (Index c = 0; c < 5; ++c) {
+    for (Index r = 0; r < 5; ++r)
+      if (M(r, c) != 0.0) S.rowidx.push_back(r), S.values.push_back(M(r, c));
+    S.colptr.push_back(static_cast<int64_t>(S.values.size()));
+  }
+  LinearOperator sparse = LinearOperator::sparse(S, true);
+  Matrix X(5, 2);
+  std::normal_distribution<double> gauss;
+  for (Index r = 0; r < 5; ++r)
+    for (Index c = 0; c < 2; ++c) X(r, c) = gauss(rng);
+  const Matrix MX = matmul(M, X);
+  CHECK(maxabs_diff(dense.apply(X), MX) <= 1e-14);
+  CHECK(maxabs_diff(sparse.apply(X), MX) <= 1e-14);
+  CHECK(maxabs_diff(LinearOperator::identity(5).apply(X), X) == 0.0);
+  Vector d{1, 2, 4, 8, 16};
+  Matrix Z = LinearOperator::jacobi(d).apply(X);
+  for (Index r = 0; r < 5; ++r)
+    for (Index c = 0; c < 2; ++c) CHECK(approx(Z(r, c), X(r, c) / d[static_cast<size_t>(r)]));
+  CHECK_THROWS_AS(LinearOperator::jacobi(Vector(3, 0.0)), std::invalid_argument);
+  CHECK_THROWS_AS(dense.apply(Matrix::Zero(4, 1)), std::invalid_argument);
+  CHECK_THROWS_AS(LinearOperator::dense(Matrix(2, 3)), std::invalid_argument);
+}
+
+TEST_CASE("pcg solves a frozen 2x2 system") {  // test_linalg.cpp:112-118
+  Matrix M(2, 2);
+  M(0, 0) = 4, M(0, 1) = 1, M(1, 0) = 1, M(1, 1) = 3;
+  PcgResult res = pcg(LinearOperator::dense(M, true), Vector{1, 2}, nullptr, 1e-12, 50);
+  CHECK(res.converged);
+  CHECK(approx(res.x(0, 0), 1.0 / 11.0, 1e-10));
+  CHECK(approx(res.x(1, 0), 7.0 / 11.0, 1e-10));
+  CHECK(res.residual <= 1e-12);
+}
+
+TEST_CASE("pcg on the identity converges in one iteration") {  // test_linalg.cpp:120-127
+  Vector b{1, -2, 3, -4};
+  PcgResult res = pcg(LinearOperator::identity(4), b, nullptr, 1e-10, 10);
+  CHECK(res.converged);
+  CHECK(res.iterations == 1);
+  double e = 0.0;
+  for (Index k = 0; k < 4; ++k) e = std::max(e, std::abs(res.x(k, 0) - b[static_cast<size_t>(k)]));
+  CHECK(e <= 1e-14);
+}
+
+TEST_CASE("pcg matches dense solves on random SPD systems") {  // test_linalg.cpp:129-144
+  std::mt19937_64 rng(29);
+  std::normal_distribution<double> gauss;
+  for (int trial = 0; trial < 8; ++trial) {
+    const Index n = 20;
+    Matrix M = random_spd(rng, n);
+    Matrix b(n, 1);
+    for (Index i = 0; i < n; ++i) b(i, 0) = gauss(rng);
+    LinearOperator op = LinearOperator::dense(M, true);
+    Vector dg(static_cast<size_t>(n));
+    for (Index i = 0; i < n; ++i) dg[static_cast<size_t>(i)] = M(i, i);
+    LinearOperator precond = LinearOperator::jacobi(dg);
+    PcgResult res = pcg(op, b, &precond, 1e-12, 400);
+    Matrix exact = dense_solve(M, b);
+    CHECK(res.converged);
+    double e = 0.0, ne = 0.0;
+    for (Index i = 0; i < n; ++i) e += std::pow(res.x(i, 0) - exact(i, 0), 2), ne += exact(i, 0) * exact(i, 0);
+    CHECK(std::sqrt(e) <= 1e-8 * (1.0 + std::sqrt(ne)));
+  }
+}
+
+TEST_CASE("pcg handles matrix-block right-hand sides") {  // test_linalg.cpp:146-160
+  std::mt19937_64 rng(31);
+  std::normal_distribution<double> gauss;
+  const Index n = 12;
+  Matrix M = random_spd(rng, n);
+  Matrix B(n, 3);
+  for (Index r = 0; r < n; ++r)
+    for (Index c = 0; c < 3; ++c) B(r, c) = gauss(rng);
+  PcgResult res = pcg(LinearOperator::dense(M, true), B, nullptr, 1e-11, 600);
+  Matrix exact = dense_solve(M, B);
+  CHECK(res.converged);
+  CHECK(maxabs_diff(res.x, exact) <= 1e-7 * (1.0 + maxabs(exact)));
+}
+
+TEST_CASE("pcg rejects indefinite operators and zero rhs is immediate") {  // test_linalg.cpp:162-174
+  Matrix Mneg(3, 3);
+  for (Index k = 0; k < 3; ++k) Mneg(k, k) = -1.0;
+  CHECK_THROWS_AS(pcg(LinearOperator::dense(Mneg, false), Vector{1, 1, 1}, nullptr, 1e-10, 10), std::runtime_error);
+  PcgResult res = pcg(LinearOperator::identity(3), Vector(3, 0.0), nullptr, 1e-10, 10);
+  CHECK(res.converged);
+  CHECK(res.iterations == 0);
+  CHECK(maxabs(res.x) == 0.0);
+}
+
+TEST_CASE("pcg and power iteration on a host functor operator") {  // LinearOperator(rows, fn) (linalg.hpp:45)
+  Matrix M(2, 2);
+  M(0, 0) = 4, M(0, 1) = 1, M(1, 0) = 1, M(1, 1) = 3;
+  int calls = 0;
+  LinearOperator op(2, [&](const Matrix& x) {
+    ++calls;
+    return matmul(M, x);
+  }, true, true);
+  PcgResult res = pcg(op, Vector{1, 2}, nullptr, 1e-12, 50);
+  CHECK(res.converged && calls >= 2);
+  CHECK(approx(res.x(0, 0), 1.0 / 11.0, 1e-10) && approx(res.x(1, 0), 7.0 / 11.0, 1e-10));
+  CHECK(approx(power_iteration(op), 3.5 + std::sqrt(1.25), 1e-8));
+  LinearOperator bad(2, [](const Matrix&) -> Matrix { throw std::invalid_argument("functor says no"); });
+  CHECK_THROWS_AS(pcg(bad, Vector{1, 2}, nullptr, 1e-12, 5), std::invalid_argument);
+}
+
+TEST_CASE("power iteration finds the top eigenvalue") {  // test_linalg.cpp:176-195
+  Matrix D = Matrix::Zero(2, 2);
+  D(0, 0) = 1.0;
+  D(1, 1) = 5.0;
+  CHECK(approx(power_iteration(LinearOperator::dense(D, true)), 5.0, 1e-8));
+  WeightedGraph g(2, {{0, 1, 1.0}});
+  CHECK(approx(power_iteration(LinearOperator::sparse(IncidenceOperator(g).laplacian(), false)), 2.0, 1e-8));
+  CHECK(power_iteration(LinearOperator::dense(Matrix::Zero(3, 3), false)) == 0.0);
+  SparseMatrix L = path3_laplacian();
+  CHECK(approx(power_iteration(LinearOperator::sparse(L, false)), sym_lambda_max(L.toDense()), 1e-8));
+}
+
+TEST_CASE("power iteration on random laplacians matches dense spectra") {  // test_linalg.cpp:197-212
+  std::mt19937_64 rng(41);
+  for (int trial = 0; trial < 6; ++trial) {
+    const Index n = 5 + static_cast<Index>(rng() % 10);
+    std::vector<Edge> edges;
+    for (Index i = 0; i + 1 < n; ++i) edges.push_back({i, i + 1, 1.0});
+    for (Index i = 0; i < n; ++i)
+      for (Index j = i + 2; j < n; ++j)
+        if ((rng() & 1u) == 0u) edges.push_back({i, j, 1.0});
+    WeightedGraph g(n, edges);
+    SparseMatrix L = IncidenceOperator(g).laplacian();
+    const double lmax = power_iteration(LinearOperator::sparse(L, false), 1e-12, 20000);
+    CHECK(approx(lmax, sym_lambda_max(L.toDense()), 1e-6));
+  }
+}
+
+TEST_CASE("norm values, prox_norm_into and project_dual_ball_into") {  // prox.hpp:14-26 (test_prox.cpp:28-60)
+  CHECK(approx(norm_value(Vector{3.0, -4.0}, PenaltyNorm::l2), 5.0, 1e-15));
+  CHECK(approx(norm_value(Vector{3.0, -4.0}, PenaltyNorm::l1), 7.0, 1e-15));
+  CHECK(approx(dual_norm_value(Vector{3.0, -4.0}, PenaltyNorm::l1), 4.0, 1e-15));
+  CHECK(approx(dual_norm_value(Vector{3.0, -4.0}, PenaltyNorm::l2), 5.0, 1e-15));
+  Vector out;
+  prox_norm_into(Vector{3.0, 4.0}, 2.5, PenaltyNorm::l2, out);
+  CHECK(approx(out[0], 1.5, 1e-15) && approx(out[1], 2.0, 1e-15));
+  project_dual_ball_into(Vector{3.0, -0.5}, 1.0, PenaltyNorm::l1, out);
+  CHECK(out[0] == 1.0 && out[1] == -0.5);
+  CHECK_THROWS_AS(prox_norm_into(Vector{1.0}, -1.0, PenaltyNorm::l2, out), std::invalid_argument);
+}
+
+TEST_CASE("solver trace rows and per-gamma centroids") {  // solvers.hpp:54-66, path.cpp:135
+  Matrix A(2, 6);
+  const double pts[6][2] = {{0, 0}, {0.1, 0}, {0, 0.1}, {3, 3}, {3.1, 3}, {3, 3.1}};
+  for (Index c = 0; c < 6; ++c) A(0, c) = pts[c][0], A(1, c) = pts[c][1];
+  DataMatrix data = make_data_matrix(A);
+  WeightedGraph g = compute_knn_weights(data, 2, 0.5);
+  SolverConfig cfg;
+  cfg.collect_trace = true;
+  ProblemInstance inst(data, g, 0.3, PenaltyNorm::l2);
+  Solution sol = solve(inst, cfg);
+  CHECK(!sol.trace.empty() && sol.trace.front().iter == 0);
+  CHECK(approx(sol.trace.back().gap, sol.termination.gap, 0.0));
+  GammaSchedule sched = make_schedule(0.01, 5.0, 5, Spacing::geometric);
+  PathResult r = run_path(data, g, PenaltyNorm::l2, sched, cfg);
+  for (size_t t = 0; t < r.assignments.size(); ++t) {
+    const ClusterAssignment& a = r.assignments[t];
+    ClusterAssignment e = extract_clusters(r.solutions[t].X, g);
+    CHECK(a.K == e.K && a.labels == e.labels);
+    CHECK(a.centroids.rows() == 2 && a.centroids.cols() == a.K);
+    CHECK(maxabs_diff(a.centroids, e.centroids) == 0.0);
+    CHECK(!r.solutions[t].trace.empty());
+  }
+  Matrix Xcopy = r.solutions[0].X;  // deep copy out of the path's shared host slab
+  Xcopy(0, 0) += 1.0;
+  CHECK(Xcopy(0, 0) != r.solutions[0].X(0, 0));
 }
 
 int main() {

@@ -231,9 +231,11 @@ def test_connected_components(cp, orc):
 def test_laplacian_lambda_max(cp, orc):
     g = cp.WeightedGraph(3, [(0, 1, 1.0), (1, 2, 1.0)])
     assert cp.IncidenceOperator(g).laplacian_lambda_max() == pytest.approx(3.0, rel=1e-8)
-    A = circle(orc, 30)
-    g, og = check_graph(cp, orc, A, 10, 0.5)
-    assert cp.IncidenceOperator(g).laplacian_lambda_max() == pytest.approx(orc.power_laplacian(og), rel=1e-12)
+    # the device reproduces the reference's CSC product order and Eigen's reduction order, so
+    # lambda_max is bitwise the oracle's (small graphs in shared memory, large ones in HBM)
+    for A in (circle(orc, 30), circle(orc, 100), mixture(orc, 4000, 3)):
+        g, og = check_graph(cp, orc, A, 10, 0.5)
+        assert cp.IncidenceOperator(g).laplacian_lambda_max() == orc.power_laplacian(og)
 
 
 # ---- prox (test_prox.cpp) ------------------------------------------------------------
