@@ -15,7 +15,10 @@ from .cluspath import (Algorithm, ClusterAssignment, Context, DataMatrix, GammaS
                        extract_clusters, flush_l2, gather_row_lists, init_comm_from_torch, knn_rows_into, nccl_unique_id, generate_gaussian_mixture, kkt_residual, launch_count,
                        make_data_matrix, make_schedule, normals, penalty_norm_from_q, timer_start, timer_stop,
                        primal_objective, project_columns, prox_jacobian, prox_jacobian_apply, ProxJacobian, shard_rows, prox_columns, prox_jacobian_diag, recover_primal, run_path,
-                       solve, ssnal_hessian_apply, ssnal_phi_gradient, ssnal_phi_value, two_point_closed_form)
+                       solve, ssnal_hessian_apply, ssnal_phi_gradient, ssnal_phi_value, two_point_closed_form,
+                       CholeskyFactor, LinearOperator, PcgResult, TraceRow, dual_norm_value, moreau_check, norm_value,
+                       pcg, pinned_empty, power_iteration, project_dual_ball, project_dual_ball_into, prox_norm,
+                       prox_norm_into)
 
 from .io import export_graph_csv, format_double, path_result_to_json, write_matrix_csv
 

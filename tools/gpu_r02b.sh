@@ -1,0 +1,3 @@
+set -x
+timeout 900 python -m pytest tests -m gpu -x -q -rA > gpurun_out/r2b_pytest.log 2>&1; echo pytest rc=$?
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/r2b_bench_c3.json 2> gpurun_out/r2b_bench_c3.err; echo bench rc=$?
