@@ -966,6 +966,124 @@ inline PathResult run_path(const DataMatrix& data, const WeightedGraph& graph, P
   return r;
 }
 
+// ---- bench.hpp: performance profiles over device solves (bench.cpp:23-116) -------
+struct BenchTask {
+  const DataMatrix* data = nullptr;
+  const WeightedGraph* graph = nullptr;
+  PenaltyNorm norm = PenaltyNorm::l2;
+  GammaSchedule schedule;
+};
+struct MethodCurve {
+  Algorithm method = Algorithm::SSNAL;
+  std::vector<std::pair<double, Index>> points;  // (tau, problems solved within tau * T)
+  Index solved_total = 0;
+  double full_time = 0.0;
+};
+struct PerfProfile {
+  double baseline_T = 0.0;
+  Index problem_count = 0;
+  std::vector<MethodCurve> curves;
+};
+struct BenchOptions {
+  double epsilon = 1e-6;
+  Index tau_max = 10;
+  std::optional<double> cutoff_override;
+  SolverConfig base_config;
+  bool warm_start = true;
+};
+namespace detail {
+struct SweepOutcome {
+  std::vector<double> finish;
+  double total_time = 0.0;
+};
+inline SweepOutcome sweep(const std::vector<BenchTask>& tasks, Algorithm method, const BenchOptions& options,
+                          const double* budget) {
+  SweepOutcome out;
+  for (const BenchTask& task : tasks) {
+    std::optional<Solution> prev;
+    for (double gamma : task.schedule.values) {
+      if (budget && out.total_time >= *budget) return out;
+      SolverConfig config = options.base_config;
+      config.algorithm = method;
+      config.epsilon = options.epsilon;
+      if (budget) {
+        const double remaining = *budget - out.total_time;
+        config.time_limit = config.time_limit ? std::min(*config.time_limit, remaining) : remaining;
+      }
+      ProblemInstance inst(*task.data, *task.graph, gamma, task.norm);
+      const Solution* warm = (options.warm_start && prev) ? &*prev : nullptr;
+      Solution sol = solve(inst, config, warm);
+      out.total_time += sol.termination.wall_time;
+      if (sol.termination.converged && (!budget || out.total_time <= *budget)) out.finish.push_back(out.total_time);
+      prev = std::move(sol);
+    }
+  }
+  return out;
+}
+}  // namespace detail
+inline PerfProfile run_bench(const std::vector<BenchTask>& tasks, const std::vector<Algorithm>& methods,
+                             const BenchOptions& options) {
+  if (methods.empty()) throw std::invalid_argument("run_bench: no methods given");
+  if (tasks.empty()) throw std::invalid_argument("run_bench: no tasks given");
+  Index problems = 0;
+  for (const BenchTask& t : tasks) {
+    if (!t.data || !t.graph) throw std::invalid_argument("run_bench: task is missing data or graph");
+    if (t.schedule.values.empty()) throw std::invalid_argument("run_bench: task has an empty schedule");
+    problems += static_cast<Index>(t.schedule.values.size());
+  }
+  if (options.tau_max < 1) throw std::invalid_argument("run_bench: tau_max must be >= 1");
+  options.base_config.validate();
+  std::vector<detail::SweepOutcome> uncapped;
+  for (Algorithm m : methods) uncapped.push_back(detail::sweep(tasks, m, options, nullptr));
+  size_t best = 0;
+  for (size_t i = 1; i < methods.size(); ++i) {
+    const bool more = uncapped[i].finish.size() > uncapped[best].finish.size();
+    const bool tie = uncapped[i].finish.size() == uncapped[best].finish.size() &&
+                     uncapped[i].total_time < uncapped[best].total_time;
+    if (more || tie) best = i;
+  }
+  if (uncapped[best].finish.empty()) throw std::runtime_error("run_bench: no baseline (no method solved any problem)");
+  const double T = uncapped[best].total_time;
+  const double cutoff = options.cutoff_override ? *options.cutoff_override : 10.0 * T;
+  PerfProfile profile;
+  profile.baseline_T = T;
+  profile.problem_count = problems;
+  for (size_t i = 0; i < methods.size(); ++i) {
+    detail::SweepOutcome rerun;
+    const detail::SweepOutcome* capped = &uncapped[i];
+    if (uncapped[i].total_time > cutoff) {
+      rerun = detail::sweep(tasks, methods[i], options, &cutoff);
+      capped = &rerun;
+    }
+    MethodCurve curve;
+    curve.method = methods[i];
+    curve.full_time = uncapped[i].total_time;
+    curve.solved_total = static_cast<Index>(capped->finish.size());
+    for (Index tau = 1; tau <= options.tau_max; ++tau) {
+      const double horizon = std::min(static_cast<double>(tau) * T, cutoff);
+      Index count = 0;
+      for (double t : capped->finish) count += t <= horizon ? 1 : 0;
+      curve.points.emplace_back(static_cast<double>(tau), count);
+    }
+    profile.curves.push_back(std::move(curve));
+  }
+  return profile;
+}
+inline std::string format_double(double value);
+inline std::string perf_profile_csv(const PerfProfile& profile) {
+  std::string csv = "method,tau,solved\n";
+  for (const MethodCurve& c : profile.curves)
+    for (const auto& [tau, solved] : c.points) {
+      csv += algorithm_name(c.method);
+      csv += ',';
+      csv += format_double(tau);
+      csv += ',';
+      csv += std::to_string(solved);
+      csv += '\n';
+    }
+  return csv;
+}
+
 // ---- output formats (io.cpp:14-18, 120-140; path.cpp:144-177) ------------------
 inline std::string format_double(double value) {
   char buf[64];

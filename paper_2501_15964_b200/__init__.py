@@ -21,5 +21,6 @@ from .cluspath import (Algorithm, ClusterAssignment, Context, DataMatrix, GammaS
                        prox_norm_into)
 
 from .io import export_graph_csv, format_double, path_result_to_json, write_matrix_csv
+from .perf import BenchOptions, BenchTask, MethodCurve, PerfProfile, perf_profile_csv, run_bench
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "cluspath/bench.hpp"
 #include "cluspath/graph.hpp"
 #include "cluspath/linalg.hpp"
 #include "cluspath/path.hpp"
@@ -756,6 +757,81 @@ TEST_CASE("solver trace rows and per-gamma centroids") {  // solvers.hpp:54-66, 
   Matrix Xcopy = r.solutions[0].X;  // deep copy out of the path's shared host slab
   Xcopy(0, 0) += 1.0;
   CHECK(Xcopy(0, 0) != r.solutions[0].X(0, 0));
+}
+
+// ---- bench (test_bench.cpp) -----------------------------------------------------------------
+struct BenchFixture {  // test_bench.cpp:14-30
+  SyntheticData synth;
+  WeightedGraph graph;
+  GammaSchedule schedule;
+  BenchFixture()
+      : synth(generate_gaussian_mixture({Vector{-2.0, 0.0}, Vector{2.0, 0.0}}, 0.4, 10, 11)),
+        graph(compute_knn_weights(synth.data, 4, 0.5)),
+        schedule(make_schedule(0.1, 2.0, 5, Spacing::geometric)) {}
+  BenchTask task() const { return BenchTask{&synth.data, &graph, PenaltyNorm::l2, schedule}; }
+};
+
+TEST_CASE("a single method is its own baseline and solves everything at tau = 1") {  // test_bench.cpp:34-52
+  BenchFixture f;
+  BenchOptions options;
+  PerfProfile profile = run_bench({f.task()}, {Algorithm::SSNAL}, options);
+  CHECK(profile.problem_count == 5 && profile.baseline_T > 0.0 && profile.curves.size() == 1);
+  const MethodCurve& curve = profile.curves[0];
+  CHECK(curve.method == Algorithm::SSNAL && curve.solved_total == 5);
+  CHECK(approx(curve.full_time, profile.baseline_T));
+  CHECK(curve.points.size() == 10 && curve.points[0].first == 1.0 && curve.points[0].second == 5);
+  for (const auto& [tau, solved] : curve.points) CHECK(solved == 5);
+}
+
+TEST_CASE("curves are nondecreasing in tau and bounded by the problem count") {  // test_bench.cpp:54-78
+  BenchFixture f;
+  BenchOptions options;
+  PerfProfile profile = run_bench({f.task()}, {Algorithm::SSNAL, Algorithm::ADMM, Algorithm::FastAMA}, options);
+  CHECK(profile.problem_count == 5 && profile.curves.size() == 3);
+  for (const MethodCurve& curve : profile.curves) {
+    Index prev = 0;
+    for (const auto& [tau, solved] : curve.points) {
+      CHECK(solved >= prev && solved <= profile.problem_count);
+      prev = solved;
+    }
+    CHECK(curve.points.back().second == curve.solved_total);
+    if (curve.solved_total == profile.problem_count) CHECK(curve.full_time >= profile.baseline_T);
+  }
+}
+
+TEST_CASE("a zero cutoff override leaves every curve at zero; bench validates inputs") {  // test_bench.cpp:80-116
+  BenchFixture f;
+  BenchOptions options;
+  options.cutoff_override = 0.0;
+  PerfProfile profile = run_bench({f.task()}, {Algorithm::SSNAL, Algorithm::ADMM}, options);
+  for (const MethodCurve& curve : profile.curves) {
+    CHECK(curve.solved_total == 0 && curve.full_time > 0.0);
+    for (const auto& [tau, solved] : curve.points) CHECK(solved == 0);
+  }
+  BenchOptions hard;
+  hard.epsilon = 1e-14;
+  hard.base_config.max_iter = 1;
+  CHECK_THROWS_AS(run_bench({f.task()}, {Algorithm::ADMM, Algorithm::FastAMA}, hard), std::runtime_error);
+  BenchOptions plain;
+  CHECK_THROWS_AS(run_bench({}, {Algorithm::SSNAL}, plain), std::invalid_argument);
+  CHECK_THROWS_AS(run_bench({f.task()}, {}, plain), std::invalid_argument);
+  BenchTask broken = f.task();
+  broken.data = nullptr;
+  CHECK_THROWS_AS(run_bench({broken}, {Algorithm::SSNAL}, plain), std::invalid_argument);
+  plain.tau_max = 0;
+  CHECK_THROWS_AS(run_bench({f.task()}, {Algorithm::SSNAL}, plain), std::invalid_argument);
+}
+
+TEST_CASE("profile CSV has one labeled row per curve point") {  // test_bench.cpp:118-140
+  BenchFixture f;
+  BenchOptions options;
+  options.tau_max = 3;
+  const std::string csv = perf_profile_csv(run_bench({f.task()}, {Algorithm::SSNAL, Algorithm::ADMM}, options));
+  CHECK(csv.rfind("method,tau,solved\n", 0) == 0);
+  CHECK(csv.find("ssnal,1,") != std::string::npos && csv.find("admm,3,") != std::string::npos);
+  int rows = 0;
+  for (char ch : csv) rows += ch == '\n';
+  CHECK(rows == 7);
 }
 
 int main() {

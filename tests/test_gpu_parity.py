@@ -576,6 +576,30 @@ def test_c1_exact_config_matches_oracle(cp, orc):
         assert res.assignments[t].K == ores["K"][t]
 
 
+@pytest.mark.parametrize("shape", ["c1", "c2cap"])
+def test_admm_matches_oracle_cholesky(cp, orc, shape):
+    """ADMM's X-update (admm.cpp:38-62): the reference factors I + rho L once (SimplicialLLT,
+    linalg.cpp:32-54) and the oracle with an exact envelope Cholesky; the device solves the
+    same system by warm-started Laplacian PCG to 1e-13.  c1: BASELINE configs[0]'s data, the
+    20-gamma ADMM path to convergence; c2cap: C2-shaped rows (d = 784) with every solve capped
+    at 25 ADMM iterations (bench-sized systems, a bounded oracle run).  X within 1e-6, labels
+    equal, the stopping iteration within one gap check."""
+    if shape == "c1":
+        A, T, cap = circle(orc, 100), 20, 0
+    else:
+        A, T, cap = mixture(orc, 100, 784, m=10, seed=42), 3, 25
+    g, og = check_graph(cp, orc, A, 10, 0.5)
+    sched = cp.make_schedule(0.01, 10.0, 20)
+    sched.values = sched.values[:T]
+    res = cp.run_path(cp.DataMatrix(A), g, 2, sched, cp.SolverConfig(algorithm=cp.Algorithm.ADMM, max_iter=cap))
+    ores = orc.run_path(A, og, 2, sched.values, orc.config("admm", max_iter=cap))
+    for t in range(T):
+        assert abs(res.stats[t].iterations - ores["terms"][t]["iterations"]) <= 1
+        assert res.stats[t].converged == bool(ores["terms"][t]["converged"])
+        assert np.linalg.norm(res.solutions[t].X - ores["X"][t]) <= 1e-6 * np.linalg.norm(ores["X"][t])
+        assert np.array_equal(res.assignments[t].labels, ores["labels"][t])
+
+
 @pytest.mark.parametrize("d", [64, 96])
 def test_edge_ring_wraps_match_oracle(cp, orc, d):
     """Short rows run the TMA edge kernels with an 8-deep per-warp ring; with

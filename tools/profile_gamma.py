@@ -1,7 +1,8 @@
 """Per-gamma kernel profile of a path: the warm-started schedule solved one
 gamma at a time through cp.solve (the same per-gamma solve run_path does),
 with the library's CUDA-event stats reset per gamma.
-usage: profile_gamma.py <config> [t0] [t1] [out.json]  (gammas t0..t1-1 are profiled; earlier ones run unprofiled)"""
+usage: profile_gamma.py <config> [t0] [t1] [out.json] [time_limit_s]
+(gammas t0..t1-1 are profiled; earlier ones run unprofiled)"""
 import json
 import os
 import sys
@@ -15,13 +16,14 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 cfg = dict(bench.CONFIGS[name])
 t0 = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 t1 = int(sys.argv[3]) if len(sys.argv) > 3 else cfg["T"]
-out = sys.argv[4] if len(sys.argv) > 4 else None
+out = sys.argv[4] if len(sys.argv) > 4 and sys.argv[4] != "-" else None
+tlim = float(sys.argv[5]) if len(sys.argv) > 5 else None
 A = bench.make_input(cp, cfg)
 ctx = cp.default_context()
 data = cp.DataMatrix(A, ctx=ctx)
 g = cp.compute_knn_weights(data, cfg["k"], cfg["phi"])
 sched = cp.make_schedule(cfg["gamma"][0], cfg["gamma"][1], cfg["T"])
-scfg = cp.SolverConfig(algorithm=cp.algorithm_from_name(cfg["algorithm"]))
+scfg = cp.SolverConfig(algorithm=cp.algorithm_from_name(cfg["algorithm"]), time_limit=tlim)
 warm = None
 rep = {"config": name, "env": {k: v for k, v in os.environ.items() if k.startswith("CPB_")}, "per_gamma": []}
 for t in range(t1):
