@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "comm.cuh"
+#include "gather.cuh"
 #include "linalg.cuh"
 #include "solve.cuh"
 
@@ -631,7 +632,14 @@ int cp_ssnal_hessian_apply(cp_ctx* ctx, const cp_data* A, const cp_graph* g, dou
     double* dd = upload(c, "api.D", D, m);
     double* Ap = c.buf<double>("api.Ap", m);
     double* part = c.buf<double>("api.hpart", 2 * static_cast<size_t>(c.sm_count) * 8 + 2);
-    cpb::hess_apply(P, dd, V, jal, jbe, thr, sigma, Ap, part);
+    unsigned *mask = nullptr, *sgn = nullptr;  // q = 1 / inf: the solver's bit-mask Hessian path
+    if (q != 2 && E > 0) {
+      const size_t words = static_cast<size_t>(E) * ((P.d() + 31) / 32);
+      mask = c.buf<unsigned>("api.mask", words + 1);
+      sgn = c.buf<unsigned>("api.sgn", words + 1);
+      cpb::edge_masks(c, *P.g, V, q == 1 ? thr : jal, P.d(), q, mask, sgn);
+    }
+    cpb::hess_apply(P, dd, V, jal, jbe, thr, sigma, Ap, part, nullptr, mask, sgn);
     cpb::d2h(c, out, Ap, m * sizeof(double));
   });
 }

@@ -376,7 +376,9 @@ __global__ void __launch_bounds__(256) k_edge_dot(const double* __restrict__ P, 
 __global__ void __launch_bounds__(256) k_edge_dot_inf(const double* __restrict__ P, const double* __restrict__ V,
                                                       const double* __restrict__ jal, const double* __restrict__ jbe,
                                                       const int* __restrict__ ei, const int* __restrict__ ej,
-                                                      const int* __restrict__ elist, int64_t e0, int64_t E, int d, double* __restrict__ bc, const int* active) {
+                                                      const int* __restrict__ elist, int64_t e0, int64_t E, int d, double* __restrict__ bc, const int* active,
+                                                      const unsigned* __restrict__ mask, const unsigned* __restrict__ sgn) {
+  const int W = (d + 31) >> 5;
   if (active && !*active) return;
   const int lane = threadIdx.x & 31;
   for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; i < E;
@@ -391,9 +393,18 @@ __global__ void __launch_bounds__(256) k_edge_dot_inf(const double* __restrict__
     const double* pb = P + static_cast<int64_t>(ej[l]) * d;
     const double* vl = V + l * d;
     double c = 0.0;
-    for (int f = lane; f < d; f += 32) {
-      const double vf = vl[f];
-      if (fabs(vf) > th) c += vf > 0.0 ? pa[f] - pb[f] : pb[f] - pa[f];
+    if (mask) {  // S and sign(v) as bits (edge_masks): no V row read
+      const unsigned* mw = mask + l * W;
+      const unsigned* sw = sgn + l * W;
+      for (int f = lane, k = 0; f < d; f += 32, ++k) {
+        const unsigned bit = 1u << lane;
+        if (mw[k] & bit) c += (sw[k] & bit) ? pa[f] - pb[f] : pb[f] - pa[f];
+      }
+    } else {
+      for (int f = lane; f < d; f += 32) {
+        const double vf = vl[f];
+        if (fabs(vf) > th) c += vf > 0.0 ? pa[f] - pb[f] : pb[f] - pa[f];
+      }
     }
     c = warp_sum(c);
     if (lane == 0) bc[l] = be * c;
@@ -409,11 +420,15 @@ __global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, co
                                                 const int* __restrict__ adj_e, const int* __restrict__ adj_o,
                                                 const int* __restrict__ order, int64_t n, int d, int nch,
                                                 double sigma, int q, double* __restrict__ Ap, double* part,
-                                                const int* active) {
+                                                const int* active, const unsigned* __restrict__ mask,
+                                                const unsigned* __restrict__ sgn) {
   if (active && !*active) return;
   __shared__ double sh[32];
   double s_a = 0.0, s_b = 0.0;
+  const int W = (d + 31) >> 5;
   ITEMS_BEGIN(n, nch)
+  const int w0 = static_cast<int>(it_ % nch) * NF;  // word of feature f0 + 32 k is w0 + k (bit = lane)
+  const unsigned lbit = 1u << lane;
   double pv[NF], acc[NF];
   double diag_coef = 0.0;  // sum over incident edges of (1 - alpha_l), q = 2
 #pragma unroll
@@ -440,15 +455,18 @@ __global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, co
         eb[u] = __shfl_sync(kFull, my_b, src);
       }
       double po[kEB][NF], vv[kEB][NF];
+      unsigned mb[kEB][NF], sb[kEB][NF];  // q = 1 / inf with masks: S membership and sign bits
 #pragma unroll
       for (int u = 0; u < kEB; ++u) {
         const bool ok = u0 + u < cnt;
-        const bool need_v = ok && (q != 2 || eb[u] != 0.0);
+        const bool need_v = ok && (q != 2 || eb[u] != 0.0) && !(mask && q != 2);
 #pragma unroll
         for (int k = 0; k < NF; ++k) {
           const int f = f0 + 32 * k;
           po[u][k] = (ok && f < d) ? __ldg(P + static_cast<int64_t>(lo[u]) * d + f) : 0.0;
           vv[u][k] = (need_v && f < d) ? __ldcs(V + static_cast<int64_t>(le[u]) * d + f) : 0.0;
+          mb[u][k] = (mask && ok && f < d) ? mask[static_cast<int64_t>(le[u]) * W + w0 + k] : 0u;
+          sb[u][k] = (sgn && ok && f < d && q == 0) ? sgn[static_cast<int64_t>(le[u]) * W + w0 + k] : 0u;
         }
       }
       if (q == 2) {
@@ -477,7 +495,9 @@ __global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, co
           for (int k = 0; k < NF; ++k) {
             const double w = plus ? pv[k] - po[u][k] : po[u][k] - pv[k];
             const double vf = vv[u][k];
-            const double y = th < 0.0 ? w : (fabs(vf) > th ? w - (vf > 0.0 ? eb[u] : -eb[u]) : 0.0);
+            const bool in_s = mask ? (mb[u][k] & lbit) != 0u : fabs(vf) > th;
+            const bool pos = mask ? (sb[u][k] & lbit) != 0u : vf > 0.0;
+            const double y = th < 0.0 ? w : (in_s ? w - (pos ? eb[u] : -eb[u]) : 0.0);
             acc[k] = plus ? acc[k] + y : acc[k] - y;
           }
         }
@@ -489,7 +509,8 @@ __global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, co
 #pragma unroll
           for (int k = 0; k < NF; ++k) {
             const double w = plus ? pv[k] - po[u][k] : po[u][k] - pv[k];
-            const double y = w - (fabs(vv[u][k]) > ea[u] ? w : 0.0);
+            const bool act = mask ? (mb[u][k] & lbit) != 0u : fabs(vv[u][k]) > ea[u];
+            const double y = w - (act ? w : 0.0);
             acc[k] = plus ? acc[k] + y : acc[k] - y;
           }
         }
@@ -882,9 +903,43 @@ int gather_grad_diag(Ctx& c, const Graph& g, const double* X, const double* A, c
   return ng.grid;
 }
 
+// Per-edge feature bits of the q = 1 / q = inf generalized Jacobian, built once per
+// Newton system from V (one coalesced pass, warp ballots): mask bit f = [|v_f| > t]
+// (q = 1) or [|v_f| > theta] (q = inf), sgn bit f = [v_f > 0].  The Hessian's gathers
+// then read 2 bits per feature instead of the 8-byte V element (same decisions, bitwise).
+__global__ void __launch_bounds__(256) k_edge_masks(const double* __restrict__ V, const double* __restrict__ thr,
+                                                    int64_t E, int d, int q, unsigned* __restrict__ mask,
+                                                    unsigned* __restrict__ sgn) {
+  const int lane = threadIdx.x & 31, W = (d + 31) >> 5;
+  for (int64_t l = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; l < E;
+       l += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const double t = thr[l];
+    const double* v = V + l * d;
+    for (int k = 0; k < W; ++k) {
+      const int f = 32 * k + lane;
+      const double vf = f < d ? __ldcs(v + f) : 0.0;
+      const unsigned m = __ballot_sync(kFull, f < d && fabs(vf) > t);
+      const unsigned sg = __ballot_sync(kFull, f < d && vf > 0.0);
+      if (lane == 0) {
+        mask[l * W + k] = m;
+        sgn[l * W + k] = sg;
+      }
+    }
+  }
+}
+
+void edge_masks(Ctx& c, const Graph& g, const double* V, const double* thr, int64_t d, int q, unsigned* mask,
+                unsigned* sgn) {
+  if (g.E == 0) return;
+  const int grid = std::max(1, std::min(cdiv(g.E, 8), c.sm_count * 8));
+  Ctx::Timer tm(&c, "edge_masks", (static_cast<double>(g.E) * d + g.E) * 8.0 + 2.0 * g.E * ((d + 31) / 32) * 4.0);
+  k_edge_masks<<<grid, 256, 0, c.s>>>(V, thr, g.E, static_cast<int>(d), q, mask, sgn);
+  CPB_LAUNCH_CHECK();
+}
+
 int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,
                   const double* thr, int64_t d, double sigma, int q, double* bc, double* Ap, double* part,
-                  const int* active) {
+                  const int* active, const unsigned* mask, const unsigned* sgn) {
   if (q == 2 && g.E > 0 && hess_tma_supported(d)) return hess_tma(c, g, P, V, jal, jbe, d, sigma, Ap, part, active);
   if (q == 2 && g.E > 0 && d % 2 == 0 && d <= 192) {
     const int np = static_cast<int>((d / 2 + 31) / 32);
@@ -917,7 +972,7 @@ int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, cons
         k_edge_dot<<<grid, 256, 0, c.s>>>(P, V, jbe, g.ei.p, g.ej.p, list, e0, cnt, static_cast<int>(d), bc, active);
       else
         k_edge_dot_inf<<<grid, 256, 0, c.s>>>(P, V, jal, jbe, g.ei.p, g.ej.p, list, e0, cnt, static_cast<int>(d), bc,
-                                              active);
+                                              active, mask, sgn);
       CPB_LAUNCH_CHECK();
     };
     if (c.comm && c.own_v1 >= 0) {
@@ -937,7 +992,8 @@ int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, cons
     ord = o.order.p, items = o.count, grid = c.sm_count * 8;
   }
   NF_DISPATCH(ng.nf, k_g_hess, <<<grid, 256, 0, c.s>>>(P, V, jal, bc, thr, g.off.p, g.adj_e.p, g.adj_o.p, ord,
-                                                        items, di, nch, sigma, q, Ap, part, active));
+                                                        items, di, nch, sigma, q, Ap, part, active,
+                                                        q != 2 ? mask : nullptr, q != 2 ? sgn : nullptr));
   CPB_LAUNCH_CHECK();
   return grid;
 }

@@ -74,8 +74,12 @@ const HaloPlan& halo_plan(Ctx& c, const Graph& g);
 // p's halo rows <- the owning ranks' rows (p is a full-size node array).
 void halo_exchange(Ctx& c, const Graph& g, double* p, int64_t d);
 
+// mask / sgn (nullable): edge_masks bits for q = 1 / inf (then V is not read by the Hessian)
 int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,
                   const double* thr, int64_t d, double sigma, int q, double* bc, double* Ap, double* part,
-                  const int* active);
+                  const int* active, const unsigned* mask = nullptr, const unsigned* sgn = nullptr);
+// Jacobian feature bits per edge from V: thr = t_l (q = 1) or theta_l (q = inf); 2 E ceil(d/32) words
+void edge_masks(Ctx& c, const Graph& g, const double* V, const double* thr, int64_t d, int q, unsigned* mask,
+                unsigned* sgn);
 
 }  // namespace cpb

@@ -858,6 +858,206 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
   }
 }
 
+// ---- q = inf edge passes with the rows staged in shared memory ----------------------------
+// Michelot's threshold (linf.cuh) walks a row several times; the generic kernels re-read it
+// from L1/L2 on every pass, which at C4 (d = 3072, 24 KB per row, 8 rows per block) thrashes
+// L1 (phi 57 ms, multiplier 175 ms per launch).  Here one warp per edge stages the rows its
+// passes revisit, 4 warps per block, and every pass after the first reads shared memory.
+// Each lane touches only the elements it wrote (f = lane + 32 k): no block barriers.
+// Per-element arithmetic and per-lane order are those of the generic kernels.
+constexpr int kLinfWarps = 4;
+inline bool linf_staged(int64_t d, int rows) {
+  return d > 32 && static_cast<size_t>(kLinfWarps) * rows * d * sizeof(double) <= 200 * 1024;
+}
+__global__ void __launch_bounds__(32 * kLinfWarps) k_phi_edge_linf_s(
+    const double* __restrict__ X, const double* __restrict__ Z, const int* __restrict__ ei,
+    const int* __restrict__ ej, const double* __restrict__ thr, const double* __restrict__ rad, EdgeSel sel, int d,
+    double sigma, double* __restrict__ V, double* __restrict__ nv, double* __restrict__ nvc, double* part) {
+  extern __shared__ double srow[];
+  __shared__ double sh[32];
+  const unsigned gm = group_mask();
+  double* sv = srow + static_cast<size_t>(threadIdx.y) * d;
+  double acc = 0.0;
+  EDGES_BEGIN(sel) {
+    const double* xa = X + static_cast<int64_t>(ei[row_]) * d;
+    const double* xb = X + static_cast<int64_t>(ej[row_]) * d;
+    const double* z = Z + row_ * d;
+    double* v = V + row_ * d;
+    const double t = thr[row_];
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double x = (xa[f] - xb[f]) + __ldcs(z + f) / sigma;
+      sv[f] = x;
+      __stcs(v + f, x);
+    }
+    int cnt;
+    const double th = linf_theta([&](int f) { return sv[f]; }, d, t, gm, &cnt);
+    double sq = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double r = th < 0.0 ? sv[f] : soft(sv[f], th);
+      sq += r * r;
+    }
+    const double env = rad[row_] * (th < 0.0 ? 0.0 : th) + (0.5 * sigma) * group_sum(sq, gm);
+    if (threadIdx.x == 0) {
+      nv[row_] = th;
+      nvc[row_] = cnt;
+      acc += env;
+    }
+    __syncwarp();
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) part[blockIdx.x] = acc;
+}
+// k_mult_inf with x = x_i - x_j and Z + sigma x (then the new Z) staged
+__global__ void __launch_bounds__(32 * kLinfWarps) k_mult_inf_s(
+    const double* __restrict__ X, double* __restrict__ Z, const double* __restrict__ V, const double* __restrict__ ps,
+    const double* __restrict__ rad, const double* __restrict__ w, const int* __restrict__ ei,
+    const int* __restrict__ ej, EdgeSel sel, int d, double sigma, double* part) {
+  extern __shared__ double srow[];
+  __shared__ double sh[32];
+  const unsigned gm = group_mask();
+  double* sx = srow + static_cast<size_t>(threadIdx.y) * 2 * d;
+  double* sz = sx + d;
+  double s[5] = {0, 0, 0, 0, 0}, mx = 0.0, err = 0.0, excess = -1.0;
+  EDGES_BEGIN(sel) {
+    const double* xa = X + static_cast<int64_t>(ei[row_]) * d;
+    const double* xb = X + static_cast<int64_t>(ej[row_]) * d;
+    double* z = Z + row_ * d;
+    const double* v = V + row_ * d;
+    const double rl = rad[row_], thv = ps[row_];
+    double m = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double x = xa[f] - xb[f];
+      const double zs = z[f] + sigma * x;
+      sx[f] = x;
+      sz[f] = zs;
+      m = fmax(m, fabs(zs));
+    }
+    mx = fmax(mx, m);
+    int cnt;
+    const double thz = linf_theta([&](int f) { return sz[f]; }, d, rl, gm, &cnt);
+    double fr = 0.0, e = 0.0, xb2 = 0.0, zz = 0.0, xm = 0.0, z1 = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double x = sx[f];
+      const double zs = sz[f];
+      const double zp = thz < 0.0 ? zs : soft(zs, thz);
+      const double vf = __ldcs(v + f);
+      const double pv = thv < 0.0 ? 0.0 : clampd(vf, thv);
+      e = fmax(e, fabs(sigma * (vf - pv) - zp));
+      z[f] = zp;
+      sz[f] = zp;
+      fr += (x - pv) * (x - pv);
+      xb2 += x * x;
+      zz += zp * zp;
+      xm = fmax(xm, fabs(x));
+      z1 += fabs(zp);
+    }
+    err = fmax(err, e);
+    const double thu = linf_theta([&](int f) { return sx[f] + sz[f]; }, d, rl, gm, &cnt);
+    double al = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double x = sx[f];
+      const double ee = x - (thu < 0.0 ? 0.0 : clampd(x + sz[f], thu));
+      al += ee * ee;
+    }
+    al = group_sum(al, gm);
+    fr = group_sum(fr, gm);
+    xb2 = group_sum(xb2, gm);
+    zz = group_sum(zz, gm);
+    const double pen = w[row_] * group_max(xm, gm);
+    excess = fmax(excess, group_sum(z1, gm) - (rl + 1e-9));
+    if (threadIdx.x == 0) {
+      s[0] += pen;
+      s[1] += al;
+      s[2] += xb2;
+      s[3] += zz;
+      s[4] += fr;
+    }
+    __syncwarp();
+  }
+  for (int k = 0; k < 5; ++k) {
+    const double r = block_sum(s[k], sh);
+    if (threadIdx.x == 0 && threadIdx.y == 0) part[9 * blockIdx.x + k] = r;
+  }
+  const double a = block_max(mx, sh);
+  const double b = block_max(err, sh);
+  const double c = block_max(excess, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    part[9 * blockIdx.x + 5] = 0.0;
+    part[9 * blockIdx.x + 6] = a;
+    part[9 * blockIdx.x + 7] = b;
+    part[9 * blockIdx.x + 8] = c;
+  }
+}
+// gap edge terms (gap_edge_terms, q = inf) with x and z staged
+__global__ void __launch_bounds__(32 * kLinfWarps) k_gap_edge_linf_s(
+    const double* __restrict__ X, const double* __restrict__ Z, const int* __restrict__ ei,
+    const int* __restrict__ ej, const double* __restrict__ rad, const double* __restrict__ w, EdgeSel sel, int d,
+    double* part) {
+  extern __shared__ double srow[];
+  __shared__ double sh[32];
+  const unsigned gm = group_mask();
+  double* sx = srow + static_cast<size_t>(threadIdx.y) * 2 * d;
+  double* sz = sx + d;
+  double s[4] = {0, 0, 0, 0}, excess = -1.0;
+  EDGES_BEGIN(sel) {
+    const double* xa = X + static_cast<int64_t>(ei[row_]) * d;
+    const double* xb = X + static_cast<int64_t>(ej[row_]) * d;
+    const double* z = Z + row_ * d;
+    const double rl = rad[row_];
+    double xb2 = 0.0, zz = 0.0, xm = 0.0, z1 = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double x = xa[f] - xb[f];
+      const double zf = z[f];
+      sx[f] = x;
+      sz[f] = zf;
+      xb2 += x * x;
+      zz += zf * zf;
+      xm = fmax(xm, fabs(x));
+      z1 += fabs(zf);
+    }
+    int cnt;
+    const double th = linf_theta([&](int f) { return sx[f] + sz[f]; }, d, rl, gm, &cnt);
+    double al = 0.0;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      const double x = sx[f];
+      const double e = x - (th < 0.0 ? 0.0 : clampd(x + sz[f], th));
+      al += e * e;
+    }
+    const double t0 = w[row_] * group_max(xm, gm), t1 = group_sum(al, gm), t2 = group_sum(xb2, gm),
+                 t3 = group_sum(zz, gm);
+    excess = fmax(excess, group_sum(z1, gm) - (rl + 1e-9));
+    if (threadIdx.x == 0) s[0] += t0, s[1] += t1, s[2] += t2, s[3] += t3;
+    __syncwarp();
+  }
+  for (int k = 0; k < 4; ++k) {
+    const double r = block_sum(s[k], sh);
+    if (threadIdx.x == 0 && threadIdx.y == 0) part[5 * blockIdx.x + k] = r;
+  }
+  const double m = block_max(excess, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) part[5 * blockIdx.x + 4] = m;
+}
+// Launch one of the staged q = inf kernels on `grid` blocks (the generic kernel's grid, so the
+// partial tables keep their shape).
+template <class K, class... Args>
+void launch_linf_s(K kernel, int rows, int64_t d, int grid, cudaStream_t s, Args... args) {
+  const size_t smem = static_cast<size_t>(kLinfWarps) * rows * d * sizeof(double);
+  CPB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  kernel<<<grid, dim3(32, kLinfWarps), smem, s>>>(args...);
+  CPB_LAUNCH_CHECK();
+}
+// gap edge terms over `sel` on `grid` blocks (5 partials per block)
+void gap_edge_launch(Ctx& c, int grid, const GroupGeom& ge, const double* X, const double* Z, const Prob& P,
+                     EdgeSel sel, int64_t d, double* pe) {
+  if (P.q == Q_LINF && linf_staged(d, 2)) {
+    launch_linf_s(k_gap_edge_linf_s, 2, d, grid, c.s, X, Z, (const int*)P.g->ei.p, (const int*)P.g->ej.p,
+                  (const double*)P.rad, (const double*)P.g->w.p, sel, static_cast<int>(d), pe);
+    return;
+  }
+  k_gap_edge<<<grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, sel,
+                                                   static_cast<int>(d), P.q, pe);
+  CPB_LAUNCH_CHECK();
+}
+
 // TMA variant of k_phi_edge (even d, 32-lane rows): x_i, x_j and Z_l are
 // streamed into the warp's shared-memory slot by cp.async.bulk (three rows in
 // flight per warp regardless of registers); V_l is written with streaming
@@ -1247,6 +1447,9 @@ double eval_phi(const Prob& P, const double* X, const double* D, double alpha, d
           k_phi_edge_t<Q_L1><<<nb, dim3(32, kMultWarps), smem, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, sel,
                                                                       static_cast<int>(d), sigma, V, nv, pe_, S);
         CPB_LAUNCH_CHECK();
+      } else if (P.q == Q_LINF && linf_staged(d, 1)) {
+        launch_linf_s(k_phi_edge_linf_s, 1, d, gg.grid, c.s, Xe, Z, (const int*)P.g->ei.p, (const int*)P.g->ej.p,
+                      thr, (const double*)P.rad, sel, static_cast<int>(d), sigma, V, nv, nv + E, pe_);
       } else {
         k_phi_edge<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(Xe, Z, P.g->ei.p, P.g->ej.p, thr, P.rad, sel,
                                                             static_cast<int>(d), sigma, P.q, V, nv, nv + E, pe_);
@@ -1304,11 +1507,12 @@ double grad_diag(const Prob& P, const double* X, const double* V, const double* 
 }
 
 int hess_apply(const Prob& P, const double* p, const double* V, const double* jal, const double* jbe,
-               const double* thr, double sigma, double* Ap, double* part, const void* st) {
+               const double* thr, double sigma, double* Ap, double* part, const void* st, const unsigned* mask,
+               const unsigned* sgn) {
   Ctx& c = *P.c;
   double* bc = c.buf<double>("hess.bc", P.E() + 1);
   return hess_two_pass(c, *P.g, p, V, jal, jbe, thr, P.d(), sigma, P.q, bc, Ap, part,
-                       cg_active_ptr(st));
+                       cg_active_ptr(st), mask, sgn);
 }
 
 PcgOut pcg_newton(const Prob& P, const double* V, const double* jal, const double* jbe, const double* thr,
@@ -1317,8 +1521,17 @@ PcgOut pcg_newton(const Prob& P, const double* V, const double* jal, const doubl
   // Algorithmic bytes per H-apply: p read + Ap write
   // (2 n d) + the active edge rows (E_a d) + two per-edge scalars + the CSR.
   const double hess_bytes = (2.0 * m + static_cast<double>(n_active) * d + 2.0 * E) * 8.0 + (2.0 * E + n + 1) * 4.0;
+  // q = 1 / inf: the Jacobian's feature sets as bits, built once for this Newton system, so
+  // the per-iteration gathers stop re-reading V (2 bits instead of 8 bytes per feature)
+  unsigned *mask = nullptr, *sgn = nullptr;
+  if (P.q != Q_L2 && E > 0) {
+    const size_t words = static_cast<size_t>(E) * ((d + 31) / 32);
+    mask = P.c->buf<unsigned>("hess.mask", words + 1);
+    sgn = P.c->buf<unsigned>("hess.sgn", words + 1);
+    edge_masks(*P.c, *P.g, V, P.q == Q_L1 ? thr : jal, d, P.q, mask, sgn);
+  }
   PcgOp op = [&](const double* p, double* Ap, double* part, const void* st) {
-    return hess_apply(P, p, V, jal, jbe, thr, sigma, Ap, part, st);
+    return hess_apply(P, p, V, jal, jbe, thr, sigma, Ap, part, st, mask, sgn);
   };
   // with a communicator the Newton system is node-partitioned over the ranks
   // (everything outside the PCG stays replicated: identical on every rank)
@@ -1377,9 +1590,7 @@ GapOut eval_gap(const Prob& P, const double* X, const double* Z) {
   double* pe = pn + 4 * static_cast<size_t>(nbn);
   if (E > 0) {
     Ctx::Timer tm(&c, "gap_edge", (E * d + n * d) * 8.0);
-    k_gap_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, sel,
-                                                        static_cast<int>(d), P.q, pe);
-    CPB_LAUNCH_CHECK();
+    gap_edge_launch(c, ge.grid, ge, X, Z, P, sel, d, pe);
   }
   return gap_from_partials(P, pn, nbn, E > 0 ? ge.grid : 0);
 }
@@ -1431,9 +1642,7 @@ double primal_objective_dev(const Prob& P, const double* X) {
   CPB_CUDA(cudaMemsetAsync(Z0, 0, static_cast<size_t>(E) * d * sizeof(double), c.s));
   GroupGeom ge = group_geom(c, E, d);
   double* pe = part_buf(c, "po.pe", 5 * static_cast<size_t>(ge.grid));
-  k_gap_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z0, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, EdgeSel{nullptr, 0, E},
-                                                      static_cast<int>(d), P.q, pe);
-  CPB_LAUNCH_CHECK();
+  gap_edge_launch(c, ge.grid, ge, X, Z0, P, EdgeSel{nullptr, 0, E}, d, pe);
   std::vector<double> e = host_cols(c, pe, ge.grid, 5, {4});
   return value + P.gamma * e[0];
 }
@@ -1454,9 +1663,7 @@ double kkt_residual_dev(const Prob& P, const double* X, const double* Z) {
   if (E == 0 || P.gamma == 0.0) return stat;
   GroupGeom ge = group_geom(c, E, d);
   double* pe = part_buf(c, "kkt.pe", 5 * static_cast<size_t>(ge.grid));
-  k_gap_edge<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, EdgeSel{nullptr, 0, E},
-                                                      static_cast<int>(d), P.q, pe);
-  CPB_LAUNCH_CHECK();
+  gap_edge_launch(c, ge.grid, ge, X, Z, P, EdgeSel{nullptr, 0, E}, d, pe);
   std::vector<double> e = host_cols(c, pe, ge.grid, 5, {4});
   return std::max(stat, std::sqrt(e[1]) / (1.0 + std::sqrt(e[2]) + std::sqrt(e[3])));
 }
@@ -1471,7 +1678,10 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
   auto run = [&](EdgeSel sel, double* pe) -> int {
     GroupGeom ge = group_geom(c, sel.count, d);
     int nb = ge.grid;
-    if (P.q == Q_LINF) {
+    if (P.q == Q_LINF && linf_staged(d, 2)) {
+      launch_linf_s(k_mult_inf_s, 2, d, ge.grid, c.s, X, Z, V, ps, (const double*)P.rad, (const double*)P.g->w.p,
+                    (const int*)P.g->ei.p, (const int*)P.g->ej.p, sel, static_cast<int>(d), sigma, pe);
+    } else if (P.q == Q_LINF) {
       k_mult_inf<<<ge.grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, V, ps, P.rad, P.g->w.p, P.g->ei.p, P.g->ej.p, sel,
                                                           static_cast<int>(d), sigma, pe);
       CPB_LAUNCH_CHECK();

@@ -61,8 +61,10 @@ int64_t jac_params(const Prob& P, const double* nv, const double* thr, double* p
 double grad_diag(const Prob& P, const double* X, const double* V, const double* ps, const double* jal,
                  const double* jbe, const double* thr, double sigma, double* G, double* diag, bool want_diag);
 // Ap = p + sigma B^T((I - M) (p B)); pAp/pp partials into `part` (2 per block).
+// mask / sgn: the edge_masks bits of q = 1 / inf (nullable: read V instead)
 int hess_apply(const Prob& P, const double* p, const double* V, const double* jal, const double* jbe,
-               const double* thr, double sigma, double* Ap, double* part, const void* cg_state = nullptr);
+               const double* thr, double sigma, double* Ap, double* part, const void* cg_state = nullptr,
+               const unsigned* mask = nullptr, const unsigned* sgn = nullptr);
 
 // Block-Jacobi PCG on the SSNAL Newton system (linalg.cpp:143-192): solves
 // H x = rhs from x0 = 0, stop on the worst relative feature-row residual.

@@ -430,6 +430,48 @@ def test_hessian_tma_path_matches_oracle(cp, orc, d):
             assert np.linalg.norm(H - OH) <= 1e-13 * np.linalg.norm(OH)
 
 
+@pytest.mark.parametrize("q", [1, 0])
+@pytest.mark.parametrize("d", [33, 64, 300, 1000])
+def test_hessian_mask_path_matches_oracle(cp, orc, q, d):
+    """q = 1 / inf Hessian (ssnal.cpp:56-64) through the per-edge Jacobian bit masks
+    (gather.cu edge_masks: [|v_f| > t] or [|v_f| > theta] and sign(v_f)), which replace the V
+    reads of the gathers: equal to the oracle's dense-Jacobian apply at rounding level."""
+    A = mixture(orc, 30, d, m=3, seed=11)
+    g, og = check_graph(cp, orc, A, 8, 0.5)
+    rng = np.random.default_rng(d + 7 * q)
+    gamma = 0.2
+    inst = cp.ProblemInstance(cp.DataMatrix(A), g, gamma, q)
+    X = A + 0.05 * rng.standard_normal(A.shape)
+    Z = orc.project_columns(q, 0.05 * rng.standard_normal((g.edge_count(), d)), gamma * og.arrays()[2])
+    D = rng.standard_normal(A.shape)
+    for sigma in (0.7, 5.0):
+        H = cp.ssnal_hessian_apply(inst, Z, sigma, X, D)
+        OH = orc.hessian_apply(A, og, gamma, q, Z, sigma, X, D)
+        assert np.linalg.norm(H - OH) <= 1e-13 * np.linalg.norm(OH)
+
+
+@pytest.mark.parametrize("q", [0, 1])
+@pytest.mark.parametrize("d", [40, 300])
+def test_ssnal_linf_l1_wide_rows_match_oracle(cp, orc, q, d):
+    """SSNAL with q = inf / 1 at d > 32: the shared-memory-staged q = inf edge passes
+    (k_phi_edge_linf_s, k_mult_inf_s, k_gap_edge_linf_s) and the bit-mask Hessian keep the
+    oracle's Newton / CG / Armijo counts, X at rounding level."""
+    A = mixture(orc, 20, d, m=3, seed=13)
+    g, og = check_graph(cp, orc, A, 6, 0.5)
+    gi, gj, gw, _ = g.arrays()
+    og = orc.Graph.from_arrays(len(A), gi, gj, gw)  # identical weights (see the AMA block test)
+    for gamma in (0.05, 0.2):
+        inst = cp.ProblemInstance(cp.DataMatrix(A), g, gamma, q)
+        sol = cp.solve(inst)
+        osol = orc.solve(A, og, gamma, q)
+        t, ot = sol.termination, osol.term
+        assert (t.iterations, t.newton, t.cg, t.armijo) == (ot["iterations"], ot["newton"], ot["cg"], ot["armijo"])
+        assert np.linalg.norm(sol.X - osol.X) <= 1e-9 * np.linalg.norm(osol.X)
+        assert cp.kkt_residual(inst, sol.X, sol.Z) == pytest.approx(orc.kkt_residual(A, og, gamma, q, sol.X, sol.Z),
+                                                                    rel=1e-9, abs=1e-15)
+        assert cp.primal_objective(inst, sol.X) == pytest.approx(orc.primal_objective(A, og, gamma, q, sol.X), rel=1e-12)
+
+
 def test_ssnal_iteration_path_matches_tma(cp, orc):
     A = mixture(orc, 30, 40, m=3, seed=4)
     g, og = check_graph(cp, orc, A, 6, 0.5)
