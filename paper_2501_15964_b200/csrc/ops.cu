@@ -884,10 +884,25 @@ __global__ void __launch_bounds__(32 * kLinfWarps) k_phi_edge_linf_s(
     const double* z = Z + row_ * d;
     double* v = V + row_ * d;
     const double t = thr[row_];
-    for (int f = threadIdx.x; f < d; f += blockDim.x) {
-      const double x = (xa[f] - xb[f]) + __ldcs(z + f) / sigma;
-      sv[f] = x;
-      __stcs(v + f, x);
+    // 8 elements per lane per batch: 24 independent loads in flight (the pass is latency-bound otherwise)
+    for (int f0 = threadIdx.x; f0 < d; f0 += 8 * 32) {
+      double a[8], b[8], c[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = f0 + 32 * u;
+        a[u] = f < d ? xa[f] : 0.0;
+        b[u] = f < d ? xb[f] : 0.0;
+        c[u] = f < d ? __ldcs(z + f) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = f0 + 32 * u;
+        if (f < d) {
+          const double x = (a[u] - b[u]) + c[u] / sigma;
+          sv[f] = x;
+          __stcs(v + f, x);
+        }
+      }
     }
     int cnt;
     const double th = linf_theta([&](int f) { return sv[f]; }, d, t, gm, &cnt);
@@ -925,17 +940,32 @@ __global__ void __launch_bounds__(32 * kLinfWarps) k_mult_inf_s(
     const double* v = V + row_ * d;
     const double rl = rad[row_], thv = ps[row_];
     double m = 0.0;
-    for (int f = threadIdx.x; f < d; f += blockDim.x) {
-      const double x = xa[f] - xb[f];
-      const double zs = z[f] + sigma * x;
-      sx[f] = x;
-      sz[f] = zs;
-      m = fmax(m, fabs(zs));
+    for (int f0 = threadIdx.x; f0 < d; f0 += 8 * 32) {  // batched loads (see k_phi_edge_linf_s)
+      double a[8], b[8], c[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = f0 + 32 * u;
+        a[u] = f < d ? xa[f] : 0.0;
+        b[u] = f < d ? xb[f] : 0.0;
+        c[u] = f < d ? z[f] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = f0 + 32 * u;
+        if (f < d) {
+          const double x = a[u] - b[u];
+          const double zs = c[u] + sigma * x;
+          sx[f] = x;
+          sz[f] = zs;
+          m = fmax(m, fabs(zs));
+        }
+      }
     }
     mx = fmax(mx, m);
     int cnt;
     const double thz = linf_theta([&](int f) { return sz[f]; }, d, rl, gm, &cnt);
     double fr = 0.0, e = 0.0, xb2 = 0.0, zz = 0.0, xm = 0.0, z1 = 0.0;
+#pragma unroll 8
     for (int f = threadIdx.x; f < d; f += blockDim.x) {
       const double x = sx[f];
       const double zs = sz[f];
@@ -1005,15 +1035,29 @@ __global__ void __launch_bounds__(32 * kLinfWarps) k_gap_edge_linf_s(
     const double* z = Z + row_ * d;
     const double rl = rad[row_];
     double xb2 = 0.0, zz = 0.0, xm = 0.0, z1 = 0.0;
-    for (int f = threadIdx.x; f < d; f += blockDim.x) {
-      const double x = xa[f] - xb[f];
-      const double zf = z[f];
-      sx[f] = x;
-      sz[f] = zf;
-      xb2 += x * x;
-      zz += zf * zf;
-      xm = fmax(xm, fabs(x));
-      z1 += fabs(zf);
+    for (int f0 = threadIdx.x; f0 < d; f0 += 8 * 32) {  // batched loads (see k_phi_edge_linf_s)
+      double a[8], b[8], c[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = f0 + 32 * u;
+        a[u] = f < d ? xa[f] : 0.0;
+        b[u] = f < d ? xb[f] : 0.0;
+        c[u] = f < d ? z[f] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = f0 + 32 * u;
+        if (f < d) {
+          const double x = a[u] - b[u];
+          const double zf = c[u];
+          sx[f] = x;
+          sz[f] = zf;
+          xb2 += x * x;
+          zz += zf * zf;
+          xm = fmax(xm, fabs(x));
+          z1 += fabs(zf);
+        }
+      }
     }
     int cnt;
     const double th = linf_theta([&](int f) { return sx[f] + sz[f]; }, d, rl, gm, &cnt);
