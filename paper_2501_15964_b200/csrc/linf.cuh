@@ -61,3 +61,81 @@ __device__ __forceinline__ double linf_theta(F val, int d, double t, unsigned gm
 __device__ __forceinline__ double clampd(double v, double th) { return fmax(fmin(v, th), -th); }
 
 }  // namespace cpb
+
+namespace cpb {
+
+// linf_theta for a warp-owned row (blockDim.x = 32) whose values val(f) are
+// cheap to re-read (staged in shared memory), d <= 32 * 32 * kLinfWords:
+// after the first counting pass each lane keeps its candidates {|v_f| >
+// threshold} as a bit set and later passes visit only those.  Exactly the
+// passes of linf_theta (same elements in the same per-lane order, so the same
+// partial sums and theta): an element dropped by one pass can only come back
+// if theta decreased, and linf_theta stops on exactly that pass (the support
+// does not shrink), as this loop does when the candidate count stops shrinking.
+constexpr int kLinfWords = 4;  // up to 128 elements per lane (d <= 4096)
+template <class F>
+__device__ __forceinline__ double linf_theta_bits(F val, int d, double t, int* cnt) {
+  const int lane = threadIdx.x & 31;
+  double s1 = 0.0;
+  for (int f = lane; f < d; f += 32) s1 += fabs(val(f));
+  s1 = warp_sum(s1);
+  if (!(s1 > t)) {
+    *cnt = 0;
+    return -1.0;
+  }
+  double theta = (s1 - t) / static_cast<double>(d);
+  int support = d;
+  unsigned m[kLinfWords];
+  bool first = true;
+  for (;;) {
+    double s = 0.0, c = 0.0;
+    if (first) {  // full pass: build the candidate bits
+#pragma unroll
+      for (int w = 0; w < kLinfWords; ++w) {
+        unsigned bits = 0u;
+        for (int b = 0; b < 32; ++b) {
+          const int f = lane + 32 * (32 * w + b);
+          if (f >= d) break;
+          const double a = fabs(val(f));
+          if (a > theta) {
+            s += a;
+            c += 1.0;
+            bits |= 1u << b;
+          }
+        }
+        m[w] = bits;
+      }
+      first = false;
+    } else {
+#pragma unroll
+      for (int w = 0; w < kLinfWords; ++w) {
+        unsigned bits = m[w], keep = 0u;
+        while (bits) {
+          const int b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          const double a = fabs(val(lane + 32 * (32 * w + b)));
+          if (a > theta) {
+            s += a;
+            c += 1.0;
+            keep |= 1u << b;
+          }
+        }
+        m[w] = keep;
+      }
+    }
+    s = warp_sum(s);
+    c = warp_sum(c);
+    const int ci = static_cast<int>(c);
+    if (ci == 0) {
+      support = 0;
+      break;
+    }
+    if (ci >= support) break;
+    theta = (s - t) / c;
+    support = ci;
+  }
+  *cnt = support;
+  return theta;
+}
+
+}  // namespace cpb

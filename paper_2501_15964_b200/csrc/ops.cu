@@ -864,10 +864,11 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
 // L1 (phi 57 ms, multiplier 175 ms per launch).  Here one warp per edge stages the rows its
 // passes revisit, 4 warps per block, and every pass after the first reads shared memory.
 // Each lane touches only the elements it wrote (f = lane + 32 k): no block barriers.
+// The threshold passes visit only each lane's surviving candidates (linf_theta_bits).
 // Per-element arithmetic and per-lane order are those of the generic kernels.
 constexpr int kLinfWarps = 4;
 inline bool linf_staged(int64_t d, int rows) {
-  return d > 32 && static_cast<size_t>(kLinfWarps) * rows * d * sizeof(double) <= 200 * 1024;
+  return d > 32 && d <= 32 * 32 * kLinfWords && static_cast<size_t>(kLinfWarps) * rows * d * sizeof(double) <= 200 * 1024;
 }
 __global__ void __launch_bounds__(32 * kLinfWarps) k_phi_edge_linf_s(
     const double* __restrict__ X, const double* __restrict__ Z, const int* __restrict__ ei,
@@ -905,7 +906,7 @@ __global__ void __launch_bounds__(32 * kLinfWarps) k_phi_edge_linf_s(
       }
     }
     int cnt;
-    const double th = linf_theta([&](int f) { return sv[f]; }, d, t, gm, &cnt);
+    const double th = linf_theta_bits([&](int f) { return sv[f]; }, d, t, &cnt);
     double sq = 0.0;
     for (int f = threadIdx.x; f < d; f += blockDim.x) {
       const double r = th < 0.0 ? sv[f] : soft(sv[f], th);
@@ -963,7 +964,7 @@ __global__ void __launch_bounds__(32 * kLinfWarps) k_mult_inf_s(
     }
     mx = fmax(mx, m);
     int cnt;
-    const double thz = linf_theta([&](int f) { return sz[f]; }, d, rl, gm, &cnt);
+    const double thz = linf_theta_bits([&](int f) { return sz[f]; }, d, rl, &cnt);
     double fr = 0.0, e = 0.0, xb2 = 0.0, zz = 0.0, xm = 0.0, z1 = 0.0;
 #pragma unroll 8
     for (int f = threadIdx.x; f < d; f += blockDim.x) {
@@ -982,7 +983,7 @@ __global__ void __launch_bounds__(32 * kLinfWarps) k_mult_inf_s(
       z1 += fabs(zp);
     }
     err = fmax(err, e);
-    const double thu = linf_theta([&](int f) { return sx[f] + sz[f]; }, d, rl, gm, &cnt);
+    const double thu = linf_theta_bits([&](int f) { return sx[f] + sz[f]; }, d, rl, &cnt);
     double al = 0.0;
     for (int f = threadIdx.x; f < d; f += blockDim.x) {
       const double x = sx[f];
@@ -1060,7 +1061,7 @@ __global__ void __launch_bounds__(32 * kLinfWarps) k_gap_edge_linf_s(
       }
     }
     int cnt;
-    const double th = linf_theta([&](int f) { return sx[f] + sz[f]; }, d, rl, gm, &cnt);
+    const double th = linf_theta_bits([&](int f) { return sx[f] + sz[f]; }, d, rl, &cnt);
     double al = 0.0;
     for (int f = threadIdx.x; f < d; f += blockDim.x) {
       const double x = sx[f];
