@@ -722,7 +722,12 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_s(
 // keeps 4 d doubles in flight without spending registers on them; the three
 // passes then run from shared memory (x_i's slot is reused for x, Z_l's for
 // Zsum / the projected Z).  Per-element arithmetic is that of k_mult_s.
-template <int Q, bool VS>
+// VM = 1: V_l staged by TMA with the other rows.  VM = 2: V_l recomputed from the staged
+// rows, v = (x_i - x_j) + z_l / sigma — the exact expression (and rounding) of the phi edge
+// pass that wrote V at the same X and Z, so it is bitwise the stored row; one HBM row fewer
+// per edge.  The host picks VM = 2 unless the last Armijo search failed (then X moved past
+// the last trial point, ssnal.cpp:172-179, and the stored V is read).
+template <int Q, int VM>
 __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
     const double* __restrict__ X, double* __restrict__ Z, const double* __restrict__ V, const double* __restrict__ ps,
     const double* __restrict__ thr, const double* __restrict__ rad, const double* __restrict__ w,
@@ -740,7 +745,7 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
   const int64_t wid = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * blockDim.y;
   const int64_t cnt = wid < sel.count ? (sel.count - wid + nw - 1) / nw : 0;  // this warp's edges: wid + e nw
-  constexpr int NR = VS ? 4 : 3;  // staged rows per edge (V_l staged or streamed)
+  constexpr int NR = VM == 1 ? 4 : 3;  // staged rows per edge
   double* const base = trow + static_cast<size_t>(threadIdx.y) * S * NR * d;
   auto issue = [&](int64_t e, int q) {  // lane 0: x_i, x_j, Z_l, V_l of edge wid + e nw into slot q
     const int64_t l = sel.at(wid + e * nw);
@@ -752,7 +757,7 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
     bulk_g2s(sx + d, X + static_cast<int64_t>(ej[l]) * d, rb, b);
     const uint64_t ef = policy_evict_first();
     bulk_g2s_hint(sx + 2 * d, Z + l * d, rb, b, ef);
-    if (VS) bulk_g2s_hint(sx + 3 * d, V + l * d, rb, b, ef);
+    if (VM == 1) bulk_g2s_hint(sx + 3 * d, V + l * d, rb, b, ef);
   };
   if (lane == 0)
     for (int q = 0; q < S && q < cnt; ++q) issue(q, q);
@@ -762,9 +767,9 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
   for (int64_t it = 0; it < cnt; ++it) {
     const int64_t row_ = sel.at(wid + it * nw);
     double* sx = base + static_cast<size_t>(q) * NR * d;  // x_i, then x = x_i - x_j
-    double* sb = sx + d;   // x_j
+    double* sb = sx + d;   // x_j, then (VM = 2) V_l
     double* sz = sb + d;   // Z_l, then Zsum, then Z_l new
-    const double* sv = VS ? sz + d : V + row_ * d;  // V_l (staged, or streamed from HBM)
+    const double* sv = VM == 1 ? sz + d : sb;  // V_l
     double* z = Z + row_ * d;
     const double rl = rad[row_], tl = thr[row_], sl = ps[row_];
     mbar_wait(&bar[q], ph);
@@ -772,8 +777,10 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
 #pragma unroll 4
     for (int f = lane; f < d; f += 32) {
       const double x = sx[f] - sb[f];
-      const double zs = sz[f] + sigma * x;
+      const double zo = sz[f];
+      const double zs = zo + sigma * x;
       sx[f] = x;
+      if (VM == 2) sb[f] = x + zo / sigma;
       sz[f] = zs;
       nn += zs * zs;
       m = fmax(m, fabs(zs));
@@ -787,7 +794,7 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_mult_t(
       const double x = sx[f];
       const double zs = sz[f];
       const double zp = (Q == Q_L2) ? ((nz <= rl) ? zs : sc * zs) : fmax(fmin(zs, rl), -rl);
-      const double vf = VS ? sv[f] : __ldcs(sv + f);
+      const double vf = sv[f];
       const double pv = (Q == Q_L2) ? sl * vf : soft(vf, tl);
       const double zenv = sigma * (vf - pv);
       e = fmax(e, fabs(zenv - zp));
@@ -1714,7 +1721,7 @@ double kkt_residual_dev(const Prob& P, const double* X, const double* Z) {
 }
 
 MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double* V, const double* ps,
-                         const double* thr, double sigma) {
+                         const double* thr, double sigma, bool v_at_x) {
   Ctx& c = *P.c;
   const int64_t d = P.d(), n = P.n(), E = P.E();
   const size_t pe_n = 9 * static_cast<size_t>(std::max(group_geom(c, E, d).grid, c.sm_count * 64));
@@ -1733,32 +1740,32 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
     } else if (ge.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1)) {
       // V_l staged with the other rows (streaming it from HBM in pass 2 with 3
       // staged rows and more warps per SM measured slower: 4.42 vs 3.46 ms at C3)
-      const bool vstage = true;
-      const int NR = 4;
+      const int VM = v_at_x ? 2 : 1;
+      const int NR = VM == 1 ? 4 : 3;
       const int S = edge_stages(d, NR);
       const size_t smem = static_cast<size_t>(kMultWarps) * S * NR * d * sizeof(double);
       if (first_on_device("k_mult_t.smem")) {
-        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CPB_CUDA(cudaFuncSetAttribute(k_mult_t<Q_L1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
       }
       int per_sm = 0;
-      CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mult_t<Q_L2, false>, 32 * kMultWarps, smem));
+      CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mult_t<Q_L2, 2>, 32 * kMultWarps, smem));
       nb = std::max(1, std::min(cdiv(sel.count, kMultWarps), c.sm_count * std::max(1, per_sm)));
       const dim3 blk(32, kMultWarps);
       const int di = static_cast<int>(d);
       const int* ei = P.g->ei.p;
       const int* ej = P.g->ej.p;
       const double* wl = P.g->w.p;
-      if (P.q == Q_L2 && vstage)
-        k_mult_t<Q_L2, true><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, sel, di, sigma, pe, S);
+      if (P.q == Q_L2 && VM == 1)
+        k_mult_t<Q_L2, 1><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, sel, di, sigma, pe, S);
       else if (P.q == Q_L2)
-        k_mult_t<Q_L2, false><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, sel, di, sigma, pe, S);
-      else if (vstage)
-        k_mult_t<Q_L1, true><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, sel, di, sigma, pe, S);
+        k_mult_t<Q_L2, 2><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, sel, di, sigma, pe, S);
+      else if (VM == 1)
+        k_mult_t<Q_L1, 1><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, sel, di, sigma, pe, S);
       else
-        k_mult_t<Q_L1, false><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, sel, di, sigma, pe, S);
+        k_mult_t<Q_L1, 2><<<nb, blk, smem, c.s>>>(X, Z, V, ps, thr, P.rad, wl, ei, ej, sel, di, sigma, pe, S);
       CPB_LAUNCH_CHECK();
     } else if (ge.gx == 32 && d <= kMultSmemMaxD && (P.q == Q_L2 || P.q == Q_L1)) {
       const size_t smem = static_cast<size_t>(kMultWarps) * 2 * d * sizeof(double);

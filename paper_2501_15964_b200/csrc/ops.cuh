@@ -104,8 +104,10 @@ struct MultOut {
   double feas = 0;  // ||XB - PV|| / (1 + ||XB||)
   double zz = 0;    // ||Z||^2 at the new Z
 };
+// v_at_x: V = X B + Z / sigma at exactly this X (the edge kernel may then recompute V_l
+// bitwise instead of reading it)
 MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double* V, const double* ps,
-                         const double* thr, double sigma);
+                         const double* thr, double sigma, bool v_at_x = false);
 
 // ---- fast AMA (ama.cpp:57-72) ---------------------------------------------
 // Xh = A - Zhat B^T

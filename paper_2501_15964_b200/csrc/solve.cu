@@ -134,6 +134,7 @@ cp_termination ssnal(Prob& P, const cp_solver_config& cfg, bool warm, double* Xo
     const double eps_k = std::max(eps / 10.0, std::pow(0.5, static_cast<double>(k)));
     make_thr(c, E, P.rad, sigma, thr);
     double phi = eval_phi(P, X, nullptr, 0.0, nullptr, Z, sigma, thr, zz, V, nv);
+    bool v_at_x = true;  // V = X B + Z / sigma at the current X (false after a failed line search)
     for (int64_t j = 0; j < cfg.ssnal_newton_max; ++j) {
       const int64_t n_active = jac_params(P, nv, thr, ps, jal, jbe);
       const double gnorm = std::sqrt(grad_diag(P, X, V, ps, jal, jbe, thr, sigma, G, w.diag, true));
@@ -167,12 +168,13 @@ cp_termination ssnal(Prob& P, const cp_solver_config& cfg, bool warm, double* Xo
       } else {
         axpy_dev(c, X, X, alpha, D, m);  // reference quirk: alpha halved a 60th time (ssnal.cpp:172-179)
       }
+      v_at_x = ok;
       std::swap(V, Vt);
       std::swap(nv, nvt);
       phi = trial;
     }
     jac_params(P, nv, thr, ps, jal, jbe);  // prox scale at the last accepted V
-    MultOut mo = ssnal_multiplier(P, X, Z, V, ps, thr, sigma);
+    MultOut mo = ssnal_multiplier(P, X, Z, V, ps, thr, sigma, v_at_x);
     zz = mo.zz;
     trace_gap(c, cfg, k, mo.gap, since(t0));
     if (accepts(mo.gap, cfg)) {
