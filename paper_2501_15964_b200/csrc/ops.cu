@@ -1026,8 +1026,10 @@ __global__ void __launch_bounds__(32 * kLinfWarps) k_mult_inf_s(
     part[9 * blockIdx.x + 8] = c;
   }
 }
-// gap edge terms (gap_edge_terms, q = inf) with x and z staged
-__global__ void __launch_bounds__(32 * kLinfWarps) k_gap_edge_linf_s(
+// gap edge terms (gap_edge_terms) with x = x_i - x_j and z staged: one streaming pass with
+// batched loads, later passes from shared memory (the generic kernel re-reads the rows)
+template <int Q>
+__global__ void __launch_bounds__(32 * kLinfWarps) k_gap_edge_s(
     const double* __restrict__ X, const double* __restrict__ Z, const int* __restrict__ ei,
     const int* __restrict__ ej, const double* __restrict__ rad, const double* __restrict__ w, EdgeSel sel, int d,
     double* part) {
@@ -1042,15 +1044,15 @@ __global__ void __launch_bounds__(32 * kLinfWarps) k_gap_edge_linf_s(
     const double* xb = X + static_cast<int64_t>(ej[row_]) * d;
     const double* z = Z + row_ * d;
     const double rl = rad[row_];
-    double xb2 = 0.0, zz = 0.0, xm = 0.0, z1 = 0.0;
-    for (int f0 = threadIdx.x; f0 < d; f0 += 8 * 32) {  // batched loads (see k_phi_edge_linf_s)
+    double xb2 = 0.0, zz = 0.0, xm = 0.0, z1 = 0.0, uu = 0.0, l1 = 0.0, zmax = 0.0;
+    for (int f0 = threadIdx.x; f0 < d; f0 += 8 * 32) {
       double a[8], b[8], c[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int f = f0 + 32 * u;
         a[u] = f < d ? xa[f] : 0.0;
         b[u] = f < d ? xb[f] : 0.0;
-        c[u] = f < d ? z[f] : 0.0;
+        c[u] = f < d ? __ldcs(z + f) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -1062,23 +1064,58 @@ __global__ void __launch_bounds__(32 * kLinfWarps) k_gap_edge_linf_s(
           sz[f] = zf;
           xb2 += x * x;
           zz += zf * zf;
-          xm = fmax(xm, fabs(x));
-          z1 += fabs(zf);
+          if (Q == Q_LINF) {
+            xm = fmax(xm, fabs(x));
+            z1 += fabs(zf);
+          } else {
+            const double uv = x + zf;
+            uu += uv * uv;
+            l1 += fabs(x);
+            zmax = fmax(zmax, fabs(zf));
+          }
         }
       }
     }
-    int cnt;
-    const double th = linf_theta_bits([&](int f) { return sx[f] + sz[f]; }, d, rl, &cnt);
-    double al = 0.0;
-    for (int f = threadIdx.x; f < d; f += blockDim.x) {
-      const double x = sx[f];
-      const double e = x - (th < 0.0 ? 0.0 : clampd(x + sz[f], th));
-      al += e * e;
+    double t0, al = 0.0;
+    xb2 = group_sum(xb2, gm);
+    zz = group_sum(zz, gm);
+    if (Q == Q_LINF) {
+      int cnt;
+      const double th = linf_theta_bits([&](int f) { return sx[f] + sz[f]; }, d, rl, &cnt);
+      for (int f = threadIdx.x; f < d; f += blockDim.x) {
+        const double x = sx[f];
+        const double e = x - (th < 0.0 ? 0.0 : clampd(x + sz[f], th));
+        al += e * e;
+      }
+      al = group_sum(al, gm);
+      t0 = w[row_] * group_max(xm, gm);
+      excess = fmax(excess, group_sum(z1, gm) - (rl + 1e-9));
+    } else if (Q == Q_L2) {
+      const double nu = sqrt(group_sum(uu, gm));
+      if (nu <= rl) {
+        al = xb2;
+      } else {
+        const double sc = 1.0 - rl / nu;
+        for (int f = threadIdx.x; f < d; f += blockDim.x) {
+          const double x = sx[f];
+          const double e = x - sc * (x + sz[f]);
+          al += e * e;
+        }
+        al = group_sum(al, gm);
+      }
+      t0 = w[row_] * sqrt(xb2);
+      excess = fmax(excess, sqrt(zz) - (rl + 1e-9));
+    } else {
+      for (int f = threadIdx.x; f < d; f += blockDim.x) {
+        const double x = sx[f];
+        const double e = x - soft(x + sz[f], rl);
+        al += e * e;
+      }
+      al = group_sum(al, gm);
+      t0 = w[row_] * group_sum(l1, gm);
+      excess = fmax(excess, group_max(zmax, gm) - (rl + 1e-9));
     }
-    const double t0 = w[row_] * group_max(xm, gm), t1 = group_sum(al, gm), t2 = group_sum(xb2, gm),
-                 t3 = group_sum(zz, gm);
-    excess = fmax(excess, group_sum(z1, gm) - (rl + 1e-9));
-    if (threadIdx.x == 0) s[0] += t0, s[1] += t1, s[2] += t2, s[3] += t3;
+    if (threadIdx.x == 0) s[0] += t0, s[1] += al, s[2] += xb2, s[3] += zz;
     __syncwarp();
   }
   for (int k = 0; k < 4; ++k) {
@@ -1087,6 +1124,48 @@ __global__ void __launch_bounds__(32 * kLinfWarps) k_gap_edge_linf_s(
   }
   const double m = block_max(excess, sh);
   if (threadIdx.x == 0 && threadIdx.y == 0) part[5 * blockIdx.x + 4] = m;
+}
+// project_columns (prox.cpp:82-93) with the row staged: q = 2 needs ||z|| before scaling and
+// q = inf its threshold passes; one streaming read with batched loads, then shared memory
+template <int Q>
+__global__ void __launch_bounds__(32 * kLinfWarps) k_project_cols_s(const double* __restrict__ Z,
+                                                                     const double* __restrict__ r, int64_t E, int d,
+                                                                     double* __restrict__ out) {
+  extern __shared__ double srow[];
+  const unsigned gm = group_mask();
+  double* sz = srow + static_cast<size_t>(threadIdx.y) * d;
+  ROWS_BEGIN(E) {
+    const double* z = Z + row_ * d;
+    double* o = out + row_ * d;
+    const double rl = r[row_];
+    double ss = 0.0;
+    for (int f0 = threadIdx.x; f0 < d; f0 += 8 * 32) {
+      double a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = f0 + 32 * u;
+        a[u] = f < d ? __ldcs(z + f) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = f0 + 32 * u;
+        if (f < d) {
+          sz[f] = a[u];
+          if (Q == Q_L2) ss += a[u] * a[u];
+        }
+      }
+    }
+    if (Q == Q_L2) {
+      const double nz = sqrt(group_sum(ss, gm));
+      const double sc = rl / nz;
+      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = (nz <= rl) ? sz[f] : sc * sz[f];
+    } else {
+      int cnt;
+      const double th = linf_theta_bits([&](int f) { return sz[f]; }, d, rl, &cnt);
+      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = th < 0.0 ? sz[f] : soft(sz[f], th);
+    }
+    __syncwarp();
+  }
 }
 // Launch one of the staged q = inf kernels on `grid` blocks (the generic kernel's grid, so the
 // partial tables keep their shape).
@@ -1100,9 +1179,17 @@ void launch_linf_s(K kernel, int rows, int64_t d, int grid, cudaStream_t s, Args
 // gap edge terms over `sel` on `grid` blocks (5 partials per block)
 void gap_edge_launch(Ctx& c, int grid, const GroupGeom& ge, const double* X, const double* Z, const Prob& P,
                      EdgeSel sel, int64_t d, double* pe) {
-  if (P.q == Q_LINF && linf_staged(d, 2)) {
-    launch_linf_s(k_gap_edge_linf_s, 2, d, grid, c.s, X, Z, (const int*)P.g->ei.p, (const int*)P.g->ej.p,
-                  (const double*)P.rad, (const double*)P.g->w.p, sel, static_cast<int>(d), pe);
+  if (linf_staged(d, 2)) {  // 32-lane rows that fit two staged rows per warp
+    auto args = [&](auto kernel) {
+      launch_linf_s(kernel, 2, d, grid, c.s, X, Z, (const int*)P.g->ei.p, (const int*)P.g->ej.p,
+                    (const double*)P.rad, (const double*)P.g->w.p, sel, static_cast<int>(d), pe);
+    };
+    if (P.q == Q_LINF)
+      args(k_gap_edge_s<Q_LINF>);
+    else if (P.q == Q_L2)
+      args(k_gap_edge_s<Q_L2>);
+    else
+      args(k_gap_edge_s<Q_L1>);
     return;
   }
   k_gap_edge<<<grid, dim3(ge.gx, ge.gy), 0, c.s>>>(X, Z, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, sel,
@@ -1446,6 +1533,13 @@ void prox_columns_dev(Ctx& c, int q, const double* V, const double* t, int64_t d
 void project_columns_dev(Ctx& c, int q, const double* Z, const double* r, int64_t d, int64_t E, double* out) {
   if (E == 0) return;
   GroupGeom gg = group_geom(c, E, d);
+  if ((q == Q_L2 || q == Q_LINF) && linf_staged(d, 1)) {  // one HBM read of Z instead of two
+    if (q == Q_L2)
+      launch_linf_s(k_project_cols_s<Q_L2>, 1, d, gg.grid, c.s, Z, r, E, static_cast<int>(d), out);
+    else
+      launch_linf_s(k_project_cols_s<Q_LINF>, 1, d, gg.grid, c.s, Z, r, E, static_cast<int>(d), out);
+    return;
+  }
   k_project_cols<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(q, Z, r, E, static_cast<int>(d), out);
   CPB_LAUNCH_CHECK();
 }

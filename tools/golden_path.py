@@ -33,6 +33,13 @@ CONFIGS = {  # bench.py CONFIGS (kept in sync by tests/test_abi_cpu.py)
     "c1": dict(n=1000, d=2, k=10, phi=0.5, q=2, algorithm="ama", centers="circle", gamma=(0.01, 10.0), T=20),
     "c2": dict(n=10000, d=784, k=10, phi=0.5, q=2, algorithm="ssnal", centers="gauss", gamma=(0.01, 10.0), T=20),
     "c3": dict(n=70000, d=784, k=10, phi=0.5, q=2, algorithm="ssnal", centers="gauss", gamma=(0.01, 10.0), T=20),
+    # C4-shaped rows (d = 3072) at n = 3000 with capped solves (C4's own gamma_1 needs hundreds of
+    # Newton steps): every solve stops after 2 outer iterations of <= 5 Newton steps of <= 60 CG
+    # iterations, identically on both sides, so the whole capped path is comparable
+    "c4s_q1": dict(n=3000, d=3072, k=10, phi=0.5, q=1, algorithm="ssnal", centers="gauss", gamma=(0.01, 10.0),
+                   T=20, max_iter=2, ssnal_newton_max=5, pcg_max_iter=60),
+    "c4s_qinf": dict(n=3000, d=3072, k=10, phi=0.5, q=0, algorithm="ssnal", centers="gauss", gamma=(0.01, 10.0),
+                     T=20, max_iter=2, ssnal_newton_max=5, pcg_max_iter=60),
 }
 
 
@@ -94,7 +101,8 @@ def main():
         wx = np.load(os.path.join(scratch, f"{name}_X_{t_start - 1}.npy"))
         wz = np.load(os.path.join(scratch, f"{name}_Z_last.npy"))
         warm = orc.Solution(wx, wz, {})
-    ocfg = orc.config(cfg["algorithm"])
+    ocfg = orc.config(cfg["algorithm"], max_iter=cfg.get("max_iter", 0),
+                      ssnal_newton_max=cfg.get("ssnal_newton_max", 50), pcg_max_iter=cfg.get("pcg_max_iter", 500))
     for t in range(t_start, T):
         t1 = time.perf_counter()
         sol = orc.solve(A, og, gam[t], cfg["q"], ocfg, warm=warm)
