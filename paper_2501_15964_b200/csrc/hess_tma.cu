@@ -31,7 +31,7 @@ namespace cpb {
 namespace {
 
 constexpr int kSegEdges = 64;
-constexpr int kMaxSlots = 8;  // row slots per warp (4 at d = 784)
+constexpr int kMaxStages = 8;  // ring depth per warp: 2 at d = 784, up to 8 for short rows
 
 
 // Per-warp shared memory: a metadata table for the current segment (<= 64
@@ -51,50 +51,35 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
                                                   const int* __restrict__ seg_end, const int* __restrict__ seg_slot,
                                                   int nseg, int d, int dp, double sigma, double* __restrict__ Ap,
                                                   double* __restrict__ partial, double* part, const int* active,
-                                                  int R, const int* __restrict__ wrange) {
+                                                  int S, const int* __restrict__ wrange) {
   if (active && !*active) return;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ double sh[32];
-  __shared__ uint64_t bars[4][kMaxSlots];
+  __shared__ uint64_t bars[4][kMaxStages];
   __shared__ int m_le[4][kSegEdges], m_lo[4][kSegEdges];
   __shared__ double m_ca[4][kSegEdges], m_be[4][kSegEdges];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // the warp's ring of R row slots (one mbarrier each): an edge takes one slot for p_other and,
-  // when active, the next for v_l, so inactive edges (most of them once clusters fuse) keep
-  // twice as many rows in flight as fixed two-row stages would
-  double* ring = reinterpret_cast<double*>(smraw) + static_cast<size_t>(warp) * R * dp;
+  double* ring = reinterpret_cast<double*>(smraw) + static_cast<size_t>(warp) * S * 2 * dp;
   uint64_t* bar = bars[warp];
   int* le = m_le[warp];
   int* lo = m_lo[warp];
   double* ca = m_ca[warp];
   double* mb = m_be[warp];
   if (lane == 0)
-    for (int s = 0; s < R; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
   fence_mbar_init();
   fence_proxy_async();
   __syncwarp();
   const unsigned row_bytes = static_cast<unsigned>(d) * 8u;
-  int cs = 0;          // next slot to consume (all lanes)
-  unsigned cph = 0u;   // per-slot mbarrier phase parities (bit s)
-  int is = 0, used = 0, qi = 0;  // lane 0: next slot to fill, slots in flight, next edge to issue
+  int cst = 0;        // next ring slot to consume
+  unsigned cph = 0;   // its mbarrier phase parity
   double s_a = 0.0, s_b = 0.0;
-  auto fill = [&](int ne) {  // lane 0: issue edges while their slots are free
-    while (qi < ne) {
-      const bool nv = mb[qi] != 0.0;
-      if (used + (nv ? 2 : 1) > R) break;
-      mbar_expect_tx(&bar[is], row_bytes);
-      bulk_g2s(ring + static_cast<size_t>(is) * dp, P + static_cast<int64_t>(lo[qi]) * d, row_bytes, &bar[is]);
-      is = (is + 1 == R) ? 0 : is + 1;
-      if (nv) {
-        mbar_expect_tx(&bar[is], row_bytes);
-        bulk_g2s(ring + static_cast<size_t>(is) * dp, V + static_cast<int64_t>(le[qi]) * d, row_bytes, &bar[is]);
-        is = (is + 1 == R) ? 0 : is + 1;
-      }
-      used += nv ? 2 : 1;
-      ++qi;
-    }
+  auto issue = [&](int q, int st) {  // lane 0: stream edge q's rows into stage st
+    const bool nv = mb[q] != 0.0;
+    mbar_expect_tx(&bar[st], nv ? 2 * row_bytes : row_bytes);
+    bulk_g2s(ring + st * 2 * dp, P + static_cast<int64_t>(lo[q]) * d, row_bytes, &bar[st]);
+    if (nv) bulk_g2s(ring + st * 2 * dp + dp, V + static_cast<int64_t>(le[q]) * d, row_bytes, &bar[st]);
   };
-
   const int wid = blockIdx.x * (blockDim.x >> 5) + warp, nw = gridDim.x * (blockDim.x >> 5);
   // each warp walks its balanced item list (wrange: offsets, then items) or, without it, every nw-th item
   const int j0 = wrange ? wrange[wid] : wid, j1 = wrange ? wrange[wid + 1] : nseg, jstep = wrange ? 1 : nw;
@@ -112,8 +97,7 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
     }
     __syncwarp();
     if (lane == 0) {
-      qi = 0;
-      fill(ne);
+      for (int s = 0, t = cst; s < S && s < ne; ++s, t = (t + 1 == S) ? 0 : t + 1) issue(s, t);
     }
     double pv[NK], acc[NK];
 #pragma unroll
@@ -124,18 +108,12 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
     }
     double dsum = 0.0;
     for (int q = 0; q < ne; ++q) {
+      const int st = cst;
       const double cq = ca[q], be = mb[q];
-      const int sp = cs, sv = (cs + 1 == R) ? 0 : cs + 1;
-      mbar_wait(&bar[sp], (cph >> sp) & 1u);
-      cph ^= 1u << sp;
-      const double* po = ring + static_cast<size_t>(sp) * dp;
-      const double* vl = ring + static_cast<size_t>(sv) * dp;
-      const int nslot = be != 0.0 ? 2 : 1;
-      if (be != 0.0) {
-        mbar_wait(&bar[sv], (cph >> sv) & 1u);
-        cph ^= 1u << sv;
-      }
-      cs = (cs + nslot) % R;
+      mbar_wait(&bar[st], cph);
+      if (++cst == S) cst = 0, cph ^= 1u;
+      const double* po = ring + st * 2 * dp;
+      const double* vl = po + dp;
       if (be != 0.0) {
         // w = p_v - p_o stays in registers: the update re-reads only v_l
         double w[NK];
@@ -165,13 +143,10 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
           if (f < d) acc[k] = __fma_rn(-cq, po[f], acc[k]);
         }
       }
-      // the warp's reads of these slots are ordered before their refill by the
+      // the warp's reads of this slot are ordered before the refill by the
       // warp barrier (only reads: no generic->async proxy fence is needed)
       __syncwarp();
-      if (lane == 0) {
-        used -= nslot;
-        fill(ne);
-      }
+      if (lane == 0 && q + S < ne) issue(q + S, st);
     }
     __syncwarp();  // metadata table is rewritten by the next segment
     if (slot < 0) {
@@ -354,8 +329,8 @@ int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const dou
   // ring depth 2 (deeper rings measured slower: C5 with 8 stages 38.8 vs 17.4 ms;
   // an L2 evict_first policy on the streamed V_l rows measured neutral-to-worse
   // at C3, 1586 vs 1541 us)
-  const int R = 4;  // row slots per warp: 2 active edges or 4 inactive ones in flight
-  const size_t smem = static_cast<size_t>(warps) * R * dp * sizeof(double);
+  const int S = 2;
+  const size_t smem = static_cast<size_t>(warps) * S * 2 * dp * sizeof(double);
   if (smem > 220 * 1024) invalid("hessian: shared-memory ring exceeds 220 KB");
   NK_DISPATCH(nk, set_smem, (static_cast<int>(smem)));
   double* partial = c.buf<double>("hess.partial", static_cast<size_t>(sp.nslots) * d + 1);
@@ -366,7 +341,7 @@ int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const dou
   NK_DISPATCH(nk, k_hess_tma, <<<grid, 32 * warps, smem, c.s>>>(P, V, jal, jbe, g.adj_e.p, g.adj_o.p, sp.node.p,
                                                                 sp.beg.p, sp.end.p, sp.slot.p, sp.nseg,
                                                                 static_cast<int>(d), dp, sigma, Ap, partial, part,
-                                                                active, R, wr));
+                                                                active, S, wr));
   CPB_LAUNCH_CHECK();
   int nb = grid;
   if (sp.nhub > 0 || parted) {
