@@ -413,15 +413,21 @@ __global__ void __launch_bounds__(256) k_edge_dot_inf(const double* __restrict__
 
 // ---- SSNAL Hessian, pass 2: node gather (ssnal.cpp:56-64) -----------------------------------
 // Ap_v = p_v + sigma sum_l +-(w - (alpha w + bc v)),  w = p_i(l) - p_j(l).
-template <int NF>
-__global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, const double* __restrict__ V,
+// QT = the penalty q as a compile-time constant: 2 reads V_l for active edges; 1 and 0
+// (q = inf) read the edge_masks bits instead and carry no V registers (C4: 245 -> fewer
+// registers per thread, more warps in flight for the p gathers).
+template <int NF, int QT>
+__global__ void __launch_bounds__(256, QT == 2 ? 1 : 2) k_g_hess(const double* __restrict__ P, const double* __restrict__ V,
                                                 const double* __restrict__ jal, const double* __restrict__ bc,
                                                 const double* __restrict__ thr, const int* __restrict__ off,
                                                 const int* __restrict__ adj_e, const int* __restrict__ adj_o,
                                                 const int* __restrict__ order, int64_t n, int d, int nch,
-                                                double sigma, int q, double* __restrict__ Ap, double* part,
+                                                double sigma, int q_unused, double* __restrict__ Ap, double* part,
                                                 const int* active, const unsigned* __restrict__ mask,
                                                 const unsigned* __restrict__ sgn) {
+  constexpr int q = QT;
+  constexpr int EB = QT == 2 ? kEB : 2;  // edges per load batch (mask variants: 2, for 2 blocks per SM)
+  (void)q_unused;
   if (active && !*active) return;
   __shared__ double sh[32];
   double s_a = 0.0, s_b = 0.0;
@@ -443,30 +449,32 @@ __global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, co
     const int my_o = lane < cnt ? adj_o[p + lane] : v;
     const double my_a = lane < cnt ? ((q == 2 || q == 0) ? jal[my_e] : thr[my_e]) : 0.0;
     const double my_b = (lane < cnt && (q == 2 || q == 0)) ? bc[my_e] : 0.0;
-    for (int u0 = 0; u0 < cnt; u0 += kEB) {
-      int le[kEB], lo[kEB];
-      double ea[kEB], eb[kEB];
+    for (int u0 = 0; u0 < cnt; u0 += EB) {
+      int le[EB], lo[EB];
+      double ea[EB], eb[EB];
 #pragma unroll
-      for (int u = 0; u < kEB; ++u) {
+      for (int u = 0; u < EB; ++u) {
         const int src = (u0 + u) & 31;
         le[u] = __shfl_sync(kFull, my_e, src);
         lo[u] = __shfl_sync(kFull, my_o, src);
         ea[u] = __shfl_sync(kFull, my_a, src);
         eb[u] = __shfl_sync(kFull, my_b, src);
       }
-      double po[kEB][NF], vv[kEB][NF];
-      unsigned mb[kEB][NF], sb[kEB][NF];  // q = 1 / inf with masks: S membership and sign bits
+      constexpr int VE = QT == 2 ? EB : 1, ME = QT == 2 ? 1 : EB, SE = QT == 0 ? EB : 1;
+      double po[EB][NF], vv[VE][NF];
+      unsigned mb[ME][NF], sb[SE][NF];  // q = 1 / inf: S membership and sign bits (edge_masks)
 #pragma unroll
-      for (int u = 0; u < kEB; ++u) {
+      for (int u = 0; u < EB; ++u) {
         const bool ok = u0 + u < cnt;
-        const bool need_v = ok && (q != 2 || eb[u] != 0.0) && !(mask && q != 2);
 #pragma unroll
         for (int k = 0; k < NF; ++k) {
           const int f = f0 + 32 * k;
           po[u][k] = (ok && f < d) ? __ldg(P + static_cast<int64_t>(lo[u]) * d + f) : 0.0;
-          vv[u][k] = (need_v && f < d) ? __ldcs(V + static_cast<int64_t>(le[u]) * d + f) : 0.0;
-          mb[u][k] = (mask && ok && f < d) ? mask[static_cast<int64_t>(le[u]) * W + w0 + k] : 0u;
-          sb[u][k] = (sgn && ok && f < d && q == 0) ? sgn[static_cast<int64_t>(le[u]) * W + w0 + k] : 0u;
+          if constexpr (QT == 2)
+            vv[u][k] = (ok && eb[u] != 0.0 && f < d) ? __ldcs(V + static_cast<int64_t>(le[u]) * d + f) : 0.0;
+          else
+            mb[u][k] = (ok && f < d) ? mask[static_cast<int64_t>(le[u]) * W + w0 + k] : 0u;
+          if constexpr (QT == 0) sb[u][k] = (ok && f < d) ? sgn[static_cast<int64_t>(le[u]) * W + w0 + k] : 0u;
         }
       }
       if (q == 2) {
@@ -474,7 +482,7 @@ __global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, co
         // (s = +1 when v is the smaller endpoint); the p_v part is summed as a
         // scalar, the rest is two FMAs per feature.
 #pragma unroll
-        for (int u = 0; u < kEB; ++u) {
+        for (int u = 0; u < EB; ++u) {
           if (u0 + u >= cnt) continue;
           const double ca = 1.0 - ea[u];
           const double cb = (lo[u] > v) ? eb[u] : -eb[u];
@@ -482,34 +490,38 @@ __global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, co
 #pragma unroll
           for (int k = 0; k < NF; ++k) {
             acc[k] = __fma_rn(-ca, po[u][k], acc[k]);
-            if (cb != 0.0) acc[k] = __fma_rn(-cb, vv[u][k], acc[k]);
+            if constexpr (QT == 2)
+              if (cb != 0.0) acc[k] = __fma_rn(-cb, vv[u][k], acc[k]);
           }
         }
       } else if (q == 0) {  // (I - M) w = 1_S (w - s bc), identity inside the ball
 #pragma unroll
-        for (int u = 0; u < kEB; ++u) {
+        for (int u = 0; u < EB; ++u) {
           if (u0 + u >= cnt) continue;
           const bool plus = lo[u] > v;
           const double th = ea[u];
 #pragma unroll
           for (int k = 0; k < NF; ++k) {
             const double w = plus ? pv[k] - po[u][k] : po[u][k] - pv[k];
-            const double vf = vv[u][k];
-            const bool in_s = mask ? (mb[u][k] & lbit) != 0u : fabs(vf) > th;
-            const bool pos = mask ? (sb[u][k] & lbit) != 0u : vf > 0.0;
+            bool in_s = false, pos = false;
+            if constexpr (QT == 0) {
+              in_s = (mb[u][k] & lbit) != 0u;
+              pos = (sb[u][k] & lbit) != 0u;
+            }
             const double y = th < 0.0 ? w : (in_s ? w - (pos ? eb[u] : -eb[u]) : 0.0);
             acc[k] = plus ? acc[k] + y : acc[k] - y;
           }
         }
       } else {
 #pragma unroll
-        for (int u = 0; u < kEB; ++u) {
+        for (int u = 0; u < EB; ++u) {
           if (u0 + u >= cnt) continue;
           const bool plus = lo[u] > v;
 #pragma unroll
           for (int k = 0; k < NF; ++k) {
             const double w = plus ? pv[k] - po[u][k] : po[u][k] - pv[k];
-            const bool act = mask ? (mb[u][k] & lbit) != 0u : fabs(vv[u][k]) > ea[u];
+            bool act = false;
+            if constexpr (QT == 1) act = (mb[u][k] & lbit) != 0u;
             const double y = w - (act ? w : 0.0);
             acc[k] = plus ? acc[k] + y : acc[k] - y;
           }
@@ -536,6 +548,13 @@ __global__ void __launch_bounds__(256) k_g_hess(const double* __restrict__ P, co
   }
 }
 
+
+template <int NF>
+constexpr auto k_g_hess2 = k_g_hess<NF, 2>;
+template <int NF>
+constexpr auto k_g_hess1 = k_g_hess<NF, 1>;
+template <int NF>
+constexpr auto k_g_hess0 = k_g_hess<NF, 0>;
 
 // ---- single-pass Hessian for short rows (q = 2, even d <= 256) --------------------------
 // One warp per node; lane l holds the feature pairs 2(l + 32k), k < NP, as
@@ -991,9 +1010,18 @@ int hess_two_pass(Ctx& c, const Graph& g, const double* P, const double* V, cons
     const OwnOrder& o = own_order(c, g);
     ord = o.order.p, items = o.count, grid = c.sm_count * 8;
   }
-  NF_DISPATCH(ng.nf, k_g_hess, <<<grid, 256, 0, c.s>>>(P, V, jal, bc, thr, g.off.p, g.adj_e.p, g.adj_o.p, ord,
-                                                        items, di, nch, sigma, q, Ap, part, active,
-                                                        q != 2 ? mask : nullptr, q != 2 ? sgn : nullptr));
+  if (q != 2 && !mask) invalid("hessian: q = 1 / inf needs the edge_masks bits");
+  if (q == 2) {
+    NF_DISPATCH(ng.nf, k_g_hess2, <<<grid, 256, 0, c.s>>>(P, V, jal, bc, thr, g.off.p, g.adj_e.p, g.adj_o.p, ord,
+                                                           items, di, nch, sigma, q, Ap, part, active, nullptr,
+                                                           nullptr));
+  } else if (q == 1) {
+    NF_DISPATCH(ng.nf, k_g_hess1, <<<grid, 256, 0, c.s>>>(P, V, jal, bc, thr, g.off.p, g.adj_e.p, g.adj_o.p, ord,
+                                                           items, di, nch, sigma, q, Ap, part, active, mask, sgn));
+  } else {
+    NF_DISPATCH(ng.nf, k_g_hess0, <<<grid, 256, 0, c.s>>>(P, V, jal, bc, thr, g.off.p, g.adj_e.p, g.adj_o.p, ord,
+                                                           items, di, nch, sigma, q, Ap, part, active, mask, sgn));
+  }
   CPB_LAUNCH_CHECK();
   return grid;
 }
