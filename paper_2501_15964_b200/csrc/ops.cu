@@ -282,9 +282,10 @@ __global__ void k_phi_edge(const double* __restrict__ X, const double* __restric
       }
     } else {
       double a = 0.0, b = 0.0;
+#pragma unroll 4
       for (int f = threadIdx.x; f < d; f += blockDim.x) {
-        const double x = (xa[f] - xb[f]) + z[f] / sigma;
-        v[f] = x;
+        const double x = (xa[f] - xb[f]) + __ldcs(z + f) / sigma;
+        __stcs(v + f, x);
         const double p = soft(x, t);
         a += fabs(p);
         b += (p - x) * (p - x);
