@@ -232,7 +232,9 @@ const int* warp_ranges(Ctx& c, SegPlan& p, int nw) {
   if (p.split_nw == nw) return p.wrange.p;
   std::vector<int64_t> cost(static_cast<size_t>(p.nseg));
   for (int i = 0; i < p.nseg; ++i) cost[i] = p.cost_prefix[i + 1] - p.cost_prefix[i];
+  trace("warp_ranges begin");
   const std::vector<int> flat = lpt_lists(cost, nw, nw);  // windows of one item per warp
+  trace("warp_ranges lpt done");
   p.wrange.resize(flat.size());
   h2d(c, p.wrange.p, flat.data(), flat.size() * sizeof(int));
   c.sync();
@@ -248,9 +250,11 @@ SegPlan& seg_plan(Ctx& c, const Graph& g) {
   p->uid = g.uid;
   p->v0 = c.own_v0;
   p->v1 = c.own_v1;
+  trace("seg_plan begin");
   std::vector<int> off, seq;
   if (g.E > 0) {
     seq = bfs_sequence(c, g, &off);
+    trace("seg_plan bfs done");
   } else {
     off.resize(static_cast<size_t>(g.n + 1));
     d2h(c, off.data(), g.off.p, off.size() * sizeof(int));
@@ -287,6 +291,7 @@ SegPlan& seg_plan(Ctx& c, const Graph& g) {
   p->nslots = slots;
   if (plans.size() > 8) plans.erase(plans.begin());
   plans.push_back(std::move(p));
+  trace("seg_plan built");
   return *plans.back();
 }
 

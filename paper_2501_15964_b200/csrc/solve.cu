@@ -597,6 +597,7 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
       CPB_CUDA(cudaEventRecord(copy_done[s], cs));
     }
   }
+  int64_t K_prev = -1;
   for (int64_t t = 0; t < T; ++t) {
     const double gamma = gammas[t];
     Prob P;
@@ -609,16 +610,22 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
     make_radii(c, g, gamma, rad);
     cp_termination term = solve_dev(P, cfg, warm, X, Z, cache);
     if (sink && sink->trace) sink->trace(sink->user, t, c.trace.data(), static_cast<int64_t>(c.trace.size()));
-    const int64_t K = extract_clusters_dev(c, g, X, d, opt.fuse_tol, lab, cent);
+    // a warm start the solver accepted as is (0 iterations, gamma > 0, edges present) leaves X
+    // bitwise unchanged, so the previous gamma's labels, K and centroids are this gamma's
+    const bool x_unchanged = warm && term.iterations == 0 && gamma > 0.0 && E > 0 && K_prev >= 0;
+    const int64_t K = x_unchanged ? K_prev : extract_clusters_dev(c, g, X, d, opt.fuse_tol, lab, cent);
+    K_prev = K;
     if (cent && !(sink->skip_identity && K == n)) {  // ClusterAssignment::centroids (path.cpp:135)
-      hcent.resize(static_cast<size_t>(K * d));
-      d2h(c, hcent.data(), cent, K * d * sizeof(double));
+      if (!x_unchanged) {
+        hcent.resize(static_cast<size_t>(K * d));
+        d2h(c, hcent.data(), cent, K * d * sizeof(double));
+      }
       sink->centroids(sink->user, t, K, d, hcent.data());
     }
     if (terms_out) terms_out[t] = term;
     if (K_out) K_out[t] = K;
     if (labels_out) {
-      d2h(c, hl.data(), lab, n * sizeof(int));
+      if (!x_unchanged) d2h(c, hl.data(), lab, n * sizeof(int));
       for (int64_t i = 0; i < n; ++i) labels_out[t * n + i] = hl[static_cast<size_t>(i)];
     }
     if (async_out) {
