@@ -3,9 +3,14 @@
 // to return codes (CP_EINVAL = std::invalid_argument, CP_ERUNTIME =
 // std::runtime_error) with a thread-local message.  There is no CPU fallback:
 // without a CUDA device cp_ctx_create fails with CP_ERUNTIME.
+#include <sys/mman.h>
+
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <thread>
 #include <random>
 #include <string>
 #include <vector>
@@ -41,6 +46,16 @@ struct cp_factor {
 
 namespace {
 thread_local std::string g_err;
+
+// page-locked blocks made by mmap + cudaHostRegister: user pointer -> (mapping base, length)
+std::map<void*, std::pair<void*, size_t>>& host_blocks() {
+  static std::map<void*, std::pair<void*, size_t>> m;
+  return m;
+}
+std::mutex& host_blocks_mu() {
+  static std::mutex mu;
+  return mu;
+}
 
 template <class F>
 int guard(cp_ctx* ctx, F f) {
@@ -204,15 +219,63 @@ int cp_flush_l2(cp_ctx* ctx) {
   });
 }
 
+// Large blocks (the path's output pool: 89 GB at C3) are page-locked from transparent huge
+// pages: anonymous mmap aligned to 2 MB, MADV_HUGEPAGE, first touch by parallel threads, then
+// cudaHostRegister (portable, mapped).  Measured on the B200 box: 48 GB in 3.8 s against
+// 19.9 s for cudaHostAlloc (tools/pin_probe.py), which is most of a cold run_path.
 int cp_host_alloc(uint64_t bytes, void** out) {
   return guard(nullptr, [&] {
     need(out, "out");
     *out = nullptr;
-    CPB_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable | cudaHostAllocMapped));
+    if (bytes < (uint64_t(64) << 20)) {
+      CPB_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable | cudaHostAllocMapped));
+      return;
+    }
+    const size_t huge = size_t(2) << 20;
+    const size_t len = static_cast<size_t>(bytes) + huge;
+    void* base = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (base == MAP_FAILED) throw std::bad_alloc();
+    char* p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(base) + huge - 1) & ~(uintptr_t(huge) - 1));
+    madvise(p, static_cast<size_t>(bytes), MADV_HUGEPAGE);
+    const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    const size_t chunk = (static_cast<size_t>(bytes) / nt + huge - 1) / huge * huge;
+    for (unsigned k = 0; k < nt; ++k) {
+      const size_t a = k * chunk;
+      if (a >= bytes) break;
+      const size_t b = std::min(static_cast<size_t>(bytes), a + chunk);
+      pool.emplace_back([p, a, b] { std::memset(p + a, 0, b - a); });
+    }
+    for (auto& t : pool) t.join();
+    const cudaError_t e = cudaHostRegister(p, static_cast<size_t>(bytes), cudaHostRegisterPortable | cudaHostRegisterMapped);
+    if (e != cudaSuccess) {
+      munmap(base, len);
+      CPB_CUDA(e);
+    }
+    {
+      std::lock_guard<std::mutex> lk(host_blocks_mu());
+      host_blocks()[p] = {base, len};
+    }
+    *out = p;
   });
 }
 void cp_host_free(void* p) {
-  if (p) cudaFreeHost(p);
+  if (!p) return;
+  std::pair<void*, size_t> blk{nullptr, 0};
+  {
+    std::lock_guard<std::mutex> lk(host_blocks_mu());
+    auto it = host_blocks().find(p);
+    if (it != host_blocks().end()) {
+      blk = it->second;
+      host_blocks().erase(it);
+    }
+  }
+  if (blk.first) {
+    cudaHostUnregister(p);
+    munmap(blk.first, blk.second);
+  } else {
+    cudaFreeHost(p);
+  }
 }
 
 int cp_gaussian_mixture(const double* centers, int64_t d, int64_t m, double spread, int64_t per_center, uint64_t seed,
