@@ -443,17 +443,43 @@ __device__ double eigen_dot(const double* a, const double* b, int n, double* sh,
   }
   return res;
 }
-// <w, w> and <v, w> at once: chains on threads 0-3 and 32-35, one barrier round.
+// <w, w> and <v, w> at once: the two dots' chains run concurrently on lanes 0-3 of warps 0
+// and 1, then lanes 0 of those warps finish them (two block barriers per iteration).
 __device__ __forceinline__ void eigen_dots2(const double* v, const double* w, int n, double* sh /* 64 */,
                                             double& sww, double& svw) {
-  const double a = eigen_dot(w, w, n, sh, 0);  // threads 0..3
-  const double b = eigen_dot(v, w, n, sh + 32, 32);  // threads 32..35 (their own barrier round)
-  if (threadIdx.x == 0) sh[8] = a;
-  if (threadIdx.x == 32) sh[40] = b;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int e2 = (n / 4) * 4;
+  const double* a = wp == 0 ? w : v;  // warp 0: <w, w>, warp 1: <v, w>
+  if (wp < 2 && lane < 4 && n >= 4) {
+    double p = __dmul_rn(a[lane], w[lane]);
+#pragma unroll 8
+    for (int k = lane + 4; k < e2; k += 4) p = __dadd_rn(p, __dmul_rn(a[k], w[k]));
+    sh[wp * 4 + lane] = p;
+  }
+  __syncthreads();
+  if (wp < 2 && lane == 0) {
+    auto f = [&](int k) { return __dmul_rn(a[k], w[k]); };
+    double res;
+    if (n < 2) {
+      res = n == 1 ? f(0) : 0.0;
+    } else {
+      double p00 = f(0), p01 = f(1);
+      if (n >= 4) {
+        p00 = __dadd_rn(sh[wp * 4 + 0], sh[wp * 4 + 2]);
+        p01 = __dadd_rn(sh[wp * 4 + 1], sh[wp * 4 + 3]);
+        if ((n / 2) * 2 > e2) {
+          p00 = __dadd_rn(p00, f(e2));
+          p01 = __dadd_rn(p01, f(e2 + 1));
+        }
+      }
+      res = __dadd_rn(p00, p01);
+      if (n & 1) res = __dadd_rn(res, f(n - 1));
+    }
+    sh[8 + wp] = res;
+  }
   __syncthreads();
   sww = sh[8];
-  svw = sh[40];
-  __syncthreads();
+  svw = sh[9];
 }
 // power_iteration (linalg.cpp:194-242) for one probe per block: w = L v in the column order of
 // L's column-major CSC (SparseDenseProduct.h: neighbours ascending with the degree term at
