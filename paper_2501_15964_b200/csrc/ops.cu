@@ -1663,7 +1663,7 @@ int hess_apply(const Prob& P, const double* p, const double* V, const double* ja
 }
 
 PcgOut pcg_newton(const Prob& P, const double* V, const double* jal, const double* jbe, const double* thr,
-                  double sigma, const double* rhs, PcgWork w, double tol, int64_t max_iter, int64_t n_active) {
+                  double sigma, const double* G, PcgWork w, double tol, int64_t max_iter, int64_t n_active) {
   const int64_t d = P.d(), n = P.n(), E = P.E(), m = d * n;
   // Algorithmic bytes per H-apply: p read + Ap write
   // (2 n d) + the active edge rows (E_a d) + two per-edge scalars + the CSR.
@@ -1684,7 +1684,7 @@ PcgOut pcg_newton(const Prob& P, const double* V, const double* jal, const doubl
   // (everything outside the PCG stays replicated: identical on every rank)
   const bool dist = P.c->comm != nullptr;
   const double op_b = dist ? hess_bytes / P.c->comm->nranks : hess_bytes;
-  return pcg_dev(*P.c, n, d, op, op_b, "hess_apply", rhs, w, tol, max_iter, false, dist, P.g);
+  return pcg_dev(*P.c, n, d, op, op_b, "hess_apply", G, w, tol, max_iter, false, dist, P.g, true);
 }
 
 // Sum (and max) the columns of a (rows x cols) block-partial table on the host,

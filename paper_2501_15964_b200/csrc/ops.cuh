@@ -85,9 +85,10 @@ using PcgOp = std::function<int(const double* p, double* Ap, double* part, const
 // buffers must hold P * ceil(n / P) rows.
 PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, const char* op_name,
                const double* rhs, PcgWork w, double tol, int64_t max_iter, bool warm, bool dist = false,
-               const Graph* halo = nullptr);  // dist: refresh p by halo exchange over this graph (else all-gather)
+               const Graph* halo = nullptr, bool neg_rhs = false);  // neg_rhs: solve for b = -rhs  // dist: refresh p by halo exchange over this graph (else all-gather)
+// the Newton system H D = -G: `G` is the gradient (negated inside the PCG's first pass)
 PcgOut pcg_newton(const Prob& P, const double* V, const double* jal, const double* jbe, const double* thr,
-                  double sigma, const double* rhs, PcgWork w, double tol, int64_t max_iter, int64_t n_active);
+                  double sigma, const double* G, PcgWork w, double tol, int64_t max_iter, int64_t n_active);
 
 // ---- objectives / gap (objective.cpp:63-113) --------------------------------
 struct GapOut {

@@ -66,7 +66,8 @@ __device__ __forceinline__ double tile_col_sum(double v, double* s8) {
   return r;
 }
 
-__global__ void __launch_bounds__(256) k_cg_init(const double* __restrict__ rhs, const double* __restrict__ Mx,
+// neg: the right-hand side is -rhs (SSNAL passes its gradient G for b = -G: no separate negation pass)
+__global__ void __launch_bounds__(256) k_cg_init(const double* __restrict__ rhs, int neg, const double* __restrict__ Mx,
                                                  const double* __restrict__ diag, int64_t n, int d, int F,
                                                  int64_t rows_per, double* __restrict__ x, double* __restrict__ r,
                                                  double* __restrict__ p, double* part_rz, double* part_bb) {
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(256) k_cg_init(const double* __restrict__ rhs,
 #pragma unroll 4
     for (int64_t v = r0 + threadIdx.y; v < r1; v += 8) {
       const int64_t i = v * d + f;
-      const double b = rhs[i];
+      const double b = neg ? -rhs[i] : rhs[i];
       const double rv = Mx ? b - Mx[i] : b;
       if (!Mx) x[i] = 0.0;
       r[i] = rv;
@@ -220,7 +221,7 @@ const int* cg_active_ptr(const void* st) { return st ? &static_cast<const CgStat
 
 PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, const char* op_name,
                const double* rhs, PcgWork w, double tol, int64_t max_iter, bool warm, bool dist,
-               const Graph* halo) {
+               const Graph* halo, bool neg_rhs) {
   if (!(tol > 0.0)) invalid("pcg: tol must be positive");
   if (max_iter < 1) invalid("pcg: max_iter must be >= 1");
   dist = dist && c.comm != nullptr;
@@ -265,7 +266,7 @@ PcgOut pcg_dev(Ctx& c, int64_t n, int64_t d, const PcgOp& op, double op_bytes, c
   }
   const int di = static_cast<int>(d);
   const dim3 tb(32, 8);
-  k_cg_init<<<nblk, tb, 0, c.s>>>(rhs + off, Mx ? Mx + off : nullptr, w.diag + off, nown, di, tg.F, tg.rows_per,
+  k_cg_init<<<nblk, tb, 0, c.s>>>(rhs + off, neg_rhs ? 1 : 0, Mx ? Mx + off : nullptr, w.diag + off, nown, di, tg.F, tg.rows_per,
                                   w.x + off, w.r + off, w.p + off, part_rz, part_rr);
   CPB_LAUNCH_CHECK();
   if (dist) {

@@ -141,8 +141,7 @@ cp_termination ssnal(Prob& P, const cp_solver_config& cfg, bool warm, double* Xo
       if (gnorm <= eps_k) break;
       ++cnt.newton;
       const double cg_tol = std::max(std::min(0.1, std::sqrt(gnorm)), 1e-12);
-      neg_dev(c, w.r, G, m);
-      PcgOut dir = pcg_newton(P, V, jal, jbe, thr, sigma, w.r, w, cg_tol, cfg.pcg_max_iter, n_active);
+      PcgOut dir = pcg_newton(P, V, jal, jbe, thr, sigma, G, w, cg_tol, cfg.pcg_max_iter, n_active);
       cnt.cg += dir.iterations;
       cnt.hess_apply += dir.iterations;
       double* D = w.x;
