@@ -43,7 +43,9 @@ constexpr int kMaxStages = 8;  // ring depth per warp: 2 at d = 784, up to 8 for
 // in registers, so the update reads only v_l back from shared memory).  An
 // edge with beta = 0 (prox zero) adds (1 - alpha)(p_v - p_o): its p_v part is
 // folded into one final FMA.
-template <int NK>
+// FULL: d >= 32 (NK - 1), so the first NK - 1 feature chunks of a row are complete and only
+// the last needs the f < d predicate (d = 784: 24 full chunks + 16 lanes).
+template <int NK, bool FULL>
 __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, const double* __restrict__ V,
                                                   const double* __restrict__ jal, const double* __restrict__ jbe,
                                                   const int* __restrict__ adj_e, const int* __restrict__ adj_o,
@@ -53,6 +55,7 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
                                                   double* __restrict__ partial, double* part, const int* active,
                                                   int S, const int* __restrict__ wrange) {
   if (active && !*active) return;
+  auto in_row = [d](int k, int f) { return (FULL && k < NK - 1) || f < d; };
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ double sh[32];
   __shared__ uint64_t bars[4][kMaxStages];
@@ -103,7 +106,7 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
 #pragma unroll
     for (int k = 0; k < NK; ++k) {
       const int f = lane + 32 * k;
-      pv[k] = f < d ? P[base + f] : 0.0;
+      pv[k] = in_row(k, f) ? P[base + f] : 0.0;
       acc[k] = 0.0;
     }
     double dsum = 0.0;
@@ -121,8 +124,8 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
 #pragma unroll
         for (int k = 0; k < NK; ++k) {
           const int f = lane + 32 * k;
-          w[k] = f < d ? pv[k] - po[f] : 0.0;
-          if (f < d) {
+          w[k] = in_row(k, f) ? pv[k] - po[f] : 0.0;
+          if (in_row(k, f)) {
             if ((k & 3) == 0) c0 = __fma_rn(vl[f], w[k], c0);
             if ((k & 3) == 1) c1 = __fma_rn(vl[f], w[k], c1);
             if ((k & 3) == 2) c2 = __fma_rn(vl[f], w[k], c2);
@@ -133,14 +136,14 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
 #pragma unroll
         for (int k = 0; k < NK; ++k) {
           const int f = lane + 32 * k;
-          if (f < d) acc[k] = __fma_rn(cq, w[k], __fma_rn(-bc, vl[f], acc[k]));
+          if (in_row(k, f)) acc[k] = __fma_rn(cq, w[k], __fma_rn(-bc, vl[f], acc[k]));
         }
       } else {
         dsum += cq;
 #pragma unroll
         for (int k = 0; k < NK; ++k) {
           const int f = lane + 32 * k;
-          if (f < d) acc[k] = __fma_rn(-cq, po[f], acc[k]);
+          if (in_row(k, f)) acc[k] = __fma_rn(-cq, po[f], acc[k]);
         }
       }
       // the warp's reads of this slot are ordered before the refill by the
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
 #pragma unroll
       for (int k = 0; k < NK; ++k) {
         const int f = lane + 32 * k;
-        if (f >= d) continue;
+        if (!in_row(k, f)) continue;
         const double o = pv[k] + sigma * __fma_rn(dsum, pv[k], acc[k]);
         Ap[base + f] = o;
         a += pv[k] * o;
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(128) k_hess_tma(const double* __restrict__ P, 
 #pragma unroll
       for (int k = 0; k < NK; ++k) {
         const int f = lane + 32 * k;
-        if (f < d) partial[static_cast<int64_t>(slot) * d + f] = __fma_rn(dsum, pv[k], acc[k]);
+        if (in_row(k, f)) partial[static_cast<int64_t>(slot) * d + f] = __fma_rn(dsum, pv[k], acc[k]);
       }
     }
   }
@@ -295,24 +298,26 @@ SegPlan& seg_plan(Ctx& c, const Graph& g) {
   return *plans.back();
 }
 
-#define NK_DISPATCH(nk, KERNEL, ...)          \
-  switch (nk) {                               \
-    case 2: KERNEL<2> __VA_ARGS__; break;     \
-    case 4: KERNEL<4> __VA_ARGS__; break;     \
-    case 8: KERNEL<8> __VA_ARGS__; break;     \
-    case 16: KERNEL<16> __VA_ARGS__; break;   \
-    case 25: KERNEL<25> __VA_ARGS__; break;   \
-    default: KERNEL<32> __VA_ARGS__; break;   \
+#define NK_DISPATCH(nk, full, KERNEL, ...)                                     \
+  switch (nk * 2 + (full ? 1 : 0)) {                                           \
+    case 2 * 8: KERNEL<8, false> __VA_ARGS__; break;                           \
+    case 2 * 8 + 1: KERNEL<8, true> __VA_ARGS__; break;                        \
+    case 2 * 16: KERNEL<16, false> __VA_ARGS__; break;                         \
+    case 2 * 16 + 1: KERNEL<16, true> __VA_ARGS__; break;                      \
+    case 2 * 25: KERNEL<25, false> __VA_ARGS__; break;                         \
+    case 2 * 25 + 1: KERNEL<25, true> __VA_ARGS__; break;                      \
+    case 2 * 32 + 1: KERNEL<32, true> __VA_ARGS__; break;                      \
+    default: KERNEL<32, false> __VA_ARGS__; break;                             \
   }
 
-template <int NK>
+template <int NK, bool FULL>
 void set_smem(int bytes) {
-  CPB_CUDA(cudaFuncSetAttribute(k_hess_tma<NK>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CPB_CUDA(cudaFuncSetAttribute(k_hess_tma<NK, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
 int nk_bucket(int64_t d) {
   const int need = static_cast<int>((d + 31) / 32);
-  for (int b : {2, 4, 8, 16, 25, 32})
+  for (int b : {8, 16, 25, 32})
     if (need <= b) return b;
   return 0;
 }
@@ -337,13 +342,14 @@ int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const dou
   const int S = 2;
   const size_t smem = static_cast<size_t>(warps) * S * 2 * dp * sizeof(double);
   if (smem > 220 * 1024) invalid("hessian: shared-memory ring exceeds 220 KB");
-  NK_DISPATCH(nk, set_smem, (static_cast<int>(smem)));
+  const bool full = d >= 32 * (nk - 1);
+  NK_DISPATCH(nk, full, set_smem, (static_cast<int>(smem)));
   double* partial = c.buf<double>("hess.partial", static_cast<size_t>(sp.nslots) * d + 1);
   // partitioned PCG: every rank launches the same grid so the partial tables line up
   const bool parted = c.own_v1 >= 0;
   const int grid = parted ? c.sm_count * 2 : std::max(1, std::min(cdiv(sp.nseg, warps), c.sm_count * 2));
   const int* wr = warp_ranges(c, sp, grid * warps);
-  NK_DISPATCH(nk, k_hess_tma, <<<grid, 32 * warps, smem, c.s>>>(P, V, jal, jbe, g.adj_e.p, g.adj_o.p, sp.node.p,
+  NK_DISPATCH(nk, full, k_hess_tma, <<<grid, 32 * warps, smem, c.s>>>(P, V, jal, jbe, g.adj_e.p, g.adj_o.p, sp.node.p,
                                                                 sp.beg.p, sp.end.p, sp.slot.p, sp.nseg,
                                                                 static_cast<int>(d), dp, sigma, Ap, partial, part,
                                                                 active, S, wr));
