@@ -23,9 +23,13 @@ bool first_on_device(const char* tag) {
   return seen.emplace(dev, tag).second;
 }
 
-void trace(const char* tag) {
+bool trace_on() {
   static const bool on = std::getenv("CPB_TRACE") != nullptr;
-  if (!on) return;
+  return on;
+}
+
+void trace(const char* tag) {
+  if (!trace_on()) return;
   static auto last = std::chrono::steady_clock::now();
   const auto now = std::chrono::steady_clock::now();
   std::fprintf(stderr, "[cpb] %s +%.3f ms\n", tag, std::chrono::duration<double, std::milli>(now - last).count());

@@ -247,6 +247,7 @@ __device__ __forceinline__ double group_max(double v, unsigned m) {
 // CPB_TRACE=1: host wall-clock trace lines "[cpb] <tag> +<ms since previous>"
 // on stderr (diagnostics for host-side stalls; off by default).
 void trace(const char* tag);
+bool trace_on();
 
 // True the first time `tag` is seen for the calling thread's current device
 // (kernel attributes such as the >48 KB shared-memory opt-in are per device;

@@ -40,7 +40,7 @@ int gather_grad_diag(Ctx& c, const Graph& g, const double* X, const double* A, c
                      bool want_diag, double* G, double* diag, double* part);
 // SSNAL Hessian (ssnal.cpp:56-64), two passes: per-edge bc_l = beta_l <v_l, p_i - p_j>,
 // then the node gather; part[2b] = <p, Ap>, part[2b+1] = <p, p>.
-// TMA-staged single-pass Hessian (hess_tma.cu): q = 2, even d in [34, 1024].
+// TMA-staged single-pass Hessian (hess_tma.cu): q = 2, even d in [256, 1024].
 bool hess_tma_supported(int64_t d);
 int hess_tma(Ctx& c, const Graph& g, const double* P, const double* V, const double* jal, const double* jbe,
              int64_t d, double sigma, double* Ap, double* part, const int* active);

@@ -137,6 +137,7 @@ cp_termination ssnal(Prob& P, const cp_solver_config& cfg, bool warm, double* Xo
     bool v_at_x = true;  // V = X B + Z / sigma at the current X (false after a failed line search)
     for (int64_t j = 0; j < cfg.ssnal_newton_max; ++j) {
       const int64_t n_active = jac_params(P, nv, thr, ps, jal, jbe);
+      if (trace_on()) trace(("newton active edges " + std::to_string(n_active) + " / " + std::to_string(E)).c_str());
       const double gnorm = std::sqrt(grad_diag(P, X, V, ps, jal, jbe, thr, sigma, G, w.diag, true));
       if (gnorm <= eps_k) break;
       ++cnt.newton;
