@@ -431,11 +431,12 @@ def test_hessian_tma_path_matches_oracle(cp, orc, d):
 
 
 @pytest.mark.parametrize("q", [1, 0])
-@pytest.mark.parametrize("d", [33, 64, 300, 1000])
+@pytest.mark.parametrize("d", [33, 64, 300, 520, 1000, 3072])
 def test_hessian_mask_path_matches_oracle(cp, orc, q, d):
     """q = 1 / inf Hessian (ssnal.cpp:56-64) through the per-edge Jacobian bit masks
     (gather.cu edge_masks: [|v_f| > t] or [|v_f| > theta] and sign(v_f)), which replace the V
-    reads of the gathers: equal to the oracle's dense-Jacobian apply at rounding level."""
+    reads of the gathers: equal to the oracle's dense-Jacobian apply at rounding level.  Even
+    d >= 512 runs the block-per-node kernel (hess_blk.cu), d = 3072 is C4's row length."""
     A = mixture(orc, 30, d, m=3, seed=11)
     g, og = check_graph(cp, orc, A, 8, 0.5)
     rng = np.random.default_rng(d + 7 * q)
@@ -451,7 +452,7 @@ def test_hessian_mask_path_matches_oracle(cp, orc, q, d):
 
 
 @pytest.mark.parametrize("q", [0, 1])
-@pytest.mark.parametrize("d", [40, 300])
+@pytest.mark.parametrize("d", [40, 300, 600])
 def test_ssnal_linf_l1_wide_rows_match_oracle(cp, orc, q, d):
     """SSNAL with q = inf / 1 at d > 32: the shared-memory-staged q = inf edge passes
     (k_phi_edge_linf_s, k_mult_inf_s, k_gap_edge_linf_s) and the bit-mask Hessian keep the
