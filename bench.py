@@ -400,8 +400,8 @@ def run_ours(args, cfg):
     achieved = hs["alg_bytes"] / (hs["ms"] / 1e3) / 1e9 if hs["ms"] > 0 else 0.0
     total_ms = sum(v["ms"] for v in stats.values())
     traffic = None
-    try:  # one ncu --set full capture of this config's Hessian (profiles/ncu_traffic_r01.json)
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")) as f:
+    try:  # one ncu --set full capture of this config's Hessian (profiles/ncu_traffic_r02.json)
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")) as f:
             traffic = json.load(f).get(args.config)
     except Exception:
         traffic = None
