@@ -24,7 +24,8 @@ of BASELINE.json).  c2 (n=10000, configs[1]) and c1 are selectable.
 * edge_op_gbps — sum of algorithmic bytes / sum of time over the edge, prox,
            CG, line-search and KKT kernels.
 * cpu_baseline — the CPU oracle (oracle/, a restatement of the single-threaded
-           reference) on the box's host, bounded sample: kNN of 400 query rows
+           reference) on the box's host with every host thread (ORC_THREADS; the
+           parallel loops are bitwise the one-thread result), bounded sample: kNN of 400 query rows
            and one call of each SSNAL building block at this config, scaled by
            the GPU path's own iteration counts (which match the oracle's; see
            tests/test_gpu_parity.py::test_ssnal_iteration_path_matches).
@@ -91,6 +92,15 @@ def host_cores():
         return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count()
+
+
+def oracle_threads():
+    """Host threads for the CPU arms: every core of this box unless ORC_THREADS is set.  The
+    oracle's parallel loops (kNN rows, per-edge prox / Jacobian, node-partitioned scatters) give
+    results bitwise equal to one thread; its reductions stay sequential in Eigen's order.
+    Must run before the oracle's first call (the thread count is read once)."""
+    os.environ.setdefault("ORC_THREADS", str(host_cores()))
+    return int(os.environ["ORC_THREADS"])
 
 
 def oracle_counts(name):
@@ -276,6 +286,7 @@ def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    threads = oracle_threads()
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as orc
     A = make_input(orc, cfg)
@@ -297,7 +308,7 @@ def run_reference(args, cfg):
     line = {"metric": "clustering-path wall s (20 gamma, KKT 1e-6)", "value": v, "unit": "s", "impl": "reference",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": False,
             "dtype": "f64", "data": "synthetic", "config": workload_config(args, cfg, world),
-            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "host_cores": host_cores(), "kind": "port",
+            "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "host_cores": host_cores(), "kind": "port",
                              "extrapolated": counts.get("algorithm") == "ssnal",
                              "counts_source": counts.get("counts_source", "profiles/path_counts (GPU path)"),
                              "sample": sample},
@@ -450,10 +461,11 @@ def run_ours(args, cfg):
         oc = oracle_counts(args.config)
         if oc is not None:  # the oracle's own iteration counts of this path
             ccounts["per_gamma"] = oc
+        threads = oracle_threads()
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import pyoracle as orc
         est, sample, spent = cpu_estimate(cfg, make_input(orc, cfg), ccounts)
-        cpu = {"value": est, "unit": "s", "cores": 1, "host_cores": host_cores(), "kind": "port",
+        cpu = {"value": est, "unit": "s", "cores": threads, "host_cores": host_cores(), "kind": "port",
                "extrapolated": cfg["algorithm"] == "ssnal",
                "counts_source": "oracle goldens" if oc is not None else "this GPU path (identical to the oracle's at C2)",
                "sample": sample, "sample_cpu_seconds": round(spent, 1)}
