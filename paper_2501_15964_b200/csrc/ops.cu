@@ -137,9 +137,12 @@ __global__ void k_prox_cols(int q, const double* __restrict__ V, const double* _
     }
   }
 }
+// In place (out == Z), rows inside the ball are not rewritten (the values would be the same
+// bits); `changed` (nullable) is set when any row moves.
 __global__ void k_project_cols(int q, const double* __restrict__ Z, const double* __restrict__ r, int64_t E, int d,
-                               double* __restrict__ out) {
+                               double* __restrict__ out, int* changed) {
   const unsigned gm = group_mask();
+  const bool inplace = out == Z;
   ROWS_BEGIN(E) {
     const double* z = Z + row_ * d;
     double* o = out + row_ * d;
@@ -149,13 +152,22 @@ __global__ void k_project_cols(int q, const double* __restrict__ Z, const double
       for (int f = threadIdx.x; f < d; f += blockDim.x) ss += z[f] * z[f];
       const double nz = sqrt(group_sum(ss, gm));
       const double s = rl / nz;
-      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = (nz <= rl) ? z[f] : s * z[f];
+      const bool inside = nz <= rl;
+      if (!inside && changed) *changed = 1;
+      if (!(inplace && inside))
+        for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = inside ? z[f] : s * z[f];
     } else if (q == Q_LINF) {
       int cnt;
       const double th = linf_theta([&](int f) { return z[f]; }, d, rl, gm, &cnt);
-      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = th < 0.0 ? z[f] : soft(z[f], th);
+      if (th >= 0.0 && changed) *changed = 1;
+      if (!(inplace && th < 0.0))
+        for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = th < 0.0 ? z[f] : soft(z[f], th);
     } else {
-      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = fmax(fmin(z[f], rl), -rl);
+      for (int f = threadIdx.x; f < d; f += blockDim.x) {
+        const double v = fmax(fmin(z[f], rl), -rl);
+        if (v != z[f] && changed) *changed = 1;
+        if (!inplace || v != z[f]) o[f] = v;
+      }
     }
   }
 }
@@ -1131,7 +1143,8 @@ __global__ void __launch_bounds__(32 * kLinfWarps) k_gap_edge_s(
 template <int Q>
 __global__ void __launch_bounds__(32 * kLinfWarps) k_project_cols_s(const double* __restrict__ Z,
                                                                      const double* __restrict__ r, int64_t E, int d,
-                                                                     double* __restrict__ out) {
+                                                                     double* __restrict__ out, int* changed) {
+  const bool inplace = out == Z;
   extern __shared__ double srow[];
   const unsigned gm = group_mask();
   double* sz = srow + static_cast<size_t>(threadIdx.y) * d;
@@ -1159,11 +1172,16 @@ __global__ void __launch_bounds__(32 * kLinfWarps) k_project_cols_s(const double
     if (Q == Q_L2) {
       const double nz = sqrt(group_sum(ss, gm));
       const double sc = rl / nz;
-      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = (nz <= rl) ? sz[f] : sc * sz[f];
+      const bool inside = nz <= rl;
+      if (!inside && changed) *changed = 1;
+      if (!(inplace && inside))
+        for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = inside ? sz[f] : sc * sz[f];
     } else {
       int cnt;
       const double th = linf_theta_bits([&](int f) { return sz[f]; }, d, rl, &cnt);
-      for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = th < 0.0 ? sz[f] : soft(sz[f], th);
+      if (th >= 0.0 && changed) *changed = 1;
+      if (!(inplace && th < 0.0))
+        for (int f = threadIdx.x; f < d; f += blockDim.x) o[f] = th < 0.0 ? sz[f] : soft(sz[f], th);
     }
     __syncwarp();
   }
@@ -1532,17 +1550,26 @@ void prox_columns_dev(Ctx& c, int q, const double* V, const double* t, int64_t d
   CPB_LAUNCH_CHECK();
 }
 void project_columns_dev(Ctx& c, int q, const double* Z, const double* r, int64_t d, int64_t E, double* out) {
+  int* changed = c.buf<int>("proj.changed", 1);
+  CPB_CUDA(cudaMemsetAsync(changed, 0, sizeof(int), c.s));
   if (E == 0) return;
   GroupGeom gg = group_geom(c, E, d);
   if ((q == Q_L2 || q == Q_LINF) && linf_staged(d, 1)) {  // one HBM read of Z instead of two
     if (q == Q_L2)
-      launch_linf_s(k_project_cols_s<Q_L2>, 1, d, gg.grid, c.s, Z, r, E, static_cast<int>(d), out);
+      launch_linf_s(k_project_cols_s<Q_L2>, 1, d, gg.grid, c.s, Z, r, E, static_cast<int>(d), out, changed);
     else
-      launch_linf_s(k_project_cols_s<Q_LINF>, 1, d, gg.grid, c.s, Z, r, E, static_cast<int>(d), out);
+      launch_linf_s(k_project_cols_s<Q_LINF>, 1, d, gg.grid, c.s, Z, r, E, static_cast<int>(d), out, changed);
     return;
   }
-  k_project_cols<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(q, Z, r, E, static_cast<int>(d), out);
+  k_project_cols<<<gg.grid, dim3(gg.gx, gg.gy), 0, c.s>>>(q, Z, r, E, static_cast<int>(d), out, changed);
   CPB_LAUNCH_CHECK();
+}
+
+bool last_projection_changed(Ctx& c) {
+  int h = 1;
+  CPB_CUDA(cudaMemcpyAsync(&h, c.buf<int>("proj.changed", 1), sizeof(int), cudaMemcpyDeviceToHost, c.s));
+  c.sync();
+  return h != 0;
 }
 void prox_jacobian_apply_dev(Ctx& c, int q, const double* V, const double* t, const double* W, int64_t d, int64_t E,
                              double* out) {

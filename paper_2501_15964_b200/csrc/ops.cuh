@@ -46,6 +46,8 @@ double max_abs_dev(Ctx& c, const double* x, int64_t count);
 // ---- prox / projection over edge columns (prox.cpp:73-93) ------------------
 void prox_columns_dev(Ctx& c, int q, const double* V, const double* t, int64_t d, int64_t E, double* out);
 void project_columns_dev(Ctx& c, int q, const double* Z, const double* r, int64_t d, int64_t E, double* out);
+// Whether the last project_columns_dev moved any column (reads a device flag; syncs).
+bool last_projection_changed(Ctx& c);
 void prox_jacobian_apply_dev(Ctx& c, int q, const double* V, const double* t, const double* W, int64_t d, int64_t E,
                              double* out);
 void prox_jacobian_diag_dev(Ctx& c, int q, const double* V, const double* t, int64_t d, int64_t E, double* out);

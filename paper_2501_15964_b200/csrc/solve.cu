@@ -1,5 +1,18 @@
 // Solver drivers and the path engine (see solve.cuh).
+#include <sched.h>
+
+#include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <exception>
+#include <mutex>
+#include <cstring>
+#include <thread>
+#include <tuple>
+#include <utility>
+#include <vector>
 #include <cstdlib>
 #include <cmath>
 #include <limits>
@@ -511,6 +524,101 @@ int64_t extract_clusters_dev(Ctx& c, const Graph& g, const double* X, int64_t d,
   return K;
 }
 
+// Host copies of whole output blocks, split over the process's CPUs (pinned outputs of a C3 path
+// are GBs: one thread copies ~10 GB/s).
+void host_copy_parallel(const std::vector<std::tuple<void*, const void*, size_t>>& segs, int spare = 0) {
+  constexpr size_t kPiece = size_t(32) << 20;
+  std::vector<std::tuple<char*, const char*, size_t>> pieces;
+  for (const auto& sg : segs)
+    for (size_t o = 0; o < std::get<2>(sg); o += kPiece)
+      pieces.emplace_back(static_cast<char*>(std::get<0>(sg)) + o, static_cast<const char*>(std::get<1>(sg)) + o,
+                          std::min(kPiece, std::get<2>(sg) - o));
+  if (pieces.empty()) return;
+  cpu_set_t cs;
+  int cpus = 1;
+  if (sched_getaffinity(0, sizeof(cs), &cs) == 0) cpus = CPU_COUNT(&cs);
+  const int nt = std::max(1, std::min<int>({cpus - spare, 32, static_cast<int>(pieces.size())}));
+  std::atomic<size_t> next{0};
+  auto work = [&] {
+    for (size_t i = next++; i < pieces.size(); i = next++)
+      std::memcpy(std::get<0>(pieces[i]), std::get<1>(pieces[i]), std::get<2>(pieces[i]));
+  };
+  std::vector<std::thread> th;
+  for (int i = 1; i < nt; ++i) th.emplace_back(work);
+  work();
+  for (auto& x : th) x.join();
+}
+
+// Host copies that wait for device work: a worker thread takes (event, blocks) items in order,
+// waits for the event (the source blocks' device-to-host copy) and copies, while the path's
+// solves go on.  The destructor drains the queue and joins.
+class HostCopier {
+ public:
+  using Segs = std::vector<std::tuple<void*, const void*, size_t>>;
+  explicit HostCopier(int dev) : dev_(dev) {}
+  ~HostCopier() {
+    join();
+    for (auto e : events_) cudaEventDestroy(e);
+  }
+  cudaEvent_t record(cudaStream_t s) {  // an event owned by the copier, recorded on s
+    cudaEvent_t e;
+    CPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    events_.push_back(e);
+    CPB_CUDA(cudaEventRecord(e, s));
+    return e;
+  }
+  void push(cudaEvent_t after, Segs segs) {
+    if (!th_.joinable()) th_ = std::thread([this] { loop(); });
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      q_.emplace_back(after, std::move(segs));
+    }
+    cv_.notify_one();
+  }
+  void finish() {  // waits for every queued copy; rethrows the worker's error
+    join();
+    if (err_) std::rethrow_exception(std::exchange(err_, nullptr));
+  }
+
+ private:
+  void join() {
+    if (!th_.joinable()) return;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      done_ = true;
+    }
+    cv_.notify_one();
+    th_.join();
+  }
+  void loop() {
+    cudaSetDevice(dev_);
+    for (;;) {
+      std::pair<cudaEvent_t, Segs> it;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return done_ || !q_.empty(); });
+        if (q_.empty()) return;
+        it = std::move(q_.front());
+        q_.pop_front();
+      }
+      try {
+        CPB_CUDA(cudaEventSynchronize(it.first));
+        host_copy_parallel(it.second, 2);  // two CPUs stay with the thread driving the solves
+      } catch (...) {
+        if (!err_) err_ = std::current_exception();
+      }
+    }
+  }
+  int dev_;
+  std::thread th_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<std::pair<cudaEvent_t, Segs>> q_;
+  bool done_ = false;
+  std::exception_ptr err_;
+  std::vector<cudaEvent_t> events_;
+};
+
 void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, int64_t T,
                   const cp_solver_config& cfg, const cp_path_options& opt, double* X_out, double* Z_out,
                   int64_t* labels_out, int64_t* K_out, cp_termination* terms_out, const cp_path_sink* sink) {
@@ -598,6 +706,20 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
     }
   }
   int64_t K_prev = -1;
+  // A gamma whose warm start the solver accepted as is (X unchanged) after a projection that moved
+  // nothing (Z unchanged) has the last shipped gamma's outputs bit for bit: its blocks are not
+  // snapshotted or sent over the link again but copied on the host from that gamma's blocks.
+  int64_t shipped = -1;
+  cudaEvent_t shipped_done = nullptr;  // the last shipped gamma's device-to-host copy (async outputs)
+  int dev = 0;
+  CPB_CUDA(cudaGetDevice(&dev));
+  HostCopier copier(dev);
+  auto dup_segs = [&](int64_t t, int64_t src) {
+    HostCopier::Segs segs;
+    if (X_out) segs.emplace_back(X_out + t * m, X_out + src * m, m * sizeof(double));
+    if (Z_out && me) segs.emplace_back(Z_out + t * me, Z_out + src * me, me * sizeof(double));
+    return segs;
+  };
   for (int64_t t = 0; t < T; ++t) {
     const double gamma = gammas[t];
     Prob P;
@@ -628,7 +750,15 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
       if (!x_unchanged) d2h(c, hl.data(), lab, n * sizeof(int));
       for (int64_t i = 0; i < n; ++i) labels_out[t * n + i] = hl[static_cast<size_t>(i)];
     }
-    if (async_out) {
+    const bool same_out = x_unchanged && shipped >= 0 && !c.comm && (X_out || Z_out) &&
+                          (!Z_out || me == 0 || !last_projection_changed(c));
+    if (same_out) {
+      if (async_out)
+        copier.push(shipped_done, dup_segs(t, shipped));  // after the source's copy, off this thread
+      else
+        host_copy_parallel(dup_segs(t, shipped));  // the source blocks are complete
+    } else if (async_out) {
+      shipped = t;
       // Snapshot the solution (D2D) and ship it to pinned host memory on the
       // copy stream while the next gamma is solved (double-buffered).
       const int s = static_cast<int>(t & 1);
@@ -648,7 +778,9 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
       if (X_out) ship(X_out + t * m, mX ? mX + t * m : nullptr, snapX[s], m);
       if (Z_out && me) ship(Z_out + t * me, mZ ? mZ + t * me : nullptr, snapZ[s], me);
       CPB_CUDA(cudaEventRecord(copy_done[s], cs));
+      shipped_done = copier.record(cs);
     } else {
+      shipped = t;
       if (X_out) d2h(c, X_out + t * m, X, m * sizeof(double));
       if (Z_out && me) d2h(c, Z_out + t * me, Z, me * sizeof(double));
     }
@@ -656,6 +788,7 @@ void run_path_dev(Ctx& c, Data& A, const Graph& g, int q, const double* gammas, 
     trace("path gamma done");
   }
   if (async_out) CPB_CUDA(cudaStreamSynchronize(cs));
+  copier.finish();
   c.sync();
 }
 

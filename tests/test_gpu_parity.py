@@ -571,6 +571,27 @@ def test_path_parity(cp, orc, algo):
         assert res.assignments[t].K == ores["K"][t]
 
 
+def test_path_outputs_of_unchanged_gammas(cp, orc):
+    """run_path does not ship a gamma's X / Z again when its warm start was accepted as is and
+    the dual projection moved nothing (the blocks are host copies of the last shipped gamma's):
+    every gamma's X and Z must still equal, bit for bit, a chain of warm-started solve() calls."""
+    A = mixture(orc, 30, 16, m=3, seed=3)  # the oracle's path: gammas 9-12 take 0 iterations
+    g, _ = check_graph(cp, orc, A, 10, 0.5)
+    sched = cp.make_schedule(0.01, 10.0, 12)
+    cfg = cp.SolverConfig()
+    res = cp.run_path(cp.DataMatrix(A), g, 2, sched, cfg, keep_solutions=True, keep_z=True)
+    data, prev = cp.DataMatrix(A), None
+    zero_iter = 0
+    for t, gamma in enumerate(sched.values):
+        sol = cp.solve(cp.ProblemInstance(data, g, gamma, 2), cfg, prev)
+        prev = sol
+        zero_iter += int(t > 0 and res.stats[t].iterations == 0)
+        assert res.stats[t].iterations == sol.termination.iterations
+        assert np.array_equal(res.solutions[t].X, sol.X)
+        assert np.array_equal(res.solutions[t].Z, sol.Z)
+    assert zero_iter >= 1  # the path exercises the host-copied outputs
+
+
 # q = inf: the device and the oracle compute the l1-ball threshold with the same Michelot
 # passes and the same 32-lane summation order (linf.cuh, oracle l1_theta), so the projected
 # iterates agree bit for bit and the d = 40 case holds the same 1e-10 bar as q = 1, 2.
