@@ -603,7 +603,14 @@ class HostCopier {
       }
       try {
         CPB_CUDA(cudaEventSynchronize(it.first));
+        const auto t0 = std::chrono::steady_clock::now();
         host_copy_parallel(it.second, 2);  // two CPUs stay with the thread driving the solves
+        if (trace_on()) {
+          size_t b = 0;
+          for (const auto& sg : it.second) b += std::get<2>(sg);
+          const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+          trace(("host copy " + std::to_string(b >> 20) + " MB in " + std::to_string(ms) + " ms").c_str());
+        }
       } catch (...) {
         if (!err_) err_ = std::current_exception();
       }
