@@ -478,7 +478,10 @@ def run_ours(args, cfg):
                 "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                         "cold_value": e2e_cold,
                         "cold_note": "first call of the process: includes allocating/pinning the host output pool",
-                        "returns": "X, labels, records per gamma" + (", Z per gamma" if keep_z else "")},
+                        "returns": "X, labels, records per gamma" + (", Z per gamma" if keep_z else ""),
+                        "d2h_note": "bytes of results delivered to host buffers; a gamma accepted as is with an "
+                                    "unchanged dual projection gets its X/Z as a host copy of the previous "
+                                    "gamma's (bitwise equal), not a second transfer over the link"},
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": int(launches),
                 "knn": knn, "edge_op_gbps": edge_op_gbps,
                 "path": {"E": E, "K": [a.K for a in res.assignments], "converged": all(s.converged for s in res.stats),
