@@ -571,10 +571,14 @@ def test_path_parity(cp, orc, algo):
         assert res.assignments[t].K == ores["K"][t]
 
 
-def test_path_outputs_of_unchanged_gammas(cp, orc):
+@pytest.mark.parametrize("pinned", [True, False])
+def test_path_outputs_of_unchanged_gammas(cp, orc, monkeypatch, pinned):
     """run_path does not ship a gamma's X / Z again when its warm start was accepted as is and
     the dual projection moved nothing (the blocks are host copies of the last shipped gamma's):
     every gamma's X and Z must still equal, bit for bit, a chain of warm-started solve() calls."""
+    if not pinned:  # pageable outputs: synchronous copies, the host copy right away
+        import paper_2501_15964_b200.cluspath as cpm
+        monkeypatch.setattr(cpm, "pinned_empty", lambda shape, dtype=np.float64: np.empty(shape, dtype))
     A = mixture(orc, 30, 16, m=3, seed=3)  # the oracle's path: gammas 9-12 take 0 iterations
     g, _ = check_graph(cp, orc, A, 10, 0.5)
     sched = cp.make_schedule(0.01, 10.0, 12)
