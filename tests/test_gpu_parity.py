@@ -435,8 +435,8 @@ def test_hessian_tma_path_matches_oracle(cp, orc, d):
 def test_hessian_mask_path_matches_oracle(cp, orc, q, d):
     """q = 1 / inf Hessian (ssnal.cpp:56-64) through the per-edge Jacobian bit masks
     (gather.cu edge_masks: [|v_f| > t] or [|v_f| > theta] and sign(v_f)), which replace the V
-    reads of the gathers: equal to the oracle's dense-Jacobian apply at rounding level.  Even
-    d >= 512 runs the block-per-node kernel (hess_blk.cu), d = 3072 is C4's row length."""
+    reads of the gathers: equal to the oracle's dense-Jacobian apply at rounding level
+    (d = 3072 is C4's row length)."""
     A = mixture(orc, 30, d, m=3, seed=11)
     g, og = check_graph(cp, orc, A, 8, 0.5)
     rng = np.random.default_rng(d + 7 * q)
