@@ -1195,9 +1195,125 @@ void launch_linf_s(K kernel, int rows, int64_t d, int grid, cudaStream_t s, Args
   kernel<<<grid, dim3(32, kLinfWarps), smem, s>>>(args...);
   CPB_LAUNCH_CHECK();
 }
+static_assert(kMultWarps == kLinfWarps, "k_gap_edge_t must assign edges to warps like k_gap_edge_s");
+// TMA variant of k_gap_edge_s for q = 2 / 1 (even d <= 1024): x_i, x_j and Z_l stream into
+// the warp's shared-memory slot by cp.async.bulk instead of batched loads.  Same edges per
+// warp, per-lane element order and group sums as k_gap_edge_s, so the partial table is
+// bitwise the same.
+template <int Q>
+__global__ void __launch_bounds__(32 * kMultWarps) k_gap_edge_t(
+    const double* __restrict__ X, const double* __restrict__ Z, const int* __restrict__ ei,
+    const int* __restrict__ ej, const double* __restrict__ rad, const double* __restrict__ w, EdgeSel sel, int d,
+    double* part, int S) {
+  extern __shared__ __align__(16) double prow[];
+  __shared__ double sh[32];
+  __shared__ uint64_t bars[kMultWarps][kEdgeMaxStages];
+  const int lane = threadIdx.x;
+  const unsigned gm = 0xffffffffu;
+  uint64_t* bar = bars[threadIdx.y];
+  if (lane == 0)
+    for (int q = 0; q < S; ++q) mbar_init(&bar[q], 1);
+  fence_mbar_init();
+  __syncwarp();
+  const unsigned rb = static_cast<unsigned>(d) * 8u;
+  const int64_t wid = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * blockDim.y;
+  const int64_t cnt = wid < sel.count ? (sel.count - wid + nw - 1) / nw : 0;
+  double* const base = prow + static_cast<size_t>(threadIdx.y) * S * 3 * d;
+  auto issue = [&](int64_t e, int q) {
+    const int64_t l = sel.at(wid + e * nw);
+    double* sa = base + static_cast<size_t>(q) * 3 * d;
+    uint64_t* b = &bar[q];
+    fence_proxy_async();
+    mbar_expect_tx(b, 3 * rb);
+    bulk_g2s(sa, X + static_cast<int64_t>(ei[l]) * d, rb, b);
+    bulk_g2s(sa + d, X + static_cast<int64_t>(ej[l]) * d, rb, b);
+    bulk_g2s_hint(sa + 2 * d, Z + l * d, rb, b, policy_evict_first());
+  };
+  if (lane == 0)
+    for (int q = 0; q < S && q < cnt; ++q) issue(q, q);
+  double s[4] = {0, 0, 0, 0}, excess = -1.0;
+  int q = 0;
+  unsigned ph = 0;
+  for (int64_t e = 0; e < cnt; ++e) {
+    const int64_t row_ = sel.at(wid + e * nw);
+    const double* sa = base + static_cast<size_t>(q) * 3 * d;
+    const double* sb = sa + d;
+    const double* sz = sb + d;
+    const double rl = rad[row_];
+    mbar_wait(&bar[q], ph);
+    double xb2 = 0.0, zz = 0.0, uu = 0.0, l1 = 0.0, zmax = 0.0;
+    for (int f = lane; f < d; f += 32) {
+      const double x = sa[f] - sb[f];
+      const double zf = sz[f];
+      xb2 += x * x;
+      zz += zf * zf;
+      const double uv = x + zf;
+      uu += uv * uv;
+      l1 += fabs(x);
+      zmax = fmax(zmax, fabs(zf));
+    }
+    double t0, al = 0.0;
+    xb2 = group_sum(xb2, gm);
+    zz = group_sum(zz, gm);
+    if (Q == Q_L2) {
+      const double nu = sqrt(group_sum(uu, gm));
+      if (nu <= rl) {
+        al = xb2;
+      } else {
+        const double sc = 1.0 - rl / nu;
+        for (int f = lane; f < d; f += 32) {
+          const double x = sa[f] - sb[f];
+          const double ev = x - sc * (x + sz[f]);
+          al += ev * ev;
+        }
+        al = group_sum(al, gm);
+      }
+      t0 = w[row_] * sqrt(xb2);
+      excess = fmax(excess, sqrt(zz) - (rl + 1e-9));
+    } else {
+      for (int f = lane; f < d; f += 32) {
+        const double x = sa[f] - sb[f];
+        const double ev = x - soft(x + sz[f], rl);
+        al += ev * ev;
+      }
+      al = group_sum(al, gm);
+      t0 = w[row_] * group_sum(l1, gm);
+      excess = fmax(excess, group_max(zmax, gm) - (rl + 1e-9));
+    }
+    if (lane == 0) s[0] += t0, s[1] += al, s[2] += xb2, s[3] += zz;
+    __syncwarp();
+    if (lane == 0 && e + S < cnt) issue(e + S, q);
+    if (++q == S) q = 0, ph ^= 1u;
+  }
+  for (int k = 0; k < 4; ++k) {
+    const double r = block_sum(s[k], sh);
+    if (threadIdx.x == 0 && threadIdx.y == 0) part[5 * blockIdx.x + k] = r;
+  }
+  const double m = block_max(excess, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) part[5 * blockIdx.x + 4] = m;
+}
+
 // gap edge terms over `sel` on `grid` blocks (5 partials per block)
 void gap_edge_launch(Ctx& c, int grid, const GroupGeom& ge, const double* X, const double* Z, const Prob& P,
                      EdgeSel sel, int64_t d, double* pe) {
+  if (P.q != Q_LINF && d > 32 && d % 2 == 0 && d <= kMultSmemMaxD && linf_staged(d, 2)) {
+    const int S = edge_stages(d, 3);
+    const size_t smem = static_cast<size_t>(kMultWarps) * S * 3 * d * sizeof(double);
+    if (first_on_device("k_gap_edge_t.smem")) {
+      CPB_CUDA(cudaFuncSetAttribute(k_gap_edge_t<Q_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      CPB_CUDA(cudaFuncSetAttribute(k_gap_edge_t<Q_L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    }
+    const dim3 blk(32, kMultWarps);
+    if (P.q == Q_L2)
+      k_gap_edge_t<Q_L2><<<grid, blk, smem, c.s>>>(X, Z, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, sel,
+                                                   static_cast<int>(d), pe, S);
+    else
+      k_gap_edge_t<Q_L1><<<grid, blk, smem, c.s>>>(X, Z, P.g->ei.p, P.g->ej.p, P.rad, P.g->w.p, sel,
+                                                   static_cast<int>(d), pe, S);
+    CPB_LAUNCH_CHECK();
+    return;
+  }
   if (linf_staged(d, 2)) {  // 32-lane rows that fit two staged rows per warp
     auto args = [&](auto kernel) {
       launch_linf_s(kernel, 2, d, grid, c.s, X, Z, (const int*)P.g->ei.p, (const int*)P.g->ej.p,
