@@ -145,6 +145,25 @@ EXPORTED = [s[0] for s in _SIGS]
 _lib = None
 
 
+def _point_at_torch_nccl():
+    """The library dlopens NCCL on first use.  A process that also imports torch must end up with
+    torch's NCCL (the pip nvidia-nccl wheel), not the system one: if the older system library
+    is loaded first, torch's import later fails on missing symbols.  CPB_NCCL_LIB names the
+    wheel's library when it is installed (comm.cu tries an already-loaded NCCL first)."""
+    if os.environ.get("CPB_NCCL_LIB"):
+        return
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        spec = None
+    for base in (list(spec.submodule_search_locations) if spec and spec.submodule_search_locations else []):
+        cand = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["CPB_NCCL_LIB"] = cand
+            return
+
+
 def load():
     """Load the in-tree shared library (raises when it has not been built)."""
     global _lib
@@ -153,6 +172,7 @@ def load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python __graft_entry__.py` (build()) — "
                           "paper_2501_15964_b200 has no CPU fallback")
+    _point_at_torch_nccl()
     lib = C.CDLL(LIB_PATH)
     for name, res, args in _SIGS:
         f = getattr(lib, name)

@@ -1,5 +1,7 @@
 // NCCL through dlopen (see comm.cuh).
 #include <dlfcn.h>
+
+#include <cstdlib>
 #include <nccl.h>
 
 #include <algorithm>
@@ -31,7 +33,12 @@ const Nccl& nccl() {
   static Nccl n;
   static std::once_flag once;
   std::call_once(once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // an NCCL already in the process (torch's), then CPB_NCCL_LIB (the Python layer points it at
+    // torch's wheel), then the loader's search path
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+    if (!h)
+      if (const char* p = std::getenv("CPB_NCCL_LIB")) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) return;
     n.get_id = reinterpret_cast<decltype(n.get_id)>(dlsym(h, "ncclGetUniqueId"));

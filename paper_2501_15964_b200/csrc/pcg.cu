@@ -164,8 +164,27 @@ __global__ void __launch_bounds__(256) k_cg_b(CgState* st, const double* __restr
   const int64_t r0 = rc * rows_per, r1 = min(n, r0 + rows_per);
   double rz = 0.0, rr = 0.0;
   if (f < d) {
-#pragma unroll 4
-    for (int64_t v = r0 + threadIdx.y; v < r1; v += 8) {
+    // batches of 8 rows: all 24 loads issued before the divisions (the z = r / diag division's
+    // latency otherwise sits between consecutive loads); sums in ascending row order as before
+    int64_t v = r0 + threadIdx.y;
+    for (; v + 56 < r1; v += 64) {
+      double rv[8], ap[8], dg[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t i = (v + 8 * u) * d + f;
+        rv[u] = r[i];
+        ap[u] = Ap[i];
+        dg[u] = diag[i];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double x = rv[u] - alpha * ap[u];
+        r[(v + 8 * u) * d + f] = x;
+        rz += x * (x / dg[u]);
+        rr += x * x;
+      }
+    }
+    for (; v < r1; v += 8) {
       const int64_t i = v * d + f;
       const double rv = r[i] - alpha * Ap[i];
       r[i] = rv;
