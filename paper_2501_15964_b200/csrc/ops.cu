@@ -100,8 +100,29 @@ __global__ void k_trial_x(const double* __restrict__ X, const double* __restrict
                           double* __restrict__ Xt, const double* __restrict__ A, int64_t m, double* part) {
   __shared__ double sh[32];
   double s = 0.0;
-  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
-       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  // batches of 4 grid-stride elements: all loads first (the sum keeps the element order)
+  for (; p + 3 * step < m; p += 4 * step) {
+    double x[4], dd[4], a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      x[u] = X[p + u * step];
+      dd[u] = D ? D[p + u * step] : 0.0;
+      a[u] = A[p + u * step];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double xv = x[u];
+      if (D) {
+        xv = xv + alpha * dd[u];
+        Xt[p + u * step] = xv;
+      }
+      const double t = xv - a[u];
+      s += t * t;
+    }
+  }
+  for (; p < m; p += step) {
     double x = X[p];
     if (D) {
       x = x + alpha * D[p];

@@ -77,18 +77,34 @@ __global__ void __launch_bounds__(256) k_cg_init(const double* __restrict__ rhs,
   const int f = fc * 32 + threadIdx.x;
   const int64_t r0 = rc * rows_per, r1 = min(n, r0 + rows_per);
   double rz = 0.0, bb = 0.0;
+  auto row = [&](int64_t i, double bin, double mx, double dg) {
+    const double b = neg ? -bin : bin;
+    const double rv = Mx ? b - mx : b;
+    if (!Mx) x[i] = 0.0;
+    r[i] = rv;
+    const double z = rv / dg;
+    p[i] = z;
+    rz += rv * z;
+    bb += b * b;
+  };
   if (f < d) {
-#pragma unroll 4
-    for (int64_t v = r0 + threadIdx.y; v < r1; v += 8) {
+    // batches of 8 rows with the loads first (see k_cg_b); sums in ascending row order
+    int64_t v = r0 + threadIdx.y;
+    for (; v + 56 < r1; v += 64) {
+      double bi[8], mi[8], dg[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t i = (v + 8 * u) * d + f;
+        bi[u] = rhs[i];
+        mi[u] = Mx ? Mx[i] : 0.0;
+        dg[u] = diag[i];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) row((v + 8 * u) * d + f, bi[u], mi[u], dg[u]);
+    }
+    for (; v < r1; v += 8) {
       const int64_t i = v * d + f;
-      const double b = neg ? -rhs[i] : rhs[i];
-      const double rv = Mx ? b - Mx[i] : b;
-      if (!Mx) x[i] = 0.0;
-      r[i] = rv;
-      const double z = rv / diag[i];
-      p[i] = z;
-      rz += rv * z;
-      bb += b * b;
+      row(i, rhs[i], Mx ? Mx[i] : 0.0, diag[i]);
     }
   }
   const double cb = tile_col_sum(bb, s8);
