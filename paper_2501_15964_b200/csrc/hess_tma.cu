@@ -193,8 +193,17 @@ __global__ void __launch_bounds__(256) k_hess_combine(const double* __restrict__
     const int v = hub_node[h], s0 = hub_slot0[h], ns = hub_nslots[h];
     const int64_t base = static_cast<int64_t>(v) * d;
     for (int f = threadIdx.x; f < d; f += blockDim.x) {
+      // segment order; 8 slots' loads in flight at a time (a hub has up to ~20 slots)
       double acc = 0.0;
-      for (int s = 0; s < ns; ++s) acc += partial[static_cast<int64_t>(s0 + s) * d + f];
+      int s = 0;
+      for (; s + 8 <= ns; s += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = partial[static_cast<int64_t>(s0 + s + u) * d + f];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += v[u];
+      }
+      for (; s < ns; ++s) acc += partial[static_cast<int64_t>(s0 + s) * d + f];
       const double pv = P[base + f];
       const double o = pv + sigma * acc;
       Ap[base + f] = o;

@@ -69,9 +69,16 @@ __global__ void k_div(const double* __restrict__ x, double s, int64_t m, double*
 __global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b, int64_t m, double* part) {
   __shared__ double sh[32];
   double s = 0.0;
-  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
-       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    s += a[p] * b[p];
+  const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (; p + 7 * step < m; p += 8 * step) {  // 8 elements' loads ahead of the ordered sum
+    double x[8], y[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = a[p + u * step], y[u] = b[p + u * step];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += x[u] * y[u];
+  }
+  for (; p < m; p += step) s += a[p] * b[p];
   s = block_sum(s, sh);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
