@@ -28,9 +28,14 @@ namespace {
 struct GroupGeom {
   int gx, gy, grid;
 };
-GroupGeom group_geom(Ctx& c, int64_t rows, int64_t d, int per_sm = 8) {
+// short = true (q = 1 / 2 edge passes): rows of 17..128 features take 8 lanes each, four rows
+// per warp, so the per-row reductions cost 3 shuffle levels shared by four rows instead of 5
+// for one (C5, d = 64).  q = inf keeps 32-lane rows: its threshold sums follow the oracle's
+// 32-lane order.
+GroupGeom group_geom(Ctx& c, int64_t rows, int64_t d, int per_sm = 8, bool short_rows = false) {
   int gx = 1;
   while (gx < d && gx < 32) gx <<= 1;
+  if (short_rows && d > 16 && d <= 128) gx = 8;
   const int gy = 256 / gx;
   const int grid = std::max(1, std::min(cdiv(rows, gy), c.sm_count * per_sm));
   return {gx, gy, grid};
@@ -1325,7 +1330,7 @@ __global__ void __launch_bounds__(32 * kMultWarps) k_gap_edge_t(
 // gap edge terms over `sel` on `grid` blocks (5 partials per block)
 void gap_edge_launch(Ctx& c, int grid, const GroupGeom& ge, const double* X, const double* Z, const Prob& P,
                      EdgeSel sel, int64_t d, double* pe) {
-  if (P.q != Q_LINF && d > 32 && d % 2 == 0 && d <= kMultSmemMaxD && linf_staged(d, 2)) {
+  if (ge.gx == 32 && P.q != Q_LINF && d > 32 && d % 2 == 0 && d <= kMultSmemMaxD && linf_staged(d, 2)) {
     const int S = edge_stages(d, 3);
     const size_t smem = static_cast<size_t>(kMultWarps) * S * 3 * d * sizeof(double);
     if (first_on_device("k_gap_edge_t.smem")) {
@@ -1342,7 +1347,7 @@ void gap_edge_launch(Ctx& c, int grid, const GroupGeom& ge, const double* X, con
     CPB_LAUNCH_CHECK();
     return;
   }
-  if (linf_staged(d, 2)) {  // 32-lane rows that fit two staged rows per warp
+  if (ge.gx == 32 && linf_staged(d, 2)) {  // 32-lane rows that fit two staged rows per warp
     auto args = [&](auto kernel) {
       launch_linf_s(kernel, 2, d, grid, c.s, X, Z, (const int*)P.g->ei.p, (const int*)P.g->ej.p,
                     (const double*)P.rad, (const double*)P.g->w.p, sel, static_cast<int>(d), pe);
@@ -1697,8 +1702,8 @@ void project_columns_dev(Ctx& c, int q, const double* Z, const double* r, int64_
   int* changed = c.buf<int>("proj.changed", 1);
   CPB_CUDA(cudaMemsetAsync(changed, 0, sizeof(int), c.s));
   if (E == 0) return;
-  GroupGeom gg = group_geom(c, E, d);
-  if ((q == Q_L2 || q == Q_LINF) && linf_staged(d, 1)) {  // one HBM read of Z instead of two
+  GroupGeom gg = group_geom(c, E, d, 8, q != Q_LINF);
+  if ((q == Q_L2 || q == Q_LINF) && gg.gx == 32 && linf_staged(d, 1)) {  // one HBM read of Z instead of two
     if (q == Q_L2)
       launch_linf_s(k_project_cols_s<Q_L2>, 1, d, gg.grid, c.s, Z, r, E, static_cast<int>(d), out, changed);
     else
@@ -1746,7 +1751,7 @@ double eval_phi(const Prob& P, const double* X, const double* D, double alpha, d
   if (E > 0) {
     // one launch over an edge selection; returns the number of block partials in pe_
     auto run = [&](EdgeSel sel, double* pe_) -> int {
-      GroupGeom gg = group_geom(c, sel.count, d);
+      GroupGeom gg = group_geom(c, sel.count, d, 8, P.q != Q_LINF);
       int nb = gg.grid;
       if (gg.gx == 32 && d <= kMultSmemMaxD && d % 2 == 0 && (P.q == Q_L2 || P.q == Q_L1)) {
         const int S = edge_stages(d, 3);
@@ -1775,7 +1780,7 @@ double eval_phi(const Prob& P, const double* X, const double* D, double alpha, d
       }
       return nb;
     };
-    const size_t pe_n = std::max(group_geom(c, E, d).grid, c.sm_count * 64);
+    const size_t pe_n = std::max(group_geom(c, E, d, 8, P.q != Q_LINF).grid, c.sm_count * 64);
     double* pe = part_buf(c, "phi.pe", pe_n);
     Ctx::Timer tm(&c, "phi_edge", (2.0 * E * d + n * d + 4.0 * E) * 8.0);
     if (!partitioned(c)) {
@@ -1897,7 +1902,7 @@ GapOut eval_gap(const Prob& P, const double* X, const double* Z) {
     const EdgePart& ep = edge_part(c, *P.g);
     sel = EdgeSel{nullptr, ep.e0, ep.e1 - ep.e0};
   }
-  GroupGeom ge = group_geom(c, sel.count, d);
+  GroupGeom ge = group_geom(c, sel.count, d, 8, P.q != Q_LINF);
   const size_t node_cap = 4 * static_cast<size_t>(c.sm_count) * 16;  // gather_gap: <= 8 * SMs blocks x 4
   double* pn = part_buf(c, "gap.pp", node_cap + 5 * static_cast<size_t>(ge.grid));
   int nbn;
@@ -1990,11 +1995,11 @@ MultOut ssnal_multiplier(const Prob& P, const double* X, double* Z, const double
                          const double* thr, double sigma, bool v_at_x) {
   Ctx& c = *P.c;
   const int64_t d = P.d(), n = P.n(), E = P.E();
-  const size_t pe_n = 9 * static_cast<size_t>(std::max(group_geom(c, E, d).grid, c.sm_count * 64));
+  const size_t pe_n = 9 * static_cast<size_t>(std::max(group_geom(c, E, d, 8, P.q != Q_LINF).grid, c.sm_count * 64));
   double* pe = part_buf(c, "mult.pe", pe_n);
   // one launch over an edge selection; returns the number of 9-wide block partials
   auto run = [&](EdgeSel sel, double* pe) -> int {
-    GroupGeom ge = group_geom(c, sel.count, d);
+    GroupGeom ge = group_geom(c, sel.count, d, 8, P.q != Q_LINF);
     int nb = ge.grid;
     if (P.q == Q_LINF && linf_staged(d, 2)) {
       launch_linf_s(k_mult_inf_s, 2, d, ge.grid, c.s, X, Z, V, ps, (const double*)P.rad, (const double*)P.g->w.p,
