@@ -565,7 +565,7 @@ constexpr auto k_g_hess0 = k_g_hess<NF, 0>;
 // and gathered every p row four times, by one pass that reads V once per
 // endpoint.
 template <int NP>
-__global__ void __launch_bounds__(256, NP == 1 ? 2 : 1) k_hess_warp(const double* __restrict__ P, const double* __restrict__ V,
+__global__ void __launch_bounds__(256, NP == 1 ? 3 : 1) k_hess_warp(const double* __restrict__ P, const double* __restrict__ V,
                                                    const double* __restrict__ jal, const double* __restrict__ jbe,
                                                    const int* __restrict__ off, const int* __restrict__ adj_e,
                                                    const int* __restrict__ adj_o, const int* __restrict__ order,
